@@ -1,0 +1,234 @@
+// driver.cpp -- oracle: Algorithm 1, explicit variant, z = infinity.
+// TEST INFRASTRUCTURE ONLY (see oracle.h).
+//
+// Schedule (reading A20): full steps for k+1 <= w; hybrid steps after.
+// Refresh after every step k >= w-1:
+//   G_{k+1} from the indicator (fraction mode A18; bootstrap A19 at k = w-1),
+//   Phi_{k+1} = POD_r([gamma_{k-w+1} - psi_k, ..., gamma_k - psi_k])   (lagged A14)
+//   psi_{k+1} = mean(gamma_{k-w+1..k})
+// Hybrid step k (O10-O13):
+//   masked RK3 on S-hat (and the band, for F) -> gappy y (Eq. 8, P = S-hat, A11)
+//   -> fill the complement with psi + Phi y -> indicator (A16/A17)
+//   -> seam filter (A21-A24) -> indicator on kept cells.
+#include <algorithm>
+#include <cmath>
+#include <deque>
+#include <vector>
+#include "common.hpp"
+
+using namespace orc;
+
+struct orc_run {
+  orc_grid g;
+  orc_params p;
+  Grid G;
+  int64_t k = 0;
+  std::deque<std::vector<double>> snaps;  // gamma_{k-w}..gamma_k (at most w+1)
+  std::vector<double> Phi, psi;           // Phi_{k+1} (D x reff), psi_{k+1}
+  std::vector<double> sigma;
+  int32_t reff = 0;
+  std::vector<uint8_t> mask_next, mask_used;
+  std::vector<double> eps, y;
+  int32_t ny_last = 0;
+  double dt = 0.0;
+  int64_t kept = 0;
+  int32_t sweeps[3] = {0, 0, 0};
+  orc_run(const orc_grid* gg, const orc_params* pp) : g(*gg), p(*pp), G(gg) {}
+};
+
+namespace {
+
+std::vector<double> mean_of(const std::deque<std::vector<double>>& s, size_t first, size_t count,
+                            int64_t D) {
+  std::vector<double> m(D, 0.0);
+  for (int64_t e = 0; e < D; ++e) {
+    double acc = 0.0;
+    for (size_t t = first; t < first + count; ++t) acc += s[t][e];
+    m[e] = acc / (double)count;
+  }
+  return m;
+}
+
+// Phi_{k+1}, psi_{k+1}, S from the current window (O14).  `lagged` = psi_k.
+void refresh_basis(orc_run* R, const std::vector<double>& psi_k) {
+  const int w = R->p.w;
+  const int64_t D = R->G.D;
+  const size_t ns = R->snaps.size();
+  // X = [gamma_{k-w+1} - psi_k, ..., gamma_k - psi_k]: the last w snapshots
+  std::vector<double> X((int64_t)w * D);
+  for (int j = 0; j < w; ++j) {
+    const auto& s = R->snaps[ns - w + j];
+    for (int64_t e = 0; e < D; ++e) X[(int64_t)j * D + e] = s[e] - psi_k[e];
+  }
+  const int r = std::min(R->p.r, w);
+  R->Phi.assign((int64_t)r * D, 0.0);
+  R->sigma.assign(w, 0.0);
+  std::vector<double> V((int64_t)w * w);
+  R->reff = orc_pod(X.data(), D, w, r, R->p.eig_rel_cutoff, R->Phi.data(), R->sigma.data(), V.data());
+  R->Phi.resize((int64_t)R->reff * D);
+  R->psi = mean_of(R->snaps, ns - w, w, D);
+}
+
+void reconstruct(const orc_run* R, const std::vector<double>& y, int64_t n, double* out) {
+  // out[v] = psi[v,n] + sum_i Phi[v*N+n, i] y_i
+  const int64_t N = R->G.N, D = R->G.D;
+  for (int v = 0; v < R->G.c; ++v) {
+    const int64_t e = v * N + n;
+    double acc = 0.0;
+    for (int i = 0; i < R->reff; ++i) acc += R->Phi[(int64_t)i * D + e] * y[i];
+    out[v] = R->psi[e] + acc;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+orc_run* orc_run_create(const orc_grid* g, const orc_params* p, const double* q0) {
+  auto* R = new orc_run(g, p);
+  R->snaps.emplace_back(q0, q0 + R->G.D);
+  R->mask_next.assign(R->G.N, 0);
+  R->mask_used.assign(R->G.N, 0);
+  R->eps.assign(R->G.N, 0.0);
+  return R;
+}
+
+void orc_run_destroy(orc_run* R) { delete R; }
+
+int32_t orc_run_step(orc_run* R, double dt_override) {
+  const Grid& G = R->G;
+  const int w = R->p.w;
+  const int64_t N = G.N, D = G.D;
+  const int64_t k = R->k + 1;
+  const std::vector<double>& prev = R->snaps.back();
+  R->dt = (dt_override > 0.0) ? dt_override : orc_dt(&R->g, prev.data());
+  std::vector<double> gam(D);
+  int32_t kind = 0;
+  if (k + 1 <= w) {
+    orc_full_step(&R->g, prev.data(), R->dt, gam.data());
+    std::fill(R->mask_used.begin(), R->mask_used.end(), 1);
+  } else {
+    kind = 1;
+    const std::vector<uint8_t>& S = R->mask_next;
+    R->mask_used = S;
+    // band B = (S (+) Q_W) \ S; the masked step runs on T = S u B (O10.1)
+    std::vector<uint8_t> sq(N), T(N);
+    orc_dilate_square(&R->g, S.data(), R->p.W, sq.data());
+    for (int64_t n = 0; n < N; ++n) T[n] = (S[n] || sq[n]) ? 1 : 0;
+    std::vector<double> F(D);
+    orc_masked_step(&R->g, prev.data(), R->dt, T.data(), R->p.h, F.data());
+    // gappy coordinates on the rows of S-hat (Eq. 8 with P = S-hat, A11, A12)
+    std::vector<int64_t> cells;
+    for (int64_t n = 0; n < N; ++n)
+      if (S[n]) cells.push_back(n);
+    const int64_t m = (int64_t)cells.size() * G.c;
+    const int reff = R->reff;
+    std::vector<double> A(m * (int64_t)reff), b(m);
+    for (size_t t = 0; t < cells.size(); ++t)
+      for (int v = 0; v < G.c; ++v) {
+        const int64_t row = (int64_t)t * G.c + v;
+        const int64_t e = v * N + cells[t];
+        b[row] = F[e] - R->psi[e];
+        for (int i = 0; i < reff; ++i) A[(int64_t)i * m + row] = R->Phi[(int64_t)i * D + e];
+      }
+    R->y.assign(reff, 0.0);
+    orc_lsq(A.data(), m, reff, b.data(), R->p.lsq_rel_cutoff, R->y.data());
+    R->ny_last = reff;
+    // assemble gamma_k: S-hat rows from the partial HDM, the rest psi + Phi y
+    std::fill(R->eps.begin(), R->eps.end(), 0.0);
+    for (int64_t n = 0; n < N; ++n) {
+      double rec[4];
+      reconstruct(R, R->y, n, rec);
+      if (S[n]) {
+        double e2 = 0.0;
+        for (int v = 0; v < G.c; ++v) {
+          gam[v * N + n] = F[v * N + n];
+          const double d = F[v * N + n] - rec[v];
+          e2 += d * d;
+        }
+        R->eps[n] = e2;  // P:363, summed over the cell's c variables (A16)
+      } else {
+        for (int v = 0; v < G.c; ++v) gam[v * N + n] = rec[v];
+      }
+    }
+    // seam filter, F valid on the band
+    std::vector<uint8_t> kept(N, 0);
+    R->kept = orc_seam_filter(&R->g, &R->p, gam.data(), F.data(), S.data(), kept.data(), R->sweeps);
+    for (int64_t n = 0; n < N; ++n)
+      if (kept[n]) {
+        double rec[4];
+        reconstruct(R, R->y, n, rec);
+        double e2 = 0.0;
+        for (int v = 0; v < G.c; ++v) {
+          const double d = gam[v * N + n] - rec[v];
+          e2 += d * d;
+        }
+        R->eps[n] = e2;
+      }
+    if (orc_positivity(&R->g, gam.data()) >= 0) {  // O11 escalation
+      orc_full_step(&R->g, prev.data(), R->dt, gam.data());
+      kind = 2;
+    }
+  }
+  R->snaps.push_back(std::move(gam));
+  while ((int)R->snaps.size() > w + 1) R->snaps.pop_front();
+  R->k = k;
+  if (k == w - 1) {
+    // offset bootstrap: psi_{w-1} = mean(gamma_0..gamma_{w-1})
+    const std::vector<double> psi0 = mean_of(R->snaps, R->snaps.size() - w, w, D);
+    refresh_basis(R, psi0);
+    // bootstrap indicator (A19): eps = sum_v [(I - Phi Phi^T)(gamma_{w-1} - psi_w)]^2
+    std::vector<double> d(D);
+    const auto& last = R->snaps.back();
+    for (int64_t e = 0; e < D; ++e) d[e] = last[e] - R->psi[e];
+    for (int i = 0; i < R->reff; ++i) {
+      const double c = dot(R->Phi.data() + (int64_t)i * D, d.data(), D);
+      for (int64_t e = 0; e < D; ++e) d[e] -= c * R->Phi[(int64_t)i * D + e];
+    }
+    for (int64_t n = 0; n < N; ++n) {
+      double e2 = 0.0;
+      for (int v = 0; v < G.c; ++v) e2 += d[v * N + n] * d[v * N + n];
+      R->eps[n] = e2;
+    }
+    orc_select(R->eps.data(), N, orc_n_g(R->p.f, N), R->mask_next.data());
+  } else if (k >= w) {
+    // psi_k = mean(gamma_{k-w..k-1}) (lagged centring, A14)
+    const std::vector<double> psik = mean_of(R->snaps, 0, w, D);
+    refresh_basis(R, psik);
+    orc_select(R->eps.data(), N, orc_n_g(R->p.f, N), R->mask_next.data());
+  }
+  return kind;
+}
+
+int64_t orc_run_k(const orc_run* R) { return R->k; }
+void orc_run_state(const orc_run* R, double* q) { std::copy(R->snaps.back().begin(), R->snaps.back().end(), q); }
+void orc_run_mask(const orc_run* R, uint8_t* m) { std::copy(R->mask_next.begin(), R->mask_next.end(), m); }
+void orc_run_mask_used(const orc_run* R, uint8_t* m) { std::copy(R->mask_used.begin(), R->mask_used.end(), m); }
+void orc_run_eps(const orc_run* R, double* e) { std::copy(R->eps.begin(), R->eps.end(), e); }
+int32_t orc_run_reff(const orc_run* R) { return R->reff; }
+void orc_run_basis(const orc_run* R, double* Phi) { std::copy(R->Phi.begin(), R->Phi.end(), Phi); }
+void orc_run_psi(const orc_run* R, double* psi) { std::copy(R->psi.begin(), R->psi.end(), psi); }
+void orc_run_sigma(const orc_run* R, double* S) { std::copy(R->sigma.begin(), R->sigma.end(), S); }
+int32_t orc_run_y(const orc_run* R, double* y) {
+  std::copy(R->y.begin(), R->y.end(), y);
+  return (int32_t)R->y.size();
+}
+double orc_run_dt(const orc_run* R) { return R->dt; }
+void orc_run_filter_stats(const orc_run* R, int64_t* kept, int32_t* sweeps) {
+  *kept = R->kept;
+  for (int i = 0; i < 3; ++i) sweeps[i] = R->sweeps[i];
+}
+
+void orc_run_set_window(orc_run* R, int64_t k, const double* snaps, int32_t nsnaps,
+                        const uint8_t* mask_next) {
+  const int64_t D = R->G.D;
+  R->snaps.clear();
+  for (int t = 0; t < nsnaps; ++t) R->snaps.emplace_back(snaps + (int64_t)t * D, snaps + (int64_t)(t + 1) * D);
+  R->k = k;
+  const int w = R->p.w;
+  const std::vector<double> psik = mean_of(R->snaps, 0, w, D);  // gamma_{k-w..k-1}
+  refresh_basis(R, psik);
+  std::copy(mask_next, mask_next + R->G.N, R->mask_next.begin());
+}
+
+}  // extern "C"

@@ -1,0 +1,190 @@
+// sampling_filter.cpp -- oracle: sampling sets, indicator selection, Shapiro seam filter.
+// TEST INFRASTRUCTURE ONLY (see oracle.h).
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include "common.hpp"
+
+using namespace orc;
+
+extern "C" {
+
+// Neighbors (Fig. 1): cross C_h = {(+-a,0),(0,+-b): a,b <= h} (O10.1).
+// Transmissive grids clip at the boundary, periodic grids wrap (reading A9).
+void orc_dilate_cross(const orc_grid* g, const uint8_t* in, int32_t h, uint8_t* out) {
+  Grid G(g);
+  for (int j = 0; j < G.ny; ++j)
+    for (int i = 0; i < G.nx; ++i) {
+      bool any = false;
+      for (int a = -h; a <= h && !any; ++a) {
+        const int ii = i + a;
+        if (G.bc == 0 && (ii < 0 || ii >= G.nx)) continue;
+        if (in[(int64_t)j * G.nx + G.ix(ii)]) any = true;
+      }
+      if (G.dim == 2)
+        for (int b = -h; b <= h && !any; ++b) {
+          const int jj = j + b;
+          if (G.bc == 0 && (jj < 0 || jj >= G.ny)) continue;
+          if (in[(int64_t)G.iy(jj) * G.nx + i]) any = true;
+        }
+      out[(int64_t)j * G.nx + i] = any ? 1 : 0;
+    }
+}
+
+// square Q_W = {(a,b): |a|,|b| <= W} (O13 band, reading A21)
+void orc_dilate_square(const orc_grid* g, const uint8_t* in, int32_t W, uint8_t* out) {
+  Grid G(g);
+  const int Wy = (G.dim == 2) ? W : 0;
+  for (int j = 0; j < G.ny; ++j)
+    for (int i = 0; i < G.nx; ++i) {
+      bool any = false;
+      for (int b = -Wy; b <= Wy && !any; ++b) {
+        const int jj = j + b;
+        if (G.bc == 0 && (jj < 0 || jj >= G.ny)) continue;
+        for (int a = -W; a <= W && !any; ++a) {
+          const int ii = i + a;
+          if (G.bc == 0 && (ii < 0 || ii >= G.nx)) continue;
+          if (in[(int64_t)G.iy(jj) * G.nx + G.ix(ii)]) any = true;
+        }
+      }
+      out[(int64_t)j * G.nx + i] = any ? 1 : 0;
+    }
+}
+
+int64_t orc_n_g(double f, int64_t N) { return (int64_t)std::ceil(f * (double)N); }
+
+// H8 / O15 (reading A18): order cells by descending eps, ties by
+// ascending index; G = the first min(n_g, #{eps>0}) cells with eps > 0.
+int64_t orc_select(const double* eps, int64_t N, int64_t n_g, uint8_t* mask_out) {
+  std::vector<int64_t> idx;
+  for (int64_t n = 0; n < N; ++n) {
+    mask_out[n] = 0;
+    if (eps[n] > 0.0) idx.push_back(n);
+  }
+  std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return eps[a] > eps[b]; });
+  const int64_t k = std::min<int64_t>(n_g, (int64_t)idx.size());
+  for (int64_t t = 0; t < k; ++t) mask_out[idx[t]] = 1;
+  return k;
+}
+
+// RRE-delta rule: smallest n_g with RRE(n_g) >= delta.
+int64_t orc_select_rre(const double* eps, int64_t N, double delta, uint8_t* mask_out) {
+  std::vector<int64_t> idx(N);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return eps[a] > eps[b]; });
+  CSum tot;
+  for (int64_t n = 0; n < N; ++n) { mask_out[n] = 0; tot.add(eps[n]); }
+  const double total = tot.value();
+  if (!(total > 0.0)) return 0;
+  CSum run;
+  int64_t ng = 0;
+  for (int64_t t = 0; t < N; ++t) {
+    run.add(eps[idx[t]]);
+    mask_out[idx[t]] = 1;
+    ng = t + 1;
+    if (run.value() / total >= delta) break;
+  }
+  return ng;
+}
+
+// Shapiro stencils (reading A24): order 2 (1,2,1)/4, 4 (-1,4,10,4,-1)/16,
+// 6 (1,-6,15,44,15,-6,1)/64.  Line ends: zeroth-order extrapolation or wrap.
+static int shapiro_coef(int order, const double** c, double* den) {
+  static const double c2[3] = {1, 2, 1};
+  static const double c4[5] = {-1, 4, 10, 4, -1};
+  static const double c6[7] = {1, -6, 15, 44, 15, -6, 1};
+  if (order == 2) { *c = c2; *den = 4.0; return 1; }
+  if (order == 4) { *c = c4; *den = 16.0; return 2; }
+  *c = c6; *den = 64.0; return 3;
+}
+
+void orc_shapiro_1d(const double* line, int32_t n, int32_t order, int32_t periodic, double* out) {
+  const double* c;
+  double den;
+  const int rad = shapiro_coef(order, &c, &den);
+  for (int i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int m = -rad; m <= rad; ++m) {
+      int k = i + m;
+      if (periodic) k = ((k % n) + n) % n;
+      else k = k < 0 ? 0 : (k >= n ? n - 1 : k);
+      s += c[m + rad] * line[k];
+    }
+    out[i] = s / den;
+  }
+}
+
+// H7 / O13 seam filter (readings A21-A24).
+int64_t orc_seam_filter(const orc_grid* g, const orc_params* p, double* v, const double* F,
+                        const uint8_t* mask_S, uint8_t* kept_out, int32_t* sweeps_out) {
+  Grid G(g);
+  std::vector<uint8_t> sq(G.N), B(G.N), kept(G.N, 0);
+  orc_dilate_square(g, mask_S, p->W, sq.data());
+  std::vector<int64_t> band;
+  for (int64_t n = 0; n < G.N; ++n) {
+    B[n] = (sq[n] && !mask_S[n]) ? 1 : 0;
+    if (B[n]) band.push_back(n);
+  }
+  std::vector<double> vp(G.D), vpp(G.D);
+  for (int oi = 0; oi < p->n_filter_orders; ++oi) {
+    const int order = p->filter_orders[oi];
+    const double* c;
+    double den;
+    const int rad = shapiro_coef(order, &c, &den);
+    int sweeps = 0;
+    for (int sw = 0; sw < p->filter_max_sweeps; ++sw) {
+      ++sweeps;
+      // v' = S^x(v) on B; off-B values unchanged (read-only)
+      std::copy(v, v + G.D, vp.begin());
+      for (int64_t n : band) {
+        const int i = (int)(n % G.nx), j = (int)(n / G.nx);
+        for (int var = 0; var < G.c; ++var) {
+          double s = 0.0;
+          for (int m = -rad; m <= rad; ++m)
+            s += c[m + rad] * v[var * G.N + (int64_t)j * G.nx + G.ix(i + m)];
+          vp[var * G.N + n] = s / den;
+        }
+      }
+      // v'' = S^y(v') on B (2D only)
+      std::copy(vp.begin(), vp.end(), vpp.begin());
+      if (G.dim == 2)
+        for (int64_t n : band) {
+          const int i = (int)(n % G.nx), j = (int)(n / G.nx);
+          for (int var = 0; var < G.c; ++var) {
+            double s = 0.0;
+            for (int m = -rad; m <= rad; ++m)
+              s += c[m + rad] * vp[var * G.N + (int64_t)G.iy(j + m) * G.nx + i];
+            vpp[var * G.N + n] = s / den;
+          }
+        }
+      // residual gate: r = max_var |v - F| per cell; keep where r_new < r_old
+      int64_t nkept = 0;
+      double maxdec = 0.0;
+      for (int64_t n : band) {
+        double rold = 0.0, rnew = 0.0;
+        for (int var = 0; var < G.c; ++var) {
+          const int64_t e = var * G.N + n;
+          rold = std::max(rold, std::fabs(v[e] - F[e]));
+          rnew = std::max(rnew, std::fabs(vpp[e] - F[e]));
+        }
+        if (rnew < rold) {
+          ++nkept;
+          kept[n] = 1;
+          maxdec = std::max(maxdec, (rold - rnew) / rold);
+          for (int var = 0; var < G.c; ++var) v[var * G.N + n] = vpp[var * G.N + n];
+        }
+      }
+      if (nkept == 0) break;                  // empty keep-set: stop this order
+      if (maxdec < p->filter_eps) break;      // relative decrease < eps_f
+    }
+    if (sweeps_out) sweeps_out[oi] = sweeps;
+  }
+  int64_t total = 0;
+  for (int64_t n = 0; n < G.N; ++n) {
+    if (kept_out) kept_out[n] = kept[n];
+    total += kept[n];
+  }
+  return total;
+}
+
+}  // extern "C"

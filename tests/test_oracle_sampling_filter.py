@@ -1,0 +1,195 @@
+"""Pins of the oracle's sampling sets, indicator selection and seam
+filter.  Brute-force set algebra, SPEC hand examples and the closed-form
+Shapiro response 1 - sin^{2n}(theta/2)."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    out = {}
+    with open(os.path.join(GOLDEN, name)) as fh:
+        for line in fh:
+            line = line.split("#")[0].strip()
+            if line:
+                k, *v = line.split()
+                out.setdefault(k, []).append(v)
+    return out
+
+
+def _wl(inputs, **kw):
+    base = dict(name="t", dim=2, nx=10, ny=10, bc=0, recon=2, w=4, r=2, f=0.2, seed=3, h=2, W=3)
+    base.update(kw)
+    return inputs.Workload(**base)
+
+
+# ---------------- dilation / sets ----------------
+def test_dilation_spec_examples(orc, inputs):
+    for row in _golden("spec_examples.txt")["dilate1d"]:
+        N, g, h = int(row[1]), int(row[3]), int(row[5])
+        exp = sorted(int(x) for x in row[7:])
+        wl = _wl(inputs, dim=1, nx=N, ny=1)
+        m = np.zeros(N, np.uint8)
+        m[g] = 1
+        out = orc.dilate_cross(wl, m, h)
+        assert sorted(np.nonzero(out)[0].tolist()) == exp
+
+
+def _brute_dilate(wl, m, offsets):
+    out = np.zeros(wl.N, np.uint8)
+    for n in range(wl.N):
+        i, j = n % wl.nx, n // wl.nx
+        for a, b in offsets:
+            ii, jj = i + a, j + b
+            if wl.bc == 1:
+                ii %= wl.nx
+                jj %= wl.ny
+            elif not (0 <= ii < wl.nx and 0 <= jj < wl.ny):
+                continue
+            if m[jj * wl.nx + ii]:
+                out[n] = 1
+    return out
+
+
+@pytest.mark.parametrize("bc", [0, 1])
+def test_dilation_brute_force_and_set_identities(orc, inputs, bc):
+    wl = _wl(inputs, bc=bc)
+    rng = np.random.default_rng(5 + bc)
+    for trial in range(5):
+        S = (rng.random(wl.N) < 0.07).astype(np.uint8)
+        for h in (1, 2, 3):
+            cross = [(a, 0) for a in range(-h, h + 1)] + [(0, b) for b in range(-h, h + 1)]
+            assert np.array_equal(orc.dilate_cross(wl, S, h), _brute_dilate(wl, S, cross))
+        sq = [(a, b) for a in range(-3, 4) for b in range(-3, 4)]
+        assert np.array_equal(orc.dilate_square(wl, S, 3), _brute_dilate(wl, S, sq))
+        # S-hat u S-breve = all, S-hat n S-breve = 0, S-tilde subset of S-breve
+        A = orc.dilate_cross(wl, S, 2)
+        Sb = 1 - S
+        St = A & Sb
+        assert np.all((S | Sb) == 1) and np.all((S & Sb) == 0) and np.all(St <= Sb)
+
+
+# ---------------- selection ----------------
+def test_n_g(orc):
+    assert orc.n_g(0.10, 1000) == 100
+    assert orc.n_g(0.15, 65536) == 9831
+    assert orc.n_g(0.10, 2048 * 2048) == 419431
+    assert orc.n_g(0.05, 2048 * 2048) == 209716
+
+
+def _brute_select(eps, ng):
+    order = sorted(range(len(eps)), key=lambda i: (-eps[i], i))
+    chosen = [i for i in order if eps[i] > 0][:ng]
+    m = np.zeros(len(eps), np.uint8)
+    m[chosen] = 1
+    return m
+
+
+def test_select_vs_brute_force_with_ties(orc):
+    rng = np.random.default_rng(9)
+    for trial in range(40):
+        N = int(rng.integers(1, 300))
+        eps = np.round(rng.random(N) * 5) / 5.0 * (rng.random(N) < 0.7)  # many ties and zeros
+        ng = int(rng.integers(0, N + 3))
+        m, k = orc.select(eps, ng)
+        assert np.array_equal(m, _brute_select(eps, ng))
+        assert k == min(ng, int((eps > 0).sum()))
+    m, k = orc.select(np.zeros(50), 10)
+    assert k == 0 and m.sum() == 0
+
+
+def test_select_rre_examples_and_minimality(orc):
+    gd = _golden("spec_examples.txt")["rre"]
+    for row in gd:
+        eps = np.array([float(x) for x in row[:4]])
+        delta = float(row[5])
+        m, k = orc.select_rre(eps, delta)
+        assert k == int(row[7])
+    rng = np.random.default_rng(4)
+    for _ in range(200):
+        eps = rng.random(int(rng.integers(1, 60))) ** 3
+        delta = float(rng.uniform(0.05, 1.0))
+        m, k = orc.select_rre(eps, delta)
+        srt = np.sort(eps)[::-1]
+        frac = np.cumsum(srt) / srt.sum()
+        assert frac[k - 1] >= delta - 1e-12
+        assert k == 1 or frac[k - 2] < delta + 1e-12
+
+
+# ---------------- Shapiro filter (A24) ----------------
+@pytest.mark.parametrize("order", [2, 4, 6])
+def test_shapiro_dc_nyquist_response(orc, order):
+    n = order // 2
+    const = np.full(17, 3.25)
+    np.testing.assert_array_equal(orc.shapiro_1d(const, order), const)
+    nyq = np.array([(-1.0) ** i for i in range(32)])
+    out = orc.shapiro_1d(nyq, order, periodic=True)
+    assert np.max(np.abs(out)) <= 1e-15
+    # response at theta = pi/2: 1 - sin^{2n}(pi/4) = 1 - 2^{-n}
+    L = 40
+    wave = np.cos(np.pi * np.arange(L) / 2)
+    out = orc.shapiro_1d(wave, order, periodic=True)
+    np.testing.assert_allclose(out, (1 - 2.0 ** (-n)) * wave, atol=1e-15)
+    # general theta: 1 - sin^{2n}(theta/2)
+    th = 2 * np.pi * 5 / L
+    wave = np.cos(th * np.arange(L))
+    out = orc.shapiro_1d(wave, order, periodic=True)
+    np.testing.assert_allclose(out, (1 - math.sin(th / 2) ** (2 * n)) * wave, atol=1e-14)
+
+
+def test_shapiro_spike_readback(orc):
+    exp = [float(x) for x in _golden("spec_examples.txt")["shapiro2_spike"][0][1:]]
+    line = np.zeros(11)
+    line[5] = 1.0
+    out = orc.shapiro_1d(line, 2)
+    np.testing.assert_array_equal(out[4:7], exp)
+    out6 = orc.shapiro_1d(line, 6)
+    np.testing.assert_allclose(out6[2:9], np.array([1, -6, 15, 44, 15, -6, 1]) / 64.0, rtol=0, atol=0)
+    # zeroth-order extrapolation at the ends: a step at the boundary stays flat
+    step = np.array([2.0] * 4 + [0.0] * 4)
+    np.testing.assert_array_equal(orc.shapiro_1d(step, 2)[:3], [2.0, 2.0, 2.0])
+
+
+# ---------------- seam filter ----------------
+def _filter_case(orc, inputs, bc, seed):
+    wl = _wl(inputs, nx=28, ny=20, bc=bc, seed=seed)
+    rng = np.random.default_rng(seed)
+    F = inputs.initial_condition(wl, "random")
+    v = F * (1.0 + 0.05 * rng.standard_normal(F.shape))
+    S = np.zeros(wl.N, np.uint8)
+    S[rng.choice(wl.N, 12, replace=False)] = 1
+    v[:, S == 1] = F[:, S == 1]  # S-hat rows are exact HDM rows (residual 0)
+    return wl, v, F, S
+
+
+@pytest.mark.parametrize("bc,seed", [(0, 1), (1, 2), (0, 3)])
+def test_seam_filter_invariants(orc, inputs, bc, seed):
+    wl, v, F, S = _filter_case(orc, inputs, bc, seed)
+    out, kept, sweeps = orc.seam_filter(wl, v, F, S)
+    B = orc.dilate_square(wl, S, wl.W) & (1 - S)
+    assert np.all(kept <= B)                       # only band cells change
+    assert np.array_equal(out[:, B == 0], v[:, B == 0])
+    assert np.array_equal(out[:, S == 1], v[:, S == 1])
+    r_in = np.max(np.abs(v - F), axis=0)
+    r_out = np.max(np.abs(out - F), axis=0)
+    assert np.all(r_out <= r_in + 1e-14)           # gate: per-cell residual never increases
+    assert np.all(r_out[kept == 1] < r_in[kept == 1])
+    assert all(1 <= s <= wl.filter_max_sweeps for s in sweeps)
+    assert kept.sum() > 0
+
+
+def test_seam_filter_degenerate_bands(orc, inputs):
+    wl, v, F, S = _filter_case(orc, inputs, 0, 4)
+    for Sd in (np.zeros(wl.N, np.uint8), np.ones(wl.N, np.uint8)):
+        out, kept, _ = orc.seam_filter(wl, v, F, Sd)
+        if Sd.sum() == 0:
+            assert np.array_equal(out, v) and kept.sum() == 0
+        else:
+            assert np.array_equal(out, v) and kept.sum() == 0
+    # residual already zero everywhere: nothing can strictly decrease
+    out, kept, _ = orc.seam_filter(wl, F, F, S)
+    assert np.array_equal(out, F) and kept.sum() == 0
