@@ -1,0 +1,150 @@
+/* hrom.h -- C ABI of libhrom, the B200 (sm_100a) hybrid-snapshot step library.
+ *
+ * Implements the data-parallel hot path of Zucatti & Zahr, "An adaptive,
+ * training-free reduced-order model for convection-dominated problems based on
+ * hybrid snapshots" (arXiv 2301.01718; /root/reference/PAPER.md, cited "P:<line>"),
+ * in its explicit variant (SSP-RK3 + MUSCL-minmod/Rusanov, BASELINE.json configs).
+ *
+ * Conventions (all entry points):
+ *  - State layout: SoA fp64 q[v*N + n], v = rho, rho*u, [rho*v,] rho*E, n = j*nx + i.
+ *  - Masks: N-bit bitmaps, row-padded: word j*ceil(nx/32) + i/32, bit i%32 (1 = cell selected).
+ *  - Pointers named dev_* must be device pointers; pointers named any_* may be
+ *    host (pageable or pinned) or device pointers (copied with cudaMemcpyDefault).
+ *    Caller-owned memory is never freed by the library; all workspaces are
+ *    allocated in hrom_create and freed in hrom_destroy; step calls never allocate.
+ *  - Asynchrony: every call enqueues on the context's stream and returns; argument
+ *    and ordering errors are returned synchronously (HROM_E_INVALID, HROM_E_STATE).
+ *    Device-side failures (non-positive density/pressure, NaN) are latched and
+ *    returned by hrom_sync (HROM_E_POSITIVITY) with the lowest cell in hrom_error_cell.
+ *  - Determinism: bitwise run-to-run reproducible (no floating-point atomics).
+ *  - Threading: a context is used by one host thread at a time.
+ */
+#ifndef HROM_H
+#define HROM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hrom_ctx hrom_ctx;
+
+typedef enum {
+  HROM_OK = 0,
+  HROM_E_INVALID = 1,     /* bad argument (e.g. r > w, h < stencil radius, f outside (0,1]) */
+  HROM_E_STATE = 2,       /* call out of order (e.g. hybrid step before the first basis) */
+  HROM_E_POSITIVITY = 3,  /* latched device error: rho <= 0 or p <= 0 or NaN */
+  HROM_E_RANK = 4,        /* gappy least-squares matrix is zero */
+  HROM_E_CUDA = 5,        /* CUDA runtime error */
+  HROM_E_NOMEM = 6        /* device allocation failed in hrom_create */
+} hrom_status;
+
+/* Grid: cell-centred Cartesian mesh on [x0,x1] x [y0,y1] (ny = 1 when dim = 1). */
+typedef struct {
+  int32_t dim, nx, ny;
+  double x0, x1, y0, y1;
+  int32_t bc;     /* 0 transmissive (zeroth-order ghosts), 1 periodic */
+  int32_t recon;  /* 1 first order, 2 MUSCL-minmod */
+} hrom_grid;
+
+/* Method parameters (notation of DESIGN.md §1 / SURVEY §0.4). */
+typedef struct {
+  int32_t window;            /* w: snapshots in the POD window */
+  int32_t rank;              /* r: POD modes ("m"), r <= w */
+  int32_t halo;              /* h: per-RK-stage stencil halo, h >= recon */
+  int32_t band;              /* W: seam-band half width (square), reading A21 */
+  int32_t filter_orders[3];  /* Shapiro cascade, default {2,4,6} */
+  int32_t n_filter_orders;
+  int32_t filter_max_sweeps; /* j_max^f = 10 */
+  double filter_eps;         /* eps_f = 1e-2, relative decrease (A23) */
+  double eig_rel_cutoff;     /* keep POD modes with lambda_i >= cut * lambda_1 (1e-8, A15) */
+  double lsq_rel_cutoff;     /* pinv cut on lambda(A^T A) (1e-12, A13) */
+  double sample_fraction;    /* f: n_g = ceil(f N) HDM cells per hybrid step (A18) */
+  int32_t gram_mode;         /* 0 incremental shifted Gram (default), 1 full DMMA Gram every step */
+  int32_t rebase_period;     /* steps between shifted-Gram re-bases (<= 0: w) */
+} hrom_params;
+
+/* Create a context for one grid.  cuda_stream: a cudaStream_t (NULL = legacy default).
+ * Allocates: ring of w+2 snapshots, Gram shift, RK stage buffers, indicator, masks,
+ * lists, small-matrix scratch (about (w+8) * 8 * c * N bytes). */
+hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const hrom_params* params,
+                        void* cuda_stream, hrom_ctx** out);
+void hrom_destroy(hrom_ctx* ctx);
+
+/* gamma_0 := q.  Resets the step counter k to 0 and drops any basis. */
+hrom_status hrom_set_state(hrom_ctx* ctx, const double* any_q);
+/* q := gamma_k (the latest snapshot). */
+hrom_status hrom_get_state(hrom_ctx* ctx, double* any_q);
+
+/* H1+H2: gamma_{k+1} = SSP-RK3 full HDM step of gamma_k (explicit F_k).
+ * dt_override > 0 replaces the CFL rule dt = cfl / max_n[(|u|+c)/dx + (|v|+c)/dy].
+ * dev_dt_out (nullable, device) receives the dt used. */
+hrom_status hrom_full_step(hrom_ctx* ctx, double dt_override, double* dev_dt_out);
+
+/* H1, H3-H7: hybrid step k+1: masked RK3 on S-hat (+ its band, for the
+ * filter residual), gappy coordinates y (Eq. 8, P = S-hat), fill of the complement
+ * with psi + Phi y, indicator eps, seam filter.
+ * dev_mask: S-hat bitmap, or NULL to use the sets built by the last hrom_sample.
+ * Requires a basis (hrom_update_basis after step >= w-1). */
+hrom_status hrom_hybrid_step(hrom_ctx* ctx, const uint32_t* dev_mask, double dt_override,
+                             double* dev_dt_out);
+
+/* H9-H12: push gamma_k into the window; Gram (incremental shifted or full DMMA),
+ * lagged centring (Eq. 9 / P:585-587), thin eigen, r_eff; psi_{k+1}.
+ * No-op while k < w-1.  At k = w-1 it also sets the bootstrap indicator (reading A19). */
+hrom_status hrom_update_basis(hrom_ctx* ctx);
+
+/* H8: S-hat_{k+1} = top ceil(f N) cells of eps > 0, ties by ascending index,
+ * then builds the stage sets, the seam band and their compacted lists.
+ * dev_eps: N indicator values, or NULL for the context's own indicator.
+ * Outputs (nullable, device): mask bitmap, ascending cell list, count (int32). */
+hrom_status hrom_sample(hrom_ctx* ctx, double fraction, const double* dev_eps, uint32_t* dev_mask_out,
+                        int32_t* dev_list_out, int32_t* dev_count_out);
+
+/* H4-H6 standalone (gappy POD): with the current basis (Phi_{k+1}, psi_{k+1}), take the
+ * values of dev_v on the cells of S-hat (dev_mask or the current sets) as HDM values,
+ * y = argmin ||Phi_S y - (v - psi)_S|| (min-norm), and overwrite dev_v off S-hat
+ * with psi + Phi y.  dev_y_out (nullable): y (r_eff values).
+ * dev_eps_out (nullable): per-cell indicator on S-hat, 0 elsewhere. */
+hrom_status hrom_reconstruct(hrom_ctx* ctx, const uint32_t* dev_mask, double* dev_v, double* dev_y_out,
+                             double* dev_eps_out);
+
+/* H7 standalone: seam filter of dev_v on the band (S-hat (+) Q_W) \ S-hat against the
+ * residual reference dev_F (readings A21-A24).  dev_kept_out (nullable):
+ * N bytes, 1 where the filtered value was kept in some sweep. */
+hrom_status hrom_filter(hrom_ctx* ctx, const uint32_t* dev_mask, double* dev_v, const double* dev_F,
+                        uint8_t* dev_kept_out);
+
+/* One step of Algorithm 1 (explicit, z = infinity): full step while k+1 <= w,
+ * hybrid step afterwards, then update_basis + sample while k >= w-1. */
+hrom_status hrom_step(hrom_ctx* ctx, double dt_override);
+
+/* Synchronise the stream; returns latched device errors. */
+hrom_status hrom_sync(hrom_ctx* ctx);
+int64_t hrom_error_cell(const hrom_ctx* ctx);        /* lowest offending cell, or -1 */
+int64_t hrom_step_index(const hrom_ctx* ctx);        /* k of the latest snapshot */
+int32_t hrom_effective_rank(hrom_ctx* ctx);          /* r_eff of the current basis (syncs) */
+const char* hrom_status_string(hrom_status s);
+
+/* ---- test / replay hooks ---- */
+/* Window gamma_{k-w}..gamma_k (w+1 snapshots, oldest first, D each, any_ memory) and the
+ * mask S-hat_{k+1}; builds the basis as hrom_update_basis would after step k (k >= w). */
+hrom_status hrom_set_window(hrom_ctx* ctx, int64_t k, const double* any_snaps, int32_t nsnaps,
+                            const uint32_t* any_mask_next);
+/* Phi_{k+1} (D x r_eff, column-major) and psi_{k+1} (D), materialised by the lift kernel. */
+hrom_status hrom_get_basis(hrom_ctx* ctx, double* dev_phi, double* dev_psi);
+hrom_status hrom_get_indicator(hrom_ctx* ctx, double* any_eps);      /* N values */
+hrom_status hrom_get_mask(hrom_ctx* ctx, uint32_t* any_mask);        /* current S-hat bitmap */
+hrom_status hrom_get_y(hrom_ctx* ctx, double* any_y);                /* y of the last gappy solve (r) */
+hrom_status hrom_get_eigen(hrom_ctx* ctx, double* any_lambda);       /* eigenvalues of X^T X (w) */
+int64_t hrom_mask_words(const hrom_ctx* ctx);                        /* words per bitmap */
+/* Gram of the listed ring columns shifted by a reference: C = (S - rho 1^T)^T (S - rho 1^T)
+ * over D rows with FP64 DMMA tensor cores (K11).  dev_cols: ncol device pointers (device array),
+ * dev_rho (nullable = 0), dev_C: ncol*ncol output. Standalone op (config 5). */
+hrom_status hrom_gram(hrom_ctx* ctx, const double* const* dev_cols, int32_t ncol, int64_t rows,
+                      const double* dev_rho, double* dev_C);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

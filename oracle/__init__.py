@@ -77,6 +77,7 @@ def lib():
             "orc_svd": (None, [d, i64, i32, d, d, d]),
             "orc_pod": (i32, [d, i64, i32, i32, C.c_double, d, d, d]),
             "orc_shapiro_1d": (None, [d, i32, i32, i32, d]),
+            "orc_gram": (None, [d, i32, i64, d, d]),
             "orc_seam_filter": (i64, [P(Grid), P(Params), d, d, u8, u8, P(C.c_int32)]),
             "orc_run_create": (C.c_void_p, [P(Grid), P(Params), d]),
             "orc_run_destroy": (None, [C.c_void_p]),
@@ -258,6 +259,16 @@ def pod(X, r, cut=1e-8):
     V = np.zeros((w, w))
     reff = lib().orc_pod(_d(Xt), m, w, r, cut, _d(Phi), _d(S), _d(V))
     return Phi[:reff].T.copy(), S, V.T.copy(), reff
+
+
+def gram(S, rho=None):
+    """S: (ncol, rows) array; C = (S - rho)(S - rho)^T with compensated sums."""
+    S = _c(S)
+    ncol, rows = S.shape
+    C_ = np.zeros((ncol, ncol))
+    r = None if rho is None else _c(rho)
+    lib().orc_gram(_d(S), ncol, rows, None if r is None else _d(r), _d(C_))
+    return C_
 
 
 def shapiro_1d(line, order, periodic=False):

@@ -187,4 +187,18 @@ int32_t orc_lsq(const double* A, int64_t m, int32_t n, const double* b, double c
   return rank;
 }
 
+void orc_gram(const double* S, int32_t ncol, int64_t rows, const double* rho, double* C) {
+  std::vector<double> a(rows), b(rows);
+  for (int i = 0; i < ncol; ++i)
+    for (int j = i; j < ncol; ++j) {
+      CSum s;
+      for (int64_t e = 0; e < rows; ++e) {
+        const double x = S[(int64_t)i * rows + e] - (rho ? rho[e] : 0.0);
+        const double y = S[(int64_t)j * rows + e] - (rho ? rho[e] : 0.0);
+        s.add(x * y);
+      }
+      C[(int64_t)i * ncol + j] = C[(int64_t)j * ncol + i] = s.value();
+    }
+}
+
 }  // extern "C"

@@ -82,6 +82,10 @@ void orc_svd(const double* X, int64_t m, int32_t n, double* U, double* S, double
 int32_t orc_pod(const double* X, int64_t m, int32_t w, int32_t r, double cut,
                 double* Phi, double* S, double* V);
 
+/* Gram of shifted columns: C_ij = sum_e (S_ie - rho_e)(S_je - rho_e), S: ncol x rows
+ * (row-major per column), rho nullable.  The snapshot Gram of the POD remark P:634. */
+void orc_gram(const double* S, int32_t ncol, int64_t rows, const double* rho, double* C);
+
 /* ---- Shapiro filters and seam filter (A21-A24) ---- */
 void orc_shapiro_1d(const double* line, int32_t n, int32_t order, int32_t periodic, double* out);
 /* seam filter on band B = (S (+) Q_W) \ S. v is updated in place (SoA state).

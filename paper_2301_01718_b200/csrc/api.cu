@@ -1,0 +1,473 @@
+// api.cu -- the C ABI of libhrom (include/hrom.h): context, schedule and orchestration.
+//
+// One hybrid step (Algorithm 1, explicit variant, z = infinity):
+//   H1 dt -> H3 masked RK3 on A1 / A2 / T = S-hat u B -> H4 gathered Gram [X_S, b] (DMMA)
+//   -> H5 one-CTA pinv solve (y, c = A y) -> H6+H9+H10 fused fill / indicator / Gram-row pass
+//   -> H7 seam filter (cooperative) -> band Gram rows
+// then hrom_update_basis (H10 reduce / re-base, H11 eigen) and hrom_sample (H8).
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include "internal.cuh"
+
+namespace hrom {
+hrom_status launch_eps_all(hrom_ctx* c);
+int filter_occupancy();
+
+namespace {
+
+__global__ void zvec_kernel(const double* __restrict__ A, const double* __restrict__ lam,
+                            const int32_t* __restrict__ reffp, int w, double* __restrict__ z) {
+  // z = e_{w-1} - V_r V_r^T e_{w-1}, V_r[:, j] = A[:, j] sqrt(lam_j)  (bootstrap indicator, A19)
+  const int re = *reffp;
+  for (int i = threadIdx.x; i < w; i += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < re; ++j) {
+      const double sl = sqrt(lam[j]);
+      s += (A[j * w + i] * sl) * (A[j * w + (w - 1)] * sl);
+    }
+    z[i] = (i == w - 1 ? 1.0 : 0.0) - s;
+  }
+}
+
+template <typename T>
+hrom_status dalloc(T** p, size_t n) {
+  if (cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) return HROM_E_NOMEM;
+  return HROM_OK;
+}
+
+Win window_at(const hrom_ctx* c, int64_t k) {
+  Win W{};
+  W.w = c->w;
+  if (k == c->w - 1) {
+    W.nU = c->w;
+    for (int i = 0; i < c->w; ++i) W.slot[i] = c->slot_of(i);
+  } else {
+    W.nU = c->w + 1;
+    for (int i = 0; i <= c->w; ++i) W.slot[i] = c->slot_of(k - c->w + i);
+  }
+  return W;
+}
+
+}  // namespace
+}  // namespace hrom
+
+using namespace hrom;
+
+extern "C" {
+
+const char* hrom_status_string(hrom_status s) {
+  switch (s) {
+    case HROM_OK: return "ok";
+    case HROM_E_INVALID: return "invalid argument";
+    case HROM_E_STATE: return "call out of order";
+    case HROM_E_POSITIVITY: return "non-positive density or pressure";
+    case HROM_E_RANK: return "zero least-squares matrix";
+    case HROM_E_CUDA: return "CUDA error";
+    case HROM_E_NOMEM: return "out of device memory";
+  }
+  return "unknown";
+}
+
+hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const hrom_params* p, void* stream,
+                        hrom_ctx** out) {
+  if (!grid || !p || !out) return HROM_E_INVALID;
+  *out = nullptr;
+  const int dim = grid->dim;
+  if (dim != 1 && dim != 2) return HROM_E_INVALID;
+  const int ny = dim == 1 ? 1 : grid->ny;
+  if (grid->nx < 1 || ny < 1 || (grid->bc != 0 && grid->bc != 1) || (grid->recon != 1 && grid->recon != 2))
+    return HROM_E_INVALID;
+  if ((int64_t)grid->nx * ny * (dim + 2) >= (int64_t)INT32_MAX * 2) return HROM_E_INVALID;
+  if (!(gamma > 1.0) || !(cfl > 0.0)) return HROM_E_INVALID;
+  if (p->window < 2 || p->window > kMaxW || p->rank < 1 || p->rank > p->window || p->rank > kMaxR)
+    return HROM_E_INVALID;
+  if (p->halo < grid->recon || p->halo > 16 || p->band < 0 || p->band > 16) return HROM_E_INVALID;
+  if (p->n_filter_orders < 0 || p->n_filter_orders > 3 || p->filter_max_sweeps < 0) return HROM_E_INVALID;
+  for (int i = 0; i < p->n_filter_orders; ++i)
+    if (p->filter_orders[i] != 2 && p->filter_orders[i] != 4 && p->filter_orders[i] != 6) return HROM_E_INVALID;
+  if (!(p->sample_fraction > 0.0 && p->sample_fraction <= 1.0)) return HROM_E_INVALID;
+  if (p->gram_mode != 0 && p->gram_mode != 1) return HROM_E_INVALID;
+
+  hrom_ctx* c = new hrom_ctx();
+  c->P = *p;
+  if (c->P.rebase_period <= 0) c->P.rebase_period = p->window;
+  c->w = p->window;
+  c->r = p->rank;
+  c->nslots = c->w + 2;
+  c->st = (cudaStream_t)stream;
+  Geo& g = c->g;
+  g.dim = dim;
+  g.nx = grid->nx;
+  g.ny = ny;
+  g.c = dim + 2;
+  g.bc = grid->bc;
+  g.recon = grid->recon;
+  g.wpr = (grid->nx + 31) / 32;
+  g.N = (int64_t)g.nx * g.ny;
+  g.D = g.c * g.N;
+  g.Dp = (g.D + 31) / 32 * 32;
+  g.dx = (grid->x1 - grid->x0) / grid->nx;
+  g.dy = dim == 2 ? (grid->y1 - grid->y0) / ny : 1.0;
+  g.gamma = gamma;
+  g.cfl = cfl;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev);
+  c->mwords = std::max<int64_t>((int64_t)g.ny * g.wpr, (g.N + 31) / 32);
+  c->fill_blocks = c->nsm;
+  c->band_blocks = c->nsm;
+  const int occ = std::max(1, std::min(4, filter_occupancy()));
+  c->filter_blocks = c->nsm * occ;
+
+  Bufs& b = c->b;
+  hrom_status s = HROM_OK;
+  auto A = [&](hrom_status r) { if (r != HROM_OK) s = r; };
+  A(dalloc(&b.ring, (size_t)c->nslots * g.Dp));
+  A(dalloc(&b.rho, g.Dp));
+  A(dalloc(&b.U1, g.Dp));
+  A(dalloc(&b.U2, g.Dp));
+  A(dalloc(&b.U3, g.Dp));
+  A(dalloc(&b.Vorig, g.Dp));
+  A(dalloc(&b.eps, g.N));
+  A(dalloc(&b.eps_elem, g.Dp));
+  A(dalloc(&b.masks, (size_t)M_COUNT * c->mwords));
+  A(dalloc(&b.lists, (size_t)L_COUNT * g.N));
+  A(dalloc(&b.counts, 16));
+  A(dalloc(&b.kept, g.N));
+  A(dalloc(&b.C, (size_t)kMaxSlots * kMaxSlots));
+  b.part_len = (int64_t)2 * c->nsm * 144 * 144;
+  A(dalloc(&b.part, b.part_len));
+  b.gpart_len = (int64_t)(c->fill_blocks + c->band_blocks) * (kMaxSlots + 1);
+  A(dalloc(&b.gpart, b.gpart_len));
+  A(dalloc(&b.K, (size_t)(kMaxW + 2) * (kMaxW + 2)));
+  A(dalloc(&b.A, (size_t)kMaxW * kMaxR));
+  A(dalloc(&b.lam, kMaxSlots));
+  A(dalloc(&b.y, kMaxR));
+  A(dalloc(&b.cvec, kMaxW));
+  A(dalloc(&b.zvec, kMaxW));
+  A(dalloc(&b.eigV, (size_t)kMaxSlots * kMaxSlots));
+  A(dalloc(&b.eigA, (size_t)kMaxSlots * kMaxSlots));
+  A(dalloc(&b.ireg, 16));
+  A(dalloc(&b.dreg, 16));
+  A(dalloc(&b.ureg, 4));
+  A(dalloc(&b.sel_val, g.N));
+  A(dalloc(&b.sel_cell, g.N));
+  b.blk_len = 8 * ((c->mwords + 255) / 256 + 2) + (g.N + 1023) / 1024 + 16;
+  A(dalloc(&b.blk, b.blk_len));
+  A(dalloc(&b.hist, 512));
+  A(dalloc(&b.fstat, c->filter_blocks));
+  A(dalloc(&b.fcnt, c->filter_blocks));
+  A(dalloc(&b.colptr, 2 * kMaxSlots));
+  A(dalloc(&b.slot_tab, 2 * kMaxSlots));
+  if (s != HROM_OK) {
+    hrom_destroy(c);
+    return s;
+  }
+  // pointer table: colptr[i] = slot (i mod nslots), so any run of consecutive slots is contiguous
+  std::vector<const double*> tab(2 * kMaxSlots);
+  for (int i = 0; i < 2 * kMaxSlots; ++i) tab[i] = b.ring + (int64_t)(i % c->nslots) * g.Dp;
+  std::vector<int32_t> stab(2 * kMaxSlots);
+  for (int i = 0; i < 2 * kMaxSlots; ++i) stab[i] = i % c->nslots;
+  if (cudaMemcpy(b.colptr, tab.data(), tab.size() * sizeof(double*), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(b.slot_tab, stab.data(), stab.size() * sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemset(b.C, 0, sizeof(double) * kMaxSlots * kMaxSlots) != cudaSuccess ||
+      cudaMemset(b.ureg, 0xff, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMemset(b.ireg, 0, 16 * sizeof(int32_t)) != cudaSuccess ||
+      cudaMemset(b.eps, 0, g.N * sizeof(double)) != cudaSuccess ||
+      cudaMemset(b.masks, 0, (size_t)M_COUNT * c->mwords * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMemset(b.counts, 0, 16 * sizeof(int32_t)) != cudaSuccess ||
+      cudaMemset(b.rho, 0, g.Dp * sizeof(double)) != cudaSuccess ||
+      cudaMemset(b.ring, 0, (size_t)c->nslots * g.Dp * sizeof(double)) != cudaSuccess) {
+    hrom_destroy(c);
+    return HROM_E_CUDA;
+  }
+  *out = c;
+  return HROM_OK;
+}
+
+void hrom_destroy(hrom_ctx* c) {
+  if (!c) return;
+  if (c->st) cudaStreamSynchronize(c->st);
+  else cudaDeviceSynchronize();
+  Bufs& b = c->b;
+  void* ptrs[] = {b.ring, b.rho, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
+                  b.kept, b.C, b.part, b.gpart, b.K, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
+                  b.dreg, b.ureg, b.sel_val, b.sel_cell, b.blk, b.hist, b.fstat, b.fcnt, (void*)b.colptr, b.slot_tab};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  delete c;
+}
+
+hrom_status hrom_set_state(hrom_ctx* c, const double* any_q) {
+  if (!c || !any_q) return HROM_E_INVALID;
+  HROM_CK(cudaMemcpyAsync(c->b.ring, any_q, c->g.D * sizeof(double), cudaMemcpyDefault, c->st));
+  HROM_CK(cudaMemsetAsync(c->b.ureg + 1, 0xff, sizeof(unsigned long long), c->st));
+  c->k = 0;
+  c->basis_ready = c->sets_ready = c->gram_row_ready = false;
+  c->rebase_k = -1000000;
+  c->last_err_cell = -1;
+  return HROM_OK;
+}
+
+hrom_status hrom_get_state(hrom_ctx* c, double* any_q) {
+  if (!c || !any_q) return HROM_E_INVALID;
+  if (c->k < 0) return HROM_E_STATE;
+  HROM_CK(cudaMemcpyAsync(any_q, c->b.ring + (int64_t)c->slot_of(c->k) * c->g.Dp, c->g.D * sizeof(double),
+                          cudaMemcpyDefault, c->st));
+  return HROM_OK;
+}
+
+hrom_status hrom_full_step(hrom_ctx* c, double dt_override, double* dev_dt_out) {
+  if (!c) return HROM_E_INVALID;
+  if (c->k < 0) return HROM_E_STATE;
+  const int64_t kn = c->k + 1;
+  const double* qn = c->b.ring + (int64_t)c->slot_of(c->k) * c->g.Dp;
+  double* out = c->b.ring + (int64_t)c->slot_of(kn) * c->g.Dp;
+  hrom_status s;
+  if ((s = launch_dt(c, qn, dt_override)) != HROM_OK) return s;
+  if (dev_dt_out) HROM_CK(cudaMemcpyAsync(dev_dt_out, c->b.dreg, sizeof(double), cudaMemcpyDefault, c->st));
+  if ((s = launch_stage(c, 1, qn, qn, c->b.U1, nullptr, 0, dt_override)) != HROM_OK) return s;
+  if ((s = launch_stage(c, 2, qn, c->b.U1, c->b.U2, nullptr, 0, dt_override)) != HROM_OK) return s;
+  if ((s = launch_stage(c, 3, qn, c->b.U2, out, nullptr, 0, dt_override)) != HROM_OK) return s;
+  c->k = kn;
+  c->gram_row_ready = false;
+  c->sets_ready = false;
+  return HROM_OK;
+}
+
+hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_override, double* dev_dt_out) {
+  if (!c) return HROM_E_INVALID;
+  if (!c->basis_ready) return HROM_E_STATE;
+  hrom_status s;
+  if (dev_mask) {
+    if ((s = build_sets(c, dev_mask)) != HROM_OK) return s;
+    c->sets_ready = true;
+  }
+  if (!c->sets_ready) return HROM_E_STATE;
+  const Geo& g = c->g;
+  Bufs& b = c->b;
+  const int64_t kn = c->k + 1;
+  const double* qn = b.ring + (int64_t)c->slot_of(c->k) * g.Dp;
+  double* out = b.ring + (int64_t)c->slot_of(kn) * g.Dp;
+  // H1
+  if ((s = launch_dt(c, qn, dt_override)) != HROM_OK) return s;
+  if (dev_dt_out) HROM_CK(cudaMemcpyAsync(dev_dt_out, b.dreg, sizeof(double), cudaMemcpyDefault, c->st));
+  // H3: stage 1 on A1, stage 2 on A2, stage 3 on T = S-hat u B (F on the band)
+  const int32_t* L = b.lists;
+  if ((s = launch_stage(c, 1, qn, qn, b.U1, L + (int64_t)L_A1 * g.N, L_A1, dt_override)) != HROM_OK) return s;
+  if ((s = launch_stage(c, 2, qn, b.U1, b.U2, L + (int64_t)L_A2 * g.N, L_A2, dt_override)) != HROM_OK) return s;
+  if ((s = launch_stage(c, 3, qn, b.U2, b.U3, L + (int64_t)L_T * g.N, L_T, dt_override)) != HROM_OK) return s;
+  // H4 + H5
+  if ((s = gram_gathered(c, b.U3)) != HROM_OK) return s;
+  if ((s = small_solve(c)) != HROM_OK) return s;
+  // H6 (+H9, H10 row)
+  HROM_CK(cudaMemsetAsync(b.eps, 0, g.N * sizeof(double), c->st));
+  if ((s = launch_fill(c, c->win, 0, b.U3, out, c->slot_of(kn))) != HROM_OK) return s;
+  if ((s = launch_eps_cells(c)) != HROM_OK) return s;
+  // H7
+  if (c->P.n_filter_orders > 0 && c->P.filter_max_sweeps > 0)
+    if ((s = launch_filter(c, out, b.U3)) != HROM_OK) return s;
+  if (c->P.gram_mode == 0)
+    if ((s = launch_band_gram(c, c->win, out)) != HROM_OK) return s;
+  if ((s = launch_positivity(c, out)) != HROM_OK) return s;
+  c->k = kn;
+  c->gram_row_ready = (c->P.gram_mode == 0);
+  c->sets_ready = false;
+  return HROM_OK;
+}
+
+hrom_status hrom_update_basis(hrom_ctx* c) {
+  if (!c) return HROM_E_INVALID;
+  if (c->k < 0) return HROM_E_STATE;
+  const int w = c->w;
+  const int64_t k = c->k;
+  if (k < w - 1) return HROM_OK;
+  hrom_status s;
+  const Win W = window_at(c, k);
+  const bool rebase = (k == w - 1) || c->P.gram_mode == 1 || (k - c->rebase_k >= c->P.rebase_period) ||
+                      (!c->gram_row_ready && !c->basis_ready);
+  if (rebase) {
+    if ((s = launch_mean(c, W, c->b.rho)) != HROM_OK) return s;
+    const int s0 = W.slot[0];
+    // consecutive slots are contiguous in the pointer table (see hrom_create)
+    // written straight into the slot-indexed Gram through the slot table
+    if ((s = gram_full(c, c->b.colptr + s0, W.nU, c->g.D, c->b.rho, c->b.C, kMaxSlots, c->b.slot_tab + s0)) != HROM_OK)
+      return s;
+    c->rebase_k = k;
+  } else if (!c->gram_row_ready) {
+    if ((s = launch_gram_row(c, c->win, c->slot_of(k))) != HROM_OK) return s;
+    if ((s = reduce_gram_row(c, c->win, c->slot_of(k), false)) != HROM_OK) return s;
+  } else {
+    if ((s = reduce_gram_row(c, c->win, c->slot_of(k), true)) != HROM_OK) return s;
+  }
+  if ((s = basis_from_gram(c, W)) != HROM_OK) return s;
+  c->win = W;
+  c->basis_ready = true;
+  c->gram_row_ready = false;
+  if (k == w - 1) {  // bootstrap indicator (reading A19)
+    zvec_kernel<<<1, 128, 0, c->st>>>(c->b.A, c->b.lam, c->b.ireg, w, c->b.zvec);
+    HROM_LAUNCH_CK();
+    if ((s = launch_fill(c, W, 2, nullptr, nullptr, -1)) != HROM_OK) return s;
+    if ((s = launch_eps_all(c)) != HROM_OK) return s;
+  }
+  return HROM_OK;
+}
+
+hrom_status hrom_sample(hrom_ctx* c, double fraction, const double* dev_eps, uint32_t* dev_mask_out,
+                        int32_t* dev_list_out, int32_t* dev_count_out) {
+  if (!c) return HROM_E_INVALID;
+  if (!(fraction > 0.0 && fraction <= 1.0)) return HROM_E_INVALID;
+  const int64_t n_g = (int64_t)std::ceil(fraction * (double)c->g.N);
+  hrom_status s;
+  if ((s = select_topn(c, dev_eps ? dev_eps : c->b.eps, n_g)) != HROM_OK) return s;
+  if ((s = build_sets(c, nullptr)) != HROM_OK) return s;
+  c->sets_ready = true;
+  if (dev_mask_out)
+    HROM_CK(cudaMemcpyAsync(dev_mask_out, c->b.masks + (int64_t)M_S * c->mwords, c->mwords * sizeof(uint32_t),
+                            cudaMemcpyDefault, c->st));
+  if (dev_list_out)
+    HROM_CK(cudaMemcpyAsync(dev_list_out, c->b.lists + (int64_t)L_S * c->g.N, c->g.N * sizeof(int32_t),
+                            cudaMemcpyDefault, c->st));
+  if (dev_count_out)
+    HROM_CK(cudaMemcpyAsync(dev_count_out, c->b.counts + L_S, sizeof(int32_t), cudaMemcpyDefault, c->st));
+  return HROM_OK;
+}
+
+hrom_status hrom_reconstruct(hrom_ctx* c, const uint32_t* dev_mask, double* dev_v, double* dev_y_out,
+                             double* dev_eps_out) {
+  if (!c || !dev_v) return HROM_E_INVALID;
+  if (!c->basis_ready) return HROM_E_STATE;
+  hrom_status s;
+  if (dev_mask) {
+    if ((s = build_sets(c, dev_mask)) != HROM_OK) return s;
+    c->sets_ready = true;
+  }
+  if (!c->sets_ready) return HROM_E_STATE;
+  if ((s = gram_gathered(c, dev_v)) != HROM_OK) return s;
+  if ((s = small_solve(c)) != HROM_OK) return s;
+  HROM_CK(cudaMemsetAsync(c->b.eps, 0, c->g.N * sizeof(double), c->st));
+  if ((s = launch_fill(c, c->win, 0, dev_v, dev_v, -1)) != HROM_OK) return s;
+  if ((s = launch_eps_cells(c)) != HROM_OK) return s;
+  if (dev_y_out) HROM_CK(cudaMemcpyAsync(dev_y_out, c->b.y, c->r * sizeof(double), cudaMemcpyDefault, c->st));
+  if (dev_eps_out)
+    HROM_CK(cudaMemcpyAsync(dev_eps_out, c->b.eps, c->g.N * sizeof(double), cudaMemcpyDefault, c->st));
+  return HROM_OK;
+}
+
+hrom_status hrom_filter(hrom_ctx* c, const uint32_t* dev_mask, double* dev_v, const double* dev_F,
+                        uint8_t* dev_kept_out) {
+  if (!c || !dev_v || !dev_F) return HROM_E_INVALID;
+  hrom_status s;
+  if (dev_mask) {
+    if ((s = build_sets(c, dev_mask)) != HROM_OK) return s;
+    c->sets_ready = true;
+  }
+  if (!c->sets_ready) return HROM_E_STATE;
+  if ((s = launch_filter(c, dev_v, dev_F)) != HROM_OK) return s;
+  if (dev_kept_out)
+    HROM_CK(cudaMemcpyAsync(dev_kept_out, c->b.kept, c->g.N, cudaMemcpyDefault, c->st));
+  return HROM_OK;
+}
+
+hrom_status hrom_step(hrom_ctx* c, double dt_override) {
+  if (!c) return HROM_E_INVALID;
+  if (c->k < 0) return HROM_E_STATE;
+  const int64_t kn = c->k + 1;
+  hrom_status s;
+  if (kn + 1 <= c->w) s = hrom_full_step(c, dt_override, nullptr);
+  else s = hrom_hybrid_step(c, nullptr, dt_override, nullptr);
+  if (s != HROM_OK) return s;
+  if (kn >= c->w - 1) {
+    if ((s = hrom_update_basis(c)) != HROM_OK) return s;
+    if ((s = hrom_sample(c, c->P.sample_fraction, nullptr, nullptr, nullptr, nullptr)) != HROM_OK) return s;
+  }
+  return HROM_OK;
+}
+
+hrom_status hrom_sync(hrom_ctx* c) {
+  if (!c) return HROM_E_INVALID;
+  HROM_CK(cudaStreamSynchronize(c->st));
+  unsigned long long bad = 0;
+  HROM_CK(cudaMemcpy(&bad, c->b.ureg + 1, sizeof(bad), cudaMemcpyDeviceToHost));
+  if (bad != ~0ull) {
+    c->last_err_cell = (int64_t)bad;
+    return HROM_E_POSITIVITY;
+  }
+  return HROM_OK;
+}
+
+int64_t hrom_error_cell(const hrom_ctx* c) { return c ? c->last_err_cell : -1; }
+int64_t hrom_step_index(const hrom_ctx* c) { return c ? c->k : -1; }
+int64_t hrom_mask_words(const hrom_ctx* c) { return c ? c->mwords : 0; }
+
+int32_t hrom_effective_rank(hrom_ctx* c) {
+  if (!c) return -1;
+  int32_t r = 0;
+  if (cudaStreamSynchronize(c->st) != cudaSuccess) return -1;
+  if (cudaMemcpy(&r, c->b.ireg, sizeof(r), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return r;
+}
+
+hrom_status hrom_set_window(hrom_ctx* c, int64_t k, const double* any_snaps, int32_t nsnaps,
+                            const uint32_t* any_mask_next) {
+  if (!c || !any_snaps) return HROM_E_INVALID;
+  if (k < c->w || nsnaps != c->w + 1) return HROM_E_INVALID;
+  for (int t = 0; t < nsnaps; ++t)
+    HROM_CK(cudaMemcpyAsync(c->b.ring + (int64_t)c->slot_of(k - c->w + t) * c->g.Dp, any_snaps + (int64_t)t * c->g.D,
+                            c->g.D * sizeof(double), cudaMemcpyDefault, c->st));
+  HROM_CK(cudaMemsetAsync(c->b.ureg + 1, 0xff, sizeof(unsigned long long), c->st));
+  c->k = k;
+  c->basis_ready = false;
+  c->gram_row_ready = false;
+  c->rebase_k = -1000000;
+  hrom_status s = hrom_update_basis(c);
+  if (s != HROM_OK) return s;
+  if (any_mask_next) {
+    uint32_t* S = c->b.masks + (int64_t)M_S * c->mwords;
+    HROM_CK(cudaMemcpyAsync(S, any_mask_next, c->mwords * sizeof(uint32_t), cudaMemcpyDefault, c->st));
+    if ((s = build_sets(c, nullptr)) != HROM_OK) return s;
+    c->sets_ready = true;
+  }
+  return HROM_OK;
+}
+
+hrom_status hrom_get_basis(hrom_ctx* c, double* dev_phi, double* dev_psi) {
+  if (!c) return HROM_E_INVALID;
+  if (!c->basis_ready) return HROM_E_STATE;
+  return lift(c, c->win, dev_phi, dev_psi);
+}
+
+hrom_status hrom_get_indicator(hrom_ctx* c, double* any_eps) {
+  if (!c || !any_eps) return HROM_E_INVALID;
+  HROM_CK(cudaMemcpyAsync(any_eps, c->b.eps, c->g.N * sizeof(double), cudaMemcpyDefault, c->st));
+  return HROM_OK;
+}
+
+hrom_status hrom_get_mask(hrom_ctx* c, uint32_t* any_mask) {
+  if (!c || !any_mask) return HROM_E_INVALID;
+  HROM_CK(cudaMemcpyAsync(any_mask, c->b.masks + (int64_t)M_S * c->mwords, c->mwords * sizeof(uint32_t),
+                          cudaMemcpyDefault, c->st));
+  return HROM_OK;
+}
+
+hrom_status hrom_get_y(hrom_ctx* c, double* any_y) {
+  if (!c || !any_y) return HROM_E_INVALID;
+  HROM_CK(cudaMemcpyAsync(any_y, c->b.y, c->r * sizeof(double), cudaMemcpyDefault, c->st));
+  return HROM_OK;
+}
+
+hrom_status hrom_get_eigen(hrom_ctx* c, double* any_lambda) {
+  if (!c || !any_lambda) return HROM_E_INVALID;
+  HROM_CK(cudaMemcpyAsync(any_lambda, c->b.lam, c->w * sizeof(double), cudaMemcpyDefault, c->st));
+  return HROM_OK;
+}
+
+hrom_status hrom_gram(hrom_ctx* c, const double* const* dev_cols, int32_t ncol, int64_t rows, const double* dev_rho,
+                      double* dev_C) {
+  if (!c || !dev_cols || !dev_C || ncol < 1 || ncol > kMaxSlots + 14 || rows < 0) return HROM_E_INVALID;
+  return gram_full(c, dev_cols, ncol, rows, dev_rho, dev_C, ncol, nullptr);
+}
+
+}  // extern "C"

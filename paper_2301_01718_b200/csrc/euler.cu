@@ -1,0 +1,241 @@
+// euler.cu -- H1 (CFL dt), H2 (full SSP-RK3 step) and H3 (masked step) kernels.
+//
+// Paper: Euler equations + ideal gas, MUSCL + minmod, explicit
+// F_k (remark P:345-347).  BASELINE.json: Rusanov flux, SSP-RK3 (BJ:7-10).
+// The full and the masked step run the SAME kernel (list == nullptr means all cells),
+// so the S-hat rows of a masked step are bitwise the rows of the full step (Eq. 7,
+// exact restriction, reading A9).
+#include <cfloat>
+#include "internal.cuh"
+
+namespace hrom {
+namespace {
+
+template <int DIM>
+__device__ __forceinline__ double pressure(const double* U, double gm1) {
+  double m2 = U[1] * U[1];
+  if (DIM == 2) m2 += U[2] * U[2];
+  return gm1 * (U[DIM + 1] - 0.5 * m2 / U[0]);
+}
+
+__device__ __forceinline__ double minmod(double a, double b) {
+  if (a * b <= 0.0) return 0.0;
+  return a > 0.0 ? fmin(a, b) : fmax(a, b);
+}
+
+// Rusanov flux along AXIS from reconstructed face states (O5)
+template <int DIM, int AXIS>
+__device__ __forceinline__ void rusanov(const double* UL, const double* UR, double gamma, double* F) {
+  constexpr int C = DIM + 2;
+  const double gm1 = gamma - 1.0;
+  const double pL = pressure<DIM>(UL, gm1), pR = pressure<DIM>(UR, gm1);
+  const double uL = UL[1 + AXIS] / UL[0], uR = UR[1 + AXIS] / UR[0];
+  const double cL = sqrt(gamma * pL / UL[0]), cR = sqrt(gamma * pR / UR[0]);
+  const double a = fmax(fabs(uL) + cL, fabs(uR) + cR);
+  double FL[C], FR[C];
+  FL[0] = UL[1 + AXIS];
+  FR[0] = UR[1 + AXIS];
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    FL[1 + d] = UL[1 + d] * uL + (d == AXIS ? pL : 0.0);
+    FR[1 + d] = UR[1 + d] * uR + (d == AXIS ? pR : 0.0);
+  }
+  FL[C - 1] = (UL[C - 1] + pL) * uL;
+  FR[C - 1] = (UR[C - 1] + pR) * uR;
+#pragma unroll
+  for (int v = 0; v < C; ++v) F[v] = 0.5 * (FL[v] + FR[v]) - 0.5 * a * (UR[v] - UL[v]);
+}
+
+// flux through the face between cells a and b (am left of a, bp right of b)
+template <int DIM, int AXIS, int RECON>
+__device__ __forceinline__ void face_flux(const double* Uam, const double* Ua, const double* Ub,
+                                          const double* Ubp, double gamma, double* F) {
+  constexpr int C = DIM + 2;
+  double UL[C], UR[C];
+#pragma unroll
+  for (int v = 0; v < C; ++v) {
+    if (RECON == 2) {
+      UL[v] = Ua[v] + 0.5 * minmod(Ua[v] - Uam[v], Ub[v] - Ua[v]);
+      UR[v] = Ub[v] - 0.5 * minmod(Ub[v] - Ua[v], Ubp[v] - Ub[v]);
+    } else {
+      UL[v] = Ua[v];
+      UR[v] = Ub[v];
+    }
+  }
+  rusanov<DIM, AXIS>(UL, UR, gamma, F);
+}
+
+__device__ __forceinline__ int wrap(int i, int n, int bc) {
+  if (bc == 1) {
+    i = i % n;
+    return i < 0 ? i + n : i;
+  }
+  return i < 0 ? 0 : (i >= n ? n - 1 : i);
+}
+
+// L at cell (i, j) of q (O6); loads the cross stencil of radius RECON
+template <int DIM, int RECON>
+__device__ __forceinline__ void cell_rhs(const Geo& g, const double* __restrict__ q, int i, int j,
+                                         double* L) {
+  constexpr int C = DIM + 2;
+  constexpr int R = RECON;
+  double Ux[2 * R + 1][C];
+  const int64_t row = (int64_t)j * g.nx;
+#pragma unroll
+  for (int m = -R; m <= R; ++m) {
+    const int64_t n = row + wrap(i + m, g.nx, g.bc);
+#pragma unroll
+    for (int v = 0; v < C; ++v) Ux[m + R][v] = __ldg(q + v * g.N + n);
+  }
+  double Fp[C], Fm[C];
+  // right face (i, i+1) uses cells i-1, i, i+1, i+2; left face uses i-2 .. i+1
+  face_flux<DIM, 0, RECON>(Ux[R - (R == 2 ? 1 : 0)], Ux[R], Ux[R + 1], Ux[R + (R == 2 ? 2 : 1)], g.gamma, Fp);
+  face_flux<DIM, 0, RECON>(Ux[0], Ux[R - 1], Ux[R], Ux[R + (R == 2 ? 1 : 0)], g.gamma, Fm);
+#pragma unroll
+  for (int v = 0; v < C; ++v) L[v] = -(Fp[v] - Fm[v]) / g.dx;
+  if (DIM == 2) {
+    double Uy[2 * R + 1][C];
+#pragma unroll
+    for (int m = -R; m <= R; ++m) {
+      if (m == 0) {
+#pragma unroll
+        for (int v = 0; v < C; ++v) Uy[R][v] = Ux[R][v];
+        continue;
+      }
+      const int64_t n = (int64_t)wrap(j + m, g.ny, g.bc) * g.nx + i;
+#pragma unroll
+      for (int v = 0; v < C; ++v) Uy[m + R][v] = __ldg(q + v * g.N + n);
+    }
+    double Gp[C], Gm[C];
+    face_flux<DIM, DIM - 1, RECON>(Uy[R - (R == 2 ? 1 : 0)], Uy[R], Uy[R + 1], Uy[R + (R == 2 ? 2 : 1)], g.gamma, Gp);
+    face_flux<DIM, DIM - 1, RECON>(Uy[0], Uy[R - 1], Uy[R], Uy[R + (R == 2 ? 1 : 0)], g.gamma, Gm);
+#pragma unroll
+    for (int v = 0; v < C; ++v) L[v] = L[v] - (Gp[v] - Gm[v]) / g.dy;
+  }
+}
+
+// One SSP-RK3 stage (O8, printed order) on all cells (list == nullptr) or a cell list.
+template <int DIM, int RECON>
+__global__ void __launch_bounds__(256) stage_kernel(Geo g, int stage, const double* __restrict__ qn,
+                                                    const double* __restrict__ qin, double* __restrict__ out,
+                                                    const int32_t* __restrict__ list,
+                                                    const int32_t* __restrict__ count,
+                                                    const double* __restrict__ dtp) {
+  constexpr int C = DIM + 2;
+  const int64_t total = list ? (int64_t)(*count) : g.N;
+  const double dt = *dtp;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = list ? (int64_t)list[t] : t;
+    const int i = (int)(n % g.nx), j = (int)(n / g.nx);
+    double L[C];
+    cell_rhs<DIM, RECON>(g, qin, i, j, L);
+#pragma unroll
+    for (int v = 0; v < C; ++v) {
+      const int64_t e = v * g.N + n;
+      double r;
+      if (stage == 1) r = qn[e] + dt * L[v];
+      else if (stage == 2) r = 0.75 * qn[e] + 0.25 * (qin[e] + dt * L[v]);
+      else r = (1.0 / 3.0) * qn[e] + (2.0 / 3.0) * (qin[e] + dt * L[v]);
+      out[e] = r;
+    }
+  }
+}
+
+// H1: max_n S_n with S_n = (|u|+c)/dx [+ (|v|+c)/dy]; S_n >= 0 so its IEEE bits order like
+// the value and an integer atomicMax is exact and order-free (deterministic).
+template <int DIM>
+__global__ void __launch_bounds__(256) smax_kernel(Geo g, const double* __restrict__ q,
+                                                   unsigned long long* __restrict__ smax) {
+  constexpr int C = DIM + 2;
+  double m = 0.0;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    double U[C];
+#pragma unroll
+    for (int v = 0; v < C; ++v) U[v] = q[v * g.N + n];
+    const double p = pressure<DIM>(U, g.gamma - 1.0);
+    const double cs = sqrt(g.gamma * p / U[0]);
+    double s = (fabs(U[1] / U[0]) + cs) / g.dx;
+    if (DIM == 2) s = s + (fabs(U[2] / U[0]) + cs) / g.dy;
+    if (!(s <= m)) m = s;  // NaN sticks
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double t = __shfl_xor_sync(0xffffffffu, m, o);
+    if (!(t <= m)) m = t;
+  }
+  __shared__ double sm[8];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+      if (!(sm[k] <= m)) m = sm[k];
+    unsigned long long bits = (unsigned long long)__double_as_longlong(m);
+    if (m != m) bits = 0x7ff8000000000000ull;  // canonical NaN (largest positive pattern class)
+    atomicMax(smax, bits);
+  }
+}
+
+__global__ void dt_finalize(const unsigned long long* smax, double cfl, double dt_override, double* dt,
+                            double* dt_out) {
+  const double s = __longlong_as_double((long long)*smax);
+  const double v = dt_override > 0.0 ? dt_override : cfl / s;
+  *dt = v;
+  if (dt_out) *dt_out = v;
+}
+
+// O11: lowest cell with rho <= 0 or p <= 0 (or NaN)
+template <int DIM>
+__global__ void __launch_bounds__(256) positivity_kernel(Geo g, const double* __restrict__ q,
+                                                         unsigned long long* __restrict__ bad) {
+  constexpr int C = DIM + 2;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    double U[C];
+#pragma unroll
+    for (int v = 0; v < C; ++v) U[v] = q[v * g.N + n];
+    const double p = pressure<DIM>(U, g.gamma - 1.0);
+    if (!(U[0] > 0.0) || !(p > 0.0)) atomicMin(bad, (unsigned long long)n);
+  }
+}
+
+}  // namespace
+
+hrom_status launch_dt(hrom_ctx* c, const double* q, double dt_override) {
+  if (dt_override <= 0.0) {
+    HROM_CK(cudaMemsetAsync(c->b.ureg, 0, sizeof(unsigned long long), c->st));
+    const int grid = c->nsm * 8;
+    if (c->g.dim == 1) smax_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg);
+    else smax_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg);
+    HROM_LAUNCH_CK();
+  }
+  dt_finalize<<<1, 1, 0, c->st>>>(c->b.ureg, c->g.cfl, dt_override, c->b.dreg, nullptr);
+  HROM_LAUNCH_CK();
+  return HROM_OK;
+}
+
+hrom_status launch_stage(hrom_ctx* c, int stage, const double* qn, const double* qin, double* out,
+                         const int32_t* list, int list_idx, double /*dt_override*/) {
+  const int grid = c->nsm * 8;
+  const int32_t* cnt = list ? c->b.counts + list_idx : nullptr;
+  const Geo& g = c->g;
+  if (g.dim == 1) {
+    if (g.recon == 1) stage_kernel<1, 1><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg);
+    else stage_kernel<1, 2><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg);
+  } else {
+    if (g.recon == 1) stage_kernel<2, 1><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg);
+    else stage_kernel<2, 2><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg);
+  }
+  HROM_LAUNCH_CK();
+  return HROM_OK;
+}
+
+hrom_status launch_positivity(hrom_ctx* c, const double* q) {
+  const int grid = c->nsm * 8;
+  if (c->g.dim == 1) positivity_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg + 1);
+  else positivity_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg + 1);
+  HROM_LAUNCH_CK();
+  return HROM_OK;
+}
+
+}  // namespace hrom

@@ -1,0 +1,345 @@
+// fill.cu -- H6 + H9 + incremental H10: ONE pass over the snapshot window per hybrid step.
+//
+// For every DOF e the kernel streams the w+1 window columns gamma_{k-w-1..k-1} and the Gram
+// shift rho through shared memory (cp.async.bulk / TMA 1-D bulk copies, mbarrier pipeline) and
+//   * fills gamma_k[e] = psi_k + Phi_k y_k = psi_cur + sum_i c_i (gamma_{x_i} - psi_prev)
+//     (Alg. 1 line P:570; Phi_k = X^{(k-1)} A kept implicit), or takes the
+//     partial-HDM value on S-hat (Eq. 6b),
+//   * writes the per-DOF squared reconstruction error on S-hat,
+//   * accumulates the new row of the shifted window Gram <gamma_k - rho, gamma_s - rho>
+//     for every window slot s (reading A14), skipping seam-band cells (added after the
+//     filter by filter.cu).
+// psi_prev / psi_cur are recomputed from the columns in registers: the
+// reference state is never stored or drifted.
+#include "internal.cuh"
+
+namespace hrom {
+namespace {
+
+constexpr int FT = 256;   // threads per CTA
+constexpr int TE = 128;   // DOFs per tile
+constexpr int PARTS = FT / TE;
+constexpr int MAXSPW = (kMaxW + 2 + (FT / 32) - 1) / (FT / 32);  // slots per warp (Gram)
+
+enum { MODE_FILL = 0, MODE_READ = 1, MODE_PROJ = 2 };
+
+struct FillArgs {
+  Geo g;
+  Win W;
+  int mode;
+  int do_gram;
+  int nstage;
+  const double* ring;
+  const double* rho;
+  const double* cvec;      // w coefficients (c = A y, or projection z)
+  const double* src_S;     // HDM values on S-hat (MODE_FILL)
+  double* out;             // gamma_k (MODE_FILL writes, MODE_READ reads)
+  const uint32_t* mS;
+  const uint32_t* mB;
+  double* eps_elem;
+  double* part;            // [grid][nU+1]
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ bool bit_of(const uint32_t* m, const Geo& g, int64_t n) {
+  const int i = (int)(n % g.nx), j = (int)(n / g.nx);
+  return (m[(int64_t)j * g.wpr + (i >> 5)] >> (i & 31)) & 1u;
+}
+
+__global__ void __launch_bounds__(FT, 1) fill_kernel(FillArgs a) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int nU = a.W.nU, w = a.W.w;
+  const int ncol = nU + 1;  // window slots + rho
+  double* stage0 = reinterpret_cast<double*>(smraw);
+  const size_t stage_elems = (size_t)ncol * TE;
+  double* gt = stage0 + a.nstage * stage_elems;      // TE: g - rho (0 on band cells)
+  double* red = gt + TE;                              // PARTS * TE * 3 partial sums
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 3 * PARTS * TE);
+  __shared__ double cs[kMaxW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Geo& g = a.g;
+  for (int i = tid; i < w; i += FT) cs[i] = a.cvec ? a.cvec[i] : 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < a.nstage; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ntiles = (g.D + TE - 1) / TE;
+  auto issue = [&](int64_t tile, int st) {
+    const int64_t e0 = tile * TE;
+    const int64_t cnt = (g.D - e0) < TE ? (g.D - e0) : TE;
+    const uint32_t bytes = (uint32_t)(((cnt + 1) / 2) * 2 * sizeof(double));
+    double* dst = stage0 + st * stage_elems;
+    mbar_expect(&bars[st], bytes * ncol);
+    for (int s = 0; s < nU; ++s) bulk_g2s(dst + (size_t)s * TE, a.ring + (int64_t)a.W.slot[s] * g.Dp + e0, bytes, &bars[st]);
+    bulk_g2s(dst + (size_t)nU * TE, a.rho + e0, bytes, &bars[st]);
+  };
+  int64_t first = blockIdx.x;
+  if (tid == 0)
+    for (int s = 0; s < a.nstage; ++s)
+      if (first + (int64_t)s * gridDim.x < ntiles) issue(first + (int64_t)s * gridDim.x, s);
+  double acc[MAXSPW];
+#pragma unroll
+  for (int q = 0; q < MAXSPW; ++q) acc[q] = 0.0;
+  double acc_self = 0.0;
+  const int e_loc = tid % TE, part = tid / TE;
+  // slot ranges per part for phase A
+  const int per = (nU + PARTS - 1) / PARTS;
+  int it = 0;
+  for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it % a.nstage;
+    const uint32_t par = (uint32_t)((it / a.nstage) & 1);
+    mbar_wait(&bars[st], par);
+    const double* T = stage0 + st * stage_elems;
+    const int64_t e0 = tile * TE;
+    const int64_t e = e0 + e_loc;
+    const bool valid = e < g.D;
+    // phase A1: partial sums for psi_prev (slots 0..w-1) and psi_cur (slots nU-w..nU-1)
+    {
+      double sp = 0.0, sc = 0.0;
+      const int s0 = part * per, s1 = min(nU, s0 + per);
+      for (int s = s0; s < s1; ++s) {
+        const double v = T[s * TE + e_loc];
+        if (s < w) sp += v;
+        if (s >= nU - w) sc += v;
+      }
+      red[(part * TE + e_loc) * 3 + 0] = sp;
+      red[(part * TE + e_loc) * 3 + 1] = sc;
+    }
+    __syncthreads();
+    double psi_prev = 0.0, psi_cur = 0.0;
+    {
+      double sp = 0.0, sc = 0.0;
+      for (int p = 0; p < PARTS; ++p) {
+        sp += red[(p * TE + e_loc) * 3 + 0];
+        sc += red[(p * TE + e_loc) * 3 + 1];
+      }
+      psi_prev = sp / (double)w;
+      psi_cur = sc / (double)w;
+    }
+    // phase A2: partial sum_i c_i (gamma_{x_i} - psi_prev), x_i = slot nU-w+i
+    {
+      double r = 0.0;
+      const int i0 = part * ((w + PARTS - 1) / PARTS), i1 = min(w, i0 + (w + PARTS - 1) / PARTS);
+      for (int i = i0; i < i1; ++i) r += cs[i] * (T[(nU - w + i) * TE + e_loc] - psi_prev);
+      __syncthreads();  // everyone has read red[...][0..1]
+      red[(part * TE + e_loc) * 3 + 2] = r;
+    }
+    __syncthreads();
+    if (part == 0) {
+      double gval = 0.0;
+      if (valid) {
+        double rs = 0.0;
+        for (int p = 0; p < PARTS; ++p) rs += red[(p * TE + e_loc) * 3 + 2];
+        const int64_t n = e % g.N;
+        if (a.mode == MODE_FILL) {
+          const double rec = psi_cur + rs;
+          if (bit_of(a.mS, g, n)) {
+            gval = a.src_S[e];
+            const double d = gval - rec;
+            a.eps_elem[e] = d * d;
+          } else {
+            gval = rec;
+          }
+          a.out[e] = gval;
+        } else if (a.mode == MODE_READ) {
+          gval = a.out[e];
+        } else {  // MODE_PROJ: residual of the projection onto the basis (bootstrap indicator)
+          a.eps_elem[e] = rs * rs;
+        }
+        const double rh = T[nU * TE + e_loc];
+        const bool skip = (a.mode == MODE_FILL && a.mB && bit_of(a.mB, g, n)) || a.mode == MODE_PROJ;
+        const double gr = skip ? 0.0 : gval - rh;
+        gt[e_loc] = gr;
+        acc_self += gr * gr;
+      } else {
+        gt[e_loc] = 0.0;
+      }
+    }
+    __syncthreads();
+    // phase B: Gram row, warp-per-slot-set, lanes over DOFs
+    if (a.do_gram) {
+      const int cnt = (int)((g.D - e0) < TE ? (g.D - e0) : TE);
+#pragma unroll
+      for (int q = 0; q < MAXSPW; ++q) {
+        const int s = warp + q * (FT / 32);
+        if (s < nU) {
+          double sacc = 0.0;
+          for (int el = lane; el < cnt; el += 32) sacc += gt[el] * (T[s * TE + el] - T[nU * TE + el]);
+          acc[q] += sacc;
+        }
+      }
+    }
+    __syncthreads();  // stage fully consumed
+    if (tid == 0) {
+      const int64_t nt = tile + (int64_t)a.nstage * gridDim.x;
+      if (nt < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(nt, st);
+      }
+    }
+  }
+  if (!a.do_gram) return;
+  // fixed-order reductions -> part[block][s], part[block][nU] = self
+  double* out = a.part + (int64_t)blockIdx.x * (nU + 1);
+#pragma unroll
+  for (int q = 0; q < MAXSPW; ++q) {
+    double v = acc[q];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int s = warp + q * (FT / 32);
+    if (lane == 0 && s < nU) out[s] = v;
+  }
+  double v = acc_self;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __shared__ double wsum[FT / 32];
+  if (lane == 0) wsum[warp] = v;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int k = 0; k < FT / 32; ++k) s += wsum[k];
+    out[nU] = s;
+  }
+}
+
+// C[new][U[s]] = sum over blocks of fill partials (+ band partials), fixed order
+__global__ void gram_row_reduce(const double* __restrict__ part, int nblk, Win W, int new_slot,
+                                double* __restrict__ C, int ldc) {
+  const int nU = W.nU;
+  for (int s = threadIdx.x; s <= nU; s += blockDim.x) {
+    double acc = 0.0;
+    for (int b = 0; b < nblk; ++b) acc += part[(int64_t)b * (nU + 1) + s];
+    if (s < nU) {
+      C[new_slot * ldc + W.slot[s]] = acc;
+      C[W.slot[s] * ldc + new_slot] = acc;
+    } else {
+      C[new_slot * ldc + new_slot] = acc;
+    }
+  }
+}
+
+// eps_n = sum_v eps_elem[v*N + n] on the listed cells (S-hat), P:363 summed over c (A16)
+__global__ void eps_cells_kernel(Geo g, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+                                 const double* __restrict__ eps_elem, double* __restrict__ eps) {
+  const int total = *count;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int64_t n = list[t];
+    double s = 0.0;
+    for (int v = 0; v < g.c; ++v) s += eps_elem[v * g.N + n];
+    eps[n] = s;
+  }
+}
+
+__global__ void eps_all_kernel(Geo g, const double* __restrict__ eps_elem, double* __restrict__ eps) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N; n += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int v = 0; v < g.c; ++v) s += eps_elem[v * g.N + n];
+    eps[n] = s;
+  }
+}
+
+// rho (or psi) = mean of the last w window slots
+__global__ void mean_kernel(Geo g, Win W, const double* __restrict__ ring, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < g.D; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int q = W.nU - W.w; q < W.nU; ++q) s += ring[(int64_t)W.slot[q] * g.Dp + e];
+    out[e] = s / (double)W.w;
+  }
+}
+
+}  // namespace
+
+static int fill_smem_stages(int nU, size_t* bytes) {
+  const size_t stage = (size_t)(nU + 1) * TE * sizeof(double);
+  const size_t fixed = (TE + 3 * PARTS * TE) * sizeof(double) + 8 * sizeof(uint64_t);
+  const size_t budget = 220 * 1024;
+  int ns = (int)((budget - fixed) / stage);
+  if (ns > 4) ns = 4;
+  *bytes = ns * stage + fixed;
+  return ns;
+}
+
+hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S, double* out, int /*out_slot*/) {
+  FillArgs a{};
+  a.g = c->g;
+  a.W = W;
+  a.mode = mode;
+  a.do_gram = (mode != MODE_PROJ) && out != nullptr && c->P.gram_mode == 0 ? 1 : 0;
+  if (mode == MODE_FILL && out != nullptr && !(out >= c->b.ring && out < c->b.ring + (int64_t)c->nslots * c->g.Dp))
+    a.do_gram = 0;  // standalone reconstruct into a caller buffer: no window Gram
+  size_t smem;
+  a.nstage = fill_smem_stages(W.nU, &smem);
+  if (a.nstage < 1) return HROM_E_INVALID;
+  a.ring = c->b.ring;
+  a.rho = c->b.rho;
+  a.cvec = (mode == MODE_PROJ) ? c->b.zvec : c->b.cvec;
+  a.src_S = src_S;
+  a.out = out;
+  a.mS = c->b.masks + (int64_t)M_S * c->mwords;
+  a.mB = (mode == MODE_FILL) ? c->b.masks + (int64_t)M_B * c->mwords : nullptr;
+  a.eps_elem = c->b.eps_elem;
+  a.part = c->b.gpart;
+  const int grid = c->fill_blocks;
+  HROM_CK(cudaFuncSetAttribute(fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fill_kernel<<<grid, FT, smem, c->st>>>(a);
+  HROM_LAUNCH_CK();
+  return HROM_OK;
+}
+
+hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot) {
+  return launch_fill(c, W, MODE_READ, nullptr, c->b.ring + (int64_t)new_slot * c->g.Dp, new_slot);
+}
+
+hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_band) {
+  const int nblk = c->fill_blocks + (with_band ? c->band_blocks : 0);
+  gram_row_reduce<<<1, 256, 0, c->st>>>(c->b.gpart, nblk, W, new_slot, c->b.C, kMaxSlots);
+  HROM_LAUNCH_CK();
+  return HROM_OK;
+}
+
+hrom_status launch_eps_cells(hrom_ctx* c) {
+  eps_cells_kernel<<<c->nsm * 4, 256, 0, c->st>>>(c->g, c->b.lists + (int64_t)L_S * c->g.N, c->b.counts + L_S,
+                                                   c->b.eps_elem, c->b.eps);
+  HROM_LAUNCH_CK();
+  return HROM_OK;
+}
+
+hrom_status launch_eps_all(hrom_ctx* c) {
+  eps_all_kernel<<<c->nsm * 4, 256, 0, c->st>>>(c->g, c->b.eps_elem, c->b.eps);
+  HROM_LAUNCH_CK();
+  return HROM_OK;
+}
+
+hrom_status launch_mean(hrom_ctx* c, const Win& W, double* out) {
+  mean_kernel<<<c->nsm * 8, 256, 0, c->st>>>(c->g, W, c->b.ring, out);
+  HROM_LAUNCH_CK();
+  return HROM_OK;
+}
+
+}  // namespace hrom

@@ -1,0 +1,146 @@
+// internal.cuh -- shared definitions of libhrom (product path; no oracle code).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <cstdio>
+#include <vector>
+#include "../../include/hrom.h"
+
+#define HROM_CK(x)                                                                        \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess) {                                                              \
+      fprintf(stderr, "libhrom: CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, \
+              __LINE__);                                                                  \
+      return HROM_E_CUDA;                                                                 \
+    }                                                                                     \
+  } while (0)
+
+#define HROM_LAUNCH_CK()                 \
+  do {                                   \
+    cudaError_t e_ = cudaGetLastError(); \
+    if (e_ != cudaSuccess) {             \
+      fprintf(stderr, "libhrom: launch error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return HROM_E_CUDA;                \
+    }                                    \
+  } while (0)
+
+namespace hrom {
+
+constexpr int kMaxW = 128;           // largest window supported (config 5)
+constexpr int kMaxSlots = kMaxW + 2; // ring slots
+constexpr int kMaxR = 64;
+
+// Geometry passed by value to kernels.
+struct Geo {
+  int dim, nx, ny, c, bc, recon, wpr;  // wpr = mask words per row
+  int64_t N, D, Dp;                    // Dp: padded slot stride (multiple of 32 doubles)
+  double dx, dy, gamma, cfl;
+};
+
+// Slot descriptor of the basis: union slots (oldest first), psi_prev = mean of the first w,
+// psi_cur = mean of the last w, X columns = the last w union slots.
+struct Win {
+  int nU, w;
+  int slot[kMaxW + 1];
+};
+
+// mask indices
+enum { M_S = 0, M_B, M_T, M_A2, M_A1, M_TMP, M_TMP2, M_KEEP, M_COUNT };
+// list indices
+enum { L_S = 0, L_B, L_T, L_A2, L_A1, L_COUNT };
+
+struct Bufs {
+  double* ring = nullptr;     // nslots * Dp
+  double* rho = nullptr;      // Dp
+  double* U1 = nullptr;       // Dp (stage outputs / filter scratch)
+  double* U2 = nullptr;
+  double* U3 = nullptr;
+  double* Vorig = nullptr;    // Dp
+  double* eps = nullptr;      // N
+  double* eps_elem = nullptr; // Dp
+  uint32_t* masks = nullptr;  // M_COUNT * mwords
+  int32_t* lists = nullptr;   // L_COUNT * N
+  int32_t* counts = nullptr;  // 16 ints (device)
+  uint8_t* kept = nullptr;    // N bytes (filter kept flags)
+  double* C = nullptr;        // kMaxSlots^2
+  double* part = nullptr;     // partial sums
+  int64_t part_len = 0;
+  double* gpart = nullptr;    // Gram-row partials (fill + band)
+  int64_t gpart_len = 0;
+  double* K = nullptr;        // (kMaxW+1)^2 gathered Gram
+  double* A = nullptr;        // w x r (column j: mode j)
+  double* lam = nullptr;      // w eigenvalues
+  double* y = nullptr;        // r
+  double* cvec = nullptr;     // w
+  double* zvec = nullptr;     // w (bootstrap projection coefficients)
+  double* eigV = nullptr;     // kMaxSlots^2 scratch (eigenvectors when not in smem)
+  double* eigA = nullptr;     // kMaxSlots^2 scratch
+  int32_t* ireg = nullptr;    // small int registers: [0] reff, [1] err cell lo, ...
+  double* dreg = nullptr;     // small double registers: [0] dt, ...
+  unsigned long long* ureg = nullptr;  // [0] smax bits, [1] min bad cell
+  // sampling scratch
+  double* sel_val = nullptr;   // N
+  int32_t* sel_cell = nullptr; // N
+  int32_t* blk = nullptr;      // block counts/offsets for compaction (max blocks * L_COUNT * 2)
+  int64_t blk_len = 0;
+  int32_t* hist = nullptr;     // 256 + select state
+  // filter stats per block
+  double* fstat = nullptr;
+  int32_t* fcnt = nullptr;
+  const double** colptr = nullptr;  // device array of column pointers (Gram)
+  int32_t* slot_tab = nullptr;      // slot_tab[i] = i mod nslots
+};
+
+}  // namespace hrom
+
+struct hrom_ctx {
+  hrom::Geo g;
+  hrom_params P;
+  int w, r, nslots;
+  cudaStream_t st;
+  int nsm;
+  int64_t mwords;
+  hrom::Bufs b;
+  // host bookkeeping
+  int64_t k = -1;            // index of the latest snapshot
+  bool basis_ready = false;  // basis for step k+1 available
+  bool sets_ready = false;   // S-hat_{k+1} sets built
+  bool gram_row_ready = false;
+  int64_t rebase_k = -1000000;
+  hrom::Win win{};           // window of the current basis
+  int fill_blocks = 0;       // grid of the fill kernel (Gram-row partial count)
+  int band_blocks = 0;
+  int filter_blocks = 0;
+  int64_t last_err_cell = -1;
+  int slot_of(int64_t kk) const { return (int)(kk % nslots); }
+};
+
+namespace hrom {
+// euler.cu
+hrom_status launch_dt(hrom_ctx* c, const double* q, double dt_override);
+hrom_status launch_stage(hrom_ctx* c, int stage, const double* qn, const double* qin, double* out,
+                         const int32_t* list, int list_idx, double dt_override);
+hrom_status launch_positivity(hrom_ctx* c, const double* q);
+// masks.cu
+hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S);
+hrom_status select_topn(hrom_ctx* c, const double* eps, int64_t n_g);
+hrom_status compact_masks(hrom_ctx* c, const int* which, int nwhich);
+// linalg.cu
+hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int ncol, int64_t rows,
+                      const double* rho, double* dev_C, int ldc, const int32_t* map);
+hrom_status gram_gathered(hrom_ctx* c, const double* src_b);
+hrom_status small_solve(hrom_ctx* c);
+hrom_status basis_from_gram(hrom_ctx* c, const Win& W);
+hrom_status lift(hrom_ctx* c, const Win& W, double* phi, double* psi);
+// fill.cu
+hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S, double* out,
+                        int out_slot);
+hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot);
+hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_band);
+hrom_status launch_eps_cells(hrom_ctx* c);
+hrom_status launch_mean(hrom_ctx* c, const Win& W, double* out);
+// filter.cu
+hrom_status launch_filter(hrom_ctx* c, double* v, const double* F);
+hrom_status launch_band_gram(hrom_ctx* c, const Win& W, const double* v);
+}  // namespace hrom

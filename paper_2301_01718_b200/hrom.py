@@ -1,0 +1,255 @@
+"""Thin ctypes binding of libhrom (include/hrom.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels of
+libhrom.so.  PyTorch provides device memory and the stream.  There is no CPU
+fallback: if libhrom.so cannot be loaded, or no CUDA device is present, every
+constructor raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhrom.so")
+
+HROM_STATUS = {0: "ok", 1: "invalid argument", 2: "call out of order", 3: "non-positive density or pressure",
+               4: "zero least-squares matrix", 5: "CUDA error", 6: "out of device memory"}
+
+
+class HromError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        super().__init__(f"{where}: {HROM_STATUS.get(code, code)} (status {code})")
+        self.code = code
+
+
+class Grid(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("nx", C.c_int32), ("ny", C.c_int32),
+                ("x0", C.c_double), ("x1", C.c_double), ("y0", C.c_double), ("y1", C.c_double),
+                ("bc", C.c_int32), ("recon", C.c_int32)]
+
+
+class Params(C.Structure):
+    _fields_ = [("window", C.c_int32), ("rank", C.c_int32), ("halo", C.c_int32), ("band", C.c_int32),
+                ("filter_orders", C.c_int32 * 3), ("n_filter_orders", C.c_int32),
+                ("filter_max_sweeps", C.c_int32), ("filter_eps", C.c_double),
+                ("eig_rel_cutoff", C.c_double), ("lsq_rel_cutoff", C.c_double),
+                ("sample_fraction", C.c_double), ("gram_mode", C.c_int32), ("rebase_period", C.c_int32)]
+
+
+# every entry point of include/hrom.h with its ctypes signature
+_VP = C.c_void_p
+_SIGS = {
+    "hrom_create": (C.c_int, [C.POINTER(Grid), C.c_double, C.c_double, C.POINTER(Params), _VP, C.POINTER(_VP)]),
+    "hrom_destroy": (None, [_VP]),
+    "hrom_set_state": (C.c_int, [_VP, _VP]),
+    "hrom_get_state": (C.c_int, [_VP, _VP]),
+    "hrom_full_step": (C.c_int, [_VP, C.c_double, _VP]),
+    "hrom_hybrid_step": (C.c_int, [_VP, _VP, C.c_double, _VP]),
+    "hrom_update_basis": (C.c_int, [_VP]),
+    "hrom_sample": (C.c_int, [_VP, C.c_double, _VP, _VP, _VP, _VP]),
+    "hrom_reconstruct": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    "hrom_filter": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    "hrom_step": (C.c_int, [_VP, C.c_double]),
+    "hrom_sync": (C.c_int, [_VP]),
+    "hrom_error_cell": (C.c_int64, [_VP]),
+    "hrom_step_index": (C.c_int64, [_VP]),
+    "hrom_effective_rank": (C.c_int32, [_VP]),
+    "hrom_status_string": (C.c_char_p, [C.c_int]),
+    "hrom_set_window": (C.c_int, [_VP, C.c_int64, _VP, C.c_int32, _VP]),
+    "hrom_get_basis": (C.c_int, [_VP, _VP, _VP]),
+    "hrom_get_indicator": (C.c_int, [_VP, _VP]),
+    "hrom_get_mask": (C.c_int, [_VP, _VP]),
+    "hrom_get_y": (C.c_int, [_VP, _VP]),
+    "hrom_get_eigen": (C.c_int, [_VP, _VP]),
+    "hrom_mask_words": (C.c_int64, [_VP]),
+    "hrom_gram": (C.c_int, [_VP, _VP, C.c_int32, C.c_int64, _VP, _VP]),
+}
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libhrom.so and bind every symbol; raises if the library or a symbol is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libhrom.so not built at {path}; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)  # AttributeError if the ABI lost a symbol
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    return C.c_void_p(t.data_ptr())
+
+
+def _ck(code: int, where: str):
+    if code != 0:
+        raise HromError(code, where)
+
+
+def mask_from_cells(wl, cells, device="cuda") -> torch.Tensor:
+    """Row-padded N-bit bitmap (hrom.h convention) of a cell list or a 0/1 array of length N."""
+    import numpy as np
+    arr = np.asarray(cells)
+    if arr.dtype == np.uint8 or arr.dtype == bool:
+        if arr.size != wl.N:
+            raise ValueError("0/1 mask must have N entries")
+        idx = np.nonzero(arr)[0]
+    else:
+        idx = arr.astype(np.int64)
+    wpr = (wl.nx + 31) // 32
+    ny = wl.ny if wl.dim == 2 else 1
+    nwords = max(ny * wpr, (wl.N + 31) // 32)
+    words = np.zeros(nwords, dtype=np.uint32)
+    i = idx % wl.nx
+    j = idx // wl.nx
+    np.bitwise_or.at(words, j * wpr + i // 32, (np.uint32(1) << (i % 32).astype(np.uint32)))
+    return torch.from_numpy(words.view(np.int32).copy()).to(device)
+
+
+def cells_from_mask(wl, words: torch.Tensor):
+    import numpy as np
+    w = words.cpu().numpy().view(np.uint32)
+    wpr = (wl.nx + 31) // 32
+    ny = wl.ny if wl.dim == 2 else 1
+    out = np.zeros(wl.N, dtype=np.uint8)
+    for j in range(ny):
+        row = w[j * wpr:(j + 1) * wpr]
+        bits = ((row[:, None] >> np.arange(32, dtype=np.uint32)[None, :]) & 1).reshape(-1)[: wl.nx]
+        out[j * wl.nx:(j + 1) * wl.nx] = bits
+    return out
+
+
+class HybridROM:
+    """One hrom_ctx: an explicit hybrid-snapshot AROM on one grid, on the current CUDA device."""
+
+    def __init__(self, wl, stream: Optional[torch.cuda.Stream] = None, gram_mode: int = 0,
+                 rebase_period: int = 0):
+        if not torch.cuda.is_available():
+            raise RuntimeError("libhrom needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+        self.lib = load_library()
+        self.wl = wl
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        g = Grid(wl.dim, wl.nx, wl.ny if wl.dim == 2 else 1, wl.x0, wl.x1, wl.y0, wl.y1, wl.bc, wl.recon)
+        fo = (C.c_int32 * 3)(*(list(wl.filter_orders) + [0, 0, 0])[:3])
+        p = Params(wl.w, wl.r, wl.h, wl.W, fo, len(wl.filter_orders), wl.filter_max_sweeps, wl.filter_eps,
+                   wl.eig_rel_cutoff, wl.lsq_rel_cutoff, wl.f, gram_mode, rebase_period)
+        h = C.c_void_p()
+        _ck(self.lib.hrom_create(C.byref(g), wl.gamma, wl.cfl, C.byref(p), C.c_void_p(self.stream.cuda_stream),
+                                 C.byref(h)), "hrom_create")
+        self.h = h
+        self.mask_words = int(self.lib.hrom_mask_words(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.hrom_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- state ----
+    def set_state(self, q: torch.Tensor):
+        assert q.dtype == torch.float64 and q.is_contiguous() and q.numel() == self.wl.D
+        _ck(self.lib.hrom_set_state(self.h, _ptr(q)), "hrom_set_state")
+
+    def get_state(self, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((self.wl.c, self.wl.N), dtype=torch.float64, device="cuda")
+        _ck(self.lib.hrom_get_state(self.h, _ptr(out)), "hrom_get_state")
+        return out
+
+    # ---- hot path ----
+    def full_step(self, dt: float = 0.0, dt_out: Optional[torch.Tensor] = None):
+        _ck(self.lib.hrom_full_step(self.h, dt, _ptr(dt_out)), "hrom_full_step")
+
+    def hybrid_step(self, mask: Optional[torch.Tensor] = None, dt: float = 0.0, dt_out: Optional[torch.Tensor] = None):
+        _ck(self.lib.hrom_hybrid_step(self.h, _ptr(mask), dt, _ptr(dt_out)), "hrom_hybrid_step")
+
+    def update_basis(self):
+        _ck(self.lib.hrom_update_basis(self.h), "hrom_update_basis")
+
+    def sample(self, fraction: Optional[float] = None, eps: Optional[torch.Tensor] = None,
+               mask_out: Optional[torch.Tensor] = None, list_out: Optional[torch.Tensor] = None,
+               count_out: Optional[torch.Tensor] = None):
+        f = self.wl.f if fraction is None else fraction
+        _ck(self.lib.hrom_sample(self.h, f, _ptr(eps), _ptr(mask_out), _ptr(list_out), _ptr(count_out)), "hrom_sample")
+
+    def reconstruct(self, v: torch.Tensor, mask: Optional[torch.Tensor] = None,
+                    y_out: Optional[torch.Tensor] = None, eps_out: Optional[torch.Tensor] = None):
+        _ck(self.lib.hrom_reconstruct(self.h, _ptr(mask), _ptr(v), _ptr(y_out), _ptr(eps_out)), "hrom_reconstruct")
+
+    def filter(self, v: torch.Tensor, F: torch.Tensor, mask: Optional[torch.Tensor] = None,
+               kept_out: Optional[torch.Tensor] = None):
+        _ck(self.lib.hrom_filter(self.h, _ptr(mask), _ptr(v), _ptr(F), _ptr(kept_out)), "hrom_filter")
+
+    def step(self, dt: float = 0.0):
+        _ck(self.lib.hrom_step(self.h, dt), "hrom_step")
+
+    def sync(self):
+        code = self.lib.hrom_sync(self.h)
+        if code == 3:
+            raise HromError(code, f"hrom_sync (cell {self.lib.hrom_error_cell(self.h)})")
+        _ck(code, "hrom_sync")
+
+    @property
+    def k(self) -> int:
+        return int(self.lib.hrom_step_index(self.h))
+
+    def effective_rank(self) -> int:
+        return int(self.lib.hrom_effective_rank(self.h))
+
+    # ---- replay / inspection hooks ----
+    def set_window(self, k: int, snaps: torch.Tensor, mask_next: Optional[torch.Tensor] = None):
+        assert snaps.dtype == torch.float64 and snaps.is_contiguous()
+        _ck(self.lib.hrom_set_window(self.h, k, _ptr(snaps), snaps.shape[0], _ptr(mask_next)), "hrom_set_window")
+
+    def basis(self):
+        r = self.effective_rank()
+        phi = torch.empty((max(r, 1), self.wl.D), dtype=torch.float64, device="cuda")
+        psi = torch.empty((self.wl.c, self.wl.N), dtype=torch.float64, device="cuda")
+        _ck(self.lib.hrom_get_basis(self.h, _ptr(phi), _ptr(psi)), "hrom_get_basis")
+        return phi[:r], psi
+
+    def indicator(self) -> torch.Tensor:
+        e = torch.empty(self.wl.N, dtype=torch.float64, device="cuda")
+        _ck(self.lib.hrom_get_indicator(self.h, _ptr(e)), "hrom_get_indicator")
+        return e
+
+    def mask(self) -> torch.Tensor:
+        m = torch.empty(self.mask_words, dtype=torch.int32, device="cuda")
+        _ck(self.lib.hrom_get_mask(self.h, _ptr(m)), "hrom_get_mask")
+        return m
+
+    def y(self) -> torch.Tensor:
+        y = torch.zeros(self.wl.r, dtype=torch.float64, device="cuda")
+        _ck(self.lib.hrom_get_y(self.h, _ptr(y)), "hrom_get_y")
+        return y
+
+    def eigenvalues(self) -> torch.Tensor:
+        lam = torch.empty(self.wl.w, dtype=torch.float64, device="cuda")
+        _ck(self.lib.hrom_get_eigen(self.h, _ptr(lam)), "hrom_get_eigen")
+        return lam
+
+    def gram(self, cols: torch.Tensor, rho: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """C = (S - rho)^T (S - rho) for the rows of a (ncol, rows) tensor (DMMA kernel)."""
+        ncol, rows = cols.shape
+        ptrs = torch.tensor([cols[i].data_ptr() for i in range(ncol)], dtype=torch.int64, device="cuda")
+        out = torch.empty((ncol, ncol), dtype=torch.float64, device="cuda")
+        _ck(self.lib.hrom_gram(self.h, _ptr(ptrs), ncol, rows, _ptr(rho), _ptr(out)), "hrom_gram")
+        return out

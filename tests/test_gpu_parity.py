@@ -1,0 +1,239 @@
+"""GPU parity: libhrom (CUDA, sm_100a) vs the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star, BJ:5): per-step state relative L2 <= 1e-12,
+200-step trajectory <= 1e-9, masks and compacted lists bit-exact when both sides are
+fed the oracle's indicator, basis subspaces principal-angle sine <= 1e-10 on the
+well-separated leading modes (reading A15).
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2301_01718_b200 import hrom as H  # noqa: E402
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def small2d(inputs, **kw):
+    wl = inputs.Workload("small2d", dim=2, nx=70, ny=45, bc=0, recon=2, cfl=0.4, w=8, r=5, f=0.12,
+                         h=2, W=3, seed=21)
+    return dataclasses.replace(wl, **kw)
+
+
+CASES = [
+    ("1d-first-transmissive", dict(dim=1, nx=1000, ny=1, bc=0, recon=1, cfl=0.5), "sod"),
+    ("1d-muscl-periodic", dict(dim=1, nx=333, ny=1, bc=1, recon=2), "random"),
+    ("2d-muscl-transmissive-ragged", dict(nx=100, ny=37, bc=0), "quadrant"),
+    ("2d-muscl-periodic", dict(nx=64, ny=48, bc=1), "blasts"),
+    ("2d-first-periodic-ragged", dict(nx=45, ny=33, bc=1, recon=1), "random"),
+]
+
+
+@pytest.mark.parametrize("name,kw,kind", CASES, ids=[c[0] for c in CASES])
+def test_full_step_parity(orc, inputs, name, kw, kind):
+    wl = small2d(inputs, **kw)
+    q = inputs.initial_condition(wl, kind)
+    rom = H.HybridROM(wl)
+    rom.set_state(dev(q))
+    dt_dev = torch.zeros(1, dtype=torch.float64, device="cuda")
+    qo = q.copy()
+    for step in range(5):
+        rom.full_step(dt_out=dt_dev)
+        dto = orc.dt(wl, qo)
+        qo = orc.full_step(wl, qo, dto)
+        torch.cuda.synchronize()
+        assert abs(dt_dev.item() - dto) <= 1e-14 * dto
+        g = rom.get_state().cpu().numpy()
+        assert rel(g, qo) <= 1e-12, (step, rel(g, qo))
+
+
+def test_full_step_conservation_and_free_stream(inputs):
+    wl = small2d(inputs, nx=96, ny=64, bc=1)
+    q = inputs.initial_condition(wl, "blasts")
+    rom = H.HybridROM(wl)
+    rom.set_state(dev(q))
+    for _ in range(10):
+        rom.full_step()
+    g = rom.get_state().cpu().numpy()
+    scale = np.abs(g).sum(axis=1)
+    assert np.all(np.abs(g.sum(axis=1) - q.sum(axis=1)) <= 1e-13 * scale)
+    u = inputs.initial_condition(wl, "uniform")
+    rom.set_state(dev(u))
+    rom.full_step()
+    assert np.array_equal(rom.get_state().cpu().numpy(), u)
+
+
+def _mask_dev(wl, m):
+    return H.mask_from_cells(wl, m.astype(np.uint8))
+
+
+def test_sample_bit_exact(orc, inputs):
+    """H8 fed the oracle's indicator: S-hat bit-exact, ties by ascending index (A18)."""
+    wl = small2d(inputs, nx=130, ny=77, bc=1)
+    rom = H.HybridROM(wl)
+    q = inputs.initial_condition(wl, "random")
+    rom.set_state(dev(q))
+    rng = np.random.default_rng(3)
+    for trial in range(6):
+        eps = np.round(rng.random(wl.N) * 50) / 50.0 * (rng.random(wl.N) < 0.4)  # ties and zeros
+        f = [0.01, 0.05, 0.1, 0.2, 0.5, 1.0][trial]
+        ng = orc.n_g(f, wl.N)
+        m_o, k_o = orc.select(eps, ng)
+        mw = torch.zeros(rom.mask_words, dtype=torch.int32, device="cuda")
+        lst = torch.zeros(wl.N, dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+        rom.sample(f, eps=dev(eps), mask_out=mw, list_out=lst, count_out=cnt)
+        torch.cuda.synchronize()
+        m_g = H.cells_from_mask(wl, mw)
+        assert np.array_equal(m_g, m_o), trial
+        n = int(cnt.item())
+        assert n == k_o
+        assert np.array_equal(lst[:n].cpu().numpy(), np.nonzero(m_o)[0])
+
+
+def _replay_case(orc, inputs, wl, seed=5, frac=0.12, amp=0.03):
+    snaps = inputs.smooth_window(wl, wl.w + 1, seed=seed, amp=amp)
+    rng = np.random.default_rng(seed)
+    S = (rng.random(wl.N) < frac).astype(np.uint8)
+    return snaps, S
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(bc=1, nx=64, ny=40), dict(dim=1, nx=500, ny=1, recon=1, w=12, r=6)],
+                         ids=["2d-transmissive", "2d-periodic", "1d"])
+def test_hybrid_step_replay_parity(orc, inputs, kw):
+    """One hybrid step from the same window and S-hat on both sides (Alg. 1)."""
+    wl = small2d(inputs, **kw)
+    snaps, S = _replay_case(orc, inputs, wl)
+    k = wl.w + 5
+    R = orc.Run(wl, snaps[0])
+    R.set_window(k, snaps, S)
+    rom = H.HybridROM(wl)
+    rom.set_window(k, dev(snaps.reshape(wl.w + 1, -1)), _mask_dev(wl, S))
+    # basis parity before the step: eigenvalues of X^T X = sigma^2
+    lam = rom.eigenvalues().cpu().numpy()
+    sig = R.sigma()
+    re = R.reff()
+    assert rom.effective_rank() == re
+    np.testing.assert_allclose(lam[:re], sig[:re] ** 2, rtol=1e-9, atol=1e-13 * sig[0] ** 2)
+    phi_g, psi_g = rom.basis()
+    phi_o = R.basis()
+    np.testing.assert_allclose(psi_g.cpu().numpy().reshape(-1), R.psi().reshape(-1), rtol=1e-14, atol=1e-15)
+    P = phi_g.cpu().numpy().T
+    # subspace of the leading j modes is fixed to ~eps*lambda_0/(lambda_{j-1}-lambda_j) (A15):
+    # check the largest j <= r_eff whose gap makes that <= 1e-12
+    lamo = sig ** 2
+    lamo_next = np.append(lamo[1:], 0.0)
+    ok = [j for j in range(1, re + 1) if 2.2e-16 * lamo[0] / max(lamo[j - 1] - lamo_next[j - 1], 1e-300) <= 1e-12]
+    nchk = max(ok) if ok else 1
+    Q = phi_o[:, :nchk]
+    sines = np.linalg.svd(P[:, :nchk] - Q @ (Q.T @ P[:, :nchk]), compute_uv=False)
+    assert sines.max() <= 1e-10, (nchk, sines.max())
+    # the step
+    dt = orc.dt(wl, snaps[-1])
+    R.step(dt)
+    rom.hybrid_step(dt=dt)
+    rom.sync()
+    g = rom.get_state().cpu().numpy()
+    o = R.state()
+    assert rel(g, o) <= 1e-12, rel(g, o)
+    # S-hat rows are exact HDM rows on both sides
+    full = orc.full_step(wl, snaps[-1], dt)
+    assert rel(g[:, S == 1], full[:, S == 1]) <= 1e-13
+    eg = rom.indicator().cpu().numpy()
+    eo = R.eps()
+    assert np.array_equal(eg > 0, eo > 0)
+    np.testing.assert_allclose(eg, eo, rtol=1e-6, atol=1e-12 * max(eo.max(), 1e-300))
+
+
+def test_masked_rows_bitwise_equal_full_step(inputs):
+    """Exact restriction (Eq. 7): S-hat rows of the GPU hybrid step == GPU full step, bitwise."""
+    wl = small2d(inputs, nx=80, ny=50, bc=1)
+    snaps = inputs.smooth_window(wl, wl.w + 1, seed=9, amp=0.05)
+    rng = np.random.default_rng(2)
+    S = (rng.random(wl.N) < 0.1).astype(np.uint8)
+    a = H.HybridROM(wl)
+    a.set_window(wl.w + 2, dev(snaps.reshape(wl.w + 1, -1)), _mask_dev(wl, S))
+    dt = 1.3e-3
+    a.hybrid_step(dt=dt)
+    b = H.HybridROM(wl)
+    b.set_state(dev(snaps[-1]))
+    b.full_step(dt=dt)
+    ga = a.get_state().cpu().numpy()
+    gb = b.get_state().cpu().numpy()
+    assert np.array_equal(ga[:, S == 1], gb[:, S == 1])
+
+
+def test_full_sample_set_equals_full_step(inputs):
+    """BJ:5: exact reconstruction of the sampled cells when the sample set covers the grid."""
+    wl = small2d(inputs, nx=48, ny=40, bc=0)
+    snaps = inputs.smooth_window(wl, wl.w + 1, seed=4, amp=0.05)
+    a = H.HybridROM(wl)
+    a.set_window(wl.w + 2, dev(snaps.reshape(wl.w + 1, -1)), _mask_dev(wl, np.ones(wl.N, np.uint8)))
+    a.hybrid_step(dt=1e-3)
+    b = H.HybridROM(wl)
+    b.set_state(dev(snaps[-1]))
+    b.full_step(dt=1e-3)
+    assert np.array_equal(a.get_state().cpu().numpy(), b.get_state().cpu().numpy())
+
+
+def test_gram_dmma_vs_oracle(orc, inputs):
+    wl = small2d(inputs)
+    rom = H.HybridROM(wl)
+    for ncol, rows in [(7, 1000), (33, 4097), (65, 20011), (130, 3001)]:
+        S = inputs.random_values(ncol + 1, ncol * rows, 0.5, 1.5).reshape(ncol, rows)
+        rho = inputs.random_values(ncol + 2, rows, 0.5, 1.5)
+        Cg = rom.gram(dev(S), dev(rho)).cpu().numpy()
+        Co = orc.gram(S, rho)
+        assert np.max(np.abs(Cg - Co)) <= 1e-13 * np.max(np.abs(Co)), ncol
+
+
+def test_trajectory_config1(orc, inputs):
+    """200-step Algorithm-1 trajectory of config 1 (BJ:7) <= 1e-9, masks compared per step."""
+    wl = inputs.config(1)
+    q0 = inputs.initial_condition(wl)
+    rom = H.HybridROM(wl)
+    rom.set_state(dev(q0))
+    R = orc.Run(wl, q0)
+    flips = 0
+    worst = 0.0
+    for k in range(1, wl.steps + 1):
+        rom.step()
+        R.step()
+        if k >= wl.w - 1:
+            mg = H.cells_from_mask(wl, rom.mask())
+            if not np.array_equal(mg, R.mask()):
+                flips += 1
+        if k % 20 == 0 or k == wl.steps:
+            g = rom.get_state().cpu().numpy()
+            worst = max(worst, rel(g, R.state()))
+    rom.sync()
+    assert flips == 0, f"{flips} mask flips"
+    assert worst <= 1e-9, worst
+
+
+def test_determinism_bitwise(inputs):
+    wl = inputs.config(1, steps=40)
+    q0 = inputs.initial_condition(wl)
+    outs = []
+    for _ in range(2):
+        rom = H.HybridROM(wl)
+        rom.set_state(dev(q0))
+        for _ in range(wl.steps):
+            rom.step()
+        outs.append(rom.get_state().cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])

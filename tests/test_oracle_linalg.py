@@ -134,3 +134,13 @@ def test_lsq_rank_deficient_cutoff(orc, inputs):
 def test_lsq_empty(orc):
     x, rank = orc.lsq(np.zeros((0, 3)), np.zeros(0))
     assert rank == 0 and np.all(x == 0)
+
+
+def test_gram_matches_definition(orc, inputs):
+    """C = (S - rho)^T (S - rho) (snapshot Gram, P:634 remark) vs LAPACK-free brute force."""
+    S = inputs.random_matrix(30, 7, 200).copy()  # 7 columns of 200 rows
+    rho = inputs.random_values(31, 200, 0.5, 1.5)
+    C = orc.gram(S, rho)
+    ref = np.array([[float(np.sum((S[i] - rho) * (S[j] - rho))) for j in range(7)] for i in range(7)])
+    np.testing.assert_allclose(C, ref, rtol=1e-13)
+    assert np.array_equal(C, C.T)
