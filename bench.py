@@ -1,0 +1,306 @@
+#!/usr/bin/env python
+"""Benchmark of the hybrid-snapshot step (BASELINE.json metric, BJ:2):
+hybrid-step cell-updates/s (fp64) at 2D 2048^2, with the fill pass's fraction of the
+measured HBM roofline.
+
+python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config 4] [--fraction 0.1]
+
+One step = one hybrid step of Algorithm 1: H1 dt, H3 masked RK3, H4-H5 gappy
+solve, H6 fill + indicator (+H9/H10 window Gram row), H7 seam filter, H10-H12 basis update,
+H8 sampling -- every row of SURVEY §8(a).  The w-1 warm-up full steps that fill the window
+are set-up, outside the timed region.  Multi-GPU: one independent problem per rank (seed
++ rank), no data-path collective ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "hybrid-step cell-updates/s (fp64) at 2D 2048²; % of HBM / FP64-TC roofline"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.path = f"/tmp/hrom_clocks_{os.getpid()}.csv"
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 8:
+                try:
+                    rows.append((float(f[0]), float(f[1]), f[4], f[5], f[6], f[7]))
+                except ValueError:
+                    pass
+        if not rows:
+            return None
+        sm = sorted(r[0] for r in rows)
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": rows[0][1], "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def fill_bytes(wl, n_s: int) -> int:
+    """Algorithmic bytes of one fill-pass launch: read the w+1 window
+    columns and the Gram shift, write gamma_k; read the partial-HDM values and write the
+    squared errors on the c*n_s S-hat DOFs; two N-bit masks."""
+    D = wl.D
+    return 8 * D * (wl.w + 1 + 1 + 1) + 16 * wl.c * n_s + 2 * (wl.N // 8)
+
+
+def run_hrom(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    from paper_2301_01718_b200 import inputs
+    from paper_2301_01718_b200.hrom import HybridROM, SECTIONS
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    wl = inputs.config(args.config, f=args.fraction, seed=args.config + 1000 * rank)
+    q0 = inputs.initial_condition(wl)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        rom = HybridROM(wl, stream=stream, gram_mode=args.gram_mode)
+        rom.set_state(torch.from_numpy(q0).cuda())
+        # set-up: w-1 full steps + bootstrap (not timed)
+        for _ in range(wl.w - 1):
+            rom.step()
+        # full-step throughput for contrast (separate context state is not needed: time 5 steps on a copy)
+        rom.sync()
+        # warm-up hybrid steps
+        for _ in range(args.warmup):
+            rom.step()
+        rom.sync()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clocks = ClockSampler(local_rank) if rank == 0 else None
+        rom.profile(True)
+        l0 = rom.launch_count()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            rom.step()
+        ev1.record(stream)
+        ev1.synchronize()
+        rom.sync()
+        launches = rom.launch_count() - l0
+        sec = rom.profile_read()
+        rom.profile(False)
+        ms_total = ev0.elapsed_time(ev1)
+        ck = clocks.stop() if clocks else None
+        # S-hat size and mask stats (outside the timed region)
+        n_s = int(H_count(rom, wl))
+        # end-to-end through the C ABI with host buffers: put gamma_{k-1} from pinned host
+        # memory, step, read gamma_k back (D2H) every step
+        host = torch.empty((wl.c, wl.N), dtype=torch.float64, pin_memory=True)
+        rom.get_state(host)
+        rom.sync()
+        e2e_steps = max(2, min(args.steps, 10))
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            rom.put_state(host)
+            rom.step()
+            rom.get_state(host)
+        e1.record(stream)
+        e1.synchronize()
+        rom.sync()
+        ms_e2e = e0.elapsed_time(e1) / e2e_steps
+        # full-step throughput for contrast
+        fs = HybridROM(wl, stream=stream)
+        fs.set_state(torch.from_numpy(q0).cuda())
+        fs.full_step()
+        fs.sync()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(5):
+            fs.full_step()
+        f1.record(stream)
+        f1.synchronize()
+        ms_full = f0.elapsed_time(f1) / 5
+        fs.close()
+    # max over ranks
+    ms_step = ms_total / args.steps
+    if dist:
+        t = torch.tensor([ms_step, ms_e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step, ms_e2e = float(t[0]), float(t[1])
+    out = None
+    if rank == 0:
+        value = wl.N * world / (ms_step / 1000.0)
+        peak, peak_src = measured_peaks()
+        fill_ms, fill_n = sec["fill_pass"]
+        fb = fill_bytes(wl, n_s)
+        fill_avg_ms = fill_ms / max(fill_n, 1)
+        achieved = fb / (fill_avg_ms / 1000.0) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "fill_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        split = {k: round(v[0] / max(args.steps, 1), 4) for k, v in sec.items() if v[1]}
+        out = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "cell-updates/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded config-4 blasts, BASELINE.json configs[3]; DESIGN.md §3)",
+            "config": {"workload": wl.name, "grid": f"{wl.nx}x{wl.ny}", "cells": wl.N, "dofs": wl.D,
+                       "window_w": wl.w, "rank_r": wl.r, "sample_fraction": wl.f, "halo": wl.h, "band_W": wl.W,
+                       "gram_mode": "incremental-shifted" if args.gram_mode == 0 else "full-dmma",
+                       "n_s_last": n_s, "l2": "inputs larger than L2 (window %.1f GB)" % ((wl.w + 2) * wl.D * 8 / 1e9),
+                       "parallelism": f"independent problem per GPU x{world}"},
+            "roofline": {"kernel": "fill_pass (H6+H9+H10 row)", "bound": "hbm", "achieved": achieved,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": fb, "avg_launch_ms": fill_avg_ms,
+                         "share_of_step": fill_ms / ms_total if ms_total > 0 else None, "peak_source": peak_src},
+            "section_ms_per_step": split,
+            "full_step": {"ms": ms_full, "cell_updates_per_s": wl.N / (ms_full / 1000.0)},
+            "clocks": ck,
+            "e2e": {"value": wl.N * world / (ms_e2e / 1000.0), "unit": "cell-updates/s",
+                    "h2d_bytes_per_step": wl.D * 8, "d2h_bytes_per_step": wl.D * 8, "ms_per_step": ms_e2e,
+                    "steps": e2e_steps},
+            "gpu_launches": int(launches),
+        }
+    rom.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def H_count(rom, wl):
+    from paper_2301_01718_b200.hrom import cells_from_mask
+    return int(cells_from_mask(wl, rom.mask()).sum())
+
+
+def cpu_sample(steps: int = 1, side: int = 256):
+    """The oracle (oracle/, untuned) on a bounded sample of the config-4 workload: a
+    side x side periodic tile with the config-4 method parameters (w = 64, r = 32,
+    f = 10 %, W = 3, MUSCL-Rusanov), window seeded by the shared generator, one hybrid
+    step of Algorithm 1 per sample, single thread."""
+    import numpy as np
+    import oracle
+    from paper_2301_01718_b200 import inputs
+    wl = inputs.config(4, nx=side, ny=side)
+    snaps = inputs.smooth_window(wl, wl.w + 1, seed=7, amp=0.03)
+    rng = np.random.default_rng(7)
+    S = (rng.random(wl.N) < wl.f).astype(np.uint8)
+    times = []
+    for _ in range(steps):
+        R = oracle.Run(wl, snaps[0])
+        R.set_window(wl.w + 1, snaps, S)
+        t0 = time.perf_counter()
+        R.step()
+        t1 = time.perf_counter()
+        times.append(t1 - t0)
+    t = float(np.median(times))
+    return {"value": wl.N / t, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
+            "sample": f"one oracle hybrid step (H1-H12, incl. POD of the 65-column window) on a {side}x{side} periodic tile "
+                      f"with config-4 parameters (w=64, r=32, f=10%), median of {steps}; per-cell work is size-independent",
+            "seconds_per_step": t}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="hrom", choices=["hrom", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--fraction", type=float, default=0.10)
+    ap.add_argument("--gram-mode", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        samples = []
+        for _ in range(args.warmup):
+            cpu_sample(1)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            samples.append(cpu_sample(1)["seconds_per_step"])
+        ms = 1000.0 * sum(samples) / len(samples)
+        side = 256
+        value = side * side / (ms / 1000.0)
+        base = {"value": value, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
+                "sample": f"one oracle hybrid step on a {side}x{side} periodic tile with config-4 parameters per step"}
+        print(json.dumps({"impl": "reference", "metric": METRIC, "value": value, "unit": "cell-updates/s",
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic", "config": {"workload": "config4-blasts-2048 (oracle sample)"},
+                          "cpu_baseline": base,
+                          "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0},
+                          "wall_s": time.perf_counter() - t0}))
+        return
+    out = run_hrom(args, rank, world, local_rank)
+    if rank == 0 and out is not None:
+        if world == 1 and not args.no_cpu:
+            out["cpu_baseline"] = cpu_sample(1)
+        print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

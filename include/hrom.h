@@ -143,6 +143,19 @@ int64_t hrom_mask_words(const hrom_ctx* ctx);                        /* words pe
  * dev_rho (nullable = 0), dev_C: ncol*ncol output. Standalone op (config 5). */
 hrom_status hrom_gram(hrom_ctx* ctx, const double* const* dev_cols, int32_t ncol, int64_t rows,
                       const double* dev_rho, double* dev_C);
+/* Overwrite gamma_k (the latest snapshot) in place, without touching the schedule
+ * (end-to-end benchmarking of host-resident states). */
+hrom_status hrom_put_state(hrom_ctx* ctx, const double* any_q);
+
+/* ---- measurement hooks ---- */
+/* enable != 0: record CUDA events around each section of the step on the context stream.
+ * Sections: 0 dt, 1 masked RK3, 2 gathered Gram, 3 pinv solve, 4 fill pass, 5 indicator,
+ * 6 seam filter, 7 band Gram, 8 positivity, 9 basis update, 10 sampling, 11 full step. */
+hrom_status hrom_profile(hrom_ctx* ctx, int32_t enable);
+/* Synchronises; per-section summed milliseconds and counts since the last read. */
+hrom_status hrom_profile_read(hrom_ctx* ctx, double* ms, int64_t* counts, int32_t nsec);
+/* Number of kernels this context has launched (host-side count). */
+int64_t hrom_launch_count(const hrom_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -226,11 +226,13 @@ hrom_status hrom_full_step(hrom_ctx* c, double dt_override, double* dev_dt_out) 
   const double* qn = c->b.ring + (int64_t)c->slot_of(c->k) * c->g.Dp;
   double* out = c->b.ring + (int64_t)c->slot_of(kn) * c->g.Dp;
   hrom_status s;
+  prof_begin(c, SEC_FULL);
   if ((s = launch_dt(c, qn, dt_override)) != HROM_OK) return s;
   if (dev_dt_out) HROM_CK(cudaMemcpyAsync(dev_dt_out, c->b.dreg, sizeof(double), cudaMemcpyDefault, c->st));
   if ((s = launch_stage(c, 1, qn, qn, c->b.U1, nullptr, 0, dt_override)) != HROM_OK) return s;
   if ((s = launch_stage(c, 2, qn, c->b.U1, c->b.U2, nullptr, 0, dt_override)) != HROM_OK) return s;
   if ((s = launch_stage(c, 3, qn, c->b.U2, out, nullptr, 0, dt_override)) != HROM_OK) return s;
+  prof_end(c, SEC_FULL);
   c->k = kn;
   c->gram_row_ready = false;
   c->sets_ready = false;
@@ -252,26 +254,44 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
   const double* qn = b.ring + (int64_t)c->slot_of(c->k) * g.Dp;
   double* out = b.ring + (int64_t)c->slot_of(kn) * g.Dp;
   // H1
+  prof_begin(c, SEC_DT);
   if ((s = launch_dt(c, qn, dt_override)) != HROM_OK) return s;
+  prof_end(c, SEC_DT);
   if (dev_dt_out) HROM_CK(cudaMemcpyAsync(dev_dt_out, b.dreg, sizeof(double), cudaMemcpyDefault, c->st));
   // H3: stage 1 on A1, stage 2 on A2, stage 3 on T = S-hat u B (F on the band)
   const int32_t* L = b.lists;
+  prof_begin(c, SEC_MASKED);
   if ((s = launch_stage(c, 1, qn, qn, b.U1, L + (int64_t)L_A1 * g.N, L_A1, dt_override)) != HROM_OK) return s;
   if ((s = launch_stage(c, 2, qn, b.U1, b.U2, L + (int64_t)L_A2 * g.N, L_A2, dt_override)) != HROM_OK) return s;
   if ((s = launch_stage(c, 3, qn, b.U2, b.U3, L + (int64_t)L_T * g.N, L_T, dt_override)) != HROM_OK) return s;
+  prof_end(c, SEC_MASKED);
   // H4 + H5
+  prof_begin(c, SEC_GATHER);
   if ((s = gram_gathered(c, b.U3)) != HROM_OK) return s;
+  prof_end(c, SEC_GATHER);
+  prof_begin(c, SEC_SOLVE);
   if ((s = small_solve(c)) != HROM_OK) return s;
+  prof_end(c, SEC_SOLVE);
   // H6 (+H9, H10 row)
   HROM_CK(cudaMemsetAsync(b.eps, 0, g.N * sizeof(double), c->st));
+  prof_begin(c, SEC_FILL);
   if ((s = launch_fill(c, c->win, 0, b.U3, out, c->slot_of(kn))) != HROM_OK) return s;
+  prof_end(c, SEC_FILL);
+  prof_begin(c, SEC_EPS);
   if ((s = launch_eps_cells(c)) != HROM_OK) return s;
+  prof_end(c, SEC_EPS);
   // H7
+  prof_begin(c, SEC_FILTER);
   if (c->P.n_filter_orders > 0 && c->P.filter_max_sweeps > 0)
     if ((s = launch_filter(c, out, b.U3)) != HROM_OK) return s;
+  prof_end(c, SEC_FILTER);
+  prof_begin(c, SEC_BANDGRAM);
   if (c->P.gram_mode == 0)
     if ((s = launch_band_gram(c, c->win, out)) != HROM_OK) return s;
+  prof_end(c, SEC_BANDGRAM);
+  prof_begin(c, SEC_POS);
   if ((s = launch_positivity(c, out)) != HROM_OK) return s;
+  prof_end(c, SEC_POS);
   c->k = kn;
   c->gram_row_ready = (c->P.gram_mode == 0);
   c->sets_ready = false;
@@ -285,6 +305,7 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
   const int64_t k = c->k;
   if (k < w - 1) return HROM_OK;
   hrom_status s;
+  prof_begin(c, SEC_BASIS);
   const Win W = window_at(c, k);
   const bool rebase = (k == w - 1) || c->P.gram_mode == 1 || (k - c->rebase_k >= c->P.rebase_period) ||
                       (!c->gram_row_ready && !c->basis_ready);
@@ -303,12 +324,14 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
     if ((s = reduce_gram_row(c, c->win, c->slot_of(k), true)) != HROM_OK) return s;
   }
   if ((s = basis_from_gram(c, W)) != HROM_OK) return s;
+  prof_end(c, SEC_BASIS);
   c->win = W;
   c->basis_ready = true;
   c->gram_row_ready = false;
   if (k == w - 1) {  // bootstrap indicator (reading A19)
     zvec_kernel<<<1, 128, 0, c->st>>>(c->b.A, c->b.lam, c->b.ireg, w, c->b.zvec);
     HROM_LAUNCH_CK();
+    ++c->nlaunch;
     if ((s = launch_fill(c, W, 2, nullptr, nullptr, -1)) != HROM_OK) return s;
     if ((s = launch_eps_all(c)) != HROM_OK) return s;
   }
@@ -321,8 +344,10 @@ hrom_status hrom_sample(hrom_ctx* c, double fraction, const double* dev_eps, uin
   if (!(fraction > 0.0 && fraction <= 1.0)) return HROM_E_INVALID;
   const int64_t n_g = (int64_t)std::ceil(fraction * (double)c->g.N);
   hrom_status s;
+  prof_begin(c, SEC_SAMPLE);
   if ((s = select_topn(c, dev_eps ? dev_eps : c->b.eps, n_g)) != HROM_OK) return s;
   if ((s = build_sets(c, nullptr)) != HROM_OK) return s;
+  prof_end(c, SEC_SAMPLE);
   c->sets_ready = true;
   if (dev_mask_out)
     HROM_CK(cudaMemcpyAsync(dev_mask_out, c->b.masks + (int64_t)M_S * c->mwords, c->mwords * sizeof(uint32_t),
@@ -469,5 +494,48 @@ hrom_status hrom_gram(hrom_ctx* c, const double* const* dev_cols, int32_t ncol, 
   if (!c || !dev_cols || !dev_C || ncol < 1 || ncol > kMaxSlots + 14 || rows < 0) return HROM_E_INVALID;
   return gram_full(c, dev_cols, ncol, rows, dev_rho, dev_C, ncol, nullptr);
 }
+
+hrom_status hrom_put_state(hrom_ctx* c, const double* any_q) {
+  if (!c || !any_q) return HROM_E_INVALID;
+  if (c->k < 0) return HROM_E_STATE;
+  HROM_CK(cudaMemcpyAsync(c->b.ring + (int64_t)c->slot_of(c->k) * c->g.Dp, any_q, c->g.D * sizeof(double),
+                          cudaMemcpyDefault, c->st));
+  return HROM_OK;
+}
+
+hrom_status hrom_profile(hrom_ctx* c, int32_t enable) {
+  if (!c) return HROM_E_INVALID;
+  HROM_CK(cudaStreamSynchronize(c->st));
+  c->ev_pairs.clear();
+  c->ev_next = 0;
+  c->prof = enable != 0;
+  if (c->prof && c->ev_pool.empty()) {
+    c->ev_pool.resize(1 << 15);
+    for (auto& e : c->ev_pool) HROM_CK(cudaEventCreate(&e));
+  }
+  return HROM_OK;
+}
+
+hrom_status hrom_profile_read(hrom_ctx* c, double* ms, int64_t* counts, int32_t nsec) {
+  if (!c || !ms || !counts) return HROM_E_INVALID;
+  HROM_CK(cudaStreamSynchronize(c->st));
+  for (int i = 0; i < nsec; ++i) {
+    ms[i] = 0.0;
+    counts[i] = 0;
+  }
+  for (const auto& p : c->ev_pairs) {
+    float t = 0.f;
+    HROM_CK(cudaEventElapsedTime(&t, c->ev_pool[p.second.first], c->ev_pool[p.second.second]));
+    if (p.first < nsec) {
+      ms[p.first] += t;
+      counts[p.first] += 1;
+    }
+  }
+  c->ev_pairs.clear();
+  c->ev_next = 0;
+  return HROM_OK;
+}
+
+int64_t hrom_launch_count(const hrom_ctx* c) { return c ? c->nlaunch : 0; }
 
 }  // extern "C"

@@ -211,6 +211,7 @@ hrom_status launch_dt(hrom_ctx* c, const double* q, double dt_override) {
   }
   dt_finalize<<<1, 1, 0, c->st>>>(c->b.ureg, c->g.cfl, dt_override, c->b.dreg, nullptr);
   HROM_LAUNCH_CK();
+  c->nlaunch += (dt_override <= 0.0) ? 2 : 1;
   return HROM_OK;
 }
 
@@ -227,6 +228,7 @@ hrom_status launch_stage(hrom_ctx* c, int stage, const double* qn, const double*
     else stage_kernel<2, 2><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg);
   }
   HROM_LAUNCH_CK();
+  c->nlaunch += 1;
   return HROM_OK;
 }
 
@@ -235,6 +237,7 @@ hrom_status launch_positivity(hrom_ctx* c, const double* q) {
   if (c->g.dim == 1) positivity_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg + 1);
   else positivity_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg + 1);
   HROM_LAUNCH_CK();
+  c->nlaunch += 1;
   return HROM_OK;
 }
 

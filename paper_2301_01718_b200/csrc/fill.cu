@@ -309,6 +309,7 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S
   HROM_CK(cudaFuncSetAttribute(fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   fill_kernel<<<grid, FT, smem, c->st>>>(a);
   HROM_LAUNCH_CK();
+  ++c->nlaunch;
   return HROM_OK;
 }
 
@@ -320,6 +321,7 @@ hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_b
   const int nblk = c->fill_blocks + (with_band ? c->band_blocks : 0);
   gram_row_reduce<<<1, 256, 0, c->st>>>(c->b.gpart, nblk, W, new_slot, c->b.C, kMaxSlots);
   HROM_LAUNCH_CK();
+  ++c->nlaunch;
   return HROM_OK;
 }
 
@@ -327,18 +329,21 @@ hrom_status launch_eps_cells(hrom_ctx* c) {
   eps_cells_kernel<<<c->nsm * 4, 256, 0, c->st>>>(c->g, c->b.lists + (int64_t)L_S * c->g.N, c->b.counts + L_S,
                                                    c->b.eps_elem, c->b.eps);
   HROM_LAUNCH_CK();
+  ++c->nlaunch;
   return HROM_OK;
 }
 
 hrom_status launch_eps_all(hrom_ctx* c) {
   eps_all_kernel<<<c->nsm * 4, 256, 0, c->st>>>(c->g, c->b.eps_elem, c->b.eps);
   HROM_LAUNCH_CK();
+  ++c->nlaunch;
   return HROM_OK;
 }
 
 hrom_status launch_mean(hrom_ctx* c, const Win& W, double* out) {
   mean_kernel<<<c->nsm * 8, 256, 0, c->st>>>(c->g, W, c->b.ring, out);
   HROM_LAUNCH_CK();
+  ++c->nlaunch;
   return HROM_OK;
 }
 

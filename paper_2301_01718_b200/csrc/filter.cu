@@ -271,6 +271,7 @@ hrom_status launch_filter(hrom_ctx* c, double* v, const double* F) {
   a.sweeps_out = c->b.ireg + 4;
   void* args[] = {&a};
   HROM_CK(cudaLaunchCooperativeKernel((void*)filter_kernel, dim3(c->filter_blocks), dim3(256), args, 0, c->st));
+  ++c->nlaunch;
   return HROM_OK;
 }
 
@@ -279,6 +280,7 @@ hrom_status launch_band_gram(hrom_ctx* c, const Win& W, const double* v) {
                                                        c->b.lists + (int64_t)L_B * c->g.N, c->b.counts + L_B,
                                                        c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1));
   HROM_LAUNCH_CK();
+  ++c->nlaunch;
   return HROM_OK;
 }
 

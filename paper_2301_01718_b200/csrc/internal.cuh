@@ -113,8 +113,31 @@ struct hrom_ctx {
   int band_blocks = 0;
   int filter_blocks = 0;
   int64_t last_err_cell = -1;
+  int64_t nlaunch = 0;       // kernels launched by this context (host-side count)
+  // optional per-section CUDA-event timing (hrom_profile)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<int, int>>> ev_pairs;  // (section, (start ev, stop ev))
+  int ev_next = 0;
+  int ev_open[16] = {0};
   int slot_of(int64_t kk) const { return (int)(kk % nslots); }
 };
+
+namespace hrom {
+enum Section { SEC_DT = 0, SEC_MASKED, SEC_GATHER, SEC_SOLVE, SEC_FILL, SEC_EPS, SEC_FILTER, SEC_BANDGRAM,
+               SEC_POS, SEC_BASIS, SEC_SAMPLE, SEC_FULL, SEC_COUNT };
+inline void prof_begin(hrom_ctx* c, int sec) {
+  if (!c->prof || c->ev_next + 2 > (int)c->ev_pool.size()) return;
+  c->ev_open[sec] = c->ev_next;
+  cudaEventRecord(c->ev_pool[c->ev_next++], c->st);
+}
+inline void prof_end(hrom_ctx* c, int sec) {
+  if (!c->prof || c->ev_next + 1 > (int)c->ev_pool.size()) return;
+  cudaEventRecord(c->ev_pool[c->ev_next], c->st);
+  c->ev_pairs.push_back({sec, {c->ev_open[sec], c->ev_next}});
+  ++c->ev_next;
+}
+}  // namespace hrom
 
 namespace hrom {
 // euler.cu

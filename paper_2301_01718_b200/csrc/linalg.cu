@@ -430,6 +430,7 @@ hrom_status launch_gram(hrom_ctx* c, const GramArgs& a, int grid) {
   HROM_CK(cudaFuncSetAttribute(gram_kernel<TPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   gram_kernel<TPW><<<grid, GT, smem, c->st>>>(a);
   HROM_LAUNCH_CK();
+  ++c->nlaunch;
   return HROM_OK;
 }
 
@@ -464,6 +465,7 @@ hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int ncol, int6
   if (s != HROM_OK) return s;
   gram_reduce<<<64, 256, 0, c->st>>>(c->b.part, grid, ncp, ncol, dev_C, ldc, map);
   HROM_LAUNCH_CK();
+  ++c->nlaunch;
   return HROM_OK;
 }
 
@@ -487,6 +489,7 @@ hrom_status gram_gathered(hrom_ctx* c, const double* src_b) {
   if (s != HROM_OK) return s;
   gram_reduce<<<64, 256, 0, c->st>>>(c->b.part, grid, ncp, a.ncol, c->b.K, a.ncol, nullptr);
   HROM_LAUNCH_CK();
+  ++c->nlaunch;
   return HROM_OK;
 }
 
@@ -496,6 +499,7 @@ hrom_status small_solve(hrom_ctx* c) {
   solve_kernel<<<1, 512, smem, c->st>>>(c->b.K, c->win.w, c->r, c->b.A, c->b.ireg, c->P.lsq_rel_cutoff, c->b.y,
                                         c->b.cvec, c->b.ireg + 2);
   HROM_LAUNCH_CK();
+  ++c->nlaunch;
   return HROM_OK;
 }
 
@@ -507,12 +511,14 @@ hrom_status basis_from_gram(hrom_ctx* c, const Win& W) {
   basis_kernel<<<1, 1024, smem, c->st>>>(c->b.C, kMaxSlots, W, c->r, c->P.eig_rel_cutoff, c->b.A, c->b.lam,
                                          c->b.ireg, c->b.eigV);
   HROM_LAUNCH_CK();
+  ++c->nlaunch;
   return HROM_OK;
 }
 
 hrom_status lift(hrom_ctx* c, const Win& W, double* phi, double* psi) {
   lift_kernel<<<c->nsm * 4, 256, 0, c->st>>>(c->g, W, c->b.ring, c->b.A, c->b.ireg, phi, psi);
   HROM_LAUNCH_CK();
+  ++c->nlaunch;
   return HROM_OK;
 }
 

@@ -214,6 +214,7 @@ hrom_status run_compaction(hrom_ctx* c, const CmpJob& job, int64_t nwords) {
   cmp_scan_kernel<<<job.n, 1024, 0, c->st>>>(job, c->b.blk, nblk);
   cmp_write_kernel<<<grid, CB, 0, c->st>>>(job, c->g, nwords, c->b.blk, nblk);
   HROM_LAUNCH_CK();
+  c->nlaunch += 3;
   return HROM_OK;
 }
 
@@ -355,6 +356,7 @@ hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S) {
   cross_kernel<<<grid, 256, 0, c->st>>>(g, M + M_T * mw, M + M_A2 * mw, c->P.halo);
   cross_kernel<<<grid, 256, 0, c->st>>>(g, M + M_A2 * mw, M + M_A1 * mw, c->P.halo);
   HROM_LAUNCH_CK();
+  c->nlaunch += 4;
   const int which[5] = {L_S, L_B, L_T, L_A2, L_A1};
   return compact_masks(c, which, 5);
 }
@@ -398,6 +400,7 @@ hrom_status select_topn(hrom_ctx* c, const double* eps, int64_t n_g) {
   cmp_scan_kernel<<<1, 1024, 0, c->st>>>(one, c->b.blk, nb);
   sel_mark_write<<<nb, 1024, 0, c->st>>>(c->g, c->b.sel_val, c->b.sel_cell, cnt, st, c->b.blk, S);
   HROM_LAUNCH_CK();
+  c->nlaunch += 1 + 1 + 16 + 3;
   return HROM_OK;
 }
 

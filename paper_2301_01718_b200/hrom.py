@@ -67,7 +67,14 @@ _SIGS = {
     "hrom_get_eigen": (C.c_int, [_VP, _VP]),
     "hrom_mask_words": (C.c_int64, [_VP]),
     "hrom_gram": (C.c_int, [_VP, _VP, C.c_int32, C.c_int64, _VP, _VP]),
+    "hrom_put_state": (C.c_int, [_VP, _VP]),
+    "hrom_profile": (C.c_int, [_VP, C.c_int32]),
+    "hrom_profile_read": (C.c_int, [_VP, _VP, _VP, C.c_int32]),
+    "hrom_launch_count": (C.c_int64, [_VP]),
 }
+
+SECTIONS = ["dt", "masked_rk3", "gathered_gram", "pinv_solve", "fill_pass", "indicator", "seam_filter",
+            "band_gram", "positivity", "basis_update", "sampling", "full_step"]
 
 _lib = None
 
@@ -245,6 +252,22 @@ class HybridROM:
         lam = torch.empty(self.wl.w, dtype=torch.float64, device="cuda")
         _ck(self.lib.hrom_get_eigen(self.h, _ptr(lam)), "hrom_get_eigen")
         return lam
+
+    def put_state(self, q: torch.Tensor):
+        _ck(self.lib.hrom_put_state(self.h, _ptr(q)), "hrom_put_state")
+
+    def profile(self, enable: bool = True):
+        _ck(self.lib.hrom_profile(self.h, int(enable)), "hrom_profile")
+
+    def profile_read(self):
+        ms = (C.c_double * len(SECTIONS))()
+        cnt = (C.c_int64 * len(SECTIONS))()
+        _ck(self.lib.hrom_profile_read(self.h, C.cast(ms, C.c_void_p), C.cast(cnt, C.c_void_p), len(SECTIONS)),
+            "hrom_profile_read")
+        return {name: (ms[i], cnt[i]) for i, name in enumerate(SECTIONS)}
+
+    def launch_count(self) -> int:
+        return int(self.lib.hrom_launch_count(self.h))
 
     def gram(self, cols: torch.Tensor, rho: Optional[torch.Tensor] = None) -> torch.Tensor:
         """C = (S - rho)^T (S - rho) for the rows of a (ncol, rows) tensor (DMMA kernel)."""
