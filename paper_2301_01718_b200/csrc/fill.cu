@@ -97,12 +97,16 @@ __global__ void __launch_bounds__(FT, 1) fill_kernel(FillArgs a) {
     const int64_t cnt = (g.D - e0) < TE ? (g.D - e0) : TE;
     const uint32_t bytes = (uint32_t)(((cnt + 1) / 2) * 2 * sizeof(double));
     double* dst = stage0 + st * stage_elems;
-    mbar_expect(&bars[st], bytes * ncol);
-    for (int s = 0; s < nU; ++s) bulk_g2s(dst + (size_t)s * TE, a.ring + (int64_t)a.W.slot[s] * g.Dp + e0, bytes, &bars[st]);
-    bulk_g2s(dst + (size_t)nU * TE, a.rho + e0, bytes, &bars[st]);
+    // warp 0 issues the ncol bulk copies lane-parallel (one elected lane arms the barrier)
+    if (lane == 0) mbar_expect(&bars[st], bytes * ncol);
+    __syncwarp();
+    for (int s = lane; s <= nU; s += 32) {
+      const double* src = (s < nU) ? a.ring + (int64_t)a.W.slot[s] * g.Dp + e0 : a.rho + e0;
+      bulk_g2s(dst + (size_t)s * TE, src, bytes, &bars[st]);
+    }
   };
   int64_t first = blockIdx.x;
-  if (tid == 0)
+  if (warp == 0)
     for (int s = 0; s < a.nstage; ++s)
       if (first + (int64_t)s * gridDim.x < ntiles) issue(first + (int64_t)s * gridDim.x, s);
   double acc[MAXSPW];
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(FT, 1) fill_kernel(FillArgs a) {
       }
     }
     __syncthreads();  // stage fully consumed
-    if (tid == 0) {
+    if (warp == 0) {
       const int64_t nt = tile + (int64_t)a.nstage * gridDim.x;
       if (nt < ntiles) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");

@@ -186,11 +186,11 @@ __device__ void jacobi_eig(double* A, double* V, int n, int ldn, double* lam, in
   if (tid == 0) {
     double m = 0.0;
     for (int i = 0; i < n; ++i) m = fmax(m, fabs(A[i * ldn + i]));
-    floor_abs = 1e-18 * m;
+    floor_abs = 1e-14 * m;  // below the Gram's own rounding level (~n eps lambda_max): not resolvable
   }
   __syncthreads();
   const int np = ne / 2;
-  for (int sweep = 0; sweep < 40; ++sweep) {
+  for (int sweep = 0; sweep < 20; ++sweep) {
     if (tid == 0) *flag = 0;
     __syncthreads();
     for (int rnd = 0; rnd < ne - 1; ++rnd) {
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(1024) basis_kernel(const double* __restrict__ 
                                                      int32_t* __restrict__ reff_out, double* __restrict__ Vg) {
   extern __shared__ double sm[];
   const int w = W.w, nU = W.nU;
-  const int ldn = w + (w & 1);
+  const int ldn = w + (w & 1) + 1;  // odd stride: column sweeps are bank-conflict free
   double* M = sm;                                   // ldn*ldn
   const bool vsm = (2 * ldn * ldn + 4 * kMaxSlots) * 8 <= 200 * 1024;
   double* V = vsm ? sm + ldn * ldn : Vg;
@@ -341,11 +341,11 @@ __global__ void __launch_bounds__(1024) solve_kernel(const double* __restrict__ 
   extern __shared__ double sm[];
   const int re = *reffp;
   const int ldk = w + 1;
-  const int ldn = re + (re & 1) > 0 ? re + (re & 1) : 2;
+  const int ldn = re + (re & 1) + 1;  // odd stride
   double* T = sm;                 // w x re  (K_XX A)
   double* G = T + w * kMaxR;      // ldn x ldn
-  double* V = G + kMaxR * kMaxR;  // ldn x ldn
-  double* rhs = V + kMaxR * kMaxR;
+  double* V = G + (kMaxR + 2) * (kMaxR + 2);  // ldn x ldn
+  double* rhs = V + (kMaxR + 2) * (kMaxR + 2);
   double* lam = rhs + kMaxR;
   double* cs = lam + kMaxR;       // 2*kMaxR
   double* y = cs + 2 * kMaxR;
@@ -494,7 +494,7 @@ hrom_status gram_gathered(hrom_ctx* c, const double* src_b) {
 }
 
 hrom_status small_solve(hrom_ctx* c) {
-  const size_t smem = (size_t)(c->win.w * kMaxR + 2 * kMaxR * kMaxR + 6 * kMaxR) * sizeof(double);
+  const size_t smem = (size_t)(c->win.w * kMaxR + 2 * (kMaxR + 2) * (kMaxR + 2) + 6 * kMaxR) * sizeof(double);
   HROM_CK(cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   solve_kernel<<<1, 512, smem, c->st>>>(c->b.K, c->win.w, c->r, c->b.A, c->b.ireg, c->P.lsq_rel_cutoff, c->b.y,
                                         c->b.cvec, c->b.ireg + 2);
@@ -504,7 +504,7 @@ hrom_status small_solve(hrom_ctx* c) {
 }
 
 hrom_status basis_from_gram(hrom_ctx* c, const Win& W) {
-  const int ldn = W.w + (W.w & 1);
+  const int ldn = W.w + (W.w & 1) + 1;
   const bool vsm = (2 * ldn * ldn + 4 * kMaxSlots) * 8 <= 200 * 1024;
   const size_t smem = (size_t)((vsm ? 2 : 1) * ldn * ldn + 4 * kMaxSlots) * sizeof(double);
   HROM_CK(cudaFuncSetAttribute(basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
