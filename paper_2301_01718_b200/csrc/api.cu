@@ -310,12 +310,16 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
   const bool rebase = (k == w - 1) || c->P.gram_mode == 1 || (k - c->rebase_k >= c->P.rebase_period) ||
                       (!c->gram_row_ready && !c->basis_ready);
   if (rebase) {
+    prof_end(c, SEC_BASIS);
+    prof_begin(c, SEC_REBASE);
     if ((s = launch_mean(c, W, c->b.rho)) != HROM_OK) return s;
     const int s0 = W.slot[0];
     // consecutive slots are contiguous in the pointer table (see hrom_create)
     // written straight into the slot-indexed Gram through the slot table
     if ((s = gram_full(c, c->b.colptr + s0, W.nU, c->g.D, c->b.rho, c->b.C, kMaxSlots, c->b.slot_tab + s0)) != HROM_OK)
       return s;
+    prof_end(c, SEC_REBASE);
+    prof_begin(c, SEC_BASIS);
     c->rebase_k = k;
   } else if (!c->gram_row_ready) {
     if ((s = launch_gram_row(c, c->win, c->slot_of(k))) != HROM_OK) return s;

@@ -113,60 +113,74 @@ __global__ void __launch_bounds__(FT, 1) fill_kernel(FillArgs a) {
 #pragma unroll
   for (int q = 0; q < MAXSPW; ++q) acc[q] = 0.0;
   double acc_self = 0.0;
+  __shared__ double csum_s;
+  if (tid == 0) {
+    double t = 0.0;
+    for (int i = 0; i < w; ++i) t += cs[i];
+    csum_s = t;
+  }
+  __syncthreads();
+  const double csum = csum_s;
   const int e_loc = tid % TE, part = tid / TE;
-  // slot ranges per part for phase A
+  // slot range of this thread's part (phase A)
   const int per = (nU + PARTS - 1) / PARTS;
+  const int s0 = part * per, s1 = min(nU, s0 + per);
+  const int xoff = nU - w;  // first X slot
   int it = 0;
   for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
     const int st = it % a.nstage;
     const uint32_t par = (uint32_t)((it / a.nstage) & 1);
-    mbar_wait(&bars[st], par);
-    const double* T = stage0 + st * stage_elems;
     const int64_t e0 = tile * TE;
     const int64_t e = e0 + e_loc;
     const bool valid = e < g.D;
-    // phase A1: partial sums for psi_prev (slots 0..w-1) and psi_cur (slots nU-w..nU-1)
+    // mask bits are fetched before waiting on the stage (latency overlap)
+    bool inS = false, inB = false;
+    int64_t n = 0;
+    if (part == 0 && valid && a.mode != MODE_PROJ) {
+      n = e % g.N;
+      if (a.mode == MODE_FILL) {
+        inS = bit_of(a.mS, g, n);
+        inB = a.mB && bit_of(a.mB, g, n);
+      }
+    }
+    double srcv = 0.0;
+    if (inS) srcv = a.src_S[e];
+    mbar_wait(&bars[st], par);
+    const double* T = stage0 + st * stage_elems;
+    const double rh = T[nU * TE + e_loc];
+    // phase A (one pass over the slots, shifted by rho):
+    //   sp = sum_{s<w} x_s, sc = sum_{s>=nU-w} x_s, tr = sum_i c_i x_{nU-w+i},  x_s = gamma_s - rho
     {
-      double sp = 0.0, sc = 0.0;
-      const int s0 = part * per, s1 = min(nU, s0 + per);
+      double sp = 0.0, sc = 0.0, tr = 0.0;
+#pragma unroll 4
       for (int s = s0; s < s1; ++s) {
-        const double v = T[s * TE + e_loc];
-        if (s < w) sp += v;
-        if (s >= nU - w) sc += v;
+        const double x = T[s * TE + e_loc] - rh;
+        if (s < w) sp += x;
+        if (s >= xoff) {
+          sc += x;
+          tr += cs[s - xoff] * x;
+        }
       }
       red[(part * TE + e_loc) * 3 + 0] = sp;
       red[(part * TE + e_loc) * 3 + 1] = sc;
-    }
-    __syncthreads();
-    double psi_prev = 0.0, psi_cur = 0.0;
-    {
-      double sp = 0.0, sc = 0.0;
-      for (int p = 0; p < PARTS; ++p) {
-        sp += red[(p * TE + e_loc) * 3 + 0];
-        sc += red[(p * TE + e_loc) * 3 + 1];
-      }
-      psi_prev = sp / (double)w;
-      psi_cur = sc / (double)w;
-    }
-    // phase A2: partial sum_i c_i (gamma_{x_i} - psi_prev), x_i = slot nU-w+i
-    {
-      double r = 0.0;
-      const int i0 = part * ((w + PARTS - 1) / PARTS), i1 = min(w, i0 + (w + PARTS - 1) / PARTS);
-      for (int i = i0; i < i1; ++i) r += cs[i] * (T[(nU - w + i) * TE + e_loc] - psi_prev);
-      __syncthreads();  // everyone has read red[...][0..1]
-      red[(part * TE + e_loc) * 3 + 2] = r;
+      red[(part * TE + e_loc) * 3 + 2] = tr;
     }
     __syncthreads();
     if (part == 0) {
       double gval = 0.0;
       if (valid) {
-        double rs = 0.0;
-        for (int p = 0; p < PARTS; ++p) rs += red[(p * TE + e_loc) * 3 + 2];
-        const int64_t n = e % g.N;
+        double sp = 0.0, sc = 0.0, tr = 0.0;
+        for (int p = 0; p < PARTS; ++p) {
+          sp += red[(p * TE + e_loc) * 3 + 0];
+          sc += red[(p * TE + e_loc) * 3 + 1];
+          tr += red[(p * TE + e_loc) * 3 + 2];
+        }
+        // psi_prev - rho = sp/w, psi_cur - rho = sc/w;  Phi y = sum_i c_i (x_i - (psi_prev - rho))
+        const double dev = tr - (sp / (double)w) * csum;
         if (a.mode == MODE_FILL) {
-          const double rec = psi_cur + rs;
-          if (bit_of(a.mS, g, n)) {
-            gval = a.src_S[e];
+          const double rec = (rh + sc / (double)w) + dev;
+          if (inS) {
+            gval = srcv;
             const double d = gval - rec;
             a.eps_elem[e] = d * d;
           } else {
@@ -176,10 +190,9 @@ __global__ void __launch_bounds__(FT, 1) fill_kernel(FillArgs a) {
         } else if (a.mode == MODE_READ) {
           gval = a.out[e];
         } else {  // MODE_PROJ: residual of the projection onto the basis (bootstrap indicator)
-          a.eps_elem[e] = rs * rs;
+          a.eps_elem[e] = dev * dev;
         }
-        const double rh = T[nU * TE + e_loc];
-        const bool skip = (a.mode == MODE_FILL && a.mB && bit_of(a.mB, g, n)) || a.mode == MODE_PROJ;
+        const bool skip = inB || a.mode == MODE_PROJ;
         const double gr = skip ? 0.0 : gval - rh;
         gt[e_loc] = gr;
         acc_self += gr * gr;
@@ -188,16 +201,20 @@ __global__ void __launch_bounds__(FT, 1) fill_kernel(FillArgs a) {
       }
     }
     __syncthreads();
-    // phase B: Gram row, warp-per-slot-set, lanes over DOFs
+    // phase B: Gram row, warp-per-slot-set, lanes over DOFs (rho and g hoisted per DOF)
     if (a.do_gram) {
       const int cnt = (int)((g.D - e0) < TE ? (g.D - e0) : TE);
 #pragma unroll
-      for (int q = 0; q < MAXSPW; ++q) {
-        const int s = warp + q * (FT / 32);
-        if (s < nU) {
-          double sacc = 0.0;
-          for (int el = lane; el < cnt; el += 32) sacc += gt[el] * (T[s * TE + el] - T[nU * TE + el]);
-          acc[q] += sacc;
+      for (int j = 0; j < TE / 32; ++j) {
+        const int el = lane + 32 * j;
+        if (el < cnt) {
+          const double gv = gt[el];
+          const double r = T[nU * TE + el];
+#pragma unroll
+          for (int q = 0; q < MAXSPW; ++q) {
+            const int s = warp + q * (FT / 32);
+            if (s < nU) acc[q] += gv * (T[s * TE + el] - r);
+          }
         }
       }
     }

@@ -125,7 +125,7 @@ struct hrom_ctx {
 
 namespace hrom {
 enum Section { SEC_DT = 0, SEC_MASKED, SEC_GATHER, SEC_SOLVE, SEC_FILL, SEC_EPS, SEC_FILTER, SEC_BANDGRAM,
-               SEC_POS, SEC_BASIS, SEC_SAMPLE, SEC_FULL, SEC_COUNT };
+               SEC_POS, SEC_BASIS, SEC_SAMPLE, SEC_FULL, SEC_REBASE, SEC_COUNT };
 inline void prof_begin(hrom_ctx* c, int sec) {
   if (!c->prof || c->ev_next + 2 > (int)c->ev_pool.size()) return;
   c->ev_open[sec] = c->ev_next;

@@ -96,9 +96,13 @@ __global__ void __launch_bounds__(GT) gram_kernel(GramArgs a) {
         tile[col * LDT + k] = v;
       }
     } else {
-      // gathered rows: row t -> (var = t / nS, idx = t % nS), element e = var*N + cell
+      // gathered rows: row t -> (var = t / nS, idx = t % nS), element e = var*N + cell.
+      // X slot s (s >= nU-w) lands in column s-(nU-w); the psi_prev-only slot (nU = w+1) in
+      // column w+1; the HDM value b in column w.  Then centre in place.
       const int nS = *a.count;
       const int nU = a.W.nU, w = a.W.w;
+      const int xoff = nU - w;
+      double* psi = smem + (size_t)ncp * LDT;  // [2][RT]
       for (int idx = threadIdx.x; idx < (nU + 1) * RT; idx += GT) {
         const int s = idx / RT, k = idx % RT;
         const int64_t row = r0 + k;
@@ -108,25 +112,32 @@ __global__ void __launch_bounds__(GT) gram_kernel(GramArgs a) {
           const int64_t e = (int64_t)var * a.g.N + a.list[ii];
           v = (s < nU) ? a.ring[(int64_t)a.W.slot[s] * a.g.Dp + e] : a.src_b[e];
         }
-        tile[s * LDT + k] = v;  // raw values, centred below
+        const int col = (s == nU) ? w : (s >= xoff ? s - xoff : w + 1);
+        tile[col * LDT + k] = v;
       }
       __syncthreads();
       if (threadIdx.x < RT) {
         const int k = threadIdx.x;
         double sp = 0.0, sc = 0.0;
-        for (int s = 0; s < w; ++s) sp += tile[s * LDT + k];
-        for (int s = nU - w; s < nU; ++s) sc += tile[s * LDT + k];
-        const double psi_prev = sp / (double)w, psi_cur = sc / (double)w;
-        const bool valid = r0 + k < total_rows;
-        // X columns 0..w-1 <- gamma_{x_i} - psi_prev, column w <- b = src - psi_cur
-        for (int i = 0; i < w; ++i)
-          tile[i * LDT + k] = valid ? tile[(nU - w + i) * LDT + k] - psi_prev : 0.0;
-        tile[w * LDT + k] = valid ? tile[nU * LDT + k] - psi_cur : 0.0;
+        for (int i = 0; i < w; ++i) sc += tile[i * LDT + k];
+        if (xoff == 1) {
+          sp = tile[(w + 1) * LDT + k];
+          for (int i = 0; i < w - 1; ++i) sp += tile[i * LDT + k];
+        } else {
+          sp = sc;
+        }
+        psi[k] = sp / (double)w;
+        psi[RT + k] = sc / (double)w;
       }
       __syncthreads();
-      for (int idx = threadIdx.x; idx < (ncp - (w + 1)) * RT; idx += GT) {
-        const int col = w + 1 + idx / RT, k = idx % RT;
-        tile[col * LDT + k] = 0.0;
+      for (int idx = threadIdx.x; idx < ncp * RT; idx += GT) {
+        const int col = idx / RT, k = idx % RT;
+        const bool valid = r0 + k < total_rows;
+        double v;
+        if (col < w) v = valid ? tile[col * LDT + k] - psi[k] : 0.0;
+        else if (col == w) v = valid ? tile[col * LDT + k] - psi[RT + k] : 0.0;
+        else v = 0.0;
+        tile[col * LDT + k] = v;
       }
     }
     __syncthreads();
@@ -202,9 +213,10 @@ __device__ void jacobi_eig(double* A, double* V, int n, int ldn, double* lam, in
         const double app = A[p * ldn + p], aqq = A[q * ldn + q], apq = A[p * ldn + q];
         double c = 1.0, s = 0.0;
         if (fabs(apq) > floor_abs && fabs(apq) > 1e-15 * sqrt(fabs(app * aqq))) {
-          const double theta = (aqq - app) / (2.0 * apq);
-          const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
-          c = 1.0 / sqrt(1.0 + t * t);
+          // t = tan(phi) of the annihilating rotation, written without 1/apq
+          const double tau = aqq - app;
+          const double t = (tau >= 0.0 ? 2.0 : -2.0) * apq / (fabs(tau) + sqrt(tau * tau + 4.0 * apq * apq));
+          c = rsqrt(1.0 + t * t);
           s = t * c;
           *flag = 1;
         }
@@ -214,35 +226,33 @@ __device__ void jacobi_eig(double* A, double* V, int n, int ldn, double* lam, in
         pq[2 * k + 1] = q;
       }
       __syncthreads();
-      // rows: A' = J^T A
-      for (int idx = tid; idx < np * ne; idx += nt) {
-        const int k = idx / ne, j = idx % ne;
-        const double c = cs[2 * k], s = cs[2 * k + 1];
-        if (s == 0.0) continue;
-        const int p = pq[2 * k], q = pq[2 * k + 1];
-        const double ap = A[p * ldn + j], aq = A[q * ldn + j];
-        A[p * ldn + j] = c * ap - s * aq;
-        A[q * ldn + j] = s * ap + c * aq;
+      // A' = J^T A J in one pass: every 2x2 block (pair k1 rows, pair k2 cols) is independent
+      for (int idx = tid; idx < np * np; idx += nt) {
+        const int k1 = idx / np, k2 = idx % np;
+        const double c1 = cs[2 * k1], s1 = cs[2 * k1 + 1], c2 = cs[2 * k2], s2 = cs[2 * k2 + 1];
+        if (s1 == 0.0 && s2 == 0.0) continue;
+        const int p1 = pq[2 * k1], q1 = pq[2 * k1 + 1], p2 = pq[2 * k2], q2 = pq[2 * k2 + 1];
+        const double b00 = A[p1 * ldn + p2], b01 = A[p1 * ldn + q2];
+        const double b10 = A[q1 * ldn + p2], b11 = A[q1 * ldn + q2];
+        const double r00 = c1 * b00 - s1 * b10, r01 = c1 * b01 - s1 * b11;
+        const double r10 = s1 * b00 + c1 * b10, r11 = s1 * b01 + c1 * b11;
+        double n00 = c2 * r00 - s2 * r01, n01 = s2 * r00 + c2 * r01;
+        double n10 = c2 * r10 - s2 * r11, n11 = s2 * r10 + c2 * r11;
+        if (k1 == k2) { n01 = 0.0; n10 = 0.0; }
+        A[p1 * ldn + p2] = n00;
+        A[p1 * ldn + q2] = n01;
+        A[q1 * ldn + p2] = n10;
+        A[q1 * ldn + q2] = n11;
       }
-      __syncthreads();
-      // columns: A'' = A' J, V' = V J
-      for (int idx = tid; idx < np * ne; idx += nt) {
-        const int k = idx / ne, i = idx % ne;
+      // V' = V J
+      for (int idx = tid; idx < ne * np; idx += nt) {
+        const int i = idx / np, k = idx % np;
         const double c = cs[2 * k], s = cs[2 * k + 1];
         if (s == 0.0) continue;
         const int p = pq[2 * k], q = pq[2 * k + 1];
-        const double ap = A[i * ldn + p], aq = A[i * ldn + q];
-        A[i * ldn + p] = c * ap - s * aq;
-        A[i * ldn + q] = s * ap + c * aq;
         const double vp = V[i * ldn + p], vq = V[i * ldn + q];
         V[i * ldn + p] = c * vp - s * vq;
         V[i * ldn + q] = s * vp + c * vq;
-      }
-      __syncthreads();
-      if (tid < np && cs[2 * tid + 1] != 0.0) {
-        const int p = pq[2 * tid], q = pq[2 * tid + 1];
-        A[p * ldn + q] = 0.0;
-        A[q * ldn + p] = 0.0;
       }
       __syncthreads();
     }
@@ -426,7 +436,7 @@ __global__ void lift_kernel(Geo g, Win W, const double* __restrict__ ring, const
 
 template <int TPW>
 hrom_status launch_gram(hrom_ctx* c, const GramArgs& a, int grid) {
-  const size_t smem = (size_t)a.nsb * 16 * LDT * sizeof(double);
+  const size_t smem = ((size_t)a.nsb * 16 * LDT + 2 * RT) * sizeof(double);
   HROM_CK(cudaFuncSetAttribute(gram_kernel<TPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   gram_kernel<TPW><<<grid, GT, smem, c->st>>>(a);
   HROM_LAUNCH_CK();
