@@ -542,4 +542,11 @@ hrom_status hrom_profile_read(hrom_ctx* c, double* ms, int64_t* counts, int32_t 
 
 int64_t hrom_launch_count(const hrom_ctx* c) { return c ? c->nlaunch : 0; }
 
+hrom_status hrom_debug_counters(hrom_ctx* c, int32_t* any_out, int32_t n) {
+  if (!c || !any_out || n < 0 || n > 16) return HROM_E_INVALID;
+  HROM_CK(cudaStreamSynchronize(c->st));
+  HROM_CK(cudaMemcpy(any_out, c->b.ireg, n * sizeof(int32_t), cudaMemcpyDefault));
+  return HROM_OK;
+}
+
 }  // extern "C"

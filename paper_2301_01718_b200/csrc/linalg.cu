@@ -184,7 +184,7 @@ __global__ void gram_reduce(const double* __restrict__ part, int nblk, int ncp, 
 // A (n x n, ld = ldn, symmetric) is overwritten; V receives eigenvectors (columns);
 // lam/perm: eigenvalues in descending order and the column permutation.
 __device__ void jacobi_eig(double* A, double* V, int n, int ldn, double* lam, int* perm, double* cs,
-                           int* pq, int* flag) {
+                           int* pq, int* flag, int32_t* sweeps_out) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int ne = n + (n & 1);  // even size (padded index has zero row/col)
   for (int idx = tid; idx < ne * ne; idx += nt) {
@@ -256,6 +256,7 @@ __device__ void jacobi_eig(double* A, double* V, int n, int ldn, double* lam, in
       }
       __syncthreads();
     }
+    if (tid == 0 && sweeps_out) *sweeps_out = sweep + 1;
     if (*flag == 0) break;
     __syncthreads();
   }
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(1024) basis_kernel(const double* __restrict__ 
     M[i * ldn + j] = ((C[xi * ldc + xj] - mi) - mj) + mu;
   }
   __syncthreads();
-  jacobi_eig(M, V, w, ldn, lam, perm, cs, pq, &flag);
+  jacobi_eig(M, V, w, ldn, lam, perm, cs, pq, &flag, reff_out + 8);
   if (tid == 0) {
     int re = 0;
     const double l0 = lam[0];
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(1024) solve_kernel(const double* __restrict__ 
     G[j * ldn + i] = s;
   }
   __syncthreads();
-  if (re > 0) jacobi_eig(G, V, re, ldn, lam, perm, cs, pq, &flag);
+  if (re > 0) jacobi_eig(G, V, re, ldn, lam, perm, cs, pq, &flag, status + 7);
   if (tid < kMaxR) y[tid] = 0.0;
   __syncthreads();
   if (tid == 0) {

@@ -71,6 +71,7 @@ _SIGS = {
     "hrom_profile": (C.c_int, [_VP, C.c_int32]),
     "hrom_profile_read": (C.c_int, [_VP, _VP, _VP, C.c_int32]),
     "hrom_launch_count": (C.c_int64, [_VP]),
+    "hrom_debug_counters": (C.c_int, [_VP, _VP, C.c_int32]),
 }
 
 SECTIONS = ["dt", "masked_rk3", "gathered_gram", "pinv_solve", "fill_pass", "indicator", "seam_filter",
@@ -268,6 +269,11 @@ class HybridROM:
 
     def launch_count(self) -> int:
         return int(self.lib.hrom_launch_count(self.h))
+
+    def debug_counters(self, n: int = 8):
+        out = (C.c_int32 * n)()
+        _ck(self.lib.hrom_debug_counters(self.h, C.cast(out, C.c_void_p), n), "hrom_debug_counters")
+        return list(out)
 
     def gram(self, cols: torch.Tensor, rho: Optional[torch.Tensor] = None) -> torch.Tensor:
         """C = (S - rho)^T (S - rho) for the rows of a (ncol, rows) tensor (DMMA kernel)."""

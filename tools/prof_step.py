@@ -1,0 +1,24 @@
+"""Config-4 hybrid steps with per-section timings and device counters (profiling helper;
+also the command ncu wraps: `ncu -k regex:fill_kernel -s 3 -c 1 python tools/prof_step.py`)."""
+import sys, os, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2301_01718_b200 import inputs
+from paper_2301_01718_b200.hrom import HybridROM
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+nh = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+f = float(sys.argv[3]) if len(sys.argv) > 3 else 0.1
+wl = inputs.config(cfg, f=f)
+rom = HybridROM(wl)
+rom.set_state(torch.from_numpy(inputs.initial_condition(wl)).cuda())
+for _ in range(wl.w - 1):
+    rom.step()
+rom.sync()
+for k in range(nh):
+    rom.profile(True)
+    rom.step()
+    sec = rom.profile_read()
+    cnt = rom.debug_counters(12)
+    print(f"hybrid {k}: " + " ".join(f"{n}={v[0]:.3f}" for n, v in sec.items() if v[1]), "counters", cnt, flush=True)
+rom.sync()
