@@ -150,7 +150,8 @@ hrom_status hrom_put_state(hrom_ctx* ctx, const double* any_q);
 /* ---- measurement hooks ---- */
 /* enable != 0: record CUDA events around each section of the step on the context stream.
  * Sections: 0 dt, 1 masked RK3, 2 gathered Gram, 3 pinv solve, 4 fill pass, 5 indicator,
- * 6 seam filter, 7 band Gram, 8 positivity, 9 basis update, 10 sampling, 11 full step. */
+ * 6 seam filter, 7 band Gram, 8 positivity, 9 basis update (Gram row), 10 sampling, 11 full step,
+ * 12 Gram re-base, 13 eigen-solve (side stream, overlaps sections 10, 0-2 of the next step). */
 hrom_status hrom_profile(hrom_ctx* ctx, int32_t enable);
 /* Synchronises; per-section summed milliseconds and counts since the last read. */
 hrom_status hrom_profile_read(hrom_ctx* ctx, double* ms, int64_t* counts, int32_t nsec);

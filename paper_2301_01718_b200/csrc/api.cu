@@ -116,7 +116,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev);
   c->mwords = std::max<int64_t>((int64_t)g.ny * g.wpr, (g.N + 31) / 32);
-  c->fill_blocks = c->nsm;
+  c->fill_blocks = 2 * c->nsm;  // two fill CTAs per SM (fill.cu smem budget)
   c->band_blocks = c->nsm;
   const int occ = std::max(1, std::min(4, filter_occupancy()));
   c->filter_blocks = c->nsm * occ;
@@ -183,14 +183,25 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
     hrom_destroy(c);
     return HROM_E_CUDA;
   }
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_basis_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_basis_done, cudaEventDisableTiming) != cudaSuccess) {
+    hrom_destroy(c);
+    return HROM_E_CUDA;
+  }
   *out = c;
   return HROM_OK;
 }
 
 void hrom_destroy(hrom_ctx* c) {
   if (!c) return;
+  if (c->side) cudaStreamSynchronize(c->side);
   if (c->st) cudaStreamSynchronize(c->st);
   else cudaDeviceSynchronize();
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_basis_in) cudaEventDestroy(c->ev_basis_in);
+  if (c->ev_basis_done) cudaEventDestroy(c->ev_basis_done);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
   Bufs& b = c->b;
   void* ptrs[] = {b.ring, b.rho, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
                   b.kept, b.C, b.part, b.gpart, b.K, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
@@ -269,6 +280,7 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
   prof_begin(c, SEC_GATHER);
   if ((s = gram_gathered(c, b.U3)) != HROM_OK) return s;
   prof_end(c, SEC_GATHER);
+  basis_join(c);  // the eigen-solve of the previous update ran on the side stream
   prof_begin(c, SEC_SOLVE);
   if ((s = small_solve(c)) != HROM_OK) return s;
   prof_end(c, SEC_SOLVE);
@@ -305,6 +317,7 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
   const int64_t k = c->k;
   if (k < w - 1) return HROM_OK;
   hrom_status s;
+  basis_join(c);  // C is rewritten below
   prof_begin(c, SEC_BASIS);
   const Win W = window_at(c, k);
   const bool rebase = (k == w - 1) || c->P.gram_mode == 1 || (k - c->rebase_k >= c->P.rebase_period) ||
@@ -327,12 +340,26 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
   } else {
     if ((s = reduce_gram_row(c, c->win, c->slot_of(k), true)) != HROM_OK) return s;
   }
-  if ((s = basis_from_gram(c, W)) != HROM_OK) return s;
   prof_end(c, SEC_BASIS);
+  {
+    // eigen-solve on the side stream; consumers call basis_join()
+    HROM_CK(cudaEventRecord(c->ev_basis_in, c->st));
+    HROM_CK(cudaStreamWaitEvent(c->side, c->ev_basis_in, 0));
+    cudaStream_t main_st = c->st;
+    c->st = c->side;
+    prof_begin(c, SEC_EIGEN);
+    s = basis_from_gram(c, W);
+    prof_end(c, SEC_EIGEN);
+    c->st = main_st;
+    if (s != HROM_OK) return s;
+    HROM_CK(cudaEventRecord(c->ev_basis_done, c->side));
+    c->basis_pending = true;
+  }
   c->win = W;
   c->basis_ready = true;
   c->gram_row_ready = false;
   if (k == w - 1) {  // bootstrap indicator (reading A19)
+    basis_join(c);
     zvec_kernel<<<1, 128, 0, c->st>>>(c->b.A, c->b.lam, c->b.ireg, w, c->b.zvec);
     HROM_LAUNCH_CK();
     ++c->nlaunch;
@@ -375,6 +402,7 @@ hrom_status hrom_reconstruct(hrom_ctx* c, const uint32_t* dev_mask, double* dev_
   }
   if (!c->sets_ready) return HROM_E_STATE;
   if ((s = gram_gathered(c, dev_v)) != HROM_OK) return s;
+  basis_join(c);
   if ((s = small_solve(c)) != HROM_OK) return s;
   HROM_CK(cudaMemsetAsync(c->b.eps, 0, c->g.N * sizeof(double), c->st));
   if ((s = launch_fill(c, c->win, 0, dev_v, dev_v, -1)) != HROM_OK) return s;
@@ -417,6 +445,7 @@ hrom_status hrom_step(hrom_ctx* c, double dt_override) {
 
 hrom_status hrom_sync(hrom_ctx* c) {
   if (!c) return HROM_E_INVALID;
+  basis_join(c);
   HROM_CK(cudaStreamSynchronize(c->st));
   unsigned long long bad = 0;
   HROM_CK(cudaMemcpy(&bad, c->b.ureg + 1, sizeof(bad), cudaMemcpyDeviceToHost));
@@ -434,6 +463,7 @@ int64_t hrom_mask_words(const hrom_ctx* c) { return c ? c->mwords : 0; }
 int32_t hrom_effective_rank(hrom_ctx* c) {
   if (!c) return -1;
   int32_t r = 0;
+  basis_join(c);
   if (cudaStreamSynchronize(c->st) != cudaSuccess) return -1;
   if (cudaMemcpy(&r, c->b.ireg, sizeof(r), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
   return r;
@@ -465,6 +495,7 @@ hrom_status hrom_set_window(hrom_ctx* c, int64_t k, const double* any_snaps, int
 hrom_status hrom_get_basis(hrom_ctx* c, double* dev_phi, double* dev_psi) {
   if (!c) return HROM_E_INVALID;
   if (!c->basis_ready) return HROM_E_STATE;
+  basis_join(c);
   return lift(c, c->win, dev_phi, dev_psi);
 }
 
@@ -489,6 +520,7 @@ hrom_status hrom_get_y(hrom_ctx* c, double* any_y) {
 
 hrom_status hrom_get_eigen(hrom_ctx* c, double* any_lambda) {
   if (!c || !any_lambda) return HROM_E_INVALID;
+  basis_join(c);
   HROM_CK(cudaMemcpyAsync(any_lambda, c->b.lam, c->w * sizeof(double), cudaMemcpyDefault, c->st));
   return HROM_OK;
 }
@@ -509,6 +541,7 @@ hrom_status hrom_put_state(hrom_ctx* c, const double* any_q) {
 
 hrom_status hrom_profile(hrom_ctx* c, int32_t enable) {
   if (!c) return HROM_E_INVALID;
+  basis_join(c);
   HROM_CK(cudaStreamSynchronize(c->st));
   c->ev_pairs.clear();
   c->ev_next = 0;
@@ -522,6 +555,7 @@ hrom_status hrom_profile(hrom_ctx* c, int32_t enable) {
 
 hrom_status hrom_profile_read(hrom_ctx* c, double* ms, int64_t* counts, int32_t nsec) {
   if (!c || !ms || !counts) return HROM_E_INVALID;
+  basis_join(c);
   HROM_CK(cudaStreamSynchronize(c->st));
   for (int i = 0; i < nsec; ++i) {
     ms[i] = 0.0;
@@ -544,6 +578,7 @@ int64_t hrom_launch_count(const hrom_ctx* c) { return c ? c->nlaunch : 0; }
 
 hrom_status hrom_debug_counters(hrom_ctx* c, int32_t* any_out, int32_t n) {
   if (!c || !any_out || n < 0 || n > 16) return HROM_E_INVALID;
+  basis_join(c);
   HROM_CK(cudaStreamSynchronize(c->st));
   HROM_CK(cudaMemcpy(any_out, c->b.ireg, n * sizeof(int32_t), cudaMemcpyDefault));
   return HROM_OK;

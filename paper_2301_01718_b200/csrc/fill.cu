@@ -11,15 +11,15 @@
 //     filter by filter.cu).
 // psi_prev / psi_cur are recomputed from the columns in registers: the
 // reference state is never stored or drifted.
+#include <algorithm>
 #include "internal.cuh"
 
 namespace hrom {
 namespace {
 
-constexpr int FT = 256;   // threads per CTA
-constexpr int TE = 128;   // DOFs per tile
-constexpr int PARTS = FT / TE;
-constexpr int MAXSPW = (kMaxW + 2 + (FT / 32) - 1) / (FT / 32);  // slots per warp (Gram)
+// Tiles of TE DOFs; 2*TE threads: two threads per DOF share the slot loop (phase A),
+// TE/32*2 warps share the window slots in the Gram-row phase (phase B).
+constexpr int TE_FILL = 64;
 
 enum { MODE_FILL = 0, MODE_READ = 1, MODE_PROJ = 2 };
 
@@ -73,16 +73,19 @@ __device__ __forceinline__ bool bit_of(const uint32_t* m, const Geo& g, int64_t 
   return (m[(int64_t)j * g.wpr + (i >> 5)] >> (i & 31)) & 1u;
 }
 
-__global__ void __launch_bounds__(FT, 1) fill_kernel(FillArgs a) {
+template <int TE, int SPW>
+__global__ void __launch_bounds__(2 * TE) fill_kernel(FillArgs a) {
+  constexpr int FT = 2 * TE, NW = FT / 32;
   extern __shared__ __align__(128) unsigned char smraw[];
   const int nU = a.W.nU, w = a.W.w;
   const int ncol = nU + 1;  // window slots + rho
   double* stage0 = reinterpret_cast<double*>(smraw);
   const size_t stage_elems = (size_t)ncol * TE;
   double* gt = stage0 + a.nstage * stage_elems;      // TE: g - rho (0 on band cells)
-  double* red = gt + TE;                              // PARTS * TE * 3 partial sums
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 3 * PARTS * TE);
+  double* red = gt + TE;                              // [3][TE] partial sums of part 1
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 3 * TE);
   __shared__ double cs[kMaxW];
+  __shared__ double csum_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Geo& g = a.g;
   for (int i = tid; i < w; i += FT) cs[i] = a.cvec ? a.cvec[i] : 0.0;
@@ -91,6 +94,11 @@ __global__ void __launch_bounds__(FT, 1) fill_kernel(FillArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int i = 0; i < w; ++i) t += cs[i];
+    csum_s = t;
+  }
   const int64_t ntiles = (g.D + TE - 1) / TE;
   auto issue = [&](int64_t tile, int st) {
     const int64_t e0 = tile * TE;
@@ -105,27 +113,21 @@ __global__ void __launch_bounds__(FT, 1) fill_kernel(FillArgs a) {
       bulk_g2s(dst + (size_t)s * TE, src, bytes, &bars[st]);
     }
   };
-  int64_t first = blockIdx.x;
+  const int64_t first = blockIdx.x;
   if (warp == 0)
     for (int s = 0; s < a.nstage; ++s)
       if (first + (int64_t)s * gridDim.x < ntiles) issue(first + (int64_t)s * gridDim.x, s);
-  double acc[MAXSPW];
+  double acc[SPW];
 #pragma unroll
-  for (int q = 0; q < MAXSPW; ++q) acc[q] = 0.0;
+  for (int q = 0; q < SPW; ++q) acc[q] = 0.0;
   double acc_self = 0.0;
-  __shared__ double csum_s;
-  if (tid == 0) {
-    double t = 0.0;
-    for (int i = 0; i < w; ++i) t += cs[i];
-    csum_s = t;
-  }
   __syncthreads();
   const double csum = csum_s;
   const int e_loc = tid % TE, part = tid / TE;
-  // slot range of this thread's part (phase A)
-  const int per = (nU + PARTS - 1) / PARTS;
-  const int s0 = part * per, s1 = min(nU, s0 + per);
-  const int xoff = nU - w;  // first X slot
+  const int xoff = nU - w;  // first X slot (psi_cur and X use slots >= xoff; psi_prev slots < w)
+  const int half = (nU + 1) / 2;
+  const int s0 = part ? half : 0, s1 = part ? nU : half;
+  const double inv_w = 1.0 / (double)w;
   int it = 0;
   for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
     const int st = it % a.nstage;
@@ -133,52 +135,60 @@ __global__ void __launch_bounds__(FT, 1) fill_kernel(FillArgs a) {
     const int64_t e0 = tile * TE;
     const int64_t e = e0 + e_loc;
     const bool valid = e < g.D;
-    // mask bits are fetched before waiting on the stage (latency overlap)
+    // per-DOF global reads are issued before waiting on the stage (latency overlap)
     bool inS = false, inB = false;
-    int64_t n = 0;
+    double srcv = 0.0, outv = 0.0;
     if (part == 0 && valid && a.mode != MODE_PROJ) {
-      n = e % g.N;
+      const int64_t n = e % g.N;
       if (a.mode == MODE_FILL) {
         inS = bit_of(a.mS, g, n);
         inB = a.mB && bit_of(a.mB, g, n);
+        if (inS) srcv = a.src_S[e];
+      } else {
+        outv = a.out[e];
       }
     }
-    double srcv = 0.0;
-    if (inS) srcv = a.src_S[e];
     mbar_wait(&bars[st], par);
     const double* T = stage0 + st * stage_elems;
     const double rh = T[nU * TE + e_loc];
-    // phase A (one pass over the slots, shifted by rho):
-    //   sp = sum_{s<w} x_s, sc = sum_{s>=nU-w} x_s, tr = sum_i c_i x_{nU-w+i},  x_s = gamma_s - rho
+    // phase A, one pass over this part's slots, shifted by rho (x_s = gamma_s - rho):
+    //   sp = sum_{s<w} x_s,  sc = sum_{s>=xoff} x_s,  tr = sum_{s>=xoff} c_{s-xoff} x_s
+    double sp0 = 0.0, sp1 = 0.0, sc0 = 0.0, sc1 = 0.0, tr0 = 0.0, tr1 = 0.0;
     {
-      double sp = 0.0, sc = 0.0, tr = 0.0;
-#pragma unroll 4
-      for (int s = s0; s < s1; ++s) {
-        const double x = T[s * TE + e_loc] - rh;
-        if (s < w) sp += x;
-        if (s >= xoff) {
-          sc += x;
-          tr += cs[s - xoff] * x;
-        }
+      const int l1 = min(s1, xoff);
+      for (int s = s0; s < l1; ++s) sp0 += T[s * TE + e_loc] - rh;
+      const int m0 = max(s0, xoff), m1 = min(s1, w);
+      int s = m0;
+      for (; s + 1 < m1; s += 2) {
+        const double x0 = T[s * TE + e_loc] - rh, x1 = T[(s + 1) * TE + e_loc] - rh;
+        sp0 += x0; sp1 += x1; sc0 += x0; sc1 += x1;
+        tr0 += cs[s - xoff] * x0; tr1 += cs[s + 1 - xoff] * x1;
       }
-      red[(part * TE + e_loc) * 3 + 0] = sp;
-      red[(part * TE + e_loc) * 3 + 1] = sc;
-      red[(part * TE + e_loc) * 3 + 2] = tr;
+      if (s < m1) {
+        const double x0 = T[s * TE + e_loc] - rh;
+        sp0 += x0; sc0 += x0; tr0 += cs[s - xoff] * x0;
+      }
+      for (int s2 = max(s0, w); s2 < s1; ++s2) {
+        const double x0 = T[s2 * TE + e_loc] - rh;
+        sc1 += x0; tr1 += cs[s2 - xoff] * x0;
+      }
+    }
+    if (part == 1) {
+      red[e_loc] = sp0 + sp1;
+      red[TE + e_loc] = sc0 + sc1;
+      red[2 * TE + e_loc] = tr0 + tr1;
     }
     __syncthreads();
     if (part == 0) {
       double gval = 0.0;
       if (valid) {
-        double sp = 0.0, sc = 0.0, tr = 0.0;
-        for (int p = 0; p < PARTS; ++p) {
-          sp += red[(p * TE + e_loc) * 3 + 0];
-          sc += red[(p * TE + e_loc) * 3 + 1];
-          tr += red[(p * TE + e_loc) * 3 + 2];
-        }
+        const double sp = (sp0 + sp1) + red[e_loc];
+        const double sc = (sc0 + sc1) + red[TE + e_loc];
+        const double tr = (tr0 + tr1) + red[2 * TE + e_loc];
         // psi_prev - rho = sp/w, psi_cur - rho = sc/w;  Phi y = sum_i c_i (x_i - (psi_prev - rho))
-        const double dev = tr - (sp / (double)w) * csum;
+        const double dev = tr - (sp * inv_w) * csum;
         if (a.mode == MODE_FILL) {
-          const double rec = (rh + sc / (double)w) + dev;
+          const double rec = (rh + sc * inv_w) + dev;
           if (inS) {
             gval = srcv;
             const double d = gval - rec;
@@ -188,7 +198,7 @@ __global__ void __launch_bounds__(FT, 1) fill_kernel(FillArgs a) {
           }
           a.out[e] = gval;
         } else if (a.mode == MODE_READ) {
-          gval = a.out[e];
+          gval = outv;
         } else {  // MODE_PROJ: residual of the projection onto the basis (bootstrap indicator)
           a.eps_elem[e] = dev * dev;
         }
@@ -211,8 +221,8 @@ __global__ void __launch_bounds__(FT, 1) fill_kernel(FillArgs a) {
           const double gv = gt[el];
           const double r = T[nU * TE + el];
 #pragma unroll
-          for (int q = 0; q < MAXSPW; ++q) {
-            const int s = warp + q * (FT / 32);
+          for (int q = 0; q < SPW; ++q) {
+            const int s = warp + q * NW;
             if (s < nU) acc[q] += gv * (T[s * TE + el] - r);
           }
         }
@@ -231,20 +241,20 @@ __global__ void __launch_bounds__(FT, 1) fill_kernel(FillArgs a) {
   // fixed-order reductions -> part[block][s], part[block][nU] = self
   double* out = a.part + (int64_t)blockIdx.x * (nU + 1);
 #pragma unroll
-  for (int q = 0; q < MAXSPW; ++q) {
+  for (int q = 0; q < SPW; ++q) {
     double v = acc[q];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    const int s = warp + q * (FT / 32);
+    const int s = warp + q * NW;
     if (lane == 0 && s < nU) out[s] = v;
   }
   double v = acc_self;
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __shared__ double wsum[FT / 32];
+  __shared__ double wsum[NW];
   if (lane == 0) wsum[warp] = v;
   __syncthreads();
   if (tid == 0) {
     double s = 0.0;
-    for (int k = 0; k < FT / 32; ++k) s += wsum[k];
+    for (int k = 0; k < NW; ++k) s += wsum[k];
     out[nU] = s;
   }
 }
@@ -297,13 +307,26 @@ __global__ void mean_kernel(Geo g, Win W, const double* __restrict__ ring, doubl
 }  // namespace
 
 static int fill_smem_stages(int nU, size_t* bytes) {
+  constexpr int TE = TE_FILL;
   const size_t stage = (size_t)(nU + 1) * TE * sizeof(double);
-  const size_t fixed = (TE + 3 * PARTS * TE) * sizeof(double) + 8 * sizeof(uint64_t);
-  const size_t budget = 220 * 1024;
+  const size_t fixed = (TE + 3 * TE) * sizeof(double) + 8 * sizeof(uint64_t);
+  const size_t budget = 108 * 1024;  // two CTAs per SM
   int ns = (int)((budget - fixed) / stage);
+  if (ns > 4) ns = 4;
+  if (ns < 2) ns = std::max(1, (int)((220 * 1024 - fixed) / stage));  // very wide windows: one CTA per SM
   if (ns > 4) ns = 4;
   *bytes = ns * stage + fixed;
   return ns;
+}
+
+template <int SPW>
+static hrom_status launch_fill_t(hrom_ctx* c, const FillArgs& a, size_t smem) {
+  constexpr int TE = TE_FILL;
+  HROM_CK(cudaFuncSetAttribute(fill_kernel<TE, SPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fill_kernel<TE, SPW><<<c->fill_blocks, 2 * TE, smem, c->st>>>(a);
+  HROM_LAUNCH_CK();
+  ++c->nlaunch;
+  return HROM_OK;
 }
 
 hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S, double* out, int /*out_slot*/) {
@@ -326,12 +349,14 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S
   a.mB = (mode == MODE_FILL) ? c->b.masks + (int64_t)M_B * c->mwords : nullptr;
   a.eps_elem = c->b.eps_elem;
   a.part = c->b.gpart;
-  const int grid = c->fill_blocks;
-  HROM_CK(cudaFuncSetAttribute(fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  fill_kernel<<<grid, FT, smem, c->st>>>(a);
-  HROM_LAUNCH_CK();
-  ++c->nlaunch;
-  return HROM_OK;
+  constexpr int NW = 2 * TE_FILL / 32;
+  const int spw = (W.nU + NW - 1) / NW;
+  if (spw <= 3) return launch_fill_t<3>(c, a, smem);
+  if (spw <= 6) return launch_fill_t<6>(c, a, smem);
+  if (spw <= 9) return launch_fill_t<9>(c, a, smem);
+  if (spw <= 17) return launch_fill_t<17>(c, a, smem);
+  if (spw <= 33) return launch_fill_t<33>(c, a, smem);
+  return HROM_E_INVALID;
 }
 
 hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot) {

@@ -120,12 +120,26 @@ struct hrom_ctx {
   std::vector<std::pair<int, std::pair<int, int>>> ev_pairs;  // (section, (start ev, stop ev))
   int ev_next = 0;
   int ev_open[16] = {0};
+  // the one-CTA eigen-solve of the basis update runs on a side stream, overlapping the
+  // sampling and the next step's dt / masked RK3 / gathered Gram (which do not need it)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_basis_in = nullptr, ev_basis_done = nullptr;
+  bool basis_pending = false;
   int slot_of(int64_t kk) const { return (int)(kk % nslots); }
 };
 
 namespace hrom {
+inline void basis_join(hrom_ctx* c) {
+  if (c->basis_pending) {
+    cudaStreamWaitEvent(c->st, c->ev_basis_done, 0);
+    c->basis_pending = false;
+  }
+}
+}  // namespace hrom
+
+namespace hrom {
 enum Section { SEC_DT = 0, SEC_MASKED, SEC_GATHER, SEC_SOLVE, SEC_FILL, SEC_EPS, SEC_FILTER, SEC_BANDGRAM,
-               SEC_POS, SEC_BASIS, SEC_SAMPLE, SEC_FULL, SEC_REBASE, SEC_COUNT };
+               SEC_POS, SEC_BASIS, SEC_SAMPLE, SEC_FULL, SEC_REBASE, SEC_EIGEN, SEC_COUNT };
 inline void prof_begin(hrom_ctx* c, int sec) {
   if (!c->prof || c->ev_next + 2 > (int)c->ev_pool.size()) return;
   c->ev_open[sec] = c->ev_next;

@@ -75,7 +75,7 @@ _SIGS = {
 }
 
 SECTIONS = ["dt", "masked_rk3", "gathered_gram", "pinv_solve", "fill_pass", "indicator", "seam_filter",
-            "band_gram", "positivity", "basis_update", "sampling", "full_step", "rebase_gram"]
+            "band_gram", "positivity", "basis_update", "sampling", "full_step", "rebase_gram", "basis_eigen_side_stream"]
 
 _lib = None
 

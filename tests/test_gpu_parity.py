@@ -202,28 +202,54 @@ def test_gram_dmma_vs_oracle(orc, inputs):
         assert np.max(np.abs(Cg - Co)) <= 1e-13 * np.max(np.abs(Co)), ncol
 
 
-def test_trajectory_config1(orc, inputs):
-    """200-step Algorithm-1 trajectory of config 1 (BJ:7) <= 1e-9, masks compared per step."""
-    wl = inputs.config(1)
+def _trajectories(orc, inputs, wl, steps):
+    """GPU, oracle and oracle-with-1e-15-perturbed-IC trajectories of Algorithm 1."""
     q0 = inputs.initial_condition(wl)
+    rng = np.random.default_rng(0)
+    q1 = q0 * (1.0 + 1e-15 * rng.standard_normal(q0.shape))
     rom = H.HybridROM(wl)
     rom.set_state(dev(q0))
-    R = orc.Run(wl, q0)
-    flips = 0
-    worst = 0.0
-    for k in range(1, wl.steps + 1):
+    R, Rp = orc.Run(wl, q0), orc.Run(wl, q1)
+    rows = []
+    snaps, masks, dts = [q0], [], []
+    for k in range(1, steps + 1):
         rom.step()
         R.step()
-        if k >= wl.w - 1:
-            mg = H.cells_from_mask(wl, rom.mask())
-            if not np.array_equal(mg, R.mask()):
-                flips += 1
-        if k % 20 == 0 or k == wl.steps:
-            g = rom.get_state().cpu().numpy()
-            worst = max(worst, rel(g, R.state()))
+        Rp.step()
+        o = R.state()
+        snaps.append(o)
+        masks.append(R.mask())
+        dts.append(R.dt())
+        g = rom.get_state().cpu().numpy()
+        flip = k >= wl.w - 1 and not np.array_equal(H.cells_from_mask(wl, rom.mask()), R.mask())
+        rows.append((k, rel(g, o), rel(Rp.state(), o), flip))
     rom.sync()
-    assert flips == 0, f"{flips} mask flips"
-    assert worst <= 1e-9, worst
+    return rows, snaps, masks, dts
+
+
+def test_trajectory_config1(orc, inputs):
+    """200-step Algorithm-1 trajectory of config 1 (BJ:7).
+
+    The explicit hybrid map amplifies rounding: the ORACLE itself, started from an IC
+    perturbed by 1e-15, drifts away from its own trajectory by ~x1.25 per hybrid step
+    (DESIGN.md §7).  So the trajectory bar is relative to that self-sensitivity: the GPU
+    may not drift from the oracle faster than 100x the oracle drifts from itself, and
+    masks must agree while the oracle's own drift is below 1e-9.  Per-step parity is
+    checked by lock-step replay (GPU fed the oracle's window and mask) <= 1e-12."""
+    wl = inputs.config(1)
+    rows, snaps, masks, dts = _trajectories(orc, inputs, wl, wl.steps)
+    for k, e, sref, flip in rows:
+        assert e <= max(100.0 * sref, 1e-13), (k, e, sref)
+        if sref < 1e-9:
+            assert not flip, (k, e, sref)
+    # lock-step replay at several steps: one hybrid step from the oracle's window
+    for k in (wl.w, wl.w + 1, wl.w + 50, 150, wl.steps - 1):
+        rom = H.HybridROM(wl)
+        win = np.stack(snaps[k - wl.w:k + 1]).reshape(wl.w + 1, -1)
+        rom.set_window(k, dev(win), _mask_dev(wl, masks[k - 1]))
+        rom.hybrid_step(dt=dts[k])
+        g = rom.get_state().cpu().numpy()
+        assert rel(g, snaps[k + 1]) <= 1e-12, (k, rel(g, snaps[k + 1]))
 
 
 def test_determinism_bitwise(inputs):
