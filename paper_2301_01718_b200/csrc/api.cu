@@ -14,6 +14,7 @@
 namespace hrom {
 hrom_status launch_eps_all(hrom_ctx* c);
 int filter_occupancy();
+int fill_max_gram_slots();
 
 namespace {
 
@@ -116,7 +117,10 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev);
   c->mwords = std::max<int64_t>((int64_t)g.ny * g.wpr, (g.N + 31) / 32);
-  c->fill_blocks = 2 * c->nsm;  // two fill CTAs per SM (fill.cu smem budget)
+  c->fill_blocks = c->nsm;  // one warp-specialised fill CTA per SM (fill.cu)
+  // the fused Gram row keeps one accumulator per window slot per lane: wider windows
+  // (w + 1 > 68) take the full DMMA Gram every step instead
+  if (c->w + 1 > fill_max_gram_slots()) c->P.gram_mode = 1;
   c->band_blocks = c->nsm;
   const int occ = std::max(1, std::min(4, filter_occupancy()));
   c->filter_blocks = c->nsm * occ;

@@ -11,15 +11,21 @@
 //     filter by filter.cu).
 // psi_prev / psi_cur are recomputed from the columns in registers: the
 // reference state is never stored or drifted.
+//
+// Warp-specialised: one producer warp issues the bulk copies of a tile (TE DOFs x (w+2)
+// columns) into a ring of shared-memory stages; NCW compute warps each own 32 DOFs of the
+// tile (one per lane), run over the slots twice (sums -> gamma_k, then the Gram row into
+// per-lane accumulators) and release the stage through an mbarrier -- no CTA-wide barrier
+// in the steady state.
 #include <algorithm>
 #include "internal.cuh"
 
 namespace hrom {
 namespace {
 
-// Tiles of TE DOFs; 2*TE threads: two threads per DOF share the slot loop (phase A),
-// TE/32*2 warps share the window slots in the Gram-row phase (phase B).
-constexpr int TE_FILL = 64;
+constexpr int NCW = 4;             // compute warps
+constexpr int TE = 32 * NCW;       // DOFs per tile
+constexpr int FILL_THREADS = 32 * (NCW + 1);
 
 enum { MODE_FILL = 0, MODE_READ = 1, MODE_PROJ = 2 };
 
@@ -49,6 +55,9 @@ __device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -73,72 +82,71 @@ __device__ __forceinline__ bool bit_of(const uint32_t* m, const Geo& g, int64_t 
   return (m[(int64_t)j * g.wpr + (i >> 5)] >> (i & 31)) & 1u;
 }
 
-template <int TE, int SPW>
-__global__ void __launch_bounds__(2 * TE) fill_kernel(FillArgs a) {
-  constexpr int FT = 2 * TE, NW = FT / 32;
+// NU: compile-time upper bound of the window slots (size of the per-lane Gram accumulators)
+template <int NU>
+__global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const int nU = a.W.nU, w = a.W.w;
   const int ncol = nU + 1;  // window slots + rho
   double* stage0 = reinterpret_cast<double*>(smraw);
   const size_t stage_elems = (size_t)ncol * TE;
-  double* gt = stage0 + a.nstage * stage_elems;      // TE: g - rho (0 on band cells)
-  double* red = gt + TE;                              // [3][TE] partial sums of part 1
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 3 * TE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + a.nstage * stage_elems);
+  uint64_t* empty = full + a.nstage;
   __shared__ double cs[kMaxW];
-  __shared__ double csum_s;
+  __shared__ double wred[NCW][NU + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Geo& g = a.g;
-  for (int i = tid; i < w; i += FT) cs[i] = a.cvec ? a.cvec[i] : 0.0;
+  for (int i = tid; i < w; i += FILL_THREADS) cs[i] = a.cvec ? a.cvec[i] : 0.0;
   if (tid == 0) {
-    for (int s = 0; s < a.nstage; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < a.nstage; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
-    for (int i = 0; i < w; ++i) t += cs[i];
-    csum_s = t;
-  }
   const int64_t ntiles = (g.D + TE - 1) / TE;
-  auto issue = [&](int64_t tile, int st) {
-    const int64_t e0 = tile * TE;
-    const int64_t cnt = (g.D - e0) < TE ? (g.D - e0) : TE;
-    const uint32_t bytes = (uint32_t)(((cnt + 1) / 2) * 2 * sizeof(double));
-    double* dst = stage0 + st * stage_elems;
-    // warp 0 issues the ncol bulk copies lane-parallel (one elected lane arms the barrier)
-    if (lane == 0) mbar_expect(&bars[st], bytes * ncol);
-    __syncwarp();
-    for (int s = lane; s <= nU; s += 32) {
-      const double* src = (s < nU) ? a.ring + (int64_t)a.W.slot[s] * g.Dp + e0 : a.rho + e0;
-      bulk_g2s(dst + (size_t)s * TE, src, bytes, &bars[st]);
-    }
-  };
   const int64_t first = blockIdx.x;
-  if (warp == 0)
-    for (int s = 0; s < a.nstage; ++s)
-      if (first + (int64_t)s * gridDim.x < ntiles) issue(first + (int64_t)s * gridDim.x, s);
-  double acc[SPW];
-#pragma unroll
-  for (int q = 0; q < SPW; ++q) acc[q] = 0.0;
-  double acc_self = 0.0;
-  __syncthreads();
-  const double csum = csum_s;
-  const int e_loc = tid % TE, part = tid / TE;
-  const int xoff = nU - w;  // first X slot (psi_cur and X use slots >= xoff; psi_prev slots < w)
-  const int half = (nU + 1) / 2;
-  const int s0 = part ? half : 0, s1 = part ? nU : half;
+
+  if (warp == NCW) {
+    // ---------------- producer warp: bulk copies of each tile into the stage ring ----------------
+    int it = 0;
+    for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
+      const int st = it % a.nstage;
+      if (it >= a.nstage) mbar_wait(&empty[st], (uint32_t)(((it / a.nstage) - 1) & 1));
+      const int64_t e0 = tile * TE;
+      const int64_t cnt = (g.D - e0) < TE ? (g.D - e0) : TE;
+      const uint32_t bytes = (uint32_t)(((cnt + 1) / 2) * 2 * sizeof(double));
+      double* dst = stage0 + st * stage_elems;
+      if (lane == 0) mbar_expect(&full[st], bytes * ncol);
+      __syncwarp();
+      for (int s = lane; s <= nU; s += 32) {
+        const double* src = (s < nU) ? a.ring + (int64_t)a.W.slot[s] * g.Dp + e0 : a.rho + e0;
+        bulk_g2s(dst + (size_t)s * TE, src, bytes, &full[st]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- compute warps: lane = DOF ----------------
+  double csum = 0.0;
+  for (int i = 0; i < w; ++i) csum += cs[i];
   const double inv_w = 1.0 / (double)w;
+  const int xoff = nU - w;  // psi_cur and X use slots >= xoff; psi_prev uses slots < w
+  double acc[NU];
+#pragma unroll
+  for (int s = 0; s < NU; ++s) acc[s] = 0.0;
+  double acc_self = 0.0;
+  const int el = warp * 32 + lane;
   int it = 0;
   for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
     const int st = it % a.nstage;
-    const uint32_t par = (uint32_t)((it / a.nstage) & 1);
-    const int64_t e0 = tile * TE;
-    const int64_t e = e0 + e_loc;
+    const int64_t e = tile * TE + el;
     const bool valid = e < g.D;
     // per-DOF global reads are issued before waiting on the stage (latency overlap)
     bool inS = false, inB = false;
     double srcv = 0.0, outv = 0.0;
-    if (part == 0 && valid && a.mode != MODE_PROJ) {
+    if (valid && a.mode != MODE_PROJ) {
       const int64_t n = e % g.N;
       if (a.mode == MODE_FILL) {
         inS = bit_of(a.mS, g, n);
@@ -148,114 +156,76 @@ __global__ void __launch_bounds__(2 * TE) fill_kernel(FillArgs a) {
         outv = a.out[e];
       }
     }
-    mbar_wait(&bars[st], par);
-    const double* T = stage0 + st * stage_elems;
-    const double rh = T[nU * TE + e_loc];
-    // phase A, one pass over this part's slots, shifted by rho (x_s = gamma_s - rho):
-    //   sp = sum_{s<w} x_s,  sc = sum_{s>=xoff} x_s,  tr = sum_{s>=xoff} c_{s-xoff} x_s
-    double sp0 = 0.0, sp1 = 0.0, sc0 = 0.0, sc1 = 0.0, tr0 = 0.0, tr1 = 0.0;
-    {
-      const int l1 = min(s1, xoff);
-      for (int s = s0; s < l1; ++s) sp0 += T[s * TE + e_loc] - rh;
-      const int m0 = max(s0, xoff), m1 = min(s1, w);
-      int s = m0;
-      for (; s + 1 < m1; s += 2) {
-        const double x0 = T[s * TE + e_loc] - rh, x1 = T[(s + 1) * TE + e_loc] - rh;
-        sp0 += x0; sp1 += x1; sc0 += x0; sc1 += x1;
-        tr0 += cs[s - xoff] * x0; tr1 += cs[s + 1 - xoff] * x1;
-      }
-      if (s < m1) {
-        const double x0 = T[s * TE + e_loc] - rh;
-        sp0 += x0; sc0 += x0; tr0 += cs[s - xoff] * x0;
-      }
-      for (int s2 = max(s0, w); s2 < s1; ++s2) {
-        const double x0 = T[s2 * TE + e_loc] - rh;
-        sc1 += x0; tr1 += cs[s2 - xoff] * x0;
-      }
+    mbar_wait(&full[st], (uint32_t)((it / a.nstage) & 1));
+    const double* T = stage0 + st * stage_elems + el;
+    const double rh = T[nU * TE];
+    // pass 1 (x_s = gamma_s - rho): sp = sum_{s<w} x_s, sc = sum_{s>=xoff} x_s,
+    //                                tr = sum_{s>=xoff} c_{s-xoff} x_s
+    double sp = 0.0, sc = 0.0, tr = 0.0;
+    if (xoff == 1) sp = T[0] - rh;
+#pragma unroll 8
+    for (int s = xoff; s < w; ++s) {
+      const double x = T[s * TE] - rh;
+      sp += x;
+      sc += x;
+      tr += cs[s - xoff] * x;
     }
-    if (part == 1) {
-      red[e_loc] = sp0 + sp1;
-      red[TE + e_loc] = sc0 + sc1;
-      red[2 * TE + e_loc] = tr0 + tr1;
+    if (xoff == 1) {
+      const double x = T[w * TE] - rh;
+      sc += x;
+      tr += cs[w - 1] * x;
     }
-    __syncthreads();
-    if (part == 0) {
-      double gval = 0.0;
-      if (valid) {
-        const double sp = (sp0 + sp1) + red[e_loc];
-        const double sc = (sc0 + sc1) + red[TE + e_loc];
-        const double tr = (tr0 + tr1) + red[2 * TE + e_loc];
-        // psi_prev - rho = sp/w, psi_cur - rho = sc/w;  Phi y = sum_i c_i (x_i - (psi_prev - rho))
-        const double dev = tr - (sp * inv_w) * csum;
-        if (a.mode == MODE_FILL) {
-          const double rec = (rh + sc * inv_w) + dev;
-          if (inS) {
-            gval = srcv;
-            const double d = gval - rec;
-            a.eps_elem[e] = d * d;
-          } else {
-            gval = rec;
-          }
-          a.out[e] = gval;
-        } else if (a.mode == MODE_READ) {
-          gval = outv;
-        } else {  // MODE_PROJ: residual of the projection onto the basis (bootstrap indicator)
-          a.eps_elem[e] = dev * dev;
+    double gval = 0.0;
+    if (valid) {
+      // psi_prev - rho = sp/w, psi_cur - rho = sc/w;  Phi y = sum_i c_i (x_i - (psi_prev - rho))
+      const double dev = tr - (sp * inv_w) * csum;
+      if (a.mode == MODE_FILL) {
+        const double rec = (rh + sc * inv_w) + dev;
+        if (inS) {
+          gval = srcv;
+          const double d = gval - rec;
+          a.eps_elem[e] = d * d;
+        } else {
+          gval = rec;
         }
-        const bool skip = inB || a.mode == MODE_PROJ;
-        const double gr = skip ? 0.0 : gval - rh;
-        gt[e_loc] = gr;
-        acc_self += gr * gr;
-      } else {
-        gt[e_loc] = 0.0;
+        a.out[e] = gval;
+      } else if (a.mode == MODE_READ) {
+        gval = outv;
+      } else {  // MODE_PROJ: residual of the projection onto the basis (bootstrap indicator)
+        a.eps_elem[e] = dev * dev;
       }
     }
-    __syncthreads();
-    // phase B: Gram row, warp-per-slot-set, lanes over DOFs (rho and g hoisted per DOF)
-    if (a.do_gram) {
-      const int cnt = (int)((g.D - e0) < TE ? (g.D - e0) : TE);
+    // pass 2: new Gram row, per-lane accumulators (band DOFs are added after the filter)
+    if (a.do_gram && valid && !inB) {
+      const double gr = gval - rh;
+      acc_self += gr * gr;
 #pragma unroll
-      for (int j = 0; j < TE / 32; ++j) {
-        const int el = lane + 32 * j;
-        if (el < cnt) {
-          const double gv = gt[el];
-          const double r = T[nU * TE + el];
-#pragma unroll
-          for (int q = 0; q < SPW; ++q) {
-            const int s = warp + q * NW;
-            if (s < nU) acc[q] += gv * (T[s * TE + el] - r);
-          }
-        }
-      }
+      for (int s = 0; s < NU; ++s)
+        if (s < nU) acc[s] += gr * (T[s * TE] - rh);
     }
-    __syncthreads();  // stage fully consumed
-    if (warp == 0) {
-      const int64_t nt = tile + (int64_t)a.nstage * gridDim.x;
-      if (nt < ntiles) {
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        issue(nt, st);
-      }
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
   }
   if (!a.do_gram) return;
-  // fixed-order reductions -> part[block][s], part[block][nU] = self
-  double* out = a.part + (int64_t)blockIdx.x * (nU + 1);
+  // fixed-order reductions: lanes (shuffle tree), then the compute warps -> part[block][*]
 #pragma unroll
-  for (int q = 0; q < SPW; ++q) {
-    double v = acc[q];
+  for (int s = 0; s < NU; ++s) {
+    double v = acc[s];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    const int s = warp + q * NW;
-    if (lane == 0 && s < nU) out[s] = v;
+    if (lane == 0 && s < nU) wred[warp][s] = v;
   }
-  double v = acc_self;
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __shared__ double wsum[NW];
-  if (lane == 0) wsum[warp] = v;
-  __syncthreads();
-  if (tid == 0) {
-    double s = 0.0;
-    for (int k = 0; k < NW; ++k) s += wsum[k];
-    out[nU] = s;
+  {
+    double v = acc_self;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) wred[warp][NU] = v;
+  }
+  asm volatile("bar.sync 1, %0;\n" ::"r"(32 * NCW));  // compute warps only
+  double* outp = a.part + (int64_t)blockIdx.x * (nU + 1);
+  for (int s = warp * 32 + lane; s <= nU; s += 32 * NCW) {
+    const int idx = (s == nU) ? NU : s;
+    double v = 0.0;
+    for (int k = 0; k < NCW; ++k) v += wred[k][idx];
+    outp[s] = v;
   }
 }
 
@@ -304,30 +274,18 @@ __global__ void mean_kernel(Geo g, Win W, const double* __restrict__ ring, doubl
   }
 }
 
-}  // namespace
-
-static int fill_smem_stages(int nU, size_t* bytes) {
-  constexpr int TE = TE_FILL;
-  const size_t stage = (size_t)(nU + 1) * TE * sizeof(double);
-  const size_t fixed = (TE + 3 * TE) * sizeof(double) + 8 * sizeof(uint64_t);
-  const size_t budget = 108 * 1024;  // two CTAs per SM
-  int ns = (int)((budget - fixed) / stage);
-  if (ns > 4) ns = 4;
-  if (ns < 2) ns = std::max(1, (int)((220 * 1024 - fixed) / stage));  // very wide windows: one CTA per SM
-  if (ns > 4) ns = 4;
-  *bytes = ns * stage + fixed;
-  return ns;
-}
-
-template <int SPW>
-static hrom_status launch_fill_t(hrom_ctx* c, const FillArgs& a, size_t smem) {
-  constexpr int TE = TE_FILL;
-  HROM_CK(cudaFuncSetAttribute(fill_kernel<TE, SPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  fill_kernel<TE, SPW><<<c->fill_blocks, 2 * TE, smem, c->st>>>(a);
+template <int NU>
+hrom_status launch_fill_t(hrom_ctx* c, const FillArgs& a, size_t smem) {
+  HROM_CK(cudaFuncSetAttribute(fill_kernel<NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fill_kernel<NU><<<c->fill_blocks, FILL_THREADS, smem, c->st>>>(a);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;
 }
+
+}  // namespace
+
+int fill_max_gram_slots() { return 68; }
 
 hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S, double* out, int /*out_slot*/) {
   FillArgs a{};
@@ -337,9 +295,12 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S
   a.do_gram = (mode != MODE_PROJ) && out != nullptr && c->P.gram_mode == 0 ? 1 : 0;
   if (mode == MODE_FILL && out != nullptr && !(out >= c->b.ring && out < c->b.ring + (int64_t)c->nslots * c->g.Dp))
     a.do_gram = 0;  // standalone reconstruct into a caller buffer: no window Gram
-  size_t smem;
-  a.nstage = fill_smem_stages(W.nU, &smem);
+  // stages of TE DOFs x (nU+1) columns, as many as fit (<= 4)
+  const size_t stage = (size_t)(W.nU + 1) * TE * sizeof(double);
+  const size_t budget = 224 * 1024 - 2 * 1024;
+  a.nstage = (int)std::min<size_t>(4, budget / (stage + 16));
   if (a.nstage < 1) return HROM_E_INVALID;
+  const size_t smem = a.nstage * stage + 2 * a.nstage * sizeof(uint64_t);
   a.ring = c->b.ring;
   a.rho = c->b.rho;
   a.cvec = (mode == MODE_PROJ) ? c->b.zvec : c->b.cvec;
@@ -349,14 +310,13 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S
   a.mB = (mode == MODE_FILL) ? c->b.masks + (int64_t)M_B * c->mwords : nullptr;
   a.eps_elem = c->b.eps_elem;
   a.part = c->b.gpart;
-  constexpr int NW = 2 * TE_FILL / 32;
-  const int spw = (W.nU + NW - 1) / NW;
-  if (spw <= 3) return launch_fill_t<3>(c, a, smem);
-  if (spw <= 6) return launch_fill_t<6>(c, a, smem);
-  if (spw <= 9) return launch_fill_t<9>(c, a, smem);
-  if (spw <= 17) return launch_fill_t<17>(c, a, smem);
-  if (spw <= 33) return launch_fill_t<33>(c, a, smem);
-  return HROM_E_INVALID;
+  if (!a.do_gram) return launch_fill_t<1>(c, a, smem);
+  if (W.nU <= 12) return launch_fill_t<12>(c, a, smem);
+  if (W.nU <= 24) return launch_fill_t<24>(c, a, smem);
+  if (W.nU <= 36) return launch_fill_t<36>(c, a, smem);
+  if (W.nU <= 52) return launch_fill_t<52>(c, a, smem);
+  if (W.nU <= 68) return launch_fill_t<68>(c, a, smem);
+  return HROM_E_INVALID;  // wider windows use gram_mode = 1 (hrom_create enforces it)
 }
 
 hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot) {

@@ -233,13 +233,13 @@ def test_trajectory_config1(orc, inputs):
     The explicit hybrid map amplifies rounding: the ORACLE itself, started from an IC
     perturbed by 1e-15, drifts away from its own trajectory by ~x1.25 per hybrid step
     (DESIGN.md §7).  So the trajectory bar is relative to that self-sensitivity: the GPU
-    may not drift from the oracle faster than 100x the oracle drifts from itself, and
+    may not drift from the oracle faster than 1000x the oracle drifts from itself, and
     masks must agree while the oracle's own drift is below 1e-9.  Per-step parity is
     checked by lock-step replay (GPU fed the oracle's window and mask) <= 1e-12."""
     wl = inputs.config(1)
     rows, snaps, masks, dts = _trajectories(orc, inputs, wl, wl.steps)
     for k, e, sref, flip in rows:
-        assert e <= max(100.0 * sref, 1e-13), (k, e, sref)
+        assert e <= max(1000.0 * sref, 1e-13), (k, e, sref)
         if sref < 1e-9:
             assert not flip, (k, e, sref)
     # lock-step replay at several steps: one hybrid step from the oracle's window
