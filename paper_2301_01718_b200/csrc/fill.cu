@@ -138,33 +138,57 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   for (int s = 0; s < NU; ++s) acc[s] = 0.0;
   double acc_self = 0.0;
   const int el = warp * 32 + lane;
+  // per-DOF global reads (mask words, HDM value / new column) are software-pipelined one
+  // tile ahead so their latency overlaps the previous tile's arithmetic
+  uint32_t wS = 0, wB = 0;
+  int bitpos = 0;
+  double pre = 0.0;
+  auto fetch = [&](int64_t tile) {
+    const int64_t e = tile * TE + el;
+    wS = wB = 0;
+    pre = 0.0;
+    if (tile < ntiles && e < g.D && a.mode != MODE_PROJ) {
+      const int64_t n = e % g.N;
+      const int i = (int)(n % g.nx), j = (int)(n / g.nx);
+      const int64_t wi = (int64_t)j * g.wpr + (i >> 5);
+      bitpos = i & 31;
+      if (a.mode == MODE_FILL) {
+        wS = a.mS[wi];
+        if (a.mB) wB = a.mB[wi];
+        pre = a.src_S[e];  // read unconditionally (U3 is allocated everywhere); used on S-hat only
+      } else {
+        pre = a.out[e];
+      }
+    }
+  };
+  fetch(first);
   int it = 0;
   for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
     const int st = it % a.nstage;
     const int64_t e = tile * TE + el;
     const bool valid = e < g.D;
-    // per-DOF global reads are issued before waiting on the stage (latency overlap)
-    bool inS = false, inB = false;
-    double srcv = 0.0, outv = 0.0;
-    if (valid && a.mode != MODE_PROJ) {
-      const int64_t n = e % g.N;
-      if (a.mode == MODE_FILL) {
-        inS = bit_of(a.mS, g, n);
-        inB = a.mB && bit_of(a.mB, g, n);
-        if (inS) srcv = a.src_S[e];
-      } else {
-        outv = a.out[e];
-      }
-    }
+    const bool inS = (wS >> bitpos) & 1u, inB = (wB >> bitpos) & 1u;
+    const double srcv = pre, outv = pre;
+    fetch(tile + gridDim.x);
     mbar_wait(&full[st], (uint32_t)((it / a.nstage) & 1));
     const double* T = stage0 + st * stage_elems + el;
     const double rh = T[nU * TE];
     // pass 1 (x_s = gamma_s - rho): sp = sum_{s<w} x_s, sc = sum_{s>=xoff} x_s,
-    //                                tr = sum_{s>=xoff} c_{s-xoff} x_s
-    double sp = 0.0, sc = 0.0, tr = 0.0;
+    //                                tr = sum_{s>=xoff} c_{s-xoff} x_s  (two partial chains each)
+    double sp = 0.0, sc = 0.0, tr = 0.0, sp2 = 0.0, sc2 = 0.0, tr2 = 0.0;
     if (xoff == 1) sp = T[0] - rh;
-#pragma unroll 8
-    for (int s = xoff; s < w; ++s) {
+    int s = xoff;
+#pragma unroll 4
+    for (; s + 1 < w; s += 2) {
+      const double x = T[s * TE] - rh, x2 = T[(s + 1) * TE] - rh;
+      sp += x;
+      sc += x;
+      tr += cs[s - xoff] * x;
+      sp2 += x2;
+      sc2 += x2;
+      tr2 += cs[s + 1 - xoff] * x2;
+    }
+    if (s < w) {
       const double x = T[s * TE] - rh;
       sp += x;
       sc += x;
@@ -172,9 +196,12 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     }
     if (xoff == 1) {
       const double x = T[w * TE] - rh;
-      sc += x;
-      tr += cs[w - 1] * x;
+      sc2 += x;
+      tr2 += cs[w - 1] * x;
     }
+    sp += sp2;
+    sc += sc2;
+    tr += tr2;
     double gval = 0.0;
     if (valid) {
       // psi_prev - rho = sp/w, psi_cur - rho = sc/w;  Phi y = sum_i c_i (x_i - (psi_prev - rho))

@@ -103,17 +103,42 @@ __global__ void __launch_bounds__(GT) gram_kernel(GramArgs a) {
       const int nU = a.W.nU, w = a.W.w;
       const int xoff = nU - w;
       double* psi = smem + (size_t)ncp * LDT;  // [2][RT]
-      for (int idx = threadIdx.x; idx < (nU + 1) * RT; idx += GT) {
-        const int s = idx / RT, k = idx % RT;
-        const int64_t row = r0 + k;
-        double v = 0.0;
+      __shared__ int64_t erow[RT];             // DOF of each tile row (-1 past the end)
+      if (threadIdx.x < RT) {
+        const int64_t row = r0 + threadIdx.x;
+        int64_t e = -1;
         if (row < total_rows) {
           const int var = (int)(row / nS), ii = (int)(row % nS);
-          const int64_t e = (int64_t)var * a.g.N + a.list[ii];
-          v = (s < nU) ? a.ring[(int64_t)a.W.slot[s] * a.g.Dp + e] : a.src_b[e];
+          e = (int64_t)var * a.g.N + a.list[ii];
         }
-        const int col = (s == nU) ? w : (s >= xoff ? s - xoff : w + 1);
-        tile[col * LDT + k] = v;
+        erow[threadIdx.x] = e;
+      }
+      __syncthreads();
+      // all loads of this thread in flight before the first shared store (memory-level parallelism)
+      constexpr int QB = 17;  // loads in flight per thread per batch
+      const int total = (nU + 1) * RT;
+      for (int base = threadIdx.x; base < total; base += QB * GT) {
+        double vbuf[QB];
+#pragma unroll
+        for (int q = 0; q < QB; ++q) {
+          const int idx = base + q * GT;
+          double v = 0.0;
+          if (idx < total) {
+            const int s = idx / RT, k = idx % RT;
+            const int64_t e = erow[k];
+            if (e >= 0) v = (s < nU) ? __ldg(a.ring + (int64_t)a.W.slot[s] * a.g.Dp + e) : __ldg(a.src_b + e);
+          }
+          vbuf[q] = v;
+        }
+#pragma unroll
+        for (int q = 0; q < QB; ++q) {
+          const int idx = base + q * GT;
+          if (idx < total) {
+            const int s = idx / RT, k = idx % RT;
+            const int col = (s == nU) ? w : (s >= xoff ? s - xoff : w + 1);
+            tile[col * LDT + k] = vbuf[q];
+          }
+        }
       }
       __syncthreads();
       if (threadIdx.x < RT) {
