@@ -117,7 +117,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev);
   c->mwords = std::max<int64_t>((int64_t)g.ny * g.wpr, (g.N + 31) / 32);
-  c->fill_blocks = c->nsm;  // one warp-specialised fill CTA per SM (fill.cu)
+  c->fill_blocks = 8 * c->nsm;  // upper bound of the fill grid (fill.cu sizes it by occupancy)
   // the fused Gram row keeps one accumulator per window slot per lane: wider windows
   // (w + 1 > 68) take the full DMMA Gram every step instead
   if (c->w + 1 > fill_max_gram_slots()) c->P.gram_mode = 1;

@@ -1,7 +1,7 @@
 // fill.cu -- H6 + H9 + incremental H10: ONE pass over the snapshot window per hybrid step.
 //
 // For every DOF e the kernel streams the w+1 window columns gamma_{k-w-1..k-1} and the Gram
-// shift rho through shared memory (cp.async.bulk / TMA 1-D bulk copies, mbarrier pipeline) and
+// shift rho once from HBM and
 //   * fills gamma_k[e] = psi_k + Phi_k y_k = psi_cur + sum_i c_i (gamma_{x_i} - psi_prev)
 //     (Alg. 1 line P:570; Phi_k = X^{(k-1)} A kept implicit), or takes the
 //     partial-HDM value on S-hat (Eq. 6b),
@@ -12,20 +12,19 @@
 // psi_prev / psi_cur are recomputed from the columns in registers: the
 // reference state is never stored or drifted.
 //
-// Warp-specialised: one producer warp issues the bulk copies of a tile (TE DOFs x (w+2)
-// columns) into a ring of shared-memory stages; NCW compute warps each own 32 DOFs of the
-// tile (one per lane), run over the slots twice (sums -> gamma_k, then the Gram row into
-// per-lane accumulators) and release the stage through an mbarrier -- no CTA-wide barrier
-// in the steady state.
+// Register streaming: a DOF is owned by a lane pair (lane l and l+16); each lane loads its
+// half of the window column values with coalesced 128-byte warp segments, all loads of a
+// DOF in flight at once, keeps them in registers for the second use (Gram row) and keeps
+// one Gram accumulator per slot.  No shared-memory staging, no CTA barrier in the stream.
 #include <algorithm>
+#include <cstdlib>
 #include "internal.cuh"
 
 namespace hrom {
 namespace {
 
-constexpr int NCW = 4;             // compute warps
-constexpr int TE = 32 * NCW;       // DOFs per tile
-constexpr int FILL_THREADS = 32 * (NCW + 1);
+constexpr int FILL_THREADS = 128;
+constexpr int FILL_WARPS = FILL_THREADS / 32;
 
 enum { MODE_FILL = 0, MODE_READ = 1, MODE_PROJ = 2 };
 
@@ -34,7 +33,6 @@ struct FillArgs {
   Win W;
   int mode;
   int do_gram;
-  int nstage;
   const double* ring;
   const double* rho;
   const double* cvec;      // w coefficients (c = A y, or projection z)
@@ -46,108 +44,45 @@ struct FillArgs {
   double* part;            // [grid][nU+1]
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+  return v;
 }
 
-__device__ __forceinline__ bool bit_of(const uint32_t* m, const Geo& g, int64_t n) {
-  const int i = (int)(n % g.nx), j = (int)(n / g.nx);
-  return (m[(int64_t)j * g.wpr + (i >> 5)] >> (i & 31)) & 1u;
-}
-
-// NU: compile-time upper bound of the window slots (size of the per-lane Gram accumulators)
-template <int NU>
-__global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
-  extern __shared__ __align__(128) unsigned char smraw[];
+// SH: compile-time slots per lane (a DOF's nU slots are split over the two half-warps)
+template <int SH>
+__global__ void __launch_bounds__(FILL_THREADS) fill_kernel(FillArgs a) {
+  __shared__ double cs[kMaxW + 2];       // c_i, indexed by slot (0 for psi_prev-only slot)
+  __shared__ double wred[FILL_WARPS][2 * SH + 1];
   const int nU = a.W.nU, w = a.W.w;
-  const int ncol = nU + 1;  // window slots + rho
-  double* stage0 = reinterpret_cast<double*>(smraw);
-  const size_t stage_elems = (size_t)ncol * TE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + a.nstage * stage_elems);
-  uint64_t* empty = full + a.nstage;
-  __shared__ double cs[kMaxW];
-  __shared__ double wred[NCW][NU + 1];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const Geo& g = a.g;
-  for (int i = tid; i < w; i += FILL_THREADS) cs[i] = a.cvec ? a.cvec[i] : 0.0;
-  if (tid == 0) {
-    for (int s = 0; s < a.nstage; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  const int64_t ntiles = (g.D + TE - 1) / TE;
-  const int64_t first = blockIdx.x;
-
-  if (warp == NCW) {
-    // ---------------- producer warp: bulk copies of each tile into the stage ring ----------------
-    int it = 0;
-    for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
-      const int st = it % a.nstage;
-      if (it >= a.nstage) mbar_wait(&empty[st], (uint32_t)(((it / a.nstage) - 1) & 1));
-      const int64_t e0 = tile * TE;
-      const int64_t cnt = (g.D - e0) < TE ? (g.D - e0) : TE;
-      const uint32_t bytes = (uint32_t)(((cnt + 1) / 2) * 2 * sizeof(double));
-      double* dst = stage0 + st * stage_elems;
-      if (lane == 0) mbar_expect(&full[st], bytes * ncol);
-      __syncwarp();
-      for (int s = lane; s <= nU; s += 32) {
-        const double* src = (s < nU) ? a.ring + (int64_t)a.W.slot[s] * g.Dp + e0 : a.rho + e0;
-        bulk_g2s(dst + (size_t)s * TE, src, bytes, &full[st]);
-      }
-    }
-    return;
-  }
-
-  // ---------------- compute warps: lane = DOF ----------------
-  double csum = 0.0;
-  for (int i = 0; i < w; ++i) csum += cs[i];
-  const double inv_w = 1.0 / (double)w;
   const int xoff = nU - w;  // psi_cur and X use slots >= xoff; psi_prev uses slots < w
-  double acc[NU];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int half = lane >> 4, sub = lane & 15;
+  const Geo& g = a.g;
+  for (int s = tid; s < nU; s += FILL_THREADS) cs[s] = (s >= xoff && a.cvec) ? a.cvec[s - xoff] : 0.0;
+  __syncthreads();
+  double csum = 0.0;
+  for (int s = xoff; s < nU; ++s) csum += cs[s];
+  const double inv_w = 1.0 / (double)w;
+  // this lane's slots: half 0 -> [0, h0), half 1 -> [h0, nU)
+  const int h0 = (nU + 1) / 2;
+  const int s_begin = half ? h0 : 0, s_end = half ? nU : h0;
+  double acc[SH];
 #pragma unroll
-  for (int s = 0; s < NU; ++s) acc[s] = 0.0;
+  for (int i = 0; i < SH; ++i) acc[i] = 0.0;
   double acc_self = 0.0;
-  const int el = warp * 32 + lane;
-  // per-DOF global reads (mask words, HDM value / new column) are software-pipelined one
-  // tile ahead so their latency overlaps the previous tile's arithmetic
+  const int64_t nchunks = (g.D + 15) / 16;
+  const int64_t stride = (int64_t)gridDim.x * FILL_WARPS;
+  // per-DOF side data (mask words, HDM value / new column) is fetched one chunk ahead
   uint32_t wS = 0, wB = 0;
   int bitpos = 0;
   double pre = 0.0;
-  auto fetch = [&](int64_t tile) {
-    const int64_t e = tile * TE + el;
+  auto fetch = [&](int64_t chunk) {
     wS = wB = 0;
     pre = 0.0;
-    if (tile < ntiles && e < g.D && a.mode != MODE_PROJ) {
+    const int64_t e = chunk * 16 + sub;
+    if (half == 0 && chunk < nchunks && e < g.D && a.mode != MODE_PROJ) {
       const int64_t n = e % g.N;
       const int i = (int)(n % g.nx), j = (int)(n / g.nx);
       const int64_t wi = (int64_t)j * g.wpr + (i >> 5);
@@ -155,103 +90,97 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
       if (a.mode == MODE_FILL) {
         wS = a.mS[wi];
         if (a.mB) wB = a.mB[wi];
-        pre = a.src_S[e];  // read unconditionally (U3 is allocated everywhere); used on S-hat only
+        pre = a.src_S[e];  // read unconditionally (allocated everywhere); used on S-hat only
       } else {
         pre = a.out[e];
       }
     }
   };
-  fetch(first);
-  int it = 0;
-  for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
-    const int st = it % a.nstage;
-    const int64_t e = tile * TE + el;
+  int64_t chunk = (int64_t)blockIdx.x * FILL_WARPS + warp;
+  fetch(chunk);
+  for (; chunk < nchunks; chunk += stride) {
+    const int64_t e = chunk * 16 + sub;
     const bool valid = e < g.D;
+    const int64_t ec = valid ? e : 0;
+    // all window loads of this lane in flight together
+    double x[SH];
+#pragma unroll
+    for (int i = 0; i < SH; ++i) {
+      const int s = s_begin + i;
+      const double* col = (s < s_end) ? a.ring + (int64_t)a.W.slot[s] * g.Dp : a.rho;
+      x[i] = ld_stream(col + ec);
+    }
+    const double rh = ld_stream(a.rho + ec);
     const bool inS = (wS >> bitpos) & 1u, inB = (wB >> bitpos) & 1u;
-    const double srcv = pre, outv = pre;
-    fetch(tile + gridDim.x);
-    mbar_wait(&full[st], (uint32_t)((it / a.nstage) & 1));
-    const double* T = stage0 + st * stage_elems + el;
-    const double rh = T[nU * TE];
-    // pass 1 (x_s = gamma_s - rho): sp = sum_{s<w} x_s, sc = sum_{s>=xoff} x_s,
-    //                                tr = sum_{s>=xoff} c_{s-xoff} x_s  (two partial chains each)
-    double sp = 0.0, sc = 0.0, tr = 0.0, sp2 = 0.0, sc2 = 0.0, tr2 = 0.0;
-    if (xoff == 1) sp = T[0] - rh;
-    int s = xoff;
-#pragma unroll 4
-    for (; s + 1 < w; s += 2) {
-      const double x = T[s * TE] - rh, x2 = T[(s + 1) * TE] - rh;
-      sp += x;
-      sc += x;
-      tr += cs[s - xoff] * x;
-      sp2 += x2;
-      sc2 += x2;
-      tr2 += cs[s + 1 - xoff] * x2;
-    }
-    if (s < w) {
-      const double x = T[s * TE] - rh;
-      sp += x;
-      sc += x;
-      tr += cs[s - xoff] * x;
-    }
-    if (xoff == 1) {
-      const double x = T[w * TE] - rh;
-      sc2 += x;
-      tr2 += cs[w - 1] * x;
-    }
-    sp += sp2;
-    sc += sc2;
-    tr += tr2;
-    double gval = 0.0;
-    if (valid) {
-      // psi_prev - rho = sp/w, psi_cur - rho = sc/w;  Phi y = sum_i c_i (x_i - (psi_prev - rho))
-      const double dev = tr - (sp * inv_w) * csum;
-      if (a.mode == MODE_FILL) {
-        const double rec = (rh + sc * inv_w) + dev;
-        if (inS) {
-          gval = srcv;
-          const double d = gval - rec;
-          a.eps_elem[e] = d * d;
-        } else {
-          gval = rec;
-        }
-        a.out[e] = gval;
-      } else if (a.mode == MODE_READ) {
-        gval = outv;
-      } else {  // MODE_PROJ: residual of the projection onto the basis (bootstrap indicator)
-        a.eps_elem[e] = dev * dev;
+    const double sidev = pre;
+    fetch(chunk + stride);
+    // pass 1 on this lane's slots (x_s = gamma_s - rho):
+    //   sp = sum_{s<w} x_s, sc = sum_{s>=xoff} x_s, tr = sum_{s>=xoff} c_{s-xoff} x_s
+    double sp = 0.0, sc = 0.0, tr = 0.0;
+#pragma unroll
+    for (int i = 0; i < SH; ++i) {
+      const int s = s_begin + i;
+      x[i] -= rh;
+      if (s < s_end) {
+        if (s < w) sp += x[i];
+        if (s >= xoff) sc += x[i];
+        tr += cs[s] * x[i];
       }
     }
-    // pass 2: new Gram row, per-lane accumulators (band DOFs are added after the filter)
-    if (a.do_gram && valid && !inB) {
-      const double gr = gval - rh;
-      acc_self += gr * gr;
-#pragma unroll
-      for (int s = 0; s < NU; ++s)
-        if (s < nU) acc[s] += gr * (T[s * TE] - rh);
+    // combine the two halves (a + b == b + a: both lanes get identical sums)
+    sp += __shfl_xor_sync(0xffffffffu, sp, 16);
+    sc += __shfl_xor_sync(0xffffffffu, sc, 16);
+    tr += __shfl_xor_sync(0xffffffffu, tr, 16);
+    const bool inS_p = __shfl_sync(0xffffffffu, inS, sub);
+    const bool inB_p = __shfl_sync(0xffffffffu, inB, sub);
+    const double side_p = __shfl_sync(0xffffffffu, sidev, sub);
+    double gval = 0.0;
+    // psi_prev - rho = sp/w, psi_cur - rho = sc/w;  Phi y = sum_i c_i (x_i - (psi_prev - rho))
+    const double dev = tr - (sp * inv_w) * csum;
+    if (a.mode == MODE_FILL) {
+      const double rec = (rh + sc * inv_w) + dev;
+      gval = inS_p ? side_p : rec;
+      if (half == 0 && valid) {
+        if (inS_p) {
+          const double d = gval - rec;
+          a.eps_elem[e] = d * d;
+        }
+        a.out[e] = gval;
+      }
+    } else if (a.mode == MODE_READ) {
+      gval = side_p;
+    } else if (half == 0 && valid) {  // MODE_PROJ: residual of the projection (bootstrap indicator)
+      a.eps_elem[e] = dev * dev;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    // pass 2: new Gram row on this lane's slots (band DOFs are added after the filter)
+    if (a.do_gram && valid && !inB_p) {
+      const double gr = gval - rh;
+      if (half == 0) acc_self += gr * gr;
+#pragma unroll
+      for (int i = 0; i < SH; ++i) acc[i] += gr * x[i];
+    }
   }
   if (!a.do_gram) return;
-  // fixed-order reductions: lanes (shuffle tree), then the compute warps -> part[block][*]
+  // fixed-order reductions: 16 lanes of each half (shuffle tree), then warps -> part[block][*]
 #pragma unroll
-  for (int s = 0; s < NU; ++s) {
-    double v = acc[s];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0 && s < nU) wred[warp][s] = v;
+  for (int i = 0; i < SH; ++i) {
+    double v = acc[i];
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (sub == 0) wred[warp][half * SH + i] = v;
   }
   {
     double v = acc_self;
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) wred[warp][NU] = v;
+    if (lane == 0) wred[warp][2 * SH] = v;
   }
-  asm volatile("bar.sync 1, %0;\n" ::"r"(32 * NCW));  // compute warps only
+  __syncthreads();
   double* outp = a.part + (int64_t)blockIdx.x * (nU + 1);
-  for (int s = warp * 32 + lane; s <= nU; s += 32 * NCW) {
-    const int idx = (s == nU) ? NU : s;
+  for (int s = tid; s <= nU; s += FILL_THREADS) {
+    int idx;
+    if (s == nU) idx = 2 * SH;
+    else idx = (s < h0) ? s : SH + (s - h0);
     double v = 0.0;
-    for (int k = 0; k < NCW; ++k) v += wred[k][idx];
+    for (int k = 0; k < FILL_WARPS; ++k) v += wred[k][idx];
     outp[s] = v;
   }
 }
@@ -301,18 +230,22 @@ __global__ void mean_kernel(Geo g, Win W, const double* __restrict__ ring, doubl
   }
 }
 
-template <int NU>
-hrom_status launch_fill_t(hrom_ctx* c, const FillArgs& a, size_t smem) {
-  HROM_CK(cudaFuncSetAttribute(fill_kernel<NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  fill_kernel<NU><<<c->fill_blocks, FILL_THREADS, smem, c->st>>>(a);
+template <int SH>
+hrom_status launch_fill_t(hrom_ctx* c, const FillArgs& a) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fill_kernel<SH>, FILL_THREADS, 0);
+  const int grid = std::min(c->fill_blocks, c->nsm * std::max(occ, 1));
+  fill_kernel<SH><<<grid, FILL_THREADS, 0, c->st>>>(a);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
+  c->fill_grid = grid;
   return HROM_OK;
 }
 
 }  // namespace
 
 int fill_max_gram_slots() { return 68; }
+hrom_status reduce_band_rows(hrom_ctx* c, const Win& W, int new_slot);
 
 hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S, double* out, int /*out_slot*/) {
   FillArgs a{};
@@ -322,12 +255,6 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S
   a.do_gram = (mode != MODE_PROJ) && out != nullptr && c->P.gram_mode == 0 ? 1 : 0;
   if (mode == MODE_FILL && out != nullptr && !(out >= c->b.ring && out < c->b.ring + (int64_t)c->nslots * c->g.Dp))
     a.do_gram = 0;  // standalone reconstruct into a caller buffer: no window Gram
-  // stages of TE DOFs x (nU+1) columns, as many as fit (<= 4)
-  const size_t stage = (size_t)(W.nU + 1) * TE * sizeof(double);
-  const size_t budget = 224 * 1024 - 2 * 1024;
-  a.nstage = (int)std::min<size_t>(4, budget / (stage + 16));
-  if (a.nstage < 1) return HROM_E_INVALID;
-  const size_t smem = a.nstage * stage + 2 * a.nstage * sizeof(uint64_t);
   a.ring = c->b.ring;
   a.rho = c->b.rho;
   a.cvec = (mode == MODE_PROJ) ? c->b.zvec : c->b.cvec;
@@ -337,13 +264,17 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S
   a.mB = (mode == MODE_FILL) ? c->b.masks + (int64_t)M_B * c->mwords : nullptr;
   a.eps_elem = c->b.eps_elem;
   a.part = c->b.gpart;
-  if (!a.do_gram) return launch_fill_t<1>(c, a, smem);
-  if (W.nU <= 12) return launch_fill_t<12>(c, a, smem);
-  if (W.nU <= 24) return launch_fill_t<24>(c, a, smem);
-  if (W.nU <= 36) return launch_fill_t<36>(c, a, smem);
-  if (W.nU <= 52) return launch_fill_t<52>(c, a, smem);
-  if (W.nU <= 68) return launch_fill_t<68>(c, a, smem);
-  return HROM_E_INVALID;  // wider windows use gram_mode = 1 (hrom_create enforces it)
+  const int sh = (W.nU + 1) / 2;
+  if (sh <= 6) return launch_fill_t<6>(c, a);
+  if (sh <= 12) return launch_fill_t<12>(c, a);
+  if (sh <= 18) return launch_fill_t<18>(c, a);
+  if (sh <= 26) return launch_fill_t<26>(c, a);
+  if (sh <= 34) return launch_fill_t<34>(c, a);
+  if (!a.do_gram) {
+    if (sh <= 50) return launch_fill_t<50>(c, a);
+    if (sh <= 66) return launch_fill_t<66>(c, a);
+  }
+  return HROM_E_INVALID;  // wider windows with a Gram row use gram_mode = 1 (hrom_create)
 }
 
 hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot) {
@@ -351,8 +282,31 @@ hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot) {
 }
 
 hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_band) {
-  const int nblk = c->fill_blocks + (with_band ? c->band_blocks : 0);
-  gram_row_reduce<<<1, 256, 0, c->st>>>(c->b.gpart, nblk, W, new_slot, c->b.C, kMaxSlots);
+  // fill partials occupy blocks [0, fill_grid); band partials follow at offset fill_blocks
+  gram_row_reduce<<<1, 256, 0, c->st>>>(c->b.gpart, c->fill_grid, W, new_slot, c->b.C, kMaxSlots);
+  HROM_LAUNCH_CK();
+  ++c->nlaunch;
+  // band partials are added into the same C entries (fixed order, after the fill part)
+  if (with_band) return reduce_band_rows(c, W, new_slot);
+  return HROM_OK;
+}
+
+__global__ void band_row_add(const double* __restrict__ part, int nblk, Win W, int new_slot, double* __restrict__ C,
+                             int ldc) {
+  const int nU = W.nU;
+  for (int s = threadIdx.x; s <= nU; s += blockDim.x) {
+    double acc = 0.0;
+    for (int b = 0; b < nblk; ++b) acc += part[(int64_t)b * (nU + 1) + s];
+    const int cs_ = (s < nU) ? W.slot[s] : new_slot;
+    const double v = C[new_slot * ldc + cs_] + acc;
+    C[new_slot * ldc + cs_] = v;
+    C[cs_ * ldc + new_slot] = v;
+  }
+}
+
+hrom_status reduce_band_rows(hrom_ctx* c, const Win& W, int new_slot) {
+  band_row_add<<<1, 256, 0, c->st>>>(c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1), c->band_blocks, W, new_slot,
+                                      c->b.C, kMaxSlots);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;

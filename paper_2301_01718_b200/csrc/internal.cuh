@@ -109,7 +109,8 @@ struct hrom_ctx {
   bool gram_row_ready = false;
   int64_t rebase_k = -1000000;
   hrom::Win win{};           // window of the current basis
-  int fill_blocks = 0;       // grid of the fill kernel (Gram-row partial count)
+  int fill_blocks = 0;       // max grid of the fill kernel (Gram-row partial slots)
+  int fill_grid = 0;         // grid of the last fill launch
   int band_blocks = 0;
   int filter_blocks = 0;
   int64_t last_err_cell = -1;

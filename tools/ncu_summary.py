@@ -30,9 +30,15 @@ def main(rep, nlines=12):
     stalls = sorted(((float(v[0]), k) for k, v in d.items() if k.startswith("smsp__pcsamp_warps_issue_stalled_")
                      and not k.endswith("not_issued") and v[0] not in ("", "n/a")), reverse=True)[:8]
     print("  top stalls:", ", ".join(f"{k.replace('smsp__pcsamp_warps_issue_stalled_', '')}={int(v)}" for v, k in stalls))
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda"],
-                         capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(out)))
+    for view in ("cuda", "sass"):
+        out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", view],
+                             capture_output=True, text=True).stdout
+        rows = [r for r in csv.reader(io.StringIO(out)) if r and r[0] != "Kernel Name"]
+        print(f"  -- {view} view --")
+        _top(rows, nlines)
+
+
+def _top(rows, nlines):
     if rows:
         hdr = rows[0]
         try:
@@ -49,7 +55,7 @@ def main(rep, nlines=12):
                 pass
         tot = sum(x[0] for x in lines) or 1
         for s, ln, src in sorted(lines, reverse=True)[:nlines]:
-            print(f"  {100*s/tot:5.1f}%  L{ln}: {src}")
+            print(f"  {100*s/tot:5.1f}%  {ln}: {src}")
 
 
 if __name__ == "__main__":
