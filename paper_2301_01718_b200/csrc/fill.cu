@@ -12,10 +12,10 @@
 // psi_prev / psi_cur are recomputed from the columns in registers: the
 // reference state is never stored or drifted.
 //
-// Register streaming: a DOF is owned by a lane pair (lane l and l+16); each lane loads its
-// half of the window column values with coalesced 128-byte warp segments, all loads of a
-// DOF in flight at once, keeps them in registers for the second use (Gram row) and keeps
-// one Gram accumulator per slot.  No shared-memory staging, no CTA barrier in the stream.
+// Register streaming: thread per DOF; all of a DOF's window loads are in flight at once
+// (coalesced 256-byte warp segments per column), the values stay in registers for their
+// second use (the Gram row) whose per-thread products accumulate in shared memory.  No
+// staging copies, no CTA barrier in the stream.
 #include <algorithm>
 #include <cstdlib>
 #include "internal.cuh"
@@ -24,7 +24,6 @@ namespace hrom {
 namespace {
 
 constexpr int FILL_THREADS = 128;
-constexpr int FILL_WARPS = FILL_THREADS / 32;
 
 enum { MODE_FILL = 0, MODE_READ = 1, MODE_PROJ = 2 };
 
@@ -50,39 +49,33 @@ __device__ __forceinline__ double ld_stream(const double* p) {
   return v;
 }
 
-// SH: compile-time slots per lane (a DOF's nU slots are split over the two half-warps)
-template <int SH>
+// Thread per DOF.  NU: compile-time bound of the window slots (register array of the
+// DOF's window values, kept between the two uses); the per-thread Gram-row products are
+// accumulated in shared memory (acc[s][thread]), conflict-free.
+template <int NU, bool GRAM>
 __global__ void __launch_bounds__(FILL_THREADS) fill_kernel(FillArgs a) {
-  __shared__ double cs[kMaxW + 2];       // c_i, indexed by slot (0 for psi_prev-only slot)
-  __shared__ double wred[FILL_WARPS][2 * SH + 1];
+  extern __shared__ double accs[];       // [NU+1][FILL_THREADS] (GRAM only)
+  __shared__ double cs[kMaxW + 2];       // c_i, indexed by slot (0 for the psi_prev-only slot)
   const int nU = a.W.nU, w = a.W.w;
   const int xoff = nU - w;  // psi_cur and X use slots >= xoff; psi_prev uses slots < w
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int half = lane >> 4, sub = lane & 15;
+  const int tid = threadIdx.x;
   const Geo& g = a.g;
   for (int s = tid; s < nU; s += FILL_THREADS) cs[s] = (s >= xoff && a.cvec) ? a.cvec[s - xoff] : 0.0;
+  if (GRAM)
+    for (int s = 0; s <= NU; ++s) accs[s * FILL_THREADS + tid] = 0.0;
   __syncthreads();
   double csum = 0.0;
   for (int s = xoff; s < nU; ++s) csum += cs[s];
   const double inv_w = 1.0 / (double)w;
-  // this lane's slots: half 0 -> [0, h0), half 1 -> [h0, nU)
-  const int h0 = (nU + 1) / 2;
-  const int s_begin = half ? h0 : 0, s_end = half ? nU : h0;
-  double acc[SH];
-#pragma unroll
-  for (int i = 0; i < SH; ++i) acc[i] = 0.0;
-  double acc_self = 0.0;
-  const int64_t nchunks = (g.D + 15) / 16;
-  const int64_t stride = (int64_t)gridDim.x * FILL_WARPS;
-  // per-DOF side data (mask words, HDM value / new column) is fetched one chunk ahead
+  const int64_t stride = (int64_t)gridDim.x * FILL_THREADS;
+  // per-DOF side data (mask words, HDM value / new column) is fetched one iteration ahead
   uint32_t wS = 0, wB = 0;
   int bitpos = 0;
   double pre = 0.0;
-  auto fetch = [&](int64_t chunk) {
+  auto fetch = [&](int64_t e) {
     wS = wB = 0;
     pre = 0.0;
-    const int64_t e = chunk * 16 + sub;
-    if (half == 0 && chunk < nchunks && e < g.D && a.mode != MODE_PROJ) {
+    if (e < g.D && a.mode != MODE_PROJ) {
       const int64_t n = e % g.N;
       const int i = (int)(n % g.nx), j = (int)(n / g.nx);
       const int64_t wi = (int64_t)j * g.wpr + (i >> 5);
@@ -96,92 +89,74 @@ __global__ void __launch_bounds__(FILL_THREADS) fill_kernel(FillArgs a) {
       }
     }
   };
-  int64_t chunk = (int64_t)blockIdx.x * FILL_WARPS + warp;
-  fetch(chunk);
-  for (; chunk < nchunks; chunk += stride) {
-    const int64_t e = chunk * 16 + sub;
-    const bool valid = e < g.D;
-    const int64_t ec = valid ? e : 0;
-    // all window loads of this lane in flight together
-    double x[SH];
+  int64_t e = (int64_t)blockIdx.x * FILL_THREADS + tid;
+  fetch(e);
+  for (; e < g.D; e += stride) {
+    // all window loads of this DOF in flight together
+    double x[NU];
 #pragma unroll
-    for (int i = 0; i < SH; ++i) {
-      const int s = s_begin + i;
-      const double* col = (s < s_end) ? a.ring + (int64_t)a.W.slot[s] * g.Dp : a.rho;
-      x[i] = ld_stream(col + ec);
-    }
-    const double rh = ld_stream(a.rho + ec);
+    for (int s = 0; s < NU; ++s)
+      if (s < nU) x[s] = ld_stream(a.ring + (int64_t)a.W.slot[s] * g.Dp + e);
+    const double rh = ld_stream(a.rho + e);
     const bool inS = (wS >> bitpos) & 1u, inB = (wB >> bitpos) & 1u;
-    const double sidev = pre;
-    fetch(chunk + stride);
-    // pass 1 on this lane's slots (x_s = gamma_s - rho):
-    //   sp = sum_{s<w} x_s, sc = sum_{s>=xoff} x_s, tr = sum_{s>=xoff} c_{s-xoff} x_s
-    double sp = 0.0, sc = 0.0, tr = 0.0;
+    const double side = pre;
+    fetch(e + stride);
+    // pass 1 (x_s = gamma_s - rho): sp = sum_{s<w} x_s, sc = sum_{s>=xoff} x_s,
+    //                                tr = sum_{s>=xoff} c_{s-xoff} x_s  (two chains each)
+    double sp = 0.0, sc = 0.0, tr = 0.0, sp2 = 0.0, sc2 = 0.0, tr2 = 0.0;
 #pragma unroll
-    for (int i = 0; i < SH; ++i) {
-      const int s = s_begin + i;
-      x[i] -= rh;
-      if (s < s_end) {
-        if (s < w) sp += x[i];
-        if (s >= xoff) sc += x[i];
-        tr += cs[s] * x[i];
+    for (int s = 0; s < NU; ++s) {
+      if (s < nU) {
+        x[s] -= rh;
+        if (s & 1) {
+          if (s < w) sp2 += x[s];
+          if (s >= xoff) sc2 += x[s];
+          tr2 += cs[s] * x[s];
+        } else {
+          if (s < w) sp += x[s];
+          if (s >= xoff) sc += x[s];
+          tr += cs[s] * x[s];
+        }
       }
     }
-    // combine the two halves (a + b == b + a: both lanes get identical sums)
-    sp += __shfl_xor_sync(0xffffffffu, sp, 16);
-    sc += __shfl_xor_sync(0xffffffffu, sc, 16);
-    tr += __shfl_xor_sync(0xffffffffu, tr, 16);
-    const bool inS_p = __shfl_sync(0xffffffffu, inS, sub);
-    const bool inB_p = __shfl_sync(0xffffffffu, inB, sub);
-    const double side_p = __shfl_sync(0xffffffffu, sidev, sub);
+    sp += sp2;
+    sc += sc2;
+    tr += tr2;
     double gval = 0.0;
     // psi_prev - rho = sp/w, psi_cur - rho = sc/w;  Phi y = sum_i c_i (x_i - (psi_prev - rho))
     const double dev = tr - (sp * inv_w) * csum;
     if (a.mode == MODE_FILL) {
       const double rec = (rh + sc * inv_w) + dev;
-      gval = inS_p ? side_p : rec;
-      if (half == 0 && valid) {
-        if (inS_p) {
-          const double d = gval - rec;
-          a.eps_elem[e] = d * d;
-        }
-        a.out[e] = gval;
+      gval = inS ? side : rec;
+      if (inS) {
+        const double d = gval - rec;
+        a.eps_elem[e] = d * d;
       }
+      a.out[e] = gval;
     } else if (a.mode == MODE_READ) {
-      gval = side_p;
-    } else if (half == 0 && valid) {  // MODE_PROJ: residual of the projection (bootstrap indicator)
+      gval = side;
+    } else {  // MODE_PROJ: residual of the projection onto the basis (bootstrap indicator)
       a.eps_elem[e] = dev * dev;
     }
-    // pass 2: new Gram row on this lane's slots (band DOFs are added after the filter)
-    if (a.do_gram && valid && !inB_p) {
+    // pass 2: new Gram row (band DOFs are added after the filter)
+    if (GRAM && !inB) {
       const double gr = gval - rh;
-      if (half == 0) acc_self += gr * gr;
 #pragma unroll
-      for (int i = 0; i < SH; ++i) acc[i] += gr * x[i];
+      for (int s = 0; s < NU; ++s)
+        if (s < nU) accs[s * FILL_THREADS + tid] += gr * x[s];
+      accs[NU * FILL_THREADS + tid] += gr * gr;
     }
   }
-  if (!a.do_gram) return;
-  // fixed-order reductions: 16 lanes of each half (shuffle tree), then warps -> part[block][*]
-#pragma unroll
-  for (int i = 0; i < SH; ++i) {
-    double v = acc[i];
-    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (sub == 0) wred[warp][half * SH + i] = v;
-  }
-  {
-    double v = acc_self;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) wred[warp][2 * SH] = v;
-  }
+  if (!GRAM) return;
+  // fixed-order reduction over the block's threads -> part[block][*]
   __syncthreads();
   double* outp = a.part + (int64_t)blockIdx.x * (nU + 1);
-  for (int s = tid; s <= nU; s += FILL_THREADS) {
-    int idx;
-    if (s == nU) idx = 2 * SH;
-    else idx = (s < h0) ? s : SH + (s - h0);
+  for (int s = tid / 32; s <= nU; s += FILL_THREADS / 32) {
+    const int row = (s == nU) ? NU : s;
     double v = 0.0;
-    for (int k = 0; k < FILL_WARPS; ++k) v += wred[k][idx];
-    outp[s] = v;
+    for (int t = tid & 31; t < FILL_THREADS; t += 32) v += accs[row * FILL_THREADS + t];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((tid & 31) == 0) outp[s] = v;
   }
 }
 
@@ -230,12 +205,14 @@ __global__ void mean_kernel(Geo g, Win W, const double* __restrict__ ring, doubl
   }
 }
 
-template <int SH>
+template <int NU, bool GRAM>
 hrom_status launch_fill_t(hrom_ctx* c, const FillArgs& a) {
+  const size_t smem = GRAM ? (size_t)(NU + 1) * FILL_THREADS * sizeof(double) : 0;
+  HROM_CK(cudaFuncSetAttribute(fill_kernel<NU, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fill_kernel<SH>, FILL_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fill_kernel<NU, GRAM>, FILL_THREADS, smem);
   const int grid = std::min(c->fill_blocks, c->nsm * std::max(occ, 1));
-  fill_kernel<SH><<<grid, FILL_THREADS, 0, c->st>>>(a);
+  fill_kernel<NU, GRAM><<<grid, FILL_THREADS, smem, c->st>>>(a);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   c->fill_grid = grid;
@@ -264,17 +241,21 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S
   a.mB = (mode == MODE_FILL) ? c->b.masks + (int64_t)M_B * c->mwords : nullptr;
   a.eps_elem = c->b.eps_elem;
   a.part = c->b.gpart;
-  const int sh = (W.nU + 1) / 2;
-  if (sh <= 6) return launch_fill_t<6>(c, a);
-  if (sh <= 12) return launch_fill_t<12>(c, a);
-  if (sh <= 18) return launch_fill_t<18>(c, a);
-  if (sh <= 26) return launch_fill_t<26>(c, a);
-  if (sh <= 34) return launch_fill_t<34>(c, a);
-  if (!a.do_gram) {
-    if (sh <= 50) return launch_fill_t<50>(c, a);
-    if (sh <= 66) return launch_fill_t<66>(c, a);
+  if (a.do_gram) {
+    if (W.nU <= 12) return launch_fill_t<12, true>(c, a);
+    if (W.nU <= 24) return launch_fill_t<24, true>(c, a);
+    if (W.nU <= 36) return launch_fill_t<36, true>(c, a);
+    if (W.nU <= 52) return launch_fill_t<52, true>(c, a);
+    if (W.nU <= 68) return launch_fill_t<68, true>(c, a);
+    return HROM_E_INVALID;  // wider windows with a Gram row use gram_mode = 1 (hrom_create)
   }
-  return HROM_E_INVALID;  // wider windows with a Gram row use gram_mode = 1 (hrom_create)
+  if (W.nU <= 12) return launch_fill_t<12, false>(c, a);
+  if (W.nU <= 24) return launch_fill_t<24, false>(c, a);
+  if (W.nU <= 36) return launch_fill_t<36, false>(c, a);
+  if (W.nU <= 68) return launch_fill_t<68, false>(c, a);
+  if (W.nU <= 100) return launch_fill_t<100, false>(c, a);
+  if (W.nU <= 132) return launch_fill_t<132, false>(c, a);
+  return HROM_E_INVALID;
 }
 
 hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot) {
