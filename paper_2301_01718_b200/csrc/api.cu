@@ -108,7 +108,8 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   g.wpr = (grid->nx + 31) / 32;
   g.N = (int64_t)g.nx * g.ny;
   g.D = g.c * g.N;
-  g.Dp = (g.D + 31) / 32 * 32;
+  g.Dp = (g.D + TILE - 1) / TILE * TILE;
+  g.nsr = c->nslots + 1;  // slab: w+2 snapshot slots + rho
   g.dx = (grid->x1 - grid->x0) / grid->nx;
   g.dy = dim == 2 ? (grid->y1 - grid->y0) / ny : 1.0;
   g.gamma = gamma;
@@ -128,8 +129,8 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   Bufs& b = c->b;
   hrom_status s = HROM_OK;
   auto A = [&](hrom_status r) { if (r != HROM_OK) s = r; };
-  A(dalloc(&b.ring, (size_t)c->nslots * g.Dp));
-  A(dalloc(&b.rho, g.Dp));
+  A(dalloc(&b.ring, (size_t)g.nsr * g.Dp));
+  if (b.ring) b.rho = b.ring + (int64_t)c->nslots * TILE;  // slab slot nslots
   A(dalloc(&b.U1, g.Dp));
   A(dalloc(&b.U2, g.Dp));
   A(dalloc(&b.U3, g.Dp));
@@ -171,7 +172,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   }
   // pointer table: colptr[i] = slot (i mod nslots), so any run of consecutive slots is contiguous
   std::vector<const double*> tab(2 * kMaxSlots);
-  for (int i = 0; i < 2 * kMaxSlots; ++i) tab[i] = b.ring + (int64_t)(i % c->nslots) * g.Dp;
+  for (int i = 0; i < 2 * kMaxSlots; ++i) tab[i] = b.ring + (int64_t)(i % c->nslots) * TILE;
   std::vector<int32_t> stab(2 * kMaxSlots);
   for (int i = 0; i < 2 * kMaxSlots; ++i) stab[i] = i % c->nslots;
   if (cudaMemcpy(b.colptr, tab.data(), tab.size() * sizeof(double*), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -182,8 +183,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
       cudaMemset(b.eps, 0, g.N * sizeof(double)) != cudaSuccess ||
       cudaMemset(b.masks, 0, (size_t)M_COUNT * c->mwords * sizeof(uint32_t)) != cudaSuccess ||
       cudaMemset(b.counts, 0, 16 * sizeof(int32_t)) != cudaSuccess ||
-      cudaMemset(b.rho, 0, g.Dp * sizeof(double)) != cudaSuccess ||
-      cudaMemset(b.ring, 0, (size_t)c->nslots * g.Dp * sizeof(double)) != cudaSuccess) {
+      cudaMemset(b.ring, 0, (size_t)g.nsr * g.Dp * sizeof(double)) != cudaSuccess) {
     hrom_destroy(c);
     return HROM_E_CUDA;
   }
@@ -207,7 +207,7 @@ void hrom_destroy(hrom_ctx* c) {
   if (c->ev_basis_done) cudaEventDestroy(c->ev_basis_done);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   Bufs& b = c->b;
-  void* ptrs[] = {b.ring, b.rho, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
+  void* ptrs[] = {b.ring, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
                   b.kept, b.C, b.part, b.gpart, b.K, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
                   b.dreg, b.ureg, b.sel_val, b.sel_cell, b.blk, b.hist, b.fstat, b.fcnt, (void*)b.colptr, b.slot_tab};
   for (void* q : ptrs)
@@ -215,9 +215,29 @@ void hrom_destroy(hrom_ctx* c) {
   delete c;
 }
 
+// plain vector <-> slab ring slot (2-D copy: TILE-element rows, pitches TILE and nsr*TILE)
+static hrom_status copy_slot(hrom_ctx* c, int slot, const double* src_plain, double* dst_plain) {
+  const int64_t D = c->g.D, full = D / TILE, tail = D - full * TILE;
+  const size_t row = TILE * sizeof(double), spitch = (size_t)c->g.nsr * TILE * sizeof(double);
+  double* base = c->b.ring + (int64_t)slot * TILE;
+  if (src_plain) {
+    if (full) HROM_CK(cudaMemcpy2DAsync(base, spitch, src_plain, row, row, full, cudaMemcpyDefault, c->st));
+    if (tail)
+      HROM_CK(cudaMemcpyAsync(base + full * c->g.nsr * TILE, src_plain + full * TILE, tail * sizeof(double),
+                              cudaMemcpyDefault, c->st));
+  } else {
+    if (full) HROM_CK(cudaMemcpy2DAsync(dst_plain, row, base, spitch, row, full, cudaMemcpyDefault, c->st));
+    if (tail)
+      HROM_CK(cudaMemcpyAsync(dst_plain + full * TILE, base + full * c->g.nsr * TILE, tail * sizeof(double),
+                              cudaMemcpyDefault, c->st));
+  }
+  return HROM_OK;
+}
+
 hrom_status hrom_set_state(hrom_ctx* c, const double* any_q) {
   if (!c || !any_q) return HROM_E_INVALID;
-  HROM_CK(cudaMemcpyAsync(c->b.ring, any_q, c->g.D * sizeof(double), cudaMemcpyDefault, c->st));
+  hrom_status s0 = copy_slot(c, 0, any_q, nullptr);
+  if (s0 != HROM_OK) return s0;
   HROM_CK(cudaMemsetAsync(c->b.ureg + 1, 0xff, sizeof(unsigned long long), c->st));
   c->k = 0;
   c->basis_ready = c->sets_ready = c->gram_row_ready = false;
@@ -229,24 +249,23 @@ hrom_status hrom_set_state(hrom_ctx* c, const double* any_q) {
 hrom_status hrom_get_state(hrom_ctx* c, double* any_q) {
   if (!c || !any_q) return HROM_E_INVALID;
   if (c->k < 0) return HROM_E_STATE;
-  HROM_CK(cudaMemcpyAsync(any_q, c->b.ring + (int64_t)c->slot_of(c->k) * c->g.Dp, c->g.D * sizeof(double),
-                          cudaMemcpyDefault, c->st));
-  return HROM_OK;
+  return copy_slot(c, c->slot_of(c->k), nullptr, any_q);
 }
 
 hrom_status hrom_full_step(hrom_ctx* c, double dt_override, double* dev_dt_out) {
   if (!c) return HROM_E_INVALID;
   if (c->k < 0) return HROM_E_STATE;
   const int64_t kn = c->k + 1;
-  const double* qn = c->b.ring + (int64_t)c->slot_of(c->k) * c->g.Dp;
-  double* out = c->b.ring + (int64_t)c->slot_of(kn) * c->g.Dp;
+  const SRef qn = c->slot_ref(c->slot_of(c->k));
+  const SRef out = c->slot_ref(c->slot_of(kn));
+  const SRef U1 = plain(c->b.U1), U2 = plain(c->b.U2);
   hrom_status s;
   prof_begin(c, SEC_FULL);
   if ((s = launch_dt(c, qn, dt_override)) != HROM_OK) return s;
   if (dev_dt_out) HROM_CK(cudaMemcpyAsync(dev_dt_out, c->b.dreg, sizeof(double), cudaMemcpyDefault, c->st));
-  if ((s = launch_stage(c, 1, qn, qn, c->b.U1, nullptr, 0, dt_override)) != HROM_OK) return s;
-  if ((s = launch_stage(c, 2, qn, c->b.U1, c->b.U2, nullptr, 0, dt_override)) != HROM_OK) return s;
-  if ((s = launch_stage(c, 3, qn, c->b.U2, out, nullptr, 0, dt_override)) != HROM_OK) return s;
+  if ((s = launch_stage(c, 1, qn, qn, U1, nullptr, 0, dt_override)) != HROM_OK) return s;
+  if ((s = launch_stage(c, 2, qn, U1, U2, nullptr, 0, dt_override)) != HROM_OK) return s;
+  if ((s = launch_stage(c, 3, qn, U2, out, nullptr, 0, dt_override)) != HROM_OK) return s;
   prof_end(c, SEC_FULL);
   c->k = kn;
   c->gram_row_ready = false;
@@ -266,8 +285,9 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
   const Geo& g = c->g;
   Bufs& b = c->b;
   const int64_t kn = c->k + 1;
-  const double* qn = b.ring + (int64_t)c->slot_of(c->k) * g.Dp;
-  double* out = b.ring + (int64_t)c->slot_of(kn) * g.Dp;
+  const SRef qn = c->slot_ref(c->slot_of(c->k));
+  const SRef out = c->slot_ref(c->slot_of(kn));
+  const SRef U1 = plain(b.U1), U2 = plain(b.U2), U3 = plain(b.U3);
   // H1
   prof_begin(c, SEC_DT);
   if ((s = launch_dt(c, qn, dt_override)) != HROM_OK) return s;
@@ -276,13 +296,13 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
   // H3: stage 1 on A1, stage 2 on A2, stage 3 on T = S-hat u B (F on the band)
   const int32_t* L = b.lists;
   prof_begin(c, SEC_MASKED);
-  if ((s = launch_stage(c, 1, qn, qn, b.U1, L + (int64_t)L_A1 * g.N, L_A1, dt_override)) != HROM_OK) return s;
-  if ((s = launch_stage(c, 2, qn, b.U1, b.U2, L + (int64_t)L_A2 * g.N, L_A2, dt_override)) != HROM_OK) return s;
-  if ((s = launch_stage(c, 3, qn, b.U2, b.U3, L + (int64_t)L_T * g.N, L_T, dt_override)) != HROM_OK) return s;
+  if ((s = launch_stage(c, 1, qn, qn, U1, L + (int64_t)L_A1 * g.N, L_A1, dt_override)) != HROM_OK) return s;
+  if ((s = launch_stage(c, 2, qn, U1, U2, L + (int64_t)L_A2 * g.N, L_A2, dt_override)) != HROM_OK) return s;
+  if ((s = launch_stage(c, 3, qn, U2, U3, L + (int64_t)L_T * g.N, L_T, dt_override)) != HROM_OK) return s;
   prof_end(c, SEC_MASKED);
   // H4 + H5
   prof_begin(c, SEC_GATHER);
-  if ((s = gram_gathered(c, b.U3)) != HROM_OK) return s;
+  if ((s = gram_gathered(c, U3)) != HROM_OK) return s;
   prof_end(c, SEC_GATHER);
   basis_join(c);  // the eigen-solve of the previous update ran on the side stream
   prof_begin(c, SEC_SOLVE);
@@ -291,7 +311,7 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
   // H6 (+H9, H10 row)
   HROM_CK(cudaMemsetAsync(b.eps, 0, g.N * sizeof(double), c->st));
   prof_begin(c, SEC_FILL);
-  if ((s = launch_fill(c, c->win, 0, b.U3, out, c->slot_of(kn))) != HROM_OK) return s;
+  if ((s = launch_fill(c, c->win, 0, U3, out, true)) != HROM_OK) return s;
   prof_end(c, SEC_FILL);
   prof_begin(c, SEC_EPS);
   if ((s = launch_eps_cells(c)) != HROM_OK) return s;
@@ -299,7 +319,7 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
   // H7
   prof_begin(c, SEC_FILTER);
   if (c->P.n_filter_orders > 0 && c->P.filter_max_sweeps > 0)
-    if ((s = launch_filter(c, out, b.U3)) != HROM_OK) return s;
+    if ((s = launch_filter(c, out, U3)) != HROM_OK) return s;
   prof_end(c, SEC_FILTER);
   prof_begin(c, SEC_BANDGRAM);
   if (c->P.gram_mode == 0)
@@ -329,11 +349,12 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
   if (rebase) {
     prof_end(c, SEC_BASIS);
     prof_begin(c, SEC_REBASE);
-    if ((s = launch_mean(c, W, c->b.rho)) != HROM_OK) return s;
+    if ((s = launch_mean(c, W, c->rho_ref())) != HROM_OK) return s;
     const int s0 = W.slot[0];
-    // consecutive slots are contiguous in the pointer table (see hrom_create)
-    // written straight into the slot-indexed Gram through the slot table
-    if ((s = gram_full(c, c->b.colptr + s0, W.nU, c->g.D, c->b.rho, c->b.C, kMaxSlots, c->b.slot_tab + s0)) != HROM_OK)
+    // consecutive slots are contiguous in the pointer table (see hrom_create); the Gram is
+    // written straight into the slot-indexed C through the slot table
+    if ((s = gram_full(c, c->b.colptr + s0, c->g.nsr, W.nU, c->g.D, c->rho_ref(), c->b.C, kMaxSlots,
+                       c->b.slot_tab + s0)) != HROM_OK)
       return s;
     prof_end(c, SEC_REBASE);
     prof_begin(c, SEC_BASIS);
@@ -367,7 +388,7 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
     zvec_kernel<<<1, 128, 0, c->st>>>(c->b.A, c->b.lam, c->b.ireg, w, c->b.zvec);
     HROM_LAUNCH_CK();
     ++c->nlaunch;
-    if ((s = launch_fill(c, W, 2, nullptr, nullptr, -1)) != HROM_OK) return s;
+    if ((s = launch_fill(c, W, 2, plain(nullptr), plain(nullptr), false)) != HROM_OK) return s;
     if ((s = launch_eps_all(c)) != HROM_OK) return s;
   }
   return HROM_OK;
@@ -405,11 +426,11 @@ hrom_status hrom_reconstruct(hrom_ctx* c, const uint32_t* dev_mask, double* dev_
     c->sets_ready = true;
   }
   if (!c->sets_ready) return HROM_E_STATE;
-  if ((s = gram_gathered(c, dev_v)) != HROM_OK) return s;
+  if ((s = gram_gathered(c, plain(dev_v))) != HROM_OK) return s;
   basis_join(c);
   if ((s = small_solve(c)) != HROM_OK) return s;
   HROM_CK(cudaMemsetAsync(c->b.eps, 0, c->g.N * sizeof(double), c->st));
-  if ((s = launch_fill(c, c->win, 0, dev_v, dev_v, -1)) != HROM_OK) return s;
+  if ((s = launch_fill(c, c->win, 0, plain(dev_v), plain(dev_v), false)) != HROM_OK) return s;
   if ((s = launch_eps_cells(c)) != HROM_OK) return s;
   if (dev_y_out) HROM_CK(cudaMemcpyAsync(dev_y_out, c->b.y, c->r * sizeof(double), cudaMemcpyDefault, c->st));
   if (dev_eps_out)
@@ -426,7 +447,7 @@ hrom_status hrom_filter(hrom_ctx* c, const uint32_t* dev_mask, double* dev_v, co
     c->sets_ready = true;
   }
   if (!c->sets_ready) return HROM_E_STATE;
-  if ((s = launch_filter(c, dev_v, dev_F)) != HROM_OK) return s;
+  if ((s = launch_filter(c, plain(dev_v), plain(dev_F))) != HROM_OK) return s;
   if (dev_kept_out)
     HROM_CK(cudaMemcpyAsync(dev_kept_out, c->b.kept, c->g.N, cudaMemcpyDefault, c->st));
   return HROM_OK;
@@ -477,9 +498,10 @@ hrom_status hrom_set_window(hrom_ctx* c, int64_t k, const double* any_snaps, int
                             const uint32_t* any_mask_next) {
   if (!c || !any_snaps) return HROM_E_INVALID;
   if (k < c->w || nsnaps != c->w + 1) return HROM_E_INVALID;
-  for (int t = 0; t < nsnaps; ++t)
-    HROM_CK(cudaMemcpyAsync(c->b.ring + (int64_t)c->slot_of(k - c->w + t) * c->g.Dp, any_snaps + (int64_t)t * c->g.D,
-                            c->g.D * sizeof(double), cudaMemcpyDefault, c->st));
+  for (int t = 0; t < nsnaps; ++t) {
+    hrom_status s0 = copy_slot(c, c->slot_of(k - c->w + t), any_snaps + (int64_t)t * c->g.D, nullptr);
+    if (s0 != HROM_OK) return s0;
+  }
   HROM_CK(cudaMemsetAsync(c->b.ureg + 1, 0xff, sizeof(unsigned long long), c->st));
   c->k = k;
   c->basis_ready = false;
@@ -532,15 +554,13 @@ hrom_status hrom_get_eigen(hrom_ctx* c, double* any_lambda) {
 hrom_status hrom_gram(hrom_ctx* c, const double* const* dev_cols, int32_t ncol, int64_t rows, const double* dev_rho,
                       double* dev_C) {
   if (!c || !dev_cols || !dev_C || ncol < 1 || ncol > kMaxSlots + 14 || rows < 0) return HROM_E_INVALID;
-  return gram_full(c, dev_cols, ncol, rows, dev_rho, dev_C, ncol, nullptr);
+  return gram_full(c, dev_cols, 1, ncol, rows, plain(dev_rho), dev_C, ncol, nullptr);
 }
 
 hrom_status hrom_put_state(hrom_ctx* c, const double* any_q) {
   if (!c || !any_q) return HROM_E_INVALID;
   if (c->k < 0) return HROM_E_STATE;
-  HROM_CK(cudaMemcpyAsync(c->b.ring + (int64_t)c->slot_of(c->k) * c->g.Dp, any_q, c->g.D * sizeof(double),
-                          cudaMemcpyDefault, c->st));
-  return HROM_OK;
+  return copy_slot(c, c->slot_of(c->k), any_q, nullptr);
 }
 
 hrom_status hrom_profile(hrom_ctx* c, int32_t enable) {

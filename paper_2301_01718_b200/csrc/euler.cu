@@ -4,7 +4,8 @@
 // F_k (remark P:345-347).  BASELINE.json: Rusanov flux, SSP-RK3 (BJ:7-10).
 // The full and the masked step run the SAME kernel (list == nullptr means all cells),
 // so the S-hat rows of a masked step are bitwise the rows of the full step (Eq. 7,
-// exact restriction, reading A9).
+// exact restriction, reading A9).  States are addressed through SRef (slab ring slot
+// or plain vector, internal.cuh).
 #include <cfloat>
 #include "internal.cuh"
 
@@ -75,8 +76,7 @@ __device__ __forceinline__ int wrap(int i, int n, int bc) {
 
 // L at cell (i, j) of q (O6); loads the cross stencil of radius RECON
 template <int DIM, int RECON>
-__device__ __forceinline__ void cell_rhs(const Geo& g, const double* __restrict__ q, int i, int j,
-                                         double* L) {
+__device__ __forceinline__ void cell_rhs(const Geo& g, const SRef q, int i, int j, double* L) {
   constexpr int C = DIM + 2;
   constexpr int R = RECON;
   double Ux[2 * R + 1][C];
@@ -85,7 +85,7 @@ __device__ __forceinline__ void cell_rhs(const Geo& g, const double* __restrict_
   for (int m = -R; m <= R; ++m) {
     const int64_t n = row + wrap(i + m, g.nx, g.bc);
 #pragma unroll
-    for (int v = 0; v < C; ++v) Ux[m + R][v] = __ldg(q + v * g.N + n);
+    for (int v = 0; v < C; ++v) Ux[m + R][v] = __ldg(q.p + sidx(q, v * g.N + n));
   }
   double Fp[C], Fm[C];
   // right face (i, i+1) uses cells i-1, i, i+1, i+2; left face uses i-2 .. i+1
@@ -104,7 +104,7 @@ __device__ __forceinline__ void cell_rhs(const Geo& g, const double* __restrict_
       }
       const int64_t n = (int64_t)wrap(j + m, g.ny, g.bc) * g.nx + i;
 #pragma unroll
-      for (int v = 0; v < C; ++v) Uy[m + R][v] = __ldg(q + v * g.N + n);
+      for (int v = 0; v < C; ++v) Uy[m + R][v] = __ldg(q.p + sidx(q, v * g.N + n));
     }
     double Gp[C], Gm[C];
     face_flux<DIM, DIM - 1, RECON>(Uy[R - (R == 2 ? 1 : 0)], Uy[R], Uy[R + 1], Uy[R + (R == 2 ? 2 : 1)], g.gamma, Gp);
@@ -116,8 +116,7 @@ __device__ __forceinline__ void cell_rhs(const Geo& g, const double* __restrict_
 
 // One SSP-RK3 stage (O8, printed order) on all cells (list == nullptr) or a cell list.
 template <int DIM, int RECON>
-__global__ void __launch_bounds__(256) stage_kernel(Geo g, int stage, const double* __restrict__ qn,
-                                                    const double* __restrict__ qin, double* __restrict__ out,
+__global__ void __launch_bounds__(256) stage_kernel(Geo g, int stage, const SRef qn, const SRef qin, const SRef out,
                                                     const int32_t* __restrict__ list,
                                                     const int32_t* __restrict__ count,
                                                     const double* __restrict__ dtp) {
@@ -133,11 +132,12 @@ __global__ void __launch_bounds__(256) stage_kernel(Geo g, int stage, const doub
 #pragma unroll
     for (int v = 0; v < C; ++v) {
       const int64_t e = v * g.N + n;
+      const double un = qn.p[sidx(qn, e)];
       double r;
-      if (stage == 1) r = qn[e] + dt * L[v];
-      else if (stage == 2) r = 0.75 * qn[e] + 0.25 * (qin[e] + dt * L[v]);
-      else r = (1.0 / 3.0) * qn[e] + (2.0 / 3.0) * (qin[e] + dt * L[v]);
-      out[e] = r;
+      if (stage == 1) r = un + dt * L[v];
+      else if (stage == 2) r = 0.75 * un + 0.25 * (qin.p[sidx(qin, e)] + dt * L[v]);
+      else r = (1.0 / 3.0) * un + (2.0 / 3.0) * (qin.p[sidx(qin, e)] + dt * L[v]);
+      out.p[sidx(out, e)] = r;
     }
   }
 }
@@ -145,15 +145,14 @@ __global__ void __launch_bounds__(256) stage_kernel(Geo g, int stage, const doub
 // H1: max_n S_n with S_n = (|u|+c)/dx [+ (|v|+c)/dy]; S_n >= 0 so its IEEE bits order like
 // the value and an integer atomicMax is exact and order-free (deterministic).
 template <int DIM>
-__global__ void __launch_bounds__(256) smax_kernel(Geo g, const double* __restrict__ q,
-                                                   unsigned long long* __restrict__ smax) {
+__global__ void __launch_bounds__(256) smax_kernel(Geo g, const SRef q, unsigned long long* __restrict__ smax) {
   constexpr int C = DIM + 2;
   double m = 0.0;
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N;
        n += (int64_t)gridDim.x * blockDim.x) {
     double U[C];
 #pragma unroll
-    for (int v = 0; v < C; ++v) U[v] = q[v * g.N + n];
+    for (int v = 0; v < C; ++v) U[v] = q.p[sidx(q, v * g.N + n)];
     const double p = pressure<DIM>(U, g.gamma - 1.0);
     const double cs = sqrt(g.gamma * p / U[0]);
     double s = (fabs(U[1] / U[0]) + cs) / g.dx;
@@ -176,24 +175,20 @@ __global__ void __launch_bounds__(256) smax_kernel(Geo g, const double* __restri
   }
 }
 
-__global__ void dt_finalize(const unsigned long long* smax, double cfl, double dt_override, double* dt,
-                            double* dt_out) {
+__global__ void dt_finalize(const unsigned long long* smax, double cfl, double dt_override, double* dt) {
   const double s = __longlong_as_double((long long)*smax);
-  const double v = dt_override > 0.0 ? dt_override : cfl / s;
-  *dt = v;
-  if (dt_out) *dt_out = v;
+  *dt = dt_override > 0.0 ? dt_override : cfl / s;
 }
 
 // O11: lowest cell with rho <= 0 or p <= 0 (or NaN)
 template <int DIM>
-__global__ void __launch_bounds__(256) positivity_kernel(Geo g, const double* __restrict__ q,
-                                                         unsigned long long* __restrict__ bad) {
+__global__ void __launch_bounds__(256) positivity_kernel(Geo g, const SRef q, unsigned long long* __restrict__ bad) {
   constexpr int C = DIM + 2;
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N;
        n += (int64_t)gridDim.x * blockDim.x) {
     double U[C];
 #pragma unroll
-    for (int v = 0; v < C; ++v) U[v] = q[v * g.N + n];
+    for (int v = 0; v < C; ++v) U[v] = q.p[sidx(q, v * g.N + n)];
     const double p = pressure<DIM>(U, g.gamma - 1.0);
     if (!(U[0] > 0.0) || !(p > 0.0)) atomicMin(bad, (unsigned long long)n);
   }
@@ -201,7 +196,7 @@ __global__ void __launch_bounds__(256) positivity_kernel(Geo g, const double* __
 
 }  // namespace
 
-hrom_status launch_dt(hrom_ctx* c, const double* q, double dt_override) {
+hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override) {
   if (dt_override <= 0.0) {
     HROM_CK(cudaMemsetAsync(c->b.ureg, 0, sizeof(unsigned long long), c->st));
     const int grid = c->nsm * 8;
@@ -209,14 +204,14 @@ hrom_status launch_dt(hrom_ctx* c, const double* q, double dt_override) {
     else smax_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg);
     HROM_LAUNCH_CK();
   }
-  dt_finalize<<<1, 1, 0, c->st>>>(c->b.ureg, c->g.cfl, dt_override, c->b.dreg, nullptr);
+  dt_finalize<<<1, 1, 0, c->st>>>(c->b.ureg, c->g.cfl, dt_override, c->b.dreg);
   HROM_LAUNCH_CK();
   c->nlaunch += (dt_override <= 0.0) ? 2 : 1;
   return HROM_OK;
 }
 
-hrom_status launch_stage(hrom_ctx* c, int stage, const double* qn, const double* qin, double* out,
-                         const int32_t* list, int list_idx, double /*dt_override*/) {
+hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, const int32_t* list, int list_idx,
+                         double /*dt_override*/) {
   const int grid = c->nsm * 8;
   const int32_t* cnt = list ? c->b.counts + list_idx : nullptr;
   const Geo& g = c->g;
@@ -232,7 +227,7 @@ hrom_status launch_stage(hrom_ctx* c, int stage, const double* qn, const double*
   return HROM_OK;
 }
 
-hrom_status launch_positivity(hrom_ctx* c, const double* q) {
+hrom_status launch_positivity(hrom_ctx* c, SRef q) {
   const int grid = c->nsm * 8;
   if (c->g.dim == 1) positivity_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg + 1);
   else positivity_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg + 1);

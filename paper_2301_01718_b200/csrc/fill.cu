@@ -12,18 +12,19 @@
 // psi_prev / psi_cur are recomputed from the columns in registers: the
 // reference state is never stored or drifted.
 //
-// Register streaming: thread per DOF; all of a DOF's window loads are in flight at once
-// (coalesced 256-byte warp segments per column), the values stay in registers for their
-// second use (the Gram row) whose per-thread products accumulate in shared memory.  No
-// staging copies, no CTA barrier in the stream.
+// Data path: the ring is in slab layout (internal.cuh), so a tile -- all w+3 slab slots of
+// TILE DOFs -- is ONE contiguous run fetched by ONE cp.async.bulk (TMA) into a ring of
+// shared-memory stages by a producer warp.  NCW compute warps each own 32 DOFs of the tile
+// (one per lane), run over the slots twice (sums -> gamma_k, then the Gram row into per-lane
+// accumulators) and release the stage through an mbarrier: no CTA-wide barrier in the stream.
 #include <algorithm>
-#include <cstdlib>
 #include "internal.cuh"
 
 namespace hrom {
 namespace {
 
-constexpr int FILL_THREADS = 128;
+constexpr int NCW = TILE / 32;  // compute warps (one DOF per lane)
+constexpr int FILL_THREADS = 32 * (NCW + 1);
 
 enum { MODE_FILL = 0, MODE_READ = 1, MODE_PROJ = 2 };
 
@@ -32,50 +33,112 @@ struct FillArgs {
   Win W;
   int mode;
   int do_gram;
+  int nstage;
+  int rho_slot;            // slab slot of rho
   const double* ring;
-  const double* rho;
   const double* cvec;      // w coefficients (c = A y, or projection z)
-  const double* src_S;     // HDM values on S-hat (MODE_FILL)
-  double* out;             // gamma_k (MODE_FILL writes, MODE_READ reads)
+  SRef src_S;              // HDM values on S-hat (MODE_FILL)
+  SRef out;                // gamma_k (MODE_FILL writes, MODE_READ reads)
   const uint32_t* mS;
   const uint32_t* mB;
   double* eps_elem;
   double* part;            // [grid][nU+1]
 };
 
-__device__ __forceinline__ double ld_stream(const double* p) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
-  return v;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
-// Thread per DOF.  NU: compile-time bound of the window slots (register array of the
-// DOF's window values, kept between the two uses); the per-thread Gram-row products are
-// accumulated in shared memory (acc[s][thread]), conflict-free.
-template <int NU, bool GRAM>
-__global__ void __launch_bounds__(FILL_THREADS) fill_kernel(FillArgs a) {
-  extern __shared__ double accs[];       // [NU+1][FILL_THREADS] (GRAM only)
-  __shared__ double cs[kMaxW + 2];       // c_i, indexed by slot (0 for the psi_prev-only slot)
+// NU: compile-time upper bound of the window slots (size of the per-lane Gram accumulators)
+template <int NU>
+__global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
+  extern __shared__ __align__(128) unsigned char smraw[];
   const int nU = a.W.nU, w = a.W.w;
-  const int xoff = nU - w;  // psi_cur and X use slots >= xoff; psi_prev uses slots < w
-  const int tid = threadIdx.x;
+  const int64_t nsr = a.g.nsr;
+  double* stage0 = reinterpret_cast<double*>(smraw);
+  const size_t stage_elems = (size_t)nsr * TILE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + a.nstage * stage_elems);
+  uint64_t* empty = full + a.nstage;
+  __shared__ double cs[kMaxW];
+  __shared__ int soff[kMaxW + 2];  // stage offset of window slot s
+  __shared__ double wred[NCW][NU + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Geo& g = a.g;
-  for (int s = tid; s < nU; s += FILL_THREADS) cs[s] = (s >= xoff && a.cvec) ? a.cvec[s - xoff] : 0.0;
-  if (GRAM)
-    for (int s = 0; s <= NU; ++s) accs[s * FILL_THREADS + tid] = 0.0;
+  for (int i = tid; i < w; i += FILL_THREADS) cs[i] = a.cvec ? a.cvec[i] : 0.0;
+  for (int s = tid; s < nU; s += FILL_THREADS) soff[s] = a.W.slot[s] * TILE;
+  if (tid == 0) {
+    for (int s = 0; s < a.nstage; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   __syncthreads();
+  const int64_t ntiles = (g.D + TILE - 1) / TILE;
+  const int64_t first = blockIdx.x;
+  const uint32_t tile_bytes = (uint32_t)(stage_elems * sizeof(double));
+
+  if (warp == NCW) {
+    // ---------------- producer warp: one bulk copy per slab tile ----------------
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % a.nstage;
+        if (it >= a.nstage) mbar_wait(&empty[st], (uint32_t)(((it / a.nstage) - 1) & 1));
+        mbar_expect(&full[st], tile_bytes);
+        bulk_g2s(stage0 + st * stage_elems, a.ring + tile * stage_elems, tile_bytes, &full[st]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- compute warps: lane = DOF ----------------
   double csum = 0.0;
-  for (int s = xoff; s < nU; ++s) csum += cs[s];
+  for (int i = 0; i < w; ++i) csum += cs[i];
   const double inv_w = 1.0 / (double)w;
-  const int64_t stride = (int64_t)gridDim.x * FILL_THREADS;
-  // per-DOF side data (mask words, HDM value / new column) is fetched one iteration ahead
+  const int xoff = nU - w;  // psi_cur and X use slots >= xoff; psi_prev uses slots < w
+  const int roff = a.rho_slot * TILE;
+  double acc[NU];
+#pragma unroll
+  for (int s = 0; s < NU; ++s) acc[s] = 0.0;
+  double acc_self = 0.0;
+  const int el = warp * 32 + lane;
+  // per-DOF side data (mask words, HDM value / new column) is fetched one tile ahead
   uint32_t wS = 0, wB = 0;
   int bitpos = 0;
   double pre = 0.0;
-  auto fetch = [&](int64_t e) {
+  auto fetch = [&](int64_t tile) {
+    const int64_t e = tile * TILE + el;
     wS = wB = 0;
     pre = 0.0;
-    if (e < g.D && a.mode != MODE_PROJ) {
+    if (tile < ntiles && e < g.D && a.mode != MODE_PROJ) {
       const int64_t n = e % g.N;
       const int i = (int)(n % g.nx), j = (int)(n / g.nx);
       const int64_t wi = (int64_t)j * g.wpr + (i >> 5);
@@ -83,84 +146,108 @@ __global__ void __launch_bounds__(FILL_THREADS) fill_kernel(FillArgs a) {
       if (a.mode == MODE_FILL) {
         wS = a.mS[wi];
         if (a.mB) wB = a.mB[wi];
-        pre = a.src_S[e];  // read unconditionally (allocated everywhere); used on S-hat only
+        pre = a.src_S.p[sidx(a.src_S, e)];  // read unconditionally; used on S-hat only
       } else {
-        pre = a.out[e];
+        pre = a.out.p[sidx(a.out, e)];
       }
     }
   };
-  int64_t e = (int64_t)blockIdx.x * FILL_THREADS + tid;
-  fetch(e);
-  for (; e < g.D; e += stride) {
-    // all window loads of this DOF in flight together
-    double x[NU];
-#pragma unroll
-    for (int s = 0; s < NU; ++s)
-      if (s < nU) x[s] = ld_stream(a.ring + (int64_t)a.W.slot[s] * g.Dp + e);
-    const double rh = ld_stream(a.rho + e);
+  fetch(first);
+  int it = 0;
+  for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it % a.nstage;
+    const int64_t e = tile * TILE + el;
+    const bool valid = e < g.D;
     const bool inS = (wS >> bitpos) & 1u, inB = (wB >> bitpos) & 1u;
     const double side = pre;
-    fetch(e + stride);
+    fetch(tile + gridDim.x);
+    mbar_wait(&full[st], (uint32_t)((it / a.nstage) & 1));
+    const double* T = stage0 + st * stage_elems + el;
+    const double rh = T[roff];
     // pass 1 (x_s = gamma_s - rho): sp = sum_{s<w} x_s, sc = sum_{s>=xoff} x_s,
     //                                tr = sum_{s>=xoff} c_{s-xoff} x_s  (two chains each)
     double sp = 0.0, sc = 0.0, tr = 0.0, sp2 = 0.0, sc2 = 0.0, tr2 = 0.0;
-#pragma unroll
-    for (int s = 0; s < NU; ++s) {
-      if (s < nU) {
-        x[s] -= rh;
-        if (s & 1) {
-          if (s < w) sp2 += x[s];
-          if (s >= xoff) sc2 += x[s];
-          tr2 += cs[s] * x[s];
-        } else {
-          if (s < w) sp += x[s];
-          if (s >= xoff) sc += x[s];
-          tr += cs[s] * x[s];
-        }
-      }
+    if (xoff == 1) sp = T[soff[0]] - rh;
+    int s = xoff;
+#pragma unroll 4
+    for (; s + 1 < w; s += 2) {
+      const double x = T[soff[s]] - rh, x2 = T[soff[s + 1]] - rh;
+      sp += x;
+      sc += x;
+      tr += cs[s - xoff] * x;
+      sp2 += x2;
+      sc2 += x2;
+      tr2 += cs[s + 1 - xoff] * x2;
+    }
+    if (s < w) {
+      const double x = T[soff[s]] - rh;
+      sp += x;
+      sc += x;
+      tr += cs[s - xoff] * x;
+    }
+    if (xoff == 1) {
+      const double x = T[soff[w]] - rh;
+      sc2 += x;
+      tr2 += cs[w - 1] * x;
     }
     sp += sp2;
     sc += sc2;
     tr += tr2;
     double gval = 0.0;
-    // psi_prev - rho = sp/w, psi_cur - rho = sc/w;  Phi y = sum_i c_i (x_i - (psi_prev - rho))
-    const double dev = tr - (sp * inv_w) * csum;
-    if (a.mode == MODE_FILL) {
-      const double rec = (rh + sc * inv_w) + dev;
-      gval = inS ? side : rec;
-      if (inS) {
-        const double d = gval - rec;
-        a.eps_elem[e] = d * d;
+    if (valid) {
+      // psi_prev - rho = sp/w, psi_cur - rho = sc/w;  Phi y = sum_i c_i (x_i - (psi_prev - rho))
+      const double dev = tr - (sp * inv_w) * csum;
+      if (a.mode == MODE_FILL) {
+        const double rec = (rh + sc * inv_w) + dev;
+        if (inS) {
+          gval = side;
+          const double d = gval - rec;
+          a.eps_elem[e] = d * d;
+        } else {
+          gval = rec;
+        }
+        a.out.p[sidx(a.out, e)] = gval;
+      } else if (a.mode == MODE_READ) {
+        gval = side;
+      } else {  // MODE_PROJ: residual of the projection onto the basis (bootstrap indicator)
+        a.eps_elem[e] = dev * dev;
       }
-      a.out[e] = gval;
-    } else if (a.mode == MODE_READ) {
-      gval = side;
-    } else {  // MODE_PROJ: residual of the projection onto the basis (bootstrap indicator)
-      a.eps_elem[e] = dev * dev;
     }
-    // pass 2: new Gram row (band DOFs are added after the filter)
-    if (GRAM && !inB) {
+    // pass 2: new Gram row, per-lane accumulators (band DOFs are added after the filter)
+    if (a.do_gram && valid && !inB) {
       const double gr = gval - rh;
+      acc_self += gr * gr;
 #pragma unroll
-      for (int s = 0; s < NU; ++s)
-        if (s < nU) accs[s * FILL_THREADS + tid] += gr * x[s];
-      accs[NU * FILL_THREADS + tid] += gr * gr;
+      for (int q = 0; q < NU; ++q)
+        if (q < nU) acc[q] += gr * (T[soff[q]] - rh);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
   }
-  if (!GRAM) return;
-  // fixed-order reduction over the block's threads -> part[block][*]
-  __syncthreads();
-  double* outp = a.part + (int64_t)blockIdx.x * (nU + 1);
-  for (int s = tid / 32; s <= nU; s += FILL_THREADS / 32) {
-    const int row = (s == nU) ? NU : s;
-    double v = 0.0;
-    for (int t = tid & 31; t < FILL_THREADS; t += 32) v += accs[row * FILL_THREADS + t];
+  if (!a.do_gram) return;
+  // fixed-order reductions: lanes (shuffle tree), then the compute warps -> part[block][*]
+#pragma unroll
+  for (int q = 0; q < NU; ++q) {
+    double v = acc[q];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((tid & 31) == 0) outp[s] = v;
+    if (lane == 0 && q < nU) wred[warp][q] = v;
+  }
+  {
+    double v = acc_self;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) wred[warp][NU] = v;
+  }
+  asm volatile("bar.sync 1, %0;\n" ::"r"(32 * NCW));  // compute warps only
+  double* outp = a.part + (int64_t)blockIdx.x * (nU + 1);
+  for (int q = warp * 32 + lane; q <= nU; q += 32 * NCW) {
+    const int idx = (q == nU) ? NU : q;
+    double v = 0.0;
+    for (int k = 0; k < NCW; ++k) v += wred[k][idx];
+    outp[q] = v;
   }
 }
 
-// C[new][U[s]] = sum over blocks of fill partials (+ band partials), fixed order
+// C[new][U[s]] = sum over blocks of fill partials, fixed order
 __global__ void gram_row_reduce(const double* __restrict__ part, int nblk, Win W, int new_slot,
                                 double* __restrict__ C, int ldc) {
   const int nU = W.nU;
@@ -173,6 +260,20 @@ __global__ void gram_row_reduce(const double* __restrict__ part, int nblk, Win W
     } else {
       C[new_slot * ldc + new_slot] = acc;
     }
+  }
+}
+
+// band partials added into the same C entries (fixed order, after the fill part)
+__global__ void band_row_add(const double* __restrict__ part, int nblk, Win W, int new_slot, double* __restrict__ C,
+                             int ldc) {
+  const int nU = W.nU;
+  for (int s = threadIdx.x; s <= nU; s += blockDim.x) {
+    double acc = 0.0;
+    for (int b = 0; b < nblk; ++b) acc += part[(int64_t)b * (nU + 1) + s];
+    const int cs_ = (s < nU) ? W.slot[s] : new_slot;
+    const double v = C[new_slot * ldc + cs_] + acc;
+    C[new_slot * ldc + cs_] = v;
+    C[cs_ * ldc + new_slot] = v;
   }
 }
 
@@ -196,44 +297,44 @@ __global__ void eps_all_kernel(Geo g, const double* __restrict__ eps_elem, doubl
   }
 }
 
-// rho (or psi) = mean of the last w window slots
-__global__ void mean_kernel(Geo g, Win W, const double* __restrict__ ring, double* __restrict__ out) {
+// out (rho or psi) = mean of the last w window slots
+__global__ void mean_kernel(Geo g, Win W, const double* __restrict__ ring, SRef out) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < g.D; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t se = sidx(SRef{nullptr, g.nsr}, e);
     double s = 0.0;
-    for (int q = W.nU - W.w; q < W.nU; ++q) s += ring[(int64_t)W.slot[q] * g.Dp + e];
-    out[e] = s / (double)W.w;
+    for (int q = W.nU - W.w; q < W.nU; ++q) s += ring[(int64_t)W.slot[q] * TILE + se];
+    out.p[sidx(out, e)] = s / (double)W.w;
   }
 }
 
-template <int NU, bool GRAM>
-hrom_status launch_fill_t(hrom_ctx* c, const FillArgs& a) {
-  const size_t smem = GRAM ? (size_t)(NU + 1) * FILL_THREADS * sizeof(double) : 0;
-  HROM_CK(cudaFuncSetAttribute(fill_kernel<NU, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fill_kernel<NU, GRAM>, FILL_THREADS, smem);
-  const int grid = std::min(c->fill_blocks, c->nsm * std::max(occ, 1));
-  fill_kernel<NU, GRAM><<<grid, FILL_THREADS, smem, c->st>>>(a);
+template <int NU>
+hrom_status launch_fill_t(hrom_ctx* c, const FillArgs& a, size_t smem) {
+  HROM_CK(cudaFuncSetAttribute(fill_kernel<NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fill_kernel<NU><<<c->nsm, FILL_THREADS, smem, c->st>>>(a);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
-  c->fill_grid = grid;
+  c->fill_grid = c->nsm;
   return HROM_OK;
 }
 
 }  // namespace
 
 int fill_max_gram_slots() { return 68; }
-hrom_status reduce_band_rows(hrom_ctx* c, const Win& W, int new_slot);
 
-hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S, double* out, int /*out_slot*/) {
+hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef out, bool out_in_ring) {
   FillArgs a{};
   a.g = c->g;
   a.W = W;
   a.mode = mode;
-  a.do_gram = (mode != MODE_PROJ) && out != nullptr && c->P.gram_mode == 0 ? 1 : 0;
-  if (mode == MODE_FILL && out != nullptr && !(out >= c->b.ring && out < c->b.ring + (int64_t)c->nslots * c->g.Dp))
-    a.do_gram = 0;  // standalone reconstruct into a caller buffer: no window Gram
+  a.do_gram = (mode != MODE_PROJ) && out_in_ring && c->P.gram_mode == 0 ? 1 : 0;
+  // stages of one slab tile each (nsr KB), as many as fit (<= 4)
+  const size_t stage = (size_t)c->g.nsr * TILE * sizeof(double);
+  const size_t budget = 224 * 1024 - 4 * 1024;
+  a.nstage = (int)std::min<size_t>(4, budget / (stage + 16));
+  if (a.nstage < 1) return HROM_E_INVALID;
+  const size_t smem = a.nstage * stage + 2 * a.nstage * sizeof(uint64_t);
+  a.rho_slot = c->nslots;
   a.ring = c->b.ring;
-  a.rho = c->b.rho;
   a.cvec = (mode == MODE_PROJ) ? c->b.zvec : c->b.cvec;
   a.src_S = src_S;
   a.out = out;
@@ -241,55 +342,29 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S
   a.mB = (mode == MODE_FILL) ? c->b.masks + (int64_t)M_B * c->mwords : nullptr;
   a.eps_elem = c->b.eps_elem;
   a.part = c->b.gpart;
-  if (a.do_gram) {
-    if (W.nU <= 12) return launch_fill_t<12, true>(c, a);
-    if (W.nU <= 24) return launch_fill_t<24, true>(c, a);
-    if (W.nU <= 36) return launch_fill_t<36, true>(c, a);
-    if (W.nU <= 52) return launch_fill_t<52, true>(c, a);
-    if (W.nU <= 68) return launch_fill_t<68, true>(c, a);
-    return HROM_E_INVALID;  // wider windows with a Gram row use gram_mode = 1 (hrom_create)
-  }
-  if (W.nU <= 12) return launch_fill_t<12, false>(c, a);
-  if (W.nU <= 24) return launch_fill_t<24, false>(c, a);
-  if (W.nU <= 36) return launch_fill_t<36, false>(c, a);
-  if (W.nU <= 68) return launch_fill_t<68, false>(c, a);
-  if (W.nU <= 100) return launch_fill_t<100, false>(c, a);
-  if (W.nU <= 132) return launch_fill_t<132, false>(c, a);
-  return HROM_E_INVALID;
+  if (!a.do_gram) return launch_fill_t<1>(c, a, smem);
+  if (W.nU <= 12) return launch_fill_t<12>(c, a, smem);
+  if (W.nU <= 24) return launch_fill_t<24>(c, a, smem);
+  if (W.nU <= 36) return launch_fill_t<36>(c, a, smem);
+  if (W.nU <= 52) return launch_fill_t<52>(c, a, smem);
+  if (W.nU <= 68) return launch_fill_t<68>(c, a, smem);
+  return HROM_E_INVALID;  // wider windows use gram_mode = 1 (hrom_create enforces it)
 }
 
 hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot) {
-  return launch_fill(c, W, MODE_READ, nullptr, c->b.ring + (int64_t)new_slot * c->g.Dp, new_slot);
+  return launch_fill(c, W, MODE_READ, plain(nullptr), c->slot_ref(new_slot), true);
 }
 
 hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_band) {
-  // fill partials occupy blocks [0, fill_grid); band partials follow at offset fill_blocks
   gram_row_reduce<<<1, 256, 0, c->st>>>(c->b.gpart, c->fill_grid, W, new_slot, c->b.C, kMaxSlots);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
-  // band partials are added into the same C entries (fixed order, after the fill part)
-  if (with_band) return reduce_band_rows(c, W, new_slot);
-  return HROM_OK;
-}
-
-__global__ void band_row_add(const double* __restrict__ part, int nblk, Win W, int new_slot, double* __restrict__ C,
-                             int ldc) {
-  const int nU = W.nU;
-  for (int s = threadIdx.x; s <= nU; s += blockDim.x) {
-    double acc = 0.0;
-    for (int b = 0; b < nblk; ++b) acc += part[(int64_t)b * (nU + 1) + s];
-    const int cs_ = (s < nU) ? W.slot[s] : new_slot;
-    const double v = C[new_slot * ldc + cs_] + acc;
-    C[new_slot * ldc + cs_] = v;
-    C[cs_ * ldc + new_slot] = v;
+  if (with_band) {
+    band_row_add<<<1, 256, 0, c->st>>>(c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1), c->band_blocks, W,
+                                        new_slot, c->b.C, kMaxSlots);
+    HROM_LAUNCH_CK();
+    ++c->nlaunch;
   }
-}
-
-hrom_status reduce_band_rows(hrom_ctx* c, const Win& W, int new_slot) {
-  band_row_add<<<1, 256, 0, c->st>>>(c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1), c->band_blocks, W, new_slot,
-                                      c->b.C, kMaxSlots);
-  HROM_LAUNCH_CK();
-  ++c->nlaunch;
   return HROM_OK;
 }
 
@@ -308,7 +383,7 @@ hrom_status launch_eps_all(hrom_ctx* c) {
   return HROM_OK;
 }
 
-hrom_status launch_mean(hrom_ctx* c, const Win& W, double* out) {
+hrom_status launch_mean(hrom_ctx* c, const Win& W, SRef out) {
   mean_kernel<<<c->nsm * 8, 256, 0, c->st>>>(c->g, W, c->b.ring, out);
   HROM_LAUNCH_CK();
   ++c->nlaunch;

@@ -23,8 +23,8 @@ struct FilterArgs {
   const int32_t* list;   // band cells
   const int32_t* count;
   const uint32_t* mB;
-  double* v;             // gamma_k (in place)
-  const double* F;       // full-step values on B
+  SRef v;                // gamma_k (in place)
+  SRef F;                // full-step values on B
   double* Vp;
   double* Vpp;
   double* Vorig;
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(256) filter_kernel(FilterArgs a) {
   __shared__ int scnt[8];
   for (int64_t t = gtid; t < nb; t += gstride) {
     const int64_t n = a.list[t];
-    for (int var = 0; var < g.c; ++var) a.Vorig[var * g.N + n] = a.v[var * g.N + n];
+    for (int var = 0; var < g.c; ++var) a.Vorig[var * g.N + n] = a.v.p[sidx(a.v, var * g.N + n)];
     a.kept[n] = 0;
   }
   grid.sync();
@@ -85,9 +85,9 @@ __global__ void __launch_bounds__(256) filter_kernel(FilterArgs a) {
         const int i = (int)(n % g.nx), j = (int)(n / g.nx);
         const int64_t row = (int64_t)j * g.nx;
         for (int var = 0; var < g.c; ++var) {
-          const double* vv = a.v + var * g.N + row;
+          const int64_t rb = var * g.N + row;
           double s = 0.0;
-          for (int m = -rad; m <= rad; ++m) s += cf[m + rad] * vv[wrapf(i + m, g.nx, g.bc)];
+          for (int m = -rad; m <= rad; ++m) s += cf[m + rad] * a.v.p[sidx(a.v, rb + wrapf(i + m, g.nx, g.bc))];
           a.Vp[var * g.N + n] = s / den;
         }
       }
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(256) filter_kernel(FilterArgs a) {
             for (int m = -rad; m <= rad; ++m) {
               const int jj = wrapf(j + m, g.ny, g.bc);
               const int64_t nn = (int64_t)jj * g.nx + i;
-              const double val = bitB(a.mB, g, i, jj) ? a.Vp[var * g.N + nn] : a.v[var * g.N + nn];
+              const double val = bitB(a.mB, g, i, jj) ? a.Vp[var * g.N + nn] : a.v.p[sidx(a.v, var * g.N + nn)];
               s += cf[m + rad] * val;
             }
             x = s / den;
@@ -116,8 +116,9 @@ __global__ void __launch_bounds__(256) filter_kernel(FilterArgs a) {
             x = a.Vp[e];
           }
           vpp[var] = x;
-          rold = fmax(rold, fabs(a.v[e] - a.F[e]));
-          rnew = fmax(rnew, fabs(x - a.F[e]));
+          const double fe = a.F.p[sidx(a.F, e)];
+          rold = fmax(rold, fabs(a.v.p[sidx(a.v, e)] - fe));
+          rnew = fmax(rnew, fabs(x - fe));
         }
         if (rnew < rold) {
           for (int var = 0; var < g.c; ++var) a.Vpp[var * g.N + n] = vpp[var];
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(256) filter_kernel(FilterArgs a) {
       for (int64_t t = gtid; t < nb; t += gstride) {
         const int64_t n = a.list[t];
         if (a.kept[n] & 2) {
-          for (int var = 0; var < g.c; ++var) a.v[var * g.N + n] = a.Vpp[var * g.N + n];
+          for (int var = 0; var < g.c; ++var) a.v.p[sidx(a.v, var * g.N + n)] = a.Vpp[var * g.N + n];
           a.kept[n] = 1;
         }
       }
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(256) filter_kernel(FilterArgs a) {
     if (a.kept[n] & 1) {
       double s = 0.0;
       for (int var = 0; var < g.c; ++var) {
-        const double d = a.v[var * g.N + n] - a.Vorig[var * g.N + n];
+        const double d = a.v.p[sidx(a.v, var * g.N + n)] - a.Vorig[var * g.N + n];
         s += d * d;
       }
       if (a.eps) a.eps[n] = s;
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(256) filter_kernel(FilterArgs a) {
 
 // Gram-row contributions of the band DOFs (final values), partials after the fill blocks
 __global__ void __launch_bounds__(256) band_gram_kernel(Geo g, Win W, const double* __restrict__ ring,
-                                                        const double* __restrict__ rho, const double* __restrict__ v,
+                                                        const SRef rho, const SRef v,
                                                         const int32_t* __restrict__ list,
                                                         const int32_t* __restrict__ count, double* __restrict__ part) {
   constexpr int CH = 128;
@@ -203,11 +204,11 @@ __global__ void __launch_bounds__(256) band_gram_kernel(Geo g, Win W, const doub
       if (t < total) {
         const int var = (int)(t / nb), idx = (int)(t % nb);
         const int64_t e = (int64_t)var * g.N + list[idx];
-        const double r = rho[e];
-        const double x = v[e] - r;
+        const double r = rho.p[sidx(rho, e)];
+        const double x = v.p[sidx(v, e)] - r;
         gt[threadIdx.x] = x;
         rh[threadIdx.x] = r;
-        es[threadIdx.x] = e;
+        es[threadIdx.x] = sidx(SRef{nullptr, g.nsr}, e);  // slab offset within a ring slot
         self += x * x;
       } else {
         gt[threadIdx.x] = 0.0;
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(256) band_gram_kernel(Geo g, Win W, const doub
     for (int q = 0; q < SPW; ++q) {
       const int s = warp + q * 8;
       if (s < nU) {
-        const double* col = ring + (int64_t)W.slot[s] * g.Dp;
+        const double* col = ring + (int64_t)W.slot[s] * TILE;
         double sacc = 0.0;
         for (int el = lane; el < CH; el += 32)
           if (es[el] >= 0) sacc += gt[el] * (col[es[el]] - rh[el]);
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(256) band_gram_kernel(Geo g, Win W, const doub
 
 }  // namespace
 
-hrom_status launch_filter(hrom_ctx* c, double* v, const double* F) {
+hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F) {
   FilterArgs a{};
   a.g = c->g;
   for (int i = 0; i < 3; ++i) a.orders[i] = c->P.filter_orders[i];
@@ -275,8 +276,8 @@ hrom_status launch_filter(hrom_ctx* c, double* v, const double* F) {
   return HROM_OK;
 }
 
-hrom_status launch_band_gram(hrom_ctx* c, const Win& W, const double* v) {
-  band_gram_kernel<<<c->band_blocks, 256, 0, c->st>>>(c->g, W, c->b.ring, c->b.rho, v,
+hrom_status launch_band_gram(hrom_ctx* c, const Win& W, SRef v) {
+  band_gram_kernel<<<c->band_blocks, 256, 0, c->st>>>(c->g, W, c->b.ring, c->rho_ref(), v,
                                                        c->b.lists + (int64_t)L_B * c->g.N, c->b.counts + L_B,
                                                        c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1));
   HROM_LAUNCH_CK();

@@ -27,6 +27,22 @@
 
 namespace hrom {
 
+// Slab layout of the snapshot ring: DOFs are grouped in tiles of TILE; tile t
+// of slot s lives at ring[(t * NSR + s) * TILE ..], NSR = w + 3 (w + 2 snapshot slots and the
+// Gram shift rho).  One fill tile -- every window column of TILE DOFs -- is therefore ONE
+// contiguous (w+3) KB run: a single TMA bulk copy (measured 7.3 TB/s vs 4.9 TB/s for w+2
+// separate 1 KB copies).  A plain vector is the same layout with NSR = 1.
+constexpr int TILE = 128;
+constexpr int TILE_SHIFT = 7;
+struct SRef {
+  double* p;   // base (ring + slot * TILE for a ring slot)
+  int64_t ns;  // slots per slab tile (1 for a plain vector)
+};
+__host__ __device__ __forceinline__ int64_t sidx(const SRef& r, int64_t e) {
+  return (((e >> TILE_SHIFT) * r.ns) << TILE_SHIFT) + (e & (TILE - 1));
+}
+__host__ __device__ __forceinline__ SRef plain(const double* p) { return SRef{const_cast<double*>(p), 1}; }
+
 constexpr int kMaxW = 128;           // largest window supported (config 5)
 constexpr int kMaxSlots = kMaxW + 2; // ring slots
 constexpr int kMaxR = 64;
@@ -34,7 +50,8 @@ constexpr int kMaxR = 64;
 // Geometry passed by value to kernels.
 struct Geo {
   int dim, nx, ny, c, bc, recon, wpr;  // wpr = mask words per row
-  int64_t N, D, Dp;                    // Dp: padded slot stride (multiple of 32 doubles)
+  int64_t N, D, Dp;                    // Dp: D rounded up to a multiple of TILE
+  int64_t nsr;                         // slab slots per tile (w + 3)
   double dx, dy, gamma, cfl;
 };
 
@@ -51,8 +68,8 @@ enum { M_S = 0, M_B, M_T, M_A2, M_A1, M_TMP, M_TMP2, M_KEEP, M_COUNT };
 enum { L_S = 0, L_B, L_T, L_A2, L_A1, L_COUNT };
 
 struct Bufs {
-  double* ring = nullptr;     // nslots * Dp
-  double* rho = nullptr;      // Dp
+  double* ring = nullptr;     // slab: (Dp / TILE) tiles x nsr slots x TILE
+  double* rho = nullptr;      // = ring + nslots * TILE (slab slot nslots)
   double* U1 = nullptr;       // Dp (stage outputs / filter scratch)
   double* U2 = nullptr;
   double* U3 = nullptr;
@@ -127,6 +144,8 @@ struct hrom_ctx {
   cudaEvent_t ev_basis_in = nullptr, ev_basis_done = nullptr;
   bool basis_pending = false;
   int slot_of(int64_t kk) const { return (int)(kk % nslots); }
+  hrom::SRef slot_ref(int s) const { return hrom::SRef{b.ring + (int64_t)s * hrom::TILE, g.nsr}; }
+  hrom::SRef rho_ref() const { return hrom::SRef{b.rho, g.nsr}; }
 };
 
 namespace hrom {
@@ -156,29 +175,29 @@ inline void prof_end(hrom_ctx* c, int sec) {
 
 namespace hrom {
 // euler.cu
-hrom_status launch_dt(hrom_ctx* c, const double* q, double dt_override);
-hrom_status launch_stage(hrom_ctx* c, int stage, const double* qn, const double* qin, double* out,
-                         const int32_t* list, int list_idx, double dt_override);
-hrom_status launch_positivity(hrom_ctx* c, const double* q);
+hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override);
+hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, const int32_t* list, int list_idx,
+                         double dt_override);
+hrom_status launch_positivity(hrom_ctx* c, SRef q);
 // masks.cu
 hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S);
 hrom_status select_topn(hrom_ctx* c, const double* eps, int64_t n_g);
 hrom_status compact_masks(hrom_ctx* c, const int* which, int nwhich);
 // linalg.cu
-hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int ncol, int64_t rows,
-                      const double* rho, double* dev_C, int ldc, const int32_t* map);
-hrom_status gram_gathered(hrom_ctx* c, const double* src_b);
+// dev_cols: column base pointers, all with slab stride ns (1 = plain vectors); rho: SRef or p == nullptr
+hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int64_t ns, int ncol, int64_t rows, SRef rho,
+                      double* dev_C, int ldc, const int32_t* map);
+hrom_status gram_gathered(hrom_ctx* c, SRef src_b);
 hrom_status small_solve(hrom_ctx* c);
 hrom_status basis_from_gram(hrom_ctx* c, const Win& W);
 hrom_status lift(hrom_ctx* c, const Win& W, double* phi, double* psi);
 // fill.cu
-hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, const double* src_S, double* out,
-                        int out_slot);
+hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef out, bool out_in_ring);
 hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot);
 hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_band);
 hrom_status launch_eps_cells(hrom_ctx* c);
-hrom_status launch_mean(hrom_ctx* c, const Win& W, double* out);
+hrom_status launch_mean(hrom_ctx* c, const Win& W, SRef out);
 // filter.cu
-hrom_status launch_filter(hrom_ctx* c, double* v, const double* F);
-hrom_status launch_band_gram(hrom_ctx* c, const Win& W, const double* v);
+hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F);
+hrom_status launch_band_gram(hrom_ctx* c, const Win& W, SRef v);
 }  // namespace hrom

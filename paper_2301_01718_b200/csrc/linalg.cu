@@ -28,14 +28,15 @@ struct GramArgs {
   int nsb;                   // super blocks (16 columns each)
   int64_t rows;              // contiguous rows (mode 0)
   const double* const* cols; // mode 0: column pointers
-  const double* rho;         // mode 0: shift (nullable)
+  int64_t ns;                // mode 0: slab stride of the columns (1 = plain)
+  SRef rho;                  // mode 0: shift (rho.p nullable)
   // mode 1
   Geo g;
   Win W;
   const double* ring;
   const int32_t* list;       // S-hat cells
   const int32_t* count;      // |S-hat|
-  const double* src_b;       // HDM values on S-hat rows
+  SRef src_b;                // HDM values on S-hat rows
   double* part;              // [grid][nsb*16][nsb*16]
 };
 
@@ -90,8 +91,8 @@ __global__ void __launch_bounds__(GT) gram_kernel(GramArgs a) {
         const int64_t row = r0 + k;
         double v = 0.0;
         if (col < a.ncol && row < total_rows) {
-          v = a.cols[col][row];
-          if (a.rho) v -= a.rho[row];
+          v = a.cols[col][sidx(SRef{nullptr, a.ns}, row)];
+          if (a.rho.p) v -= a.rho.p[sidx(a.rho, row)];
         }
         tile[col * LDT + k] = v;
       }
@@ -126,7 +127,9 @@ __global__ void __launch_bounds__(GT) gram_kernel(GramArgs a) {
           if (idx < total) {
             const int s = idx / RT, k = idx % RT;
             const int64_t e = erow[k];
-            if (e >= 0) v = (s < nU) ? __ldg(a.ring + (int64_t)a.W.slot[s] * a.g.Dp + e) : __ldg(a.src_b + e);
+            if (e >= 0)
+              v = (s < nU) ? __ldg(a.ring + (int64_t)a.W.slot[s] * TILE + sidx(SRef{nullptr, a.g.nsr}, e))
+                           : __ldg(a.src_b.p + sidx(a.src_b, e));
           }
           vbuf[q] = v;
         }
@@ -446,15 +449,16 @@ __global__ void lift_kernel(Geo g, Win W, const double* __restrict__ ring, const
   const int re = *reffp;
   const int w = W.w, nU = W.nU;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < g.D; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t se = sidx(SRef{nullptr, g.nsr}, e);
     double sp = 0.0, sc = 0.0;
-    for (int s = 0; s < w; ++s) sp += ring[(int64_t)W.slot[s] * g.Dp + e];
-    for (int s = nU - w; s < nU; ++s) sc += ring[(int64_t)W.slot[s] * g.Dp + e];
+    for (int s = 0; s < w; ++s) sp += ring[(int64_t)W.slot[s] * TILE + se];
+    for (int s = nU - w; s < nU; ++s) sc += ring[(int64_t)W.slot[s] * TILE + se];
     const double pp = sp / (double)w;
     if (psi) psi[e] = sc / (double)w;
     if (phi)
       for (int j = 0; j < re; ++j) {
         double acc = 0.0;
-        for (int i = 0; i < w; ++i) acc += (ring[(int64_t)W.slot[nU - w + i] * g.Dp + e] - pp) * A[j * w + i];
+        for (int i = 0; i < w; ++i) acc += (ring[(int64_t)W.slot[nU - w + i] * TILE + se] - pp) * A[j * w + i];
         phi[(int64_t)j * g.D + e] = acc;
       }
   }
@@ -484,7 +488,7 @@ hrom_status dispatch_gram(hrom_ctx* c, GramArgs a, int grid) {
 }  // namespace
 
 // Full Gram of ncol columns over `rows` rows, shifted by rho (nullable): dev_C[i*ldc+j].
-hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int ncol, int64_t rows, const double* rho,
+hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int64_t ns, int ncol, int64_t rows, SRef rho,
                       double* dev_C, int ldc, const int32_t* map) {
   GramArgs a{};
   a.mode = 0;
@@ -492,6 +496,7 @@ hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int ncol, int6
   a.nsb = (ncol + 15) / 16;
   a.rows = rows;
   a.cols = dev_cols;
+  a.ns = ns;
   a.rho = rho;
   const int grid = c->nsm * 2;
   const int ncp = a.nsb * 16;
@@ -506,7 +511,7 @@ hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int ncol, int6
 }
 
 // gathered Gram of [X_S, b] over the rows of S-hat -> b.K ((w+1) x (w+1))
-hrom_status gram_gathered(hrom_ctx* c, const double* src_b) {
+hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   GramArgs a{};
   a.mode = 1;
   a.ncol = c->win.w + 1;
