@@ -23,8 +23,9 @@
 namespace hrom {
 namespace {
 
-constexpr int NCW = TILE / 32;  // compute warps (one DOF per lane)
-constexpr int FILL_THREADS = 32 * (NCW + 1);
+constexpr int NCW = TILE / 32;  // compute warps per group (one DOF per lane)
+constexpr int NCG = 2;          // compute groups (each consumes every NCG-th tile)
+constexpr int FILL_THREADS = 32 * (NCG * NCW + 1);
 
 enum { MODE_FILL = 0, MODE_READ = 1, MODE_PROJ = 2 };
 
@@ -34,6 +35,7 @@ struct FillArgs {
   int mode;
   int do_gram;
   int nstage;
+  int nslots;              // physical snapshot slots (w + 2)
   int rho_slot;            // slab slot of rho
   const double* ring;
   const double* cvec;      // w coefficients (c = A y, or projection z)
@@ -76,27 +78,34 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// NU: compile-time upper bound of the window slots (size of the per-lane Gram accumulators)
-template <int NU>
+// NSL: compile-time upper bound of the physical ring slots (w + 2; per-lane Gram accumulators)
+template <int NSL>
 __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
-  const int nU = a.W.nU, w = a.W.w;
+  const int nU = a.W.nU, w = a.W.w, nsl = a.nslots;
   const int64_t nsr = a.g.nsr;
   double* stage0 = reinterpret_cast<double*>(smraw);
   const size_t stage_elems = (size_t)nsr * TILE;
   uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + a.nstage * stage_elems);
   uint64_t* empty = full + a.nstage;
-  __shared__ double cs[kMaxW];
-  __shared__ int soff[kMaxW + 2];  // stage offset of window slot s
-  __shared__ double wred[NCW][NU + 1];
+  // per PHYSICAL slot p: membership of psi_prev (cP), of psi_cur (cC), coefficient c (cX)
+  __shared__ double cP[kMaxSlots], cC[kMaxSlots], cX[kMaxSlots];
+  __shared__ double wred[NCG * NCW][NSL + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Geo& g = a.g;
-  for (int i = tid; i < w; i += FILL_THREADS) cs[i] = a.cvec ? a.cvec[i] : 0.0;
-  for (int s = tid; s < nU; s += FILL_THREADS) soff[s] = a.W.slot[s] * TILE;
+  const int xoff = nU - w;  // logical: psi_cur and X use slots >= xoff; psi_prev uses slots < w
+  for (int q = tid; q < nsl; q += FILL_THREADS) cP[q] = cC[q] = cX[q] = 0.0;
+  __syncthreads();
+  for (int s = tid; s < nU; s += FILL_THREADS) {
+    const int q = a.W.slot[s];
+    cP[q] = (s < w) ? 1.0 : 0.0;
+    cC[q] = (s >= xoff) ? 1.0 : 0.0;
+    cX[q] = (s >= xoff && a.cvec) ? a.cvec[s - xoff] : 0.0;
+  }
   if (tid == 0) {
-    for (int s = 0; s < a.nstage; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCW);
+    for (int q = 0; q < a.nstage; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -105,7 +114,7 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   const int64_t first = blockIdx.x;
   const uint32_t tile_bytes = (uint32_t)(stage_elems * sizeof(double));
 
-  if (warp == NCW) {
+  if (warp == NCG * NCW) {
     // ---------------- producer warp: one bulk copy per slab tile ----------------
     if (lane == 0) {
       int it = 0;
@@ -119,17 +128,17 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     return;
   }
 
-  // ---------------- compute warps: lane = DOF ----------------
+  // ---------------- compute groups (NCG x NCW warps): lane = DOF; group grp takes every NCG-th tile
+  const int grp = warp / NCW;
   double csum = 0.0;
-  for (int i = 0; i < w; ++i) csum += cs[i];
+  for (int q = 0; q < nsl; ++q) csum += cX[q];
   const double inv_w = 1.0 / (double)w;
-  const int xoff = nU - w;  // psi_cur and X use slots >= xoff; psi_prev uses slots < w
   const int roff = a.rho_slot * TILE;
-  double acc[NU];
+  double acc[NSL];
 #pragma unroll
-  for (int s = 0; s < NU; ++s) acc[s] = 0.0;
+  for (int q = 0; q < NSL; ++q) acc[q] = 0.0;
   double acc_self = 0.0;
-  const int el = warp * 32 + lane;
+  const int el = (warp % NCW) * 32 + lane;
   // per-DOF side data (mask words, HDM value / new column) is fetched one tile ahead
   uint32_t wS = 0, wB = 0;
   int bitpos = 0;
@@ -152,43 +161,36 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
       }
     }
   };
-  fetch(first);
-  int it = 0;
-  for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
+  const int64_t gstride = (int64_t)gridDim.x * NCG;
+  fetch(first + (int64_t)grp * gridDim.x);
+  for (int it = grp; first + (int64_t)it * gridDim.x < ntiles; it += NCG) {
+    const int64_t tile = first + (int64_t)it * gridDim.x;
     const int st = it % a.nstage;
     const int64_t e = tile * TILE + el;
     const bool valid = e < g.D;
     const bool inS = (wS >> bitpos) & 1u, inB = (wB >> bitpos) & 1u;
     const double side = pre;
-    fetch(tile + gridDim.x);
+    fetch(tile + gstride);
     mbar_wait(&full[st], (uint32_t)((it / a.nstage) & 1));
     const double* T = stage0 + st * stage_elems + el;
     const double rh = T[roff];
-    // pass 1 (x_s = gamma_s - rho): sp = sum_{s<w} x_s, sc = sum_{s>=xoff} x_s,
-    //                                tr = sum_{s>=xoff} c_{s-xoff} x_s  (two chains each)
+    // pass 1 over the physical slots (x = gamma - rho, coefficients broadcast from smem):
+    //   sp = sum_{s<w} x_s, sc = sum_{s>=xoff} x_s, tr = sum_{s>=xoff} c_{s-xoff} x_s
     double sp = 0.0, sc = 0.0, tr = 0.0, sp2 = 0.0, sc2 = 0.0, tr2 = 0.0;
-    if (xoff == 1) sp = T[soff[0]] - rh;
-    int s = xoff;
-#pragma unroll 4
-    for (; s + 1 < w; s += 2) {
-      const double x = T[soff[s]] - rh, x2 = T[soff[s + 1]] - rh;
-      sp += x;
-      sc += x;
-      tr += cs[s - xoff] * x;
-      sp2 += x2;
-      sc2 += x2;
-      tr2 += cs[s + 1 - xoff] * x2;
-    }
-    if (s < w) {
-      const double x = T[soff[s]] - rh;
-      sp += x;
-      sc += x;
-      tr += cs[s - xoff] * x;
-    }
-    if (xoff == 1) {
-      const double x = T[soff[w]] - rh;
-      sc2 += x;
-      tr2 += cs[w - 1] * x;
+#pragma unroll
+    for (int q = 0; q < NSL; q += 2) {
+      if (q < nsl) {
+        const double x = T[q * TILE] - rh;
+        sp = fma(cP[q], x, sp);
+        sc = fma(cC[q], x, sc);
+        tr = fma(cX[q], x, tr);
+      }
+      if (q + 1 < nsl) {
+        const double x2 = T[(q + 1) * TILE] - rh;
+        sp2 = fma(cP[q + 1], x2, sp2);
+        sc2 = fma(cC[q + 1], x2, sc2);
+        tr2 = fma(cX[q + 1], x2, tr2);
+      }
     }
     sp += sp2;
     sc += sc2;
@@ -213,37 +215,37 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
         a.eps_elem[e] = dev * dev;
       }
     }
-    // pass 2: new Gram row, per-lane accumulators (band DOFs are added after the filter)
+    // pass 2: new Gram row per physical slot (band DOFs are added after the filter)
     if (a.do_gram && valid && !inB) {
       const double gr = gval - rh;
       acc_self += gr * gr;
 #pragma unroll
-      for (int q = 0; q < NU; ++q)
-        if (q < nU) acc[q] += gr * (T[soff[q]] - rh);
+      for (int q = 0; q < NSL; ++q)
+        if (q < nsl) acc[q] = fma(gr, T[q * TILE] - rh, acc[q]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
   if (!a.do_gram) return;
-  // fixed-order reductions: lanes (shuffle tree), then the compute warps -> part[block][*]
+  // fixed-order reductions: lanes (shuffle tree), then the compute warps -> part[block][s]
 #pragma unroll
-  for (int q = 0; q < NU; ++q) {
+  for (int q = 0; q < NSL; ++q) {
     double v = acc[q];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0 && q < nU) wred[warp][q] = v;
+    if (lane == 0 && q < nsl) wred[warp][q] = v;
   }
   {
     double v = acc_self;
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) wred[warp][NU] = v;
+    if (lane == 0) wred[warp][NSL] = v;
   }
-  asm volatile("bar.sync 1, %0;\n" ::"r"(32 * NCW));  // compute warps only
+  asm volatile("bar.sync 1, %0;\n" ::"r"(32 * NCG * NCW));  // compute warps only
   double* outp = a.part + (int64_t)blockIdx.x * (nU + 1);
-  for (int q = warp * 32 + lane; q <= nU; q += 32 * NCW) {
-    const int idx = (q == nU) ? NU : q;
+  for (int s = tid; s <= nU; s += 32 * NCG * NCW) {
+    const int idx = (s == nU) ? NSL : a.W.slot[s];
     double v = 0.0;
-    for (int k = 0; k < NCW; ++k) v += wred[k][idx];
-    outp[q] = v;
+    for (int k = 0; k < NCG * NCW; ++k) v += wred[k][idx];
+    outp[s] = v;
   }
 }
 
@@ -334,6 +336,7 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef ou
   if (a.nstage < 1) return HROM_E_INVALID;
   const size_t smem = a.nstage * stage + 2 * a.nstage * sizeof(uint64_t);
   a.rho_slot = c->nslots;
+  a.nslots = c->nslots;
   a.ring = c->b.ring;
   a.cvec = (mode == MODE_PROJ) ? c->b.zvec : c->b.cvec;
   a.src_S = src_S;
@@ -343,11 +346,11 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef ou
   a.eps_elem = c->b.eps_elem;
   a.part = c->b.gpart;
   if (!a.do_gram) return launch_fill_t<1>(c, a, smem);
-  if (W.nU <= 12) return launch_fill_t<12>(c, a, smem);
-  if (W.nU <= 24) return launch_fill_t<24>(c, a, smem);
-  if (W.nU <= 36) return launch_fill_t<36>(c, a, smem);
-  if (W.nU <= 52) return launch_fill_t<52>(c, a, smem);
-  if (W.nU <= 68) return launch_fill_t<68>(c, a, smem);
+  if (c->nslots <= 12) return launch_fill_t<12>(c, a, smem);
+  if (c->nslots <= 24) return launch_fill_t<24>(c, a, smem);
+  if (c->nslots <= 36) return launch_fill_t<36>(c, a, smem);
+  if (c->nslots <= 52) return launch_fill_t<52>(c, a, smem);
+  if (c->nslots <= 68) return launch_fill_t<68>(c, a, smem);
   return HROM_E_INVALID;  // wider windows use gram_mode = 1 (hrom_create enforces it)
 }
 
