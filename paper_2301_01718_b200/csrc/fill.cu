@@ -23,9 +23,9 @@
 namespace hrom {
 namespace {
 
-constexpr int NCW = TILE / 32;  // compute warps per group (one DOF per lane)
-constexpr int NCG = 2;          // compute groups (each consumes every NCG-th tile)
-constexpr int FILL_THREADS = 32 * (NCG * NCW + 1);
+constexpr int NCW = TILE / 16;  // warps (16 DOFs each: one lane pair per DOF); thread 0 also issues the copies
+constexpr int FILL_STAGES = 2;  // slab-tile stages in shared memory
+constexpr int FILL_THREADS = 32 * NCW;
 
 enum { MODE_FILL = 0, MODE_READ = 1, MODE_PROJ = 2 };
 
@@ -78,8 +78,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// NSL: compile-time upper bound of the physical ring slots (w + 2; per-lane Gram accumulators)
-template <int NSL>
+// SH: compile-time upper bound of the physical slots per half (ceil((w + 2) / 2)).
+// A DOF is owned by a lane pair (l, l ^ 16) of a compute warp; each lane holds its half of
+// the DOF's slot values in registers (SH doubles) and SH Gram accumulators.
+template <int SH>
 __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const int nU = a.W.nU, w = a.W.w, nsl = a.nslots;
@@ -88,18 +90,17 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   const size_t stage_elems = (size_t)nsr * TILE;
   uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + a.nstage * stage_elems);
   uint64_t* empty = full + a.nstage;
-  // per PHYSICAL slot p: membership of psi_prev (cP), of psi_cur (cC), coefficient c (cX)
-  __shared__ double cP[kMaxSlots], cC[kMaxSlots], cX[kMaxSlots];
-  __shared__ double wred[NCG * NCW][NSL + 1];
+  // per PHYSICAL slot p: in-window flag (cA) and coefficient c (cX)
+  __shared__ double cA[kMaxSlots + 2], cX[kMaxSlots + 2];
+  __shared__ double wred[NCW][2 * SH + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Geo& g = a.g;
   const int xoff = nU - w;  // logical: psi_cur and X use slots >= xoff; psi_prev uses slots < w
-  for (int q = tid; q < nsl; q += FILL_THREADS) cP[q] = cC[q] = cX[q] = 0.0;
+  for (int q = tid; q < kMaxSlots + 2; q += FILL_THREADS) cA[q] = cX[q] = 0.0;
   __syncthreads();
   for (int s = tid; s < nU; s += FILL_THREADS) {
     const int q = a.W.slot[s];
-    cP[q] = (s < w) ? 1.0 : 0.0;
-    cC[q] = (s >= xoff) ? 1.0 : 0.0;
+    cA[q] = 1.0;
     cX[q] = (s >= xoff && a.cvec) ? a.cvec[s - xoff] : 0.0;
   }
   if (tid == 0) {
@@ -114,31 +115,31 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   const int64_t first = blockIdx.x;
   const uint32_t tile_bytes = (uint32_t)(stage_elems * sizeof(double));
 
-  if (warp == NCG * NCW) {
-    // ---------------- producer warp: one bulk copy per slab tile ----------------
-    if (lane == 0) {
-      int it = 0;
-      for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
-        const int st = it % a.nstage;
-        if (it >= a.nstage) mbar_wait(&empty[st], (uint32_t)(((it / a.nstage) - 1) & 1));
-        mbar_expect(&full[st], tile_bytes);
-        bulk_g2s(stage0 + st * stage_elems, a.ring + tile * stage_elems, tile_bytes, &full[st]);
-      }
-    }
-    return;
-  }
+  // producer role: thread 0 keeps FILL_STAGES slab tiles in flight, one bulk copy each
+  auto issue = [&](int it2) {
+    const int64_t tile = first + (int64_t)it2 * gridDim.x;
+    if (tile >= ntiles) return;
+    const int st = it2 % a.nstage;
+    mbar_expect(&full[st], tile_bytes);
+    bulk_g2s(stage0 + st * stage_elems, a.ring + tile * stage_elems, tile_bytes, &full[st]);
+  };
+  if (tid == 0)
+    for (int q = 0; q < a.nstage; ++q) issue(q);
 
-  // ---------------- compute groups (NCG x NCW warps): lane = DOF; group grp takes every NCG-th tile
-  const int grp = warp / NCW;
+  // ---------------- compute warps: DOF el = warp*16 + (lane & 15), slot half = lane >> 4
+  const int half = lane >> 4;
+  const int el = warp * 16 + (lane & 15);
+  const int h0 = (nsl + 1) / 2;                  // physical slots [0, h0) | [h0, nsl)
+  const int q0 = half ? h0 : 0, qn = half ? nsl : h0;
+  const int p_first = a.W.slot[0], p_last = a.W.slot[nU - 1];
   double csum = 0.0;
   for (int q = 0; q < nsl; ++q) csum += cX[q];
   const double inv_w = 1.0 / (double)w;
   const int roff = a.rho_slot * TILE;
-  double acc[NSL];
+  double acc[SH];
 #pragma unroll
-  for (int q = 0; q < NSL; ++q) acc[q] = 0.0;
+  for (int i = 0; i < SH; ++i) acc[i] = 0.0;
   double acc_self = 0.0;
-  const int el = (warp % NCW) * 32 + lane;
   // per-DOF side data (mask words, HDM value / new column) is fetched one tile ahead
   uint32_t wS = 0, wB = 0;
   int bitpos = 0;
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     const int64_t e = tile * TILE + el;
     wS = wB = 0;
     pre = 0.0;
-    if (tile < ntiles && e < g.D && a.mode != MODE_PROJ) {
+    if (half == 0 && tile < ntiles && e < g.D && a.mode != MODE_PROJ) {
       const int64_t n = e % g.N;
       const int i = (int)(n % g.nx), j = (int)(n / g.nx);
       const int64_t wi = (int64_t)j * g.wpr + (i >> 5);
@@ -161,90 +162,112 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
       }
     }
   };
-  const int64_t gstride = (int64_t)gridDim.x * NCG;
-  fetch(first + (int64_t)grp * gridDim.x);
-  for (int it = grp; first + (int64_t)it * gridDim.x < ntiles; it += NCG) {
-    const int64_t tile = first + (int64_t)it * gridDim.x;
+  fetch(first);
+  int it = 0;
+  for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
     const int st = it % a.nstage;
+    if (tid == 0 && it >= 1) {
+      // the stage of tile it-1 is free once every warp released it: refill it with tile it-1+stages
+      const int pst = (it - 1) % a.nstage;
+      mbar_wait(&empty[pst], (uint32_t)(((it - 1) / a.nstage) & 1));
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(it - 1 + a.nstage);
+    }
     const int64_t e = tile * TILE + el;
     const bool valid = e < g.D;
-    const bool inS = (wS >> bitpos) & 1u, inB = (wB >> bitpos) & 1u;
-    const double side = pre;
-    fetch(tile + gstride);
+    const bool inS = __shfl_sync(0xffffffffu, (wS >> bitpos) & 1u, lane & 15);
+    const bool inB = __shfl_sync(0xffffffffu, (wB >> bitpos) & 1u, lane & 15);
+    const double side = __shfl_sync(0xffffffffu, pre, lane & 15);
+    fetch(tile + gridDim.x);
     mbar_wait(&full[st], (uint32_t)((it / a.nstage) & 1));
     const double* T = stage0 + st * stage_elems + el;
     const double rh = T[roff];
-    // pass 1 over the physical slots (x = gamma - rho, coefficients broadcast from smem):
-    //   sp = sum_{s<w} x_s, sc = sum_{s>=xoff} x_s, tr = sum_{s>=xoff} c_{s-xoff} x_s
-    double sp = 0.0, sc = 0.0, tr = 0.0, sp2 = 0.0, sc2 = 0.0, tr2 = 0.0;
+    // pass 1 on this lane's physical slots (x = gamma - rho, kept in registers for pass 2):
+    //   sa = sum of the window slots, tr = sum_{s>=xoff} c_{s-xoff} x_s
+    double x[SH];
+    double sa = 0.0, tr = 0.0, sa2 = 0.0, tr2 = 0.0;
 #pragma unroll
-    for (int q = 0; q < NSL; q += 2) {
-      if (q < nsl) {
-        const double x = T[q * TILE] - rh;
-        sp = fma(cP[q], x, sp);
-        sc = fma(cC[q], x, sc);
-        tr = fma(cX[q], x, tr);
-      }
-      if (q + 1 < nsl) {
-        const double x2 = T[(q + 1) * TILE] - rh;
-        sp2 = fma(cP[q + 1], x2, sp2);
-        sc2 = fma(cC[q + 1], x2, sc2);
-        tr2 = fma(cX[q + 1], x2, tr2);
+    for (int i = 0; i < SH; ++i) {
+      const int q = q0 + i;
+      if (q < qn) {
+        x[i] = T[q * TILE] - rh;
+        if (i & 1) {
+          sa2 = fma(cA[q], x[i], sa2);
+          tr2 = fma(cX[q], x[i], tr2);
+        } else {
+          sa = fma(cA[q], x[i], sa);
+          tr = fma(cX[q], x[i], tr);
+        }
+      } else {
+        x[i] = 0.0;
       }
     }
-    sp += sp2;
-    sc += sc2;
+    sa += sa2;
     tr += tr2;
+    // combine the two halves (a + b == b + a: both lanes of the pair get identical sums)
+    sa += __shfl_xor_sync(0xffffffffu, sa, 16);
+    tr += __shfl_xor_sync(0xffffffffu, tr, 16);
+    // psi_prev and psi_cur differ from the window sum by one end slot each (when nU = w + 1)
+    double sp = sa, sc = sa;
+    if (xoff == 1) {
+      sp -= T[p_last * TILE] - rh;
+      sc -= T[p_first * TILE] - rh;
+    }
     double gval = 0.0;
     if (valid) {
       // psi_prev - rho = sp/w, psi_cur - rho = sc/w;  Phi y = sum_i c_i (x_i - (psi_prev - rho))
       const double dev = tr - (sp * inv_w) * csum;
       if (a.mode == MODE_FILL) {
         const double rec = (rh + sc * inv_w) + dev;
-        if (inS) {
-          gval = side;
-          const double d = gval - rec;
-          a.eps_elem[e] = d * d;
-        } else {
-          gval = rec;
+        gval = inS ? side : rec;
+        if (half == 0) {
+          if (inS) {
+            const double d = gval - rec;
+            a.eps_elem[e] = d * d;
+          }
+          a.out.p[sidx(a.out, e)] = gval;
         }
-        a.out.p[sidx(a.out, e)] = gval;
       } else if (a.mode == MODE_READ) {
         gval = side;
-      } else {  // MODE_PROJ: residual of the projection onto the basis (bootstrap indicator)
+      } else if (half == 0) {  // MODE_PROJ: residual of the projection (bootstrap indicator)
         a.eps_elem[e] = dev * dev;
       }
     }
-    // pass 2: new Gram row per physical slot (band DOFs are added after the filter)
+    // pass 2: new Gram row on this lane's physical slots (band DOFs are added after the filter)
     if (a.do_gram && valid && !inB) {
       const double gr = gval - rh;
-      acc_self += gr * gr;
+      if (half == 0) acc_self += gr * gr;
 #pragma unroll
-      for (int q = 0; q < NSL; ++q)
-        if (q < nsl) acc[q] = fma(gr, T[q * TILE] - rh, acc[q]);
+      for (int i = 0; i < SH; ++i) acc[i] = fma(gr, x[i], acc[i]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
   if (!a.do_gram) return;
-  // fixed-order reductions: lanes (shuffle tree), then the compute warps -> part[block][s]
+  // fixed-order reductions: the 16 lanes of each half (shuffle tree), then warps -> part[block][s]
 #pragma unroll
-  for (int q = 0; q < NSL; ++q) {
-    double v = acc[q];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0 && q < nsl) wred[warp][q] = v;
+  for (int i = 0; i < SH; ++i) {
+    double v = acc[i];
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((lane & 15) == 0) wred[warp][half * SH + i] = v;
   }
   {
     double v = acc_self;
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) wred[warp][NSL] = v;
+    if (lane == 0) wred[warp][2 * SH] = v;
   }
-  asm volatile("bar.sync 1, %0;\n" ::"r"(32 * NCG * NCW));  // compute warps only
+  __syncthreads();
   double* outp = a.part + (int64_t)blockIdx.x * (nU + 1);
-  for (int s = tid; s <= nU; s += 32 * NCG * NCW) {
-    const int idx = (s == nU) ? NSL : a.W.slot[s];
+  for (int s = tid; s <= nU; s += 32 * NCW) {
+    int idx;
+    if (s == nU) {
+      idx = 2 * SH;
+    } else {
+      const int q = a.W.slot[s];
+      idx = (q < h0) ? q : SH + (q - h0);
+    }
     double v = 0.0;
-    for (int k = 0; k < NCG * NCW; ++k) v += wred[k][idx];
+    for (int k = 0; k < NCW; ++k) v += wred[k][idx];
     outp[s] = v;
   }
 }
@@ -329,11 +352,9 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef ou
   a.W = W;
   a.mode = mode;
   a.do_gram = (mode != MODE_PROJ) && out_in_ring && c->P.gram_mode == 0 ? 1 : 0;
-  // stages of one slab tile each (nsr KB), as many as fit (<= 4)
   const size_t stage = (size_t)c->g.nsr * TILE * sizeof(double);
-  const size_t budget = 224 * 1024 - 4 * 1024;
-  a.nstage = (int)std::min<size_t>(4, budget / (stage + 16));
-  if (a.nstage < 1) return HROM_E_INVALID;
+  a.nstage = FILL_STAGES;
+  if (a.nstage * stage > 216 * 1024) return HROM_E_INVALID;
   const size_t smem = a.nstage * stage + 2 * a.nstage * sizeof(uint64_t);
   a.rho_slot = c->nslots;
   a.nslots = c->nslots;
@@ -345,12 +366,14 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef ou
   a.mB = (mode == MODE_FILL) ? c->b.masks + (int64_t)M_B * c->mwords : nullptr;
   a.eps_elem = c->b.eps_elem;
   a.part = c->b.gpart;
-  if (!a.do_gram) return launch_fill_t<1>(c, a, smem);
-  if (c->nslots <= 12) return launch_fill_t<12>(c, a, smem);
-  if (c->nslots <= 24) return launch_fill_t<24>(c, a, smem);
-  if (c->nslots <= 36) return launch_fill_t<36>(c, a, smem);
-  if (c->nslots <= 52) return launch_fill_t<52>(c, a, smem);
-  if (c->nslots <= 68) return launch_fill_t<68>(c, a, smem);
+  const int sh = (c->nslots + 1) / 2;
+  if (sh <= 6) return launch_fill_t<6>(c, a, smem);
+  if (sh <= 12) return launch_fill_t<12>(c, a, smem);
+  if (sh <= 18) return launch_fill_t<18>(c, a, smem);
+  if (sh <= 26) return launch_fill_t<26>(c, a, smem);
+  if (sh <= 34) return launch_fill_t<34>(c, a, smem);
+  if (!a.do_gram && sh <= 50) return launch_fill_t<50>(c, a, smem);
+  if (!a.do_gram && sh <= 66) return launch_fill_t<66>(c, a, smem);
   return HROM_E_INVALID;  // wider windows use gram_mode = 1 (hrom_create enforces it)
 }
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 #include "../../include/hrom.h"
 
@@ -16,8 +17,14 @@
     }                                                                                     \
   } while (0)
 
+// HROM_SYNC_DEBUG=1: synchronise after every launch so a fault names its kernel (debug only)
+inline bool hrom_sync_debug() {
+  static const bool on = getenv("HROM_SYNC_DEBUG") != nullptr;
+  return on;
+}
 #define HROM_LAUNCH_CK()                 \
   do {                                   \
+    if (hrom_sync_debug()) cudaDeviceSynchronize(); \
     cudaError_t e_ = cudaGetLastError(); \
     if (e_ != cudaSuccess) {             \
       fprintf(stderr, "libhrom: launch error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
