@@ -70,7 +70,7 @@ __device__ __forceinline__ void gram_tile(const double* tile, int nsb, double (&
 }
 
 template <int TPW>
-__global__ void __launch_bounds__(GT) gram_kernel(GramArgs a) {
+__global__ void __launch_bounds__(GT, 2) gram_kernel(GramArgs a) {
   extern __shared__ double smem[];
   double* tile = smem;                      // [nsb*16][LDT]
   const int ncp = a.nsb * 16;
