@@ -70,7 +70,7 @@ __device__ __forceinline__ void gram_tile(const double* tile, int nsb, double (&
 }
 
 template <int TPW>
-__global__ void __launch_bounds__(GT, 2) gram_kernel(GramArgs a) {
+__global__ void __launch_bounds__(GT, (TPW <= 2) ? 2 : 1) gram_kernel(GramArgs a) {
   extern __shared__ double smem[];
   double* tile = smem;                      // [nsb*16][LDT]
   const int ncp = a.nsb * 16;
@@ -229,18 +229,28 @@ __device__ void jacobi_eig(double* A, double* V, int n, int ldn, double* lam, in
   }
   __syncthreads();
   const int np = ne / 2;
+  // round-robin tournament schedule, precomputed: round r pairs positions k and ne-1-k,
+  // player(pos) = pos == 0 ? 0 : ((pos - 1 + r) mod (ne - 1)) + 1
+  __shared__ short2 ptab[(kMaxSlots - 1) * (kMaxSlots / 2)];
+  for (int idx = tid; idx < (ne - 1) * np; idx += nt) {
+    const int r = idx / np, k = idx % np;
+    auto player = [&](int pos) { return pos == 0 ? 0 : ((pos - 1 + r) % (ne - 1)) + 1; };
+    int p = player(k), q = player(ne - 1 - k);
+    if (p > q) { const int t = p; p = q; q = t; }
+    ptab[idx] = make_short2((short)p, (short)q);
+  }
+  __syncthreads();
   for (int sweep = 0; sweep < 20; ++sweep) {
     if (tid == 0) *flag = 0;
     __syncthreads();
     for (int rnd = 0; rnd < ne - 1; ++rnd) {
       if (tid < np) {
         const int k = tid;
-        auto player = [&](int pos) { return pos == 0 ? 0 : ((pos - 1 + rnd) % (ne - 1)) + 1; };
-        int p = player(k), q = player(ne - 1 - k);
-        if (p > q) { const int t = p; p = q; q = t; }
+        const short2 pr = ptab[rnd * np + k];
+        const int p = pr.x, q = pr.y;
         const double app = A[p * ldn + p], aqq = A[q * ldn + q], apq = A[p * ldn + q];
         double c = 1.0, s = 0.0;
-        if (fabs(apq) > floor_abs && fabs(apq) > 1e-15 * sqrt(fabs(app * aqq))) {
+        if (fabs(apq) > floor_abs && fabs(apq) > 1e-14 * sqrt(fabs(app * aqq))) {
           // t = tan(phi) of the annihilating rotation, written without 1/apq
           const double tau = aqq - app;
           const double t = (tau >= 0.0 ? 2.0 : -2.0) * apq / (fabs(tau) + sqrt(tau * tau + 4.0 * apq * apq));
@@ -255,8 +265,8 @@ __device__ void jacobi_eig(double* A, double* V, int n, int ldn, double* lam, in
       }
       __syncthreads();
       // A' = J^T A J in one pass: every 2x2 block (pair k1 rows, pair k2 cols) is independent
-      for (int idx = tid; idx < np * np; idx += nt) {
-        const int k1 = idx / np, k2 = idx % np;
+      for (int idx = tid, k1 = tid / np, k2 = tid % np; idx < np * np;
+           idx += nt, k2 += nt % np, k1 += nt / np + (k2 >= np ? 1 : 0), k2 -= (k2 >= np ? np : 0)) {
         const double c1 = cs[2 * k1], s1 = cs[2 * k1 + 1], c2 = cs[2 * k2], s2 = cs[2 * k2 + 1];
         if (s1 == 0.0 && s2 == 0.0) continue;
         const int p1 = pq[2 * k1], q1 = pq[2 * k1 + 1], p2 = pq[2 * k2], q2 = pq[2 * k2 + 1];
@@ -273,8 +283,8 @@ __device__ void jacobi_eig(double* A, double* V, int n, int ldn, double* lam, in
         A[q1 * ldn + q2] = n11;
       }
       // V' = V J
-      for (int idx = tid; idx < ne * np; idx += nt) {
-        const int i = idx / np, k = idx % np;
+      for (int idx = tid, i = tid / np, k = tid % np; idx < ne * np;
+           idx += nt, k += nt % np, i += nt / np + (k >= np ? 1 : 0), k -= (k >= np ? np : 0)) {
         const double c = cs[2 * k], s = cs[2 * k + 1];
         if (s == 0.0) continue;
         const int p = pq[2 * k], q = pq[2 * k + 1];
@@ -537,7 +547,7 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
 hrom_status small_solve(hrom_ctx* c) {
   const size_t smem = (size_t)(c->win.w * kMaxR + 2 * (kMaxR + 2) * (kMaxR + 2) + 6 * kMaxR) * sizeof(double);
   HROM_CK(cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  solve_kernel<<<1, 512, smem, c->st>>>(c->b.K, c->win.w, c->r, c->b.A, c->b.ireg, c->P.lsq_rel_cutoff, c->b.y,
+  solve_kernel<<<1, 256, smem, c->st>>>(c->b.K, c->win.w, c->r, c->b.A, c->b.ireg, c->P.lsq_rel_cutoff, c->b.y,
                                         c->b.cvec, c->b.ireg + 2);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
@@ -549,7 +559,7 @@ hrom_status basis_from_gram(hrom_ctx* c, const Win& W) {
   const bool vsm = (2 * ldn * ldn + 4 * kMaxSlots) * 8 <= 200 * 1024;
   const size_t smem = (size_t)((vsm ? 2 : 1) * ldn * ldn + 4 * kMaxSlots) * sizeof(double);
   HROM_CK(cudaFuncSetAttribute(basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  basis_kernel<<<1, 1024, smem, c->st>>>(c->b.C, kMaxSlots, W, c->r, c->P.eig_rel_cutoff, c->b.A, c->b.lam,
+  basis_kernel<<<1, 512, smem, c->st>>>(c->b.C, kMaxSlots, W, c->r, c->P.eig_rel_cutoff, c->b.A, c->b.lam,
                                          c->b.ireg, c->b.eigV);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
