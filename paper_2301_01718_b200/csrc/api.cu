@@ -124,7 +124,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   if (c->w + 1 > fill_max_gram_slots()) c->P.gram_mode = 1;
   c->band_blocks = c->nsm;
   const int occ = std::max(1, std::min(4, filter_occupancy()));
-  c->filter_blocks = c->nsm * occ;
+  c->filter_blocks = c->nsm * std::min(occ, 1);  // one block per SM: cheapest grid barrier
 
   Bufs& b = c->b;
   hrom_status s = HROM_OK;

@@ -69,17 +69,22 @@ __global__ void __launch_bounds__(256) filter_kernel(FilterArgs a) {
   for (int64_t t = gtid; t < nb; t += gstride) {
     const int64_t n = a.list[t];
     for (int var = 0; var < g.c; ++var) a.Vorig[var * g.N + n] = a.v.p[sidx(a.v, var * g.N + n)];
-    a.kept[n] = 0;
   }
   grid.sync();
+  // Two grid barriers per sweep: the keep-set of sweep s (flag bit 1 + (s & 1), values in Vpp)
+  // is applied lazily by the x-pass of sweep s+1, which reads cur(m) = kept_s(m) ? Vpp(m) : v(m)
+  // and writes its own cell; every block takes the same stop decision from per-block stats.
+  int gs = 0;  // sweeps done over all orders
   for (int oi = 0; oi < a.norders; ++oi) {
     const double* cf;
     double den;
     const int rad = shapiro(a.orders[oi], &cf, &den);
     int sweeps = 0;
-    for (int sw = 0; sw < a.maxsw; ++sw) {
+    for (int sw = 0; sw < a.maxsw; ++sw, ++gs) {
       ++sweeps;
-      // P1: v' = S^x(v) on B
+      const uint8_t pbit = (uint8_t)(2u << ((gs + 1) & 1));  // keep bit of the previous sweep
+      const uint8_t cbit = (uint8_t)(2u << (gs & 1));        // keep bit of this sweep
+      // P1: apply the previous keep-set to the own cell, v' = S^x(cur) on B
       for (int64_t t = gtid; t < nb; t += gstride) {
         const int64_t n = a.list[t];
         const int i = (int)(n % g.nx), j = (int)(n / g.nx);
@@ -87,9 +92,16 @@ __global__ void __launch_bounds__(256) filter_kernel(FilterArgs a) {
         for (int var = 0; var < g.c; ++var) {
           const int64_t rb = var * g.N + row;
           double s = 0.0;
-          for (int m = -rad; m <= rad; ++m) s += cf[m + rad] * a.v.p[sidx(a.v, rb + wrapf(i + m, g.nx, g.bc))];
+          for (int m = -rad; m <= rad; ++m) {
+            const int64_t nn = row + wrapf(i + m, g.nx, g.bc);
+            const int64_t e = rb + (nn - row);
+            const double cur = (gs > 0 && (a.kept[nn] & pbit)) ? a.Vpp[e] : a.v.p[sidx(a.v, e)];
+            s += cf[m + rad] * cur;
+          }
           a.Vp[var * g.N + n] = s / den;
         }
+        if (gs > 0 && (a.kept[n] & pbit))
+          for (int var = 0; var < g.c; ++var) a.v.p[sidx(a.v, var * g.N + n)] = a.Vpp[var * g.N + n];
       }
       grid.sync();
       // P2: v'' = S^y(v') on B, residual gate
@@ -120,12 +132,14 @@ __global__ void __launch_bounds__(256) filter_kernel(FilterArgs a) {
           rold = fmax(rold, fabs(a.v.p[sidx(a.v, e)] - fe));
           rnew = fmax(rnew, fabs(x - fe));
         }
+        uint8_t fl = (uint8_t)(a.kept[n] & ~(pbit | cbit));
         if (rnew < rold) {
           for (int var = 0; var < g.c; ++var) a.Vpp[var * g.N + n] = vpp[var];
-          a.kept[n] |= 2;
+          fl |= (uint8_t)(cbit | 1u);
           mdec = fmax(mdec, (rold - rnew) / rold);
           ++cnt;
         }
+        a.kept[n] = fl;
       }
       for (int o = 16; o > 0; o >>= 1) {
         mdec = fmax(mdec, __shfl_xor_sync(0xffffffffu, mdec, o));
@@ -147,24 +161,28 @@ __global__ void __launch_bounds__(256) filter_kernel(FilterArgs a) {
         a.fcnt[blockIdx.x] = c;
       }
       grid.sync();
-      // P3: identical decision in every block (fixed-order reduction), apply the keep-set
+      // identical stop decision in every block (fixed-order reduction of the block stats)
       double md = 0.0;
       long long tot = 0;
       for (int b = 0; b < (int)gridDim.x; ++b) {
         md = fmax(md, a.fstat[b]);
         tot += a.fcnt[b];
       }
-      for (int64_t t = gtid; t < nb; t += gstride) {
-        const int64_t n = a.list[t];
-        if (a.kept[n] & 2) {
-          for (int var = 0; var < g.c; ++var) a.v.p[sidx(a.v, var * g.N + n)] = a.Vpp[var * g.N + n];
-          a.kept[n] = 1;
-        }
+      if (tot == 0 || md < a.eps_f) {
+        ++gs;
+        break;
       }
-      grid.sync();
-      if (tot == 0 || md < a.eps_f) break;
     }
     if (gtid == 0 && a.sweeps_out) a.sweeps_out[oi] = sweeps;
+  }
+  // apply the last pending keep-set
+  if (gs > 0) {
+    const uint8_t pbit = (uint8_t)(2u << ((gs + 1) & 1));
+    for (int64_t t = gtid; t < nb; t += gstride) {
+      const int64_t n = a.list[t];
+      if (a.kept[n] & pbit)
+        for (int var = 0; var < g.c; ++var) a.v.p[sidx(a.v, var * g.N + n)] = a.Vpp[var * g.N + n];
+    }
   }
   // indicator on kept band cells: eps_n = sum_v (v - (psi + Phi y))^2, pre-filter value = psi + Phi y
   for (int64_t t = gtid; t < nb; t += gstride) {
@@ -270,6 +288,7 @@ hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F) {
   a.fstat = c->b.fstat;
   a.fcnt = c->b.fcnt;
   a.sweeps_out = c->b.ireg + 4;
+  HROM_CK(cudaMemsetAsync(c->b.kept, 0, c->g.N, c->st));  // keep flags are read at band neighbours
   void* args[] = {&a};
   HROM_CK(cudaLaunchCooperativeKernel((void*)filter_kernel, dim3(c->filter_blocks), dim3(256), args, 0, c->st));
   ++c->nlaunch;
