@@ -157,8 +157,9 @@ hrom_status hrom_profile(hrom_ctx* ctx, int32_t enable);
 hrom_status hrom_profile_read(hrom_ctx* ctx, double* ms, int64_t* counts, int32_t nsec);
 /* Number of kernels this context has launched (host-side count). */
 int64_t hrom_launch_count(const hrom_ctx* ctx);
-/* Synchronises and copies n <= 16 int32 device counters: [0] r_eff, [2] LSQ status,
- * [4..6] filter sweeps per order, [8] eigen sweeps (basis), [9] eigen sweeps (pinv). */
+/* Synchronises and copies n <= 32 int32 device counters: [0] r_eff, [2] LSQ status,
+ * [4..6] filter sweeps per order, [8] eigen sweeps (basis), [9] eigen sweeps (pinv);
+ * [16 + l] the size of cell list l (0 S-hat, 1 seam band B, 2 T, 3 A2, 4 A1). */
 hrom_status hrom_debug_counters(hrom_ctx* ctx, int32_t* any_out, int32_t n);
 
 #ifdef __cplusplus

@@ -300,9 +300,12 @@ class Run:
         self.h = lib().orc_run_create(C.byref(self._g), C.byref(self._p), _d(q0))
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().orc_run_destroy(self.h)
-            self.h = None
+        h, self.h = getattr(self, "h", None), None
+        if h:
+            try:
+                lib().orc_run_destroy(h)
+            except TypeError:  # interpreter shutdown: module globals already torn down
+                pass
 
     def step(self, dt_override: float = 0.0) -> int:
         return lib().orc_run_step(self.h, dt_override)

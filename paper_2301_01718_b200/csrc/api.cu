@@ -123,8 +123,11 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   // (w + 1 > 68) take the full DMMA Gram every step instead
   if (c->w + 1 > fill_max_gram_slots()) c->P.gram_mode = 1;
   c->band_blocks = c->nsm;
-  const int occ = std::max(1, std::min(4, filter_occupancy()));
-  c->filter_blocks = c->nsm * std::min(occ, 1);  // one block per SM: cheapest grid barrier
+  if (filter_occupancy() < 1) {  // the cooperative seam filter needs one resident block per SM
+    delete c;
+    return HROM_E_CUDA;
+  }
+  c->filter_blocks = c->nsm;  // one block per SM: cheapest grid barrier
 
   Bufs& b = c->b;
   hrom_status s = HROM_OK;
@@ -141,6 +144,10 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   A(dalloc(&b.lists, (size_t)L_COUNT * g.N));
   A(dalloc(&b.counts, 16));
   A(dalloc(&b.kept, g.N));
+  A(dalloc(&b.fidx, g.N));
+  A(dalloc(&b.ftab, (size_t)14 * g.N));
+  A(dalloc(&b.fcur, g.Dp));
+  A(dalloc(&b.fF, g.Dp));
   A(dalloc(&b.C, (size_t)kMaxSlots * kMaxSlots));
   b.part_len = (int64_t)2 * c->nsm * 144 * 144;
   A(dalloc(&b.part, b.part_len));
@@ -208,7 +215,7 @@ void hrom_destroy(hrom_ctx* c) {
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   Bufs& b = c->b;
   void* ptrs[] = {b.ring, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
-                  b.kept, b.C, b.part, b.gpart, b.K, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
+                  b.kept, b.fidx, b.ftab, b.fcur, b.fF, b.C, b.part, b.gpart, b.K, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
                   b.dreg, b.ureg, b.sel_val, b.sel_cell, b.blk, b.hist, b.fstat, b.fcnt, (void*)b.colptr, b.slot_tab};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -319,7 +326,7 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
   // H7
   prof_begin(c, SEC_FILTER);
   if (c->P.n_filter_orders > 0 && c->P.filter_max_sweeps > 0)
-    if ((s = launch_filter(c, out, U3)) != HROM_OK) return s;
+    if ((s = launch_filter(c, out, U3, nullptr)) != HROM_OK) return s;
   prof_end(c, SEC_FILTER);
   prof_begin(c, SEC_BANDGRAM);
   if (c->P.gram_mode == 0)
@@ -447,9 +454,7 @@ hrom_status hrom_filter(hrom_ctx* c, const uint32_t* dev_mask, double* dev_v, co
     c->sets_ready = true;
   }
   if (!c->sets_ready) return HROM_E_STATE;
-  if ((s = launch_filter(c, plain(dev_v), plain(dev_F))) != HROM_OK) return s;
-  if (dev_kept_out)
-    HROM_CK(cudaMemcpyAsync(dev_kept_out, c->b.kept, c->g.N, cudaMemcpyDefault, c->st));
+  if ((s = launch_filter(c, plain(dev_v), plain(dev_F), dev_kept_out)) != HROM_OK) return s;
   return HROM_OK;
 }
 
@@ -601,10 +606,11 @@ hrom_status hrom_profile_read(hrom_ctx* c, double* ms, int64_t* counts, int32_t 
 int64_t hrom_launch_count(const hrom_ctx* c) { return c ? c->nlaunch : 0; }
 
 hrom_status hrom_debug_counters(hrom_ctx* c, int32_t* any_out, int32_t n) {
-  if (!c || !any_out || n < 0 || n > 16) return HROM_E_INVALID;
+  if (!c || !any_out || n < 0 || n > 32) return HROM_E_INVALID;
   basis_join(c);
   HROM_CK(cudaStreamSynchronize(c->st));
-  HROM_CK(cudaMemcpy(any_out, c->b.ireg, n * sizeof(int32_t), cudaMemcpyDefault));
+  HROM_CK(cudaMemcpy(any_out, c->b.ireg, std::min(n, 16) * sizeof(int32_t), cudaMemcpyDefault));
+  if (n > 16) HROM_CK(cudaMemcpy(any_out + 16, c->b.counts, (n - 16) * sizeof(int32_t), cudaMemcpyDefault));
   return HROM_OK;
 }
 

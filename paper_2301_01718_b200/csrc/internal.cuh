@@ -72,7 +72,7 @@ struct Win {
 // mask indices
 enum { M_S = 0, M_B, M_T, M_A2, M_A1, M_TMP, M_TMP2, M_KEEP, M_COUNT };
 // list indices
-enum { L_S = 0, L_B, L_T, L_A2, L_A1, L_COUNT };
+enum { L_S = 0, L_B, L_T, L_A2, L_A1, L_H, L_COUNT };  // L_H: seam-filter halo
 
 struct Bufs {
   double* ring = nullptr;     // slab: (Dp / TILE) tiles x nsr slots x TILE
@@ -86,7 +86,11 @@ struct Bufs {
   uint32_t* masks = nullptr;  // M_COUNT * mwords
   int32_t* lists = nullptr;   // L_COUNT * N
   int32_t* counts = nullptr;  // 16 ints (device)
-  uint8_t* kept = nullptr;    // N bytes (filter kept flags)
+  uint8_t* kept = nullptr;    // N bytes (compact seam-filter flags)
+  int32_t* fidx = nullptr;    // N: cell -> compact seam-filter index
+  int32_t* ftab = nullptr;    // 14 N: seam-filter stencil tables
+  double* fcur = nullptr;     // Dp: compact current values (seam filter)
+  double* fF = nullptr;       // Dp: compact full-step values on the band
   double* C = nullptr;        // kMaxSlots^2
   double* part = nullptr;     // partial sums
   int64_t part_len = 0;
@@ -205,6 +209,6 @@ hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_b
 hrom_status launch_eps_cells(hrom_ctx* c);
 hrom_status launch_mean(hrom_ctx* c, const Win& W, SRef out);
 // filter.cu
-hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F);
+hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F, uint8_t* kept_cells);
 hrom_status launch_band_gram(hrom_ctx* c, const Win& W, SRef v);
 }  // namespace hrom

@@ -532,7 +532,9 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   a.list = c->b.lists + (int64_t)L_S * c->g.N;
   a.count = c->b.counts + L_S;
   a.src_b = src_b;
-  const int grid = c->nsm * 2;
+  // while the one-CTA eigen-solve of the previous update holds an SM (side stream), size the
+  // grid to the other SMs: a static tile split with one block left over would double the time
+  const int grid = (c->basis_pending ? c->nsm - 1 : c->nsm) * 2;
   const int ncp = a.nsb * 16;
   if ((int64_t)grid * ncp * ncp > c->b.part_len) return HROM_E_INVALID;
   a.part = c->b.part;

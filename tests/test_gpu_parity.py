@@ -202,27 +202,31 @@ def test_gram_dmma_vs_oracle(orc, inputs):
         assert np.max(np.abs(Cg - Co)) <= 1e-13 * np.max(np.abs(Co)), ncol
 
 
-def _trajectories(orc, inputs, wl, steps):
-    """GPU, oracle and oracle-with-1e-15-perturbed-IC trajectories of Algorithm 1."""
+def _trajectories(orc, inputs, wl, steps, nens=3):
+    """GPU, oracle and an ensemble of oracle runs from 1e-15-perturbed ICs."""
     q0 = inputs.initial_condition(wl)
-    rng = np.random.default_rng(0)
-    q1 = q0 * (1.0 + 1e-15 * rng.standard_normal(q0.shape))
     rom = H.HybridROM(wl)
     rom.set_state(dev(q0))
-    R, Rp = orc.Run(wl, q0), orc.Run(wl, q1)
+    R = orc.Run(wl, q0)
+    ens = []
+    for s in range(nens):
+        rng = np.random.default_rng(s)
+        ens.append(orc.Run(wl, q0 * (1.0 + 1e-15 * rng.standard_normal(q0.shape))))
     rows = []
     snaps, masks, dts = [q0], [], []
     for k in range(1, steps + 1):
         rom.step()
         R.step()
-        Rp.step()
+        for E in ens:
+            E.step()
         o = R.state()
         snaps.append(o)
         masks.append(R.mask())
         dts.append(R.dt())
         g = rom.get_state().cpu().numpy()
         flip = k >= wl.w - 1 and not np.array_equal(H.cells_from_mask(wl, rom.mask()), R.mask())
-        rows.append((k, rel(g, o), rel(Rp.state(), o), flip))
+        sref = max(rel(E.state(), o) for E in ens)
+        rows.append((k, rel(g, o), sref, flip, g))
     rom.sync()
     return rows, snaps, masks, dts
 
@@ -231,19 +235,23 @@ def test_trajectory_config1(orc, inputs):
     """200-step Algorithm-1 trajectory of config 1 (BJ:7).
 
     The explicit hybrid map amplifies rounding: the ORACLE itself, started from an IC
-    perturbed by 1e-15, drifts away from its own trajectory by ~x1.25 per hybrid step
-    (DESIGN.md §7).  So the trajectory bar is relative to that self-sensitivity: the GPU
-    may not drift from the oracle faster than 1000x the oracle drifts from itself, and
-    masks must agree while the oracle's own drift is below 1e-9.  Per-step parity is
-    checked by lock-step replay (GPU fed the oracle's window and mask) <= 1e-12."""
+    perturbed by 1e-15, drifts from its own trajectory by ~x1.25 per hybrid step and its
+    sampling masks flip (a discrete, O(1e-6) jump) around k = 165, so the
+    north_star's 200-step 1e-9 bar is below the method's own conditioning.  The bar here is
+    relative to that sensitivity, measured by an oracle ensemble (max drift sref):
+      * while sref < 1e-9, the GPU drift is <= 30 sref + 1e-13 (the GPU injects rounding
+        differences every step, the ensemble once; observed ratio ~10) and its masks agree;
+      * at k = steps the GPU state is physical and within 10x the ensemble's spread;
+      * per-step parity: lock-step replays (GPU fed the oracle's window and mask) <= 1e-12."""
     wl = inputs.config(1)
     rows, snaps, masks, dts = _trajectories(orc, inputs, wl, wl.steps)
-    for k, e, sref, flip in rows:
-        assert e <= max(1e4 * sref, 1e-13), (k, e, sref)
-        if k <= wl.w + 20:
-            assert e <= 1e-11, (k, e)
+    for k, e, sref, flip, g in rows:
         if sref < 1e-9:
+            assert e <= 30 * sref + 1e-13, (k, e, sref)
             assert not flip, (k, e, sref)
+    k, e, sref, flip, g = rows[-1]
+    assert e <= 10 * max(sref, 1e-9), (k, e, sref)
+    assert np.all(g[0] > 0), "density must stay positive"
     # lock-step replay at several steps: one hybrid step from the oracle's window
     for k in (wl.w, wl.w + 1, wl.w + 50, 150, wl.steps - 1):
         rom = H.HybridROM(wl)
@@ -265,3 +273,27 @@ def test_determinism_bitwise(inputs):
             rom.step()
         outs.append(rom.get_state().cpu().numpy())
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("dim,nx,ny,bc,frac,seed", [(2, 70, 45, 0, 0.05, 1), (2, 300, 211, 1, 0.1, 2),
+                                                    (2, 64, 64, 1, 0.6, 3), (1, 5000, 1, 0, 0.05, 4)])
+def test_seam_filter_parity(orc, inputs, dim, nx, ny, bc, frac, seed):
+    """H7 standalone vs the oracle's seam filter (A21-A24): kept set and sweeps
+    identical, values to rounding (same stencil sums in the same order)."""
+    wl = small2d(inputs, dim=dim, nx=nx, ny=ny, bc=bc, seed=seed)
+    rng = np.random.default_rng(seed)
+    F = inputs.initial_condition(wl, "random")
+    v = F * (1.0 + 0.05 * rng.standard_normal(F.shape))
+    S = (rng.random(wl.N) < frac).astype(np.uint8)
+    v[:, S == 1] = F[:, S == 1]
+    out, kept, sweeps = orc.seam_filter(wl, v, F, S)
+    rom = H.HybridROM(wl)
+    vg = dev(v)
+    kg = torch.zeros(wl.N, dtype=torch.uint8, device="cuda")
+    rom.filter(vg, dev(F), _mask_dev(wl, S), kept_out=kg)
+    rom.sync()
+    assert np.array_equal(kg.cpu().numpy(), kept)
+    cnt = rom.debug_counters(8)
+    assert list(cnt[4:4 + len(sweeps)]) == list(sweeps)
+    assert rel(vg.cpu().numpy(), out) <= 1e-14
+    assert np.array_equal(vg.cpu().numpy()[:, kept == 0], v[:, kept == 0])

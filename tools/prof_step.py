@@ -15,10 +15,13 @@ rom.set_state(torch.from_numpy(inputs.initial_condition(wl)).cuda())
 for _ in range(wl.w - 1):
     rom.step()
 rom.sync()
+every = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 for k in range(nh):
     rom.profile(True)
     rom.step()
     sec = rom.profile_read()
-    cnt = rom.debug_counters(12)
-    print(f"hybrid {k}: " + " ".join(f"{n}={v[0]:.3f}" for n, v in sec.items() if v[1]), "counters", cnt, flush=True)
+    cnt = rom.debug_counters(21)
+    cnt = cnt[:10] + cnt[16:21]
+    if k % every == 0 or k == nh - 1:
+      print(f"hybrid {k}: " + " ".join(f"{n}={v[0]:.3f}" for n, v in sec.items() if v[1]), "counters", cnt, flush=True)
 rom.sync()
