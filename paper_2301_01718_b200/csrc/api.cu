@@ -160,7 +160,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   A(dalloc(&b.cvec, kMaxW));
   A(dalloc(&b.zvec, kMaxW));
   A(dalloc(&b.eigV, (size_t)kMaxSlots * kMaxSlots));
-  A(dalloc(&b.eigA, (size_t)kMaxSlots * kMaxSlots));
+  A(dalloc(&b.eigA, (size_t)5 * kMaxSlots * (kMaxR + 1)));  // eigen-solve LU workspace when not in smem
   A(dalloc(&b.ireg, 16));
   A(dalloc(&b.dreg, 16));
   A(dalloc(&b.ureg, 4));

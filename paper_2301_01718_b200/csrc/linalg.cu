@@ -8,6 +8,7 @@
 // periodic re-base), A15 (Gram + Jacobi eigen, keep lambda_i >= 1e-8 lambda_1, sign on V).
 #include <algorithm>
 #include "internal.cuh"
+#include "eig.cuh"
 
 namespace hrom {
 namespace {
@@ -208,139 +209,55 @@ __global__ void gram_reduce(const double* __restrict__ part, int nblk, int ncp, 
   }
 }
 
-// ---------------- one-CTA cyclic Jacobi eigen-solver (n <= 130) ----------------
-// A (n x n, ld = ldn, symmetric) is overwritten; V receives eigenvectors (columns);
-// lam/perm: eigenvalues in descending order and the column permutation.
-__device__ void jacobi_eig(double* A, double* V, int n, int ldn, double* lam, int* perm, double* cs,
-                           int* pq, int* flag, int32_t* sweeps_out) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int ne = n + (n & 1);  // even size (padded index has zero row/col)
-  for (int idx = tid; idx < ne * ne; idx += nt) {
-    const int i = idx / ne, j = idx % ne;
-    V[i * ldn + j] = (i == j) ? 1.0 : 0.0;
-    if (i >= n || j >= n) A[i * ldn + j] = 0.0;
-  }
-  __syncthreads();
-  __shared__ double floor_abs;
-  if (tid == 0) {
-    double m = 0.0;
-    for (int i = 0; i < n; ++i) m = fmax(m, fabs(A[i * ldn + i]));
-    floor_abs = 1e-14 * m;  // below the Gram's own rounding level (~n eps lambda_max): not resolvable
-  }
-  __syncthreads();
-  const int np = ne / 2;
-  // round-robin tournament schedule, precomputed: round r pairs positions k and ne-1-k,
-  // player(pos) = pos == 0 ? 0 : ((pos - 1 + r) mod (ne - 1)) + 1
-  __shared__ short2 ptab[(kMaxSlots - 1) * (kMaxSlots / 2)];
-  for (int idx = tid; idx < (ne - 1) * np; idx += nt) {
-    const int r = idx / np, k = idx % np;
-    auto player = [&](int pos) { return pos == 0 ? 0 : ((pos - 1 + r) % (ne - 1)) + 1; };
-    int p = player(k), q = player(ne - 1 - k);
-    if (p > q) { const int t = p; p = q; q = t; }
-    ptab[idx] = make_short2((short)p, (short)q);
-  }
-  __syncthreads();
-  for (int sweep = 0; sweep < 20; ++sweep) {
-    if (tid == 0) *flag = 0;
-    __syncthreads();
-    for (int rnd = 0; rnd < ne - 1; ++rnd) {
-      if (tid < np) {
-        const int k = tid;
-        const short2 pr = ptab[rnd * np + k];
-        const int p = pr.x, q = pr.y;
-        const double app = A[p * ldn + p], aqq = A[q * ldn + q], apq = A[p * ldn + q];
-        double c = 1.0, s = 0.0;
-        if (fabs(apq) > floor_abs && fabs(apq) > 1e-14 * sqrt(fabs(app * aqq))) {
-          // t = tan(phi) of the annihilating rotation, written without 1/apq
-          const double tau = aqq - app;
-          const double t = (tau >= 0.0 ? 2.0 : -2.0) * apq / (fabs(tau) + sqrt(tau * tau + 4.0 * apq * apq));
-          c = rsqrt(1.0 + t * t);
-          s = t * c;
-          *flag = 1;
-        }
-        cs[2 * k] = c;
-        cs[2 * k + 1] = s;
-        pq[2 * k] = p;
-        pq[2 * k + 1] = q;
-      }
-      __syncthreads();
-      // A' = J^T A J in one pass: every 2x2 block (pair k1 rows, pair k2 cols) is independent
-      for (int idx = tid, k1 = tid / np, k2 = tid % np; idx < np * np;
-           idx += nt, k2 += nt % np, k1 += nt / np + (k2 >= np ? 1 : 0), k2 -= (k2 >= np ? np : 0)) {
-        const double c1 = cs[2 * k1], s1 = cs[2 * k1 + 1], c2 = cs[2 * k2], s2 = cs[2 * k2 + 1];
-        if (s1 == 0.0 && s2 == 0.0) continue;
-        const int p1 = pq[2 * k1], q1 = pq[2 * k1 + 1], p2 = pq[2 * k2], q2 = pq[2 * k2 + 1];
-        const double b00 = A[p1 * ldn + p2], b01 = A[p1 * ldn + q2];
-        const double b10 = A[q1 * ldn + p2], b11 = A[q1 * ldn + q2];
-        const double r00 = c1 * b00 - s1 * b10, r01 = c1 * b01 - s1 * b11;
-        const double r10 = s1 * b00 + c1 * b10, r11 = s1 * b01 + c1 * b11;
-        double n00 = c2 * r00 - s2 * r01, n01 = s2 * r00 + c2 * r01;
-        double n10 = c2 * r10 - s2 * r11, n11 = s2 * r10 + c2 * r11;
-        if (k1 == k2) { n01 = 0.0; n10 = 0.0; }
-        A[p1 * ldn + p2] = n00;
-        A[p1 * ldn + q2] = n01;
-        A[q1 * ldn + p2] = n10;
-        A[q1 * ldn + q2] = n11;
-      }
-      // V' = V J
-      for (int idx = tid, i = tid / np, k = tid % np; idx < ne * np;
-           idx += nt, k += nt % np, i += nt / np + (k >= np ? 1 : 0), k -= (k >= np ? np : 0)) {
-        const double c = cs[2 * k], s = cs[2 * k + 1];
-        if (s == 0.0) continue;
-        const int p = pq[2 * k], q = pq[2 * k + 1];
-        const double vp = V[i * ldn + p], vq = V[i * ldn + q];
-        V[i * ldn + p] = c * vp - s * vq;
-        V[i * ldn + q] = s * vp + c * vq;
-      }
-      __syncthreads();
-    }
-    if (tid == 0 && sweeps_out) *sweeps_out = sweep + 1;
-    if (*flag == 0) break;
-    __syncthreads();
-  }
-  // descending order, ties by index
-  for (int i = tid; i < n; i += nt) {
-    const double li = A[i * ldn + i];
-    int rank = 0;
-    for (int j = 0; j < n; ++j) {
-      const double lj = A[j * ldn + j];
-      if (lj > li || (lj == li && j < i)) ++rank;
-    }
-    perm[rank] = i;
-  }
-  __syncthreads();
-  for (int r = tid; r < n; r += nt) lam[r] = A[perm[r] * ldn + perm[r]];
-  // sign: largest |V_i,col| (ties lowest i) positive
-  for (int col = tid; col < n; col += nt) {
-    int im = 0;
-    double vm = -1.0;
-    for (int i = 0; i < n; ++i) {
-      const double a = fabs(V[i * ldn + col]);
-      if (a > vm) { vm = a; im = i; }
-    }
-    if (V[im * ldn + col] < 0.0)
-      for (int i = 0; i < n; ++i) V[i * ldn + col] = -V[i * ldn + col];
-  }
-  __syncthreads();
+// smem layout of the eigen-solve workspace (eig.cuh), shared by the basis and solve kernels
+struct EigLayout {
+  int ldn, ldz;
+  bool fac_smem;
+  size_t doubles;  // dynamic smem doubles (matrix + Z + vectors [+ LU workspace])
+  size_t bytes;
+};
+__host__ __device__ inline EigLayout eig_layout(int n, int nvec_cap) {
+  EigLayout L;
+  L.ldn = n + (n & 1) + 1;  // odd strides: column accesses are bank-conflict free
+  L.ldz = nvec_cap | 1;
+  const size_t base = (size_t)L.ldn * L.ldn + (size_t)n * L.ldz + 8 * kMaxSlots + 64;
+  const size_t fac = (size_t)4 * n * L.ldz + ((size_t)n * L.ldz + 7) / 8;
+  L.fac_smem = (base + fac) * 8 <= 200 * 1024;
+  L.doubles = base + (L.fac_smem ? fac : 0);
+  L.bytes = L.doubles * sizeof(double);
+  return L;
+}
+__device__ inline EigWork eig_work(double* sm, int n, const EigLayout& L, double* gfac) {
+  EigWork W;
+  double* p = sm + (size_t)L.ldn * L.ldn;
+  W.Z = p;
+  p += (size_t)n * L.ldz;
+  W.ldz = L.ldz;
+  W.d = p; p += kMaxSlots;
+  W.e = p; p += kMaxSlots;
+  W.tau = p; p += kMaxSlots;
+  W.vv = p; p += kMaxSlots;
+  W.pp = p; p += kMaxSlots;
+  W.lam = p; p += kMaxSlots;
+  p += 2 * kMaxSlots;  // caller scratch (mrow, rhs / y)
+  W.red = p; p += 64;
+  W.fac = L.fac_smem ? p : gfac;
+  W.swp = (uint8_t*)(W.fac + (size_t)4 * n * L.ldz);
+  return W;
 }
 
 // basis from the shifted Gram (one CTA): M = X^T X by lagged centring, eigen, A = V_r L_r^-1/2
-__global__ void __launch_bounds__(1024) basis_kernel(const double* __restrict__ C, int ldc, Win W, int r, double cut,
-                                                     double* __restrict__ Aout, double* __restrict__ lam_out,
-                                                     int32_t* __restrict__ reff_out, double* __restrict__ Vg) {
+__global__ void __launch_bounds__(512) basis_kernel(const double* __restrict__ C, int ldc, Win W, int r, double cut,
+                                                    double* __restrict__ Aout, double* __restrict__ lam_out,
+                                                    int32_t* __restrict__ reff_out, double* __restrict__ gfac) {
   extern __shared__ double sm[];
   const int w = W.w, nU = W.nU;
-  const int ldn = w + (w & 1) + 1;  // odd stride: column sweeps are bank-conflict free
-  double* M = sm;                                   // ldn*ldn
-  const bool vsm = (2 * ldn * ldn + 4 * kMaxSlots) * 8 <= 200 * 1024;
-  double* V = vsm ? sm + ldn * ldn : Vg;
-  double* lam = sm + (vsm ? 2 : 1) * ldn * ldn;     // kMaxSlots
-  double* mrow = lam + kMaxSlots;                   // kMaxSlots
-  double* cs = mrow + kMaxSlots;                    // 2*kMaxSlots
-  __shared__ int perm[kMaxSlots];
-  __shared__ int pq[2 * kMaxSlots];
-  __shared__ int flag;
-  __shared__ double mu;
+  const EigLayout L = eig_layout(w, r);
+  const int ldn = L.ldn;
+  double* M = sm;
+  const EigWork E = eig_work(sm, w, L, gfac);
+  double* mrow = E.lam + kMaxSlots;  // kMaxSlots
+  double* msum = mrow + kMaxSlots;   // kMaxSlots
   const int tid = threadIdx.x;
   // m_i = (1/w) sum_{p<w} C[x_i][u_p];  mu = (1/w^2) sum_{p,q<w} C[u_p][u_q]
   for (int i = tid; i < w; i += blockDim.x) {
@@ -349,13 +266,15 @@ __global__ void __launch_bounds__(1024) basis_kernel(const double* __restrict__ 
     for (int p = 0; p < w; ++p) s += C[xi * ldc + W.slot[p]];
     mrow[i] = s / (double)w;
   }
-  if (tid == 0) {
+  for (int p = tid; p < w; p += blockDim.x) {
     double s = 0.0;
-    for (int p = 0; p < w; ++p)
-      for (int q = 0; q < w; ++q) s += C[W.slot[p] * ldc + W.slot[q]];
-    mu = s / ((double)w * (double)w);
+    for (int q = 0; q < w; ++q) s += C[W.slot[p] * ldc + W.slot[q]];
+    msum[p] = s;
   }
   __syncthreads();
+  double mu = 0.0;
+  for (int p = 0; p < w; ++p) mu += msum[p];
+  mu /= (double)w * (double)w;
   for (int idx = tid; idx < w * w; idx += blockDim.x) {
     const int i = idx / w, j = idx % w;
     const int xi = W.slot[nU - w + i], xj = W.slot[nU - w + j];
@@ -364,43 +283,35 @@ __global__ void __launch_bounds__(1024) basis_kernel(const double* __restrict__ 
     M[i * ldn + j] = ((C[xi * ldc + xj] - mi) - mj) + mu;
   }
   __syncthreads();
-  jacobi_eig(M, V, w, ldn, lam, perm, cs, pq, &flag, reff_out + 8);
+  const int re = sym_eig(M, w, ldn, E, r, cut, reff_out + 10);
   if (tid == 0) {
-    int re = 0;
-    const double l0 = lam[0];
-    for (int i = 0; i < r && i < w; ++i)
-      if (l0 > 0.0 && lam[i] >= cut * l0) ++re;
-      else break;
     *reff_out = re;
+    reff_out[8] = 0;
   }
-  __syncthreads();
-  const int re = *reff_out;
   for (int idx = tid; idx < w * r; idx += blockDim.x) {
     const int i = idx % w, j = idx / w;  // A column-major: A[j*w + i]
-    Aout[j * w + i] = (j < re) ? V[i * ldn + perm[j]] / sqrt(lam[j]) : 0.0;
+    Aout[j * w + i] = (j < re) ? E.Z[i * E.ldz + j] / sqrt(E.lam[j]) : 0.0;
   }
-  for (int i = tid; i < w; i += blockDim.x) lam_out[i] = lam[i];
+  for (int i = tid; i < w; i += blockDim.x) lam_out[i] = E.lam[i];
 }
 
 // H5: G = A^T K_XX A, rhs = A^T K_Xb, y = G^+ rhs (cut on lambda), c = A y
-__global__ void __launch_bounds__(1024) solve_kernel(const double* __restrict__ K, int w, int r,
-                                                     const double* __restrict__ A, const int32_t* __restrict__ reffp,
-                                                     double cut, double* __restrict__ y_out,
-                                                     double* __restrict__ c_out, int32_t* __restrict__ status) {
+__global__ void __launch_bounds__(512) solve_kernel(const double* __restrict__ K, int w, int r,
+                                                    const double* __restrict__ A, const int32_t* __restrict__ reffp,
+                                                    double cut, double* __restrict__ y_out,
+                                                    double* __restrict__ c_out, int32_t* __restrict__ status,
+                                                    double* __restrict__ gfac, bool fac_smem) {
   extern __shared__ double sm[];
   const int re = *reffp;
   const int ldk = w + 1;
-  const int ldn = re + (re & 1) + 1;  // odd stride
-  double* T = sm;                 // w x re  (K_XX A)
-  double* G = T + w * kMaxR;      // ldn x ldn
-  double* V = G + (kMaxR + 2) * (kMaxR + 2);  // ldn x ldn
-  double* rhs = V + (kMaxR + 2) * (kMaxR + 2);
-  double* lam = rhs + kMaxR;
-  double* cs = lam + kMaxR;       // 2*kMaxR
-  double* y = cs + 2 * kMaxR;
-  __shared__ int perm[kMaxR];
-  __shared__ int pq[2 * kMaxR];
-  __shared__ int flag;
+  EigLayout L = eig_layout(re > 0 ? re : 1, re > 0 ? re : 1);
+  L.fac_smem = fac_smem;  // the host sized the smem for r >= r_eff: its choice is safe
+  const int ldn = L.ldn;
+  double* T = sm;                       // w x re  (K_XX A)
+  double* G = T + (size_t)w * kMaxR;    // eigen workspace starts here
+  const EigWork E = eig_work(G, re > 0 ? re : 1, L, gfac);
+  double* rhs = E.lam + kMaxSlots;
+  double* y = rhs + kMaxSlots;
   const int tid = threadIdx.x;
   for (int idx = tid; idx < w * re; idx += blockDim.x) {
     const int i = idx % w, j = idx / w;
@@ -423,25 +334,21 @@ __global__ void __launch_bounds__(1024) solve_kernel(const double* __restrict__ 
     G[j * ldn + i] = s;
   }
   __syncthreads();
-  if (re > 0) jacobi_eig(G, V, re, ldn, lam, perm, cs, pq, &flag, status + 7);
-  if (tid < kMaxR) y[tid] = 0.0;
-  __syncthreads();
+  const int nk = re > 0 ? sym_eig(G, re, ldn, E, re, cut) : 0;
   if (tid == 0) {
-    int st = 0;
-    if (re == 0 || !(lam[0] > 0.0)) st = 1;
-    *status = st;
+    *status = (re == 0 || !(E.lam[0] > 0.0)) ? 1 : 0;
+    status[7] = 0;
   }
-  // y = sum_{kept} v_k (v_k^T rhs) / lam_k
+  // y = sum_{kept} z_k (z_k^T rhs) / lam_k
+  for (int kk = tid; kk < nk; kk += blockDim.x) {
+    double d = 0.0;
+    for (int p = 0; p < re; ++p) d += E.Z[p * E.ldz + kk] * rhs[p];
+    E.pp[kk] = d / E.lam[kk];
+  }
+  __syncthreads();
   for (int i = tid; i < re; i += blockDim.x) {
     double s = 0.0;
-    if (lam[0] > 0.0)
-      for (int kk = 0; kk < re; ++kk) {
-        if (!(lam[kk] >= cut * lam[0])) break;
-        const int col = perm[kk];
-        double d = 0.0;
-        for (int p = 0; p < re; ++p) d += V[p * ldn + col] * rhs[p];
-        s += V[i * ldn + col] * (d / lam[kk]);
-      }
+    for (int kk = 0; kk < nk; ++kk) s += E.Z[i * E.ldz + kk] * E.pp[kk];
     y[i] = s;
   }
   __syncthreads();
@@ -547,22 +454,22 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
 }
 
 hrom_status small_solve(hrom_ctx* c) {
-  const size_t smem = (size_t)(c->win.w * kMaxR + 2 * (kMaxR + 2) * (kMaxR + 2) + 6 * kMaxR) * sizeof(double);
+  // the solve reads r_eff on the device: size the workspace for the largest possible (r)
+  const EigLayout L = eig_layout(c->r, c->r);
+  const size_t smem = ((size_t)c->win.w * kMaxR) * sizeof(double) + L.bytes;
   HROM_CK(cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   solve_kernel<<<1, 256, smem, c->st>>>(c->b.K, c->win.w, c->r, c->b.A, c->b.ireg, c->P.lsq_rel_cutoff, c->b.y,
-                                        c->b.cvec, c->b.ireg + 2);
+                                        c->b.cvec, c->b.ireg + 2, c->b.eigA, L.fac_smem);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;
 }
 
 hrom_status basis_from_gram(hrom_ctx* c, const Win& W) {
-  const int ldn = W.w + (W.w & 1) + 1;
-  const bool vsm = (2 * ldn * ldn + 4 * kMaxSlots) * 8 <= 200 * 1024;
-  const size_t smem = (size_t)((vsm ? 2 : 1) * ldn * ldn + 4 * kMaxSlots) * sizeof(double);
-  HROM_CK(cudaFuncSetAttribute(basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  basis_kernel<<<1, 512, smem, c->st>>>(c->b.C, kMaxSlots, W, c->r, c->P.eig_rel_cutoff, c->b.A, c->b.lam,
-                                         c->b.ireg, c->b.eigV);
+  const EigLayout L = eig_layout(W.w, c->r);
+  HROM_CK(cudaFuncSetAttribute(basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
+  basis_kernel<<<1, 512, L.bytes, c->st>>>(c->b.C, kMaxSlots, W, c->r, c->P.eig_rel_cutoff, c->b.A, c->b.lam,
+                                           c->b.ireg, c->b.eigA);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;

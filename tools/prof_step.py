@@ -21,7 +21,7 @@ for k in range(nh):
     rom.step()
     sec = rom.profile_read()
     cnt = rom.debug_counters(21)
-    cnt = cnt[:10] + cnt[16:21]
+    cnt = cnt[:16] + cnt[16:21]
     if k % every == 0 or k == nh - 1:
       print(f"hybrid {k}: " + " ".join(f"{n}={v[0]:.3f}" for n, v in sec.items() if v[1]), "counters", cnt, flush=True)
 rom.sync()
