@@ -195,6 +195,180 @@ __global__ void __launch_bounds__(GT, (TPW <= 2) ? 2 : 1) gram_kernel(GramArgs a
   }
 }
 
+// ---------------- H4: gathered Gram of the S-hat rows, cp.async pipeline ----------------
+// R = [U - rho, b - rho]^T [U - rho, b - rho] over the c |S-hat| rows (U: the nU union slots in
+// window order, b: the HDM value, rho: the Gram shift); the lagged centring (A14) is applied to
+// the small R afterwards (centre_kernel), exactly as for the window Gram C.  One CTA per SM
+// with GG_STAGES tiles in flight: each thread issues its 8-byte cp.async gathers for the tile
+// GG_STAGES-1 ahead, so the scattered loads overlap the DMMA of the current tile.
+constexpr int GG_T = 512;        // threads
+constexpr int GG_RT = 64;        // rows per tile
+constexpr int GG_LDT = GG_RT + 4;
+constexpr int GG_STAGES = 3;
+constexpr int GG_NCP = 80;       // padded columns (nU + 1 <= 66 real; 5 super blocks of 16)
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+struct GGArgs {
+  Geo g;
+  Win W;
+  const double* ring;
+  SRef rho;
+  const int32_t* list;
+  const int32_t* count;
+  SRef src_b;
+  double* part;  // [grid][GG_NCP][GG_NCP]
+};
+
+__global__ void __launch_bounds__(GG_T, 1) gather_gram_kernel(GGArgs a) {
+  extern __shared__ double smem[];
+  const int nS = *a.count;
+  const int64_t total_rows = (int64_t)nS * a.g.c;
+  const int64_t ntiles = (total_rows + GG_RT - 1) / GG_RT;
+  const int nU = a.W.nU, ncol = nU + 1;  // union slots + b
+  const int k = threadIdx.x % GG_RT, sub = threadIdx.x / GG_RT;  // row, column group
+  constexpr int NSUB = GG_T / GG_RT;                               // 8 column groups
+  const SRef slab{nullptr, a.g.nsr};
+  for (int i = threadIdx.x; i < GG_STAGES * GG_NCP * GG_LDT; i += GG_T) smem[i] = 0.0;  // padding columns stay 0
+  __syncthreads();
+  // per-thread row state: the S-hat list entry of a tile is loaded one iteration before its
+  // gathers are issued (no dependent-load stall in the issue path); rho rides in registers
+  auto row_cell = [&](int64_t tl, int* var) -> int {
+    const int64_t row = tl * GG_RT + k;
+    if (tl >= ntiles || row >= total_rows) return -1;
+    *var = (int)(row / nS);
+    return __ldg(a.list + (row - (int64_t)(*var) * nS));
+  };
+  double rq0 = 0.0, rq1 = 0.0, rq2 = 0.0;
+  auto issue = [&](int cell, int var, int st) {
+    double* tile = smem + (size_t)st * GG_NCP * GG_LDT;
+    double r = 0.0;
+    if (cell >= 0) {
+      const int64_t e = (int64_t)var * a.g.N + cell;
+      const int64_t se = sidx(slab, e);
+      for (int col = sub; col < ncol; col += NSUB) {
+        const double* src = col < nU ? a.ring + (int64_t)a.W.slot[col] * TILE + se : a.src_b.p + sidx(a.src_b, e);
+        cp_async8(tile + col * GG_LDT + k, src);
+      }
+      r = __ldg(a.rho.p + sidx(a.rho, e));
+    } else {
+      for (int col = sub; col < ncol; col += NSUB) tile[col * GG_LDT + k] = 0.0;
+    }
+    if (st == 0) rq0 = r;
+    else if (st == 1) rq1 = r;
+    else rq2 = r;
+    cp_async_commit();
+  };
+  double acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  constexpr int nsb = GG_NCP / 16, ntask = nsb * (nsb + 1) / 2;  // 15 upper super-block pairs
+  int sa = 0, rem = warp;
+  while (sa < nsb && rem >= nsb - sa) { rem -= nsb - sa; ++sa; }
+  const int sb = sa + rem;
+  const bool has_task = warp < ntask;
+  static_assert(GG_STAGES == 3, "rho registers rq0..rq2");
+  int64_t tl = blockIdx.x;
+  // prologue: GG_STAGES - 1 tiles in flight, the list entry of the next one loaded
+  {
+    int v0 = 0, v1 = 0;
+    const int c0 = row_cell(tl, &v0), c1 = row_cell(tl + gridDim.x, &v1);
+    issue(c0, v0, 0);
+    issue(c1, v1, 1);
+  }
+  int nvar = 0;
+  int ncell = row_cell(tl + (int64_t)(GG_STAGES - 1) * gridDim.x, &nvar);
+  for (int it = 0; tl < ntiles; ++it, tl += gridDim.x) {
+    const int st = it % GG_STAGES;
+    cp_async_wait<GG_STAGES - 2>();
+    // shift by rho in place (own elements: visible to this thread after the wait)
+    {
+      double* tile = smem + (size_t)st * GG_NCP * GG_LDT;
+      const double r = st == 0 ? rq0 : (st == 1 ? rq1 : rq2);
+      for (int col = sub; col < ncol; col += NSUB) tile[col * GG_LDT + k] -= r;
+    }
+    __syncthreads();
+    // next tile into the stage consumed in the previous iteration; prefetch the list entry after it
+    issue(ncell, nvar, (it + GG_STAGES - 1) % GG_STAGES);
+    ncell = row_cell(tl + (int64_t)GG_STAGES * gridDim.x, &nvar);
+    if (has_task) {
+      const double* tile = smem + (size_t)st * GG_NCP * GG_LDT;
+#pragma unroll
+      for (int kk = 0; kk < GG_RT; kk += 4) {
+        const double a0 = tile[(16 * sa + gid) * GG_LDT + kk + tig];
+        const double a1 = tile[(16 * sa + 8 + gid) * GG_LDT + kk + tig];
+        const double b0 = tile[(16 * sb + gid) * GG_LDT + kk + tig];
+        const double b1 = tile[(16 * sb + 8 + gid) * GG_LDT + kk + tig];
+        dmma(acc[0], acc[1], a0, b0);
+        dmma(acc[2], acc[3], a0, b1);
+        dmma(acc[4], acc[5], a1, b0);
+        dmma(acc[6], acc[7], a1, b1);
+      }
+    }
+    __syncthreads();  // the stage is re-filled two iterations later
+  }
+  cp_async_wait<0>();
+  double* out = a.part + (int64_t)blockIdx.x * GG_NCP * GG_NCP;
+  if (has_task) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int bi = 16 * sa + 8 * (q >> 1), bj = 16 * sb + 8 * (q & 1);
+      out[(bi + gid) * GG_NCP + bj + 2 * tig] = acc[2 * q];
+      out[(bi + gid) * GG_NCP + bj + 2 * tig + 1] = acc[2 * q + 1];
+    }
+  }
+}
+
+// lagged centring of the gathered Gram (A14): R over [U - rho, b - rho] (ld nU + 1) ->
+// K = [X_c, b_c]^T [X_c, b_c] (ld w + 1), X_c = U[:, xoff:] - psi_prev, b_c = b - psi_cur,
+// psi_prev = mean of U[:, :w], psi_cur = mean of U[:, xoff:] (xoff = nU - w)
+__global__ void centre_kernel(const double* __restrict__ R, Win W, double* __restrict__ K) {
+  __shared__ double mp[kMaxW + 2], mc[kMaxW + 2];  // row means over the psi_prev / psi_cur slots
+  __shared__ double g[3];                           // mean-mean terms: pp, pc, cc
+  const int nU = W.nU, w = W.w, xoff = nU - w, ldr = nU + 1;
+  for (int a = threadIdx.x; a <= nU; a += blockDim.x) {
+    double sp = 0.0, sc = 0.0;
+    for (int s = 0; s < w; ++s) sp += R[a * ldr + s];
+    for (int s = xoff; s < nU; ++s) sc += R[a * ldr + s];
+    mp[a] = sp / (double)w;
+    mc[a] = sc / (double)w;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double pp = 0.0, pc = 0.0, cc = 0.0;
+    for (int s = 0; s < w; ++s) pp += mp[s];
+    for (int s = 0; s < w; ++s) pc += mc[s];
+    for (int s = xoff; s < nU; ++s) cc += mc[s];
+    g[0] = pp / (double)w;
+    g[1] = pc / (double)w;
+    g[2] = cc / (double)w;
+  }
+  __syncthreads();
+  const int ldk = w + 1;
+  for (int idx = threadIdx.x; idx < ldk * ldk; idx += blockDim.x) {
+    const int i = idx / ldk, j = idx % ldk;
+    double v;
+    if (i < w && j < w) {
+      const int a = xoff + i, b = xoff + j;
+      v = ((R[a * ldr + b] - mp[a]) - mp[b]) + g[0];
+    } else if (i < w || j < w) {
+      const int a = xoff + (i < w ? i : j);  // X column against b (column nU of R)
+      v = ((R[a * ldr + nU] - mc[a]) - mp[nU]) + g[1];
+    } else {
+      v = ((R[nU * ldr + nU] - mc[nU]) - mc[nU]) + g[2];
+    }
+    K[i * ldk + j] = v;
+  }
+}
+
 // deterministic fixed-order reduction over CTAs; C[i][j] for i <= j mirrored
 __global__ void gram_reduce(const double* __restrict__ part, int nblk, int ncp, int ncol, double* __restrict__ C,
                             int ldc, const int32_t* __restrict__ map) {
@@ -427,27 +601,33 @@ hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int64_t ns, in
   return HROM_OK;
 }
 
-// gathered Gram of [X_S, b] over the rows of S-hat -> b.K ((w+1) x (w+1))
+// gathered Gram of [X_S, b] over the rows of S-hat -> b.K ((w+1) x (w+1), centred)
 hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
-  GramArgs a{};
-  a.mode = 1;
-  a.ncol = c->win.w + 1;
-  a.nsb = (c->win.w + 2 + 15) / 16;  // tile holds the raw w+1 slots + b before centring
+  GGArgs a{};
   a.g = c->g;
   a.W = c->win;
   a.ring = c->b.ring;
+  a.rho = c->rho_ref();
   a.list = c->b.lists + (int64_t)L_S * c->g.N;
   a.count = c->b.counts + L_S;
   a.src_b = src_b;
-  // while the one-CTA eigen-solve of the previous update holds an SM (side stream), size the
-  // grid to the other SMs: a static tile split with one block left over would double the time
-  const int grid = (c->basis_pending ? c->nsm - 1 : c->nsm) * 2;
-  const int ncp = a.nsb * 16;
-  if ((int64_t)grid * ncp * ncp > c->b.part_len) return HROM_E_INVALID;
+  if (a.W.nU + 1 > GG_NCP) return HROM_E_INVALID;
+  // while the one-CTA eigen-solve of the previous update holds an SM (side stream), leave it
+  // out: a static tile split with one block left over would double the time
+  const int grid = c->basis_pending ? c->nsm - 1 : c->nsm;
+  if ((int64_t)grid * GG_NCP * GG_NCP > c->b.part_len) return HROM_E_INVALID;
   a.part = c->b.part;
-  hrom_status s = dispatch_gram(c, a, grid);
-  if (s != HROM_OK) return s;
-  gram_reduce<<<64, 256, 0, c->st>>>(c->b.part, grid, ncp, a.ncol, c->b.K, a.ncol, nullptr);
+  const size_t smem = (size_t)GG_STAGES * GG_NCP * GG_LDT * sizeof(double);
+  HROM_CK(cudaFuncSetAttribute(gather_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  gather_gram_kernel<<<grid, GG_T, smem, c->st>>>(a);
+  HROM_LAUNCH_CK();
+  ++c->nlaunch;
+  const int ncol = a.W.nU + 1;
+  double* R = c->b.eigV;  // (nU+1)^2 scratch
+  gram_reduce<<<64, 256, 0, c->st>>>(c->b.part, grid, GG_NCP, ncol, R, ncol, nullptr);
+  HROM_LAUNCH_CK();
+  ++c->nlaunch;
+  centre_kernel<<<1, 256, 0, c->st>>>(R, a.W, c->b.K);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;
