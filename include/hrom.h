@@ -161,6 +161,9 @@ int64_t hrom_launch_count(const hrom_ctx* ctx);
  * [4..6] filter sweeps per order, [8] eigen sweeps (basis), [9] eigen sweeps (pinv);
  * [16 + l] the size of cell list l (0 S-hat, 1 seam band B, 2 T, 3 A2, 4 A1). */
 hrom_status hrom_debug_counters(hrom_ctx* ctx, int32_t* any_out, int32_t n);
+/* Synchronises and copies n <= 64 device timestamps (ns, %globaltimer) written by the last
+ * seam-filter launch: [0] start, [1] after the compaction prologue, [2 + s] after sweep s. */
+hrom_status hrom_debug_timers(hrom_ctx* ctx, int64_t* host_out, int32_t n);
 
 #ifdef __cplusplus
 }

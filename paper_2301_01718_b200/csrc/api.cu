@@ -122,7 +122,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   // the fused Gram row keeps one accumulator per window slot per lane: wider windows
   // (w + 1 > 68) take the full DMMA Gram every step instead
   if (c->w + 1 > fill_max_gram_slots()) c->P.gram_mode = 1;
-  c->band_blocks = c->nsm;
+  c->band_blocks = 4 * c->nsm;
   if (filter_occupancy() < 1) {  // the cooperative seam filter needs one resident block per SM
     delete c;
     return HROM_E_CUDA;
@@ -164,6 +164,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   A(dalloc(&b.ireg, 16));
   A(dalloc(&b.dreg, 16));
   A(dalloc(&b.ureg, 4));
+  A(dalloc(&b.dbg, 64));
   A(dalloc(&b.sel_val, g.N));
   A(dalloc(&b.sel_cell, g.N));
   b.blk_len = 8 * ((c->mwords + 255) / 256 + 2) + (g.N + 1023) / 1024 + 16;
@@ -216,7 +217,7 @@ void hrom_destroy(hrom_ctx* c) {
   Bufs& b = c->b;
   void* ptrs[] = {b.ring, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
                   b.kept, b.fidx, b.ftab, b.fcur, b.fF, b.C, b.part, b.gpart, b.K, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
-                  b.dreg, b.ureg, b.sel_val, b.sel_cell, b.blk, b.hist, b.fstat, b.fcnt, (void*)b.colptr, b.slot_tab};
+                  b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.fstat, b.fcnt, (void*)b.colptr, b.slot_tab};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete c;
@@ -611,6 +612,14 @@ hrom_status hrom_debug_counters(hrom_ctx* c, int32_t* any_out, int32_t n) {
   HROM_CK(cudaStreamSynchronize(c->st));
   HROM_CK(cudaMemcpy(any_out, c->b.ireg, std::min(n, 16) * sizeof(int32_t), cudaMemcpyDefault));
   if (n > 16) HROM_CK(cudaMemcpy(any_out + 16, c->b.counts, (n - 16) * sizeof(int32_t), cudaMemcpyDefault));
+  return HROM_OK;
+}
+
+hrom_status hrom_debug_timers(hrom_ctx* c, int64_t* host_out, int32_t n) {
+  if (!c || !host_out || n < 0 || n > 64) return HROM_E_INVALID;
+  basis_join(c);
+  HROM_CK(cudaStreamSynchronize(c->st));
+  HROM_CK(cudaMemcpy(host_out, c->b.dbg, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
   return HROM_OK;
 }
 

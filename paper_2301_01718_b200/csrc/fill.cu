@@ -273,32 +273,31 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
 }
 
 // C[new][U[s]] = sum over blocks of fill partials, fixed order
-__global__ void gram_row_reduce(const double* __restrict__ part, int nblk, Win W, int new_slot,
-                                double* __restrict__ C, int ldc) {
+// C row of the new slot = sum of the fill partials (+ the seam-band partials), 16 threads per
+// entry with a fixed-order tree (deterministic)
+__global__ void __launch_bounds__(1024) gram_row_reduce(const double* __restrict__ part, int nblk,
+                                                        const double* __restrict__ bpart, int nbblk, Win W,
+                                                        int new_slot, double* __restrict__ C, int ldc) {
   const int nU = W.nU;
-  for (int s = threadIdx.x; s <= nU; s += blockDim.x) {
-    double acc = 0.0;
-    for (int b = 0; b < nblk; ++b) acc += part[(int64_t)b * (nU + 1) + s];
-    if (s < nU) {
-      C[new_slot * ldc + W.slot[s]] = acc;
-      C[W.slot[s] * ldc + new_slot] = acc;
-    } else {
-      C[new_slot * ldc + new_slot] = acc;
+  constexpr int TPE = 16;
+  for (int base = 0; base < (nU + 1) * TPE; base += blockDim.x) {
+    const int idx = base + threadIdx.x, s = idx / TPE, sub = idx % TPE;
+    double a = 0.0, bsum = 0.0;
+    if (s <= nU) {
+      for (int b = sub; b < nblk; b += TPE) a += part[(int64_t)b * (nU + 1) + s];
+      if (bpart)
+        for (int b = sub; b < nbblk; b += TPE) bsum += bpart[(int64_t)b * (nU + 1) + s];
     }
-  }
-}
-
-// band partials added into the same C entries (fixed order, after the fill part)
-__global__ void band_row_add(const double* __restrict__ part, int nblk, Win W, int new_slot, double* __restrict__ C,
-                             int ldc) {
-  const int nU = W.nU;
-  for (int s = threadIdx.x; s <= nU; s += blockDim.x) {
-    double acc = 0.0;
-    for (int b = 0; b < nblk; ++b) acc += part[(int64_t)b * (nU + 1) + s];
-    const int cs_ = (s < nU) ? W.slot[s] : new_slot;
-    const double v = C[new_slot * ldc + cs_] + acc;
-    C[new_slot * ldc + cs_] = v;
-    C[cs_ * ldc + new_slot] = v;
+    for (int o = TPE / 2; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
+    }
+    if (s <= nU && sub == 0) {
+      const double v = a + bsum;
+      const int cs_ = (s < nU) ? W.slot[s] : new_slot;
+      C[new_slot * ldc + cs_] = v;
+      C[cs_ * ldc + new_slot] = v;
+    }
   }
 }
 
@@ -382,15 +381,11 @@ hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot) {
 }
 
 hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_band) {
-  gram_row_reduce<<<1, 256, 0, c->st>>>(c->b.gpart, c->fill_grid, W, new_slot, c->b.C, kMaxSlots);
+  gram_row_reduce<<<1, 1024, 0, c->st>>>(c->b.gpart, c->fill_grid,
+                                         with_band ? c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1) : nullptr,
+                                         c->band_blocks, W, new_slot, c->b.C, kMaxSlots);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
-  if (with_band) {
-    band_row_add<<<1, 256, 0, c->st>>>(c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1), c->band_blocks, W,
-                                        new_slot, c->b.C, kMaxSlots);
-    HROM_LAUNCH_CK();
-    ++c->nlaunch;
-  }
   return HROM_OK;
 }
 

@@ -42,9 +42,18 @@ struct FilterArgs {
   double* fstat;         // [grid]
   int32_t* fcnt;         // [grid]
   int32_t* sweeps_out;   // [3]
+  long long* tdbg;       // 64 timestamps (debug)
 };
 
 constexpr int FT = 512;  // filter threads per block (one block per SM)
+
+__device__ __forceinline__ void stamp(long long* t, int i) {
+  if (t && i < 64 && blockIdx.x == 0 && threadIdx.x == 0) {
+    long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    t[i] = g;
+  }
+}
 
 __device__ __forceinline__ int wrapf(int i, int n, int bc) {
   if (bc == 1) {
@@ -85,6 +94,7 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
   __shared__ int scnt[FT / 32];
   __shared__ int sscan[FT];
   __shared__ int sbase;
+  stamp(a.tdbg, 0);
   // S0: mark the halo
   for (int64_t t = gtid; t < nb; t += gstride) {
     const int64_t n = a.list[t];
@@ -169,83 +179,92 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
     }
   }
   grid.sync();
-  // Sweeps, two grid barriers each: the keep-set of sweep s (flag bit 1 + (s & 1), values in
-  // Vpp) is applied lazily by the x-pass of sweep s+1, which reads cur(m) = kept_s(m) ? Vpp(m)
-  // : cur(m) and writes its own cell; every block takes the same stop decision.
+  stamp(a.tdbg, 1);
+  // Sweeps, two grid barriers each.  The y-pass owns its cell: a kept value is written straight
+  // into cur (no other thread of that phase reads cur at a band cell -- the y-stencil reads Vp),
+  // so the next x-pass sees the applied keep-set without a separate apply phase.
+  const int32_t* __restrict__ tab = a.tab;
+  double* __restrict__ cur = a.cur;
+  double* __restrict__ Vp = a.Vp;
+  const double* __restrict__ Fb = a.Fb;
+  uint8_t* __restrict__ flag = a.flag;
+  __shared__ double s_md[FT / 32];
+  __shared__ long long s_tot[FT / 32];
   int gs = 0;  // sweeps done over all orders
   for (int oi = 0; oi < a.norders; ++oi) {
     const double* cf;
     double den;
     const int rad = shapiro(a.orders[oi], &cf, &den);
+    double cfr[7];
+#pragma unroll
+    for (int m = 0; m < 7; ++m) cfr[m] = m <= 2 * rad ? cf[m] : 0.0;
     int sweeps = 0;
     for (int sw = 0; sw < a.maxsw; ++sw, ++gs) {
       ++sweeps;
-      const uint8_t pbit = (uint8_t)(2u << ((gs + 1) & 1));  // keep bit of the previous sweep
-      const uint8_t cbit = (uint8_t)(2u << (gs & 1));        // keep bit of this sweep
       // P1: v' = S^x(cur) on B
       for (int64_t t = gtid; t < nb; t += gstride) {
         int nbr[7];
-        bool kp[7];
 #pragma unroll
-        for (int m = 0; m < 7; ++m) {
-          nbr[m] = m <= 2 * rad ? a.tab[(int64_t)(m - rad + 3) * N + t] : 0;
-          kp[m] = m <= 2 * rad && gs > 0 && (a.flag[nbr[m]] & pbit);
-        }
-        const bool own = gs > 0 && (a.flag[t] & pbit);
-        for (int var = 0; var < g.c; ++var) {
-          const int64_t vb = var * N;
-          double s = 0.0;
+        for (int m = 0; m < 7; ++m) nbr[m] = m <= 2 * rad ? __ldcg(tab + (int64_t)(m - rad + 3) * N + t) : 0;
+        double x[4][7];
 #pragma unroll
-          for (int m = 0; m < 7; ++m) {
-            if (m > 2 * rad) break;
-            const double x = kp[m] ? a.Vpp[vb + nbr[m]] : a.cur[vb + nbr[m]];
-            s += cf[m] * x;
-          }
-          a.Vp[vb + t] = s / den;
-          if (own) a.cur[vb + t] = a.Vpp[vb + t];
+        for (int var = 0; var < 4; ++var)
+#pragma unroll
+          for (int m = 0; m < 7; ++m) x[var][m] = (var < g.c && m <= 2 * rad) ? __ldcg(cur + var * N + nbr[m]) : 0.0;
+#pragma unroll
+        for (int var = 0; var < 4; ++var) {
+          if (var >= g.c) break;
+          double sx = 0.0;
+#pragma unroll
+          for (int m = 0; m < 7; ++m)
+            if (m <= 2 * rad) sx += cfr[m] * x[var][m];
+          Vp[var * N + t] = sx / den;
         }
       }
       grid.sync();
-      // P2: v'' = S^y(v') on B, residual gate
+      // P2: v'' = S^y(v') on B, residual gate, kept values applied in place
       double mdec = 0.0;
       int cnt = 0;
       for (int64_t t = gtid; t < nb; t += gstride) {
         int nbr[7];
 #pragma unroll
-        for (int m = 0; m < 7; ++m) nbr[m] = (g.dim == 2 && m <= 2 * rad) ? a.tab[(int64_t)(7 + m - rad + 3) * N + t] : 0;
+        for (int m = 0; m < 7; ++m)
+          nbr[m] = (g.dim == 2 && m <= 2 * rad) ? __ldcg(tab + (int64_t)(7 + m - rad + 3) * N + t) : 0;
+        double own[4], fe[4], y[4][7];
+#pragma unroll
+        for (int var = 0; var < 4; ++var) {
+          own[var] = var < g.c ? __ldcg(cur + var * N + t) : 0.0;
+          fe[var] = var < g.c ? __ldcg(Fb + var * N + t) : 0.0;
+#pragma unroll
+          for (int m = 0; m < 7; ++m) y[var][m] = (g.dim == 2 && var < g.c && m <= 2 * rad) ? __ldcg(Vp + var * N + nbr[m]) : 0.0;
+        }
         double rold = 0.0, rnew = 0.0;
         double vpp[4];
 #pragma unroll
         for (int var = 0; var < 4; ++var) {
           if (var >= g.c) break;
-          const int64_t vb = var * N;
-          double x;
+          double xv;
           if (g.dim == 2) {
-            double s = 0.0;
+            double sy = 0.0;
 #pragma unroll
-            for (int m = 0; m < 7; ++m) {
-              if (m > 2 * rad) break;
-              s += cf[m] * a.Vp[vb + nbr[m]];
-            }
-            x = s / den;
+            for (int m = 0; m < 7; ++m)
+              if (m <= 2 * rad) sy += cfr[m] * y[var][m];
+            xv = sy / den;
           } else {
-            x = a.Vp[vb + t];
+            xv = __ldcg(Vp + var * N + t);  // 1-D: no y-pass
           }
-          vpp[var] = x;
-          const double fe = a.Fb[vb + t];
-          rold = fmax(rold, fabs(a.cur[vb + t] - fe));
-          rnew = fmax(rnew, fabs(x - fe));
+          vpp[var] = xv;
+          rold = fmax(rold, fabs(own[var] - fe[var]));
+          rnew = fmax(rnew, fabs(xv - fe[var]));
         }
-        uint8_t fl = (uint8_t)(a.flag[t] & ~(pbit | cbit));
         if (rnew < rold) {
 #pragma unroll
           for (int var = 0; var < 4; ++var)
-            if (var < g.c) a.Vpp[var * N + t] = vpp[var];
-          fl |= (uint8_t)(cbit | 1u);
+            if (var < g.c) cur[var * N + t] = vpp[var];
+          if (!(flag[t] & 1)) flag[t] = 1;
           mdec = fmax(mdec, (rold - rnew) / rold);
           ++cnt;
         }
-        a.flag[t] = fl;
       }
       for (int o = 16; o > 0; o >>= 1) {
         mdec = fmax(mdec, __shfl_xor_sync(0xffffffffu, mdec, o));
@@ -267,31 +286,47 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
         a.fcnt[blockIdx.x] = c;
       }
       grid.sync();
-      // identical stop decision in every block (fixed-order reduction of the block stats)
-      double md = 0.0;
-      long long tot = 0;
-      for (int b = 0; b < (int)gridDim.x; ++b) {
-        md = fmax(md, a.fstat[b]);
-        tot += a.fcnt[b];
-      }
-      if (tot == 0 || md < a.eps_f) {
-        ++gs;
-        break;
+      // identical stop decision in every block (max and integer sum: order-independent)
+      {
+        double md = 0.0;
+        long long tot = 0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+          md = fmax(md, __ldcg(a.fstat + b));
+          tot += __ldcg(a.fcnt + b);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
+          tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+          s_md[threadIdx.x >> 5] = md;
+          s_tot[threadIdx.x >> 5] = tot;
+        }
+        __syncthreads();
+        md = 0.0;
+        tot = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+          md = fmax(md, s_md[k]);
+          tot += s_tot[k];
+        }
+        __syncthreads();  // s_md / s_tot are rewritten by the next sweep
+        stamp(a.tdbg, 2 + gs);
+        if (tot == 0 || md < a.eps_f) {
+          ++gs;
+          break;
+        }
       }
     }
     if (gtid == 0 && a.sweeps_out) a.sweeps_out[oi] = sweeps;
   }
-  // apply the last pending keep-set, write the kept band values back, and the indicator on
-  // kept band cells: eps_n = sum_v (v - (psi + Phi y))^2 (pre-filter value = psi + Phi y)
-  const uint8_t pbit = (uint8_t)(2u << ((gs + 1) & 1));
+  // write the kept band values back, and the indicator on kept band cells:
+  // eps_n = sum_v (v - (psi + Phi y))^2 (pre-filter value = psi + Phi y)
   for (int64_t t = gtid; t < nb; t += gstride) {
-    const uint8_t fl = a.flag[t];
-    if (!(fl & 1)) continue;
+    if (!(flag[t] & 1)) continue;
     const int64_t n = a.list[t];
-    const bool pend = gs > 0 && (fl & pbit);
     double s = 0.0;
     for (int var = 0; var < g.c; ++var) {
-      const double x = pend ? a.Vpp[var * N + t] : a.cur[var * N + t];
+      const double x = cur[var * N + t];
       a.v.p[sidx(a.v, var * N + n)] = x;
       const double d = x - a.cur0[var * N + t];
       s += d * d;
@@ -301,71 +336,61 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
   }
 }
 
-// Gram-row contributions of the band DOFs (final values), partials after the fill blocks
-__global__ void __launch_bounds__(256) band_gram_kernel(Geo g, Win W, const double* __restrict__ ring,
-                                                        const SRef rho, const SRef v,
-                                                        const int32_t* __restrict__ list,
-                                                        const int32_t* __restrict__ count, double* __restrict__ part) {
-  constexpr int CH = 128;
-  constexpr int SPW = (kMaxW + 2 + 7) / 8;
-  __shared__ double gt[CH], rh[CH];
-  __shared__ int64_t es[CH];
-  __shared__ double wsum[8];
+// Gram-row contributions of the band DOFs (final values), partials after the fill blocks:
+// part[blk][s] = sum_e x_e (col_s(e) - rho_e), part[blk][nU] = sum_e x_e^2, x = v - rho.
+// Four threads per DOF, each owning every fourth window slot: up to 17 independent slab
+// loads in flight per thread (the loads are scattered: one 32-byte sector per slot and DOF).
+constexpr int BG_T = 256;
+constexpr int BG_Q = 4;                            // threads per DOF
+__global__ void __launch_bounds__(BG_T) band_gram_kernel(Geo g, Win W, const double* __restrict__ ring,
+                                                         const SRef rho, const SRef v,
+                                                         const int32_t* __restrict__ list,
+                                                         const int32_t* __restrict__ count, double* __restrict__ part) {
+  constexpr int SPT = 17;  // nU <= 68 (the fused Gram row is limited to fill_max_gram_slots())
+  __shared__ double red[BG_T / 32][BG_Q * SPT + 1];
   const int nU = W.nU;
   const int nb = *count;
   const int64_t total = (int64_t)nb * g.c;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double acc[SPW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, q = lane & (BG_Q - 1);
+  const SRef slab{nullptr, g.nsr};
+  double acc[SPT];
 #pragma unroll
-  for (int q = 0; q < SPW; ++q) acc[q] = 0.0;
+  for (int j = 0; j < SPT; ++j) acc[j] = 0.0;
   double self = 0.0;
-  for (int64_t base = (int64_t)blockIdx.x * CH; base < total; base += (int64_t)gridDim.x * CH) {
-    if (threadIdx.x < CH) {
-      const int64_t t = base + threadIdx.x;
-      if (t < total) {
-        const int var = (int)(t / nb), idx = (int)(t % nb);
-        const int64_t e = (int64_t)var * g.N + list[idx];
-        const double r = rho.p[sidx(rho, e)];
-        const double x = v.p[sidx(v, e)] - r;
-        gt[threadIdx.x] = x;
-        rh[threadIdx.x] = r;
-        es[threadIdx.x] = sidx(SRef{nullptr, g.nsr}, e);  // slab offset within a ring slot
-        self += x * x;
-      } else {
-        gt[threadIdx.x] = 0.0;
-        rh[threadIdx.x] = 0.0;
-        es[threadIdx.x] = -1;
-      }
-    }
-    __syncthreads();
+  const int64_t per_pass = (int64_t)gridDim.x * (BG_T / BG_Q);
+  for (int64_t t = (int64_t)blockIdx.x * (BG_T / BG_Q) + (threadIdx.x / BG_Q); t < total; t += per_pass) {
+    const int var = (int)(t / nb), idx = (int)(t - (int64_t)var * nb);
+    const int64_t e = (int64_t)var * g.N + list[idx];
+    const double r = rho.p[sidx(rho, e)];
+    const double x = v.p[sidx(v, e)] - r;
+    const int64_t se = sidx(slab, e);
+    double val[SPT];
 #pragma unroll
-    for (int q = 0; q < SPW; ++q) {
-      const int s = warp + q * 8;
-      if (s < nU) {
-        const double* col = ring + (int64_t)W.slot[s] * TILE;
-        double sacc = 0.0;
-        for (int el = lane; el < CH; el += 32)
-          if (es[el] >= 0) sacc += gt[el] * (col[es[el]] - rh[el]);
-        acc[q] += sacc;
-      }
+    for (int j = 0; j < SPT; ++j) {
+      const int sl = q + BG_Q * j;
+      val[j] = sl < nU ? __ldg(ring + (int64_t)W.slot[sl] * TILE + se) : r;
     }
-    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < SPT; ++j) acc[j] += x * (val[j] - r);
+    if (q == 0) self += x * x;
   }
-  double* out = part + (int64_t)blockIdx.x * (nU + 1);
 #pragma unroll
-  for (int q = 0; q < SPW; ++q) {
-    double x = acc[q];
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    const int s = warp + q * 8;
-    if (lane == 0 && s < nU) out[s] = x;
+  for (int j = 0; j < SPT; ++j) {
+    double y = acc[j];
+    y += __shfl_xor_sync(0xffffffffu, y, 4);
+    y += __shfl_xor_sync(0xffffffffu, y, 8);
+    y += __shfl_xor_sync(0xffffffffu, y, 16);
+    if (lane < BG_Q) red[warp][lane + BG_Q * j] = y;
   }
   for (int o = 16; o > 0; o >>= 1) self += __shfl_xor_sync(0xffffffffu, self, o);
-  if (lane == 0) wsum[warp] = self;
+  if (lane == 0) red[warp][BG_Q * SPT] = self;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int k = 0; k < 8; ++k) s += wsum[k];
-    out[nU] = s;
+  double* out = part + (int64_t)blockIdx.x * (nU + 1);
+  for (int sl = threadIdx.x; sl <= nU; sl += BG_T) {
+    const int col = sl < nU ? sl : BG_Q * SPT;
+    double y = 0.0;
+    for (int w8 = 0; w8 < BG_T / 32; ++w8) y += red[w8][col];
+    out[sl] = y;
   }
 }
 
@@ -401,6 +426,7 @@ hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F, uint8_t* kept_cells) {
   a.fstat = c->b.fstat;
   a.fcnt = c->b.fcnt;
   a.sweeps_out = c->b.ireg + 4;
+  a.tdbg = c->b.dbg;
   HROM_CK(cudaMemsetAsync(a.mH, 0, (size_t)c->g.ny * c->g.wpr * sizeof(uint32_t), c->st));
   if (kept_cells) HROM_CK(cudaMemsetAsync(kept_cells, 0, c->g.N, c->st));
   void* args[] = {&a};
@@ -410,7 +436,8 @@ hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F, uint8_t* kept_cells) {
 }
 
 hrom_status launch_band_gram(hrom_ctx* c, const Win& W, SRef v) {
-  band_gram_kernel<<<c->band_blocks, 256, 0, c->st>>>(c->g, W, c->b.ring, c->rho_ref(), v,
+  if (W.nU > 68) return HROM_E_INVALID;  // covered by the fused-row limit (fill_max_gram_slots)
+  band_gram_kernel<<<c->band_blocks, BG_T, 0, c->st>>>(c->g, W, c->b.ring, c->rho_ref(), v,
                                                        c->b.lists + (int64_t)L_B * c->g.N, c->b.counts + L_B,
                                                        c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1));
   HROM_LAUNCH_CK();

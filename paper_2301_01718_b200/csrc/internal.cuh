@@ -107,6 +107,7 @@ struct Bufs {
   int32_t* ireg = nullptr;    // small int registers: [0] reff, [1] err cell lo, ...
   double* dreg = nullptr;     // small double registers: [0] dt, ...
   unsigned long long* ureg = nullptr;  // [0] smax bits, [1] min bad cell
+  long long* dbg = nullptr;   // 64 debug timestamps (seam filter)
   // sampling scratch
   double* sel_val = nullptr;   // N
   int32_t* sel_cell = nullptr; // N

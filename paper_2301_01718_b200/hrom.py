@@ -72,6 +72,7 @@ _SIGS = {
     "hrom_profile_read": (C.c_int, [_VP, _VP, _VP, C.c_int32]),
     "hrom_launch_count": (C.c_int64, [_VP]),
     "hrom_debug_counters": (C.c_int, [_VP, _VP, C.c_int32]),
+    "hrom_debug_timers": (C.c_int, [_VP, _VP, C.c_int32]),
 }
 
 SECTIONS = ["dt", "masked_rk3", "gathered_gram", "pinv_solve", "fill_pass", "indicator", "seam_filter",
@@ -269,6 +270,11 @@ class HybridROM:
 
     def launch_count(self) -> int:
         return int(self.lib.hrom_launch_count(self.h))
+
+    def debug_timers(self, n: int = 32):
+        out = (C.c_int64 * n)()
+        _ck(self.lib.hrom_debug_timers(self.h, C.cast(out, C.c_void_p), n), "hrom_debug_timers")
+        return list(out)
 
     def debug_counters(self, n: int = 8):
         out = (C.c_int32 * n)()
