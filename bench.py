@@ -79,6 +79,26 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": rows[0][1], "reasons": sorted(reasons), "samples": len(rows)}
 
 
+def rank_seed(config: int, rank: int) -> int:
+    """Each rank runs an independent problem of the same shape (weak scaling)."""
+    return config + 1000 * rank
+
+
+def reduce_max_over_ranks(vals, dist=None, device="cpu"):
+    """Max over ranks of the per-rank device times (the only collective of the bench)."""
+    if dist is None:
+        return [float(v) for v in vals]
+    import torch
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.cpu()]
+
+
+def whole_job_value(cells_per_rank: int, world: int, ms_step: float) -> float:
+    """Whole-job cell-updates/s: the cells of all ranks over the slowest rank's step time."""
+    return cells_per_rank * world / (ms_step / 1000.0)
+
+
 def fill_bytes(wl, n_s: int) -> int:
     """Algorithmic bytes of one fill-pass launch: read the w+1 window
     columns and the Gram shift, write gamma_k; read the partial-HDM values and write the
@@ -97,7 +117,7 @@ def run_hrom(args, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
-    wl = inputs.config(args.config, f=args.fraction, seed=args.config + 1000 * rank)
+    wl = inputs.config(args.config, f=args.fraction, seed=rank_seed(args.config, rank))
     q0 = inputs.initial_condition(wl)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
@@ -171,13 +191,10 @@ def run_hrom(args, rank, world, local_rank):
         fs.close()
     # max over ranks
     ms_step = ms_total / args.steps
-    if dist:
-        t = torch.tensor([ms_step, ms_e2e], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step, ms_e2e = float(t[0]), float(t[1])
+    ms_step, ms_e2e = reduce_max_over_ranks([ms_step, ms_e2e], dist, "cuda")
     out = None
     if rank == 0:
-        value = wl.N * world / (ms_step / 1000.0)
+        value = whole_job_value(wl.N, world, ms_step)
         peak, peak_src = measured_peaks()
         fill_ms, fill_n = sec["fill_pass"]
         fb = fill_bytes(wl, n_s)
@@ -216,7 +233,7 @@ def run_hrom(args, rank, world, local_rank):
             "section_ms_per_step": split,
             "full_step": {"ms": ms_full, "cell_updates_per_s": wl.N / (ms_full / 1000.0)},
             "clocks": ck,
-            "e2e": {"value": wl.N * world / (ms_e2e / 1000.0), "unit": "cell-updates/s",
+            "e2e": {"value": whole_job_value(wl.N, world, ms_e2e), "unit": "cell-updates/s",
                     "h2d_bytes_per_step": wl.D * 8, "d2h_bytes_per_step": wl.D * 8, "ms_per_step": ms_e2e,
                     "steps": e2e_steps},
             "gpu_launches": int(launches),
