@@ -327,48 +327,6 @@ __global__ void __launch_bounds__(GG_T, 1) gather_gram_kernel(GGArgs a) {
   }
 }
 
-// lagged centring of the gathered Gram (A14): R over [U - rho, b - rho] (ld nU + 1) ->
-// K = [X_c, b_c]^T [X_c, b_c] (ld w + 1), X_c = U[:, xoff:] - psi_prev, b_c = b - psi_cur,
-// psi_prev = mean of U[:, :w], psi_cur = mean of U[:, xoff:] (xoff = nU - w)
-__global__ void centre_kernel(const double* __restrict__ R, Win W, double* __restrict__ K) {
-  __shared__ double mp[kMaxW + 2], mc[kMaxW + 2];  // row means over the psi_prev / psi_cur slots
-  __shared__ double g[3];                           // mean-mean terms: pp, pc, cc
-  const int nU = W.nU, w = W.w, xoff = nU - w, ldr = nU + 1;
-  for (int a = threadIdx.x; a <= nU; a += blockDim.x) {
-    double sp = 0.0, sc = 0.0;
-    for (int s = 0; s < w; ++s) sp += R[a * ldr + s];
-    for (int s = xoff; s < nU; ++s) sc += R[a * ldr + s];
-    mp[a] = sp / (double)w;
-    mc[a] = sc / (double)w;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double pp = 0.0, pc = 0.0, cc = 0.0;
-    for (int s = 0; s < w; ++s) pp += mp[s];
-    for (int s = 0; s < w; ++s) pc += mc[s];
-    for (int s = xoff; s < nU; ++s) cc += mc[s];
-    g[0] = pp / (double)w;
-    g[1] = pc / (double)w;
-    g[2] = cc / (double)w;
-  }
-  __syncthreads();
-  const int ldk = w + 1;
-  for (int idx = threadIdx.x; idx < ldk * ldk; idx += blockDim.x) {
-    const int i = idx / ldk, j = idx % ldk;
-    double v;
-    if (i < w && j < w) {
-      const int a = xoff + i, b = xoff + j;
-      v = ((R[a * ldr + b] - mp[a]) - mp[b]) + g[0];
-    } else if (i < w || j < w) {
-      const int a = xoff + (i < w ? i : j);  // X column against b (column nU of R)
-      v = ((R[a * ldr + nU] - mc[a]) - mp[nU]) + g[1];
-    } else {
-      v = ((R[nU * ldr + nU] - mc[nU]) - mc[nU]) + g[2];
-    }
-    K[i * ldk + j] = v;
-  }
-}
-
 // deterministic fixed-order reduction over CTAs; C[i][j] for i <= j mirrored
 __global__ void gram_reduce(const double* __restrict__ part, int nblk, int ncp, int ncol, double* __restrict__ C,
                             int ldc, const int32_t* __restrict__ map) {
@@ -469,67 +427,209 @@ __global__ void __launch_bounds__(512) basis_kernel(const double* __restrict__ C
   for (int i = tid; i < w; i += blockDim.x) lam_out[i] = E.lam[i];
 }
 
-// H5: G = A^T K_XX A, rhs = A^T K_Xb, y = G^+ rhs (cut on lambda), c = A y
-__global__ void __launch_bounds__(512) solve_kernel(const double* __restrict__ K, int w, int r,
-                                                    const double* __restrict__ A, const int32_t* __restrict__ reffp,
-                                                    double cut, double* __restrict__ y_out,
-                                                    double* __restrict__ c_out, int32_t* __restrict__ status,
-                                                    double* __restrict__ gfac, bool fac_smem) {
+// H5 (one CTA): K = lagged centring of the gathered R (A14), G = A^T K_XX A, g = A^T K_Xb,
+// y = G^+ g with the 1e-12 cut on lambda (A13), c = A y.
+// Fast path: Cholesky G = L L^T.  lambda_min >= 1 / trace(G^-1) = 1 / ||L^-1||_F^2 and
+// lambda_max <= ||G||_F, so when 1 / ||L^-1||_F^2 >= 1e-10 ||G||_F no eigenvalue is within
+// two orders of magnitude of the cut and y = G^-1 g exactly; otherwise the eigen route (eig.cuh).
+constexpr int SV_T = 256;
+struct SolveLayout {
+  size_t ks, as, t, mp, mc, lm, li, vec, eig, total;  // offsets in doubles
+  bool ks_smem;                                       // K in smem (else the global scratch)
+};
+__host__ __device__ inline SolveLayout solve_layout(int w, int r, bool ks_smem) {
+  SolveLayout S;
+  S.ks_smem = ks_smem;
+  S.ks = 0;
+  S.as = S.ks + (ks_smem ? (size_t)(w + 1) * (w + 1) : 0);
+  S.t = S.as + (size_t)w * r;
+  // T (w x r) is dead once G is formed: the Cholesky factor and its inverse (r x r each) reuse it
+  const size_t treg = (size_t)w * r > (size_t)2 * r * r ? (size_t)w * r : (size_t)2 * r * r;
+  S.lm = S.t;
+  S.li = S.t + (size_t)r * r;
+  S.mp = S.t + treg;
+  S.mc = S.mp + (kMaxW + 2);
+  S.vec = S.mc + (kMaxW + 2);           // rhs, y, u, misc: 4 * kMaxSlots
+  S.eig = S.vec + 4 * kMaxSlots;
+  S.total = S.eig;                       // + EigLayout(r).doubles
+  return S;
+}
+
+__global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ R, Win W, int r,
+                                                     const double* __restrict__ A, const int32_t* __restrict__ reffp,
+                                                     double cut, double* __restrict__ y_out,
+                                                     double* __restrict__ c_out, int32_t* __restrict__ status,
+                                                     double* __restrict__ gfac, bool fac_smem,
+                                                     double* __restrict__ Kg, bool ks_smem) {
   extern __shared__ double sm[];
   const int re = *reffp;
-  const int ldk = w + 1;
+  const int w = W.w, nU = W.nU, xoff = nU - w, ldr = nU + 1, ldk = w + 1, ldl = re;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const SolveLayout S = solve_layout(w, r, ks_smem);
+  double* Ks = ks_smem ? sm + S.ks : Kg;
+  double* As = sm + S.as;  // A[j * w + i]
+  double* T = sm + S.t;
+  double* mp = sm + S.mp;
+  double* mc = sm + S.mc;
+  double* Lm = sm + S.lm;
+  double* Li = sm + S.li;
+  double* rhs = sm + S.vec;
+  double* y = rhs + kMaxSlots;
+  double* u = y + kMaxSlots;
+  double* misc = u + kMaxSlots;
   EigLayout L = eig_layout(re > 0 ? re : 1, re > 0 ? re : 1);
   L.fac_smem = fac_smem;  // the host sized the smem for r >= r_eff: its choice is safe
   const int ldn = L.ldn;
-  double* T = sm;                       // w x re  (K_XX A)
-  double* G = T + (size_t)w * kMaxR;    // eigen workspace starts here
+  double* G = sm + S.eig;
   const EigWork E = eig_work(G, re > 0 ? re : 1, L, gfac);
-  double* rhs = E.lam + kMaxSlots;
-  double* y = rhs + kMaxSlots;
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < w * re; idx += blockDim.x) {
+  __shared__ double gm[3];
+  __shared__ int s_fast;
+  // ---- centring of R into K (same algebra as the window Gram, A14) ----
+  for (int i = tid; i < w * re; i += nt) As[i] = A[(i / w) * w + (i % w)];
+  for (int a = tid; a <= nU; a += nt) {
+    double sp = 0.0, sc = 0.0;
+    for (int q = 0; q < w; ++q) sp += R[a * ldr + q];
+    for (int q = xoff; q < nU; ++q) sc += R[a * ldr + q];
+    mp[a] = sp / (double)w;
+    mc[a] = sc / (double)w;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double pp = 0.0, pc = 0.0, cc = 0.0;
+    for (int q = 0; q < w; ++q) pp += mp[q];
+    for (int q = 0; q < w; ++q) pc += mc[q];
+    for (int q = xoff; q < nU; ++q) cc += mc[q];
+    gm[0] = pp / (double)w;
+    gm[1] = pc / (double)w;
+    gm[2] = cc / (double)w;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < ldk * ldk; idx += nt) {
+    const int i = idx / ldk, j = idx % ldk;
+    double v;
+    if (i < w && j < w) {
+      const int a = xoff + i, b = xoff + j;
+      v = ((R[a * ldr + b] - mp[a]) - mp[b]) + gm[0];
+    } else if (i < w || j < w) {
+      const int a = xoff + (i < w ? i : j);
+      v = ((R[a * ldr + nU] - mc[a]) - mp[nU]) + gm[1];
+    } else {
+      v = ((R[nU * ldr + nU] - mc[nU]) - mc[nU]) + gm[2];
+    }
+    Ks[i * ldk + j] = v;
+  }
+  __syncthreads();
+  // ---- T = K_XX A, g = A^T K_Xb, G = A^T T ----
+  for (int idx = tid; idx < w * re; idx += nt) {
     const int i = idx % w, j = idx / w;
     double s = 0.0;
-    for (int p = 0; p < w; ++p) s += K[i * ldk + p] * A[j * w + p];
+    for (int p = 0; p < w; ++p) s += Ks[i * ldk + p] * As[j * w + p];
     T[j * w + i] = s;
   }
-  for (int j = tid; j < re; j += blockDim.x) {
+  for (int j = tid; j < re; j += nt) {
     double s = 0.0;
-    for (int p = 0; p < w; ++p) s += A[j * w + p] * K[p * ldk + w];
+    for (int p = 0; p < w; ++p) s += As[j * w + p] * Ks[p * ldk + w];
     rhs[j] = s;
   }
   __syncthreads();
-  for (int idx = tid; idx < re * re; idx += blockDim.x) {
+  for (int idx = tid; idx < re * re; idx += nt) {
     const int i = idx / re, j = idx % re;
     if (j < i) continue;
     double s = 0.0;
-    for (int p = 0; p < w; ++p) s += A[i * w + p] * T[j * w + p];
+    for (int p = 0; p < w; ++p) s += As[i * w + p] * T[j * w + p];
     G[i * ldn + j] = s;
     G[j * ldn + i] = s;
   }
   __syncthreads();
-  const int nk = re > 0 ? sym_eig(G, re, ldn, E, re, cut) : 0;
-  if (tid == 0) {
-    *status = (re == 0 || !(E.lam[0] > 0.0)) ? 1 : 0;
-    status[7] = 0;
-  }
-  // y = sum_{kept} z_k (z_k^T rhs) / lam_k
-  for (int kk = tid; kk < nk; kk += blockDim.x) {
-    double d = 0.0;
-    for (int p = 0; p < re; ++p) d += E.Z[p * E.ldz + kk] * rhs[p];
-    E.pp[kk] = d / E.lam[kk];
-  }
+  for (int idx = tid; idx < re * re; idx += nt) Lm[idx] = G[(idx / re) * ldn + idx % re];  // T is dead now
   __syncthreads();
-  for (int i = tid; i < re; i += blockDim.x) {
-    double s = 0.0;
-    for (int kk = 0; kk < nk; ++kk) s += E.Z[i * E.ldz + kk] * E.pp[kk];
-    y[i] = s;
+  // ---- fast path: Cholesky + trace(G^-1) bound ----
+  bool ok = re > 0;
+  for (int j = 0; j < re && ok; ++j) {
+    const double djj = Lm[j * ldl + j];
+    if (!(djj > 0.0)) {
+      ok = false;  // uniform: every thread read the same value
+      break;
+    }
+    const double ljj = sqrt(djj);
+    for (int i = j + 1 + tid; i < re; i += nt) Lm[i * ldl + j] /= ljj;
+    __syncthreads();
+    if (tid == 0) Lm[j * ldl + j] = ljj;
+    const int m = re - j - 1;
+    for (int idx = tid; idx < m * m; idx += nt) {
+      const int i = j + 1 + idx / m, k = j + 1 + idx % m;
+      if (k <= i) Lm[i * ldl + k] -= Lm[i * ldl + j] * Lm[k * ldl + j];
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  for (int i = tid; i < kMaxR; i += blockDim.x) y_out[i] = (i < re) ? y[i] : 0.0;
-  for (int i = tid; i < w; i += blockDim.x) {
+  if (ok) {
+    // Li = L^-1 (lower), one thread per column
+    for (int cc = tid; cc < re; cc += nt) {
+      for (int i = 0; i < cc; ++i) Li[i * ldl + cc] = 0.0;
+      for (int i = cc; i < re; ++i) {
+        double s = (i == cc) ? 1.0 : 0.0;
+        for (int k = cc; k < i; ++k) s -= Lm[i * ldl + k] * Li[k * ldl + cc];
+        Li[i * ldl + cc] = s / Lm[i * ldl + i];
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double tr = 0.0, gf = 0.0;
+      for (int i = lane; i < re; i += 32)
+        for (int k = 0; k < re; ++k) {
+          tr += Li[i * ldl + k] * Li[i * ldl + k];
+          gf += G[i * ldn + k] * G[i * ldn + k];
+        }
+      for (int o = 16; o > 0; o >>= 1) {
+        tr += __shfl_xor_sync(0xffffffffu, tr, o);
+        gf += __shfl_xor_sync(0xffffffffu, gf, o);
+      }
+      if (lane == 0) s_fast = (tr > 0.0 && isfinite(tr) && 1.0 / tr >= 1e-10 * sqrt(gf)) ? 1 : 0;
+    }
+    __syncthreads();
+    ok = s_fast != 0;
+  }
+  if (ok) {
+    for (int i = tid; i < re; i += nt) {
+      double s = 0.0;
+      for (int k = 0; k <= i; ++k) s += Li[i * ldl + k] * rhs[k];
+      u[i] = s;
+    }
+    __syncthreads();
+    for (int k = tid; k < re; k += nt) {
+      double s = 0.0;
+      for (int i = k; i < re; ++i) s += Li[i * ldl + k] * u[i];
+      y[k] = s;
+    }
+    if (tid == 0) {
+      *status = 0;
+      status[7] = 0;  // fast path
+    }
+    __syncthreads();
+  } else {
+    const int nk = re > 0 ? sym_eig(G, re, ldn, E, re, cut) : 0;
+    if (tid == 0) {
+      *status = (re == 0 || !(E.lam[0] > 0.0)) ? 1 : 0;
+      status[7] = 1;  // eigen route
+    }
+    // y = sum_{kept} z_k (z_k^T rhs) / lam_k
+    for (int kk = tid; kk < nk; kk += nt) {
+      double d = 0.0;
+      for (int p = 0; p < re; ++p) d += E.Z[p * E.ldz + kk] * rhs[p];
+      misc[kk] = d / E.lam[kk];
+    }
+    __syncthreads();
+    for (int i = tid; i < re; i += nt) {
+      double s = 0.0;
+      for (int kk = 0; kk < nk; ++kk) s += E.Z[i * E.ldz + kk] * misc[kk];
+      y[i] = s;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < kMaxR; i += nt) y_out[i] = (i < re) ? y[i] : 0.0;
+  for (int i = tid; i < w; i += nt) {
     double s = 0.0;
-    for (int j = 0; j < re; ++j) s += A[j * w + i] * y[j];
+    for (int j = 0; j < re; ++j) s += As[j * w + i] * y[j];
     c_out[i] = s;
   }
 }
@@ -627,19 +727,18 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   gram_reduce<<<64, 256, 0, c->st>>>(c->b.part, grid, GG_NCP, ncol, R, ncol, nullptr);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
-  centre_kernel<<<1, 256, 0, c->st>>>(R, a.W, c->b.K);
-  HROM_LAUNCH_CK();
-  ++c->nlaunch;
-  return HROM_OK;
+  return HROM_OK;  // the lagged centring of R is applied by solve_kernel
 }
 
 hrom_status small_solve(hrom_ctx* c) {
   // the solve reads r_eff on the device: size the workspace for the largest possible (r)
   const EigLayout L = eig_layout(c->r, c->r);
-  const size_t smem = ((size_t)c->win.w * kMaxR) * sizeof(double) + L.bytes;
+  SolveLayout S = solve_layout(c->win.w, c->r, true);
+  if ((S.total * sizeof(double) + L.bytes) > 220 * 1024) S = solve_layout(c->win.w, c->r, false);  // wide windows
+  const size_t smem = S.total * sizeof(double) + L.bytes;
   HROM_CK(cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  solve_kernel<<<1, 256, smem, c->st>>>(c->b.K, c->win.w, c->r, c->b.A, c->b.ireg, c->P.lsq_rel_cutoff, c->b.y,
-                                        c->b.cvec, c->b.ireg + 2, c->b.eigA, L.fac_smem);
+  solve_kernel<<<1, SV_T, smem, c->st>>>(c->b.eigV, c->win, c->r, c->b.A, c->b.ireg, c->P.lsq_rel_cutoff, c->b.y,
+                                         c->b.cvec, c->b.ireg + 2, c->b.eigA, L.fac_smem, c->b.K, S.ks_smem);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;

@@ -297,3 +297,26 @@ def test_seam_filter_parity(orc, inputs, dim, nx, ny, bc, frac, seed):
     assert list(cnt[4:4 + len(sweeps)]) == list(sweeps)
     assert rel(vg.cpu().numpy(), out) <= 1e-14
     assert np.array_equal(vg.cpu().numpy()[:, kept == 0], v[:, kept == 0])
+
+
+@pytest.mark.parametrize("ncells,w,r", [(1, 10, 8), (2, 12, 10)])
+def test_rank_deficient_gappy_solve(orc, inputs, ncells, w, r):
+    """H5 with fewer sampled rows than modes (c*|S-hat| < r_eff): G is singular, the solve takes
+    the eigen route with the 1e-12 cut (A13) and returns the min-norm y; the filled state matches
+    the oracle's min-norm LSQ (QR + SVD) step."""
+    wl = small2d(inputs, w=w, r=r, nx=40, ny=30)
+    snaps, _ = _replay_case(orc, inputs, wl, seed=11)
+    S = np.zeros(wl.N, np.uint8)
+    S[np.linspace(wl.N // 5, wl.N - wl.N // 5, ncells).astype(int)] = 1
+    k = wl.w + 3
+    R = orc.Run(wl, snaps[0])
+    R.set_window(k, snaps, S)
+    rom = H.HybridROM(wl)
+    rom.set_window(k, dev(snaps.reshape(wl.w + 1, -1)), _mask_dev(wl, S))
+    assert wl.c * ncells < rom.effective_rank()
+    dt = orc.dt(wl, snaps[-1])
+    R.step(dt)
+    rom.hybrid_step(dt=dt)
+    rom.sync()
+    assert rom.debug_counters(10)[9] == 1  # eigen route taken
+    assert rel(rom.get_state().cpu().numpy(), R.state()) <= 1e-12
