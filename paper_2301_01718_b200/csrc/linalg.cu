@@ -9,6 +9,7 @@
 #include <algorithm>
 #include "internal.cuh"
 #include "eig.cuh"
+#include "async.cuh"
 
 namespace hrom {
 namespace {
@@ -195,25 +196,25 @@ __global__ void __launch_bounds__(GT, (TPW <= 2) ? 2 : 1) gram_kernel(GramArgs a
   }
 }
 
-// ---------------- H4: gathered Gram of the S-hat rows, cp.async pipeline ----------------
+// ---------------- H4: gathered Gram of the S-hat rows ----------------
 // R = [U - rho, b - rho]^T [U - rho, b - rho] over the c |S-hat| rows (U: the nU union slots in
 // window order, b: the HDM value, rho: the Gram shift); the lagged centring (A14) is applied to
-// the small R afterwards (centre_kernel), exactly as for the window Gram C.  One CTA per SM
-// with GG_STAGES tiles in flight: each thread issues its 8-byte cp.async gathers for the tile
-// GG_STAGES-1 ahead, so the scattered loads overlap the DMMA of the current tile.
-constexpr int GG_T = 512;        // threads
-constexpr int GG_RT = 64;        // rows per tile
-constexpr int GG_LDT = GG_RT + 4;
-constexpr int GG_STAGES = 3;
-constexpr int GG_NCP = 80;       // padded columns (nU + 1 <= 66 real; 5 super blocks of 16)
-
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+// the small R by solve_kernel, exactly as for the window Gram C.
+// Warp-specialised, one CTA per SM: GG_PW producer warps own one tile row per thread and gather
+// its nU + 1 values with 8-byte cp.async one tile ahead, subtract rho once they land and arrive
+// on full[s]; GG_CW consumer warps each own one 16 x 16 super-block pair of the upper triangle
+// (DMMA m8n8k4) and release the stage through empty[s].  No CTA-wide barrier in the stream.
+// NSB 16-column super blocks (ncol <= 16 NSB), RT rows per tile (= producer threads),
+// TPW super-block pairs per consumer warp, CW consumer warps.
+template <int NSB, int RT, int TPW, int CW, int STAGES>
+struct GGCfg {
+  static constexpr int nsb = NSB, rt = RT, tpw = TPW, cw = CW, stages = STAGES;
+  static constexpr int pw = RT / 32, ncp = 16 * NSB, ldt = RT + 4, threads = 32 * (RT / 32 + CW);
+  static constexpr size_t smem = (size_t)STAGES * ncp * ldt * sizeof(double);
+  static_assert(CW * TPW >= NSB * (NSB + 1) / 2, "tasks");
+};
+using GGSmall = GGCfg<5, 64, 1, 15, 3>;  // ncol <= 80 (w <= 78)
+using GGWide = GGCfg<9, 32, 3, 15, 3>;   // ncol <= 144 (w <= kMaxW)
 
 struct GGArgs {
   Geo g;
@@ -223,106 +224,136 @@ struct GGArgs {
   const int32_t* list;
   const int32_t* count;
   SRef src_b;
-  double* part;  // [grid][GG_NCP][GG_NCP]
+  double* part;  // [grid][ncp][ncp]
 };
 
-__global__ void __launch_bounds__(GG_T, 1) gather_gram_kernel(GGArgs a) {
+template <class CFG>
+__global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) {
+  constexpr int RT = CFG::rt, NSB = CFG::nsb, NCP = CFG::ncp, LDT = CFG::ldt, ST = CFG::stages;
   extern __shared__ double smem[];
+  __shared__ __align__(8) uint64_t full[ST], empty[ST];
   const int nS = *a.count;
   const int64_t total_rows = (int64_t)nS * a.g.c;
-  const int64_t ntiles = (total_rows + GG_RT - 1) / GG_RT;
+  const int64_t ntiles = (total_rows + RT - 1) / RT;
   const int nU = a.W.nU, ncol = nU + 1;  // union slots + b
-  const int k = threadIdx.x % GG_RT, sub = threadIdx.x / GG_RT;  // row, column group
-  constexpr int NSUB = GG_T / GG_RT;                               // 8 column groups
-  const SRef slab{nullptr, a.g.nsr};
-  for (int i = threadIdx.x; i < GG_STAGES * GG_NCP * GG_LDT; i += GG_T) smem[i] = 0.0;  // padding columns stay 0
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < ST * NCP * LDT; i += CFG::threads) smem[i] = 0.0;  // padding stays 0
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < ST; ++q) {
+      mbar_init(&full[q], RT);
+      mbar_init(&empty[q], CFG::cw);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   __syncthreads();
-  // per-thread row state: the S-hat list entry of a tile is loaded one iteration before its
-  // gathers are issued (no dependent-load stall in the issue path); rho rides in registers
-  auto row_cell = [&](int64_t tl, int* var) -> int {
-    const int64_t row = tl * GG_RT + k;
-    if (tl >= ntiles || row >= total_rows) return -1;
-    *var = (int)(row / nS);
-    return __ldg(a.list + (row - (int64_t)(*var) * nS));
-  };
-  double rq0 = 0.0, rq1 = 0.0, rq2 = 0.0;
-  auto issue = [&](int cell, int var, int st) {
-    double* tile = smem + (size_t)st * GG_NCP * GG_LDT;
-    double r = 0.0;
-    if (cell >= 0) {
-      const int64_t e = (int64_t)var * a.g.N + cell;
-      const int64_t se = sidx(slab, e);
-      for (int col = sub; col < ncol; col += NSUB) {
-        const double* src = col < nU ? a.ring + (int64_t)a.W.slot[col] * TILE + se : a.src_b.p + sidx(a.src_b, e);
-        cp_async8(tile + col * GG_LDT + k, src);
+  const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (warp < CFG::pw) {
+    // ---- producers: thread k owns row k of every tile ----
+    const int k = threadIdx.x;
+    const SRef slab{nullptr, a.g.nsr};
+    double r_prev = 0.0;
+    bool v_prev = false;
+    for (int64_t it = 0; it <= my_tiles; ++it) {
+      double r_cur = 0.0;
+      bool v_cur = false;
+      if (it < my_tiles) {
+        const int st = (int)(it % ST);
+        if (it >= ST) mbar_wait(&empty[st], (uint32_t)(((it / ST) - 1) & 1));
+        double* tile = smem + (size_t)st * NCP * LDT;
+        const int64_t row = (blockIdx.x + it * gridDim.x) * RT + k;
+        if (row < total_rows) {
+          const int var = (int)(row / nS);
+          const int64_t e = (int64_t)var * a.g.N + __ldg(a.list + (row - (int64_t)var * nS));
+          const int64_t se = sidx(slab, e);
+          for (int col = 0; col < nU; ++col)
+            cp_async8(tile + col * LDT + k, a.ring + (int64_t)a.W.slot[col] * TILE + se);
+          cp_async8(tile + nU * LDT + k, a.src_b.p + sidx(a.src_b, e));
+          r_cur = __ldg(a.rho.p + sidx(a.rho, e));
+          v_cur = true;
+        } else {
+          for (int col = 0; col < ncol; ++col) tile[col * LDT + k] = 0.0;
+        }
       }
-      r = __ldg(a.rho.p + sidx(a.rho, e));
-    } else {
-      for (int col = sub; col < ncol; col += NSUB) tile[col * GG_LDT + k] = 0.0;
-    }
-    if (st == 0) rq0 = r;
-    else if (st == 1) rq1 = r;
-    else rq2 = r;
-    cp_async_commit();
-  };
-  double acc[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gid = lane >> 2, tig = lane & 3;
-  constexpr int nsb = GG_NCP / 16, ntask = nsb * (nsb + 1) / 2;  // 15 upper super-block pairs
-  int sa = 0, rem = warp;
-  while (sa < nsb && rem >= nsb - sa) { rem -= nsb - sa; ++sa; }
-  const int sb = sa + rem;
-  const bool has_task = warp < ntask;
-  static_assert(GG_STAGES == 3, "rho registers rq0..rq2");
-  int64_t tl = blockIdx.x;
-  // prologue: GG_STAGES - 1 tiles in flight, the list entry of the next one loaded
-  {
-    int v0 = 0, v1 = 0;
-    const int c0 = row_cell(tl, &v0), c1 = row_cell(tl + gridDim.x, &v1);
-    issue(c0, v0, 0);
-    issue(c1, v1, 1);
-  }
-  int nvar = 0;
-  int ncell = row_cell(tl + (int64_t)(GG_STAGES - 1) * gridDim.x, &nvar);
-  for (int it = 0; tl < ntiles; ++it, tl += gridDim.x) {
-    const int st = it % GG_STAGES;
-    cp_async_wait<GG_STAGES - 2>();
-    // shift by rho in place (own elements: visible to this thread after the wait)
-    {
-      double* tile = smem + (size_t)st * GG_NCP * GG_LDT;
-      const double r = st == 0 ? rq0 : (st == 1 ? rq1 : rq2);
-      for (int col = sub; col < ncol; col += NSUB) tile[col * GG_LDT + k] -= r;
-    }
-    __syncthreads();
-    // next tile into the stage consumed in the previous iteration; prefetch the list entry after it
-    issue(ncell, nvar, (it + GG_STAGES - 1) % GG_STAGES);
-    ncell = row_cell(tl + (int64_t)GG_STAGES * gridDim.x, &nvar);
-    if (has_task) {
-      const double* tile = smem + (size_t)st * GG_NCP * GG_LDT;
-#pragma unroll
-      for (int kk = 0; kk < GG_RT; kk += 4) {
-        const double a0 = tile[(16 * sa + gid) * GG_LDT + kk + tig];
-        const double a1 = tile[(16 * sa + 8 + gid) * GG_LDT + kk + tig];
-        const double b0 = tile[(16 * sb + gid) * GG_LDT + kk + tig];
-        const double b1 = tile[(16 * sb + 8 + gid) * GG_LDT + kk + tig];
-        dmma(acc[0], acc[1], a0, b0);
-        dmma(acc[2], acc[3], a0, b1);
-        dmma(acc[4], acc[5], a1, b0);
-        dmma(acc[6], acc[7], a1, b1);
+      cp_async_commit();
+      if (it >= 1) {  // tile it-1 has landed: shift by rho, publish
+        cp_async_wait<1>();
+        const int ps = (int)((it - 1) % ST);
+        double* tile = smem + (size_t)ps * NCP * LDT;
+        if (v_prev)
+          for (int col = 0; col < ncol; ++col) tile[col * LDT + k] -= r_prev;
+        mbar_arrive(&full[ps]);
       }
+      r_prev = r_cur;
+      v_prev = v_cur;
     }
-    __syncthreads();  // the stage is re-filled two iterations later
-  }
-  cp_async_wait<0>();
-  double* out = a.part + (int64_t)blockIdx.x * GG_NCP * GG_NCP;
-  if (has_task) {
+    cp_async_wait<0>();
+  } else {
+    // ---- consumers: TPW upper super-block pairs (sa <= sb) per warp ----
+    const int cwarp = warp - CFG::pw;
+    const int gid = lane >> 2, tig = lane & 3;
+    // the last super block holds ncol - 16 (NSB - 1) real columns: when <= 8, its pairs only
+    // need the first 8-column half (fewer DMMAs, same result: the rest is padding)
+    const bool last_half = ncol <= 16 * (NSB - 1) + 8;
+    int sa[CFG::tpw], sb[CFG::tpw];
+    bool has[CFG::tpw];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int bi = 16 * sa + 8 * (q >> 1), bj = 16 * sb + 8 * (q & 1);
-      out[(bi + gid) * GG_NCP + bj + 2 * tig] = acc[2 * q];
-      out[(bi + gid) * GG_NCP + bj + 2 * tig + 1] = acc[2 * q + 1];
+    for (int t = 0; t < CFG::tpw; ++t) {
+      const int task = cwarp + t * CFG::cw;
+      has[t] = task < NSB * (NSB + 1) / 2;
+      int x = 0, rem = has[t] ? task : 0;
+      while (rem >= NSB - x) {
+        rem -= NSB - x;
+        ++x;
+      }
+      sa[t] = x;
+      sb[t] = x + rem;
+    }
+    double acc[CFG::tpw][8];
+#pragma unroll
+    for (int t = 0; t < CFG::tpw; ++t)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[t][q] = 0.0;
+    for (int64_t it = 0; it < my_tiles; ++it) {
+      const int st = (int)(it % ST);
+      mbar_wait(&full[st], (uint32_t)((it / ST) & 1));
+      const double* tile = smem + (size_t)st * NCP * LDT;
+#pragma unroll
+      for (int t = 0; t < CFG::tpw; ++t) {
+        if (!has[t]) continue;
+        const bool bh = last_half && sb[t] == NSB - 1;  // b: first half only
+        const bool ah = last_half && sa[t] == NSB - 1;  // a: first half only
+#pragma unroll
+        for (int kk = 0; kk < RT; kk += 4) {
+          const double a0 = tile[(16 * sa[t] + gid) * LDT + kk + tig];
+          const double b0 = tile[(16 * sb[t] + gid) * LDT + kk + tig];
+          dmma(acc[t][0], acc[t][1], a0, b0);
+          if (!bh) {
+            const double b1 = tile[(16 * sb[t] + 8 + gid) * LDT + kk + tig];
+            dmma(acc[t][2], acc[t][3], a0, b1);
+            if (!ah) {
+              const double a1 = tile[(16 * sa[t] + 8 + gid) * LDT + kk + tig];
+              if (sa[t] != sb[t]) dmma(acc[t][4], acc[t][5], a1, b0);  // diagonal pair: lower block unused
+              dmma(acc[t][6], acc[t][7], a1, b1);
+            }
+          } else if (!ah) {
+            const double a1 = tile[(16 * sa[t] + 8 + gid) * LDT + kk + tig];
+            dmma(acc[t][4], acc[t][5], a1, b0);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    double* out = a.part + (int64_t)blockIdx.x * NCP * NCP;
+#pragma unroll
+    for (int t = 0; t < CFG::tpw; ++t) {
+      if (!has[t]) continue;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int bi = 16 * sa[t] + 8 * (q >> 1), bj = 16 * sb[t] + 8 * (q & 1);
+        out[(bi + gid) * NCP + bj + 2 * tig] = acc[t][2 * q];
+        out[(bi + gid) * NCP + bj + 2 * tig + 1] = acc[t][2 * q + 1];
+      }
     }
   }
 }
@@ -711,20 +742,31 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   a.list = c->b.lists + (int64_t)L_S * c->g.N;
   a.count = c->b.counts + L_S;
   a.src_b = src_b;
-  if (a.W.nU + 1 > GG_NCP) return HROM_E_INVALID;
   // while the one-CTA eigen-solve of the previous update holds an SM (side stream), leave it
   // out: a static tile split with one block left over would double the time
   const int grid = c->basis_pending ? c->nsm - 1 : c->nsm;
-  if ((int64_t)grid * GG_NCP * GG_NCP > c->b.part_len) return HROM_E_INVALID;
   a.part = c->b.part;
-  const size_t smem = (size_t)GG_STAGES * GG_NCP * GG_LDT * sizeof(double);
-  HROM_CK(cudaFuncSetAttribute(gather_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  gather_gram_kernel<<<grid, GG_T, smem, c->st>>>(a);
+  int ncp;
+  if (a.W.nU + 1 <= GGSmall::ncp) {
+    ncp = GGSmall::ncp;
+    if ((int64_t)grid * ncp * ncp > c->b.part_len) return HROM_E_INVALID;
+    HROM_CK(cudaFuncSetAttribute(gather_gram_kernel<GGSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)GGSmall::smem));
+    gather_gram_kernel<GGSmall><<<grid, GGSmall::threads, GGSmall::smem, c->st>>>(a);
+  } else if (a.W.nU + 1 <= GGWide::ncp) {
+    ncp = GGWide::ncp;
+    if ((int64_t)grid * ncp * ncp > c->b.part_len) return HROM_E_INVALID;
+    HROM_CK(cudaFuncSetAttribute(gather_gram_kernel<GGWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)GGWide::smem));
+    gather_gram_kernel<GGWide><<<grid, GGWide::threads, GGWide::smem, c->st>>>(a);
+  } else {
+    return HROM_E_INVALID;
+  }
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   const int ncol = a.W.nU + 1;
   double* R = c->b.eigV;  // (nU+1)^2 scratch
-  gram_reduce<<<64, 256, 0, c->st>>>(c->b.part, grid, GG_NCP, ncol, R, ncol, nullptr);
+  gram_reduce<<<64, 256, 0, c->st>>>(c->b.part, grid, ncp, ncol, R, ncol, nullptr);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;  // the lagged centring of R is applied by solve_kernel
