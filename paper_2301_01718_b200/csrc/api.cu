@@ -56,6 +56,26 @@ Win window_at(const hrom_ctx* c, int64_t k) {
 
 using namespace hrom;
 
+namespace hrom {
+hrom_status flush_eigen(hrom_ctx* c) {
+  if (!c->eig_todo) return HROM_OK;
+  c->eig_todo = false;
+  HROM_CK(cudaEventRecord(c->ev_basis_in, c->st));
+  HROM_CK(cudaStreamWaitEvent(c->side, c->ev_basis_in, 0));
+  cudaStream_t main_st = c->st;
+  c->st = c->side;
+  prof_begin(c, SEC_EIGEN);
+  const hrom_status s = basis_from_gram(c, c->eig_win);
+  prof_end(c, SEC_EIGEN);
+  c->st = main_st;
+  if (s != HROM_OK) return s;
+  HROM_CK(cudaEventRecord(c->ev_basis_done, c->side));
+  c->basis_pending = true;
+  return HROM_OK;
+}
+
+}  // namespace hrom
+
 extern "C" {
 
 const char* hrom_status_string(hrom_status s) {
@@ -128,6 +148,11 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
     return HROM_E_CUDA;
   }
   c->filter_blocks = c->nsm;  // one block per SM: cheapest grid barrier
+  if (sets_occupancy() < 1) {
+    delete c;
+    return HROM_E_CUDA;
+  }
+  c->sets_blocks = c->nsm;
 
   Bufs& b = c->b;
   hrom_status s = HROM_OK;
@@ -167,9 +192,9 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   A(dalloc(&b.dbg, 64));
   A(dalloc(&b.sel_val, g.N));
   A(dalloc(&b.sel_cell, g.N));
-  b.blk_len = 8 * ((c->mwords + 255) / 256 + 2) + (g.N + 1023) / 1024 + 16;
+  b.blk_len = std::max<int64_t>(8 * ((c->mwords + 255) / 256 + 2) + (g.N + 1023) / 1024 + 16, 8 * (int64_t)c->nsm + 64);
   A(dalloc(&b.blk, b.blk_len));
-  A(dalloc(&b.hist, 512));
+  A(dalloc(&b.hist, 3 * 2048));
   A(dalloc(&b.fstat, c->filter_blocks));
   A(dalloc(&b.fcnt, c->filter_blocks));
   A(dalloc(&b.colptr, 2 * kMaxSlots));
@@ -229,6 +254,7 @@ static hrom_status copy_slot(hrom_ctx* c, int slot, const double* src_plain, dou
   const size_t row = TILE * sizeof(double), spitch = (size_t)c->g.nsr * TILE * sizeof(double);
   double* base = c->b.ring + (int64_t)slot * TILE;
   if (src_plain) {
+    c->smax_k = -1;  // the state changed under the fused wave-speed maximum
     if (full) HROM_CK(cudaMemcpy2DAsync(base, spitch, src_plain, row, row, full, cudaMemcpyDefault, c->st));
     if (tail)
       HROM_CK(cudaMemcpyAsync(base + full * c->g.nsr * TILE, src_plain + full * TILE, tail * sizeof(double),
@@ -269,7 +295,7 @@ hrom_status hrom_full_step(hrom_ctx* c, double dt_override, double* dev_dt_out) 
   const SRef U1 = plain(c->b.U1), U2 = plain(c->b.U2);
   hrom_status s;
   prof_begin(c, SEC_FULL);
-  if ((s = launch_dt(c, qn, dt_override)) != HROM_OK) return s;
+  if ((s = launch_dt(c, qn, dt_override, c->k)) != HROM_OK) return s;
   if (dev_dt_out) HROM_CK(cudaMemcpyAsync(dev_dt_out, c->b.dreg, sizeof(double), cudaMemcpyDefault, c->st));
   if ((s = launch_stage(c, 1, qn, qn, U1, nullptr, 0, dt_override)) != HROM_OK) return s;
   if ((s = launch_stage(c, 2, qn, U1, U2, nullptr, 0, dt_override)) != HROM_OK) return s;
@@ -285,6 +311,7 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
   if (!c) return HROM_E_INVALID;
   if (!c->basis_ready) return HROM_E_STATE;
   hrom_status s;
+  if ((s = flush_eigen(c)) != HROM_OK) return s;
   if (dev_mask) {
     if ((s = build_sets(c, dev_mask)) != HROM_OK) return s;
     c->sets_ready = true;
@@ -298,7 +325,7 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
   const SRef U1 = plain(b.U1), U2 = plain(b.U2), U3 = plain(b.U3);
   // H1
   prof_begin(c, SEC_DT);
-  if ((s = launch_dt(c, qn, dt_override)) != HROM_OK) return s;
+  if ((s = launch_dt(c, qn, dt_override, c->k)) != HROM_OK) return s;
   prof_end(c, SEC_DT);
   if (dev_dt_out) HROM_CK(cudaMemcpyAsync(dev_dt_out, b.dreg, sizeof(double), cudaMemcpyDefault, c->st));
   // H3: stage 1 on A1, stage 2 on A2, stage 3 on T = S-hat u B (F on the band)
@@ -334,7 +361,7 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
     if ((s = launch_band_gram(c, c->win, out)) != HROM_OK) return s;
   prof_end(c, SEC_BANDGRAM);
   prof_begin(c, SEC_POS);
-  if ((s = launch_positivity(c, out)) != HROM_OK) return s;
+  if ((s = launch_positivity(c, out, kn)) != HROM_OK) return s;
   prof_end(c, SEC_POS);
   c->k = kn;
   c->gram_row_ready = (c->P.gram_mode == 0);
@@ -374,20 +401,11 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
     if ((s = reduce_gram_row(c, c->win, c->slot_of(k), true)) != HROM_OK) return s;
   }
   prof_end(c, SEC_BASIS);
-  {
-    // eigen-solve on the side stream; consumers call basis_join()
-    HROM_CK(cudaEventRecord(c->ev_basis_in, c->st));
-    HROM_CK(cudaStreamWaitEvent(c->side, c->ev_basis_in, 0));
-    cudaStream_t main_st = c->st;
-    c->st = c->side;
-    prof_begin(c, SEC_EIGEN);
-    s = basis_from_gram(c, W);
-    prof_end(c, SEC_EIGEN);
-    c->st = main_st;
-    if (s != HROM_OK) return s;
-    HROM_CK(cudaEventRecord(c->ev_basis_done, c->side));
-    c->basis_pending = true;
-  }
+  // eigen-solve: deferred to the side stream after the sampling kernel (a cooperative kernel
+  // that needs every SM), overlapping the next step's dt / masked RK3 / gathered Gram;
+  // consumers call basis_join()
+  c->eig_win = W;
+  c->eig_todo = true;
   c->win = W;
   c->basis_ready = true;
   c->gram_row_ready = false;
@@ -409,8 +427,8 @@ hrom_status hrom_sample(hrom_ctx* c, double fraction, const double* dev_eps, uin
   const int64_t n_g = (int64_t)std::ceil(fraction * (double)c->g.N);
   hrom_status s;
   prof_begin(c, SEC_SAMPLE);
-  if ((s = select_topn(c, dev_eps ? dev_eps : c->b.eps, n_g)) != HROM_OK) return s;
-  if ((s = build_sets(c, nullptr)) != HROM_OK) return s;
+  if ((s = select_and_build(c, dev_eps ? dev_eps : c->b.eps, n_g)) != HROM_OK) return s;
+  if ((s = flush_eigen(c)) != HROM_OK) return s;
   prof_end(c, SEC_SAMPLE);
   c->sets_ready = true;
   if (dev_mask_out)
@@ -429,6 +447,7 @@ hrom_status hrom_reconstruct(hrom_ctx* c, const uint32_t* dev_mask, double* dev_
   if (!c || !dev_v) return HROM_E_INVALID;
   if (!c->basis_ready) return HROM_E_STATE;
   hrom_status s;
+  if ((s = flush_eigen(c)) != HROM_OK) return s;
   if (dev_mask) {
     if ((s = build_sets(c, dev_mask)) != HROM_OK) return s;
     c->sets_ready = true;

@@ -180,10 +180,13 @@ __global__ void dt_finalize(const unsigned long long* smax, double cfl, double d
   *dt = dt_override > 0.0 ? dt_override : cfl / s;
 }
 
-// O11: lowest cell with rho <= 0 or p <= 0 (or NaN)
+// O11: lowest cell with rho <= 0 or p <= 0 (or NaN); fused with H1's max wave speed of the same
+// state (the next step's dt reads it instead of a second pass over the state)
 template <int DIM>
-__global__ void __launch_bounds__(256) positivity_kernel(Geo g, const SRef q, unsigned long long* __restrict__ bad) {
+__global__ void __launch_bounds__(256) positivity_kernel(Geo g, const SRef q, unsigned long long* __restrict__ bad,
+                                                         unsigned long long* __restrict__ smax) {
   constexpr int C = DIM + 2;
+  double m = 0.0;
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N;
        n += (int64_t)gridDim.x * blockDim.x) {
     double U[C];
@@ -191,22 +194,47 @@ __global__ void __launch_bounds__(256) positivity_kernel(Geo g, const SRef q, un
     for (int v = 0; v < C; ++v) U[v] = q.p[sidx(q, v * g.N + n)];
     const double p = pressure<DIM>(U, g.gamma - 1.0);
     if (!(U[0] > 0.0) || !(p > 0.0)) atomicMin(bad, (unsigned long long)n);
+    const double cs = sqrt(g.gamma * p / U[0]);
+    double s = (fabs(U[1] / U[0]) + cs) / g.dx;
+    if (DIM == 2) s = s + (fabs(U[2] / U[0]) + cs) / g.dy;
+    if (!(s <= m)) m = s;  // NaN sticks
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double t = __shfl_xor_sync(0xffffffffu, m, o);
+    if (!(t <= m)) m = t;
+  }
+  __shared__ double sm[8];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+      if (!(sm[k] <= m)) m = sm[k];
+    unsigned long long bits = (unsigned long long)__double_as_longlong(m);
+    if (m != m) bits = 0x7ff8000000000000ull;
+    atomicMax(smax, bits);
   }
 }
 
 }  // namespace
 
-hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override) {
+hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override, int64_t kq) {
+  const unsigned long long* smax = c->b.ureg;
+  int nl = 1;
   if (dt_override <= 0.0) {
-    HROM_CK(cudaMemsetAsync(c->b.ureg, 0, sizeof(unsigned long long), c->st));
-    const int grid = c->nsm * 8;
-    if (c->g.dim == 1) smax_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg);
-    else smax_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg);
-    HROM_LAUNCH_CK();
+    if (c->smax_k == kq) {
+      smax = c->b.ureg + 2;  // computed by the positivity pass that closed step kq
+    } else {
+      HROM_CK(cudaMemsetAsync(c->b.ureg, 0, sizeof(unsigned long long), c->st));
+      const int grid = c->nsm * 8;
+      if (c->g.dim == 1) smax_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg);
+      else smax_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg);
+      HROM_LAUNCH_CK();
+      ++nl;
+    }
   }
-  dt_finalize<<<1, 1, 0, c->st>>>(c->b.ureg, c->g.cfl, dt_override, c->b.dreg);
+  dt_finalize<<<1, 1, 0, c->st>>>(smax, c->g.cfl, dt_override, c->b.dreg);
   HROM_LAUNCH_CK();
-  c->nlaunch += (dt_override <= 0.0) ? 2 : 1;
+  c->nlaunch += nl;
   return HROM_OK;
 }
 
@@ -227,12 +255,14 @@ hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, co
   return HROM_OK;
 }
 
-hrom_status launch_positivity(hrom_ctx* c, SRef q) {
+hrom_status launch_positivity(hrom_ctx* c, SRef q, int64_t kq) {
   const int grid = c->nsm * 8;
-  if (c->g.dim == 1) positivity_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg + 1);
-  else positivity_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg + 1);
+  HROM_CK(cudaMemsetAsync(c->b.ureg + 2, 0, sizeof(unsigned long long), c->st));
+  if (c->g.dim == 1) positivity_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg + 1, c->b.ureg + 2);
+  else positivity_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg + 1, c->b.ureg + 2);
   HROM_LAUNCH_CK();
   c->nlaunch += 1;
+  c->smax_k = kq;
   return HROM_OK;
 }
 

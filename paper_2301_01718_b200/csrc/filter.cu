@@ -24,9 +24,8 @@ struct FilterArgs {
   const int32_t* list;   // band cells B (ascending)
   const int32_t* count;  // |B|
   const uint32_t* mB;    // band bit mask
-  uint32_t* mH;          // halo bit mask (zeroed by the launcher)
-  int32_t* hlist;        // halo cells (ascending), written here
-  int32_t* hcount;       // |halo| (written here)
+  const int32_t* hlist;  // halo cells (ascending), built with the sets
+  const int32_t* hcount; // |halo|
   int32_t* idx;          // cell -> compact index (band t < nb, halo nb + h); N entries
   int32_t* tab;          // stencil tables: row (d * 7 + m + 3) * N + t, d = 0 x, 1 y
   SRef v;                // gamma_k (read, band values written back)
@@ -55,18 +54,6 @@ __device__ __forceinline__ void stamp(long long* t, int i) {
   }
 }
 
-__device__ __forceinline__ int wrapf(int i, int n, int bc) {
-  if (bc == 1) {
-    i %= n;
-    return i < 0 ? i + n : i;
-  }
-  return i < 0 ? 0 : (i >= n ? n - 1 : i);
-}
-
-__device__ __forceinline__ bool bitB(const uint32_t* m, const Geo& g, int i, int j) {
-  return (m[(int64_t)j * g.wpr + (i >> 5)] >> (i & 31)) & 1u;
-}
-
 // (1,2,1)/4, (-1,4,10,4,-1)/16, (1,-6,15,44,15,-6,1)/64  (A24)
 __constant__ double c2[3] = {1, 2, 1};
 __constant__ double c4[5] = {-1, 4, 10, 4, -1};
@@ -92,70 +79,12 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   __shared__ double sdec[FT / 32];
   __shared__ int scnt[FT / 32];
-  __shared__ int sscan[FT];
-  __shared__ int sbase;
   stamp(a.tdbg, 0);
-  // S0: mark the halo
-  for (int64_t t = gtid; t < nb; t += gstride) {
-    const int64_t n = a.list[t];
-    const int i = (int)(n % g.nx), j = (int)(n / g.nx);
-    for (int m = -a.rmax; m <= a.rmax; ++m) {
-      if (m == 0) continue;
-      const int ii = wrapf(i + m, g.nx, g.bc);
-      if (!bitB(a.mB, g, ii, j)) atomicOr(&a.mH[(int64_t)j * g.wpr + (ii >> 5)], 1u << (ii & 31));
-      if (g.dim == 2) {
-        const int jj = wrapf(j + m, g.ny, g.bc);
-        if (!bitB(a.mB, g, i, jj)) atomicOr(&a.mH[(int64_t)jj * g.wpr + (i >> 5)], 1u << (i & 31));
-      }
-    }
-  }
-  grid.sync();
-  // S1: ordered compaction of the halo mask -- block b owns a contiguous word range
-  const int64_t nw = (int64_t)g.ny * g.wpr;
-  const int64_t bchunk = (nw + gridDim.x - 1) / gridDim.x;
-  const int64_t tchunk = (bchunk + blockDim.x - 1) / blockDim.x;
-  const int64_t w0 = blockIdx.x * bchunk + threadIdx.x * tchunk;
-  const int64_t w1 = min(min(w0 + tchunk, (int64_t)(blockIdx.x + 1) * bchunk), nw);
-  int mine = 0;
-  for (int64_t wi = w0; wi < w1; ++wi) mine += __popc(a.mH[wi]);
-  sscan[threadIdx.x] = mine;
-  __syncthreads();
-  for (int o = 1; o < (int)blockDim.x; o <<= 1) {  // inclusive Hillis-Steele scan
-    const int x = threadIdx.x >= o ? sscan[threadIdx.x - o] : 0;
-    __syncthreads();
-    sscan[threadIdx.x] += x;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) a.fcnt[blockIdx.x] = sscan[blockDim.x - 1];
-  grid.sync();
-  if (threadIdx.x == 0) {
-    int base = 0, tot = 0;
-    for (int b = 0; b < (int)gridDim.x; ++b) {
-      if (b < (int)blockIdx.x) base += a.fcnt[b];
-      tot += a.fcnt[b];
-    }
-    sbase = base;
-    if (blockIdx.x == 0) *a.hcount = tot;
-  }
-  __syncthreads();
-  {
-    int pos = sbase + sscan[threadIdx.x] - mine;
-    for (int64_t wi = w0; wi < w1; ++wi) {
-      uint32_t bits = a.mH[wi];
-      const int64_t j = wi / g.wpr, i0 = (wi % g.wpr) * 32;
-      while (bits) {
-        const int bpos = __ffs(bits) - 1;
-        bits &= bits - 1;
-        a.hlist[pos++] = (int32_t)(j * g.nx + i0 + bpos);
-      }
-    }
-  }
-  grid.sync();
+  // gathers into the compact band + halo arrays (halo list, index map and stencil tables were
+  // built with the sets, masks.cu sets_kernel)
   const int nh = *a.hcount;
-  // S2: index map and gathers
   for (int64_t t = gtid; t < nb + nh; t += gstride) {
     const int64_t n = t < nb ? a.list[t] : a.hlist[t - nb];
-    a.idx[n] = (int32_t)t;
     for (int var = 0; var < g.c; ++var) {
       const double x = a.v.p[sidx(a.v, var * N + n)];
       a.cur[var * N + t] = x;
@@ -167,16 +96,6 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
       }
     }
     a.flag[t] = 0;
-  }
-  grid.sync();
-  // S3: stencil tables
-  for (int64_t t = gtid; t < nb; t += gstride) {
-    const int64_t n = a.list[t];
-    const int i = (int)(n % g.nx), j = (int)(n / g.nx);
-    for (int m = -a.rmax; m <= a.rmax; ++m) {
-      a.tab[(int64_t)(m + 3) * N + t] = a.idx[(int64_t)j * g.nx + wrapf(i + m, g.nx, g.bc)];
-      if (g.dim == 2) a.tab[(int64_t)(7 + m + 3) * N + t] = a.idx[(int64_t)wrapf(j + m, g.ny, g.bc) * g.nx + i];
-    }
   }
   grid.sync();
   stamp(a.tdbg, 1);
@@ -408,7 +327,6 @@ hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F, uint8_t* kept_cells) {
   a.list = c->b.lists + (int64_t)L_B * c->g.N;
   a.count = c->b.counts + L_B;
   a.mB = c->b.masks + (int64_t)M_B * c->mwords;
-  a.mH = c->b.masks + (int64_t)M_TMP * c->mwords;
   a.hlist = c->b.lists + (int64_t)L_H * c->g.N;
   a.hcount = c->b.counts + L_H;
   a.idx = c->b.fidx;
@@ -427,7 +345,6 @@ hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F, uint8_t* kept_cells) {
   a.fcnt = c->b.fcnt;
   a.sweeps_out = c->b.ireg + 4;
   a.tdbg = c->b.dbg;
-  HROM_CK(cudaMemsetAsync(a.mH, 0, (size_t)c->g.ny * c->g.wpr * sizeof(uint32_t), c->st));
   if (kept_cells) HROM_CK(cudaMemsetAsync(kept_cells, 0, c->g.N, c->st));
   void* args[] = {&a};
   HROM_CK(cudaLaunchCooperativeKernel((void*)filter_kernel, dim3(c->filter_blocks), dim3(FT), args, 0, c->st));

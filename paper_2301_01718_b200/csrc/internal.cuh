@@ -70,7 +70,7 @@ struct Win {
 };
 
 // mask indices
-enum { M_S = 0, M_B, M_T, M_A2, M_A1, M_TMP, M_TMP2, M_KEEP, M_COUNT };
+enum { M_S = 0, M_B, M_T, M_A2, M_A1, M_TMP, M_TMP2, M_H, M_COUNT };  // M_H: seam-filter halo
 // list indices
 enum { L_S = 0, L_B, L_T, L_A2, L_A1, L_H, L_COUNT };  // L_H: seam-filter halo
 
@@ -113,7 +113,7 @@ struct Bufs {
   int32_t* sel_cell = nullptr; // N
   int32_t* blk = nullptr;      // block counts/offsets for compaction (max blocks * L_COUNT * 2)
   int64_t blk_len = 0;
-  int32_t* hist = nullptr;     // 256 + select state
+  int32_t* hist = nullptr;     // 3 x 2048 radix histograms
   // filter stats per block
   double* fstat = nullptr;
   int32_t* fcnt = nullptr;
@@ -142,7 +142,9 @@ struct hrom_ctx {
   int fill_grid = 0;         // grid of the last fill launch
   int band_blocks = 0;
   int filter_blocks = 0;
+  int sets_blocks = 0;       // cooperative sets kernel grid (one block per SM)
   int64_t last_err_cell = -1;
+  int64_t smax_k = -1;       // state index whose max wave speed is in ureg[2] (positivity pass)
   int64_t nlaunch = 0;       // kernels launched by this context (host-side count)
   // optional per-section CUDA-event timing (hrom_profile)
   bool prof = false;
@@ -154,14 +156,18 @@ struct hrom_ctx {
   // sampling and the next step's dt / masked RK3 / gathered Gram (which do not need it)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_basis_in = nullptr, ev_basis_done = nullptr;
-  bool basis_pending = false;
+  bool basis_pending = false;  // eigen-solve launched on the side stream, not yet joined
+  bool eig_todo = false;       // eigen-solve deferred (launched after the sampling kernel)
+  hrom::Win eig_win{};
   int slot_of(int64_t kk) const { return (int)(kk % nslots); }
   hrom::SRef slot_ref(int s) const { return hrom::SRef{b.ring + (int64_t)s * hrom::TILE, g.nsr}; }
   hrom::SRef rho_ref() const { return hrom::SRef{b.rho, g.nsr}; }
 };
 
 namespace hrom {
+hrom_status flush_eigen(hrom_ctx* c);  // api.cu: launch a deferred eigen-solve on the side stream
 inline void basis_join(hrom_ctx* c) {
+  if (c->eig_todo) flush_eigen(c);
   if (c->basis_pending) {
     cudaStreamWaitEvent(c->st, c->ev_basis_done, 0);
     c->basis_pending = false;
@@ -187,14 +193,14 @@ inline void prof_end(hrom_ctx* c, int sec) {
 
 namespace hrom {
 // euler.cu
-hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override);
+hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override, int64_t kq);
 hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, const int32_t* list, int list_idx,
                          double dt_override);
-hrom_status launch_positivity(hrom_ctx* c, SRef q);
+hrom_status launch_positivity(hrom_ctx* c, SRef q, int64_t kq);
 // masks.cu
 hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S);
-hrom_status select_topn(hrom_ctx* c, const double* eps, int64_t n_g);
-hrom_status compact_masks(hrom_ctx* c, const int* which, int nwhich);
+hrom_status select_and_build(hrom_ctx* c, const double* eps, int64_t n_g);
+int sets_occupancy();
 // linalg.cu
 // dev_cols: column base pointers, all with slab stride ns (1 = plain vectors); rho: SRef or p == nullptr
 hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int64_t ns, int ncol, int64_t rows, SRef rho,

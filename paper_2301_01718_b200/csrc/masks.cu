@@ -6,9 +6,13 @@
 // union / setdiff, ordering of the pointwise error.
 // Readings: A9 (per-stage cross dilations), A18 (fraction mode, ties by ascending
 // index), A21 (square seam band).  Everything here is integer work: bit-exact.
+#include <cooperative_groups.h>
 #include "internal.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace hrom {
+hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long long n_g);
 namespace {
 
 __device__ __forceinline__ int wrapi(int i, int n, int bc, bool* valid) {
@@ -22,7 +26,7 @@ __device__ __forceinline__ int wrapi(int i, int n, int bc, bool* valid) {
 }
 
 __device__ __forceinline__ uint32_t get_bit(const uint32_t* m, const Geo& g, int i, int j) {
-  return (m[(int64_t)j * g.wpr + (i >> 5)] >> (i & 31)) & 1u;
+  return (__ldcg(m + (int64_t)j * g.wpr + (i >> 5)) >> (i & 31)) & 1u;
 }
 
 // valid-bit mask of word wi in a row
@@ -34,7 +38,7 @@ __device__ __forceinline__ uint32_t row_valid(const Geo& g, int wi) {
 // x-dilation of one word by radius h: OR_{|a|<=h} in[i+a]
 __device__ uint32_t xdil_word(const uint32_t* in, const Geo& g, int j, int wi, int h) {
   const uint32_t* row = in + (int64_t)j * g.wpr;
-  const uint32_t cur = row[wi];
+  const uint32_t cur = __ldcg(row + wi);
   if (g.bc == 1 && (g.nx & 31)) {  // periodic with a ragged last word: per-bit
     uint32_t out = 0;
     const uint32_t vm = row_valid(g, wi);
@@ -53,11 +57,11 @@ __device__ uint32_t xdil_word(const uint32_t* in, const Geo& g, int j, int wi, i
   }
   uint32_t prev, next;
   if (g.bc == 1) {
-    prev = row[(wi - 1 + g.wpr) % g.wpr];
-    next = row[(wi + 1) % g.wpr];
+    prev = __ldcg(row + (wi - 1 + g.wpr) % g.wpr);
+    next = __ldcg(row + (wi + 1) % g.wpr);
   } else {
-    prev = wi > 0 ? row[wi - 1] : 0u;
-    next = wi + 1 < g.wpr ? row[wi + 1] : 0u;
+    prev = wi > 0 ? __ldcg(row + wi - 1) : 0u;
+    next = wi + 1 < g.wpr ? __ldcg(row + wi + 1) : 0u;
   }
   uint32_t out = cur;
   const unsigned long long hi = ((unsigned long long)next << 32) | cur;   // bits of i+a
@@ -75,333 +79,482 @@ __device__ __forceinline__ uint32_t ydil_word(const uint32_t* in, const Geo& g, 
   for (int b = -h; b <= h; ++b) {
     bool ok;
     const int jj = wrapi(j + b, g.ny, g.bc, &ok);
-    if (ok) out |= in[(int64_t)jj * g.wpr + wi];
+    if (ok) out |= __ldcg(in + (int64_t)jj * g.wpr + wi);
   }
   return out;
 }
 
-// cross dilation C_h (x and y arms of the original set)
-__global__ void cross_kernel(Geo g, const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int h) {
-  const int64_t nw = (int64_t)g.ny * g.wpr;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(w / g.wpr), wi = (int)(w % g.wpr);
-    uint32_t o = xdil_word(in, g, j, wi, h);
-    if (g.dim == 2) o |= ydil_word(in, g, j, wi, h);
-    out[w] = o;
-  }
-}
+// ---------------- H8 + set construction + seam-filter tables: one cooperative kernel ----------------
+// Phases (grid barriers between them): [select: eps > 0 bitmap -> ordered compaction ->
+// 11-bit radix select of the n_g-th largest IEEE pattern (6 passes) -> mark S-hat, ties by
+// ascending cell] -> x/y dilations (B, T, A2, A1) -> ordered compaction of the 5 sets ->
+// seam-filter halo (cells within the largest Shapiro radius of B, not in B), its compaction,
+// the cell -> compact index map and the stencil tables used by filter_kernel.
+constexpr int ST_T = 1024;
+constexpr int RADIX = 11, NBIN = 1 << RADIX;
 
-__global__ void xdil_kernel(Geo g, const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int h) {
-  const int64_t nw = (int64_t)g.ny * g.wpr;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x)
-    out[w] = xdil_word(in, g, (int)(w / g.wpr), (int)(w % g.wpr), h);
-}
-
-// band: B = ydil(xdil(S)) \ S, T = S u B
-__global__ void band_kernel(Geo g, const uint32_t* __restrict__ xs, const uint32_t* __restrict__ S,
-                            uint32_t* __restrict__ B, uint32_t* __restrict__ T, int W) {
-  const int64_t nw = (int64_t)g.ny * g.wpr;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(w / g.wpr), wi = (int)(w % g.wpr);
-    const uint32_t sq = (g.dim == 2) ? ydil_word(xs, g, j, wi, W) : xs[w];
-    const uint32_t s = S[w];
-    B[w] = sq & ~s;
-    T[w] = sq | s;
-  }
-}
-
-// ---------------- ordered compaction (count / scan / write) ----------------
-constexpr int CB = 256;  // words per compaction block
-
-struct CmpJob {
-  int n;                       // number of masks
-  const uint32_t* mask[8];
-  int32_t* list[8];
-  double* vals[8];             // optional values gathered from src (flat mode)
-  const double* src[8];
-  int32_t* count_out[8];
-  int flat[8];                 // 1: word w covers cells 32w..32w+31 (no rows)
+struct SetsArgs {
+  Geo g;
+  int do_select;
+  const double* eps;
+  long long n_g;
+  int halo, band, rmax;
+  uint32_t* masks;     // M_COUNT masks of mwords
+  int64_t mwords;
+  int32_t* lists;      // L_COUNT lists of N
+  int32_t* counts;     // [l] sizes; [8] #eps > 0
+  double* sel_val;
+  int32_t* sel_cell;
+  int32_t* blk;        // per-block scratch (>= 8 * grid)
+  int32_t* hist;       // 3 * NBIN
+  int32_t* idx;        // cell -> compact filter index
+  int32_t* tab;        // stencil tables (14 N)
+  long long* tdbg;     // debug timestamps [40..63]
 };
 
-__global__ void cmp_count_kernel(CmpJob job, int64_t nwords, int32_t* __restrict__ blkcnt, int nblk) {
-  const int m = blockIdx.y;
-  const int64_t w = (int64_t)blockIdx.x * CB + threadIdx.x;
-  int c = (w < nwords) ? __popc(job.mask[m][w]) : 0;
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  __shared__ int s[CB / 32];
-  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int k = 0; k < CB / 32; ++k) t += s[k];
-    blkcnt[(int64_t)m * nblk + blockIdx.x] = t;
+__device__ __forceinline__ void sstamp(long long* t, int& i) {
+  if (t && blockIdx.x == 0 && threadIdx.x == 0 && i < 64) {
+    long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    t[i] = gt;
   }
+  ++i;
 }
 
-__global__ void cmp_scan_kernel(CmpJob job, int32_t* __restrict__ blkcnt, int nblk) {
-  // one block per mask: exclusive scan in place, total -> count_out
-  const int m = blockIdx.x;
-  int32_t* a = blkcnt + (int64_t)m * nblk;
-  __shared__ int carry;
-  __shared__ int ws[32];
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < nblk; base += blockDim.x) {
-    const int i = base + threadIdx.x;
-    const int v = i < nblk ? a[i] : 0;
-    int x = v;  // inclusive warp scan
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, x, o);
-      if ((threadIdx.x & 31) >= o) x += t;
-    }
-    if ((threadIdx.x & 31) == 31) ws[threadIdx.x >> 5] = x;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      int y = threadIdx.x < (int)(blockDim.x >> 5) ? ws[threadIdx.x] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, y, o);
-        if (threadIdx.x >= o) y += t;
-      }
-      ws[threadIdx.x] = y;  // inclusive over warps
-    }
-    __syncthreads();
-    const int wpre = (threadIdx.x >> 5) ? ws[(threadIdx.x >> 5) - 1] : 0;
-    const int excl = carry + wpre + x - v;
-    __syncthreads();
-    if (i < nblk) a[i] = excl;
-    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0 && job.count_out[m]) *job.count_out[m] = carry;
+struct BlockRange {
+  int64_t w0, w1;  // this thread's contiguous sub-range
+};
+__device__ __forceinline__ BlockRange thread_range(int64_t n) {
+  const int64_t bchunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t tchunk = (bchunk + blockDim.x - 1) / blockDim.x;
+  const int64_t b0 = (int64_t)blockIdx.x * bchunk, b1 = min(b0 + bchunk, n);
+  BlockRange r;
+  r.w0 = min(b0 + (int64_t)threadIdx.x * tchunk, b1);
+  r.w1 = min(r.w0 + tchunk, b1);
+  return r;
 }
 
-__global__ void cmp_write_kernel(CmpJob job, Geo g, int64_t nwords, const int32_t* __restrict__ blkoff, int nblk) {
-  const int m = blockIdx.y;
-  const int64_t w = (int64_t)blockIdx.x * CB + threadIdx.x;
-  const uint32_t bits = (w < nwords) ? job.mask[m][w] : 0u;
-  const int c = __popc(bits);
-  int x = c;
+// exclusive block scan of one int per thread (returns exclusive prefix, *total = block sum)
+__device__ __forceinline__ int block_excl_scan(int v, int* total, int* sbuf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
   for (int o = 1; o < 32; o <<= 1) {
     const int t = __shfl_up_sync(0xffffffffu, x, o);
-    if ((threadIdx.x & 31) >= o) x += t;
-  }
-  __shared__ int ws[CB / 32];
-  if ((threadIdx.x & 31) == 31) ws[threadIdx.x >> 5] = x;
-  __syncthreads();
-  int wpre = 0;
-  for (int k = 0; k < (int)(threadIdx.x >> 5); ++k) wpre += ws[k];
-  int pos = blkoff[(int64_t)m * nblk + blockIdx.x] + wpre + x - c;
-  if (!bits) return;
-  int64_t cell0;
-  if (job.flat[m]) cell0 = 32 * w;
-  else cell0 = (w / g.wpr) * (int64_t)g.nx + 32 * (w % g.wpr);
-  uint32_t b = bits;
-  while (b) {
-    const int bit = __ffs(b) - 1;
-    b &= b - 1;
-    const int64_t cell = cell0 + bit;
-    job.list[m][pos] = (int32_t)cell;
-    if (job.vals[m]) job.vals[m][pos] = job.src[m][cell];
-    ++pos;
-  }
-}
-
-hrom_status run_compaction(hrom_ctx* c, const CmpJob& job, int64_t nwords) {
-  const int nblk = (int)((nwords + CB - 1) / CB);
-  if ((int64_t)nblk * job.n > c->b.blk_len) return HROM_E_INVALID;
-  dim3 grid(nblk, job.n);
-  cmp_count_kernel<<<grid, CB, 0, c->st>>>(job, nwords, c->b.blk, nblk);
-  cmp_scan_kernel<<<job.n, 1024, 0, c->st>>>(job, c->b.blk, nblk);
-  cmp_write_kernel<<<grid, CB, 0, c->st>>>(job, c->g, nwords, c->b.blk, nblk);
-  HROM_LAUNCH_CK();
-  c->nlaunch += 3;
-  return HROM_OK;
-}
-
-// ---------------- top-n selection ----------------
-// flat bitmap of eps > 0 (word w: cells 32w..32w+31)
-__global__ void nz_kernel(const double* __restrict__ eps, int64_t N, uint32_t* __restrict__ out) {
-  const int64_t nthreads = ((N + 31) / 32) * 32;
-  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < nthreads; n += (int64_t)gridDim.x * blockDim.x) {
-    const bool p = n < N && eps[n] > 0.0;
-    const uint32_t b = __ballot_sync(0xffffffffu, p);
-    if ((threadIdx.x & 31) == 0) out[n >> 5] = b;
-  }
-}
-
-// selection state in hist[256 ..]: [0] prefix lo, [1] prefix hi, [2] remaining rank, [3] count_gt,
-// [4] mode (0: take all, 1: threshold), [5] need ties
-__global__ void sel_init(int32_t* st, const int32_t* cnt, long long n_g) {
-  const int total = *cnt;
-  st[0] = 0;
-  st[1] = 0;
-  st[2] = (int)(n_g < total ? n_g : total);
-  st[3] = 0;
-  st[4] = (n_g < total) ? 1 : 0;
-  st[5] = 0;
-}
-
-__global__ void sel_hist(const double* __restrict__ vals, const int32_t* __restrict__ cnt,
-                         int32_t* __restrict__ hist, const int32_t* __restrict__ st, int shift) {
-  if (st[4] == 0) return;
-  __shared__ int h[256];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
-  __syncthreads();
-  const unsigned long long prefix = ((unsigned long long)(unsigned)st[1] << 32) | (unsigned)st[0];
-  const unsigned long long hm = (shift >= 56) ? 0ull : (~0ull << (shift + 8));
-  const int total = *cnt;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(vals[t]);
-    if ((b & hm) == prefix) atomicAdd(&h[(b >> shift) & 255], 1);
+    if (lane >= o) x += t;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 256; i += blockDim.x)
-    if (h[i]) atomicAdd(&hist[i], h[i]);
-}
-
-__global__ void sel_pick(int32_t* hist, int32_t* st, int shift) {
-  if (st[4] == 0) return;
-  int rem = st[2];
-  int above = 0;
-  int d = 255;
-  for (; d > 0; --d) {
-    if (above + hist[d] >= rem) break;
-    above += hist[d];
-  }
-  st[2] = rem - above;
-  st[3] += above;
-  unsigned long long prefix = ((unsigned long long)(unsigned)st[1] << 32) | (unsigned)st[0];
-  prefix |= (unsigned long long)d << shift;
-  st[0] = (int)(unsigned)(prefix & 0xffffffffull);
-  st[1] = (int)(unsigned)(prefix >> 32);
-  if (shift == 0) st[5] = st[2];  // ties to take at the threshold value
-  for (int i = 0; i < 256; ++i) hist[i] = 0;
-}
-
-// mark selected cells into the (row-padded) S bitmap; ties at tau by ascending cell
-__global__ void sel_mark_count(const double* __restrict__ vals, const int32_t* __restrict__ cnt,
-                               const int32_t* __restrict__ st, int32_t* __restrict__ blkcnt) {
-  const int total = *cnt;
-  const unsigned long long tau = ((unsigned long long)(unsigned)st[1] << 32) | (unsigned)st[0];
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool tie = st[4] && t < total && (unsigned long long)__double_as_longlong(vals[t]) == tau;
-  int c = __popc(__ballot_sync(0xffffffffu, tie));
-  __shared__ int s[32];
-  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+  if (lane == 31) sbuf[warp] = x;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int tt = 0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) tt += s[k];
-    blkcnt[blockIdx.x] = tt;
+  if (warp == 0) {
+    int y = lane < nw ? sbuf[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += t;
+    }
+    sbuf[lane] = y;
+  }
+  __syncthreads();
+  *total = sbuf[nw - 1];
+  const int wpre = warp ? sbuf[warp - 1] : 0;
+  return wpre + x - v;
+}
+
+// offset of this block among all blocks' counts blk[q * G + b], and the total (read via L2):
+// one count per thread and a block scan (gridDim.x <= blockDim.x), not a serial loop of loads
+__device__ __forceinline__ void block_offset(const int32_t* blk, int q, int* off, int* tot, int* sbuf) {
+  __shared__ int s_off;
+  const int v = threadIdx.x < gridDim.x ? __ldcg(blk + q * gridDim.x + threadIdx.x) : 0;
+  int t;
+  const int ex = block_excl_scan(v, &t, sbuf);
+  if (threadIdx.x == blockIdx.x) s_off = ex;
+  __syncthreads();
+  *off = s_off;
+  *tot = t;
+  __syncthreads();
+}
+
+// ---- warp-cooperative ordered compaction of a block's word range [b0, b1) ----
+// Each warp owns a contiguous sub-range; words are read once per lane-stride for the count and
+// once per word (broadcast) for the write, where lane b emits bit b: coalesced list/value I/O.
+__device__ __forceinline__ void warp_range(int64_t b0, int64_t b1, int64_t* w0, int64_t* w1) {
+  const int nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5;
+  const int64_t wc = (b1 - b0 + nwarp - 1) / nwarp;
+  *w0 = min(b0 + (int64_t)warp * wc, b1);
+  *w1 = min(*w0 + wc, b1);
+}
+// per-warp counts into wcnt[warp]; returns the block total (all threads)
+__device__ __forceinline__ int blk_count(const uint32_t* M, int64_t b0, int64_t b1, int* wcnt) {
+  int64_t w0, w1;
+  warp_range(b0, b1, &w0, &w1);
+  const int lane = threadIdx.x & 31;
+  int c = 0;
+  for (int64_t w = w0 + lane; w < w1; w += 32) c += __popc(__ldcg(M + w));
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  __syncthreads();
+  if (lane == 0) wcnt[threadIdx.x >> 5] = c;
+  __syncthreads();
+  int t = 0;
+  for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += wcnt[k];
+  return t;
+}
+// write the set bits of [b0, b1) in order from position base (block offset); flat: word w
+// covers cells 32w.. (else row-padded words); optional value gather and index map
+__device__ __forceinline__ void blk_write(const uint32_t* M, int64_t b0, int64_t b1, int base, const int* wcnt,
+                                          const Geo& g, bool flat, int32_t* __restrict__ list,
+                                          const double* __restrict__ src, double* __restrict__ vals,
+                                          int32_t* __restrict__ idx, int idx_base) {
+  int64_t w0, w1;
+  warp_range(b0, b1, &w0, &w1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int pos = base;
+  for (int k = 0; k < warp; ++k) pos += wcnt[k];
+  for (int64_t wb = w0; wb < w1; wb += 32) {
+    // 32 words per coalesced load, broadcast one by one (no load in the dependent chain)
+    const uint32_t mine = wb + lane < w1 ? __ldcg(M + wb + lane) : 0u;
+    const int nwk = (int)min((int64_t)32, w1 - wb);
+    for (int k = 0; k < nwk; ++k) {
+      const uint32_t bits = __shfl_sync(0xffffffffu, mine, k);
+      const int64_t w = wb + k;
+      if ((bits >> lane) & 1u) {
+        const int p = pos + __popc(bits & ((1u << lane) - 1u));
+        const int64_t cell = (flat ? 32 * w : (w / g.wpr) * (int64_t)g.nx + 32 * (w % g.wpr)) + lane;
+        list[p] = (int32_t)cell;
+        if (vals) vals[p] = src[cell];
+        if (idx) idx[cell] = idx_base + p;
+      }
+      pos += __popc(bits);
+    }
   }
 }
 
-__global__ void sel_mark_write(Geo g, const double* __restrict__ vals, const int32_t* __restrict__ cells,
-                               const int32_t* __restrict__ cnt, const int32_t* __restrict__ st,
-                               const int32_t* __restrict__ blkoff, uint32_t* __restrict__ S) {
-  const int total = *cnt;
-  const unsigned long long tau = ((unsigned long long)(unsigned)st[1] << 32) | (unsigned)st[0];
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool in = t < total;
-  const unsigned long long b = in ? (unsigned long long)__double_as_longlong(vals[t]) : 0ull;
-  const bool tie = st[4] && in && b == tau;
-  const unsigned bal = __ballot_sync(0xffffffffu, tie);
-  __shared__ int s[32];
-  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = __popc(bal);
-  __syncthreads();
-  int pre = blkoff[blockIdx.x];
-  for (int k = 0; k < (int)(threadIdx.x >> 5); ++k) pre += s[k];
-  pre += __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
-  bool sel = false;
-  if (in) {
-    if (st[4] == 0) sel = true;
-    else if (b > tau) sel = true;
-    else if (tie && pre < st[5]) sel = true;
+
+__global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  const Geo& g = a.g;
+  const int64_t N = g.N, mw = a.mwords, nw = (int64_t)g.ny * g.wpr;
+  uint32_t* S = a.masks + (int64_t)M_S * mw;
+  uint32_t* TMP = a.masks + (int64_t)M_TMP * mw;
+  uint32_t* FLAT = a.masks + (int64_t)M_TMP2 * mw;
+  uint32_t* HM = a.masks + (int64_t)M_H * mw;
+  __shared__ int sbuf[32];
+  __shared__ int wcnt[32];
+  __shared__ int shist[NBIN];
+  __shared__ int s_digit, s_above;
+  const int tid = threadIdx.x;
+  const int G = gridDim.x;
+  int ts = 40;
+  sstamp(a.tdbg, ts);
+  // ================= select =================
+  if (a.do_select) {
+    const int64_t fw = (N + 31) / 32;
+    // A1: eps > 0 bitmap (flat words; one warp ballot per word, coalesced), zero S-hat, count
+    {
+      const int64_t bchunk = (fw + G - 1) / G;
+      const int64_t b0 = min((int64_t)blockIdx.x * bchunk, fw), b1 = min(b0 + bchunk, fw);
+      const int lane = tid & 31, warp = tid >> 5;
+      int mine = 0;
+      constexpr int U = 8;  // words per warp iteration: U independent loads in flight
+      const int nwarp = blockDim.x >> 5;
+      for (int64_t w = b0 + (int64_t)warp * U; w < b1; w += (int64_t)nwarp * U) {
+        double e[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t n = 32 * (w + u) + lane;
+          e[u] = (w + u < b1 && n < N) ? a.eps[n] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t bits = __ballot_sync(0xffffffffu, e[u] > 0.0);
+          if (lane == 0 && w + u < b1) {
+            FLAT[w + u] = bits;
+            mine += __popc(bits);
+          }
+        }
+      }
+      const BlockRange rs = thread_range(nw);
+      for (int64_t w = rs.w0; w < rs.w1; ++w) S[w] = 0u;
+      int tot;
+      block_excl_scan(mine, &tot, sbuf);
+      if (tid == 0) a.blk[0 * G + blockIdx.x] = tot;
+    }
+    grid.sync();
+  sstamp(a.tdbg, ts);
+    // A2: ordered compaction of eps > 0 -> (sel_cell, sel_val)
+    {
+      const int64_t bchunk = (fw + G - 1) / G;
+      const int64_t b0 = min((int64_t)blockIdx.x * bchunk, fw), b1 = min(b0 + bchunk, fw);
+      int off, tot;
+      block_offset(a.blk, 0, &off, &tot, sbuf);
+      blk_count(FLAT, b0, b1, wcnt);
+      blk_write(FLAT, b0, b1, off, wcnt, g, true, a.sel_cell, a.eps, a.sel_val, nullptr, 0);
+      if (blockIdx.x == 0 && tid == 0) a.counts[8] = tot;
+      // zero the first two histogram buffers
+      for (int i = blockIdx.x * blockDim.x + tid; i < 2 * NBIN; i += G * blockDim.x) a.hist[i] = 0;
+    }
+    grid.sync();
+  sstamp(a.tdbg, ts);
+    const int total = __ldcg(a.counts + 8);
+    const int ng = (int)(a.n_g < total ? a.n_g : total);
+    const bool thresh = a.n_g < total;
+    unsigned long long prefix = 0ull;
+    int rem = ng;
+    // contiguous block chunk of the compacted values
+    const int64_t vchunk = ((int64_t)total + G - 1) / G;
+    const int64_t v0 = min((int64_t)blockIdx.x * vchunk, (int64_t)total), v1 = min(v0 + vchunk, (int64_t)total);
+    if (thresh) {
+      for (int p = 0; p < 6; ++p) {
+        const int shift = p < 5 ? 53 - RADIX * p : 0;  // 53, 42, 31, 20, 9, 0
+        const int width = (shift == 0) ? 9 : RADIX;
+        const unsigned long long hm = (p == 0) ? 0ull : (~0ull << (shift + width));
+        for (int i = tid; i < NBIN; i += blockDim.x) shist[i] = 0;
+        __syncthreads();
+        for (int64_t t = v0 + tid; t < v1; t += blockDim.x) {
+          const unsigned long long bb = (unsigned long long)__double_as_longlong(a.sel_val[t]);
+          if ((bb & hm) == prefix) atomicAdd(&shist[(bb >> shift) & (NBIN - 1)], 1);
+        }
+        __syncthreads();
+        int32_t* gh = a.hist + (p % 3) * NBIN;
+        for (int i = tid; i < NBIN; i += blockDim.x)
+          if (shist[i]) atomicAdd(gh + i, shist[i]);
+        if (blockIdx.x == 0)  // buffer of pass p+1 (last read in pass p-2's pick)
+          for (int i = tid; i < NBIN; i += blockDim.x) a.hist[((p + 1) % 3) * NBIN + i] = 0;
+        grid.sync();
+  sstamp(a.tdbg, ts);
+        // pick (every block, identical): highest digit d with #(> d) < rem <= #(>= d)
+        {
+          constexpr int PER = NBIN / ST_T;  // bins per thread, top-down
+          int cnt[PER];
+          int mine = 0;
+          for (int q = 0; q < PER; ++q) {
+            const int bin = NBIN - 1 - (tid * PER + q);
+            cnt[q] = __ldcg(gh + bin);
+            mine += cnt[q];
+          }
+          int btot;
+          int above = block_excl_scan(mine, &btot, sbuf);  // count in higher bins
+          for (int q = 0; q < PER; ++q) {
+            if (above < rem && above + cnt[q] >= rem) {
+              s_digit = NBIN - 1 - (tid * PER + q);
+              s_above = above;
+            }
+            above += cnt[q];
+          }
+          __syncthreads();
+          prefix |= (unsigned long long)s_digit << shift;
+          rem -= s_above;
+          __syncthreads();
+        }
+      }
+    }
+    // A3: ties at tau by ascending cell (the compacted array is in cell order)
+    const unsigned long long tau = prefix;
+    {
+      int mine = 0;
+      if (thresh)
+        for (int64_t t = v0 + tid; t < v1; t += blockDim.x)
+          mine += ((unsigned long long)__double_as_longlong(a.sel_val[t]) == tau);
+      int btot;
+      block_excl_scan(mine, &btot, sbuf);
+      if (tid == 0) a.blk[1 * G + blockIdx.x] = btot;
+    }
+    grid.sync();
+  sstamp(a.tdbg, ts);
+    {
+      int off, tot;
+      block_offset(a.blk, 1, &off, &tot, sbuf);
+      // per-thread contiguous sub-chunk keeps the tie order = cell order
+      const int64_t len = v1 - v0;
+      const int64_t tch = (len + blockDim.x - 1) / blockDim.x;
+      const int64_t t0 = min(v0 + tid * tch, v1), t1 = min(t0 + tch, v1);
+      int mine = 0;
+      if (thresh)
+        for (int64_t t = t0; t < t1; ++t) mine += ((unsigned long long)__double_as_longlong(a.sel_val[t]) == tau);
+      int btot;
+      int tie_rank = off + block_excl_scan(mine, &btot, sbuf);
+      for (int64_t t = t0; t < t1; ++t) {
+        const unsigned long long bb = (unsigned long long)__double_as_longlong(a.sel_val[t]);
+        bool sel = !thresh || bb > tau;
+        if (thresh && bb == tau) {
+          sel = tie_rank < rem;
+          ++tie_rank;
+        }
+        if (sel) {
+          const int64_t cell = a.sel_cell[t];
+          const int i = (int)(cell % g.nx), j = (int)(cell / g.nx);
+          atomicOr(&S[(int64_t)j * g.wpr + (i >> 5)], 1u << (i & 31));
+        }
+      }
+    }
+    grid.sync();
+  sstamp(a.tdbg, ts);
   }
-  if (sel) {
-    const int64_t cell = cells[t];
-    const int i = (int)(cell % g.nx), j = (int)(cell / g.nx);
-    atomicOr(&S[(int64_t)j * g.wpr + (i >> 5)], 1u << (i & 31));
+  // ================= sets =================
+  uint32_t* B = a.masks + (int64_t)M_B * mw;
+  uint32_t* T = a.masks + (int64_t)M_T * mw;
+  uint32_t* A2 = a.masks + (int64_t)M_A2 * mw;
+  uint32_t* A1 = a.masks + (int64_t)M_A1 * mw;
+  {
+    const BlockRange r = thread_range(nw);
+    for (int64_t w = r.w0; w < r.w1; ++w) {
+      TMP[w] = xdil_word(S, g, (int)(w / g.wpr), (int)(w % g.wpr), a.band);
+      HM[w] = 0u;
+    }
+  }
+  grid.sync();
+  sstamp(a.tdbg, ts);
+  {
+    const BlockRange r = thread_range(nw);
+    for (int64_t w = r.w0; w < r.w1; ++w) {
+      const int j = (int)(w / g.wpr), wi = (int)(w % g.wpr);
+      const uint32_t sq = (g.dim == 2) ? ydil_word(TMP, g, j, wi, a.band) : __ldcg(TMP + w);
+      const uint32_t sv = __ldcg(S + w);
+      B[w] = sq & ~sv;
+      T[w] = sq | sv;
+    }
+  }
+  grid.sync();
+  sstamp(a.tdbg, ts);
+  for (int q = 0; q < 2; ++q) {
+    const uint32_t* cin = q == 0 ? T : A2;
+    uint32_t* cout_ = q == 0 ? A2 : A1;
+    const BlockRange r = thread_range(nw);
+    for (int64_t w = r.w0; w < r.w1; ++w) {
+      const int j = (int)(w / g.wpr), wi = (int)(w % g.wpr);
+      uint32_t o = xdil_word(cin, g, j, wi, a.halo);
+      if (g.dim == 2) o |= ydil_word(cin, g, j, wi, a.halo);
+      cout_[w] = o;
+    }
+    grid.sync();
+  sstamp(a.tdbg, ts);
+  }
+  // ordered compaction of S, B, T, A2, A1 (mask index == list index)
+  const int64_t rchunk = (nw + G - 1) / G;
+  const int64_t rb0 = min((int64_t)blockIdx.x * rchunk, nw), rb1 = min(rb0 + rchunk, nw);
+  for (int m = 0; m < 5; ++m) {
+    const int t = blk_count(a.masks + (int64_t)m * mw, rb0, rb1, wcnt);
+    if (tid == 0) a.blk[(2 + m) * G + blockIdx.x] = t;
+  }
+  grid.sync();
+  sstamp(a.tdbg, ts);
+  for (int m = 0; m < 5; ++m) {
+    const uint32_t* M = a.masks + (int64_t)m * mw;
+    int off, tot;
+    block_offset(a.blk, 2 + m, &off, &tot, sbuf);
+    blk_count(M, rb0, rb1, wcnt);
+    blk_write(M, rb0, rb1, off, wcnt, g, false, a.lists + (int64_t)m * N, nullptr, nullptr,
+              m == L_B ? a.idx : nullptr, 0);
+    if (blockIdx.x == 0 && tid == 0) a.counts[m] = tot;
+  }
+  grid.sync();
+  sstamp(a.tdbg, ts);
+  // ================= seam-filter halo, index map, stencil tables =================
+  if (a.rmax <= 0) return;
+  const int nb = __ldcg(a.counts + L_B);
+  const int32_t* LB = a.lists + (int64_t)L_B * N;
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + tid, gstride = (int64_t)G * blockDim.x;
+  for (int64_t t = gtid; t < nb; t += gstride) {
+    const int64_t n = LB[t];
+    const int i = (int)(n % g.nx), j = (int)(n / g.nx);
+    for (int m = -a.rmax; m <= a.rmax; ++m) {
+      if (m == 0) continue;
+      bool ok;
+      const int ii = wrapi(i + m, g.nx, g.bc, &ok) ;
+      const int iic = ok ? ii : (i + m < 0 ? 0 : g.nx - 1);  // transmissive: clamp
+      if (!get_bit(B, g, iic, j)) atomicOr(&HM[(int64_t)j * g.wpr + (iic >> 5)], 1u << (iic & 31));
+      if (g.dim == 2) {
+        const int jj = wrapi(j + m, g.ny, g.bc, &ok);
+        const int jjc = ok ? jj : (j + m < 0 ? 0 : g.ny - 1);
+        if (!get_bit(B, g, i, jjc)) atomicOr(&HM[(int64_t)jjc * g.wpr + (i >> 5)], 1u << (i & 31));
+      }
+    }
+  }
+  grid.sync();
+  sstamp(a.tdbg, ts);
+  {
+    const int t = blk_count(HM, rb0, rb1, wcnt);
+    if (tid == 0) a.blk[7 * G + blockIdx.x] = t;
+  }
+  grid.sync();
+  sstamp(a.tdbg, ts);
+  {
+    int off, tot;
+    block_offset(a.blk, 7, &off, &tot, sbuf);
+    blk_count(HM, rb0, rb1, wcnt);
+    blk_write(HM, rb0, rb1, off, wcnt, g, false, a.lists + (int64_t)L_H * N, nullptr, nullptr, a.idx, nb);
+    if (blockIdx.x == 0 && tid == 0) a.counts[L_H] = tot;
+  }
+  grid.sync();
+  sstamp(a.tdbg, ts);
+  for (int64_t t = gtid; t < nb; t += gstride) {
+    const int64_t n = LB[t];
+    const int i = (int)(n % g.nx), j = (int)(n / g.nx);
+    for (int m = -a.rmax; m <= a.rmax; ++m) {
+      bool ok;
+      int ii = wrapi(i + m, g.nx, g.bc, &ok);
+      if (!ok) ii = i + m < 0 ? 0 : g.nx - 1;
+      a.tab[(int64_t)(m + 3) * N + t] = __ldcg(a.idx + (int64_t)j * g.nx + ii);
+      if (g.dim == 2) {
+        int jj = wrapi(j + m, g.ny, g.bc, &ok);
+        if (!ok) jj = j + m < 0 ? 0 : g.ny - 1;
+        a.tab[(int64_t)(7 + m + 3) * N + t] = __ldcg(a.idx + (int64_t)jj * g.nx + i);
+      }
+    }
   }
 }
 
 }  // namespace
 
-hrom_status compact_masks(hrom_ctx* c, const int* which, int nwhich) {
-  CmpJob job{};
-  job.n = nwhich;
-  for (int k = 0; k < nwhich; ++k) {
-    const int l = which[k];  // list index == mask index for S, B, T, A2, A1
-    job.mask[k] = c->b.masks + (int64_t)l * c->mwords;
-    job.list[k] = c->b.lists + (int64_t)l * c->g.N;
-    job.vals[k] = nullptr;
-    job.src[k] = nullptr;
-    job.count_out[k] = c->b.counts + l;
-    job.flat[k] = 0;
-  }
-  return run_compaction(c, job, c->mwords);
-}
-
-// S-hat bitmap (in masks[M_S]) -> B, T, A2, A1 bitmaps and their ascending lists.
-hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S) {
-  const Geo& g = c->g;
-  uint32_t* M = c->b.masks;
-  const int64_t mw = c->mwords;
-  uint32_t* S = M + M_S * mw;
-  if (dev_mask_S && dev_mask_S != S)
-    HROM_CK(cudaMemcpyAsync(S, dev_mask_S, mw * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->st));
-  const int grid = (int)std::min<int64_t>((mw + 255) / 256, (int64_t)c->nsm * 16);
-  xdil_kernel<<<grid, 256, 0, c->st>>>(g, S, M + M_TMP * mw, c->P.band);
-  band_kernel<<<grid, 256, 0, c->st>>>(g, M + M_TMP * mw, S, M + M_B * mw, M + M_T * mw, c->P.band);
-  cross_kernel<<<grid, 256, 0, c->st>>>(g, M + M_T * mw, M + M_A2 * mw, c->P.halo);
-  cross_kernel<<<grid, 256, 0, c->st>>>(g, M + M_A2 * mw, M + M_A1 * mw, c->P.halo);
-  HROM_LAUNCH_CK();
-  c->nlaunch += 4;
-  const int which[5] = {L_S, L_B, L_T, L_A2, L_A1};
-  return compact_masks(c, which, 5);
-}
-
-// top-n_g of eps > 0 -> S bitmap (masks[M_S]); ties at the threshold by ascending cell.
-hrom_status select_topn(hrom_ctx* c, const double* eps, int64_t n_g) {
-  const int64_t N = c->g.N;
-  const int64_t fw = (N + 31) / 32;
-  uint32_t* flat = c->b.masks + (int64_t)M_TMP2 * c->mwords;  // mwords >= fw
-  int32_t* cnt = c->b.counts + 8;
-  int32_t* hist = c->b.hist;
-  int32_t* st = c->b.hist + 256;
-  const int grid = c->nsm * 8;
-  nz_kernel<<<grid, 256, 0, c->st>>>(eps, N, flat);
-  HROM_LAUNCH_CK();
-  CmpJob job{};
-  job.n = 1;
-  job.mask[0] = flat;
-  job.list[0] = c->b.sel_cell;
-  job.vals[0] = c->b.sel_val;
-  job.src[0] = eps;
-  job.count_out[0] = cnt;
-  job.flat[0] = 1;
-  hrom_status s = run_compaction(c, job, fw);
-  if (s != HROM_OK) return s;
-  HROM_CK(cudaMemsetAsync(hist, 0, 256 * sizeof(int32_t), c->st));
-  sel_init<<<1, 1, 0, c->st>>>(st, cnt, (long long)n_g);
-  for (int shift = 56; shift >= 0; shift -= 8) {
-    sel_hist<<<c->nsm * 2, 512, 0, c->st>>>(c->b.sel_val, cnt, hist, st, shift);
-    sel_pick<<<1, 1, 0, c->st>>>(hist, st, shift);
-  }
-  HROM_LAUNCH_CK();
-  // mark: count ties per block, scan, write
-  uint32_t* S = c->b.masks + (int64_t)M_S * c->mwords;
-  HROM_CK(cudaMemsetAsync(S, 0, c->mwords * sizeof(uint32_t), c->st));
-  const int nb = (int)((N + 1023) / 1024);
-  sel_mark_count<<<nb, 1024, 0, c->st>>>(c->b.sel_val, cnt, st, c->b.blk);
-  CmpJob one{};
-  one.n = 1;
-  one.count_out[0] = nullptr;
-  cmp_scan_kernel<<<1, 1024, 0, c->st>>>(one, c->b.blk, nb);
-  sel_mark_write<<<nb, 1024, 0, c->st>>>(c->g, c->b.sel_val, c->b.sel_cell, cnt, st, c->b.blk, S);
-  HROM_LAUNCH_CK();
-  c->nlaunch += 1 + 1 + 16 + 3;
+hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long long n_g) {
+  SetsArgs a{};
+  a.g = c->g;
+  a.do_select = do_select ? 1 : 0;
+  a.eps = eps;
+  a.n_g = n_g;
+  a.halo = c->P.halo;
+  a.band = c->P.band;
+  a.rmax = 0;
+  if (c->P.filter_max_sweeps > 0)
+    for (int i = 0; i < c->P.n_filter_orders; ++i) a.rmax = std::max(a.rmax, c->P.filter_orders[i] / 2);
+  a.masks = c->b.masks;
+  a.mwords = c->mwords;
+  a.lists = c->b.lists;
+  a.counts = c->b.counts;
+  a.sel_val = c->b.sel_val;
+  a.sel_cell = c->b.sel_cell;
+  a.blk = c->b.blk;
+  a.hist = c->b.hist;
+  a.idx = c->b.fidx;
+  a.tab = c->b.ftab;
+  a.tdbg = c->b.dbg;
+  if ((int64_t)8 * c->sets_blocks > c->b.blk_len) return HROM_E_INVALID;
+  void* args[] = {&a};
+  HROM_CK(cudaLaunchCooperativeKernel((void*)sets_kernel, dim3(c->sets_blocks), dim3(ST_T), args, 0, c->st));
+  ++c->nlaunch;
   return HROM_OK;
+}
+
+int sets_occupancy() {
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sets_kernel, ST_T, 0);
+  return nb;
+}
+
+namespace {
+
+}  // namespace
+
+// S-hat bitmap (in masks[M_S]) -> B, T, A2, A1 bitmaps, their ascending lists and the
+// seam-filter tables.
+hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S) {
+  uint32_t* S = c->b.masks + (int64_t)M_S * c->mwords;
+  if (dev_mask_S && dev_mask_S != S)
+    HROM_CK(cudaMemcpyAsync(S, dev_mask_S, c->mwords * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->st));
+  return launch_sets(c, false, nullptr, 0);
+}
+
+// top-n_g of eps > 0 -> S-hat (ties at the threshold by ascending cell), then build_sets.
+hrom_status select_and_build(hrom_ctx* c, const double* eps, int64_t n_g) {
+  return launch_sets(c, true, eps, (long long)n_g);
 }
 
 }  // namespace hrom

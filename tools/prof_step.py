@@ -24,7 +24,9 @@ for k in range(nh):
     cnt = cnt[:16] + cnt[16:21]
     if k % every == 0 or k == nh - 1:
       print(f"hybrid {k}: " + " ".join(f"{n}={v[0]:.3f}" for n, v in sec.items() if v[1]), "counters", cnt, flush=True)
-      t = rom.debug_timers(40)
+      t = rom.debug_timers(64)
+      ts = [x for x in t[40:64] if x > 0]
+      print("  sets us: " + " ".join("%.1f" % ((ts[i + 1] - ts[i]) / 1000) for i in range(len(ts) - 1) if ts[i + 1] > ts[i]), flush=True)
       d = [(t[i + 1] - t[i]) / 1000 for i in range(39) if t[i + 1] > t[i] and t[i] > 0 and t[i + 1] - t[i] < 1e8]
       print("  filter us: prologue %.1f sweeps %s" % (d[0] if d else -1, " ".join("%.1f" % x for x in d[1:])), flush=True)
 rom.sync()
