@@ -280,7 +280,8 @@ def cpu_sample(steps: int = 1, side: int = 256):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=64,
+                    help="timed hybrid steps; the default w = 64 spans one Gram re-base period (amortised in)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="hrom", choices=["hrom", "reference"])
     ap.add_argument("--config", type=int, default=4)

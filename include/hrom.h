@@ -85,7 +85,11 @@ hrom_status hrom_full_step(hrom_ctx* ctx, double dt_override, double* dev_dt_out
  * filter residual), gappy coordinates y (Eq. 8, P = S-hat), fill of the complement
  * with psi + Phi y, indicator eps, seam filter.
  * dev_mask: S-hat bitmap, or NULL to use the sets built by the last hrom_sample.
- * Requires a basis (hrom_update_basis after step >= w-1). */
+ * Requires a basis (hrom_update_basis after step >= w-1).
+ * Positivity (O11): if the hybrid state has rho <= 0 or p <= 0 anywhere, the step is
+ * redone on the device as a full step from gamma_k with the same dt (the indicator of the
+ * hybrid step is kept, as in the oracle); only a failure of that full step is latched and
+ * returned by hrom_sync.  Escalations are counted in debug counter [15]. */
 hrom_status hrom_hybrid_step(hrom_ctx* ctx, const uint32_t* dev_mask, double dt_override,
                              double* dev_dt_out);
 
@@ -131,6 +135,11 @@ const char* hrom_status_string(hrom_status s);
  * mask S-hat_{k+1}; builds the basis as hrom_update_basis would after step k (k >= w). */
 hrom_status hrom_set_window(hrom_ctx* ctx, int64_t k, const double* any_snaps, int32_t nsnaps,
                             const uint32_t* any_mask_next);
+/* Write gamma_k into its ring slot (streams a window column by column, config 5, without a
+ * (w+1) x D staging buffer); no basis work.  hrom_rebuild_basis(k) then treats
+ * gamma_{k-w}..gamma_k as the window and builds the basis exactly as hrom_set_window. */
+hrom_status hrom_put_snapshot(hrom_ctx* ctx, int64_t k, const double* any_q);
+hrom_status hrom_rebuild_basis(hrom_ctx* ctx, int64_t k, const uint32_t* any_mask_next);
 /* Phi_{k+1} (D x r_eff, column-major) and psi_{k+1} (D), materialised by the lift kernel. */
 hrom_status hrom_get_basis(hrom_ctx* ctx, double* dev_phi, double* dev_psi);
 hrom_status hrom_get_indicator(hrom_ctx* ctx, double* any_eps);      /* N values */
@@ -144,7 +153,9 @@ int64_t hrom_mask_words(const hrom_ctx* ctx);                        /* words pe
 hrom_status hrom_gram(hrom_ctx* ctx, const double* const* dev_cols, int32_t ncol, int64_t rows,
                       const double* dev_rho, double* dev_C);
 /* Overwrite gamma_k (the latest snapshot) in place, without touching the schedule
- * (end-to-end benchmarking of host-resident states). */
+ * (end-to-end benchmarking of host-resident states).  The window Gram and the basis already
+ * built from gamma_k are kept: the caller supplies the same state (e.g. a host round trip);
+ * to change the trajectory use hrom_set_state / hrom_set_window. */
 hrom_status hrom_put_state(hrom_ctx* ctx, const double* any_q);
 
 /* ---- measurement hooks ---- */
@@ -159,7 +170,8 @@ hrom_status hrom_profile_read(hrom_ctx* ctx, double* ms, int64_t* counts, int32_
 int64_t hrom_launch_count(const hrom_ctx* ctx);
 /* Synchronises and copies n <= 32 int32 device counters: [0] r_eff, [2] LSQ status,
  * [4..6] filter sweeps per order, [8] eigen sweeps (basis), [9] eigen sweeps (pinv);
- * [16 + l] the size of cell list l (0 S-hat, 1 seam band B, 2 T, 3 A2, 4 A1). */
+ * [10..14] eigen-solve phase timings (kcycles), [15] positivity escalations;
+ * [16 + l] the size of cell list l (0 S-hat, 1 seam band B, 2 T, 3 A2, 4 A1, 5 filter halo). */
 hrom_status hrom_debug_counters(hrom_ctx* ctx, int32_t* any_out, int32_t n);
 /* Synchronises and copies n <= 64 device timestamps (ns, %globaltimer) written by the last
  * seam-filter launch: [0] start, [1] after the compaction prologue, [2 + s] after sweep s. */

@@ -274,6 +274,7 @@ hrom_status hrom_set_state(hrom_ctx* c, const double* any_q) {
   if (s0 != HROM_OK) return s0;
   HROM_CK(cudaMemsetAsync(c->b.ureg + 1, 0xff, sizeof(unsigned long long), c->st));
   c->k = 0;
+  c->last_hybrid = false;
   c->basis_ready = c->sets_ready = c->gram_row_ready = false;
   c->rebase_k = -1000000;
   c->last_err_cell = -1;
@@ -302,6 +303,7 @@ hrom_status hrom_full_step(hrom_ctx* c, double dt_override, double* dev_dt_out) 
   if ((s = launch_stage(c, 3, qn, U2, out, nullptr, 0, dt_override)) != HROM_OK) return s;
   prof_end(c, SEC_FULL);
   c->k = kn;
+  c->last_hybrid = false;
   c->gram_row_ready = false;
   c->sets_ready = false;
   return HROM_OK;
@@ -361,9 +363,10 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
     if ((s = launch_band_gram(c, c->win, out)) != HROM_OK) return s;
   prof_end(c, SEC_BANDGRAM);
   prof_begin(c, SEC_POS);
-  if ((s = launch_positivity(c, out, kn)) != HROM_OK) return s;
+  if ((s = launch_positivity(c, qn, out, kn)) != HROM_OK) return s;
   prof_end(c, SEC_POS);
   c->k = kn;
+  c->last_hybrid = true;
   c->gram_row_ready = (c->P.gram_mode == 0);
   c->sets_ready = false;
   return HROM_OK;
@@ -398,7 +401,11 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
     if ((s = launch_gram_row(c, c->win, c->slot_of(k))) != HROM_OK) return s;
     if ((s = reduce_gram_row(c, c->win, c->slot_of(k), false)) != HROM_OK) return s;
   } else {
-    if ((s = reduce_gram_row(c, c->win, c->slot_of(k), true)) != HROM_OK) return s;
+    // fused row of the fill pass + band; if the step was redone as a full step (device flag
+    // ureg[3]), the row is recomputed from the final gamma_k instead
+    const unsigned long long* esc = c->last_hybrid ? c->b.ureg + 3 : nullptr;
+    if (esc && (s = launch_gram_row(c, c->win, c->slot_of(k), esc)) != HROM_OK) return s;
+    if ((s = reduce_gram_row(c, c->win, c->slot_of(k), true, esc)) != HROM_OK) return s;
   }
   prof_end(c, SEC_BASIS);
   // eigen-solve: deferred to the side stream after the sampling kernel (a cooperative kernel
@@ -453,11 +460,17 @@ hrom_status hrom_reconstruct(hrom_ctx* c, const uint32_t* dev_mask, double* dev_
     c->sets_ready = true;
   }
   if (!c->sets_ready) return HROM_E_STATE;
+  prof_begin(c, SEC_GATHER);
   if ((s = gram_gathered(c, plain(dev_v))) != HROM_OK) return s;
+  prof_end(c, SEC_GATHER);
   basis_join(c);
+  prof_begin(c, SEC_SOLVE);
   if ((s = small_solve(c)) != HROM_OK) return s;
+  prof_end(c, SEC_SOLVE);
   HROM_CK(cudaMemsetAsync(c->b.eps, 0, c->g.N * sizeof(double), c->st));
+  prof_begin(c, SEC_FILL);
   if ((s = launch_fill(c, c->win, 0, plain(dev_v), plain(dev_v), false)) != HROM_OK) return s;
+  prof_end(c, SEC_FILL);
   if ((s = launch_eps_cells(c)) != HROM_OK) return s;
   if (dev_y_out) HROM_CK(cudaMemcpyAsync(dev_y_out, c->b.y, c->r * sizeof(double), cudaMemcpyDefault, c->st));
   if (dev_eps_out)
@@ -474,7 +487,9 @@ hrom_status hrom_filter(hrom_ctx* c, const uint32_t* dev_mask, double* dev_v, co
     c->sets_ready = true;
   }
   if (!c->sets_ready) return HROM_E_STATE;
+  prof_begin(c, SEC_FILTER);
   if ((s = launch_filter(c, plain(dev_v), plain(dev_F), dev_kept_out)) != HROM_OK) return s;
+  prof_end(c, SEC_FILTER);
   return HROM_OK;
 }
 
@@ -519,16 +534,18 @@ int32_t hrom_effective_rank(hrom_ctx* c) {
   return r;
 }
 
-hrom_status hrom_set_window(hrom_ctx* c, int64_t k, const double* any_snaps, int32_t nsnaps,
-                            const uint32_t* any_mask_next) {
-  if (!c || !any_snaps) return HROM_E_INVALID;
-  if (k < c->w || nsnaps != c->w + 1) return HROM_E_INVALID;
-  for (int t = 0; t < nsnaps; ++t) {
-    hrom_status s0 = copy_slot(c, c->slot_of(k - c->w + t), any_snaps + (int64_t)t * c->g.D, nullptr);
-    if (s0 != HROM_OK) return s0;
-  }
+hrom_status hrom_put_snapshot(hrom_ctx* c, int64_t k, const double* any_q) {
+  if (!c || !any_q || k < 0) return HROM_E_INVALID;
+  return copy_slot(c, c->slot_of(k), any_q, nullptr);
+}
+
+hrom_status hrom_rebuild_basis(hrom_ctx* c, int64_t k, const uint32_t* any_mask_next) {
+  if (!c) return HROM_E_INVALID;
+  if (k < c->w) return HROM_E_INVALID;
+  basis_join(c);
   HROM_CK(cudaMemsetAsync(c->b.ureg + 1, 0xff, sizeof(unsigned long long), c->st));
   c->k = k;
+  c->last_hybrid = false;
   c->basis_ready = false;
   c->gram_row_ready = false;
   c->rebase_k = -1000000;
@@ -541,6 +558,17 @@ hrom_status hrom_set_window(hrom_ctx* c, int64_t k, const double* any_snaps, int
     c->sets_ready = true;
   }
   return HROM_OK;
+}
+
+hrom_status hrom_set_window(hrom_ctx* c, int64_t k, const double* any_snaps, int32_t nsnaps,
+                            const uint32_t* any_mask_next) {
+  if (!c || !any_snaps) return HROM_E_INVALID;
+  if (k < c->w || nsnaps != c->w + 1) return HROM_E_INVALID;
+  for (int t = 0; t < nsnaps; ++t) {
+    hrom_status s0 = hrom_put_snapshot(c, k - c->w + t, any_snaps + (int64_t)t * c->g.D);
+    if (s0 != HROM_OK) return s0;
+  }
+  return hrom_rebuild_basis(c, k, any_mask_next);
 }
 
 hrom_status hrom_get_basis(hrom_ctx* c, double* dev_phi, double* dev_psi) {

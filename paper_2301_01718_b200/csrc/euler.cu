@@ -119,8 +119,12 @@ template <int DIM, int RECON>
 __global__ void __launch_bounds__(256) stage_kernel(Geo g, int stage, const SRef qn, const SRef qin, const SRef out,
                                                     const int32_t* __restrict__ list,
                                                     const int32_t* __restrict__ count,
-                                                    const double* __restrict__ dtp) {
+                                                    const double* __restrict__ dtp,
+                                                    const unsigned long long* __restrict__ run_if,
+                                                    int32_t* __restrict__ esc_count) {
   constexpr int C = DIM + 2;
+  if (run_if && *run_if == ~0ull) return;  // conditional full-step re-run (positivity escalation)
+  if (run_if && esc_count && stage == 1 && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(esc_count, 1);
   const int64_t total = list ? (int64_t)(*count) : g.N;
   const double dt = *dtp;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -175,8 +179,11 @@ __global__ void __launch_bounds__(256) smax_kernel(Geo g, const SRef q, unsigned
   }
 }
 
-__global__ void dt_finalize(const unsigned long long* smax, double cfl, double dt_override, double* dt) {
-  const double s = __longlong_as_double((long long)*smax);
+__global__ void dt_finalize(const unsigned long long* smax, const unsigned long long* smax_alt,
+                            const unsigned long long* esc, double cfl, double dt_override, double* dt) {
+  // smax_alt: the escalated state's maximum when the previous step was redone as a full step
+  const unsigned long long* src = (esc && *esc != ~0ull) ? smax_alt : smax;
+  const double s = __longlong_as_double((long long)*src);
   *dt = dt_override > 0.0 ? dt_override : cfl / s;
 }
 
@@ -184,8 +191,10 @@ __global__ void dt_finalize(const unsigned long long* smax, double cfl, double d
 // state (the next step's dt reads it instead of a second pass over the state)
 template <int DIM>
 __global__ void __launch_bounds__(256) positivity_kernel(Geo g, const SRef q, unsigned long long* __restrict__ bad,
-                                                         unsigned long long* __restrict__ smax) {
+                                                         unsigned long long* __restrict__ smax,
+                                                         const unsigned long long* __restrict__ run_if) {
   constexpr int C = DIM + 2;
+  if (run_if && *run_if == ~0ull) return;
   double m = 0.0;
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N;
        n += (int64_t)gridDim.x * blockDim.x) {
@@ -219,10 +228,15 @@ __global__ void __launch_bounds__(256) positivity_kernel(Geo g, const SRef q, un
 
 hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override, int64_t kq) {
   const unsigned long long* smax = c->b.ureg;
+  const unsigned long long *alt = nullptr, *esc = nullptr;
   int nl = 1;
   if (dt_override <= 0.0) {
     if (c->smax_k == kq) {
-      smax = c->b.ureg + 2;  // computed by the positivity pass that closed step kq
+      // computed by the positivity pass that closed step kq (ureg[2]); ureg[0] if that step
+      // was redone as a full step (ureg[3] != ~0)
+      smax = c->b.ureg + 2;
+      alt = c->b.ureg;
+      esc = c->b.ureg + 3;
     } else {
       HROM_CK(cudaMemsetAsync(c->b.ureg, 0, sizeof(unsigned long long), c->st));
       const int grid = c->nsm * 8;
@@ -232,34 +246,50 @@ hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override, int64_t kq) {
       ++nl;
     }
   }
-  dt_finalize<<<1, 1, 0, c->st>>>(smax, c->g.cfl, dt_override, c->b.dreg);
+  dt_finalize<<<1, 1, 0, c->st>>>(smax, alt, esc, c->g.cfl, dt_override, c->b.dreg);
   HROM_LAUNCH_CK();
   c->nlaunch += nl;
   return HROM_OK;
 }
 
 hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, const int32_t* list, int list_idx,
-                         double /*dt_override*/) {
+                         double /*dt_override*/, const unsigned long long* run_if) {
   const int grid = c->nsm * 8;
   const int32_t* cnt = list ? c->b.counts + list_idx : nullptr;
   const Geo& g = c->g;
+  int32_t* ec = c->b.ireg + 15;
   if (g.dim == 1) {
-    if (g.recon == 1) stage_kernel<1, 1><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg);
-    else stage_kernel<1, 2><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg);
+    if (g.recon == 1) stage_kernel<1, 1><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg, run_if, ec);
+    else stage_kernel<1, 2><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg, run_if, ec);
   } else {
-    if (g.recon == 1) stage_kernel<2, 1><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg);
-    else stage_kernel<2, 2><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg);
+    if (g.recon == 1) stage_kernel<2, 1><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg, run_if, ec);
+    else stage_kernel<2, 2><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg, run_if, ec);
   }
   HROM_LAUNCH_CK();
   c->nlaunch += 1;
   return HROM_OK;
 }
 
-hrom_status launch_positivity(hrom_ctx* c, SRef q, int64_t kq) {
+// O11 after a hybrid step: per-step flag ureg[3] and the wave-speed maximum ureg[2]; then, only
+// if the flag is set (device-side condition, S:478 escalation): the step is redone as a full
+// step from gamma_{k-1} with the same dt, re-checked (latched error ureg[1], maximum ureg[0]).
+hrom_status launch_positivity(hrom_ctx* c, SRef qprev, SRef q, int64_t kq) {
   const int grid = c->nsm * 8;
-  HROM_CK(cudaMemsetAsync(c->b.ureg + 2, 0, sizeof(unsigned long long), c->st));
-  if (c->g.dim == 1) positivity_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg + 1, c->b.ureg + 2);
-  else positivity_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg + 1, c->b.ureg + 2);
+  unsigned long long* u = c->b.ureg;
+  HROM_CK(cudaMemsetAsync(u + 2, 0, sizeof(unsigned long long), c->st));
+  HROM_CK(cudaMemsetAsync(u + 3, 0xff, sizeof(unsigned long long), c->st));
+  HROM_CK(cudaMemsetAsync(u, 0, sizeof(unsigned long long), c->st));
+  if (c->g.dim == 1) positivity_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, u + 3, u + 2, nullptr);
+  else positivity_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, u + 3, u + 2, nullptr);
+  HROM_LAUNCH_CK();
+  c->nlaunch += 1;
+  hrom_status s;
+  const SRef U1 = plain(c->b.U1), U2 = plain(c->b.U2);
+  if ((s = launch_stage(c, 1, qprev, qprev, U1, nullptr, 0, 0.0, u + 3)) != HROM_OK) return s;
+  if ((s = launch_stage(c, 2, qprev, U1, U2, nullptr, 0, 0.0, u + 3)) != HROM_OK) return s;
+  if ((s = launch_stage(c, 3, qprev, U2, q, nullptr, 0, 0.0, u + 3)) != HROM_OK) return s;
+  if (c->g.dim == 1) positivity_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, u + 1, u, u + 3);
+  else positivity_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, u + 1, u, u + 3);
   HROM_LAUNCH_CK();
   c->nlaunch += 1;
   c->smax_k = kq;

@@ -46,6 +46,7 @@ struct FillArgs {
   const uint32_t* mB;
   double* eps_elem;
   double* part;            // [grid][nU+1]
+  const unsigned long long* run_if;  // nullable: run only if *run_if != ~0 (escalated step)
 };
 
 // SH: compile-time upper bound of the physical slots per half (ceil((w + 2) / 2)).
@@ -53,6 +54,7 @@ struct FillArgs {
 // the DOF's slot values in registers (SH doubles) and SH Gram accumulators.
 template <int SH>
 __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
+  if (a.run_if && *a.run_if == ~0ull) return;  // conditional re-run (positivity escalation)
   extern __shared__ __align__(128) unsigned char smraw[];
   const int nU = a.W.nU, w = a.W.w, nsl = a.nslots;
   const int64_t nsr = a.g.nsr;
@@ -247,8 +249,10 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
 // entry with a fixed-order tree (deterministic)
 __global__ void __launch_bounds__(1024) gram_row_reduce(const double* __restrict__ part, int nblk,
                                                         const double* __restrict__ bpart, int nbblk, Win W,
-                                                        int new_slot, double* __restrict__ C, int ldc) {
+                                                        int new_slot, double* __restrict__ C, int ldc,
+                                                        const unsigned long long* __restrict__ esc) {
   const int nU = W.nU;
+  if (esc && *esc != ~0ull) bpart = nullptr;  // escalated step: the row was recomputed from gamma_k
   constexpr int TPE = 16;
   for (int base = 0; base < (nU + 1) * TPE; base += blockDim.x) {
     const int idx = base + threadIdx.x, s = idx / TPE, sub = idx % TPE;
@@ -315,8 +319,10 @@ hrom_status launch_fill_t(hrom_ctx* c, const FillArgs& a, size_t smem) {
 
 int fill_max_gram_slots() { return 68; }
 
-hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef out, bool out_in_ring) {
+hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef out, bool out_in_ring,
+                        const unsigned long long* run_if) {
   FillArgs a{};
+  a.run_if = run_if;
   a.g = c->g;
   a.W = W;
   a.mode = mode;
@@ -346,14 +352,15 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef ou
   return HROM_E_INVALID;  // wider windows use gram_mode = 1 (hrom_create enforces it)
 }
 
-hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot) {
-  return launch_fill(c, W, MODE_READ, plain(nullptr), c->slot_ref(new_slot), true);
+hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot, const unsigned long long* run_if) {
+  return launch_fill(c, W, MODE_READ, plain(nullptr), c->slot_ref(new_slot), true, run_if);
 }
 
-hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_band) {
+hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_band,
+                            const unsigned long long* esc) {
   gram_row_reduce<<<1, 1024, 0, c->st>>>(c->b.gpart, c->fill_grid,
                                          with_band ? c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1) : nullptr,
-                                         c->band_blocks, W, new_slot, c->b.C, kMaxSlots);
+                                         c->band_blocks, W, new_slot, c->b.C, kMaxSlots, esc);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;

@@ -106,7 +106,7 @@ struct Bufs {
   double* eigA = nullptr;     // kMaxSlots^2 scratch
   int32_t* ireg = nullptr;    // small int registers: [0] reff, [1] err cell lo, ...
   double* dreg = nullptr;     // small double registers: [0] dt, ...
-  unsigned long long* ureg = nullptr;  // [0] smax bits, [1] min bad cell
+  unsigned long long* ureg = nullptr;  // [0] smax bits, [1] latched min bad cell, [2] fused smax, [3] step flag
   long long* dbg = nullptr;   // 64 debug timestamps (seam filter)
   // sampling scratch
   double* sel_val = nullptr;   // N
@@ -145,6 +145,7 @@ struct hrom_ctx {
   int sets_blocks = 0;       // cooperative sets kernel grid (one block per SM)
   int64_t last_err_cell = -1;
   int64_t smax_k = -1;       // state index whose max wave speed is in ureg[2] (positivity pass)
+  bool last_hybrid = false;  // the latest step was a hybrid step (its positivity flag is ureg[3])
   int64_t nlaunch = 0;       // kernels launched by this context (host-side count)
   // optional per-section CUDA-event timing (hrom_profile)
   bool prof = false;
@@ -195,8 +196,8 @@ namespace hrom {
 // euler.cu
 hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override, int64_t kq);
 hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, const int32_t* list, int list_idx,
-                         double dt_override);
-hrom_status launch_positivity(hrom_ctx* c, SRef q, int64_t kq);
+                         double dt_override, const unsigned long long* run_if = nullptr);
+hrom_status launch_positivity(hrom_ctx* c, SRef qprev, SRef q, int64_t kq);
 // masks.cu
 hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S);
 hrom_status select_and_build(hrom_ctx* c, const double* eps, int64_t n_g);
@@ -210,9 +211,11 @@ hrom_status small_solve(hrom_ctx* c);
 hrom_status basis_from_gram(hrom_ctx* c, const Win& W);
 hrom_status lift(hrom_ctx* c, const Win& W, double* phi, double* psi);
 // fill.cu
-hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef out, bool out_in_ring);
-hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot);
-hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_band);
+hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef out, bool out_in_ring,
+                        const unsigned long long* run_if = nullptr);
+hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot, const unsigned long long* run_if = nullptr);
+hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_band,
+                            const unsigned long long* esc = nullptr);
 hrom_status launch_eps_cells(hrom_ctx* c);
 hrom_status launch_mean(hrom_ctx* c, const Win& W, SRef out);
 // filter.cu

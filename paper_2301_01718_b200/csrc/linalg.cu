@@ -14,186 +14,11 @@
 namespace hrom {
 namespace {
 
-constexpr int RT = 64;        // rows per Gram tile
-constexpr int LDT = RT + 4;   // padded column stride in smem (conflict-free fragments)
-constexpr int GT = 256;       // threads per Gram CTA
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
-}
-
-struct GramArgs {
-  int mode;                  // 0 contiguous columns (shift rho), 1 gathered rows of S-hat
-  int ncol;                  // real columns
-  int nsb;                   // super blocks (16 columns each)
-  int64_t rows;              // contiguous rows (mode 0)
-  const double* const* cols; // mode 0: column pointers
-  int64_t ns;                // mode 0: slab stride of the columns (1 = plain)
-  SRef rho;                  // mode 0: shift (rho.p nullable)
-  // mode 1
-  Geo g;
-  Win W;
-  const double* ring;
-  const int32_t* list;       // S-hat cells
-  const int32_t* count;      // |S-hat|
-  SRef src_b;                // HDM values on S-hat rows
-  double* part;              // [grid][nsb*16][nsb*16]
-};
-
-// One tile of the Gram: C += T^T T over RT rows, T in smem column-major (ld LDT).
-template <int TPW>
-__device__ __forceinline__ void gram_tile(const double* tile, int nsb, double (&acc)[TPW][8]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gid = lane >> 2, tig = lane & 3;
-  const int ntask = nsb * (nsb + 1) / 2;
-#pragma unroll
-  for (int kk = 0; kk < RT; kk += 4) {
-#pragma unroll
-    for (int t = 0; t < TPW; ++t) {
-      const int task = warp + t * (GT / 32);
-      if (task < ntask) {
-        // task -> (sa, sb), sa <= sb, row-major over the upper triangle
-        int sa = 0, rem = task;
-        while (rem >= nsb - sa) { rem -= nsb - sa; ++sa; }
-        const int sb = sa + rem;
-        const double a0 = tile[(16 * sa + gid) * LDT + kk + tig];
-        const double a1 = tile[(16 * sa + 8 + gid) * LDT + kk + tig];
-        const double b0 = tile[(16 * sb + gid) * LDT + kk + tig];
-        const double b1 = tile[(16 * sb + 8 + gid) * LDT + kk + tig];
-        dmma(acc[t][0], acc[t][1], a0, b0);
-        dmma(acc[t][2], acc[t][3], a0, b1);
-        dmma(acc[t][4], acc[t][5], a1, b0);
-        dmma(acc[t][6], acc[t][7], a1, b1);
-      }
-    }
-  }
-}
-
-template <int TPW>
-__global__ void __launch_bounds__(GT, (TPW <= 2) ? 2 : 1) gram_kernel(GramArgs a) {
-  extern __shared__ double smem[];
-  double* tile = smem;                      // [nsb*16][LDT]
-  const int ncp = a.nsb * 16;
-  double acc[TPW][8];
-#pragma unroll
-  for (int t = 0; t < TPW; ++t)
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[t][q] = 0.0;
-  int64_t total_rows;
-  if (a.mode == 0) total_rows = a.rows;
-  else total_rows = (int64_t)(*a.count) * a.g.c;
-  const int64_t ntiles = (total_rows + RT - 1) / RT;
-  for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-    const int64_t r0 = tl * RT;
-    if (a.mode == 0) {
-      for (int idx = threadIdx.x; idx < ncp * RT; idx += GT) {
-        const int col = idx / RT, k = idx % RT;
-        const int64_t row = r0 + k;
-        double v = 0.0;
-        if (col < a.ncol && row < total_rows) {
-          v = a.cols[col][sidx(SRef{nullptr, a.ns}, row)];
-          if (a.rho.p) v -= a.rho.p[sidx(a.rho, row)];
-        }
-        tile[col * LDT + k] = v;
-      }
-    } else {
-      // gathered rows: row t -> (var = t / nS, idx = t % nS), element e = var*N + cell.
-      // X slot s (s >= nU-w) lands in column s-(nU-w); the psi_prev-only slot (nU = w+1) in
-      // column w+1; the HDM value b in column w.  Then centre in place.
-      const int nS = *a.count;
-      const int nU = a.W.nU, w = a.W.w;
-      const int xoff = nU - w;
-      double* psi = smem + (size_t)ncp * LDT;  // [2][RT]
-      __shared__ int64_t erow[RT];             // DOF of each tile row (-1 past the end)
-      if (threadIdx.x < RT) {
-        const int64_t row = r0 + threadIdx.x;
-        int64_t e = -1;
-        if (row < total_rows) {
-          const int var = (int)(row / nS), ii = (int)(row % nS);
-          e = (int64_t)var * a.g.N + a.list[ii];
-        }
-        erow[threadIdx.x] = e;
-      }
-      __syncthreads();
-      // all loads of this thread in flight before the first shared store (memory-level parallelism)
-      constexpr int QB = 17;  // loads in flight per thread per batch
-      const int total = (nU + 1) * RT;
-      for (int base = threadIdx.x; base < total; base += QB * GT) {
-        double vbuf[QB];
-#pragma unroll
-        for (int q = 0; q < QB; ++q) {
-          const int idx = base + q * GT;
-          double v = 0.0;
-          if (idx < total) {
-            const int s = idx / RT, k = idx % RT;
-            const int64_t e = erow[k];
-            if (e >= 0)
-              v = (s < nU) ? __ldg(a.ring + (int64_t)a.W.slot[s] * TILE + sidx(SRef{nullptr, a.g.nsr}, e))
-                           : __ldg(a.src_b.p + sidx(a.src_b, e));
-          }
-          vbuf[q] = v;
-        }
-#pragma unroll
-        for (int q = 0; q < QB; ++q) {
-          const int idx = base + q * GT;
-          if (idx < total) {
-            const int s = idx / RT, k = idx % RT;
-            const int col = (s == nU) ? w : (s >= xoff ? s - xoff : w + 1);
-            tile[col * LDT + k] = vbuf[q];
-          }
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x < RT) {
-        const int k = threadIdx.x;
-        double sp = 0.0, sc = 0.0;
-        for (int i = 0; i < w; ++i) sc += tile[i * LDT + k];
-        if (xoff == 1) {
-          sp = tile[(w + 1) * LDT + k];
-          for (int i = 0; i < w - 1; ++i) sp += tile[i * LDT + k];
-        } else {
-          sp = sc;
-        }
-        psi[k] = sp / (double)w;
-        psi[RT + k] = sc / (double)w;
-      }
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < ncp * RT; idx += GT) {
-        const int col = idx / RT, k = idx % RT;
-        const bool valid = r0 + k < total_rows;
-        double v;
-        if (col < w) v = valid ? tile[col * LDT + k] - psi[k] : 0.0;
-        else if (col == w) v = valid ? tile[col * LDT + k] - psi[RT + k] : 0.0;
-        else v = 0.0;
-        tile[col * LDT + k] = v;
-      }
-    }
-    __syncthreads();
-    gram_tile<TPW>(tile, a.nsb, acc);
-    __syncthreads();
-  }
-  // write this CTA's partial (upper super-block pairs)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gid = lane >> 2, tig = lane & 3;
-  const int ntask = a.nsb * (a.nsb + 1) / 2;
-  double* out = a.part + (int64_t)blockIdx.x * ncp * ncp;
-#pragma unroll
-  for (int t = 0; t < TPW; ++t) {
-    const int task = warp + t * (GT / 32);
-    if (task < ntask) {
-      int sa = 0, rem = task;
-      while (rem >= a.nsb - sa) { rem -= a.nsb - sa; ++sa; }
-      const int sb = sa + rem;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int bi = 16 * sa + 8 * (q >> 1), bj = 16 * sb + 8 * (q & 1);
-        out[(bi + gid) * ncp + bj + 2 * tig] = acc[t][2 * q];
-        out[(bi + gid) * ncp + bj + 2 * tig + 1] = acc[t][2 * q + 1];
-      }
-    }
-  }
 }
 
 // ---------------- H4: gathered Gram of the S-hat rows ----------------
@@ -217,14 +42,22 @@ using GGSmall = GGCfg<5, 64, 1, 15, 3>;  // ncol <= 80 (w <= 78)
 using GGWide = GGCfg<9, 32, 3, 15, 3>;   // ncol <= 144 (w <= kMaxW)
 
 struct GGArgs {
+  int mode;                  // 0: contiguous rows of ncol columns (cols, slab stride ns), 1: S-hat rows
+  // mode 0
+  const double* const* cols;
+  int64_t ns;
+  int ncol0;
+  int64_t rows;
+  // mode 1
   Geo g;
   Win W;
   const double* ring;
-  SRef rho;
   const int32_t* list;
   const int32_t* count;
   SRef src_b;
-  double* part;  // [grid][ncp][ncp]
+  // both
+  SRef rho;                  // shift (rho.p nullable in mode 0)
+  double* part;              // [grid][ncp][ncp]
 };
 
 template <class CFG>
@@ -232,10 +65,14 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
   constexpr int RT = CFG::rt, NSB = CFG::nsb, NCP = CFG::ncp, LDT = CFG::ldt, ST = CFG::stages;
   extern __shared__ double smem[];
   __shared__ __align__(8) uint64_t full[ST], empty[ST];
-  const int nS = *a.count;
-  const int64_t total_rows = (int64_t)nS * a.g.c;
+  __shared__ const double* scol[NCP];  // column base pointers (mode 0: caller's; mode 1: ring slots)
+  const int nS = a.mode == 1 ? *a.count : 0;
+  const int64_t total_rows = a.mode == 1 ? (int64_t)nS * a.g.c : a.rows;
   const int64_t ntiles = (total_rows + RT - 1) / RT;
-  const int nU = a.W.nU, ncol = nU + 1;  // union slots + b
+  const int nU = a.mode == 1 ? a.W.nU : a.ncol0;
+  const int ncol = a.mode == 1 ? nU + 1 : a.ncol0;  // mode 1: union slots + b
+  for (int col = threadIdx.x; col < ncol; col += CFG::threads)
+    scol[col] = a.mode == 1 ? (col < nU ? a.ring + (int64_t)a.W.slot[col] * TILE : nullptr) : a.cols[col];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < ST * NCP * LDT; i += CFG::threads) smem[i] = 0.0;  // padding stays 0
   if (threadIdx.x == 0) {
@@ -250,7 +87,7 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
   if (warp < CFG::pw) {
     // ---- producers: thread k owns row k of every tile ----
     const int k = threadIdx.x;
-    const SRef slab{nullptr, a.g.nsr};
+    const SRef slab{nullptr, a.mode == 1 ? a.g.nsr : a.ns};
     double r_prev = 0.0;
     bool v_prev = false;
     for (int64_t it = 0; it <= my_tiles; ++it) {
@@ -262,13 +99,19 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
         double* tile = smem + (size_t)st * NCP * LDT;
         const int64_t row = (blockIdx.x + it * gridDim.x) * RT + k;
         if (row < total_rows) {
-          const int var = (int)(row / nS);
-          const int64_t e = (int64_t)var * a.g.N + __ldg(a.list + (row - (int64_t)var * nS));
-          const int64_t se = sidx(slab, e);
-          for (int col = 0; col < nU; ++col)
-            cp_async8(tile + col * LDT + k, a.ring + (int64_t)a.W.slot[col] * TILE + se);
-          cp_async8(tile + nU * LDT + k, a.src_b.p + sidx(a.src_b, e));
-          r_cur = __ldg(a.rho.p + sidx(a.rho, e));
+          int64_t e;
+          if (a.mode == 1) {
+            const int var = (int)(row / nS);
+            e = (int64_t)var * a.g.N + __ldg(a.list + (row - (int64_t)var * nS));
+            const int64_t se = sidx(slab, e);
+            for (int col = 0; col < nU; ++col) cp_async8(tile + col * LDT + k, scol[col] + se);
+            cp_async8(tile + nU * LDT + k, a.src_b.p + sidx(a.src_b, e));
+          } else {
+            e = row;
+            const int64_t se = sidx(slab, e);
+            for (int col = 0; col < ncol; ++col) cp_async8(tile + col * LDT + k, scol[col] + se);
+          }
+          r_cur = a.rho.p ? __ldg(a.rho.p + sidx(a.rho, e)) : 0.0;
           v_cur = true;
         } else {
           for (int col = 0; col < ncol; ++col) tile[col * LDT + k] = 0.0;
@@ -686,25 +529,32 @@ __global__ void lift_kernel(Geo g, Win W, const double* __restrict__ ring, const
   }
 }
 
-template <int TPW>
-hrom_status launch_gram(hrom_ctx* c, const GramArgs& a, int grid) {
-  const size_t smem = ((size_t)a.nsb * 16 * LDT + 2 * RT) * sizeof(double);
-  HROM_CK(cudaFuncSetAttribute(gram_kernel<TPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  gram_kernel<TPW><<<grid, GT, smem, c->st>>>(a);
+// launch the pipelined Gram (both modes) and reduce its per-CTA partials into C
+hrom_status run_gather_gram(hrom_ctx* c, GGArgs& a, int ncol, int grid, double* dev_C, int ldc,
+                                   const int32_t* map) {
+  a.part = c->b.part;
+  int ncp;
+  if (ncol <= GGSmall::ncp) {
+    ncp = GGSmall::ncp;
+    if ((int64_t)grid * ncp * ncp > c->b.part_len) return HROM_E_INVALID;
+    HROM_CK(cudaFuncSetAttribute(gather_gram_kernel<GGSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)GGSmall::smem));
+    gather_gram_kernel<GGSmall><<<grid, GGSmall::threads, GGSmall::smem, c->st>>>(a);
+  } else if (ncol <= GGWide::ncp) {
+    ncp = GGWide::ncp;
+    if ((int64_t)grid * ncp * ncp > c->b.part_len) return HROM_E_INVALID;
+    HROM_CK(cudaFuncSetAttribute(gather_gram_kernel<GGWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)GGWide::smem));
+    gather_gram_kernel<GGWide><<<grid, GGWide::threads, GGWide::smem, c->st>>>(a);
+  } else {
+    return HROM_E_INVALID;
+  }
+  HROM_LAUNCH_CK();
+  ++c->nlaunch;
+  gram_reduce<<<64, 256, 0, c->st>>>(c->b.part, grid, ncp, ncol, dev_C, ldc, map);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;
-}
-
-hrom_status dispatch_gram(hrom_ctx* c, GramArgs a, int grid) {
-  const int ntask = a.nsb * (a.nsb + 1) / 2;
-  const int tpw = (ntask + GT / 32 - 1) / (GT / 32);
-  if (tpw <= 1) return launch_gram<1>(c, a, grid);
-  if (tpw <= 2) return launch_gram<2>(c, a, grid);
-  if (tpw <= 4) return launch_gram<4>(c, a, grid);
-  if (tpw <= 6) return launch_gram<6>(c, a, grid);
-  if (tpw <= 9) return launch_gram<9>(c, a, grid);
-  return HROM_E_INVALID;
 }
 
 }  // namespace
@@ -712,24 +562,14 @@ hrom_status dispatch_gram(hrom_ctx* c, GramArgs a, int grid) {
 // Full Gram of ncol columns over `rows` rows, shifted by rho (nullable): dev_C[i*ldc+j].
 hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int64_t ns, int ncol, int64_t rows, SRef rho,
                       double* dev_C, int ldc, const int32_t* map) {
-  GramArgs a{};
+  GGArgs a{};
   a.mode = 0;
-  a.ncol = ncol;
-  a.nsb = (ncol + 15) / 16;
-  a.rows = rows;
   a.cols = dev_cols;
   a.ns = ns;
+  a.ncol0 = ncol;
+  a.rows = rows;
   a.rho = rho;
-  const int grid = c->nsm * 2;
-  const int ncp = a.nsb * 16;
-  if ((int64_t)grid * ncp * ncp > c->b.part_len) return HROM_E_INVALID;
-  a.part = c->b.part;
-  hrom_status s = dispatch_gram(c, a, grid);
-  if (s != HROM_OK) return s;
-  gram_reduce<<<64, 256, 0, c->st>>>(c->b.part, grid, ncp, ncol, dev_C, ldc, map);
-  HROM_LAUNCH_CK();
-  ++c->nlaunch;
-  return HROM_OK;
+  return run_gather_gram(c, a, ncol, c->basis_pending ? c->nsm - 1 : c->nsm, dev_C, ldc, map);
 }
 
 // gathered Gram of [X_S, b] over the rows of S-hat -> b.K ((w+1) x (w+1), centred)
@@ -742,33 +582,13 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   a.list = c->b.lists + (int64_t)L_S * c->g.N;
   a.count = c->b.counts + L_S;
   a.src_b = src_b;
+  a.mode = 1;
   // while the one-CTA eigen-solve of the previous update holds an SM (side stream), leave it
   // out: a static tile split with one block left over would double the time
   const int grid = c->basis_pending ? c->nsm - 1 : c->nsm;
-  a.part = c->b.part;
-  int ncp;
-  if (a.W.nU + 1 <= GGSmall::ncp) {
-    ncp = GGSmall::ncp;
-    if ((int64_t)grid * ncp * ncp > c->b.part_len) return HROM_E_INVALID;
-    HROM_CK(cudaFuncSetAttribute(gather_gram_kernel<GGSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)GGSmall::smem));
-    gather_gram_kernel<GGSmall><<<grid, GGSmall::threads, GGSmall::smem, c->st>>>(a);
-  } else if (a.W.nU + 1 <= GGWide::ncp) {
-    ncp = GGWide::ncp;
-    if ((int64_t)grid * ncp * ncp > c->b.part_len) return HROM_E_INVALID;
-    HROM_CK(cudaFuncSetAttribute(gather_gram_kernel<GGWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)GGWide::smem));
-    gather_gram_kernel<GGWide><<<grid, GGWide::threads, GGWide::smem, c->st>>>(a);
-  } else {
-    return HROM_E_INVALID;
-  }
-  HROM_LAUNCH_CK();
-  ++c->nlaunch;
   const int ncol = a.W.nU + 1;
-  double* R = c->b.eigV;  // (nU+1)^2 scratch
-  gram_reduce<<<64, 256, 0, c->st>>>(c->b.part, grid, ncp, ncol, R, ncol, nullptr);
-  HROM_LAUNCH_CK();
-  ++c->nlaunch;
+  hrom_status s = run_gather_gram(c, a, ncol, grid, c->b.eigV, ncol, nullptr);  // R: (nU+1)^2 scratch
+  if (s != HROM_OK) return s;
   return HROM_OK;  // the lagged centring of R is applied by solve_kernel
 }
 

@@ -60,6 +60,8 @@ _SIGS = {
     "hrom_effective_rank": (C.c_int32, [_VP]),
     "hrom_status_string": (C.c_char_p, [C.c_int]),
     "hrom_set_window": (C.c_int, [_VP, C.c_int64, _VP, C.c_int32, _VP]),
+    "hrom_put_snapshot": (C.c_int, [_VP, C.c_int64, _VP]),
+    "hrom_rebuild_basis": (C.c_int, [_VP, C.c_int64, _VP]),
     "hrom_get_basis": (C.c_int, [_VP, _VP, _VP]),
     "hrom_get_indicator": (C.c_int, [_VP, _VP]),
     "hrom_get_mask": (C.c_int, [_VP, _VP]),
@@ -227,6 +229,15 @@ class HybridROM:
     def set_window(self, k: int, snaps: torch.Tensor, mask_next: Optional[torch.Tensor] = None):
         assert snaps.dtype == torch.float64 and snaps.is_contiguous()
         _ck(self.lib.hrom_set_window(self.h, k, _ptr(snaps), snaps.shape[0], _ptr(mask_next)), "hrom_set_window")
+
+    def put_snapshot(self, k: int, q: torch.Tensor):
+        """Write gamma_k into its ring slot (window streaming, no basis work)."""
+        assert q.dtype == torch.float64 and q.is_contiguous()
+        _ck(self.lib.hrom_put_snapshot(self.h, k, _ptr(q)), "hrom_put_snapshot")
+
+    def rebuild_basis(self, k: int, mask_next: Optional[torch.Tensor] = None):
+        """Basis from the window gamma_{k-w}..gamma_k written with put_snapshot."""
+        _ck(self.lib.hrom_rebuild_basis(self.h, k, _ptr(mask_next)), "hrom_rebuild_basis")
 
     def basis(self):
         r = self.effective_rank()

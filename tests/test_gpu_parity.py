@@ -321,3 +321,34 @@ def test_rank_deficient_gappy_solve(orc, inputs, ncells, w, r):
     rom.sync()
     assert rom.debug_counters(10)[9] == 1  # eigen route taken
     assert rel(rom.get_state().cpu().numpy(), R.state()) <= 1e-12
+
+
+@pytest.mark.parametrize("seed", [1, 5])
+def test_positivity_escalation(orc, inputs, seed):
+    """O11: a hybrid state with rho <= 0 or p <= 0 is redone as a full step with the
+    same dt, on the device; the window Gram row is then recomputed from the final state, so the
+    next basis matches the oracle's (which refreshes from the escalated snapshot)."""
+    wl = small2d(inputs, nx=40, ny=30, w=8, r=2)
+    snaps = inputs.smooth_window(wl, wl.w + 1, seed=seed, amp=0.9)
+    rng = np.random.default_rng(seed)
+    S = (rng.random(wl.N) < 0.15).astype(np.uint8)
+    k = wl.w + 3
+    R = orc.Run(wl, snaps[0])
+    R.set_window(k, snaps, S)
+    dt = orc.dt(wl, snaps[-1])
+    assert R.step(dt) == 2  # the oracle escalated
+    rom = H.HybridROM(wl)
+    rom.set_window(k, dev(snaps.reshape(wl.w + 1, -1)), _mask_dev(wl, S))
+    before = rom.debug_counters(16)[15]
+    rom.hybrid_step(dt=dt)
+    rom.sync()  # the full step is admissible: nothing latched
+    assert rom.debug_counters(16)[15] == before + 1
+    full = orc.full_step(wl, snaps[-1], dt)
+    assert rel(rom.get_state().cpu().numpy(), full) <= 1e-13
+    assert rel(rom.get_state().cpu().numpy(), R.state()) <= 1e-13
+    # basis of the window ending at the escalated snapshot
+    rom.update_basis()
+    lam = rom.eigenvalues().cpu().numpy()
+    sig = R.sigma()
+    re = R.reff()
+    np.testing.assert_allclose(lam[:re], sig[:re] ** 2, rtol=1e-9, atol=1e-13 * sig[0] ** 2)
