@@ -329,6 +329,7 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef ou
   a.do_gram = (mode != MODE_PROJ) && out_in_ring && c->P.gram_mode == 0 ? 1 : 0;
   const size_t stage = (size_t)c->g.nsr * TILE * sizeof(double);
   a.nstage = FILL_STAGES;
+  while (a.nstage > 1 && a.nstage * stage > 216 * 1024) --a.nstage;  // wide windows (w = 128): one stage
   if (a.nstage * stage > 216 * 1024) return HROM_E_INVALID;
   const size_t smem = a.nstage * stage + 2 * a.nstage * sizeof(uint64_t);
   a.rho_slot = c->nslots;

@@ -509,23 +509,112 @@ __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ 
 }
 
 // Phi_{k+1}[:, j] = X A[:, j] (materialised; tests/config 5), psi_cur
-__global__ void lift_kernel(Geo g, Win W, const double* __restrict__ ring, const double* __restrict__ A,
-                            const int32_t* __restrict__ reffp, double* __restrict__ phi, double* __restrict__ psi) {
+// H12 lift on FP64 tensor cores: Phi[:, j] = (X - psi_prev 1^T) A[:, j] (D x r, column-major),
+// psi_cur = mean of the last w slots.  Warp-specialised like the gathered Gram: 2 producer
+// warps gather a 64-DOF tile of all nU window slots (cp.async), form X - psi_prev in place and
+// publish it; 16 consumer warps each own one 8-DOF block x four 8-mode blocks of the product
+// with A (staged in smem once per CTA) and write Phi straight from the accumulators.
+constexpr int LF_RT = 64, LF_LDT = LF_RT + 4, LF_PW = 2, LF_CW = 16, LF_T = 32 * (LF_PW + LF_CW);
+constexpr int LF_STAGES = 2, LF_NCOL = kMaxW + 5, LF_LDA = kMaxR + 4;
+
+__global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const double* __restrict__ ring,
+                                                       const double* __restrict__ A, const int32_t* __restrict__ reffp,
+                                                       double* __restrict__ phi, double* __restrict__ psi) {
+  extern __shared__ double smem[];
+  __shared__ __align__(8) uint64_t full[LF_STAGES], empty[LF_STAGES];
   const int re = *reffp;
-  const int w = W.w, nU = W.nU;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < g.D; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t se = sidx(SRef{nullptr, g.nsr}, e);
-    double sp = 0.0, sc = 0.0;
-    for (int s = 0; s < w; ++s) sp += ring[(int64_t)W.slot[s] * TILE + se];
-    for (int s = nU - w; s < nU; ++s) sc += ring[(int64_t)W.slot[s] * TILE + se];
-    const double pp = sp / (double)w;
-    if (psi) psi[e] = sc / (double)w;
-    if (phi)
-      for (int j = 0; j < re; ++j) {
-        double acc = 0.0;
-        for (int i = 0; i < w; ++i) acc += (ring[(int64_t)W.slot[nU - w + i] * TILE + se] - pp) * A[j * w + i];
-        phi[(int64_t)j * g.D + e] = acc;
+  const int w = W.w, nU = W.nU, xoff = nU - w;
+  const int kpad = (w + 3) & ~3;
+  double* As = smem;                                // kpad x LF_LDA: As[i][j] = A[j*w + i]
+  double* tiles = smem + (size_t)kpad * LF_LDA;     // LF_STAGES x LF_NCOL x LF_LDT
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kpad * LF_LDA; i += LF_T) {
+    const int si = i / LF_LDA, j = i % LF_LDA;
+    As[i] = (si < w && j < re) ? A[j * w + si] : 0.0;
+  }
+  for (int i = threadIdx.x; i < LF_STAGES * LF_NCOL * LF_LDT; i += LF_T) tiles[i] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < LF_STAGES; ++q) {
+      mbar_init(&full[q], LF_RT);
+      mbar_init(&empty[q], LF_CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ntiles = (g.D + LF_RT - 1) / LF_RT;
+  const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const double inv_w = 1.0 / (double)w;
+  if (warp < LF_PW) {
+    const int k = threadIdx.x;
+    const SRef slab{nullptr, g.nsr};
+    int64_t e_prev = -1;
+    for (int64_t it = 0; it <= my_tiles; ++it) {
+      int64_t e_cur = -1;
+      if (it < my_tiles) {
+        const int st = (int)(it % LF_STAGES);
+        if (it >= LF_STAGES) mbar_wait(&empty[st], (uint32_t)(((it / LF_STAGES) - 1) & 1));
+        double* tile = tiles + (size_t)st * LF_NCOL * LF_LDT;
+        const int64_t e = (blockIdx.x + it * gridDim.x) * LF_RT + k;
+        if (e < g.D) {
+          const int64_t se = sidx(slab, e);
+          for (int col = 0; col < nU; ++col) cp_async8(tile + col * LF_LDT + k, ring + (int64_t)W.slot[col] * TILE + se);
+          e_cur = e;
+        } else {
+          for (int col = 0; col < nU; ++col) tile[col * LF_LDT + k] = 0.0;
+        }
       }
+      cp_async_commit();
+      if (it >= 1) {
+        cp_async_wait<1>();
+        const int ps = (int)((it - 1) % LF_STAGES);
+        double* tile = tiles + (size_t)ps * LF_NCOL * LF_LDT;
+        if (e_prev >= 0) {
+          double sp = 0.0, sc = 0.0;
+          for (int s = 0; s < w; ++s) sp += tile[s * LF_LDT + k];
+          for (int s = xoff; s < nU; ++s) sc += tile[s * LF_LDT + k];
+          if (psi) psi[e_prev] = sc * inv_w;
+          const double pp = sp * inv_w;
+          for (int s = xoff; s < nU; ++s) tile[s * LF_LDT + k] -= pp;
+        }
+        mbar_arrive(&full[ps]);
+      }
+      e_prev = e_cur;
+    }
+    cp_async_wait<0>();
+  } else {
+    const int cw = warp - LF_PW;
+    const int db = cw & 7, mb0 = (cw >> 3) * 4;
+    const int gid = lane >> 2, tig = lane & 3;
+    for (int64_t it = 0; it < my_tiles; ++it) {
+      const int st = (int)(it % LF_STAGES);
+      mbar_wait(&full[st], (uint32_t)((it / LF_STAGES) & 1));
+      const double* tile = tiles + (size_t)st * LF_NCOL * LF_LDT;
+      double acc[4][2];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
+      if (phi && 8 * mb0 < re) {
+        for (int kk = 0; kk < kpad; kk += 4) {
+          const double av = tile[(xoff + kk + tig) * LF_LDT + 8 * db + gid];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double bv = As[(kk + tig) * LF_LDA + 8 * (mb0 + q) + gid];
+            dmma(acc[q][0], acc[q][1], av, bv);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (phi) {
+        const int64_t e0 = (blockIdx.x + it * gridDim.x) * LF_RT + 8 * db + gid;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = 8 * (mb0 + q) + 2 * tig + h;
+            if (j < re && e0 < g.D) phi[(int64_t)j * g.D + e0] = acc[q][h];
+          }
+      }
+    }
   }
 }
 
@@ -617,7 +706,11 @@ hrom_status basis_from_gram(hrom_ctx* c, const Win& W) {
 }
 
 hrom_status lift(hrom_ctx* c, const Win& W, double* phi, double* psi) {
-  lift_kernel<<<c->nsm * 4, 256, 0, c->st>>>(c->g, W, c->b.ring, c->b.A, c->b.ireg, phi, psi);
+  if (W.w > kMaxW || c->r > kMaxR) return HROM_E_INVALID;
+  const int kpad = (W.w + 3) & ~3;
+  const size_t smem = ((size_t)kpad * LF_LDA + (size_t)LF_STAGES * LF_NCOL * LF_LDT) * sizeof(double);
+  HROM_CK(cudaFuncSetAttribute(lift_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  lift_kernel<<<c->nsm, LF_T, smem, c->st>>>(c->g, W, c->b.ring, c->b.A, c->b.ireg, phi, psi);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;
