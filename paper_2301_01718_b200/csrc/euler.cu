@@ -180,10 +180,16 @@ __global__ void __launch_bounds__(256) smax_kernel(Geo g, const SRef q, unsigned
 }
 
 __global__ void dt_finalize(const unsigned long long* smax, const unsigned long long* smax_alt,
-                            const unsigned long long* esc, double cfl, double dt_override, double* dt) {
+                            const unsigned long long* esc, double cfl, double dt_override, double* dt,
+                            unsigned long long* ureg) {
   // smax_alt: the escalated state's maximum when the previous step was redone as a full step
   const unsigned long long* src = (esc && *esc != ~0ull) ? smax_alt : smax;
   const double s = __longlong_as_double((long long)*src);
+  // reset the registers of this step's positivity pass (maximum ureg[2], step flag ureg[3],
+  // escalated maximum ureg[0]) -- no separate memsets on the critical path
+  ureg[0] = 0ull;
+  ureg[2] = 0ull;
+  ureg[3] = ~0ull;
   *dt = dt_override > 0.0 ? dt_override : cfl / s;
 }
 
@@ -246,7 +252,7 @@ hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override, int64_t kq) {
       ++nl;
     }
   }
-  dt_finalize<<<1, 1, 0, c->st>>>(smax, alt, esc, c->g.cfl, dt_override, c->b.dreg);
+  dt_finalize<<<1, 1, 0, c->st>>>(smax, alt, esc, c->g.cfl, dt_override, c->b.dreg, c->b.ureg);
   HROM_LAUNCH_CK();
   c->nlaunch += nl;
   return HROM_OK;
@@ -254,7 +260,8 @@ hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override, int64_t kq) {
 
 hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, const int32_t* list, int list_idx,
                          double /*dt_override*/, const unsigned long long* run_if) {
-  const int grid = c->nsm * 8;
+  // conditional (escalation) launches almost always exit at once: a small grid-stride grid
+  const int grid = run_if ? c->nsm * 2 : c->nsm * 8;
   const int32_t* cnt = list ? c->b.counts + list_idx : nullptr;
   const Geo& g = c->g;
   int32_t* ec = c->b.ireg + 15;
@@ -276,9 +283,7 @@ hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, co
 hrom_status launch_positivity(hrom_ctx* c, SRef qprev, SRef q, int64_t kq) {
   const int grid = c->nsm * 8;
   unsigned long long* u = c->b.ureg;
-  HROM_CK(cudaMemsetAsync(u + 2, 0, sizeof(unsigned long long), c->st));
-  HROM_CK(cudaMemsetAsync(u + 3, 0xff, sizeof(unsigned long long), c->st));
-  HROM_CK(cudaMemsetAsync(u, 0, sizeof(unsigned long long), c->st));
+  // ureg[0] = 0, ureg[2] = 0, ureg[3] = ~0 were set by this step's dt_finalize
   if (c->g.dim == 1) positivity_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, u + 3, u + 2, nullptr);
   else positivity_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, u + 3, u + 2, nullptr);
   HROM_LAUNCH_CK();
@@ -288,8 +293,8 @@ hrom_status launch_positivity(hrom_ctx* c, SRef qprev, SRef q, int64_t kq) {
   if ((s = launch_stage(c, 1, qprev, qprev, U1, nullptr, 0, 0.0, u + 3)) != HROM_OK) return s;
   if ((s = launch_stage(c, 2, qprev, U1, U2, nullptr, 0, 0.0, u + 3)) != HROM_OK) return s;
   if ((s = launch_stage(c, 3, qprev, U2, q, nullptr, 0, 0.0, u + 3)) != HROM_OK) return s;
-  if (c->g.dim == 1) positivity_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, u + 1, u, u + 3);
-  else positivity_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, u + 1, u, u + 3);
+  if (c->g.dim == 1) positivity_kernel<1><<<c->nsm * 2, 256, 0, c->st>>>(c->g, q, u + 1, u, u + 3);
+  else positivity_kernel<2><<<c->nsm * 2, 256, 0, c->st>>>(c->g, q, u + 1, u, u + 3);
   HROM_LAUNCH_CK();
   c->nlaunch += 1;
   c->smax_k = kq;

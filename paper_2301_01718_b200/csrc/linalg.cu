@@ -31,15 +31,18 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // (DMMA m8n8k4) and release the stage through empty[s].  No CTA-wide barrier in the stream.
 // NSB 16-column super blocks (ncol <= 16 NSB), RT rows per tile (= producer threads),
 // TPW super-block pairs per consumer warp, CW consumer warps.
-template <int NSB, int RT, int TPW, int CW, int STAGES>
+template <int NSB, int RT, int TPW, int CW, int STAGES, int PW, int LOOK>
 struct GGCfg {
-  static constexpr int nsb = NSB, rt = RT, tpw = TPW, cw = CW, stages = STAGES;
-  static constexpr int pw = RT / 32, ncp = 16 * NSB, ldt = RT + 4, threads = 32 * (RT / 32 + CW);
+  static constexpr int nsb = NSB, rt = RT, tpw = TPW, cw = CW, stages = STAGES, look = LOOK;
+  static constexpr int pw = PW, ncp = 16 * NSB, ldt = RT + 4, threads = 32 * (PW + CW);
+  static constexpr int parts = 32 * PW / RT;  // producer threads per tile row (columns split)
   static constexpr size_t smem = (size_t)STAGES * ncp * ldt * sizeof(double);
   static_assert(CW * TPW >= NSB * (NSB + 1) / 2, "tasks");
+  static_assert((32 * PW) % RT == 0 && STAGES >= LOOK + 2, "producer layout");
 };
-using GGSmall = GGCfg<5, 64, 1, 15, 3>;  // ncol <= 80 (w <= 78)
-using GGWide = GGCfg<9, 32, 3, 15, 3>;   // ncol <= 144 (w <= kMaxW)
+// producers run LOOK tiles ahead of the tile they publish (DRAM latency of the 8-byte gathers)
+using GGSmall = GGCfg<5, 64, 1, 15, 4, 4, 2>;  // ncol <= 80 (w <= 78)
+using GGWide = GGCfg<9, 32, 3, 15, 4, 2, 2>;   // ncol <= 144 (w <= kMaxW)
 
 struct GGArgs {
   int mode;                  // 0: contiguous rows of ncol columns (cols, slab stride ns), 1: S-hat rows
@@ -77,7 +80,7 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
   for (int i = threadIdx.x; i < ST * NCP * LDT; i += CFG::threads) smem[i] = 0.0;  // padding stays 0
   if (threadIdx.x == 0) {
     for (int q = 0; q < ST; ++q) {
-      mbar_init(&full[q], RT);
+      mbar_init(&full[q], 32 * CFG::pw);
       mbar_init(&empty[q], CFG::cw);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -85,12 +88,18 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
   __syncthreads();
   const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (warp < CFG::pw) {
-    // ---- producers: thread k owns row k of every tile ----
-    const int k = threadIdx.x;
+    // ---- producers: thread (k, part) owns row k, columns part, part + parts, ... of every tile ----
+    constexpr int PARTS = CFG::parts, LOOK = CFG::look;
+    const int k = threadIdx.x % RT, part = threadIdx.x / RT;
     const SRef slab{nullptr, a.mode == 1 ? a.g.nsr : a.ns};
-    double r_prev = 0.0;
-    bool v_prev = false;
-    for (int64_t it = 0; it <= my_tiles; ++it) {
+    double rq[LOOK + 1];
+    bool vq[LOOK + 1];
+#pragma unroll
+    for (int q = 0; q <= LOOK; ++q) {
+      rq[q] = 0.0;
+      vq[q] = false;
+    }
+    for (int64_t it = 0; it < my_tiles + LOOK; ++it) {
       double r_cur = 0.0;
       bool v_cur = false;
       if (it < my_tiles) {
@@ -104,30 +113,36 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
             const int var = (int)(row / nS);
             e = (int64_t)var * a.g.N + __ldg(a.list + (row - (int64_t)var * nS));
             const int64_t se = sidx(slab, e);
-            for (int col = 0; col < nU; ++col) cp_async8(tile + col * LDT + k, scol[col] + se);
-            cp_async8(tile + nU * LDT + k, a.src_b.p + sidx(a.src_b, e));
+            for (int col = part; col < nU; col += PARTS) cp_async8(tile + col * LDT + k, scol[col] + se);
+            if (nU % PARTS == part) cp_async8(tile + nU * LDT + k, a.src_b.p + sidx(a.src_b, e));
           } else {
             e = row;
             const int64_t se = sidx(slab, e);
-            for (int col = 0; col < ncol; ++col) cp_async8(tile + col * LDT + k, scol[col] + se);
+            for (int col = part; col < ncol; col += PARTS) cp_async8(tile + col * LDT + k, scol[col] + se);
           }
           r_cur = a.rho.p ? __ldg(a.rho.p + sidx(a.rho, e)) : 0.0;
           v_cur = true;
         } else {
-          for (int col = 0; col < ncol; ++col) tile[col * LDT + k] = 0.0;
+          for (int col = part; col < ncol; col += PARTS) tile[col * LDT + k] = 0.0;
         }
       }
       cp_async_commit();
-      if (it >= 1) {  // tile it-1 has landed: shift by rho, publish
-        cp_async_wait<1>();
-        const int ps = (int)((it - 1) % ST);
+      // register ring of the shifts of the tiles in flight (static indices after unrolling)
+#pragma unroll
+      for (int q = 0; q < LOOK; ++q) {
+        rq[q] = rq[q + 1];
+        vq[q] = vq[q + 1];
+      }
+      rq[LOOK] = r_cur;
+      vq[LOOK] = v_cur;
+      if (it >= LOOK) {  // tile it-LOOK has landed: shift by rho, publish
+        cp_async_wait<LOOK>();
+        const int ps = (int)((it - LOOK) % ST);
         double* tile = smem + (size_t)ps * NCP * LDT;
-        if (v_prev)
-          for (int col = 0; col < ncol; ++col) tile[col * LDT + k] -= r_prev;
+        if (vq[0])
+          for (int col = part; col < ncol; col += PARTS) tile[col * LDT + k] -= rq[0];
         mbar_arrive(&full[ps]);
       }
-      r_prev = r_cur;
-      v_prev = v_cur;
     }
     cp_async_wait<0>();
   } else {
