@@ -42,9 +42,11 @@ struct FilterArgs {
   int32_t* fcnt;         // [grid]
   int32_t* sweeps_out;   // [3]
   long long* tdbg;       // 64 timestamps (debug)
+  int smem_bytes;        // dynamic shared memory of the launch (tables staged when they fit)
 };
 
 constexpr int FT = 512;  // filter threads per block (one block per SM)
+constexpr int FILTER_SMEM = 200 * 1024;
 
 __device__ __forceinline__ void stamp(long long* t, int i) {
   if (t && i < 64 && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -99,6 +101,24 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
   }
   grid.sync();
   stamp(a.tdbg, 1);
+  // each CTA owns a contiguous chunk of the band: its stencil tables and F values are staged in
+  // shared memory once (the sweeps then pay one L2 round trip per phase, for the values only)
+  extern __shared__ double fsm[];
+  const int64_t chunk = ((int64_t)nb + gridDim.x - 1) / gridDim.x;
+  const int64_t c0 = min((int64_t)blockIdx.x * chunk, (int64_t)nb), c1 = min(c0 + chunk, (int64_t)nb);
+  const bool tsm = chunk * (14 * sizeof(int32_t) + g.c * sizeof(double)) <= (size_t)a.smem_bytes;
+  double* sFb = fsm;                                      // [var][chunk]
+  int32_t* stab = reinterpret_cast<int32_t*>(fsm + (tsm ? g.c * chunk : 0));  // [14][chunk]
+  if (tsm) {
+    for (int64_t t = c0 + threadIdx.x; t < c1; t += blockDim.x) {
+      const int64_t lt = t - c0;
+#pragma unroll
+      for (int m = 0; m < 14; ++m)
+        if (g.dim == 2 || m < 7) stab[m * chunk + lt] = __ldcg(a.tab + (int64_t)m * N + t);
+      for (int var = 0; var < g.c; ++var) sFb[var * chunk + lt] = __ldcg(a.Fb + var * N + t);
+    }
+    __syncthreads();
+  }
   // Sweeps, two grid barriers each.  The y-pass owns its cell: a kept value is written straight
   // into cur (no other thread of that phase reads cur at a band cell -- the y-stencil reads Vp),
   // so the next x-pass sees the applied keep-set without a separate apply phase.
@@ -121,10 +141,12 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
     for (int sw = 0; sw < a.maxsw; ++sw, ++gs) {
       ++sweeps;
       // P1: v' = S^x(cur) on B
-      for (int64_t t = gtid; t < nb; t += gstride) {
+      for (int64_t t = c0 + threadIdx.x; t < c1; t += blockDim.x) {
+        const int64_t lt = t - c0;
         int nbr[7];
 #pragma unroll
-        for (int m = 0; m < 7; ++m) nbr[m] = m <= 2 * rad ? __ldcg(tab + (int64_t)(m - rad + 3) * N + t) : 0;
+        for (int m = 0; m < 7; ++m)
+          nbr[m] = m <= 2 * rad ? (tsm ? stab[(m - rad + 3) * chunk + lt] : __ldcg(tab + (int64_t)(m - rad + 3) * N + t)) : 0;
         double x[4][7];
 #pragma unroll
         for (int var = 0; var < 4; ++var)
@@ -144,16 +166,19 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
       // P2: v'' = S^y(v') on B, residual gate, kept values applied in place
       double mdec = 0.0;
       int cnt = 0;
-      for (int64_t t = gtid; t < nb; t += gstride) {
+      for (int64_t t = c0 + threadIdx.x; t < c1; t += blockDim.x) {
+        const int64_t lt = t - c0;
         int nbr[7];
 #pragma unroll
         for (int m = 0; m < 7; ++m)
-          nbr[m] = (g.dim == 2 && m <= 2 * rad) ? __ldcg(tab + (int64_t)(7 + m - rad + 3) * N + t) : 0;
+          nbr[m] = (g.dim == 2 && m <= 2 * rad)
+                       ? (tsm ? stab[(7 + m - rad + 3) * chunk + lt] : __ldcg(tab + (int64_t)(7 + m - rad + 3) * N + t))
+                       : 0;
         double own[4], fe[4], y[4][7];
 #pragma unroll
         for (int var = 0; var < 4; ++var) {
           own[var] = var < g.c ? __ldcg(cur + var * N + t) : 0.0;
-          fe[var] = var < g.c ? __ldcg(Fb + var * N + t) : 0.0;
+          fe[var] = var < g.c ? (tsm ? sFb[var * chunk + lt] : __ldcg(Fb + var * N + t)) : 0.0;
 #pragma unroll
           for (int m = 0; m < 7; ++m) y[var][m] = (g.dim == 2 && var < g.c && m <= 2 * rad) ? __ldcg(Vp + var * N + nbr[m]) : 0.0;
         }
@@ -346,8 +371,11 @@ hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F, uint8_t* kept_cells) {
   a.sweeps_out = c->b.ireg + 4;
   a.tdbg = c->b.dbg;
   if (kept_cells) HROM_CK(cudaMemsetAsync(kept_cells, 0, c->g.N, c->st));
+  a.smem_bytes = FILTER_SMEM;
+  HROM_CK(cudaFuncSetAttribute(filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FILTER_SMEM));
   void* args[] = {&a};
-  HROM_CK(cudaLaunchCooperativeKernel((void*)filter_kernel, dim3(c->filter_blocks), dim3(FT), args, 0, c->st));
+  HROM_CK(cudaLaunchCooperativeKernel((void*)filter_kernel, dim3(c->filter_blocks), dim3(FT), args, FILTER_SMEM,
+                                      c->st));
   ++c->nlaunch;
   return HROM_OK;
 }
@@ -364,7 +392,8 @@ hrom_status launch_band_gram(hrom_ctx* c, const Win& W, SRef v) {
 
 int filter_occupancy() {
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, filter_kernel, FT, 0);
+  cudaFuncSetAttribute(filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FILTER_SMEM);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, filter_kernel, FT, FILTER_SMEM);
   return nb;
 }
 
