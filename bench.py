@@ -295,21 +295,24 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
+        # each timed step: one oracle hybrid step on a 128^2 tile (~1 s), so that the default
+        # K = 64 run ends within a few minutes
+        side = 128
         samples = []
         for _ in range(args.warmup):
-            cpu_sample(1)
+            cpu_sample(1, side)
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            samples.append(cpu_sample(1)["seconds_per_step"])
+            samples.append(cpu_sample(1, side)["seconds_per_step"])
         ms = 1000.0 * sum(samples) / len(samples)
-        side = 256
         value = side * side / (ms / 1000.0)
         base = {"value": value, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
                 "sample": f"one oracle hybrid step on a {side}x{side} periodic tile with config-4 parameters per step"}
         print(json.dumps({"impl": "reference", "metric": METRIC, "value": value, "unit": "cell-updates/s",
                           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                          "data": "synthetic", "config": {"workload": "config4-blasts-2048 (oracle sample)"},
+                          "data": "synthetic", "config": {"workload": "config4-blasts-2048",
+                                                                     "sample": f"one oracle hybrid step on a {side}x{side} tile per step"},
                           "cpu_baseline": base,
                           "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
                                   "d2h_bytes_per_step": 0},
@@ -318,7 +321,7 @@ def main():
     out = run_hrom(args, rank, world, local_rank)
     if rank == 0 and out is not None:
         if world == 1 and not args.no_cpu:
-            out["cpu_baseline"] = cpu_sample(1)
+            out["cpu_baseline"] = cpu_sample(3)  # ~13 s of single-thread oracle work
         print(json.dumps(out))
 
 
