@@ -352,3 +352,46 @@ def test_positivity_escalation(orc, inputs, seed):
     sig = R.sigma()
     re = R.reff()
     np.testing.assert_allclose(lam[:re], sig[:re] ** 2, rtol=1e-9, atol=1e-13 * sig[0] ** 2)
+
+
+def test_empty_sample_set_fills_with_psi(orc, inputs):
+    """S-hat = {} (all eps = 0, A18): no gappy rows, y = G^+ g = 0 and the whole state is
+    psi_{k+1} + Phi*0; the oracle's min-norm LSQ of an empty system gives the same."""
+    wl = small2d(inputs, bc=1, nx=48, ny=32)
+    snaps, _ = _replay_case(orc, inputs, wl, seed=13)
+    S = np.zeros(wl.N, np.uint8)
+    k = wl.w + 2
+    R = orc.Run(wl, snaps[0])
+    R.set_window(k, snaps, S)
+    dt = orc.dt(wl, snaps[-1])
+    R.step(dt)
+    rom = H.HybridROM(wl)
+    rom.set_window(k, dev(snaps.reshape(wl.w + 1, -1)), _mask_dev(wl, S))
+    rom.hybrid_step(dt=dt)
+    rom.sync()
+    g = rom.get_state().cpu().numpy()
+    psi_next = snaps[1:].mean(axis=0)
+    assert rel(g, R.state()) <= 1e-13
+    assert rel(g, psi_next) <= 1e-13
+
+
+def test_abi_argument_and_state_errors(inputs):
+    """hrom.h error behaviour: invalid parameters are rejected at create, calls out of order
+    return HROM_E_STATE, and a hybrid step before any basis is refused."""
+    import dataclasses
+    wl = small2d(inputs)
+    with pytest.raises(H.HromError) as e:
+        H.HybridROM(dataclasses.replace(wl, r=wl.w + 1))  # r > w
+    assert e.value.code == 1
+    with pytest.raises(H.HromError):
+        H.HybridROM(dataclasses.replace(wl, f=0.0))  # fraction outside (0, 1]
+    rom = H.HybridROM(wl)
+    with pytest.raises(H.HromError) as e:
+        rom.full_step()  # no state yet
+    assert e.value.code == 2
+    rom.set_state(dev(inputs.initial_condition(wl)))
+    with pytest.raises(H.HromError) as e:
+        rom.hybrid_step()  # no basis yet
+    assert e.value.code == 2
+    rom.full_step()
+    rom.sync()
