@@ -41,7 +41,7 @@ struct GGCfg {
   static_assert((32 * PW) % RT == 0 && STAGES >= LOOK + 2, "producer layout");
 };
 // producers run LOOK tiles ahead of the tile they publish (DRAM latency of the 8-byte gathers)
-using GGSmall = GGCfg<5, 64, 1, 15, 4, 4, 2>;  // ncol <= 80 (w <= 78)
+using GGSmall = GGCfg<5, 64, 1, 15, 4, 6, 2>;  // ncol <= 80 (w <= 78)
 using GGWide = GGCfg<9, 32, 3, 15, 4, 2, 2>;   // ncol <= 144 (w <= kMaxW)
 
 struct GGArgs {
