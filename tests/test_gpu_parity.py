@@ -395,3 +395,24 @@ def test_abi_argument_and_state_errors(inputs):
     assert e.value.code == 2
     rom.full_step()
     rom.sync()
+
+
+def test_trajectory_config2_short(orc, inputs):
+    """Config 2 (BJ:8, 256^2 four-quadrant problem, MUSCL, transmissive): the Algorithm-1
+    trajectory through the bootstrap and 8 hybrid steps agrees with the oracle step by step
+    (the explicit map's rounding amplification is still small this early, G6)."""
+    wl = inputs.config(2, steps=inputs.config(2).w + 8)
+    q0 = inputs.initial_condition(wl)
+    rom = H.HybridROM(wl)
+    rom.set_state(dev(q0))
+    R = orc.Run(wl, q0)
+    worst = 0.0
+    for k in range(1, wl.steps + 1):
+        rom.step()
+        R.step()
+        e = rel(rom.get_state().cpu().numpy(), R.state())
+        worst = max(worst, e)
+        if k >= wl.w - 1:
+            assert np.array_equal(H.cells_from_mask(wl, rom.mask()), R.mask()), k
+    rom.sync()
+    assert worst <= 1e-11, worst
