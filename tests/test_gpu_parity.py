@@ -6,6 +6,7 @@ fed the oracle's indicator, basis subspaces principal-angle sine <= 1e-10 on the
 well-separated leading modes (reading A15).
 """
 import dataclasses
+import math
 
 import numpy as np
 import pytest
@@ -416,3 +417,51 @@ def test_trajectory_config2_short(orc, inputs):
             assert np.array_equal(H.cells_from_mask(wl, rom.mask()), R.mask()), k
     rom.sync()
     assert worst <= 1e-11, worst
+
+
+def test_fullsize_config4_properties(orc, inputs):
+    """Config 4 at full size (2048^2, BJ:10) in bench.py's launch configuration, checked where
+    the oracle can follow: (i) S-hat rows of the hybrid step equal the oracle's full step there
+    (exact restriction, Eq. 7); (ii) every cell outside S-hat (+) Q_W holds psi + Phi y
+    with the GPU's own Phi, psi (lifted) and y; (iii) the next S-hat is bit-exactly the top
+    ceil(fN) of the GPU's indicator, ties by ascending index (A18)."""
+    wl = inputs.config(4)
+    rom = H.HybridROM(wl)
+    rom.set_state(dev(inputs.initial_condition(wl)))
+    for _ in range(wl.w + 1):
+        rom.step()
+    g0 = rom.get_state().cpu().numpy()
+    phi, psi = rom.basis()
+    S = H.cells_from_mask(wl, rom.mask()).astype(bool)
+    dtt = torch.zeros(1, dtype=torch.float64, device="cuda")
+    rom.hybrid_step(dt_out=dtt)
+    rom.sync()
+    dt = float(dtt.item())
+    g1 = rom.get_state()
+    # (i) S-hat rows vs the oracle's full step (whole grid, ~8 s single-thread)
+    full = orc.full_step(wl, g0, dt)
+    g1n = g1.cpu().numpy()
+    assert rel(g1n[:, S], full[:, S]) <= 1e-13
+    # (ii) fill outside the seam band
+    S2 = S.reshape(wl.ny, wl.nx)
+    T2 = S2.copy()
+    for dy in range(-wl.W, wl.W + 1):  # square dilation Q_W, periodic (A21)
+        for dx in range(-wl.W, wl.W + 1):
+            T2 |= np.roll(np.roll(S2, dy, 0), dx, 1)
+    T = T2.reshape(-1)
+    y = rom.y()[: phi.shape[0]]
+    rec = (psi.reshape(-1) + phi.T @ y).reshape(wl.c, wl.N)
+    off = torch.from_numpy(~T).cuda()
+    num = torch.linalg.norm((g1 - rec)[:, off]).item()
+    den = torch.linalg.norm(g1[:, off]).item()
+    assert num / den <= 1e-12, num / den
+    # (iii) next sample set
+    eps = rom.indicator().cpu().numpy()
+    rom.update_basis()
+    rom.sample()
+    nz = np.nonzero(eps > 0)[0]
+    n_g = min(int(math.ceil(wl.f * wl.N)), nz.size)
+    order = np.lexsort((nz, -eps[nz]))  # descending eps, ties by ascending cell
+    want = np.zeros(wl.N, np.uint8)
+    want[nz[order[:n_g]]] = 1
+    assert np.array_equal(H.cells_from_mask(wl, rom.mask()), want)
