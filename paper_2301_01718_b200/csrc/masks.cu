@@ -212,17 +212,21 @@ __device__ __forceinline__ void blk_write(const uint32_t* M, int64_t b0, int64_t
     // 32 words per coalesced load, broadcast one by one (no load in the dependent chain)
     const uint32_t mine = wb + lane < w1 ? __ldcg(M + wb + lane) : 0u;
     const int nwk = (int)min((int64_t)32, w1 - wb);
+    int jrow = flat ? 0 : (int)wb / g.wpr, wcol = flat ? (int)wb : (int)wb - jrow * g.wpr;  // no 64-bit division
     for (int k = 0; k < nwk; ++k) {
       const uint32_t bits = __shfl_sync(0xffffffffu, mine, k);
-      const int64_t w = wb + k;
       if ((bits >> lane) & 1u) {
         const int p = pos + __popc(bits & ((1u << lane) - 1u));
-        const int64_t cell = (flat ? 32 * w : (w / g.wpr) * (int64_t)g.nx + 32 * (w % g.wpr)) + lane;
-        list[p] = (int32_t)cell;
+        const int cell = (flat ? 32 * wcol : jrow * g.nx + 32 * wcol) + lane;
+        list[p] = cell;
         if (vals) vals[p] = src[cell];
         if (idx) idx[cell] = idx_base + p;
       }
       pos += __popc(bits);
+      if (++wcol == g.wpr && !flat) {
+        wcol = 0;
+        ++jrow;
+      }
     }
   }
 }
@@ -380,7 +384,7 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
         }
         if (sel) {
           const int64_t cell = a.sel_cell[t];
-          const int i = (int)(cell % g.nx), j = (int)(cell / g.nx);
+          const int ci = (int)cell, j = ci / g.nx, i = ci - j * g.nx;
           atomicOr(&S[(int64_t)j * g.wpr + (i >> 5)], 1u << (i & 31));
         }
       }
@@ -396,7 +400,8 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
   {
     const BlockRange r = thread_range(nw);
     for (int64_t w = r.w0; w < r.w1; ++w) {
-      TMP[w] = xdil_word(S, g, (int)(w / g.wpr), (int)(w % g.wpr), a.band);
+      const int wq = (int)w, jq = wq / g.wpr;
+      TMP[w] = xdil_word(S, g, jq, wq - jq * g.wpr, a.band);
       HM[w] = 0u;
     }
   }
@@ -405,7 +410,7 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
   {
     const BlockRange r = thread_range(nw);
     for (int64_t w = r.w0; w < r.w1; ++w) {
-      const int j = (int)(w / g.wpr), wi = (int)(w % g.wpr);
+      const int j = (int)w / g.wpr, wi = (int)w - j * g.wpr;
       const uint32_t sq = (g.dim == 2) ? ydil_word(TMP, g, j, wi, a.band) : __ldcg(TMP + w);
       const uint32_t sv = __ldcg(S + w);
       B[w] = sq & ~sv;
@@ -419,7 +424,7 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
     uint32_t* cout_ = q == 0 ? A2 : A1;
     const BlockRange r = thread_range(nw);
     for (int64_t w = r.w0; w < r.w1; ++w) {
-      const int j = (int)(w / g.wpr), wi = (int)(w % g.wpr);
+      const int j = (int)w / g.wpr, wi = (int)w - j * g.wpr;
       uint32_t o = xdil_word(cin, g, j, wi, a.halo);
       if (g.dim == 2) o |= ydil_word(cin, g, j, wi, a.halo);
       cout_[w] = o;
@@ -427,23 +432,86 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
     grid.sync();
   sstamp(a.tdbg, ts);
   }
-  // ordered compaction of S, B, T, A2, A1 (mask index == list index)
+  // ordered compaction of S, B, T, A2, A1 (mask index == list index), all five at once: each
+  // warp loads its words of the five masks once (kept in registers when the warp's range is
+  // <= 32 words), per-warp counts stay in shared memory across the grid barrier
   const int64_t rchunk = (nw + G - 1) / G;
   const int64_t rb0 = min((int64_t)blockIdx.x * rchunk, nw), rb1 = min(rb0 + rchunk, nw);
-  for (int m = 0; m < 5; ++m) {
-    const int t = blk_count(a.masks + (int64_t)m * mw, rb0, rb1, wcnt);
-    if (tid == 0) a.blk[(2 + m) * G + blockIdx.x] = t;
-  }
-  grid.sync();
-  sstamp(a.tdbg, ts);
-  for (int m = 0; m < 5; ++m) {
-    const uint32_t* M = a.masks + (int64_t)m * mw;
-    int off, tot;
-    block_offset(a.blk, 2 + m, &off, &tot, sbuf);
-    blk_count(M, rb0, rb1, wcnt);
-    blk_write(M, rb0, rb1, off, wcnt, g, false, a.lists + (int64_t)m * N, nullptr, nullptr,
-              m == L_B ? a.idx : nullptr, 0);
-    if (blockIdx.x == 0 && tid == 0) a.counts[m] = tot;
+  __shared__ int wc5[5][32];
+  __shared__ int soff5[5], stot5[5];
+  {
+    int64_t ww0, ww1;
+    warp_range(rb0, rb1, &ww0, &ww1);
+    const int lane = tid & 31, warp = tid >> 5;
+    const bool fast = ww1 - ww0 <= 32;  // uniform: every warp gets the same range length
+    uint32_t wd[5];
+    int c5[5];
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+      wd[m] = (fast && ww0 + lane < ww1) ? __ldcg(a.masks + (int64_t)m * mw + ww0 + lane) : 0u;
+      c5[m] = __popc(wd[m]);
+    }
+    if (!fast)
+#pragma unroll
+      for (int m = 0; m < 5; ++m)
+        for (int64_t w = ww0 + lane; w < ww1; w += 32) c5[m] += __popc(__ldcg(a.masks + (int64_t)m * mw + w));
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+      for (int o = 16; o > 0; o >>= 1) c5[m] += __shfl_xor_sync(0xffffffffu, c5[m], o);
+      if (lane == 0) wc5[m][warp] = c5[m];
+    }
+    __syncthreads();
+    if (tid < 5) {
+      int t = 0;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += wc5[tid][k];
+      a.blk[(2 + tid) * G + blockIdx.x] = t;
+    }
+    grid.sync();
+    sstamp(a.tdbg, ts);
+    if (warp < 5) {  // warp m: this block's offset in list m and its total
+      int o = 0, t = 0;
+      for (int b = lane; b < G; b += 32) {
+        const int v = __ldcg(a.blk + (2 + warp) * G + b);
+        if (b < (int)blockIdx.x) o += v;
+        t += v;
+      }
+      for (int q = 16; q > 0; q >>= 1) {
+        o += __shfl_xor_sync(0xffffffffu, o, q);
+        t += __shfl_xor_sync(0xffffffffu, t, q);
+      }
+      if (lane == 0) {
+        soff5[warp] = o;
+        stot5[warp] = t;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+      int pos = soff5[m];
+      for (int k = 0; k < warp; ++k) pos += wc5[m][k];
+      int32_t* L = a.lists + (int64_t)m * N;
+      int32_t* idx = m == L_B ? a.idx : nullptr;
+      for (int64_t wb = ww0; wb < ww1; wb += 32) {
+        const uint32_t mine = fast ? wd[m] : (wb + lane < ww1 ? __ldcg(a.masks + (int64_t)m * mw + wb + lane) : 0u);
+        const int nwk = (int)min((int64_t)32, ww1 - wb);
+        int jrow = (int)wb / g.wpr, wcol = (int)wb - jrow * g.wpr;  // tracked incrementally
+        for (int k = 0; k < nwk; ++k) {
+          const uint32_t bits = __shfl_sync(0xffffffffu, mine, k);
+          if ((bits >> lane) & 1u) {
+            const int p = pos + __popc(bits & ((1u << lane) - 1u));
+            const int cell = jrow * g.nx + 32 * wcol + lane;
+            L[p] = cell;
+            if (idx) idx[cell] = p;
+          }
+          pos += __popc(bits);
+          if (++wcol == g.wpr) {
+            wcol = 0;
+            ++jrow;
+          }
+        }
+      }
+      if (blockIdx.x == 0 && tid == 0) a.counts[m] = stot5[m];
+    }
   }
   grid.sync();
   sstamp(a.tdbg, ts);
@@ -454,7 +522,7 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + tid, gstride = (int64_t)G * blockDim.x;
   for (int64_t t = gtid; t < nb; t += gstride) {
     const int64_t n = LB[t];
-    const int i = (int)(n % g.nx), j = (int)(n / g.nx);
+    const int j = (int)n / g.nx, i = (int)n - j * g.nx;
     for (int m = -a.rmax; m <= a.rmax; ++m) {
       if (m == 0) continue;
       bool ok;
@@ -487,7 +555,7 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
   sstamp(a.tdbg, ts);
   for (int64_t t = gtid; t < nb; t += gstride) {
     const int64_t n = LB[t];
-    const int i = (int)(n % g.nx), j = (int)(n / g.nx);
+    const int j = (int)n / g.nx, i = (int)n - j * g.nx;
     for (int m = -a.rmax; m <= a.rmax; ++m) {
       bool ok;
       int ii = wrapi(i + m, g.nx, g.bc, &ok);
