@@ -110,8 +110,8 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
         if (row < total_rows) {
           int64_t e;
           if (a.mode == 1) {
-            const int var = (int)(row / nS);
-            e = (int64_t)var * a.g.N + __ldg(a.list + (row - (int64_t)var * nS));
+            const int var = (int)row / nS;  // 32-bit: c * |S-hat| < 2^31
+            e = (int64_t)var * a.g.N + __ldg(a.list + ((int)row - var * nS));
             const int64_t se = sidx(slab, e);
             for (int col = part; col < nU; col += PARTS) cp_async8(tile + col * LDT + k, scol[col] + se);
             if (nU % PARTS == part) cp_async8(tile + nU * LDT + k, a.src_b.p + sidx(a.src_b, e));
