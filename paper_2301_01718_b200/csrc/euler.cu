@@ -12,6 +12,11 @@
 namespace hrom {
 namespace {
 
+__device__ __forceinline__ double minmod(double a, double b) {
+  if (a * b <= 0.0) return 0.0;
+  return a > 0.0 ? fmin(a, b) : fmax(a, b);
+}
+
 template <int DIM>
 __device__ __forceinline__ double pressure(const double* U, double gm1) {
   double m2 = U[1] * U[1];
@@ -19,19 +24,24 @@ __device__ __forceinline__ double pressure(const double* U, double gm1) {
   return gm1 * (U[DIM + 1] - 0.5 * m2 / U[0]);
 }
 
-__device__ __forceinline__ double minmod(double a, double b) {
-  if (a * b <= 0.0) return 0.0;
-  return a > 0.0 ? fmin(a, b) : fmax(a, b);
+// pressure with the reciprocal density supplied (one division per state instead of three)
+template <int DIM>
+__device__ __forceinline__ double pressure_r(const double* U, double rinv, double gm1) {
+  double m2 = U[1] * U[1];
+  if (DIM == 2) m2 += U[2] * U[2];
+  return gm1 * (U[DIM + 1] - 0.5 * m2 * rinv);
 }
 
-// Rusanov flux along AXIS from reconstructed face states (O5)
+// Rusanov flux along AXIS from reconstructed face states (O5).  1/rho is formed once per state
+// (u = m / rho, p, c = sqrt(gamma p / rho) all use it): equal to the divided forms to ~1 ulp.
 template <int DIM, int AXIS>
 __device__ __forceinline__ void rusanov(const double* UL, const double* UR, double gamma, double* F) {
   constexpr int C = DIM + 2;
   const double gm1 = gamma - 1.0;
-  const double pL = pressure<DIM>(UL, gm1), pR = pressure<DIM>(UR, gm1);
-  const double uL = UL[1 + AXIS] / UL[0], uR = UR[1 + AXIS] / UR[0];
-  const double cL = sqrt(gamma * pL / UL[0]), cR = sqrt(gamma * pR / UR[0]);
+  const double rL = 1.0 / UL[0], rR = 1.0 / UR[0];
+  const double pL = pressure_r<DIM>(UL, rL, gm1), pR = pressure_r<DIM>(UR, rR, gm1);
+  const double uL = UL[1 + AXIS] * rL, uR = UR[1 + AXIS] * rR;
+  const double cL = sqrt(gamma * pL * rL), cR = sqrt(gamma * pR * rR);
   const double a = fmax(fabs(uL) + cL, fabs(uR) + cR);
   double FL[C], FR[C];
   FL[0] = UL[1 + AXIS];
@@ -254,6 +264,7 @@ __global__ void __launch_bounds__(256) smax_kernel(Geo g, const SRef q, unsigned
     double U[C];
 #pragma unroll
     for (int v = 0; v < C; ++v) U[v] = q.p[sidx(q, v * g.N + n)];
+    // the divided forms of the CFL rule (O7): dt matches the oracle's bit for bit
     const double p = pressure<DIM>(U, g.gamma - 1.0);
     const double cs = sqrt(g.gamma * p / U[0]);
     double s = (fabs(U[1] / U[0]) + cs) / g.dx;
@@ -304,6 +315,7 @@ __global__ void __launch_bounds__(256) positivity_kernel(Geo g, const SRef q, un
     double U[C];
 #pragma unroll
     for (int v = 0; v < C; ++v) U[v] = q.p[sidx(q, v * g.N + n)];
+    // the divided forms of the CFL rule (O7): dt matches the oracle's bit for bit
     const double p = pressure<DIM>(U, g.gamma - 1.0);
     if (!(U[0] > 0.0) || !(p > 0.0)) atomicMin(bad, (unsigned long long)n);
     const double cs = sqrt(g.gamma * p / U[0]);
