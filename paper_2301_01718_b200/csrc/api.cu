@@ -222,7 +222,9 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   }
   if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_basis_in, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_basis_done, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->ev_basis_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_bg_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_bg_done, cudaEventDisableTiming) != cudaSuccess) {
     hrom_destroy(c);
     return HROM_E_CUDA;
   }
@@ -238,6 +240,8 @@ void hrom_destroy(hrom_ctx* c) {
   if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_basis_in) cudaEventDestroy(c->ev_basis_in);
   if (c->ev_basis_done) cudaEventDestroy(c->ev_basis_done);
+  if (c->ev_bg_in) cudaEventDestroy(c->ev_bg_in);
+  if (c->ev_bg_done) cudaEventDestroy(c->ev_bg_done);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   Bufs& b = c->b;
   void* ptrs[] = {b.ring, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
@@ -358,10 +362,21 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
   if (c->P.n_filter_orders > 0 && c->P.filter_max_sweeps > 0)
     if ((s = launch_filter(c, out, U3, nullptr)) != HROM_OK) return s;
   prof_end(c, SEC_FILTER);
-  prof_begin(c, SEC_BANDGRAM);
-  if (c->P.gram_mode == 0)
-    if ((s = launch_band_gram(c, c->win, out)) != HROM_OK) return s;
-  prof_end(c, SEC_BANDGRAM);
+  if (c->P.gram_mode == 0) {
+    // H10 band part on the side stream, concurrently with the positivity pass (both only read
+    // gamma_k; an escalated step discards the band partials); joined in basis_join()
+    HROM_CK(cudaEventRecord(c->ev_bg_in, c->st));
+    HROM_CK(cudaStreamWaitEvent(c->side, c->ev_bg_in, 0));
+    cudaStream_t main_st = c->st;
+    c->st = c->side;
+    prof_begin(c, SEC_BANDGRAM);
+    s = launch_band_gram(c, c->win, out);
+    prof_end(c, SEC_BANDGRAM);
+    c->st = main_st;
+    if (s != HROM_OK) return s;
+    HROM_CK(cudaEventRecord(c->ev_bg_done, c->side));
+    c->bg_pending = true;
+  }
   prof_begin(c, SEC_POS);
   if ((s = launch_positivity(c, qn, out, kn)) != HROM_OK) return s;
   prof_end(c, SEC_POS);

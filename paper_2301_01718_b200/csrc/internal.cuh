@@ -159,6 +159,8 @@ struct hrom_ctx {
   cudaEvent_t ev_basis_in = nullptr, ev_basis_done = nullptr;
   bool basis_pending = false;  // eigen-solve launched on the side stream, not yet joined
   bool eig_todo = false;       // eigen-solve deferred (launched after the sampling kernel)
+  cudaEvent_t ev_bg_in = nullptr, ev_bg_done = nullptr;
+  bool bg_pending = false;     // band Gram partials computed on the side stream, not yet joined
   hrom::Win eig_win{};
   int slot_of(int64_t kk) const { return (int)(kk % nslots); }
   hrom::SRef slot_ref(int s) const { return hrom::SRef{b.ring + (int64_t)s * hrom::TILE, g.nsr}; }
@@ -168,6 +170,10 @@ struct hrom_ctx {
 namespace hrom {
 hrom_status flush_eigen(hrom_ctx* c);  // api.cu: launch a deferred eigen-solve on the side stream
 inline void basis_join(hrom_ctx* c) {
+  if (c->bg_pending) {
+    cudaStreamWaitEvent(c->st, c->ev_bg_done, 0);
+    c->bg_pending = false;
+  }
   if (c->eig_todo) flush_eigen(c);
   if (c->basis_pending) {
     cudaStreamWaitEvent(c->st, c->ev_basis_done, 0);
