@@ -62,6 +62,9 @@ typedef struct {
   double sample_fraction;    /* f: n_g = ceil(f N) HDM cells per hybrid step (A18) */
   int32_t gram_mode;         /* 0 incremental shifted Gram (default), 1 full DMMA Gram every step */
   int32_t rebase_period;     /* steps between shifted-Gram re-bases (<= 0: w) */
+  int32_t gather_mode;       /* 0: gathered Gram of the S-hat rows updated from the previous
+                                step (S-hat churn rows + the new snapshot and HDM columns),
+                                1: recomputed over all S-hat rows every step (G7) */
 } hrom_params;
 
 /* Create a context for one grid.  cuda_stream: a cudaStream_t (NULL = legacy default).

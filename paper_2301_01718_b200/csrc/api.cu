@@ -110,6 +110,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
     if (p->filter_orders[i] != 2 && p->filter_orders[i] != 4 && p->filter_orders[i] != 6) return HROM_E_INVALID;
   if (!(p->sample_fraction > 0.0 && p->sample_fraction <= 1.0)) return HROM_E_INVALID;
   if (p->gram_mode != 0 && p->gram_mode != 1) return HROM_E_INVALID;
+  if (p->gather_mode != 0 && p->gather_mode != 1) return HROM_E_INVALID;
 
   hrom_ctx* c = new hrom_ctx();
   c->P = *p;
@@ -179,6 +180,10 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   b.gpart_len = (int64_t)(c->fill_blocks + c->band_blocks) * (kMaxSlots + 1);
   A(dalloc(&b.gpart, b.gpart_len));
   A(dalloc(&b.K, (size_t)(kMaxW + 2) * (kMaxW + 2)));
+  A(dalloc(&b.Khi, (size_t)kMaxSlots * kMaxSlots));
+  A(dalloc(&b.Klo, (size_t)kMaxSlots * kMaxSlots));
+  A(dalloc(&b.Rd, (size_t)2 * (kMaxW + 2) * (kMaxW + 2)));
+  A(dalloc(&b.vpart, (size_t)8 * c->nsm * (2 * kMaxSlots + 2)));
   A(dalloc(&b.A, (size_t)kMaxW * kMaxR));
   A(dalloc(&b.lam, kMaxSlots));
   A(dalloc(&b.y, kMaxR));
@@ -192,7 +197,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   A(dalloc(&b.dbg, 64));
   A(dalloc(&b.sel_val, g.N));
   A(dalloc(&b.sel_cell, g.N));
-  b.blk_len = std::max<int64_t>(8 * ((c->mwords + 255) / 256 + 2) + (g.N + 1023) / 1024 + 16, 8 * (int64_t)c->nsm + 64);
+  b.blk_len = std::max<int64_t>(8 * ((c->mwords + 255) / 256 + 2) + (g.N + 1023) / 1024 + 16, 16 * (int64_t)c->nsm + 64);
   A(dalloc(&b.blk, b.blk_len));
   A(dalloc(&b.hist, 3 * 2048));
   A(dalloc(&b.fstat, c->filter_blocks));
@@ -245,7 +250,7 @@ void hrom_destroy(hrom_ctx* c) {
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   Bufs& b = c->b;
   void* ptrs[] = {b.ring, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
-                  b.kept, b.fidx, b.ftab, b.fcur, b.fF, b.C, b.part, b.gpart, b.K, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
+                  b.kept, b.fidx, b.ftab, b.fcur, b.fF, b.C, b.part, b.gpart, b.K, b.Khi, b.Klo, b.Rd, b.vpart, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
                   b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.fstat, b.fcnt, (void*)b.colptr, b.slot_tab};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -279,6 +284,7 @@ hrom_status hrom_set_state(hrom_ctx* c, const double* any_q) {
   HROM_CK(cudaMemsetAsync(c->b.ureg + 1, 0xff, sizeof(unsigned long long), c->st));
   c->k = 0;
   c->last_hybrid = false;
+  c->kinc_valid = false;
   c->basis_ready = c->sets_ready = c->gram_row_ready = false;
   c->rebase_k = -1000000;
   c->last_err_cell = -1;
@@ -561,6 +567,7 @@ hrom_status hrom_rebuild_basis(hrom_ctx* c, int64_t k, const uint32_t* any_mask_
   HROM_CK(cudaMemsetAsync(c->b.ureg + 1, 0xff, sizeof(unsigned long long), c->st));
   c->k = k;
   c->last_hybrid = false;
+  c->kinc_valid = false;
   c->basis_ready = false;
   c->gram_row_ready = false;
   c->rebase_k = -1000000;

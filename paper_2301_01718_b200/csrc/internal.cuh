@@ -70,9 +70,11 @@ struct Win {
 };
 
 // mask indices
-enum { M_S = 0, M_B, M_T, M_A2, M_A1, M_TMP, M_TMP2, M_H, M_COUNT };  // M_H: seam-filter halo
+// M_H: seam-filter halo; M_SPREV: S-hat of the previous sampling; M_ADD / M_REM: its churn
+enum { M_S = 0, M_B, M_T, M_A2, M_A1, M_TMP, M_TMP2, M_H, M_SPREV, M_ADD, M_REM, M_COUNT };
 // list indices
-enum { L_S = 0, L_B, L_T, L_A2, L_A1, L_H, L_COUNT };  // L_H: seam-filter halo
+// L_H: seam-filter halo; L_ADD / L_REM: cells entering / leaving S-hat at the last sampling
+enum { L_S = 0, L_B, L_T, L_A2, L_A1, L_H, L_ADD, L_REM, L_COUNT };
 
 struct Bufs {
   double* ring = nullptr;     // slab: (Dp / TILE) tiles x nsr slots x TILE
@@ -97,6 +99,10 @@ struct Bufs {
   double* gpart = nullptr;    // Gram-row partials (fill + band)
   int64_t gpart_len = 0;
   double* K = nullptr;        // (kMaxW+1)^2 gathered Gram
+  double* Khi = nullptr;      // kMaxSlots^2: incremental gathered Gram by ring slot (double-double)
+  double* Klo = nullptr;
+  double* Rd = nullptr;       // 2 (kMaxW+2)^2: Gram of the rows entering / leaving S-hat
+  double* vpart = nullptr;    // per-CTA partials of the S-hat GEMVs
   double* A = nullptr;        // w x r (column j: mode j)
   double* lam = nullptr;      // w eigenvalues
   double* y = nullptr;        // r
@@ -161,6 +167,11 @@ struct hrom_ctx {
   bool eig_todo = false;       // eigen-solve deferred (launched after the sampling kernel)
   cudaEvent_t ev_bg_in = nullptr, ev_bg_done = nullptr;
   bool bg_pending = false;     // band Gram partials computed on the side stream, not yet joined
+  // incremental gathered Gram (G7): valid for the S-hat of the last sampling, shift rebase_k and
+  // the union whose newest snapshot is kinc_newest
+  bool kinc_valid = false;
+  int samples_since_gather = 99;  // samplings since the last gathered Gram (churn lists valid iff 1)
+  int64_t kinc_newest = -1, kinc_rebase = -1;
   hrom::Win eig_win{};
   int slot_of(int64_t kk) const { return (int)(kk % nslots); }
   hrom::SRef slot_ref(int s) const { return hrom::SRef{b.ring + (int64_t)s * hrom::TILE, g.nsr}; }

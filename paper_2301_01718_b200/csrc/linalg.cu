@@ -14,6 +14,8 @@
 namespace hrom {
 namespace {
 
+constexpr int GR_TPE = 16;  // threads per entry of the fixed-order partial reductions
+
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -216,14 +218,179 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
   }
 }
 
-// deterministic fixed-order reduction over CTAs; C[i][j] for i <= j mirrored
-__global__ void gram_reduce(const double* __restrict__ part, int nblk, int ncp, int ncol, double* __restrict__ C,
-                            int ldc, const int32_t* __restrict__ map) {
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < ncol * ncol; idx += gridDim.x * blockDim.x) {
-    const int i = idx / ncol, j = idx % ncol;
-    if (i > j) continue;
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * ncp * ncp + i * ncp + j];
+// ---------------- G7: incremental gathered Gram ----------------
+// S-hat moves little from one step to the next (measured churn ~0.1-1 % of its cells at config
+// 4), and the union window shifts by one snapshot.  So the Gram of the old columns over the rows
+// of S-hat_{k+1} is the previous one plus the Gram of the entering rows minus that of the leaving
+// rows (kept per ring slot in double-double), while the columns that are new every step -- the
+// newest snapshot and the HDM values b -- come from two GEMVs over all S-hat rows (memory-bound,
+// no DMMA).  Re-initialised by the full gathered Gram at a re-base, after set-window/explicit
+// masks, or when the previous step was not the preceding hybrid step.
+
+// S-hat GEMVs: v_new[i] = sum_r x_i x_new, v_b[i] = sum_r x_i b, bb = sum_r b^2 over the rows of
+// S-hat (x = slot - rho, b = src_b - rho).  Lanes own consecutive rows (one slot load per warp
+// instruction = 32 consecutive list DOFs, coalesced); warp w of the CTA owns slots w, w + 8, ...;
+// GV_U row chunks in flight per lane.  Per-CTA partials [blk][2 nU + 1], reduced in fixed order.
+constexpr int GV_T = 256, GV_W = GV_T / 32, GV_U = 2;
+template <int SPW>
+__global__ void __launch_bounds__(GV_T) gemv_gather_kernel(Geo g, Win W, const double* __restrict__ ring,
+                                                           const SRef rho, const int32_t* __restrict__ list,
+                                                           const int32_t* __restrict__ count, const SRef src_b,
+                                                           double* __restrict__ vpart) {
+  __shared__ double red[GV_W][2 * SPW + 1];
+  const int nU = W.nU, nS = *count;
+  const int64_t total = (int64_t)nS * g.c;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const SRef slab{nullptr, g.nsr};
+  const double* xnew_col = ring + (int64_t)W.slot[nU - 1] * TILE;
+  const double* col[SPW];
+#pragma unroll
+  for (int j = 0; j < SPW; ++j) {
+    const int sl = warp + GV_W * j;
+    col[j] = sl < nU ? ring + (int64_t)W.slot[sl] * TILE : nullptr;
+  }
+  double an[SPW], ab[SPW];
+#pragma unroll
+  for (int j = 0; j < SPW; ++j) an[j] = ab[j] = 0.0;
+  double bb = 0.0;
+  for (int64_t base = (int64_t)blockIdx.x * 32 * GV_U; base < total; base += (int64_t)gridDim.x * 32 * GV_U) {
+    int64_t se[GV_U];
+    double xn[GV_U], bv[GV_U], r[GV_U];
+    bool ok[GV_U];
+#pragma unroll
+    for (int u = 0; u < GV_U; ++u) {
+      const int64_t t = base + 32 * u + lane;
+      ok[u] = t < total;
+      int64_t e = 0;
+      if (ok[u]) {
+        const int var = (int)t / nS, idx = (int)t - var * nS;
+        e = (int64_t)var * g.N + __ldg(list + idx);
+      }
+      se[u] = sidx(slab, e);
+      r[u] = ok[u] ? __ldg(rho.p + sidx(rho, e)) : 0.0;
+      xn[u] = ok[u] ? __ldg(xnew_col + se[u]) : 0.0;
+      bv[u] = ok[u] ? __ldg(src_b.p + sidx(src_b, e)) : 0.0;
+    }
+    double val[GV_U][SPW];
+#pragma unroll
+    for (int u = 0; u < GV_U; ++u)
+#pragma unroll
+      for (int j = 0; j < SPW; ++j) val[u][j] = (ok[u] && col[j]) ? __ldg(col[j] + se[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < GV_U; ++u) {
+      if (!ok[u]) continue;
+      const double x = xn[u] - r[u], y = bv[u] - r[u];
+#pragma unroll
+      for (int j = 0; j < SPW; ++j) {
+        const double v = val[u][j] - r[u];
+        an[j] += v * x;
+        ab[j] += v * y;
+      }
+      if (warp == 0) bb += y * y;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < SPW; ++j) {
+    double x = an[j], y = ab[j];
+    for (int o = 16; o > 0; o >>= 1) {
+      x += __shfl_xor_sync(0xffffffffu, x, o);
+      y += __shfl_xor_sync(0xffffffffu, y, o);
+    }
+    if (lane == 0) {
+      red[warp][j] = x;
+      red[warp][SPW + j] = y;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) bb += __shfl_xor_sync(0xffffffffu, bb, o);
+  if (lane == 0) red[warp][2 * SPW] = bb;
+  __syncthreads();
+  double* out = vpart + (int64_t)blockIdx.x * (2 * nU + 1);
+  for (int k = threadIdx.x; k <= 2 * nU; k += GV_T) {
+    double v;
+    if (k == 2 * nU) {
+      v = red[0][2 * SPW];
+    } else {
+      const int sl = k < nU ? k : k - nU;  // slot sl is (warp sl % GV_W, j = sl / GV_W)
+      v = red[sl % GV_W][(k < nU ? 0 : SPW) + sl / GV_W];
+    }
+    out[k] = v;
+  }
+}
+
+// fixed-order reduce of the GEMV partials, 16 threads per entry
+__global__ void __launch_bounds__(256) vpart_reduce(const double* __restrict__ vpart, int nblk, int n,
+                                                    double* __restrict__ v) {
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int k = (int)(gt / GR_TPE), sub = (int)(gt % GR_TPE);
+  double s = 0.0;
+  if (k < n)
+    for (int b = sub; b < nblk; b += GR_TPE) s += vpart[(int64_t)b * n + k];
+  for (int o = GR_TPE / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (k < n && sub == 0) v[k] = s;
+}
+
+__device__ __forceinline__ void dd_add(double& hi, double& lo, double x) {  // (hi, lo) += x
+  const double s = hi + x;
+  const double bp = s - hi;
+  const double e = (hi - (s - bp)) + (x - bp);  // TwoSum error
+  lo += e;
+  hi = s + lo;
+  lo = lo - (hi - s);
+}
+
+// Ks (by ring slot) <- update; Rout ((nU+1)^2, union order) <- the gathered Gram for the solve.
+// init: Rout holds a full gathered Gram -> Ks = Rout.  Otherwise: old-old block += R+ - R-,
+// newest-slot row/column and the b row/column from the reduced GEMV partials.
+__global__ void __launch_bounds__(512) kinc_update_kernel(Win W, int init, const double* __restrict__ Rp,
+                                                          const double* __restrict__ Rm, const double* __restrict__ v,
+                                                          double* __restrict__ Khi, double* __restrict__ Klo,
+                                                          double* __restrict__ Rout) {
+  const int nU = W.nU, ldr = nU + 1;
+  if (init) {
+    for (int idx = threadIdx.x; idx < nU * nU; idx += blockDim.x) {
+      const int i = idx / nU, j = idx % nU;
+      Khi[W.slot[i] * kMaxSlots + W.slot[j]] = Rout[i * ldr + j];
+      Klo[W.slot[i] * kMaxSlots + W.slot[j]] = 0.0;
+    }
+    return;
+  }
+  for (int idx = threadIdx.x; idx < nU * nU; idx += blockDim.x) {
+    const int i = idx / nU, j = idx % nU;
+    const int si = W.slot[i], sj = W.slot[j];
+    double hi, lo;
+    if (i == nU - 1 || j == nU - 1) {
+      hi = v[i == nU - 1 ? j : i];
+      lo = 0.0;
+    } else {
+      hi = Khi[si * kMaxSlots + sj];
+      lo = Klo[si * kMaxSlots + sj];
+      dd_add(hi, lo, Rp[i * ldr + j]);
+      dd_add(hi, lo, -Rm[i * ldr + j]);
+    }
+    Khi[si * kMaxSlots + sj] = hi;
+    Klo[si * kMaxSlots + sj] = lo;
+    Rout[i * ldr + j] = hi + lo;
+  }
+  for (int i = threadIdx.x; i < nU; i += blockDim.x) {
+    Rout[i * ldr + nU] = v[nU + i];
+    Rout[nU * ldr + i] = v[nU + i];
+  }
+  if (threadIdx.x == 0) Rout[nU * ldr + nU] = v[2 * nU];
+}
+
+// deterministic fixed-order reduction over CTAs, 16 threads per entry (block-strided sub-sums,
+// then a fixed shuffle tree); C[i][j] for i <= j mirrored
+__global__ void __launch_bounds__(256) gram_reduce(const double* __restrict__ part, int nblk, int ncp, int ncol,
+                                                   double* __restrict__ C, int ldc, const int32_t* __restrict__ map) {
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int idx = (int)(gt / GR_TPE), sub = (int)(gt % GR_TPE);
+  const int i = idx / ncol, j = idx % ncol;
+  const bool act = idx < ncol * ncol && i <= j;
+  double s = 0.0;
+  if (act)
+    for (int b = sub; b < nblk; b += GR_TPE) s += part[(int64_t)b * ncp * ncp + i * ncp + j];
+  for (int o = GR_TPE / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (act && sub == 0) {
     const int ci = map ? map[i] : i, cj = map ? map[j] : j;
     C[ci * ldc + cj] = s;
     C[cj * ldc + ci] = s;
@@ -655,7 +822,7 @@ hrom_status run_gather_gram(hrom_ctx* c, GGArgs& a, int ncol, int grid, double* 
   }
   HROM_LAUNCH_CK();
   ++c->nlaunch;
-  gram_reduce<<<64, 256, 0, c->st>>>(c->b.part, grid, ncp, ncol, dev_C, ldc, map);
+  gram_reduce<<<(ncol * ncol * GR_TPE + 255) / 256, 256, 0, c->st>>>(c->b.part, grid, ncp, ncol, dev_C, ldc, map);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;
@@ -676,7 +843,8 @@ hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int64_t ns, in
   return run_gather_gram(c, a, ncol, c->basis_pending ? c->nsm - 1 : c->nsm, dev_C, ldc, map);
 }
 
-// gathered Gram of [X_S, b] over the rows of S-hat -> b.K ((w+1) x (w+1), centred)
+// gathered Gram R of [U, b] over the rows of S-hat (shifted by rho, union order, (nU+1)^2 in
+// b.eigV); the lagged centring is applied by solve_kernel
 hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   GGArgs a{};
   a.g = c->g;
@@ -691,9 +859,50 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   // out: a static tile split with one block left over would double the time
   const int grid = c->basis_pending ? c->nsm - 1 : c->nsm;
   const int ncol = a.W.nU + 1;
-  hrom_status s = run_gather_gram(c, a, ncol, grid, c->b.eigV, ncol, nullptr);  // R: (nU+1)^2 scratch
-  if (s != HROM_OK) return s;
-  return HROM_OK;  // the lagged centring of R is applied by solve_kernel
+  double* R = c->b.eigV;
+  const bool inc = c->P.gather_mode == 0 && c->kinc_valid && c->samples_since_gather == 1 && c->kinc_newest == c->k - 1 &&
+                   c->kinc_rebase == c->rebase_k;
+  hrom_status s;
+  if (!inc) {
+    if ((s = run_gather_gram(c, a, ncol, grid, R, ncol, nullptr)) != HROM_OK) return s;
+    if (c->P.gather_mode == 0) {
+      kinc_update_kernel<<<1, 512, 0, c->st>>>(a.W, 1, nullptr, nullptr, nullptr, c->b.Khi, c->b.Klo, R);
+      HROM_LAUNCH_CK();
+      ++c->nlaunch;
+    }
+  } else {
+    // rows entering and leaving S-hat (cells of the last sampling's churn)
+    double* Rp = c->b.Rd;
+    double* Rm = c->b.Rd + (size_t)(kMaxW + 2) * (kMaxW + 2);
+    GGArgs d = a;
+    d.list = c->b.lists + (int64_t)L_ADD * c->g.N;
+    d.count = c->b.counts + L_ADD;
+    if ((s = run_gather_gram(c, d, ncol, grid, Rp, ncol, nullptr)) != HROM_OK) return s;
+    d.list = c->b.lists + (int64_t)L_REM * c->g.N;
+    d.count = c->b.counts + L_REM;
+    if ((s = run_gather_gram(c, d, ncol, grid, Rm, ncol, nullptr)) != HROM_OK) return s;
+    // GEMVs of the newest snapshot and of b over all S-hat rows
+    const int gblocks = 4 * c->nsm;
+    const int nv = 2 * a.W.nU + 1;
+    if (a.W.nU <= 9 * GV_W)
+      gemv_gather_kernel<9><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b, c->b.vpart);
+    else
+      gemv_gather_kernel<17><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b, c->b.vpart);
+    HROM_LAUNCH_CK();
+    double* v = c->b.vpart + (size_t)gblocks * nv;
+    vpart_reduce<<<(nv * GR_TPE + 255) / 256, 256, 0, c->st>>>(c->b.vpart, gblocks, nv, v);
+    HROM_LAUNCH_CK();
+    kinc_update_kernel<<<1, 512, 0, c->st>>>(a.W, 0, Rp, Rm, v, c->b.Khi, c->b.Klo, R);
+    HROM_LAUNCH_CK();
+    c->nlaunch += 3;
+  }
+  if (c->P.gather_mode == 0) {
+    c->kinc_valid = true;
+    c->kinc_newest = c->k;
+    c->kinc_rebase = c->rebase_k;
+  }
+  c->samples_since_gather = 0;
+  return HROM_OK;
 }
 
 hrom_status small_solve(hrom_ctx* c) {

@@ -240,6 +240,9 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
   uint32_t* TMP = a.masks + (int64_t)M_TMP * mw;
   uint32_t* FLAT = a.masks + (int64_t)M_TMP2 * mw;
   uint32_t* HM = a.masks + (int64_t)M_H * mw;
+  uint32_t* SPREV = a.masks + (int64_t)M_SPREV * mw;
+  uint32_t* MADD = a.masks + (int64_t)M_ADD * mw;
+  uint32_t* MREM = a.masks + (int64_t)M_REM * mw;
   __shared__ int sbuf[32];
   __shared__ int wcnt[32];
   __shared__ int shist[NBIN];
@@ -276,7 +279,10 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
         }
       }
       const BlockRange rs = thread_range(nw);
-      for (int64_t w = rs.w0; w < rs.w1; ++w) S[w] = 0u;
+      for (int64_t w = rs.w0; w < rs.w1; ++w) {
+        SPREV[w] = S[w];  // the churn of S-hat feeds the incremental gathered Gram (G7)
+        S[w] = 0u;
+      }
       int tot;
       block_excl_scan(mine, &tot, sbuf);
       if (tid == 0) a.blk[0 * G + blockIdx.x] = tot;
@@ -403,6 +409,9 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
       const int wq = (int)w, jq = wq / g.wpr;
       TMP[w] = xdil_word(S, g, jq, wq - jq * g.wpr, a.band);
       HM[w] = 0u;
+      const uint32_t sn = __ldcg(S + w), sp = a.do_select ? SPREV[w] : sn;
+      MADD[w] = sn & ~sp;
+      MREM[w] = sp & ~sn;
     }
   }
   grid.sync();
@@ -432,46 +441,49 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
     grid.sync();
   sstamp(a.tdbg, ts);
   }
-  // ordered compaction of S, B, T, A2, A1 (mask index == list index), all five at once: each
-  // warp loads its words of the five masks once (kept in registers when the warp's range is
-  // <= 32 words), per-warp counts stay in shared memory across the grid barrier
+  // ordered compaction of S, B, T, A2, A1 and the S-hat churn (entering / leaving cells), all
+  // seven at once: each warp loads its words of the seven masks once (kept in registers when the
+  // warp's range is <= 32 words), per-warp counts stay in shared memory across the grid barrier
   const int64_t rchunk = (nw + G - 1) / G;
   const int64_t rb0 = min((int64_t)blockIdx.x * rchunk, nw), rb1 = min(rb0 + rchunk, nw);
-  __shared__ int wc5[5][32];
-  __shared__ int soff5[5], stot5[5];
+  constexpr int NSET = 7;
+  const int mk[NSET] = {M_S, M_B, M_T, M_A2, M_A1, M_ADD, M_REM};
+  const int lk[NSET] = {L_S, L_B, L_T, L_A2, L_A1, L_ADD, L_REM};
+  __shared__ int wc5[NSET][32];
+  __shared__ int soff5[NSET], stot5[NSET];
   {
     int64_t ww0, ww1;
     warp_range(rb0, rb1, &ww0, &ww1);
     const int lane = tid & 31, warp = tid >> 5;
     const bool fast = ww1 - ww0 <= 32;  // uniform: every warp gets the same range length
-    uint32_t wd[5];
-    int c5[5];
+    uint32_t wd[NSET];
+    int c5[NSET];
 #pragma unroll
-    for (int m = 0; m < 5; ++m) {
-      wd[m] = (fast && ww0 + lane < ww1) ? __ldcg(a.masks + (int64_t)m * mw + ww0 + lane) : 0u;
+    for (int m = 0; m < NSET; ++m) {
+      wd[m] = (fast && ww0 + lane < ww1) ? __ldcg(a.masks + (int64_t)mk[m] * mw + ww0 + lane) : 0u;
       c5[m] = __popc(wd[m]);
     }
     if (!fast)
 #pragma unroll
-      for (int m = 0; m < 5; ++m)
-        for (int64_t w = ww0 + lane; w < ww1; w += 32) c5[m] += __popc(__ldcg(a.masks + (int64_t)m * mw + w));
+      for (int m = 0; m < NSET; ++m)
+        for (int64_t w = ww0 + lane; w < ww1; w += 32) c5[m] += __popc(__ldcg(a.masks + (int64_t)mk[m] * mw + w));
 #pragma unroll
-    for (int m = 0; m < 5; ++m) {
+    for (int m = 0; m < NSET; ++m) {
       for (int o = 16; o > 0; o >>= 1) c5[m] += __shfl_xor_sync(0xffffffffu, c5[m], o);
       if (lane == 0) wc5[m][warp] = c5[m];
     }
     __syncthreads();
-    if (tid < 5) {
+    if (tid < NSET) {
       int t = 0;
       for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += wc5[tid][k];
-      a.blk[(2 + tid) * G + blockIdx.x] = t;
+      a.blk[(8 + tid) * G + blockIdx.x] = t;
     }
     grid.sync();
     sstamp(a.tdbg, ts);
-    if (warp < 5) {  // warp m: this block's offset in list m and its total
+    if (warp < NSET) {  // warp m: this block's offset in list m and its total
       int o = 0, t = 0;
       for (int b = lane; b < G; b += 32) {
-        const int v = __ldcg(a.blk + (2 + warp) * G + b);
+        const int v = __ldcg(a.blk + (8 + warp) * G + b);
         if (b < (int)blockIdx.x) o += v;
         t += v;
       }
@@ -486,13 +498,13 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
     }
     __syncthreads();
 #pragma unroll
-    for (int m = 0; m < 5; ++m) {
+    for (int m = 0; m < NSET; ++m) {
       int pos = soff5[m];
       for (int k = 0; k < warp; ++k) pos += wc5[m][k];
-      int32_t* L = a.lists + (int64_t)m * N;
-      int32_t* idx = m == L_B ? a.idx : nullptr;
+      int32_t* L = a.lists + (int64_t)lk[m] * N;
+      int32_t* idx = lk[m] == L_B ? a.idx : nullptr;
       for (int64_t wb = ww0; wb < ww1; wb += 32) {
-        const uint32_t mine = fast ? wd[m] : (wb + lane < ww1 ? __ldcg(a.masks + (int64_t)m * mw + wb + lane) : 0u);
+        const uint32_t mine = fast ? wd[m] : (wb + lane < ww1 ? __ldcg(a.masks + (int64_t)mk[m] * mw + wb + lane) : 0u);
         const int nwk = (int)min((int64_t)32, ww1 - wb);
         int jrow = (int)wb / g.wpr, wcol = (int)wb - jrow * g.wpr;  // tracked incrementally
         for (int k = 0; k < nwk; ++k) {
@@ -510,7 +522,7 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
           }
         }
       }
-      if (blockIdx.x == 0 && tid == 0) a.counts[m] = stot5[m];
+      if (blockIdx.x == 0 && tid == 0) a.counts[lk[m]] = stot5[m];
     }
   }
   grid.sync();
@@ -594,7 +606,7 @@ hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long lon
   a.idx = c->b.fidx;
   a.tab = c->b.ftab;
   a.tdbg = c->b.dbg;
-  if ((int64_t)8 * c->sets_blocks > c->b.blk_len) return HROM_E_INVALID;
+  if ((int64_t)16 * c->sets_blocks > c->b.blk_len) return HROM_E_INVALID;
   void* args[] = {&a};
   HROM_CK(cudaLaunchCooperativeKernel((void*)sets_kernel, dim3(c->sets_blocks), dim3(ST_T), args, 0, c->st));
   ++c->nlaunch;
@@ -614,6 +626,7 @@ namespace {
 // S-hat bitmap (in masks[M_S]) -> B, T, A2, A1 bitmaps, their ascending lists and the
 // seam-filter tables.
 hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S) {
+  c->samples_since_gather = 99;  // an explicit S-hat: no churn lists for the incremental Gram
   uint32_t* S = c->b.masks + (int64_t)M_S * c->mwords;
   if (dev_mask_S && dev_mask_S != S)
     HROM_CK(cudaMemcpyAsync(S, dev_mask_S, c->mwords * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->st));
@@ -622,6 +635,7 @@ hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S) {
 
 // top-n_g of eps > 0 -> S-hat (ties at the threshold by ascending cell), then build_sets.
 hrom_status select_and_build(hrom_ctx* c, const double* eps, int64_t n_g) {
+  ++c->samples_since_gather;
   return launch_sets(c, true, eps, (long long)n_g);
 }
 

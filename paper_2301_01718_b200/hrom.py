@@ -37,7 +37,8 @@ class Params(C.Structure):
                 ("filter_orders", C.c_int32 * 3), ("n_filter_orders", C.c_int32),
                 ("filter_max_sweeps", C.c_int32), ("filter_eps", C.c_double),
                 ("eig_rel_cutoff", C.c_double), ("lsq_rel_cutoff", C.c_double),
-                ("sample_fraction", C.c_double), ("gram_mode", C.c_int32), ("rebase_period", C.c_int32)]
+                ("sample_fraction", C.c_double), ("gram_mode", C.c_int32), ("rebase_period", C.c_int32),
+                ("gather_mode", C.c_int32)]
 
 
 # every entry point of include/hrom.h with its ctypes signature
@@ -147,7 +148,7 @@ class HybridROM:
     """One hrom_ctx: an explicit hybrid-snapshot AROM on one grid, on the current CUDA device."""
 
     def __init__(self, wl, stream: Optional[torch.cuda.Stream] = None, gram_mode: int = 0,
-                 rebase_period: int = 0):
+                 rebase_period: int = 0, gather_mode: int = 0):
         if not torch.cuda.is_available():
             raise RuntimeError("libhrom needs a CUDA device (B200, sm_100a); no CPU fallback exists")
         self.lib = load_library()
@@ -156,7 +157,7 @@ class HybridROM:
         g = Grid(wl.dim, wl.nx, wl.ny if wl.dim == 2 else 1, wl.x0, wl.x1, wl.y0, wl.y1, wl.bc, wl.recon)
         fo = (C.c_int32 * 3)(*(list(wl.filter_orders) + [0, 0, 0])[:3])
         p = Params(wl.w, wl.r, wl.h, wl.W, fo, len(wl.filter_orders), wl.filter_max_sweeps, wl.filter_eps,
-                   wl.eig_rel_cutoff, wl.lsq_rel_cutoff, wl.f, gram_mode, rebase_period)
+                   wl.eig_rel_cutoff, wl.lsq_rel_cutoff, wl.f, gram_mode, rebase_period, gather_mode)
         h = C.c_void_p()
         _ck(self.lib.hrom_create(C.byref(g), wl.gamma, wl.cfl, C.byref(p), C.c_void_p(self.stream.cuda_stream),
                                  C.byref(h)), "hrom_create")
