@@ -174,11 +174,15 @@ __device__ int sym_eig(double* A, int n, int ldn, const EigWork& W, int nvec_cap
   const double tol = 4.0 * DBL_EPSILON * tn;
   glo -= 2.0 * tol + pivmin;
   ghi += 2.0 * tol + pivmin;
+  // only the nl = min(n, nvec_cap) largest eigenvalues are needed (the cut and the basis use
+  // lambda_0 .. lambda_{r-1}); lam[j >= nl] are left 0
+  const int nl = nvec_cap < n ? nvec_cap : n;
+  for (int j = nl + tid; j < n; j += nt) W.lam[j] = 0.0;
   int G = 1;
-  while (G < 32 && 2 * G * n <= nt) G *= 2;
+  while (G < 32 && 2 * G * nl <= nt) G *= 2;
   const int P = G > 1 ? G - 1 : 1;  // evaluation points per group
   const int ngrp = nt / G, grp = tid / G, gl = tid % G, gbase = (lane / G) * G;
-  for (int k0 = 0; k0 < n; k0 += ngrp) {
+  for (int k0 = n - nl; k0 < n; k0 += ngrp) {
     const int k = k0 + grp;  // ascending index
     double lo = glo, hi = ghi;
     for (int round = 0; round < 256; ++round) {
@@ -326,29 +330,21 @@ __device__ int sym_eig(double* A, int n, int ldn, const EigWork& W, int nvec_cap
     __syncthreads();
   }
   mark(3);
-  // ---- 4. back-transformation Z <- H_0 ... H_{n-3} Z ----
-  int TPC = 1;  // threads per column for the dot products
-  while (TPC < 32 && 2 * TPC * nvec <= nt) TPC *= 2;
-  for (int k = n - 3; k >= 0; --k) {
-    const double tau = W.tau[k];
-    if (tau == 0.0) continue;  // uniform
-    const int m = n - k - 1;
-    for (int base = 0; base < nvec * TPC; base += nt) {
-      const int idx = base + tid, col = idx / TPC, sub = idx % TPC;
+  // ---- 4. back-transformation Z <- H_0 ... H_{n-3} Z: one warp per eigenvector, all reflectors
+  // applied with warp reductions only (the reflectors are read-only now: no block barriers) ----
+  for (int j = warp; j < nvec; j += nw) {
+    for (int k = n - 3; k >= 0; --k) {
+      const double tau = W.tau[k];
+      if (tau == 0.0) continue;  // uniform within the warp
+      const int m = n - k - 1;
       double s = 0.0;
-      if (col < nvec)
-        for (int i = sub; i < m; i += TPC) s += (i == 0 ? 1.0 : A[(k + 1 + i) * ldn + k]) * W.Z[(k + 1 + i) * ldz + col];
-      for (int o = TPC >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (col < nvec && sub == 0) W.pp[col] = tau * s;
+      for (int i = lane; i < m; i += 32) s += (i == 0 ? 1.0 : A[(k + 1 + i) * ldn + k]) * W.Z[(k + 1 + i) * ldz + j];
+      s = eig_warp_sum(s) * tau;
+      for (int i = lane; i < m; i += 32) W.Z[(k + 1 + i) * ldz + j] -= (i == 0 ? 1.0 : A[(k + 1 + i) * ldn + k]) * s;
+      __syncwarp();
     }
-    __syncthreads();
-    for (int idx = tid; idx < m * nvec; idx += nt) {
-      const int i = idx / nvec, col = idx - i * nvec;
-      const double vi = i == 0 ? 1.0 : A[(k + 1 + i) * ldn + k];
-      W.Z[(k + 1 + i) * ldz + col] -= vi * W.pp[col];
-    }
-    __syncthreads();
   }
+  __syncthreads();
   // ---- sign ----
   for (int j = tid; j < nvec; j += nt) {
     int im = 0;

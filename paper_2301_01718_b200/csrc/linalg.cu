@@ -882,7 +882,7 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
     d.count = c->b.counts + L_REM;
     if ((s = run_gather_gram(c, d, ncol, grid, Rm, ncol, nullptr)) != HROM_OK) return s;
     // GEMVs of the newest snapshot and of b over all S-hat rows
-    const int gblocks = 4 * c->nsm;
+    const int gblocks = 4 * (c->basis_pending ? c->nsm - 1 : c->nsm);  // static split: avoid the eigen's SM
     const int nv = 2 * a.W.nU + 1;
     if (a.W.nU <= 9 * GV_W)
       gemv_gather_kernel<9><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b, c->b.vpart);
