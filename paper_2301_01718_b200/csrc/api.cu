@@ -376,7 +376,7 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
     cudaStream_t main_st = c->st;
     c->st = c->side;
     prof_begin(c, SEC_BANDGRAM);
-    s = launch_band_gram(c, c->win, out);
+    s = band_gram_rows(c, c->win, out);
     prof_end(c, SEC_BANDGRAM);
     c->st = main_st;
     if (s != HROM_OK) return s;

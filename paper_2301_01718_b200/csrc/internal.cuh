@@ -224,6 +224,7 @@ int sets_occupancy();
 hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int64_t ns, int ncol, int64_t rows, SRef rho,
                       double* dev_C, int ldc, const int32_t* map);
 hrom_status gram_gathered(hrom_ctx* c, SRef src_b);
+hrom_status band_gram_rows(hrom_ctx* c, const Win& W, SRef v);
 hrom_status small_solve(hrom_ctx* c);
 hrom_status basis_from_gram(hrom_ctx* c, const Win& W);
 hrom_status lift(hrom_ctx* c, const Win& W, double* phi, double* psi);

@@ -232,7 +232,9 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
 // instruction = 32 consecutive list DOFs, coalesced); warp w of the CTA owns slots w, w + 8, ...;
 // GV_U row chunks in flight per lane.  Per-CTA partials [blk][2 nU + 1], reduced in fixed order.
 constexpr int GV_T = 256, GV_W = GV_T / 32, GV_U = 2;
-template <int SPW>
+// NEWCOL = false, BANDOUT = true: the seam-band part of the new window Gram row (H10): one
+// product vector b = gamma_k on the band rows, partials [blk][nU + 1] ([nU] = sum b^2).
+template <int SPW, bool NEWCOL = true, bool BANDOUT = false>
 __global__ void __launch_bounds__(GV_T) gemv_gather_kernel(Geo g, Win W, const double* __restrict__ ring,
                                                            const SRef rho, const int32_t* __restrict__ list,
                                                            const int32_t* __restrict__ count, const SRef src_b,
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(GV_T) gemv_gather_kernel(Geo g, Win W, const d
       }
       se[u] = sidx(slab, e);
       r[u] = ok[u] ? __ldg(rho.p + sidx(rho, e)) : 0.0;
-      xn[u] = ok[u] ? __ldg(xnew_col + se[u]) : 0.0;
+      xn[u] = (NEWCOL && ok[u]) ? __ldg(xnew_col + se[u]) : 0.0;
       bv[u] = ok[u] ? __ldg(src_b.p + sidx(src_b, e)) : 0.0;
     }
     double val[GV_U][SPW];
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(GV_T) gemv_gather_kernel(Geo g, Win W, const d
 #pragma unroll
       for (int j = 0; j < SPW; ++j) {
         const double v = val[u][j] - r[u];
-        an[j] += v * x;
+        if (NEWCOL) an[j] += v * x;
         ab[j] += v * y;
       }
       if (warp == 0) bb += y * y;
@@ -304,6 +306,11 @@ __global__ void __launch_bounds__(GV_T) gemv_gather_kernel(Geo g, Win W, const d
   for (int o = 16; o > 0; o >>= 1) bb += __shfl_xor_sync(0xffffffffu, bb, o);
   if (lane == 0) red[warp][2 * SPW] = bb;
   __syncthreads();
+  if (BANDOUT) {
+    double* out = vpart + (int64_t)blockIdx.x * (nU + 1);
+    for (int k = threadIdx.x; k <= nU; k += GV_T) out[k] = k == nU ? red[0][2 * SPW] : red[k % GV_W][SPW + k / GV_W];
+    return;
+  }
   double* out = vpart + (int64_t)blockIdx.x * (2 * nU + 1);
   for (int k = threadIdx.x; k <= 2 * nU; k += GV_T) {
     double v;
@@ -902,6 +909,17 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
     c->kinc_rebase = c->rebase_k;
   }
   c->samples_since_gather = 0;
+  return HROM_OK;
+}
+
+// seam-band part of the new window Gram row (band DOFs' final values), partials after the fill's
+hrom_status band_gram_rows(hrom_ctx* c, const Win& W, SRef v) {
+  if (W.nU > 9 * GV_W) return HROM_E_INVALID;  // the fused row is limited to nU <= 68 anyway
+  gemv_gather_kernel<9, false, true><<<c->band_blocks, GV_T, 0, c->st>>>(
+      c->g, W, c->b.ring, c->rho_ref(), c->b.lists + (int64_t)L_B * c->g.N, c->b.counts + L_B, v,
+      c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1));
+  HROM_LAUNCH_CK();
+  ++c->nlaunch;
   return HROM_OK;
 }
 
