@@ -408,7 +408,13 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
   if (rebase) {
     prof_end(c, SEC_BASIS);
     prof_begin(c, SEC_REBASE);
-    if ((s = launch_mean(c, W, c->rho_ref())) != HROM_OK) return s;
+    // Gram shift rho := the newest snapshot (any fixed reference inside the window controls the
+    // cancellation of the centring algebra, G2; a slab-strided copy instead of a mean pass)
+    {
+      const size_t pitch = (size_t)c->g.nsr * TILE * sizeof(double);
+      HROM_CK(cudaMemcpy2DAsync(c->b.rho, pitch, c->b.ring + (int64_t)c->slot_of(k) * TILE, pitch,
+                                TILE * sizeof(double), (size_t)(c->g.Dp / TILE), cudaMemcpyDeviceToDevice, c->st));
+    }
     const int s0 = W.slot[0];
     // consecutive slots are contiguous in the pointer table (see hrom_create); the Gram is
     // written straight into the slot-indexed C through the slot table
