@@ -296,14 +296,6 @@ __global__ void eps_all_kernel(Geo g, const double* __restrict__ eps_elem, doubl
 }
 
 // out (rho or psi) = mean of the last w window slots
-__global__ void mean_kernel(Geo g, Win W, const double* __restrict__ ring, SRef out) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < g.D; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t se = sidx(SRef{nullptr, g.nsr}, e);
-    double s = 0.0;
-    for (int q = W.nU - W.w; q < W.nU; ++q) s += ring[(int64_t)W.slot[q] * TILE + se];
-    out.p[sidx(out, e)] = s / (double)W.w;
-  }
-}
 
 template <int NU>
 hrom_status launch_fill_t(hrom_ctx* c, const FillArgs& a, size_t smem) {
@@ -382,11 +374,5 @@ hrom_status launch_eps_all(hrom_ctx* c) {
   return HROM_OK;
 }
 
-hrom_status launch_mean(hrom_ctx* c, const Win& W, SRef out) {
-  mean_kernel<<<c->nsm * 8, 256, 0, c->st>>>(c->g, W, c->b.ring, out);
-  HROM_LAUNCH_CK();
-  ++c->nlaunch;
-  return HROM_OK;
-}
 
 }  // namespace hrom

@@ -1,5 +1,5 @@
-// filter.cu -- H7: residual-gated Shapiro seam filter (one cooperative kernel), plus the
-// window-Gram contributions of the seam-band DOFs once their values are final.
+// filter.cu -- H7: residual-gated Shapiro seam filter (one cooperative kernel).  The window-Gram
+// contributions of the seam-band DOFs (final values) are computed by band_gram_rows (linalg.cu).
 //
 // Paper: explicit Shapiro filters applied dimension by dimension,
 // zeroth-order boundary extrapolation, residual gate: keep filtered values only
@@ -280,64 +280,6 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
   }
 }
 
-// Gram-row contributions of the band DOFs (final values), partials after the fill blocks:
-// part[blk][s] = sum_e x_e (col_s(e) - rho_e), part[blk][nU] = sum_e x_e^2, x = v - rho.
-// Four threads per DOF, each owning every fourth window slot: up to 17 independent slab
-// loads in flight per thread (the loads are scattered: one 32-byte sector per slot and DOF).
-constexpr int BG_T = 256;
-constexpr int BG_Q = 4;                            // threads per DOF
-__global__ void __launch_bounds__(BG_T) band_gram_kernel(Geo g, Win W, const double* __restrict__ ring,
-                                                         const SRef rho, const SRef v,
-                                                         const int32_t* __restrict__ list,
-                                                         const int32_t* __restrict__ count, double* __restrict__ part) {
-  constexpr int SPT = 17;  // nU <= 68 (the fused Gram row is limited to fill_max_gram_slots())
-  __shared__ double red[BG_T / 32][BG_Q * SPT + 1];
-  const int nU = W.nU;
-  const int nb = *count;
-  const int64_t total = (int64_t)nb * g.c;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, q = lane & (BG_Q - 1);
-  const SRef slab{nullptr, g.nsr};
-  double acc[SPT];
-#pragma unroll
-  for (int j = 0; j < SPT; ++j) acc[j] = 0.0;
-  double self = 0.0;
-  const int64_t per_pass = (int64_t)gridDim.x * (BG_T / BG_Q);
-  for (int64_t t = (int64_t)blockIdx.x * (BG_T / BG_Q) + (threadIdx.x / BG_Q); t < total; t += per_pass) {
-    const int var = (int)(t / nb), idx = (int)(t - (int64_t)var * nb);
-    const int64_t e = (int64_t)var * g.N + list[idx];
-    const double r = rho.p[sidx(rho, e)];
-    const double x = v.p[sidx(v, e)] - r;
-    const int64_t se = sidx(slab, e);
-    double val[SPT];
-#pragma unroll
-    for (int j = 0; j < SPT; ++j) {
-      const int sl = q + BG_Q * j;
-      val[j] = sl < nU ? __ldg(ring + (int64_t)W.slot[sl] * TILE + se) : r;
-    }
-#pragma unroll
-    for (int j = 0; j < SPT; ++j) acc[j] += x * (val[j] - r);
-    if (q == 0) self += x * x;
-  }
-#pragma unroll
-  for (int j = 0; j < SPT; ++j) {
-    double y = acc[j];
-    y += __shfl_xor_sync(0xffffffffu, y, 4);
-    y += __shfl_xor_sync(0xffffffffu, y, 8);
-    y += __shfl_xor_sync(0xffffffffu, y, 16);
-    if (lane < BG_Q) red[warp][lane + BG_Q * j] = y;
-  }
-  for (int o = 16; o > 0; o >>= 1) self += __shfl_xor_sync(0xffffffffu, self, o);
-  if (lane == 0) red[warp][BG_Q * SPT] = self;
-  __syncthreads();
-  double* out = part + (int64_t)blockIdx.x * (nU + 1);
-  for (int sl = threadIdx.x; sl <= nU; sl += BG_T) {
-    const int col = sl < nU ? sl : BG_Q * SPT;
-    double y = 0.0;
-    for (int w8 = 0; w8 < BG_T / 32; ++w8) y += red[w8][col];
-    out[sl] = y;
-  }
-}
-
 }  // namespace
 
 hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F, uint8_t* kept_cells) {
@@ -376,16 +318,6 @@ hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F, uint8_t* kept_cells) {
   void* args[] = {&a};
   HROM_CK(cudaLaunchCooperativeKernel((void*)filter_kernel, dim3(c->filter_blocks), dim3(FT), args, FILTER_SMEM,
                                       c->st));
-  ++c->nlaunch;
-  return HROM_OK;
-}
-
-hrom_status launch_band_gram(hrom_ctx* c, const Win& W, SRef v) {
-  if (W.nU > 68) return HROM_E_INVALID;  // covered by the fused-row limit (fill_max_gram_slots)
-  band_gram_kernel<<<c->band_blocks, BG_T, 0, c->st>>>(c->g, W, c->b.ring, c->rho_ref(), v,
-                                                       c->b.lists + (int64_t)L_B * c->g.N, c->b.counts + L_B,
-                                                       c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1));
-  HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;
 }

@@ -235,8 +235,6 @@ hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot, const unsig
 hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_band,
                             const unsigned long long* esc = nullptr);
 hrom_status launch_eps_cells(hrom_ctx* c);
-hrom_status launch_mean(hrom_ctx* c, const Win& W, SRef out);
 // filter.cu
 hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F, uint8_t* kept_cells);
-hrom_status launch_band_gram(hrom_ctx* c, const Win& W, SRef v);
 }  // namespace hrom
