@@ -460,9 +460,11 @@ hrom_status hrom_sample(hrom_ctx* c, double fraction, const double* dev_eps, uin
   if (!(fraction > 0.0 && fraction <= 1.0)) return HROM_E_INVALID;
   const int64_t n_g = (int64_t)std::ceil(fraction * (double)c->g.N);
   hrom_status s;
+  // the deferred eigen-solve starts first on the side stream; the cooperative sampling kernel
+  // then runs on the other SMs (grid nsm - 1), so the eigen overlaps the sampling too
+  if ((s = flush_eigen(c)) != HROM_OK) return s;
   prof_begin(c, SEC_SAMPLE);
   if ((s = select_and_build(c, dev_eps ? dev_eps : c->b.eps, n_g)) != HROM_OK) return s;
-  if ((s = flush_eigen(c)) != HROM_OK) return s;
   prof_end(c, SEC_SAMPLE);
   c->sets_ready = true;
   if (dev_mask_out)

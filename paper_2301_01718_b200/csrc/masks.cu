@@ -608,7 +608,8 @@ hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long lon
   a.tdbg = c->b.dbg;
   if ((int64_t)16 * c->sets_blocks > c->b.blk_len) return HROM_E_INVALID;
   void* args[] = {&a};
-  HROM_CK(cudaLaunchCooperativeKernel((void*)sets_kernel, dim3(c->sets_blocks), dim3(ST_T), args, 0, c->st));
+  const int grid = c->basis_pending ? c->sets_blocks - 1 : c->sets_blocks;  // leave the eigen's SM
+  HROM_CK(cudaLaunchCooperativeKernel((void*)sets_kernel, dim3(grid), dim3(ST_T), args, 0, c->st));
   ++c->nlaunch;
   return HROM_OK;
 }
