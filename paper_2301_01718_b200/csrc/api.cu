@@ -285,6 +285,7 @@ hrom_status hrom_set_state(hrom_ctx* c, const double* any_q) {
   c->k = 0;
   c->last_hybrid = false;
   c->kinc_valid = false;
+  c->eps_sparse = false;
   c->basis_ready = c->sets_ready = c->gram_row_ready = false;
   c->rebase_k = -1000000;
   c->last_err_cell = -1;
@@ -388,6 +389,7 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
   prof_end(c, SEC_POS);
   c->k = kn;
   c->last_hybrid = true;
+  c->eps_sparse = true;  // eps: memset, then written on S-hat (fill) and kept band cells (filter)
   c->gram_row_ready = (c->P.gram_mode == 0);
   c->sets_ready = false;
   return HROM_OK;
@@ -450,6 +452,7 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
     ++c->nlaunch;
     if ((s = launch_fill(c, W, 2, plain(nullptr), plain(nullptr), false)) != HROM_OK) return s;
     if ((s = launch_eps_all(c)) != HROM_OK) return s;
+    c->eps_sparse = false;
   }
   return HROM_OK;
 }
@@ -576,6 +579,7 @@ hrom_status hrom_rebuild_basis(hrom_ctx* c, int64_t k, const uint32_t* any_mask_
   c->k = k;
   c->last_hybrid = false;
   c->kinc_valid = false;
+  c->eps_sparse = false;
   c->basis_ready = false;
   c->gram_row_ready = false;
   c->rebase_k = -1000000;

@@ -171,6 +171,7 @@ struct hrom_ctx {
   // the union whose newest snapshot is kinc_newest
   bool kinc_valid = false;
   int samples_since_gather = 99;  // samplings since the last gathered Gram (churn lists valid iff 1)
+  bool eps_sparse = false;   // the indicator is nonzero only on the T list (set by a hybrid step)
   int64_t kinc_newest = -1, kinc_rebase = -1;
   hrom::Win eig_win{};
   int slot_of(int64_t kk) const { return (int)(kk % nslots); }

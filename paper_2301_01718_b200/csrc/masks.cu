@@ -12,7 +12,7 @@
 namespace cg = cooperative_groups;
 
 namespace hrom {
-hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long long n_g);
+hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long long n_g, bool sparse = false);
 namespace {
 
 __device__ __forceinline__ int wrapi(int i, int n, int bc, bool* valid) {
@@ -110,6 +110,8 @@ struct SetsArgs {
   int32_t* idx;        // cell -> compact filter index
   int32_t* tab;        // stencil tables (14 N)
   long long* tdbg;     // debug timestamps [40..63]
+  const int32_t* cand; // nullable: sorted candidate cells for eps > 0 (T list of the current sets)
+  const int32_t* ncand;
 };
 
 __device__ __forceinline__ void sstamp(long long* t, int& i) {
@@ -254,8 +256,26 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
   // ================= select =================
   if (a.do_select) {
     const int64_t fw = (N + 31) / 32;
-    // A1: eps > 0 bitmap (flat words; one warp ballot per word, coalesced), zero S-hat, count
-    {
+    // A1: eps > 0 bitmap (flat words; one warp ballot per word, coalesced), zero S-hat, count.
+    // Sparse indicator (after a hybrid step eps is nonzero only on S-hat u B, i.e. the T list of
+    // the current sets): the candidates are that sorted list instead of all N cells.
+    const int ncand = a.cand ? __ldcg(a.ncand) : 0;
+    const int64_t cchunk = ((int64_t)ncand + G - 1) / G;
+    const int64_t c0 = min((int64_t)blockIdx.x * cchunk, (int64_t)ncand), c1 = min(c0 + cchunk, (int64_t)ncand);
+    if (a.cand) {
+      int mine = 0;
+      const int64_t tch = (c1 - c0 + blockDim.x - 1) / blockDim.x;
+      const int64_t t0 = min(c0 + tid * tch, c1), t1 = min(t0 + tch, c1);
+      for (int64_t t = t0; t < t1; ++t) mine += a.eps[__ldcg(a.cand + t)] > 0.0;
+      const BlockRange rs = thread_range(nw);
+      for (int64_t w = rs.w0; w < rs.w1; ++w) {
+        SPREV[w] = S[w];
+        S[w] = 0u;
+      }
+      int tot;
+      block_excl_scan(mine, &tot, sbuf);
+      if (tid == 0) a.blk[0 * G + blockIdx.x] = tot;
+    } else {
       const int64_t bchunk = (fw + G - 1) / G;
       const int64_t b0 = min((int64_t)blockIdx.x * bchunk, fw), b1 = min(b0 + bchunk, fw);
       const int lane = tid & 31, warp = tid >> 5;
@@ -290,7 +310,27 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
     grid.sync();
   sstamp(a.tdbg, ts);
     // A2: ordered compaction of eps > 0 -> (sel_cell, sel_val)
-    {
+    if (a.cand) {
+      int off, tot;
+      block_offset(a.blk, 0, &off, &tot, sbuf);
+      const int64_t tch = (c1 - c0 + blockDim.x - 1) / blockDim.x;
+      const int64_t t0 = min(c0 + tid * tch, c1), t1 = min(t0 + tch, c1);
+      int mine = 0;
+      for (int64_t t = t0; t < t1; ++t) mine += a.eps[__ldcg(a.cand + t)] > 0.0;
+      int btot;
+      int pos = off + block_excl_scan(mine, &btot, sbuf);
+      for (int64_t t = t0; t < t1; ++t) {
+        const int cell = __ldcg(a.cand + t);
+        const double e = a.eps[cell];
+        if (e > 0.0) {
+          a.sel_cell[pos] = cell;
+          a.sel_val[pos] = e;
+          ++pos;
+        }
+      }
+      if (blockIdx.x == 0 && tid == 0) a.counts[8] = tot;
+      for (int i = blockIdx.x * blockDim.x + tid; i < 2 * NBIN; i += G * blockDim.x) a.hist[i] = 0;
+    } else {
       const int64_t bchunk = (fw + G - 1) / G;
       const int64_t b0 = min((int64_t)blockIdx.x * bchunk, fw), b1 = min(b0 + bchunk, fw);
       int off, tot;
@@ -584,8 +624,10 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
 
 }  // namespace
 
-hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long long n_g) {
+hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long long n_g, bool sparse) {
   SetsArgs a{};
+  a.cand = sparse ? c->b.lists + (int64_t)L_T * c->g.N : nullptr;
+  a.ncand = c->b.counts + L_T;
   a.g = c->g;
   a.do_select = do_select ? 1 : 0;
   a.eps = eps;
@@ -637,7 +679,9 @@ hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S) {
 // top-n_g of eps > 0 -> S-hat (ties at the threshold by ascending cell), then build_sets.
 hrom_status select_and_build(hrom_ctx* c, const double* eps, int64_t n_g) {
   ++c->samples_since_gather;
-  return launch_sets(c, true, eps, (long long)n_g);
+  // the step's own indicator is nonzero only on S-hat u B (the T list): scan that list only
+  const bool sparse = eps == c->b.eps && c->eps_sparse;
+  return launch_sets(c, true, eps, (long long)n_g, sparse);
 }
 
 }  // namespace hrom
