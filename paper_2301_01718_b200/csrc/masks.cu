@@ -539,6 +539,10 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
     __syncthreads();
 #pragma unroll
     for (int m = 0; m < NSET; ++m) {
+      if (g.dim == 2 && (lk[m] == L_A2 || lk[m] == L_A1)) {  // 2-D stages read the bitmaps, not the lists
+        if (blockIdx.x == 0 && tid == 0) a.counts[lk[m]] = stot5[m];
+        continue;
+      }
       int pos = soff5[m];
       for (int k = 0; k < warp; ++k) pos += wc5[m][k];
       int32_t* L = a.lists + (int64_t)lk[m] * N;
