@@ -135,6 +135,13 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   g.dy = dim == 2 ? (grid->y1 - grid->y0) / ny : 1.0;
   g.gamma = gamma;
   g.cfl = cfl;
+  {
+    int ex = 0, ey = 0;
+    const bool px = std::frexp(g.dx, &ex) == 0.5, py = std::frexp(g.dy, &ey) == 0.5;
+    g.pow2 = (px && py) ? 1 : 0;
+    g.rdx = 1.0 / g.dx;
+    g.rdy = 1.0 / g.dy;
+  }
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev);

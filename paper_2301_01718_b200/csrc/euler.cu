@@ -102,7 +102,7 @@ __device__ __forceinline__ void cell_rhs(const Geo& g, const SRef q, int i, int 
   face_flux<DIM, 0, RECON>(Ux[R - (R == 2 ? 1 : 0)], Ux[R], Ux[R + 1], Ux[R + (R == 2 ? 2 : 1)], g.gamma, Fp);
   face_flux<DIM, 0, RECON>(Ux[0], Ux[R - 1], Ux[R], Ux[R + (R == 2 ? 1 : 0)], g.gamma, Fm);
 #pragma unroll
-  for (int v = 0; v < C; ++v) L[v] = -(Fp[v] - Fm[v]) / g.dx;
+  for (int v = 0; v < C; ++v) L[v] = -div_dx(g, Fp[v] - Fm[v]);
   if (DIM == 2) {
     double Uy[2 * R + 1][C];
 #pragma unroll
@@ -120,7 +120,7 @@ __device__ __forceinline__ void cell_rhs(const Geo& g, const SRef q, int i, int 
     face_flux<DIM, DIM - 1, RECON>(Uy[R - (R == 2 ? 1 : 0)], Uy[R], Uy[R + 1], Uy[R + (R == 2 ? 2 : 1)], g.gamma, Gp);
     face_flux<DIM, DIM - 1, RECON>(Uy[0], Uy[R - 1], Uy[R], Uy[R + (R == 2 ? 1 : 0)], g.gamma, Gm);
 #pragma unroll
-    for (int v = 0; v < C; ++v) L[v] = L[v] - (Gp[v] - Gm[v]) / g.dy;
+    for (int v = 0; v < C; ++v) L[v] = L[v] - div_dy(g, Gp[v] - Gm[v]);
   }
 }
 
@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(TX * TY) stage_tile_kernel(Geo g, int stage, c
   const int64_t n = (int64_t)j * g.nx + i;
 #pragma unroll
   for (int v = 0; v < C; ++v) {
-    double L = -(Fx[v][ty][tx + 1] - Fx[v][ty][tx]) / g.dx;
-    L = L - (Fy[v][ty + 1][tx] - Fy[v][ty][tx]) / g.dy;
+    double L = -div_dx(g, Fx[v][ty][tx + 1] - Fx[v][ty][tx]);
+    L = L - div_dy(g, Fy[v][ty + 1][tx] - Fy[v][ty][tx]);
     const int64_t e = v * g.N + n;
     const double un = qn.p[sidx(qn, e)];
     double r;
@@ -267,8 +267,8 @@ __global__ void __launch_bounds__(256) smax_kernel(Geo g, const SRef q, unsigned
     // the divided forms of the CFL rule (O7): dt matches the oracle's bit for bit
     const double p = pressure<DIM>(U, g.gamma - 1.0);
     const double cs = sqrt(g.gamma * p / U[0]);
-    double s = (fabs(U[1] / U[0]) + cs) / g.dx;
-    if (DIM == 2) s = s + (fabs(U[2] / U[0]) + cs) / g.dy;
+    double s = div_dx(g, fabs(U[1] / U[0]) + cs);
+    if (DIM == 2) s = s + div_dy(g, fabs(U[2] / U[0]) + cs);
     if (!(s <= m)) m = s;  // NaN sticks
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -319,8 +319,8 @@ __global__ void __launch_bounds__(256) positivity_kernel(Geo g, const SRef q, un
     const double p = pressure<DIM>(U, g.gamma - 1.0);
     if (!(U[0] > 0.0) || !(p > 0.0)) atomicMin(bad, (unsigned long long)n);
     const double cs = sqrt(g.gamma * p / U[0]);
-    double s = (fabs(U[1] / U[0]) + cs) / g.dx;
-    if (DIM == 2) s = s + (fabs(U[2] / U[0]) + cs) / g.dy;
+    double s = div_dx(g, fabs(U[1] / U[0]) + cs);
+    if (DIM == 2) s = s + div_dy(g, fabs(U[2] / U[0]) + cs);
     if (!(s <= m)) m = s;  // NaN sticks
   }
   for (int o = 16; o > 0; o >>= 1) {

@@ -60,6 +60,8 @@ struct Geo {
   int64_t N, D, Dp;                    // Dp: D rounded up to a multiple of TILE
   int64_t nsr;                         // slab slots per tile (w + 3)
   double dx, dy, gamma, cfl;
+  double rdx, rdy;  // 1/dx, 1/dy: used instead of the divisions only when dx, dy are powers of two
+  int pow2;         // (then x / dx == x * rdx bit for bit)
 };
 
 // Slot descriptor of the basis: union slots (oldest first), psi_prev = mean of the first w,
@@ -211,6 +213,8 @@ inline void prof_end(hrom_ctx* c, int sec) {
 }  // namespace hrom
 
 namespace hrom {
+__host__ __device__ __forceinline__ double div_dx(const Geo& g, double x) { return g.pow2 ? x * g.rdx : x / g.dx; }
+__host__ __device__ __forceinline__ double div_dy(const Geo& g, double x) { return g.pow2 ? x * g.rdy : x / g.dy; }
 // euler.cu
 hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override, int64_t kq);
 hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, const int32_t* list, int list_idx,
