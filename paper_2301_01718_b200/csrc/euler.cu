@@ -6,6 +6,7 @@
 // so the S-hat rows of a masked step are bitwise the rows of the full step (Eq. 7,
 // exact restriction, reading A9).  States are addressed through SRef (slab ring slot
 // or plain vector, internal.cuh).
+#include <algorithm>
 #include <cfloat>
 #include "internal.cuh"
 
@@ -166,90 +167,96 @@ constexpr int TX = 32, TY = 8, TH = 2;  // tile, halo (MUSCL radius)
 template <int RECON>
 __global__ void __launch_bounds__(TX * TY) stage_tile_kernel(Geo g, int stage, const SRef qn, const SRef qin,
                                                            const SRef out, const uint32_t* __restrict__ mask,
-                                                           const double* __restrict__ dtp) {
+                                                           const double* __restrict__ dtp,
+                                                           const int32_t* __restrict__ tiles,
+                                                           const int32_t* __restrict__ ntiles_p) {
   constexpr int C = 4, R = RECON;
   constexpr int SX = TX + 2 * TH, SY = TY + 2 * TH;
   __shared__ double U[C][SY][SX];        // cross region (corners unused)
   __shared__ double Fx[C][TY][TX + 1];   // x-face i - 1/2 of tile column i
   __shared__ double Fy[C][TY + 1][TX];   // y-face j - 1/2 of tile row j
+  __shared__ int any;
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int ntx = (g.nx + TX - 1) / TX;
-  const int bx = blockIdx.x % ntx, by = blockIdx.x / ntx;
-  const int i0 = bx * TX, j0 = by * TY;
-  const int i = i0 + tx, j = j0 + ty;
-  // active tile?
-  uint32_t myword = 0;
-  if (mask) {
-    __shared__ int any;
-    if (threadIdx.x == 0) any = 0;
-    __syncthreads();
-    if (tx == 0 && j < g.ny) {
-      myword = mask[(int64_t)j * g.wpr + bx];
-      if (myword) any = 1;
+  // tiles: persistent loop over the listed active tiles (masked stages), or one tile per block
+  const int ntiles = tiles ? *ntiles_p : (int)gridDim.x;
+  for (int it = blockIdx.x; it < ntiles; it += (tiles ? (int)gridDim.x : ntiles)) {
+    const int tile = tiles ? tiles[it] : it;
+    const int bx = tile % ntx, by = tile / ntx;
+    const int i0 = bx * TX, j0 = by * TY;
+    const int i = i0 + tx, j = j0 + ty;
+    // active for this stage's set?
+    uint32_t myword = 0;
+    if (mask) {
+      __syncthreads();  // U / Fx / Fy / any of the previous tile are consumed
+      if (threadIdx.x == 0) any = 0;
+      __syncthreads();
+      if (j < g.ny) myword = mask[(int64_t)j * g.wpr + bx];
+      if (tx == 0 && myword) any = 1;
+      __syncthreads();
+      if (!any) continue;  // uniform
+    }
+    // stage the cross region: rows j0-2 .. j0+9 over the tile columns, and the x-halo columns
+    for (int idx = threadIdx.x; idx < SY * SX; idx += TX * TY) {
+      const int ly = idx / SX, lx = idx % SX;
+      const bool xin = lx >= TH && lx < TH + TX, yin = ly >= TH && ly < TH + TY;
+      if (!xin && !yin) continue;  // corner
+      const int gi = wrap(i0 + lx - TH, g.nx, g.bc), gj = wrap(j0 + ly - TH, g.ny, g.bc);
+      const int64_t n = (int64_t)gj * g.nx + gi;
+#pragma unroll
+      for (int v = 0; v < C; ++v) U[v][ly][lx] = __ldg(qin.p + sidx(qin, v * g.N + n));
     }
     __syncthreads();
-    if (!any) return;
-    myword = (j < g.ny) ? mask[(int64_t)j * g.wpr + bx] : 0u;
-  }
-  // stage the cross region: rows j0-2 .. j0+9 over the tile columns, and the x-halo columns
-  for (int idx = threadIdx.x; idx < SY * SX; idx += TX * TY) {
-    const int ly = idx / SX, lx = idx % SX;
-    const bool xin = lx >= TH && lx < TH + TX, yin = ly >= TH && ly < TH + TY;
-    if (!xin && !yin) continue;  // corner
-    const int gi = wrap(i0 + lx - TH, g.nx, g.bc), gj = wrap(j0 + ly - TH, g.ny, g.bc);
-    const int64_t n = (int64_t)gj * g.nx + gi;
+    // x-faces: face f between local columns f-1 and f (f = 0..TX), rows 0..TY-1
+    for (int f = threadIdx.x; f < (TX + 1) * TY; f += TX * TY) {
+      const int fy = f / (TX + 1), fx = f % (TX + 1);
+      const int ly = fy + TH, lx = fx + TH;  // cell "b" (right of the face) in the staged region
+      double Uam[C], Ua[C], Ub[C], Ubp[C], F[C];
 #pragma unroll
-    for (int v = 0; v < C; ++v) U[v][ly][lx] = __ldg(qin.p + sidx(qin, v * g.N + n));
-  }
-  __syncthreads();
-  // x-faces: face f between local columns f-1 and f (f = 0..TX), rows 0..TY-1
-  for (int f = threadIdx.x; f < (TX + 1) * TY; f += TX * TY) {
-    const int fy = f / (TX + 1), fx = f % (TX + 1);
-    const int ly = fy + TH, lx = fx + TH;  // cell "b" (right of the face) in the staged region
-    double Uam[C], Ua[C], Ub[C], Ubp[C], F[C];
+      for (int v = 0; v < C; ++v) {
+        Uam[v] = U[v][ly][lx - (R == 2 ? 2 : 1)];
+        Ua[v] = U[v][ly][lx - 1];
+        Ub[v] = U[v][ly][lx];
+        Ubp[v] = U[v][ly][lx + (R == 2 ? 1 : 0)];
+      }
+      face_flux<2, 0, RECON>(Uam, Ua, Ub, Ubp, g.gamma, F);
 #pragma unroll
-    for (int v = 0; v < C; ++v) {
-      Uam[v] = U[v][ly][lx - (R == 2 ? 2 : 1)];
-      Ua[v] = U[v][ly][lx - 1];
-      Ub[v] = U[v][ly][lx];
-      Ubp[v] = U[v][ly][lx + (R == 2 ? 1 : 0)];
+      for (int v = 0; v < C; ++v) Fx[v][fy][fx] = F[v];
     }
-    face_flux<2, 0, RECON>(Uam, Ua, Ub, Ubp, g.gamma, F);
+    // y-faces: face f between local rows f-1 and f (f = 0..TY), columns 0..TX-1
+    for (int f = threadIdx.x; f < (TY + 1) * TX; f += TX * TY) {
+      const int fy = f / TX, fx = f % TX;
+      const int ly = fy + TH, lx = fx + TH;
+      double Uam[C], Ua[C], Ub[C], Ubp[C], F[C];
 #pragma unroll
-    for (int v = 0; v < C; ++v) Fx[v][fy][fx] = F[v];
-  }
-  // y-faces: face f between local rows f-1 and f (f = 0..TY), columns 0..TX-1
-  for (int f = threadIdx.x; f < (TY + 1) * TX; f += TX * TY) {
-    const int fy = f / TX, fx = f % TX;
-    const int ly = fy + TH, lx = fx + TH;
-    double Uam[C], Ua[C], Ub[C], Ubp[C], F[C];
+      for (int v = 0; v < C; ++v) {
+        Uam[v] = U[v][ly - (R == 2 ? 2 : 1)][lx];
+        Ua[v] = U[v][ly - 1][lx];
+        Ub[v] = U[v][ly][lx];
+        Ubp[v] = U[v][ly + (R == 2 ? 1 : 0)][lx];
+      }
+      face_flux<2, 1, RECON>(Uam, Ua, Ub, Ubp, g.gamma, F);
 #pragma unroll
-    for (int v = 0; v < C; ++v) {
-      Uam[v] = U[v][ly - (R == 2 ? 2 : 1)][lx];
-      Ua[v] = U[v][ly - 1][lx];
-      Ub[v] = U[v][ly][lx];
-      Ubp[v] = U[v][ly + (R == 2 ? 1 : 0)][lx];
+      for (int v = 0; v < C; ++v) Fy[v][fy][fx] = F[v];
     }
-    face_flux<2, 1, RECON>(Uam, Ua, Ub, Ubp, g.gamma, F);
+    __syncthreads();
+    if (i < g.nx && j < g.ny && (!mask || ((myword >> tx) & 1u))) {
+      const double dt = *dtp;
+      const int64_t n = (int64_t)j * g.nx + i;
 #pragma unroll
-    for (int v = 0; v < C; ++v) Fy[v][fy][fx] = F[v];
-  }
-  __syncthreads();
-  if (i >= g.nx || j >= g.ny) return;
-  if (mask && !((myword >> tx) & 1u)) return;
-  const double dt = *dtp;
-  const int64_t n = (int64_t)j * g.nx + i;
-#pragma unroll
-  for (int v = 0; v < C; ++v) {
-    double L = -div_dx(g, Fx[v][ty][tx + 1] - Fx[v][ty][tx]);
-    L = L - div_dy(g, Fy[v][ty + 1][tx] - Fy[v][ty][tx]);
-    const int64_t e = v * g.N + n;
-    const double un = qn.p[sidx(qn, e)];
-    double r;
-    if (stage == 1) r = un + dt * L;
-    else if (stage == 2) r = 0.75 * un + 0.25 * (U[v][ty + TH][tx + TH] + dt * L);
-    else r = (1.0 / 3.0) * un + (2.0 / 3.0) * (U[v][ty + TH][tx + TH] + dt * L);
-    out.p[sidx(out, e)] = r;
+      for (int v = 0; v < C; ++v) {
+        double L = -div_dx(g, Fx[v][ty][tx + 1] - Fx[v][ty][tx]);
+        L = L - div_dy(g, Fy[v][ty + 1][tx] - Fy[v][ty][tx]);
+        const int64_t e = v * g.N + n;
+        const double un = qn.p[sidx(qn, e)];
+        double r;
+        if (stage == 1) r = un + dt * L;
+        else if (stage == 2) r = 0.75 * un + 0.25 * (U[v][ty + TH][tx + TH] + dt * L);
+        else r = (1.0 / 3.0) * un + (2.0 / 3.0) * (U[v][ty + TH][tx + TH] + dt * L);
+        out.p[sidx(out, e)] = r;
+      }
+    }
+    if (!tiles) break;
   }
 }
 
@@ -376,10 +383,15 @@ hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, co
   int32_t* ec = c->b.ireg + 15;
   if (g.dim == 2 && !run_if) {
     // tile kernel: every face once; masked stages restrict to the set's bitmap (A1, A2, T)
+    // masked stages: a persistent grid over the active tiles of A1 (listed by the sets kernel;
+    // A1 >= A2 >= T), each tile re-checked against its own stage's bitmap
     const uint32_t* mask = list ? c->b.masks + (int64_t)list_idx * c->mwords : nullptr;
     const int tiles = ((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
-    if (g.recon == 1) stage_tile_kernel<1><<<tiles, TX * TY, 0, c->st>>>(g, stage, qn, qin, out, mask, c->b.dreg);
-    else stage_tile_kernel<2><<<tiles, TX * TY, 0, c->st>>>(g, stage, qn, qin, out, mask, c->b.dreg);
+    const int32_t* tl = list ? c->b.lists + (int64_t)L_A2 * g.N : nullptr;  // tile list (2-D)
+    const int32_t* tn = c->b.counts + 10;
+    const int grid = list ? std::min(tiles, 8 * c->nsm) : tiles;
+    if (g.recon == 1) stage_tile_kernel<1><<<grid, TX * TY, 0, c->st>>>(g, stage, qn, qin, out, mask, c->b.dreg, tl, tn);
+    else stage_tile_kernel<2><<<grid, TX * TY, 0, c->st>>>(g, stage, qn, qin, out, mask, c->b.dreg, tl, tn);
   } else if (g.dim == 1) {
     if (g.recon == 1) stage_kernel<1, 1><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg, run_if, ec);
     else stage_kernel<1, 2><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg, run_if, ec);

@@ -491,6 +491,25 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
   const int lk[NSET] = {L_S, L_B, L_T, L_A2, L_A1, L_ADD, L_REM};
   __shared__ int wc5[NSET][32];
   __shared__ int soff5[NSET], stot5[NSET];
+  // active 32 x 8 tiles of A1 (2-D): tile (bx, by) <-> words A1[(8 by + r) * wpr + bx], r < 8
+  const int ntile = g.dim == 2 ? g.wpr * ((g.ny + 7) / 8) : 0;
+  const int64_t tchunk = ((int64_t)ntile + G - 1) / G;
+  const int64_t tb0 = min((int64_t)blockIdx.x * tchunk, (int64_t)ntile), tb1 = min(tb0 + tchunk, (int64_t)ntile);
+  const int64_t ttch = (tb1 - tb0 + blockDim.x - 1) / blockDim.x;
+  const int64_t tt0 = min(tb0 + tid * ttch, tb1), tt1 = min(tt0 + ttch, tb1);
+  auto tile_active = [&](int64_t t) -> bool {
+    const int bx = (int)(t % g.wpr), by = (int)(t / g.wpr);
+    uint32_t o = 0u;
+    for (int r = 0; r < 8 && 8 * by + r < g.ny; ++r) o |= __ldcg(a.masks + (int64_t)M_A1 * mw + (int64_t)(8 * by + r) * g.wpr + bx);
+    return o != 0u;
+  };
+  int tmine = 0, texcl = 0;
+  if (g.dim == 2) {
+    for (int64_t t = tt0; t < tt1; ++t) tmine += tile_active(t);
+    int tbt;
+    texcl = block_excl_scan(tmine, &tbt, sbuf);
+    if (tid == 0) a.blk[15 * G + blockIdx.x] = tbt;
+  }
   {
     int64_t ww0, ww1;
     warp_range(rb0, rb1, &ww0, &ww1);
@@ -567,6 +586,15 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
         }
       }
       if (blockIdx.x == 0 && tid == 0) a.counts[lk[m]] = stot5[m];
+    }
+    if (g.dim == 2) {  // the tile list (into the A2 list, unused in 2-D)
+      int off, tot;
+      block_offset(a.blk, 15, &off, &tot, sbuf);
+      int pos = off + texcl;
+      int32_t* TL = a.lists + (int64_t)L_A2 * N;
+      for (int64_t t = tt0; t < tt1; ++t)
+        if (tile_active(t)) TL[pos++] = (int32_t)t;
+      if (blockIdx.x == 0 && tid == 0) a.counts[10] = tot;
     }
   }
   grid.sync();
