@@ -176,8 +176,9 @@ int64_t hrom_launch_count(const hrom_ctx* ctx);
  * [10..14] eigen-solve phase timings (kcycles), [15] positivity escalations;
  * [16 + l] the size of cell list l (0 S-hat, 1 seam band B, 2 T, 3 A2, 4 A1, 5 filter halo). */
 hrom_status hrom_debug_counters(hrom_ctx* ctx, int32_t* any_out, int32_t n);
-/* Synchronises and copies n <= 64 device timestamps (ns, %globaltimer) written by the last
- * seam-filter launch: [0] start, [1] after the compaction prologue, [2 + s] after sweep s. */
+/* Synchronises and copies n <= 128 device timestamps (ns, %globaltimer) written by the last
+ * launches: seam filter [0] start, [1] after the compaction prologue, [2 + s] after sweep s;
+ * sets kernel [40 + phase]; LSQ solve [64 + phase] (only while profiling is enabled). */
 hrom_status hrom_debug_timers(hrom_ctx* ctx, int64_t* host_out, int32_t n);
 
 #ifdef __cplusplus

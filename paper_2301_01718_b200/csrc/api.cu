@@ -201,7 +201,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   A(dalloc(&b.ireg, 16));
   A(dalloc(&b.dreg, 16));
   A(dalloc(&b.ureg, 4));
-  A(dalloc(&b.dbg, 64));
+  A(dalloc(&b.dbg, 128));
   A(dalloc(&b.sel_val, g.N));
   A(dalloc(&b.sel_cell, g.N));
   b.blk_len = std::max<int64_t>(8 * ((c->mwords + 255) / 256 + 2) + (g.N + 1023) / 1024 + 16, 16 * (int64_t)c->nsm + 64);
@@ -704,7 +704,7 @@ hrom_status hrom_debug_counters(hrom_ctx* c, int32_t* any_out, int32_t n) {
 }
 
 hrom_status hrom_debug_timers(hrom_ctx* c, int64_t* host_out, int32_t n) {
-  if (!c || !host_out || n < 0 || n > 64) return HROM_E_INVALID;
+  if (!c || !host_out || n < 0 || n > 128) return HROM_E_INVALID;
   basis_join(c);
   HROM_CK(cudaStreamSynchronize(c->st));
   HROM_CK(cudaMemcpy(host_out, c->b.dbg, n * sizeof(int64_t), cudaMemcpyDeviceToHost));

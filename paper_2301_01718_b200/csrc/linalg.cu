@@ -495,27 +495,182 @@ __global__ void __launch_bounds__(512) basis_kernel(const double* __restrict__ C
 // Fast path: Cholesky G = L L^T.  lambda_min >= 1 / trace(G^-1) = 1 / ||L^-1||_F^2 and
 // lambda_max <= ||G||_F, so when 1 / ||L^-1||_F^2 >= 1e-10 ||G||_F no eigenvalue is within
 // two orders of magnitude of the cut and y = G^-1 g exactly; otherwise the eigen route (eig.cuh).
-constexpr int SV_T = 256;
+// debug timestamps (thread 0 of block 0; t nullable)
+__device__ __forceinline__ void sstamp(long long* t, int& i) {
+  if (t && blockIdx.x == 0 && threadIdx.x == 0 && i < 16) {
+    long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    t[i] = gt;
+  }
+  ++i;
+}
+
+constexpr int SV_T = 256, SV_W = SV_T / 32;
 struct SolveLayout {
-  size_t ks, as, t, mp, mc, lm, li, vec, eig, total;  // offsets in doubles
-  bool ks_smem;                                       // K in smem (else the global scratch)
+  size_t ks, rs, as, t, mp, mc, lm, vec, eig, total;  // offsets in doubles
+  int mode;  // 2: R staged + K in smem, 1: K in smem (R read from global), 0: K in the global scratch
 };
-__host__ __device__ inline SolveLayout solve_layout(int w, int r, bool ks_smem) {
+// As and T are stored with the odd leading dimension w + 1, the Cholesky factor with r + 1
+// (conflict-free walks along either index)
+__host__ __device__ inline SolveLayout solve_layout(int w, int r, int mode) {
   SolveLayout S;
-  S.ks_smem = ks_smem;
+  S.mode = mode;
   S.ks = 0;
-  S.as = S.ks + (ks_smem ? (size_t)(w + 1) * (w + 1) : 0);
-  S.t = S.as + (size_t)w * r;
-  // T (w x r) is dead once G is formed: the Cholesky factor and its inverse (r x r each) reuse it
-  const size_t treg = (size_t)w * r > (size_t)2 * r * r ? (size_t)w * r : (size_t)2 * r * r;
+  S.rs = S.ks + (mode >= 1 ? (size_t)(w + 1) * (w + 1) : 0);
+  S.as = S.rs + (mode == 2 ? (size_t)(w + 2) * (w + 2) : 0);
+  S.t = S.as + (size_t)(w + 1) * r;
+  // T (w x r) is dead once G is formed: the Cholesky factor reuses it
+  const size_t treg = (size_t)(w + 1) * r > (size_t)r * (r + 1) ? (size_t)(w + 1) * r : (size_t)r * (r + 1);
   S.lm = S.t;
-  S.li = S.t + (size_t)r * r;
   S.mp = S.t + treg;
   S.mc = S.mp + (kMaxW + 2);
   S.vec = S.mc + (kMaxW + 2);           // rhs, y, u, misc: 4 * kMaxSlots
-  S.eig = S.vec + 4 * kMaxSlots;
+  S.eig = S.vec + 4 * kMaxSlots + 2 * SV_W;
   S.total = S.eig;                       // + EigLayout(r).doubles
   return S;
+}
+
+// out(m, n) = sum_p X[m ldx + p] Y[n ldy + p] over p < P, m < M, n < N (shared memory operands).
+// Register blocks of RM rows (stride ceil(M / RM): consecutive threads walk consecutive X rows,
+// conflict-free for odd ldx) x CN columns (warp-uniform: broadcast Y loads); RM x CN independent
+// FMA chains per thread.  Only blocks with some n >= m when UPPER.
+template <int RM, int CN, bool UPPER, class F>
+__device__ __forceinline__ void smem_gemm_nt(const double* X, int ldx, const double* Y, int ldy, int M, int N, int P,
+                                             F store) {
+  const int mb = (M + RM - 1) / RM, nb = (N + CN - 1) / CN;
+  for (int blk = threadIdx.x; blk < mb * nb; blk += blockDim.x) {
+    const int m0 = blk % mb, n0 = CN * (blk / mb);
+    if (UPPER && n0 + CN - 1 < m0) continue;
+    const double* xr[RM];
+    const double* yr[CN];
+#pragma unroll
+    for (int q = 0; q < RM; ++q) xr[q] = X + (int64_t)min(m0 + q * mb, M - 1) * ldx;
+#pragma unroll
+    for (int c = 0; c < CN; ++c) yr[c] = Y + (int64_t)min(n0 + c, N - 1) * ldy;
+    double acc[RM][CN];
+#pragma unroll
+    for (int q = 0; q < RM; ++q)
+#pragma unroll
+      for (int c = 0; c < CN; ++c) acc[q][c] = 0.0;
+    for (int p = 0; p < P; ++p) {
+      double xv[RM];
+#pragma unroll
+      for (int q = 0; q < RM; ++q) xv[q] = xr[q][p];
+#pragma unroll
+      for (int c = 0; c < CN; ++c) {
+        const double yv = yr[c][p];
+#pragma unroll
+        for (int q = 0; q < RM; ++q) acc[q][c] += xv[q] * yv;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RM; ++q)
+#pragma unroll
+      for (int c = 0; c < CN; ++c)
+        if (m0 + q * mb < M && n0 + c < N) store(m0 + q * mb, n0 + c, acc[q][c]);
+  }
+}
+
+// One warp, in place: the n x n SPD matrix M (leading dimension ld, odd) -> its lower Cholesky
+// factor L (right-looking; lanes own rows i = lane, lane + 32).  Uniformly false when a pivot is
+// not positive.  Kept as loops: this code runs once per launch, so an unrolled body would be
+// instruction-fetch bound.
+__device__ bool chol_warp(double* M, int ld, int n, double* dinv) {
+  const int lane = threadIdx.x & 31;
+  for (int j = 0; j < n; ++j) {
+    const double d = M[j * ld + j];
+    if (!(d > 0.0)) return false;
+    const double ljj = sqrt(d), rj = 1.0 / ljj;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      if (i > j) M[i * ld + j] *= rj;
+      else if (i == j) {
+        M[j * ld + j] = ljj;
+        dinv[j] = rj;
+      }
+    }
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      if (i <= j) continue;
+      const double lij = M[i * ld + j];
+      double* Mi = M + i * ld;
+      int k = j + 1;
+      for (; k + 3 <= i; k += 4) {  // loads first: four independent updates in flight
+        const double a0 = M[k * ld + j], a1 = M[(k + 1) * ld + j], a2 = M[(k + 2) * ld + j], a3 = M[(k + 3) * ld + j];
+        const double b0 = Mi[k], b1 = Mi[k + 1], b2 = Mi[k + 2], b3 = Mi[k + 3];
+        Mi[k] = b0 - lij * a0;
+        Mi[k + 1] = b1 - lij * a1;
+        Mi[k + 2] = b2 - lij * a2;
+        Mi[k + 3] = b3 - lij * a3;
+      }
+      for (; k <= i; ++k) Mi[k] -= lij * M[k * ld + j];
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+// Forward substitution L x = e_c for the columns c = warp, warp + SV_W, ... (< n: columns of
+// L^-1, only their squared norms are kept) and c = n (x = L^-1 g -> u).  Lanes own rows
+// lane, lane + 32; the CPW columns of a warp advance together (independent chains).
+constexpr int SV_CPW = (kMaxR + 1 + SV_W - 1) / SV_W;
+__device__ double trinv_cols(const double* Lm, int ld, int n, const double* dinv, const double* g, double* u) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double x[SV_CPW][2];
+#pragma unroll
+  for (int m = 0; m < SV_CPW; ++m) {
+    const int c = warp + SV_W * m;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = lane + 32 * h;
+      x[m][h] = c < n ? (i == c ? 1.0 : 0.0) : (c == n && i < n ? g[i] : 0.0);
+    }
+  }
+  for (int k = 0; k < n; ++k) {  // (the columns c > k are still zero above the diagonal)
+    const double rk = dinv[k];
+    const double l0 = lane > k && lane < n ? Lm[lane * ld + k] : 0.0;
+    const double l1 = lane + 32 > k && lane + 32 < n ? Lm[(lane + 32) * ld + k] : 0.0;
+#pragma unroll
+    for (int m = 0; m < SV_CPW; ++m) {
+      if (warp + SV_W * m > n) break;
+      const double xk = __shfl_sync(0xffffffffu, k < 32 ? x[m][0] : x[m][1], k & 31) * rk;
+      if (lane == (k & 31)) {
+        if (k < 32) x[m][0] = xk;
+        else x[m][1] = xk;
+      }
+      x[m][0] -= l0 * xk;
+      x[m][1] -= l1 * xk;
+    }
+  }
+  double tr = 0.0;
+#pragma unroll
+  for (int m = 0; m < SV_CPW; ++m) {
+    const int c = warp + SV_W * m;
+    if (c < n) tr += x[m][0] * x[m][0] + x[m][1] * x[m][1];
+    if (c == n) {
+      u[lane] = x[m][0];
+      if (lane + 32 < n) u[lane + 32] = x[m][1];
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+  return tr;
+}
+
+// One warp: back substitution L^T y = u (lanes own rows k = lane, lane + 32)
+__device__ void trsolve_t_warp(const double* Lm, int ld, int n, const double* dinv, const double* u, double* y) {
+  const int lane = threadIdx.x & 31;
+  double v0 = lane < n ? u[lane] : 0.0, v1 = lane + 32 < n ? u[lane + 32] : 0.0;
+  for (int i = n - 1; i >= 0; --i) {
+    const double yi = __shfl_sync(0xffffffffu, i < 32 ? v0 : v1, i & 31) * dinv[i];
+    if (lane == (i & 31)) {
+      if (i < 32) v0 = yi;
+      else v1 = yi;
+    }
+    if (lane < i) v0 -= Lm[i * ld + lane] * yi;
+    if (lane + 32 < i) v1 -= Lm[i * ld + lane + 32] * yi;
+  }
+  if (lane < n) y[lane] = v0;
+  if (lane + 32 < n) y[lane + 32] = v1;
 }
 
 __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ R, Win W, int r,
@@ -523,23 +678,25 @@ __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ 
                                                      double cut, double* __restrict__ y_out,
                                                      double* __restrict__ c_out, int32_t* __restrict__ status,
                                                      double* __restrict__ gfac, bool fac_smem,
-                                                     double* __restrict__ Kg, bool ks_smem) {
+                                                     double* __restrict__ Kg, int mode, long long* tdbg) {
   extern __shared__ double sm[];
+  int ts = 0;
+  sstamp(tdbg, ts);
   const int re = *reffp;
-  const int w = W.w, nU = W.nU, xoff = nU - w, ldr = nU + 1, ldk = w + 1, ldl = re;
+  const int w = W.w, nU = W.nU, xoff = nU - w, ldk = w + 1, lda = w + 1, ldl = re | 1;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  const SolveLayout S = solve_layout(w, r, ks_smem);
-  double* Ks = ks_smem ? sm + S.ks : Kg;
-  double* As = sm + S.as;  // A[j * w + i]
-  double* T = sm + S.t;
+  const SolveLayout S = solve_layout(w, r, mode);
+  double* Ks = mode >= 1 ? sm + S.ks : Kg;
+  double* As = sm + S.as;  // As[j * lda + i] = A[j * w + i]
+  double* T = sm + S.t;    // T[j * lda + i]
   double* mp = sm + S.mp;
   double* mc = sm + S.mc;
-  double* Lm = sm + S.lm;
-  double* Li = sm + S.li;
+  double* Lm = sm + S.lm;  // Lm[i * ldl + k]
   double* rhs = sm + S.vec;
   double* y = rhs + kMaxSlots;
   double* u = y + kMaxSlots;
   double* misc = u + kMaxSlots;
+  double* wtr = misc + kMaxSlots;  // per-warp partials
   EigLayout L = eig_layout(re > 0 ? re : 1, re > 0 ? re : 1);
   L.fac_smem = fac_smem;  // the host sized the smem for r >= r_eff: its choice is safe
   const int ldn = L.ldn;
@@ -548,23 +705,50 @@ __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ 
   __shared__ double gm[3];
   __shared__ int s_fast;
   // ---- centring of R into K (same algebra as the window Gram, A14) ----
-  for (int i = tid; i < w * re; i += nt) As[i] = A[(i / w) * w + (i % w)];
-  for (int a = tid; a <= nU; a += nt) {
+  int ldr = nU + 1;
+  const double* Rr = R;
+  for (int i = tid; i < w * re; i += nt) As[(i / w) * lda + (i % w)] = A[i];
+  if (mode == 2) {  // stage R (coalesced, all loads independent)
+    double* Rs = sm + S.rs;
+    for (int i = tid; i < ldr * ldr; i += nt) Rs[i] = R[i];
+    Rr = Rs;
+    __syncthreads();
+  }
+  for (int a = warp; a <= nU; a += SV_W) {  // warp per row of R
     double sp = 0.0, sc = 0.0;
-    for (int q = 0; q < w; ++q) sp += R[a * ldr + q];
-    for (int q = xoff; q < nU; ++q) sc += R[a * ldr + q];
-    mp[a] = sp / (double)w;
-    mc[a] = sc / (double)w;
+    for (int q = lane; q < nU; q += 32) {
+      const double v = Rr[a * ldr + q];
+      if (q < w) sp += v;
+      if (q >= xoff) sc += v;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      sp += __shfl_xor_sync(0xffffffffu, sp, o);
+      sc += __shfl_xor_sync(0xffffffffu, sc, o);
+    }
+    if (lane == 0) {
+      mp[a] = sp / (double)w;
+      mc[a] = sc / (double)w;
+    }
   }
   __syncthreads();
-  if (tid == 0) {
+  sstamp(tdbg, ts);
+  if (warp == 0) {
     double pp = 0.0, pc = 0.0, cc = 0.0;
-    for (int q = 0; q < w; ++q) pp += mp[q];
-    for (int q = 0; q < w; ++q) pc += mc[q];
-    for (int q = xoff; q < nU; ++q) cc += mc[q];
-    gm[0] = pp / (double)w;
-    gm[1] = pc / (double)w;
-    gm[2] = cc / (double)w;
+    for (int q = lane; q < w; q += 32) {
+      pp += mp[q];
+      pc += mc[q];
+      cc += mc[xoff + q];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      pp += __shfl_xor_sync(0xffffffffu, pp, o);
+      pc += __shfl_xor_sync(0xffffffffu, pc, o);
+      cc += __shfl_xor_sync(0xffffffffu, cc, o);
+    }
+    if (lane == 0) {
+      gm[0] = pp / (double)w;
+      gm[1] = pc / (double)w;
+      gm[2] = cc / (double)w;
+    }
   }
   __syncthreads();
   for (int idx = tid; idx < ldk * ldk; idx += nt) {
@@ -572,98 +756,71 @@ __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ 
     double v;
     if (i < w && j < w) {
       const int a = xoff + i, b = xoff + j;
-      v = ((R[a * ldr + b] - mp[a]) - mp[b]) + gm[0];
+      v = ((Rr[a * ldr + b] - mp[a]) - mp[b]) + gm[0];
     } else if (i < w || j < w) {
       const int a = xoff + (i < w ? i : j);
-      v = ((R[a * ldr + nU] - mc[a]) - mp[nU]) + gm[1];
+      v = ((Rr[a * ldr + nU] - mc[a]) - mp[nU]) + gm[1];
     } else {
-      v = ((R[nU * ldr + nU] - mc[nU]) - mc[nU]) + gm[2];
+      v = ((Rr[nU * ldr + nU] - mc[nU]) - mc[nU]) + gm[2];
     }
     Ks[i * ldk + j] = v;
   }
   __syncthreads();
+  sstamp(tdbg, ts);
   // ---- T = K_XX A, g = A^T K_Xb, G = A^T T ----
-  for (int idx = tid; idx < w * re; idx += nt) {
-    const int i = idx % w, j = idx / w;
-    double s = 0.0;
-    for (int p = 0; p < w; ++p) s += Ks[i * ldk + p] * As[j * w + p];
-    T[j * w + i] = s;
-  }
+  smem_gemm_nt<2, 4, false>(Ks, ldk, As, lda, w, re, w, [&](int i, int j, double v) { T[j * lda + i] = v; });
   for (int j = tid; j < re; j += nt) {
     double s = 0.0;
-    for (int p = 0; p < w; ++p) s += As[j * w + p] * Ks[p * ldk + w];
+    for (int p = 0; p < w; ++p) s += As[j * lda + p] * Ks[p * ldk + w];
     rhs[j] = s;
   }
   __syncthreads();
+  sstamp(tdbg, ts);
+  smem_gemm_nt<1, 4, true>(As, lda, T, lda, re, re, w, [&](int i, int j, double v) {
+    if (j >= i) {
+      G[i * ldn + j] = v;
+      G[j * ldn + i] = v;
+    }
+  });
+  __syncthreads();
+  sstamp(tdbg, ts);
+  // ---- fast path: Cholesky G = L L^T + trace(G^-1) bound ----
+  double gf = 0.0;  // ||G||_F^2
   for (int idx = tid; idx < re * re; idx += nt) {
-    const int i = idx / re, j = idx % re;
-    if (j < i) continue;
-    double s = 0.0;
-    for (int p = 0; p < w; ++p) s += As[i * w + p] * T[j * w + p];
-    G[i * ldn + j] = s;
-    G[j * ldn + i] = s;
+    const double v = G[(idx / re) * ldn + idx % re];
+    Lm[(idx / re) * ldl + idx % re] = v;
+    gf += v * v;
+  }
+  for (int o = 16; o > 0; o >>= 1) gf += __shfl_xor_sync(0xffffffffu, gf, o);
+  if (lane == 0) wtr[SV_W + warp] = gf;
+  __syncthreads();
+  if (warp == 0) {
+    const bool f = re > 0 && chol_warp(Lm, ldl, re, misc);
+    if (lane == 0) s_fast = f ? 1 : 0;
   }
   __syncthreads();
-  for (int idx = tid; idx < re * re; idx += nt) Lm[idx] = G[(idx / re) * ldn + idx % re];  // T is dead now
-  __syncthreads();
-  // ---- fast path: Cholesky + trace(G^-1) bound ----
-  bool ok = re > 0;
-  for (int j = 0; j < re && ok; ++j) {
-    const double djj = Lm[j * ldl + j];
-    if (!(djj > 0.0)) {
-      ok = false;  // uniform: every thread read the same value
-      break;
-    }
-    const double ljj = sqrt(djj);
-    for (int i = j + 1 + tid; i < re; i += nt) Lm[i * ldl + j] /= ljj;
-    __syncthreads();
-    if (tid == 0) Lm[j * ldl + j] = ljj;
-    const int m = re - j - 1;
-    for (int idx = tid; idx < m * m; idx += nt) {
-      const int i = j + 1 + idx / m, k = j + 1 + idx % m;
-      if (k <= i) Lm[i * ldl + k] -= Lm[i * ldl + j] * Lm[k * ldl + j];
-    }
-    __syncthreads();
-  }
+  bool ok = s_fast != 0;
+  sstamp(tdbg, ts);
   if (ok) {
-    // Li = L^-1 (lower), one thread per column
-    for (int cc = tid; cc < re; cc += nt) {
-      for (int i = 0; i < cc; ++i) Li[i * ldl + cc] = 0.0;
-      for (int i = cc; i < re; ++i) {
-        double s = (i == cc) ? 1.0 : 0.0;
-        for (int k = cc; k < i; ++k) s -= Lm[i * ldl + k] * Li[k * ldl + cc];
-        Li[i * ldl + cc] = s / Lm[i * ldl + i];
-      }
-    }
+    const double tr = trinv_cols(Lm, ldl, re, misc, rhs, u);  // trace(G^-1) = ||L^-1||_F^2, u = L^-1 g
+    if (lane == 0) wtr[warp] = tr;
     __syncthreads();
     if (warp == 0) {
-      double tr = 0.0, gf = 0.0;
-      for (int i = lane; i < re; i += 32)
-        for (int k = 0; k < re; ++k) {
-          tr += Li[i * ldl + k] * Li[i * ldl + k];
-          gf += G[i * ldn + k] * G[i * ldn + k];
-        }
+      double t = lane < SV_W ? wtr[lane] : 0.0;
+      gf = lane < SV_W ? wtr[SV_W + lane] : 0.0;
       for (int o = 16; o > 0; o >>= 1) {
-        tr += __shfl_xor_sync(0xffffffffu, tr, o);
+        t += __shfl_xor_sync(0xffffffffu, t, o);
         gf += __shfl_xor_sync(0xffffffffu, gf, o);
       }
-      if (lane == 0) s_fast = (tr > 0.0 && isfinite(tr) && 1.0 / tr >= 1e-10 * sqrt(gf)) ? 1 : 0;
+      const bool f = t > 0.0 && isfinite(t) && 1.0 / t >= 1e-10 * sqrt(gf);
+      if (f) trsolve_t_warp(Lm, ldl, re, misc, u, y);
+      if (lane == 0) s_fast = f ? 1 : 0;
     }
     __syncthreads();
     ok = s_fast != 0;
   }
+  sstamp(tdbg, ts);
   if (ok) {
-    for (int i = tid; i < re; i += nt) {
-      double s = 0.0;
-      for (int k = 0; k <= i; ++k) s += Li[i * ldl + k] * rhs[k];
-      u[i] = s;
-    }
-    __syncthreads();
-    for (int k = tid; k < re; k += nt) {
-      double s = 0.0;
-      for (int i = k; i < re; ++i) s += Li[i * ldl + k] * u[i];
-      y[k] = s;
-    }
     if (tid == 0) {
       *status = 0;
       status[7] = 0;  // fast path
@@ -689,10 +846,11 @@ __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ 
     }
     __syncthreads();
   }
+  sstamp(tdbg, ts);
   for (int i = tid; i < kMaxR; i += nt) y_out[i] = (i < re) ? y[i] : 0.0;
   for (int i = tid; i < w; i += nt) {
     double s = 0.0;
-    for (int j = 0; j < re; ++j) s += As[j * w + i] * y[j];
+    for (int j = 0; j < re; ++j) s += As[j * lda + i] * y[j];
     c_out[i] = s;
   }
 }
@@ -926,12 +1084,14 @@ hrom_status band_gram_rows(hrom_ctx* c, const Win& W, SRef v) {
 hrom_status small_solve(hrom_ctx* c) {
   // the solve reads r_eff on the device: size the workspace for the largest possible (r)
   const EigLayout L = eig_layout(c->r, c->r);
-  SolveLayout S = solve_layout(c->win.w, c->r, true);
-  if ((S.total * sizeof(double) + L.bytes) > 220 * 1024) S = solve_layout(c->win.w, c->r, false);  // wide windows
+  SolveLayout S = solve_layout(c->win.w, c->r, 2);
+  if ((S.total * sizeof(double) + L.bytes) > 220 * 1024) S = solve_layout(c->win.w, c->r, 1);  // wide windows
+  if ((S.total * sizeof(double) + L.bytes) > 220 * 1024) S = solve_layout(c->win.w, c->r, 0);
   const size_t smem = S.total * sizeof(double) + L.bytes;
   HROM_CK(cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   solve_kernel<<<1, SV_T, smem, c->st>>>(c->b.eigV, c->win, c->r, c->b.A, c->b.ireg, c->P.lsq_rel_cutoff, c->b.y,
-                                         c->b.cvec, c->b.ireg + 2, c->b.eigA, L.fac_smem, c->b.K, S.ks_smem);
+                                         c->b.cvec, c->b.ireg + 2, c->b.eigA, L.fac_smem, c->b.K, S.mode,
+                                         c->prof ? c->b.dbg + 64 : nullptr);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;
