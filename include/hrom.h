@@ -65,6 +65,9 @@ typedef struct {
   int32_t gather_mode;       /* 0: gathered Gram of the S-hat rows updated from the previous
                                 step (S-hat churn rows + the new snapshot and HDM columns),
                                 1: recomputed over all S-hat rows every step (G7) */
+  int32_t full_period;       /* z of Algorithm 1: step k is a full HDM step when
+                                k+1 <= w or k mod z = 0, and the basis update + sampling after
+                                step k is skipped when (k+1) mod z = 0; <= 0: z = infinity */
 } hrom_params;
 
 /* Create a context for one grid.  cuda_stream: a cudaStream_t (NULL = legacy default).
@@ -122,9 +125,21 @@ hrom_status hrom_reconstruct(hrom_ctx* ctx, const uint32_t* dev_mask, double* de
 hrom_status hrom_filter(hrom_ctx* ctx, const uint32_t* dev_mask, double* dev_v, const double* dev_F,
                         uint8_t* dev_kept_out);
 
-/* One step of Algorithm 1 (explicit, z = infinity): full step while k+1 <= w,
- * hybrid step afterwards, then update_basis + sample while k >= w-1. */
+/* One step k of Algorithm 1 (explicit variant) with z = params.full_period:
+ * a full step when k+1 <= w or k mod z = 0, else a hybrid step; then, when k >= w-1 and
+ * (k+1) mod z != 0, update_basis + sample.  After a full step k >= w the sampling indicator
+ * is the projection error of gamma_k on the new basis (the bootstrap rule A19 applied at k;
+ * DESIGN.md G8).  A skipped update owes the window-Gram row of gamma_k, computed at the next
+ * update.  dev_count_out (nullable, device int32): |S-hat| used by this step (N for a full
+ * step), for the sampling averages s-bar, s-bar* of P:715-727. */
 hrom_status hrom_step(hrom_ctx* ctx, double dt_override);
+hrom_status hrom_step_ex(hrom_ctx* ctx, double dt_override, int32_t* dev_count_out);
+
+/* Relative L1 error of Algorithm 1: e = sum |a - b| / sum |b| over the D entries
+ * of two device states (uniform cell volumes; the per-cell 1-norm over the c variables).
+ * Enqueued on the context stream; synchronises and writes the value to *host_out.
+ * Fixed-order reductions: bitwise reproducible. */
+hrom_status hrom_rel_l1_error(hrom_ctx* ctx, const double* dev_a, const double* dev_b, double* host_out);
 
 /* Synchronise the stream; returns latched device errors. */
 hrom_status hrom_sync(hrom_ctx* ctx);

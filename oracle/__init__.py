@@ -82,6 +82,7 @@ def lib():
             "orc_run_create": (C.c_void_p, [P(Grid), P(Params), d]),
             "orc_run_destroy": (None, [C.c_void_p]),
             "orc_run_step": (i32, [C.c_void_p, C.c_double]),
+            "orc_run_set_full_period": (None, [C.c_void_p, i32]),
             "orc_run_k": (i64, [C.c_void_p]),
             "orc_run_state": (None, [C.c_void_p, d]),
             "orc_run_mask": (None, [C.c_void_p, u8]),
@@ -290,7 +291,7 @@ def seam_filter(wl, v, F, mask_S):
 
 
 class Run:
-    """Algorithm 1 (explicit, z = inf) driver of the oracle."""
+    """Algorithm 1 (explicit; z = wl.z, 0 = infinity) driver of the oracle."""
 
     def __init__(self, wl, q0):
         self.wl = wl
@@ -298,6 +299,8 @@ class Run:
         self._p = params_of(wl)
         q0 = _c(q0)
         self.h = lib().orc_run_create(C.byref(self._g), C.byref(self._p), _d(q0))
+        if getattr(wl, "z", 0) > 0:
+            lib().orc_run_set_full_period(self.h, int(wl.z))
 
     def __del__(self):
         h, self.h = getattr(self, "h", None), None

@@ -1,9 +1,11 @@
-// driver.cpp -- oracle: Algorithm 1, explicit variant, z = infinity.
+// driver.cpp -- oracle: Algorithm 1, explicit variant, full-HDM period z.
 // TEST INFRASTRUCTURE ONLY (see oracle.h).
 //
-// Schedule (reading A20): full steps for k+1 <= w; hybrid steps after.
-// Refresh after every step k >= w-1:
-//   G_{k+1} from the indicator (fraction mode A18; bootstrap A19 at k = w-1),
+// Schedule: full steps for k+1 <= w or k mod z = 0 (z = infinity by default, A20);
+// hybrid steps otherwise.
+// Refresh after every step k >= w-1 with (k+1) mod z != 0:
+//   G_{k+1} from the indicator (fraction mode A18; bootstrap A19 at k = w-1;
+//   after a full step k >= w the same projection rule with Phi_{k+1}, psi_{k+1}, reading G8),
 //   Phi_{k+1} = POD_r([gamma_{k-w+1} - psi_k, ..., gamma_k - psi_k])   (lagged A14)
 //   psi_{k+1} = mean(gamma_{k-w+1..k})
 // Hybrid step k (O10-O13):
@@ -33,6 +35,7 @@ struct orc_run {
   double dt = 0.0;
   int64_t kept = 0;
   int32_t sweeps[3] = {0, 0, 0};
+  int32_t z = 0;  // full-HDM period; <= 0: infinity
   orc_run(const orc_grid* gg, const orc_params* pp) : g(*gg), p(*pp), G(gg) {}
 };
 
@@ -80,6 +83,24 @@ void reconstruct(const orc_run* R, const std::vector<double>& y, int64_t n, doub
   }
 }
 
+// eps_n = sum_v [(I - Phi_{k+1} Phi_{k+1}^T)(gamma_k - psi_{k+1})]^2_{v,n}: the projection
+// error of the newest snapshot on the basis just built (A19 at k = w-1; G8 after full steps)
+void projection_indicator(orc_run* R) {
+  const int64_t N = R->G.N, D = R->G.D;
+  std::vector<double> d(D);
+  const auto& last = R->snaps.back();
+  for (int64_t e = 0; e < D; ++e) d[e] = last[e] - R->psi[e];
+  for (int i = 0; i < R->reff; ++i) {
+    const double c = dot(R->Phi.data() + (int64_t)i * D, d.data(), D);
+    for (int64_t e = 0; e < D; ++e) d[e] -= c * R->Phi[(int64_t)i * D + e];
+  }
+  for (int64_t n = 0; n < N; ++n) {
+    double e2 = 0.0;
+    for (int v = 0; v < R->G.c; ++v) e2 += d[v * N + n] * d[v * N + n];
+    R->eps[n] = e2;
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -104,8 +125,8 @@ int32_t orc_run_step(orc_run* R, double dt_override) {
   R->dt = (dt_override > 0.0) ? dt_override : orc_dt(&R->g, prev.data());
   std::vector<double> gam(D);
   int32_t kind = 0;
-  if (k + 1 <= w) {
-    orc_full_step(&R->g, prev.data(), R->dt, gam.data());  // P:558
+  if (k + 1 <= w || (R->z > 0 && k % R->z == 0)) {
+    orc_full_step(&R->g, prev.data(), R->dt, gam.data());  // P:557-558
     std::fill(R->mask_used.begin(), R->mask_used.end(), 1);
   } else {
     kind = 1;
@@ -173,32 +194,25 @@ int32_t orc_run_step(orc_run* R, double dt_override) {
   R->snaps.push_back(std::move(gam));
   while ((int)R->snaps.size() > w + 1) R->snaps.pop_front();
   R->k = k;
+  if (R->z > 0 && (k + 1) % R->z == 0) return kind;  // no refresh before a full step
   if (k == w - 1) {
     // offset bootstrap: psi_{w-1} = mean(gamma_0..gamma_{w-1})
     const std::vector<double> psi0 = mean_of(R->snaps, R->snaps.size() - w, w, D);
     refresh_basis(R, psi0);
-    // bootstrap indicator (A19): eps = sum_v [(I - Phi Phi^T)(gamma_{w-1} - psi_w)]^2
-    std::vector<double> d(D);
-    const auto& last = R->snaps.back();
-    for (int64_t e = 0; e < D; ++e) d[e] = last[e] - R->psi[e];
-    for (int i = 0; i < R->reff; ++i) {
-      const double c = dot(R->Phi.data() + (int64_t)i * D, d.data(), D);
-      for (int64_t e = 0; e < D; ++e) d[e] -= c * R->Phi[(int64_t)i * D + e];
-    }
-    for (int64_t n = 0; n < N; ++n) {
-      double e2 = 0.0;
-      for (int v = 0; v < G.c; ++v) e2 += d[v * N + n] * d[v * N + n];
-      R->eps[n] = e2;
-    }
+    projection_indicator(R);  // bootstrap indicator (A19)
     orc_select(R->eps.data(), N, orc_n_g(R->p.f, N), R->mask_next.data());
   } else if (k >= w) {
-    // psi_k = mean(gamma_{k-w..k-1}) (lagged centring, A14)
+    // psi_k = mean(gamma_{k-w..k-1}) (lagged centring, A14; by its formula also
+    // when the refresh after step k-1 was skipped, reading G8)
     const std::vector<double> psik = mean_of(R->snaps, 0, w, D);
     refresh_basis(R, psik);
+    if (kind == 0) projection_indicator(R);  // after a full step (finite z): reading G8
     orc_select(R->eps.data(), N, orc_n_g(R->p.f, N), R->mask_next.data());
   }
   return kind;
 }
+
+void orc_run_set_full_period(orc_run* R, int32_t z) { R->z = z; }
 
 int64_t orc_run_k(const orc_run* R) { return R->k; }
 void orc_run_state(const orc_run* R, double* q) { std::copy(R->snaps.back().begin(), R->snaps.back().end(), q); }

@@ -94,13 +94,15 @@ void orc_shapiro_1d(const double* line, int32_t n, int32_t order, int32_t period
 int64_t orc_seam_filter(const orc_grid* g, const orc_params* p, double* v, const double* F,
                         const uint8_t* mask_S, uint8_t* kept_out, int32_t* sweeps_out);
 
-/* ---- Algorithm 1, explicit variant, z = infinity (O1-O16) ---- */
+/* ---- Algorithm 1, explicit variant (O1-O16), z = infinity unless set ---- */
 typedef struct orc_run orc_run;
 orc_run* orc_run_create(const orc_grid* g, const orc_params* p, const double* q0);
 void orc_run_destroy(orc_run* R);
 /* one step k -> k+1.  dt_override <= 0 uses the CFL rule.  returns 0 full, 1 hybrid,
  * 2 hybrid escalated to full (positivity). */
 int32_t orc_run_step(orc_run* R, double dt_override);
+/* full-HDM period z of Algorithm 1; <= 0: infinity (the default) */
+void orc_run_set_full_period(orc_run* R, int32_t z);
 int64_t orc_run_k(const orc_run* R);
 void orc_run_state(const orc_run* R, double* q);             /* gamma_k */
 void orc_run_mask(const orc_run* R, uint8_t* m);             /* S-hat for the NEXT step */

@@ -19,16 +19,84 @@ int fill_max_gram_slots();
 namespace {
 
 __global__ void zvec_kernel(const double* __restrict__ A, const double* __restrict__ lam,
-                            const int32_t* __restrict__ reffp, int w, double* __restrict__ z) {
-  // z = e_{w-1} - V_r V_r^T e_{w-1}, V_r[:, j] = A[:, j] sqrt(lam_j)  (bootstrap indicator, A19)
+                            const int32_t* __restrict__ reffp, int w, double am, double* __restrict__ z) {
+  // projection indicator (A19 at k = w-1; G8 after a full step k >= w): gamma_k - psi_{k+1} =
+  // X alpha with alpha = e_{w-1} - am 1 (am = 0 at the bootstrap, where psi_{w-1} = psi_w;
+  // am = 1/w for the lagged centring, k >= w), and Phi Phi^T X alpha = X V_r V_r^T alpha, so
+  // the residual is X z with z = alpha - V_r V_r^T alpha, V_r[:, j] = A[:, j] sqrt(lam_j)
   const int re = *reffp;
+  __shared__ double t[kMaxR];
+  for (int j = threadIdx.x; j < re; j += blockDim.x) {  // t_j = sqrt(lam_j) A[:, j]^T alpha
+    const double sl = sqrt(lam[j]);
+    double sum = 0.0;
+    for (int i = 0; i < w; ++i) sum += A[j * w + i];
+    t[j] = A[j * w + (w - 1)] * sl - am * (sum * sl);
+  }
+  __syncthreads();
   for (int i = threadIdx.x; i < w; i += blockDim.x) {
     double s = 0.0;
-    for (int j = 0; j < re; ++j) {
-      const double sl = sqrt(lam[j]);
-      s += (A[j * w + i] * sl) * (A[j * w + (w - 1)] * sl);
+    for (int j = 0; j < re; ++j) s += (A[j * w + i] * sqrt(lam[j])) * t[j];
+    z[i] = ((i == w - 1 ? 1.0 : 0.0) - am) - s;
+  }
+}
+
+__global__ void set_i32_kernel(int32_t* p, int32_t v) { *p = v; }
+
+// relative L1 error: per-block partial sums over a fixed grid-stride assignment,
+// then one block sums the partials in a fixed tree order (bitwise reproducible)
+__global__ void __launch_bounds__(256) l1_partial_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                                         int64_t n, double* __restrict__ part) {
+  __shared__ double s0[8], s1[8];
+  double num = 0.0, den = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double bv = b[i];
+    num += fabs(a[i] - bv);
+    den += fabs(bv);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    num += __shfl_xor_sync(0xffffffffu, num, o);
+    den += __shfl_xor_sync(0xffffffffu, den, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s0[threadIdx.x >> 5] = num;
+    s1[threadIdx.x >> 5] = den;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      x += s0[k];
+      y += s1[k];
     }
-    z[i] = (i == w - 1 ? 1.0 : 0.0) - s;
+    part[blockIdx.x] = x;
+    part[gridDim.x + blockIdx.x] = y;
+  }
+}
+
+__global__ void __launch_bounds__(1024) l1_final_kernel(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  __shared__ double s0[32], s1[32];
+  double x = 0.0, y = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    x += part[i];
+    y += part[nb + i];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    x += __shfl_xor_sync(0xffffffffu, x, o);
+    y += __shfl_xor_sync(0xffffffffu, y, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s0[threadIdx.x >> 5] = x;
+    s1[threadIdx.x >> 5] = y;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < 32; ++k) {
+      a += s0[k];
+      b += s1[k];
+    }
+    out[0] = a;
+    out[1] = b;
   }
 }
 
@@ -208,6 +276,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   A(dalloc(&b.blk, b.blk_len));
   A(dalloc(&b.hist, 3 * 2048));
   A(dalloc(&b.fstat, c->filter_blocks));
+  A(dalloc(&b.l1part, 2 * kL1Blocks));
   A(dalloc(&b.fcnt, c->filter_blocks));
   A(dalloc(&b.colptr, 2 * kMaxSlots));
   A(dalloc(&b.slot_tab, 2 * kMaxSlots));
@@ -258,7 +327,7 @@ void hrom_destroy(hrom_ctx* c) {
   Bufs& b = c->b;
   void* ptrs[] = {b.ring, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
                   b.kept, b.fidx, b.ftab, b.fcur, b.fF, b.C, b.part, b.gpart, b.K, b.Khi, b.Klo, b.Rd, b.vpart, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
-                  b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.fstat, b.fcnt, (void*)b.colptr, b.slot_tab};
+                  b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.fstat, b.l1part, b.fcnt, (void*)b.colptr, b.slot_tab};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete c;
@@ -291,6 +360,8 @@ hrom_status hrom_set_state(hrom_ctx* c, const double* any_q) {
   HROM_CK(cudaMemsetAsync(c->b.ureg + 1, 0xff, sizeof(unsigned long long), c->st));
   c->k = 0;
   c->last_hybrid = false;
+  c->full_since_update = false;
+  c->n_owed = 0;
   c->kinc_valid = false;
   c->eps_sparse = false;
   c->basis_ready = c->sets_ready = c->gram_row_ready = false;
@@ -322,6 +393,7 @@ hrom_status hrom_full_step(hrom_ctx* c, double dt_override, double* dev_dt_out) 
   prof_end(c, SEC_FULL);
   c->k = kn;
   c->last_hybrid = false;
+  c->full_since_update = true;
   c->gram_row_ready = false;
   c->sets_ready = false;
   return HROM_OK;
@@ -433,6 +505,17 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
     prof_end(c, SEC_REBASE);
     prof_begin(c, SEC_BASIS);
     c->rebase_k = k;
+  } else if (c->n_owed > 0) {
+    // rows owed by skipped updates (finite z) and this step's row (a full step: a skip
+    // at k-1 means k mod z = 0), each against the whole new window (covers the pairs between them)
+    for (int i = 0; i < c->n_owed; ++i) {
+      const int64_t kk = c->owed_rows[i];
+      if (kk <= k - w || kk >= k) continue;
+      if ((s = launch_gram_row(c, W, c->slot_of(kk))) != HROM_OK) return s;
+      if ((s = reduce_gram_row(c, W, c->slot_of(kk), false)) != HROM_OK) return s;
+    }
+    if ((s = launch_gram_row(c, W, c->slot_of(k))) != HROM_OK) return s;
+    if ((s = reduce_gram_row(c, W, c->slot_of(k), false)) != HROM_OK) return s;
   } else if (!c->gram_row_ready) {
     if ((s = launch_gram_row(c, c->win, c->slot_of(k))) != HROM_OK) return s;
     if ((s = reduce_gram_row(c, c->win, c->slot_of(k), false)) != HROM_OK) return s;
@@ -452,9 +535,12 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
   c->win = W;
   c->basis_ready = true;
   c->gram_row_ready = false;
-  if (k == w - 1) {  // bootstrap indicator (reading A19)
+  c->n_owed = 0;
+  const bool proj = k == w - 1 || c->full_since_update;
+  c->full_since_update = false;
+  if (proj) {  // projection indicator: bootstrap (reading A19), or after a full step k >= w (G8)
     basis_join(c);
-    zvec_kernel<<<1, 128, 0, c->st>>>(c->b.A, c->b.lam, c->b.ireg, w, c->b.zvec);
+    zvec_kernel<<<1, 128, 0, c->st>>>(c->b.A, c->b.lam, c->b.ireg, w, k == w - 1 ? 0.0 : 1.0 / w, c->b.zvec);
     HROM_LAUNCH_CK();
     ++c->nlaunch;
     if ((s = launch_fill(c, W, 2, plain(nullptr), plain(nullptr), false)) != HROM_OK) return s;
@@ -532,18 +618,59 @@ hrom_status hrom_filter(hrom_ctx* c, const uint32_t* dev_mask, double* dev_v, co
   return HROM_OK;
 }
 
-hrom_status hrom_step(hrom_ctx* c, double dt_override) {
+hrom_status hrom_step_ex(hrom_ctx* c, double dt_override, int32_t* dev_count_out) {
   if (!c) return HROM_E_INVALID;
   if (c->k < 0) return HROM_E_STATE;
   const int64_t kn = c->k + 1;
+  const int64_t z = c->P.full_period;
+  // Algorithm 1 line P:557: full HDM step while k+1 <= w or k mod z = 0
+  const bool full = (kn + 1 <= c->w) || (z > 0 && kn % z == 0);
   hrom_status s;
-  if (kn + 1 <= c->w) s = hrom_full_step(c, dt_override, nullptr);
-  else s = hrom_hybrid_step(c, nullptr, dt_override, nullptr);
+  if (full) {
+    s = hrom_full_step(c, dt_override, nullptr);
+    if (s == HROM_OK && dev_count_out) {
+      set_i32_kernel<<<1, 1, 0, c->st>>>(dev_count_out, (int32_t)c->g.N);
+      HROM_LAUNCH_CK();
+      ++c->nlaunch;
+    }
+  } else {
+    s = hrom_hybrid_step(c, nullptr, dt_override, nullptr);
+    if (s == HROM_OK && dev_count_out)
+      HROM_CK(cudaMemcpyAsync(dev_count_out, c->b.counts + L_S, sizeof(int32_t), cudaMemcpyDeviceToDevice, c->st));
+  }
   if (s != HROM_OK) return s;
   if (kn >= c->w - 1) {
-    if ((s = hrom_update_basis(c)) != HROM_OK) return s;
-    if ((s = hrom_sample(c, c->P.sample_fraction, nullptr, nullptr, nullptr, nullptr)) != HROM_OK) return s;
+    if (z > 0 && (kn + 1) % z == 0) {
+      // no basis update / sampling before a full step; the window-Gram row of
+      // gamma_kn is owed to the next update (only the last w can still be in a window)
+      if (c->n_owed == 4) {
+        for (int i = 0; i < 3; ++i) c->owed_rows[i] = c->owed_rows[i + 1];
+        c->n_owed = 3;
+      }
+      c->owed_rows[c->n_owed++] = kn;
+      c->full_since_update = false;  // the next update follows the next (full) step
+    } else {
+      if ((s = hrom_update_basis(c)) != HROM_OK) return s;
+      if ((s = hrom_sample(c, c->P.sample_fraction, nullptr, nullptr, nullptr, nullptr)) != HROM_OK) return s;
+    }
   }
+  return HROM_OK;
+}
+
+hrom_status hrom_step(hrom_ctx* c, double dt_override) { return hrom_step_ex(c, dt_override, nullptr); }
+
+hrom_status hrom_rel_l1_error(hrom_ctx* c, const double* dev_a, const double* dev_b, double* host_out) {
+  if (!c || !dev_a || !dev_b || !host_out) return HROM_E_INVALID;
+  const int nb = std::min<int64_t>(kL1Blocks, std::max<int64_t>(1, (c->g.D + 255) / 256));
+  l1_partial_kernel<<<nb, 256, 0, c->st>>>(dev_a, dev_b, c->g.D, c->b.l1part);
+  HROM_LAUNCH_CK();
+  l1_final_kernel<<<1, 1024, 0, c->st>>>(c->b.l1part, nb, c->b.dreg + 8);
+  HROM_LAUNCH_CK();
+  c->nlaunch += 2;
+  double r[2];
+  HROM_CK(cudaMemcpyAsync(r, c->b.dreg + 8, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  HROM_CK(cudaStreamSynchronize(c->st));
+  *host_out = r[0] / r[1];
   return HROM_OK;
 }
 
@@ -585,6 +712,8 @@ hrom_status hrom_rebuild_basis(hrom_ctx* c, int64_t k, const uint32_t* any_mask_
   HROM_CK(cudaMemsetAsync(c->b.ureg + 1, 0xff, sizeof(unsigned long long), c->st));
   c->k = k;
   c->last_hybrid = false;
+  c->full_since_update = false;
+  c->n_owed = 0;
   c->kinc_valid = false;
   c->eps_sparse = false;
   c->basis_ready = false;

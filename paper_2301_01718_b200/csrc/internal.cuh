@@ -53,6 +53,7 @@ __host__ __device__ __forceinline__ SRef plain(const double* p) { return SRef{co
 constexpr int kMaxW = 128;           // largest window supported (config 5)
 constexpr int kMaxSlots = kMaxW + 2; // ring slots
 constexpr int kMaxR = 64;
+constexpr int kL1Blocks = 1024;  // relative-L1 partial sums
 
 // Geometry passed by value to kernels.
 struct Geo {
@@ -124,6 +125,7 @@ struct Bufs {
   int32_t* hist = nullptr;     // 3 x 2048 radix histograms
   // filter stats per block
   double* fstat = nullptr;
+  double* l1part = nullptr;   // 2 * kL1Blocks partial sums (relative L1 error)
   int32_t* fcnt = nullptr;
   const double** colptr = nullptr;  // device array of column pointers (Gram)
   int32_t* slot_tab = nullptr;      // slot_tab[i] = i mod nslots
@@ -145,6 +147,11 @@ struct hrom_ctx {
   bool sets_ready = false;   // S-hat_{k+1} sets built
   bool gram_row_ready = false;
   int64_t rebase_k = -1000000;
+  // Algorithm 1 with finite z: the last step was a full step (the update after it sets the
+  // projection indicator, G8); window-Gram rows owed by skipped updates
+  bool full_since_update = false;
+  int64_t owed_rows[4] = {0, 0, 0, 0};
+  int n_owed = 0;
   hrom::Win win{};           // window of the current basis
   int fill_blocks = 0;       // max grid of the fill kernel (Gram-row partial slots)
   int fill_grid = 0;         // grid of the last fill launch

@@ -38,7 +38,7 @@ class Params(C.Structure):
                 ("filter_max_sweeps", C.c_int32), ("filter_eps", C.c_double),
                 ("eig_rel_cutoff", C.c_double), ("lsq_rel_cutoff", C.c_double),
                 ("sample_fraction", C.c_double), ("gram_mode", C.c_int32), ("rebase_period", C.c_int32),
-                ("gather_mode", C.c_int32)]
+                ("gather_mode", C.c_int32), ("full_period", C.c_int32)]
 
 
 # every entry point of include/hrom.h with its ctypes signature
@@ -55,6 +55,8 @@ _SIGS = {
     "hrom_reconstruct": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "hrom_filter": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "hrom_step": (C.c_int, [_VP, C.c_double]),
+    "hrom_step_ex": (C.c_int, [_VP, C.c_double, _VP]),
+    "hrom_rel_l1_error": (C.c_int, [_VP, _VP, _VP, C.POINTER(C.c_double)]),
     "hrom_sync": (C.c_int, [_VP]),
     "hrom_error_cell": (C.c_int64, [_VP]),
     "hrom_step_index": (C.c_int64, [_VP]),
@@ -148,7 +150,7 @@ class HybridROM:
     """One hrom_ctx: an explicit hybrid-snapshot AROM on one grid, on the current CUDA device."""
 
     def __init__(self, wl, stream: Optional[torch.cuda.Stream] = None, gram_mode: int = 0,
-                 rebase_period: int = 0, gather_mode: int = 0):
+                 rebase_period: int = 0, gather_mode: int = 0, full_period: Optional[int] = None):
         if not torch.cuda.is_available():
             raise RuntimeError("libhrom needs a CUDA device (B200, sm_100a); no CPU fallback exists")
         self.lib = load_library()
@@ -157,7 +159,8 @@ class HybridROM:
         g = Grid(wl.dim, wl.nx, wl.ny if wl.dim == 2 else 1, wl.x0, wl.x1, wl.y0, wl.y1, wl.bc, wl.recon)
         fo = (C.c_int32 * 3)(*(list(wl.filter_orders) + [0, 0, 0])[:3])
         p = Params(wl.w, wl.r, wl.h, wl.W, fo, len(wl.filter_orders), wl.filter_max_sweeps, wl.filter_eps,
-                   wl.eig_rel_cutoff, wl.lsq_rel_cutoff, wl.f, gram_mode, rebase_period, gather_mode)
+                   wl.eig_rel_cutoff, wl.lsq_rel_cutoff, wl.f, gram_mode, rebase_period, gather_mode,
+                   getattr(wl, "z", 0) if full_period is None else full_period)
         h = C.c_void_p()
         _ck(self.lib.hrom_create(C.byref(g), wl.gamma, wl.cfl, C.byref(p), C.c_void_p(self.stream.cuda_stream),
                                  C.byref(h)), "hrom_create")
@@ -210,8 +213,21 @@ class HybridROM:
                kept_out: Optional[torch.Tensor] = None):
         _ck(self.lib.hrom_filter(self.h, _ptr(mask), _ptr(v), _ptr(F), _ptr(kept_out)), "hrom_filter")
 
-    def step(self, dt: float = 0.0):
-        _ck(self.lib.hrom_step(self.h, dt), "hrom_step")
+    def step(self, dt: float = 0.0, count_out: Optional[torch.Tensor] = None):
+        """One step of Algorithm 1; count_out (device int32, 1 element): |S-hat| used (N if full)."""
+        if count_out is None:
+            _ck(self.lib.hrom_step(self.h, dt), "hrom_step")
+        else:
+            assert count_out.dtype == torch.int32 and count_out.is_cuda
+            _ck(self.lib.hrom_step_ex(self.h, dt, _ptr(count_out)), "hrom_step_ex")
+
+    def rel_l1_error(self, a: torch.Tensor, b: torch.Tensor) -> float:
+        """e = sum|a - b| / sum|b| over the D entries, on the device."""
+        assert a.dtype == b.dtype == torch.float64 and a.numel() == b.numel() == self.wl.D
+        out = C.c_double()
+        _ck(self.lib.hrom_rel_l1_error(self.h, _ptr(a.contiguous()), _ptr(b.contiguous()), C.byref(out)),
+            "hrom_rel_l1_error")
+        return out.value
 
     def sync(self):
         code = self.lib.hrom_sync(self.h)

@@ -96,6 +96,7 @@ class Workload:
     filter_eps: float = 1e-2
     eig_rel_cutoff: float = 1e-8
     lsq_rel_cutoff: float = 1e-12
+    z: int = 0             # full-HDM period of Algorithm 1; 0 = infinity (A20)
 
     @property
     def c(self) -> int:

@@ -509,3 +509,94 @@ def test_incremental_gathered_gram_matches_full(inputs, cfg):
     a.sync()
     b.sync()
     assert worst <= 1e-12, worst
+
+
+# ---- Algorithm 1 with a finite full-HDM period z ----
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_z1_is_the_full_hdm_bitwise(inputs, cfg):
+    """z = 1 makes every step a full HDM step, bitwise equal to hrom_full_step."""
+    wl = inputs.config(cfg, z=1)
+    q0 = dev(inputs.initial_condition(wl))
+    a, b = H.HybridROM(wl), H.HybridROM(wl)
+    a.set_state(q0)
+    b.set_state(q0)
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for _ in range(wl.w + 6):
+        a.step(count_out=cnt)
+        b.full_step()
+        assert int(cnt.item()) == wl.N
+        assert torch.equal(a.get_state(), b.get_state())
+    a.sync()
+    b.sync()
+
+
+def test_trajectory_finite_z_config2(orc, inputs):
+    """Config 2 with z = 4 (w = 32): the bootstrap refresh is skipped ((w) mod 4 = 0), step 32
+    is full, refreshes after full steps use the projection indicator (G8), the refresh before
+    each full step is skipped and its window-Gram row is owed to the next update.  Step by step
+    the GPU state and S-hat agree with the oracle, and the per-step sample counts are N on
+    full steps and |S-hat| on hybrid steps (s-bar, s-bar* of P:715-727)."""
+    z = 4
+    wl = inputs.config(2, steps=inputs.config(2).w + 14, z=z)
+    q0 = inputs.initial_condition(wl)
+    rom = H.HybridROM(wl)
+    rom.set_state(dev(q0))
+    R = orc.Run(wl, q0)
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    worst = 0.0
+    kinds = []
+    for k in range(1, wl.steps + 1):
+        rom.step(count_out=cnt)
+        kind = R.step()
+        kinds.append(kind)
+        full = k + 1 <= wl.w or k % z == 0
+        assert (kind == 0) == full
+        n = int(cnt.item())
+        assert n == (wl.N if full else int(R.mask_used().sum())), (k, n)
+        e = rel(rom.get_state().cpu().numpy(), R.state())
+        worst = max(worst, e)
+        if k >= wl.w and (k + 1) % z != 0:
+            assert np.array_equal(H.cells_from_mask(wl, rom.mask()), R.mask()), k
+            if full:  # projection indicator after a full step (G8)
+                eg, eo = rom.indicator().cpu().numpy(), R.eps()
+                np.testing.assert_allclose(eg, eo, rtol=1e-6, atol=1e-9 * eo.max())
+    rom.sync()
+    assert kinds.count(1) + kinds.count(2) >= 8
+    assert worst <= 1e-11, worst
+
+
+def test_rel_l1_error_matches_definition(inputs):
+    """e_k of P:704-709 (uniform cells): sum |a - b| / sum |b| over the D entries."""
+    wl = small2d(inputs, nx=333, ny=129)
+    rom = H.HybridROM(wl)
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((wl.c, wl.N))
+    b = a + 1e-3 * rng.standard_normal((wl.c, wl.N))
+    e = rom.rel_l1_error(dev(a), dev(b))
+    ref = np.abs(a - b).sum() / np.abs(b).sum()
+    assert abs(e - ref) <= 1e-13 * ref
+    assert rom.rel_l1_error(dev(b), dev(b)) == 0.0
+    assert rom.rel_l1_error(dev(a), dev(b)) == e  # bitwise reproducible
+
+
+def test_algorithm1_metrics_driver(inputs):
+    """e_k, e-bar, s-bar, s-bar*, p-bar, S from the device driver."""
+    from paper_2301_01718_b200 import algorithm1 as A1
+    wl = inputs.config(1)
+    m = A1.run(wl, steps=60, z=7)
+    assert len(m.e) == 60 and len(m.n_gamma) == 60
+    # warm-up full steps are the HDM itself: e_k = 0 exactly
+    assert all(e == 0.0 for e in m.e[: wl.w - 1])
+    for k in range(1, 61):
+        full = k + 1 <= wl.w or k % 7 == 0
+        assert m.hybrid[k - 1] == (not full)
+        if full:
+            assert m.n_gamma[k - 1] == wl.N
+        else:
+            assert 0 < m.n_gamma[k - 1] <= math.ceil(wl.f * wl.N)
+    assert 0.0 < m.e_bar < 0.1
+    assert m.s_bar_star is not None and m.s_bar_star < m.s_bar < wl.N
+    assert m.p_bar == 0.0 and m.speedup > 0.0
+    s = m.summary()
+    assert s["hybrid_steps"] == sum(m.hybrid)

@@ -113,3 +113,58 @@ def test_config1_trajectory_runs_and_stays_positive(orc, inputs):
     assert 2 not in kinds
     assert orc.positivity(wl, R.state()) == -1
     assert R.mask().sum() == orc.n_g(wl.f, wl.N)
+
+
+# ---- finite full-HDM period z (NEXT-3, G8) ----
+
+def test_z1_is_the_full_hdm_trajectory(orc, inputs):
+    """S:448 / P:557: with z = 1 every step is a full HDM step (k mod 1 = 0) and no refresh
+    runs ((k+1) mod 1 = 0), so the trajectory equals repeated full steps bitwise."""
+    wl = _small(inputs, z=1)
+    q0 = inputs.initial_condition(wl, "quadrant")
+    R = orc.Run(wl, q0)
+    q = q0.copy()
+    for _ in range(wl.w + 4):
+        assert R.step() == 0
+        q = orc.full_step(wl, q, orc.dt(wl, q))
+        assert np.array_equal(R.state(), q)
+
+
+def test_finite_z_schedule_skip_and_projection_indicator(orc, inputs):
+    """P:557 full iff k+1 <= w or k mod z = 0; P:578 refresh iff (k+1) mod z != 0; after a
+    full step k >= w the indicator is the projection error of gamma_k - psi_{k+1} on
+    Phi_{k+1} (G8), pinned against a LAPACK SVD of Eq. 9's X."""
+    z = 4
+    wl = _small(inputs, z=z)
+    q0 = inputs.initial_condition(wl, "quadrant")
+    R = orc.Run(wl, q0)
+    traj = [q0]
+    seen_full_refresh = False
+    for k in range(1, 3 * wl.w + 1):
+        mask_before, psi_before = R.mask(), R.psi()
+        kind = R.step()
+        traj.append(R.state())
+        full = k + 1 <= wl.w or k % z == 0
+        assert (kind == 0) == full, (k, kind)
+        if k >= wl.w - 1 and (k + 1) % z == 0:
+            # skipped refresh: S-hat_{k+1} and psi are left as they were
+            assert np.array_equal(R.mask(), mask_before)
+            assert np.array_equal(R.psi(), psi_before)
+        if k >= wl.w and full and (k + 1) % z != 0:
+            seen_full_refresh = True
+            psik = np.mean(np.stack(traj[k - wl.w:k]), axis=0)
+            psik1 = np.mean(np.stack(traj[k - wl.w + 1:k + 1]), axis=0)
+            np.testing.assert_allclose(R.psi(), psik1, rtol=1e-14, atol=1e-15)
+            X = np.stack([(traj[j] - psik).reshape(-1) for j in range(k - wl.w + 1, k + 1)], axis=1)
+            U, S, _ = np.linalg.svd(X, full_matrices=False)
+            r = R.reff()
+            Q = U[:, :r]
+            d = (traj[k] - psik1).reshape(-1)
+            res = d - Q @ (Q.T @ d)
+            eps_exp = (res.reshape(wl.c, wl.N) ** 2).sum(axis=0)
+            np.testing.assert_allclose(R.eps(), eps_exp, rtol=1e-8, atol=1e-10 * eps_exp.max())
+            # G8 algebra: d lies in range(X) (psi_{k+1} - psi_k = (gamma_k - gamma_{k-w}) / w)
+            alpha = np.full(wl.w, -1.0 / wl.w)
+            alpha[-1] += 1.0
+            np.testing.assert_allclose(X @ alpha, d, rtol=0, atol=1e-13 * np.abs(d).max())
+    assert seen_full_refresh
