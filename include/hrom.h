@@ -55,7 +55,7 @@ typedef struct {
   int32_t band;              /* W: seam-band half width (square), reading A21 */
   int32_t filter_orders[3];  /* Shapiro cascade, default {2,4,6} */
   int32_t n_filter_orders;
-  int32_t filter_max_sweeps; /* j_max^f = 10 */
+  int32_t filter_max_sweeps; /* j_max^f = 10; n_filter_orders * j_max^f <= 64 */
   double filter_eps;         /* eps_f = 1e-2, relative decrease (A23) */
   double eig_rel_cutoff;     /* keep POD modes with lambda_i >= cut * lambda_1 (1e-8, A15) */
   double lsq_rel_cutoff;     /* pinv cut on lambda(A^T A) (1e-12, A13) */

@@ -173,7 +173,9 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   if (p->window < 2 || p->window > kMaxW || p->rank < 1 || p->rank > p->window || p->rank > kMaxR)
     return HROM_E_INVALID;
   if (p->halo < grid->recon || p->halo > 16 || p->band < 0 || p->band > 16) return HROM_E_INVALID;
-  if (p->n_filter_orders < 0 || p->n_filter_orders > 3 || p->filter_max_sweeps < 0) return HROM_E_INVALID;
+  if (p->n_filter_orders < 0 || p->n_filter_orders > 3 || p->filter_max_sweeps < 0 ||
+      p->n_filter_orders * p->filter_max_sweeps > 64)
+    return HROM_E_INVALID;
   for (int i = 0; i < p->n_filter_orders; ++i)
     if (p->filter_orders[i] != 2 && p->filter_orders[i] != 4 && p->filter_orders[i] != 6) return HROM_E_INVALID;
   if (!(p->sample_fraction > 0.0 && p->sample_fraction <= 1.0)) return HROM_E_INVALID;
@@ -275,7 +277,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   b.blk_len = std::max<int64_t>(8 * ((c->mwords + 255) / 256 + 2) + (g.N + 1023) / 1024 + 16, 16 * (int64_t)c->nsm + 64);
   A(dalloc(&b.blk, b.blk_len));
   A(dalloc(&b.hist, 3 * 2048));
-  A(dalloc(&b.fstat, c->filter_blocks));
+  A(dalloc(&b.fstat, std::max(c->filter_blocks, 128)));  // also the filter's per-sweep slots
   A(dalloc(&b.l1part, 2 * kL1Blocks));
   A(dalloc(&b.fcnt, c->filter_blocks));
   A(dalloc(&b.colptr, 2 * kMaxSlots));

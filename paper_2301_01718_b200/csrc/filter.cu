@@ -38,14 +38,14 @@ struct FilterArgs {
   uint8_t* flag;         // compact: bit0 ever kept, bits 1/2 keep-set of even/odd sweeps
   uint8_t* kept_cells;   // nullable: per-cell 1 where kept in some sweep (zeroed by the launcher)
   double* eps;
-  double* fstat;         // [grid]
-  int32_t* fcnt;         // [grid]
+  unsigned long long* fdec;  // [2 kFilterSlots]: per sweep, max decrease (bits) and kept count
   int32_t* sweeps_out;   // [3]
   long long* tdbg;       // 64 timestamps (debug)
   int smem_bytes;        // dynamic shared memory of the launch (tables staged when they fit)
 };
 
 constexpr int FT = 512;  // filter threads per block (one block per SM)
+constexpr int kFilterSlots = 64;  // >= orders * max sweeps
 constexpr int FILTER_SMEM = 200 * 1024;
 
 __device__ __forceinline__ void stamp(long long* t, int i) {
@@ -99,6 +99,8 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
     }
     a.flag[t] = 0;
   }
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < 2 * kFilterSlots; i += blockDim.x) a.fdec[i] = 0ull;
   grid.sync();
   stamp(a.tdbg, 1);
   // each CTA owns a contiguous chunk of the band: its stencil tables and F values are staged in
@@ -127,8 +129,6 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
   double* __restrict__ Vp = a.Vp;
   const double* __restrict__ Fb = a.Fb;
   uint8_t* __restrict__ flag = a.flag;
-  __shared__ double s_md[FT / 32];
-  __shared__ long long s_tot[FT / 32];
   int gs = 0;  // sweeps done over all orders
   for (int oi = 0; oi < a.norders; ++oi) {
     const double* cf;
@@ -226,34 +226,16 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
           md = fmax(md, sdec[k]);
           c += scnt[k];
         }
-        a.fstat[blockIdx.x] = md;
-        a.fcnt[blockIdx.x] = c;
+        // one atomic max (non-negative doubles order like their bit patterns) and one integer
+        // add per CTA into this sweep's slot: order-independent, so every CTA reads the same
+        atomicMax(a.fdec + gs, (unsigned long long)__double_as_longlong(md));
+        atomicAdd(a.fdec + kFilterSlots + gs, (unsigned long long)c);
       }
       grid.sync();
-      // identical stop decision in every block (max and integer sum: order-independent)
+      // identical stop decision in every block
       {
-        double md = 0.0;
-        long long tot = 0;
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-          md = fmax(md, __ldcg(a.fstat + b));
-          tot += __ldcg(a.fcnt + b);
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-          md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
-          tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        }
-        if ((threadIdx.x & 31) == 0) {
-          s_md[threadIdx.x >> 5] = md;
-          s_tot[threadIdx.x >> 5] = tot;
-        }
-        __syncthreads();
-        md = 0.0;
-        tot = 0;
-        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
-          md = fmax(md, s_md[k]);
-          tot += s_tot[k];
-        }
-        __syncthreads();  // s_md / s_tot are rewritten by the next sweep
+        const double md = __longlong_as_double((long long)__ldcg(a.fdec + gs));
+        const long long tot = (long long)__ldcg(a.fdec + kFilterSlots + gs);
         stamp(a.tdbg, 2 + gs);
         if (tot == 0 || md < a.eps_f) {
           ++gs;
@@ -308,8 +290,7 @@ hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F, uint8_t* kept_cells) {
   a.flag = c->b.kept;
   a.kept_cells = kept_cells;
   a.eps = c->b.eps;
-  a.fstat = c->b.fstat;
-  a.fcnt = c->b.fcnt;
+  a.fdec = reinterpret_cast<unsigned long long*>(c->b.fstat);
   a.sweeps_out = c->b.ireg + 4;
   a.tdbg = c->b.dbg;
   if (kept_cells) HROM_CK(cudaMemsetAsync(kept_cells, 0, c->g.N, c->st));

@@ -255,7 +255,27 @@ __global__ void __launch_bounds__(GV_T) gemv_gather_kernel(Geo g, Win W, const d
 #pragma unroll
   for (int j = 0; j < SPW; ++j) an[j] = ab[j] = 0.0;
   double bb = 0.0;
-  for (int64_t base = (int64_t)blockIdx.x * 32 * GV_U; base < total; base += (int64_t)gridDim.x * 32 * GV_U) {
+  const int64_t gstep = (int64_t)gridDim.x * 32 * GV_U;
+  // the S-hat list entries of the next chunk are fetched one iteration ahead (the value loads
+  // depend on them: without the prefetch every chunk pays two dependent memory latencies)
+  int32_t lnext[GV_U];
+  auto fetch_list = [&](int64_t b0) {
+#pragma unroll
+    for (int u = 0; u < GV_U; ++u) {
+      const int64_t t = b0 + 32 * u + lane;
+      lnext[u] = 0;
+      if (t < total) {
+        const int var = (int)t / nS;
+        lnext[u] = __ldg(list + ((int)t - var * nS));
+      }
+    }
+  };
+  fetch_list((int64_t)blockIdx.x * 32 * GV_U);
+  for (int64_t base = (int64_t)blockIdx.x * 32 * GV_U; base < total; base += gstep) {
+    int32_t lcur[GV_U];
+#pragma unroll
+    for (int u = 0; u < GV_U; ++u) lcur[u] = lnext[u];
+    fetch_list(base + gstep);
     int64_t se[GV_U];
     double xn[GV_U], bv[GV_U], r[GV_U];
     bool ok[GV_U];
@@ -265,8 +285,8 @@ __global__ void __launch_bounds__(GV_T) gemv_gather_kernel(Geo g, Win W, const d
       ok[u] = t < total;
       int64_t e = 0;
       if (ok[u]) {
-        const int var = (int)t / nS, idx = (int)t - var * nS;
-        e = (int64_t)var * g.N + __ldg(list + idx);
+        const int var = (int)t / nS;
+        e = (int64_t)var * g.N + lcur[u];
       }
       se[u] = sidx(slab, e);
       r[u] = ok[u] ? __ldg(rho.p + sidx(rho, e)) : 0.0;
@@ -1047,7 +1067,8 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
     d.count = c->b.counts + L_REM;
     if ((s = run_gather_gram(c, d, ncol, grid, Rm, ncol, nullptr)) != HROM_OK) return s;
     // GEMVs of the newest snapshot and of b over all S-hat rows
-    const int gblocks = 4 * (c->basis_pending ? c->nsm - 1 : c->nsm);  // static split: avoid the eigen's SM
+    // one wave (2 CTAs per SM at 126 registers); static split: avoid the eigen's SM
+    const int gblocks = 2 * (c->basis_pending ? c->nsm - 1 : c->nsm);
     const int nv = 2 * a.W.nU + 1;
     if (a.W.nU <= 9 * GV_W)
       gemv_gather_kernel<9><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b, c->b.vpart);

@@ -28,7 +28,8 @@ for k in range(nh):
       ts = [x for x in t[40:64] if x > 0]
       print("  sets us: " + " ".join("%.1f" % ((ts[i + 1] - ts[i]) / 1000) for i in range(len(ts) - 1) if ts[i + 1] > ts[i]), flush=True)
       d = [(t[i + 1] - t[i]) / 1000 for i in range(39) if t[i + 1] > t[i] and t[i] > 0 and t[i + 1] - t[i] < 1e8]
-      sv = [x for x in rom.debug_timers(80)[64:80] if x > 0]
+      tt = rom.debug_timers(96)
+      sv = [x for x in tt[64:80] if x > 0]
       print("  solve us: " + " ".join("%.1f" % ((sv[i + 1] - sv[i]) / 1000) for i in range(len(sv) - 1)), flush=True)
       print("  filter us: prologue %.1f sweeps %s" % (d[0] if d else -1, " ".join("%.1f" % x for x in d[1:])), flush=True)
 rom.sync()
