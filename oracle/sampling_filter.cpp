@@ -2,6 +2,7 @@
 // TEST INFRASTRUCTURE ONLY (see oracle.h).
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <numeric>
 #include "common.hpp"
 
@@ -67,22 +68,99 @@ int64_t orc_select(const double* eps, int64_t N, int64_t n_g, uint8_t* mask_out)
   return k;
 }
 
-// RRE-delta rule: smallest n_g with RRE(n_g) >= delta.
+// RRE-delta rule (Eq. rre): order cells by descending eps (ties by ascending index,
+// as in the fraction rule) and take the smallest n_g with
+//   RRE(n_g) = sum_{j <= n_g} eps_{i_j} / sum_j eps_j >= delta.
+// The sums are the exact real sums (reading A35: no rounding decides the integer n_g): every
+// double eps >= 0 is an integer multiple of 2^-1074, so the sums are exact big integers in that
+// unit, and RRE(n) >= delta  <=>  S_n >= delta T  <=>  S_n >= ceil(delta T) (S_n integer).
+// An all-zero indicator selects nothing.
+namespace {
+struct BigNat {  // little-endian base-2^32 natural number
+  std::vector<uint64_t> l;
+  void add_shifted(uint64_t m, int shift) {  // += m * 2^shift
+    const int w = shift / 32, b = shift % 32;
+    unsigned __int128 v = (unsigned __int128)m << b;
+    size_t i = (size_t)w;
+    while (v != 0) {
+      if (l.size() <= i) l.resize(i + 1, 0);
+      const unsigned __int128 t = (unsigned __int128)l[i] + (uint64_t)(v & 0xffffffffu);
+      l[i] = (uint64_t)(t & 0xffffffffu);
+      v = (v >> 32) + (t >> 32);
+      ++i;
+    }
+  }
+  void trim() {
+    while (!l.empty() && l.back() == 0) l.pop_back();
+  }
+};
+int cmp(BigNat a, BigNat b) {
+  a.trim();
+  b.trim();
+  if (a.l.size() != b.l.size()) return a.l.size() < b.l.size() ? -1 : 1;
+  for (size_t i = a.l.size(); i-- > 0;)
+    if (a.l[i] != b.l[i]) return a.l[i] < b.l[i] ? -1 : 1;
+  return 0;
+}
+// eps = m * 2^(e - 1074) with m < 2^53 an integer (e >= 0)
+void split(double x, uint64_t* m, int* e) {
+  uint64_t bits;
+  std::memcpy(&bits, &x, 8);
+  const int be = (int)((bits >> 52) & 0x7ff);
+  const uint64_t f = bits & ((1ull << 52) - 1);
+  *m = be == 0 ? f : (f | (1ull << 52));
+  *e = be == 0 ? 0 : be - 1;
+}
+}  // namespace
+
 int64_t orc_select_rre(const double* eps, int64_t N, double delta, uint8_t* mask_out) {
-  std::vector<int64_t> idx(N);
-  std::iota(idx.begin(), idx.end(), 0);
+  std::vector<int64_t> idx;
+  BigNat T;
+  for (int64_t n = 0; n < N; ++n) {
+    mask_out[n] = 0;
+    if (eps[n] > 0.0) {
+      idx.push_back(n);
+      uint64_t m;
+      int e;
+      split(eps[n], &m, &e);
+      T.add_shifted(m, e);
+    }
+  }
+  if (idx.empty() || !(delta > 0.0)) return 0;
   std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return eps[a] > eps[b]; });
-  CSum tot;
-  for (int64_t n = 0; n < N; ++n) { mask_out[n] = 0; tot.add(eps[n]); }
-  const double total = tot.value();
-  if (!(total > 0.0)) return 0;
-  CSum run;
+  // R = ceil(delta T): delta = dm 2^-sh (dm < 2^53), R = ceil(T dm / 2^sh)
+  int ex;
+  const double mant = std::frexp(delta, &ex);
+  const uint64_t dm = (uint64_t)std::ldexp(mant, 53);
+  const int sh = 53 - ex;
+  BigNat P;  // T * dm
+  for (size_t i = 0; i < T.l.size(); ++i)
+    if (T.l[i]) {
+      P.add_shifted(T.l[i] * (dm & 0xffffffffu), 32 * (int)i);
+      P.add_shifted(T.l[i] * (dm >> 32), 32 * (int)i + 32);
+    }
+  BigNat R;  // floor(P / 2^sh) + (remainder != 0)
+  bool rem = false;
+  for (size_t i = 0; i < P.l.size(); ++i) {
+    const int bitpos = 32 * (int)i;  // limb i covers bits [bitpos, bitpos + 32)
+    for (int b = 0; b < 32; ++b) {
+      if (!((P.l[i] >> b) & 1u)) continue;
+      const int q = bitpos + b - sh;
+      if (q < 0) rem = true;
+      else R.add_shifted(1, q);
+    }
+  }
+  if (rem) R.add_shifted(1, 0);
+  BigNat S;
   int64_t ng = 0;
-  for (int64_t t = 0; t < N; ++t) {
-    run.add(eps[idx[t]]);
+  for (size_t t = 0; t < idx.size(); ++t) {
+    uint64_t m;
+    int e;
+    split(eps[idx[t]], &m, &e);
+    S.add_shifted(m, e);
     mask_out[idx[t]] = 1;
-    ng = t + 1;
-    if (run.value() / total >= delta) break;
+    ng = (int64_t)t + 1;
+    if (cmp(S, R) >= 0) break;
   }
   return ng;
 }

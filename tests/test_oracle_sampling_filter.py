@@ -120,6 +120,52 @@ def test_select_rre_examples_and_minimality(orc):
         assert k == 1 or frac[k - 2] < delta + 1e-12
 
 
+def _rre_exact(eps, delta):
+    """Brute force with exact rationals: descending order, ties by ascending index, smallest
+    n_g with sum_{j<=n_g} eps / sum eps >= delta (reading A35)."""
+    from fractions import Fraction
+    order = sorted(range(len(eps)), key=lambda i: (-eps[i], i))
+    pos = [i for i in order if eps[i] > 0]
+    T = sum(Fraction(float(eps[i])) for i in pos)
+    sel = np.zeros(len(eps), np.uint8)
+    if T == 0:
+        return sel, 0
+    target = Fraction(delta) * T
+    S = Fraction(0)
+    for n, i in enumerate(pos, 1):
+        S += Fraction(float(eps[i]))
+        sel[i] = 1
+        if S >= target:
+            return sel, n
+    raise AssertionError("unreachable for delta <= 1")
+
+
+def test_select_rre_exact_sums(orc):
+    """The RRE decision is exact: wide exponent ranges (incl. subnormals and huge values), ties,
+    zeros, delta = 1 (every positive cell), and deltas placed exactly on a prefix ratio."""
+    rng = np.random.default_rng(7)
+    cases = []
+    for _ in range(120):
+        n = int(rng.integers(1, 80))
+        e = rng.random(n) * 2.0 ** rng.integers(-1074, 1000, n).astype(float)
+        e[rng.random(n) < 0.2] = 0.0
+        if n > 3:
+            e[1] = e[2] = e[3]  # ties
+        cases.append((e, float(rng.choice([1e-300, 0.3, 0.5, 0.9, 0.999999, 1.0]))))
+    # a delta exactly equal to a prefix ratio: eps = (3, 1) -> RRE(1) = 3/4
+    cases.append((np.array([1.0, 3.0]), 0.75))
+    cases.append((np.array([5e-324, 5e-324, 1.0]), 1.0))     # delta = 1 needs the subnormals too
+    cases.append((np.array([1e308, 1e308, 1e-308]), 1.0))
+    cases.append((np.array([2.0 ** -1074] * 5), 0.5))          # all tied subnormals: ceil(2.5) = 3
+    for eps, delta in cases:
+        m, k = orc.select_rre(eps, delta)
+        me, ke = _rre_exact(eps, delta)
+        assert k == ke, (eps, delta, k, ke)
+        assert np.array_equal(m, me)
+    m, k = orc.select_rre(np.zeros(9), 0.5)
+    assert k == 0 and m.sum() == 0
+
+
 # ---------------- Shapiro filter (A24) ----------------
 @pytest.mark.parametrize("order", [2, 4, 6])
 def test_shapiro_dc_nyquist_response(orc, order):
