@@ -68,6 +68,8 @@ typedef struct {
   int32_t full_period;       /* z of Algorithm 1: step k is a full HDM step when
                                 k+1 <= w or k mod z = 0, and the basis update + sampling after
                                 step k is skipped when (k+1) mod z = 0; <= 0: z = infinity */
+  int32_t sample_mode;       /* selection rule of hrom_step: 0 fixed fraction (A18), 1 RRE-delta */
+  double rre_delta;          /* delta of the RRE rule, in (0, 1] (sample_mode 1) */
 } hrom_params;
 
 /* Create a context for one grid.  cuda_stream: a cudaStream_t (NULL = legacy default).
@@ -110,6 +112,15 @@ hrom_status hrom_update_basis(hrom_ctx* ctx);
  * Outputs (nullable, device): mask bitmap, ascending cell list, count (int32). */
 hrom_status hrom_sample(hrom_ctx* ctx, double fraction, const double* dev_eps, uint32_t* dev_mask_out,
                         int32_t* dev_list_out, int32_t* dev_count_out);
+
+/* H8, RRE-delta rule (Eq. rre): S-hat_{k+1} = the n_g cells of largest eps (ties by
+ * ascending index), n_g the smallest count whose relative retained error
+ * RRE(n_g) = sum of the n_g largest eps / sum of all eps reaches delta.  The sums are exact
+ * (integer arithmetic in units of 2^-1074; reading A35), so n_g is decided without rounding.
+ * delta in (0, 1] (else HROM_E_INVALID); all-zero eps selects nothing.  Then builds the sets
+ * as hrom_sample; same outputs (dev_count_out receives n_g). */
+hrom_status hrom_sample_rre(hrom_ctx* ctx, double delta, const double* dev_eps, uint32_t* dev_mask_out,
+                            int32_t* dev_list_out, int32_t* dev_count_out);
 
 /* H4-H6 standalone (gappy POD): with the current basis (Phi_{k+1}, psi_{k+1}), take the
  * values of dev_v on the cells of S-hat (dev_mask or the current sets) as HDM values,

@@ -83,6 +83,7 @@ def lib():
             "orc_run_destroy": (None, [C.c_void_p]),
             "orc_run_step": (i32, [C.c_void_p, C.c_double]),
             "orc_run_set_full_period": (None, [C.c_void_p, i32]),
+            "orc_run_set_rre": (None, [C.c_void_p, C.c_double]),
             "orc_run_k": (i64, [C.c_void_p]),
             "orc_run_state": (None, [C.c_void_p, d]),
             "orc_run_mask": (None, [C.c_void_p, u8]),
@@ -301,6 +302,8 @@ class Run:
         self.h = lib().orc_run_create(C.byref(self._g), C.byref(self._p), _d(q0))
         if getattr(wl, "z", 0) > 0:
             lib().orc_run_set_full_period(self.h, int(wl.z))
+        if getattr(wl, "delta", 0.0) > 0.0:
+            lib().orc_run_set_rre(self.h, float(wl.delta))
 
     def __del__(self):
         h, self.h = getattr(self, "h", None), None

@@ -36,6 +36,7 @@ struct orc_run {
   int64_t kept = 0;
   int32_t sweeps[3] = {0, 0, 0};
   int32_t z = 0;  // full-HDM period; <= 0: infinity
+  double delta = 0.0;  // > 0: RRE-delta selection instead of the fraction f
   orc_run(const orc_grid* gg, const orc_params* pp) : g(*gg), p(*pp), G(gg) {}
 };
 
@@ -70,6 +71,13 @@ void refresh_basis(orc_run* R, const std::vector<double>& psi_k) {
   R->reff = orc_pod(X.data(), D, w, r, R->p.eig_rel_cutoff, R->Phi.data(), R->sigma.data(), V.data());
   R->Phi.resize((int64_t)R->reff * D);
   R->psi = mean_of(R->snaps, ns - w, w, D);
+}
+
+// S-hat_{k+1} from eps: the fraction rule (A18) or, when set, the RRE-delta rule
+void select_next(orc_run* R) {
+  const int64_t N = R->g.nx * (int64_t)R->g.ny;
+  if (R->delta > 0.0) orc_select_rre(R->eps.data(), N, R->delta, R->mask_next.data());
+  else orc_select(R->eps.data(), N, orc_n_g(R->p.f, N), R->mask_next.data());
 }
 
 void reconstruct(const orc_run* R, const std::vector<double>& y, int64_t n, double* out) {
@@ -200,19 +208,20 @@ int32_t orc_run_step(orc_run* R, double dt_override) {
     const std::vector<double> psi0 = mean_of(R->snaps, R->snaps.size() - w, w, D);
     refresh_basis(R, psi0);
     projection_indicator(R);  // bootstrap indicator (A19)
-    orc_select(R->eps.data(), N, orc_n_g(R->p.f, N), R->mask_next.data());
+    select_next(R);
   } else if (k >= w) {
     // psi_k = mean(gamma_{k-w..k-1}) (lagged centring, A14; by its formula also
     // when the refresh after step k-1 was skipped, reading G8)
     const std::vector<double> psik = mean_of(R->snaps, 0, w, D);
     refresh_basis(R, psik);
     if (kind == 0) projection_indicator(R);  // after a full step (finite z): reading G8
-    orc_select(R->eps.data(), N, orc_n_g(R->p.f, N), R->mask_next.data());
+    select_next(R);
   }
   return kind;
 }
 
 void orc_run_set_full_period(orc_run* R, int32_t z) { R->z = z; }
+void orc_run_set_rre(orc_run* R, double delta) { R->delta = delta; }
 
 int64_t orc_run_k(const orc_run* R) { return R->k; }
 void orc_run_state(const orc_run* R, double* q) { std::copy(R->snaps.back().begin(), R->snaps.back().end(), q); }

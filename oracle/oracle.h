@@ -103,6 +103,7 @@ void orc_run_destroy(orc_run* R);
 int32_t orc_run_step(orc_run* R, double dt_override);
 /* full-HDM period z of Algorithm 1; <= 0: infinity (the default) */
 void orc_run_set_full_period(orc_run* R, int32_t z);
+void orc_run_set_rre(orc_run* R, double delta);  /* > 0: RRE-delta sampling */
 int64_t orc_run_k(const orc_run* R);
 void orc_run_state(const orc_run* R, double* q);             /* gamma_k */
 void orc_run_mask(const orc_run* R, uint8_t* m);             /* S-hat for the NEXT step */

@@ -179,6 +179,8 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   for (int i = 0; i < p->n_filter_orders; ++i)
     if (p->filter_orders[i] != 2 && p->filter_orders[i] != 4 && p->filter_orders[i] != 6) return HROM_E_INVALID;
   if (!(p->sample_fraction > 0.0 && p->sample_fraction <= 1.0)) return HROM_E_INVALID;
+  if (p->sample_mode != 0 && p->sample_mode != 1) return HROM_E_INVALID;
+  if (p->sample_mode == 1 && !(p->rre_delta > 0.0 && p->rre_delta <= 1.0)) return HROM_E_INVALID;
   if (p->gram_mode != 0 && p->gram_mode != 1) return HROM_E_INVALID;
   if (p->gather_mode != 0 && p->gather_mode != 1) return HROM_E_INVALID;
 
@@ -277,6 +279,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   b.blk_len = std::max<int64_t>(8 * ((c->mwords + 255) / 256 + 2) + (g.N + 1023) / 1024 + 16, 16 * (int64_t)c->nsm + 64);
   A(dalloc(&b.blk, b.blk_len));
   A(dalloc(&b.hist, 3 * 2048));
+  A(dalloc(&b.hsum, 3 * 2 * 2048));
   A(dalloc(&b.fstat, std::max(c->filter_blocks, 128)));  // also the filter's per-sweep slots
   A(dalloc(&b.l1part, 2 * kL1Blocks));
   A(dalloc(&b.fcnt, c->filter_blocks));
@@ -329,7 +332,7 @@ void hrom_destroy(hrom_ctx* c) {
   Bufs& b = c->b;
   void* ptrs[] = {b.ring, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
                   b.kept, b.fidx, b.ftab, b.fcur, b.fF, b.C, b.part, b.gpart, b.K, b.Khi, b.Klo, b.Rd, b.vpart, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
-                  b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.fstat, b.l1part, b.fcnt, (void*)b.colptr, b.slot_tab};
+                  b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.hsum, b.fstat, b.l1part, b.fcnt, (void*)b.colptr, b.slot_tab};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete c;
@@ -552,6 +555,9 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
   return HROM_OK;
 }
 
+static hrom_status sample_outputs(hrom_ctx* c, uint32_t* dev_mask_out, int32_t* dev_list_out,
+                                  int32_t* dev_count_out);
+
 hrom_status hrom_sample(hrom_ctx* c, double fraction, const double* dev_eps, uint32_t* dev_mask_out,
                         int32_t* dev_list_out, int32_t* dev_count_out) {
   if (!c) return HROM_E_INVALID;
@@ -565,6 +571,11 @@ hrom_status hrom_sample(hrom_ctx* c, double fraction, const double* dev_eps, uin
   if ((s = select_and_build(c, dev_eps ? dev_eps : c->b.eps, n_g)) != HROM_OK) return s;
   prof_end(c, SEC_SAMPLE);
   c->sets_ready = true;
+  return sample_outputs(c, dev_mask_out, dev_list_out, dev_count_out);
+}
+
+static hrom_status sample_outputs(hrom_ctx* c, uint32_t* dev_mask_out, int32_t* dev_list_out,
+                                  int32_t* dev_count_out) {
   if (dev_mask_out)
     HROM_CK(cudaMemcpyAsync(dev_mask_out, c->b.masks + (int64_t)M_S * c->mwords, c->mwords * sizeof(uint32_t),
                             cudaMemcpyDefault, c->st));
@@ -574,6 +585,19 @@ hrom_status hrom_sample(hrom_ctx* c, double fraction, const double* dev_eps, uin
   if (dev_count_out)
     HROM_CK(cudaMemcpyAsync(dev_count_out, c->b.counts + L_S, sizeof(int32_t), cudaMemcpyDefault, c->st));
   return HROM_OK;
+}
+
+hrom_status hrom_sample_rre(hrom_ctx* c, double delta, const double* dev_eps, uint32_t* dev_mask_out,
+                            int32_t* dev_list_out, int32_t* dev_count_out) {
+  if (!c) return HROM_E_INVALID;
+  if (!(delta > 0.0 && delta <= 1.0)) return HROM_E_INVALID;
+  hrom_status s;
+  if ((s = flush_eigen(c)) != HROM_OK) return s;
+  prof_begin(c, SEC_SAMPLE);
+  if ((s = select_and_build(c, dev_eps ? dev_eps : c->b.eps, 0, delta)) != HROM_OK) return s;
+  prof_end(c, SEC_SAMPLE);
+  c->sets_ready = true;
+  return sample_outputs(c, dev_mask_out, dev_list_out, dev_count_out);
 }
 
 hrom_status hrom_reconstruct(hrom_ctx* c, const uint32_t* dev_mask, double* dev_v, double* dev_y_out,
@@ -653,7 +677,9 @@ hrom_status hrom_step_ex(hrom_ctx* c, double dt_override, int32_t* dev_count_out
       c->full_since_update = false;  // the next update follows the next (full) step
     } else {
       if ((s = hrom_update_basis(c)) != HROM_OK) return s;
-      if ((s = hrom_sample(c, c->P.sample_fraction, nullptr, nullptr, nullptr, nullptr)) != HROM_OK) return s;
+      s = c->P.sample_mode == 1 ? hrom_sample_rre(c, c->P.rre_delta, nullptr, nullptr, nullptr, nullptr)
+                                : hrom_sample(c, c->P.sample_fraction, nullptr, nullptr, nullptr, nullptr);
+      if (s != HROM_OK) return s;
     }
   }
   return HROM_OK;

@@ -123,6 +123,7 @@ struct Bufs {
   int32_t* blk = nullptr;      // block counts/offsets for compaction (max blocks * L_COUNT * 2)
   int64_t blk_len = 0;
   int32_t* hist = nullptr;     // 3 x 2048 radix histograms
+  unsigned long long* hsum = nullptr;  // 3 x 2 x 2048 exact radix bucket sums (RRE-delta)
   // filter stats per block
   double* fstat = nullptr;
   double* l1part = nullptr;   // 2 * kL1Blocks partial sums (relative L1 error)
@@ -229,7 +230,7 @@ hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, co
 hrom_status launch_positivity(hrom_ctx* c, SRef qprev, SRef q, int64_t kq);
 // masks.cu
 hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S);
-hrom_status select_and_build(hrom_ctx* c, const double* eps, int64_t n_g);
+hrom_status select_and_build(hrom_ctx* c, const double* eps, int64_t n_g, double rre_delta = 0.0);
 int sets_occupancy();
 // linalg.cu
 // dev_cols: column base pointers, all with slab stride ns (1 = plain vectors); rho: SRef or p == nullptr

@@ -7,12 +7,14 @@
 // Readings: A9 (per-stage cross dilations), A18 (fraction mode, ties by ascending
 // index), A21 (square seam band).  Everything here is integer work: bit-exact.
 #include <cooperative_groups.h>
+#include <cmath>
 #include "internal.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace hrom {
-hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long long n_g, bool sparse = false);
+hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long long n_g, bool sparse = false,
+                        double rre_delta = 0.0);
 namespace {
 
 __device__ __forceinline__ int wrapi(int i, int n, int bc, bool* valid) {
@@ -98,6 +100,10 @@ struct SetsArgs {
   int do_select;
   const double* eps;
   long long n_g;
+  int rre;                 // 1: RRE-delta rule instead of n_g
+  unsigned long long rre_dm;  // delta = rre_dm * 2^-rre_sh exactly (rre_dm < 2^53)
+  int rre_sh;
+  unsigned long long* hsum;  // 3 x 2 x NBIN exact bucket sums (RRE mode)
   int halo, band, rmax;
   uint32_t* masks;     // M_COUNT masks of mwords
   int64_t mwords;
@@ -234,6 +240,134 @@ __device__ __forceinline__ void blk_write(const uint32_t* M, int64_t b0, int64_t
 }
 
 
+// ---- RRE-delta selection: exact integer arithmetic (reading A35) ----
+// A positive double is m 2^(max(be,1) - 1) in units of 2^-1074 (m < 2^53 an integer).  Radix
+// bucket b0 = pattern bits 63..53 holds the biased exponents 2 b0 and 2 b0 + 1, so with the
+// bucket unit 2^ub, ub = max(2 b0 - 1, 0), every value of the bucket is the integer m or 2m.
+// Pass 0 (the bucket b0) works on big naturals (T = sum of all eps, R = ceil(delta T)); the
+// later passes stay inside one bucket, where every partial sum is < 2^80 units: 128-bit.
+constexpr int RRE_LIMBS = 72;  // 2304 bits > 2^(2046 + 80 + 53)
+typedef unsigned __int128 u128;
+__device__ __forceinline__ int rre_ub(unsigned b0) { return b0 ? 2 * (int)b0 - 1 : 0; }
+__device__ __forceinline__ unsigned long long rre_contrib(unsigned long long bb) {
+  const int be = (int)(bb >> 52);
+  const unsigned long long f = bb & ((1ull << 52) - 1ull);
+  const unsigned long long m = be ? (f | (1ull << 52)) : f;
+  return m << ((be ? be - 1 : 0) - rre_ub((unsigned)(bb >> 53)));
+}
+__device__ __forceinline__ u128 shfl_up_u128(u128 v, int o) {
+  const unsigned long long lo = __shfl_up_sync(0xffffffffu, (unsigned long long)v, o);
+  const unsigned long long hi = __shfl_up_sync(0xffffffffu, (unsigned long long)(v >> 64), o);
+  return ((u128)hi << 64) | lo;
+}
+// exclusive block scan of one u128 per thread
+__device__ __forceinline__ u128 block_excl_scan_u128(u128 v, u128* sbuf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  u128 x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const u128 t = shfl_up_u128(x, o);
+    if (lane >= o) x += t;
+  }
+  __syncthreads();
+  if (lane == 31) sbuf[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    u128 y = lane < nw ? sbuf[lane] : (u128)0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const u128 t = shfl_up_u128(y, o);
+      if (lane >= o) y += t;
+    }
+    sbuf[lane] = y;
+  }
+  __syncthreads();
+  const u128 wpre = warp ? sbuf[warp - 1] : (u128)0;
+  __syncthreads();
+  return wpre + x - v;
+}
+// Pass-0 pick of the RRE rule, thread 0 of the block (identical in every block).
+// lo/hi: the 1024 bucket sums of pass 0 (sum = hi 2^32 + lo, units 2^ub(b)); acc: T in
+// non-normalised 32-bit limbs (u64 each).  Returns the bucket b0 whose cumulative sum (from
+// the top) first reaches R = ceil(delta T), and D = ceil((R - sum above b0) / 2^ub(b0)).
+__device__ void rre_pick0(const unsigned long long* lo, const unsigned long long* hi, const unsigned long long* acc,
+                          unsigned long long dm, int sh, uint32_t* big, int* b_out, u128* D_out) {
+  uint32_t T[RRE_LIMBS];
+  unsigned long long carry = 0;
+  for (int i = 0; i < RRE_LIMBS; ++i) {
+    const unsigned long long t = acc[i] + carry;
+    T[i] = (uint32_t)t;
+    carry = t >> 32;
+  }
+  // P = T dm (dm < 2^53), in place over T's limbs, then R = ceil(P / 2^sh) into big
+  {
+    u128 cy = 0;
+    for (int i = 0; i < RRE_LIMBS; ++i) {
+      const u128 t = (u128)T[i] * dm + cy;
+      T[i] = (uint32_t)t;
+      cy = t >> 32;
+    }
+  }
+  const int q = sh >> 5, s = sh & 31;
+  bool sticky = false;
+  for (int i = 0; i < RRE_LIMBS; ++i) {
+    if (i < q) sticky |= T[i] != 0u;
+  }
+  if (s) sticky |= (q < RRE_LIMBS) && (T[q] & ((1u << s) - 1u)) != 0u;
+  for (int i = 0; i < RRE_LIMBS; ++i) {
+    const int k = i + q;
+    const uint32_t a0 = k < RRE_LIMBS ? T[k] : 0u, a1 = k + 1 < RRE_LIMBS ? T[k + 1] : 0u;
+    big[i] = s ? (a0 >> s) | (a1 << (32 - s)) : a0;
+  }
+  if (sticky)
+    for (int i = 0; i < RRE_LIMBS; ++i)
+      if (++big[i] != 0u) break;
+  int top = RRE_LIMBS - 1;
+  while (top > 0 && big[top] == 0u) --top;
+  // descend the buckets: Dif = R - (sum of the buckets above) > 0
+  for (int b = 1023; b >= 0; --b) {
+    if (lo[b] == 0ull && hi[b] == 0ull) continue;
+    const int ub = rre_ub((unsigned)b), L = ub >> 5;
+    const u128 sb = (((u128)hi[b]) << 32) + lo[b];
+    const u128 s2 = sb << (ub & 31);  // < 2^111
+    uint32_t p[4];
+    for (int k = 0; k < 4; ++k) p[k] = (uint32_t)(s2 >> (32 * k));
+    int cmp = 0;  // sign of (S_b - Dif)
+    if (top > L + 3) cmp = -1;
+    else {
+      for (int i = L + 3; i >= L && cmp == 0; --i) {
+        const uint32_t d = big[i];
+        if (p[i - L] != d) cmp = p[i - L] > d ? 1 : -1;
+      }
+      if (cmp == 0) {
+        cmp = 1;  // S_b >= Dif unless Dif has bits below limb L
+        for (int i = 0; i < L; ++i)
+          if (big[i]) cmp = -1;
+      }
+    }
+    if (cmp >= 0) {  // found: D = ceil(Dif / 2^ub)
+      u128 V = 0;
+      for (int i = min(top, L + 3); i >= L; --i) V = (V << 32) | big[i];
+      const int sb2 = ub & 31;
+      bool st = sb2 ? (V & ((((u128)1) << sb2) - 1)) != 0 : false;
+      for (int i = 0; i < L; ++i) st |= big[i] != 0u;
+      *D_out = (V >> sb2) + (st ? 1 : 0);
+      *b_out = b;
+      return;
+    }
+    // Dif -= S_b
+    unsigned long long br = 0;
+    for (int i = L; i < RRE_LIMBS; ++i) {
+      const unsigned long long sub = (i - L < 4 ? p[i - L] : 0u) + br;
+      const unsigned long long d = big[i];
+      big[i] = (uint32_t)(d - sub);
+      br = d < sub ? 1ull : 0ull;
+      if (i - L >= 3 && br == 0) break;
+    }
+    while (top > 0 && big[top] == 0u) --top;
+  }
+  *b_out = -1;  // R > T: cannot happen for delta <= 1
+  *D_out = 0;
+}
+
 __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
   cg::grid_group grid = cg::this_grid();
   const Geo& g = a.g;
@@ -249,6 +383,10 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
   __shared__ int wcnt[32];
   __shared__ int shist[NBIN];
   __shared__ int s_digit, s_above;
+  __shared__ unsigned long long s_lo[NBIN], s_hi[NBIN], s_acc[RRE_LIMBS];
+  __shared__ uint32_t s_big[RRE_LIMBS];
+  __shared__ u128 s_u128[32];
+  __shared__ u128 s_D;
   const int tid = threadIdx.x;
   const int G = gridDim.x;
   int ts = 40;
@@ -345,13 +483,102 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
   sstamp(a.tdbg, ts);
     const int total = __ldcg(a.counts + 8);
     const int ng = (int)(a.n_g < total ? a.n_g : total);
-    const bool thresh = a.n_g < total;
+    bool thresh = a.rre ? total > 0 : a.n_g < total;
     unsigned long long prefix = 0ull;
-    int rem = ng;
+    int rem = a.rre ? 0 : ng;
     // contiguous block chunk of the compacted values
     const int64_t vchunk = ((int64_t)total + G - 1) / G;
     const int64_t v0 = min((int64_t)blockIdx.x * vchunk, (int64_t)total), v1 = min(v0 + vchunk, (int64_t)total);
-    if (thresh) {
+    if (a.rre && thresh) {
+      // RRE-delta: the same 6 radix passes over the IEEE patterns, on exact per-digit sums
+      // instead of counts; the target is the remaining sum D (units of the pass-0 bucket)
+      u128 Drem = 0;
+      for (int p = 0; p < 6; ++p) {
+        const int shift = p < 5 ? 53 - RADIX * p : 0;
+        const int width = (shift == 0) ? 9 : RADIX;
+        const unsigned long long hm = (p == 0) ? 0ull : (~0ull << (shift + width));
+        for (int i = tid; i < NBIN; i += blockDim.x) s_lo[i] = s_hi[i] = 0ull;
+        __syncthreads();
+        for (int64_t t = v0 + tid; t < v1; t += blockDim.x) {
+          const unsigned long long bb = (unsigned long long)__double_as_longlong(a.sel_val[t]);
+          if ((bb & hm) == prefix) {
+            const unsigned long long cv = rre_contrib(bb);
+            const int bin = (int)((bb >> shift) & (NBIN - 1));
+            atomicAdd(&s_lo[bin], cv & 0xffffffffull);
+            if (cv >> 32) atomicAdd(&s_hi[bin], cv >> 32);
+          }
+        }
+        __syncthreads();
+        unsigned long long* gs = a.hsum + (p % 3) * 2 * NBIN;
+        for (int i = tid; i < NBIN; i += blockDim.x) {
+          if (s_lo[i]) atomicAdd(gs + i, s_lo[i]);
+          if (s_hi[i]) atomicAdd(gs + NBIN + i, s_hi[i]);
+        }
+        if (blockIdx.x == 0)
+          for (int i = tid; i < 2 * NBIN; i += blockDim.x) a.hsum[((p + 1) % 3) * 2 * NBIN + i] = 0ull;
+        grid.sync();
+  sstamp(a.tdbg, ts);
+        for (int i = tid; i < NBIN; i += blockDim.x) {
+          s_lo[i] = __ldcg(gs + i);
+          s_hi[i] = __ldcg(gs + NBIN + i);
+        }
+        __syncthreads();
+        if (p == 0) {
+          for (int i = tid; i < RRE_LIMBS; i += blockDim.x) s_acc[i] = 0ull;
+          __syncthreads();
+          for (int b = tid; b < 1024; b += blockDim.x) {
+            if (s_lo[b] == 0ull && s_hi[b] == 0ull) continue;
+            const int ub = rre_ub((unsigned)b), L = ub >> 5;
+            const u128 s2 = ((((u128)s_hi[b]) << 32) + s_lo[b]) << (ub & 31);
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t piece = (uint32_t)(s2 >> (32 * k));
+              if (piece) atomicAdd(&s_acc[L + k], (unsigned long long)piece);
+            }
+          }
+          __syncthreads();
+          if (tid == 0) {
+            int b0;
+            u128 D;
+            rre_pick0(s_lo, s_hi, s_acc, a.rre_dm, a.rre_sh, s_big, &b0, &D);
+            s_digit = b0;
+            s_D = D;
+          }
+          __syncthreads();
+          if (s_digit < 0) {
+            thresh = false;  // R > T (delta > 1): every eps > 0 is selected
+            break;
+          }
+          prefix = (unsigned long long)s_digit << 53;
+          Drem = s_D;
+          __syncthreads();
+        } else {
+          constexpr int PER = NBIN / ST_T;
+          u128 sq[PER];
+          u128 mine = 0;
+          for (int q = 0; q < PER; ++q) {
+            const int bin = NBIN - 1 - (tid * PER + q);
+            sq[q] = (((u128)s_hi[bin]) << 32) + s_lo[bin];
+            mine += sq[q];
+          }
+          u128 above = block_excl_scan_u128(mine, s_u128);
+          for (int q = 0; q < PER; ++q) {
+            if (above < Drem && above + sq[q] >= Drem) {
+              s_digit = NBIN - 1 - (tid * PER + q);
+              s_D = above;
+            }
+            above += sq[q];
+          }
+          __syncthreads();
+          prefix |= (unsigned long long)s_digit << shift;
+          Drem -= s_D;
+          __syncthreads();
+        }
+      }
+      if (thresh) {
+        const unsigned long long vt = rre_contrib(prefix);  // tau in the pass-0 bucket's units
+        rem = (int)((Drem + vt - 1) / vt);
+      }
+    } else if (thresh) {
       for (int p = 0; p < 6; ++p) {
         const int shift = p < 5 ? 53 - RADIX * p : 0;  // 53, 42, 31, 20, 9, 0
         const int width = (shift == 0) ? 9 : RADIX;
@@ -656,8 +883,17 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
 
 }  // namespace
 
-hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long long n_g, bool sparse) {
+hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long long n_g, bool sparse,
+                        double rre_delta) {
   SetsArgs a{};
+  if (rre_delta > 0.0) {  // delta = dm 2^-sh exactly
+    int ex;
+    const double mant = std::frexp(rre_delta, &ex);
+    a.rre = 1;
+    a.rre_dm = (unsigned long long)std::ldexp(mant, 53);
+    a.rre_sh = 53 - ex;
+  }
+  a.hsum = c->b.hsum;
   a.cand = sparse ? c->b.lists + (int64_t)L_T * c->g.N : nullptr;
   a.ncand = c->b.counts + L_T;
   a.g = c->g;
@@ -709,11 +945,11 @@ hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S) {
 }
 
 // top-n_g of eps > 0 -> S-hat (ties at the threshold by ascending cell), then build_sets.
-hrom_status select_and_build(hrom_ctx* c, const double* eps, int64_t n_g) {
+hrom_status select_and_build(hrom_ctx* c, const double* eps, int64_t n_g, double rre_delta) {
   ++c->samples_since_gather;
   // the step's own indicator is nonzero only on S-hat u B (the T list): scan that list only
   const bool sparse = eps == c->b.eps && c->eps_sparse;
-  return launch_sets(c, true, eps, (long long)n_g, sparse);
+  return launch_sets(c, true, eps, (long long)n_g, sparse, rre_delta);
 }
 
 }  // namespace hrom

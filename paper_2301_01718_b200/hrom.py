@@ -38,7 +38,8 @@ class Params(C.Structure):
                 ("filter_max_sweeps", C.c_int32), ("filter_eps", C.c_double),
                 ("eig_rel_cutoff", C.c_double), ("lsq_rel_cutoff", C.c_double),
                 ("sample_fraction", C.c_double), ("gram_mode", C.c_int32), ("rebase_period", C.c_int32),
-                ("gather_mode", C.c_int32), ("full_period", C.c_int32)]
+                ("gather_mode", C.c_int32), ("full_period", C.c_int32),
+                ("sample_mode", C.c_int32), ("rre_delta", C.c_double)]
 
 
 # every entry point of include/hrom.h with its ctypes signature
@@ -52,6 +53,7 @@ _SIGS = {
     "hrom_hybrid_step": (C.c_int, [_VP, _VP, C.c_double, _VP]),
     "hrom_update_basis": (C.c_int, [_VP]),
     "hrom_sample": (C.c_int, [_VP, C.c_double, _VP, _VP, _VP, _VP]),
+    "hrom_sample_rre": (C.c_int, [_VP, C.c_double, _VP, _VP, _VP, _VP]),
     "hrom_reconstruct": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "hrom_filter": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "hrom_step": (C.c_int, [_VP, C.c_double]),
@@ -160,7 +162,8 @@ class HybridROM:
         fo = (C.c_int32 * 3)(*(list(wl.filter_orders) + [0, 0, 0])[:3])
         p = Params(wl.w, wl.r, wl.h, wl.W, fo, len(wl.filter_orders), wl.filter_max_sweeps, wl.filter_eps,
                    wl.eig_rel_cutoff, wl.lsq_rel_cutoff, wl.f, gram_mode, rebase_period, gather_mode,
-                   getattr(wl, "z", 0) if full_period is None else full_period)
+                   getattr(wl, "z", 0) if full_period is None else full_period,
+                   1 if getattr(wl, "delta", 0.0) > 0.0 else 0, float(getattr(wl, "delta", 0.0)))
         h = C.c_void_p()
         _ck(self.lib.hrom_create(C.byref(g), wl.gamma, wl.cfl, C.byref(p), C.c_void_p(self.stream.cuda_stream),
                                  C.byref(h)), "hrom_create")
@@ -204,6 +207,13 @@ class HybridROM:
                count_out: Optional[torch.Tensor] = None):
         f = self.wl.f if fraction is None else fraction
         _ck(self.lib.hrom_sample(self.h, f, _ptr(eps), _ptr(mask_out), _ptr(list_out), _ptr(count_out)), "hrom_sample")
+
+    def sample_rre(self, delta: Optional[float] = None, eps: Optional[torch.Tensor] = None,
+                   mask_out: Optional[torch.Tensor] = None, list_out: Optional[torch.Tensor] = None,
+                   count_out: Optional[torch.Tensor] = None):
+        d = self.wl.delta if delta is None else delta
+        _ck(self.lib.hrom_sample_rre(self.h, d, _ptr(eps), _ptr(mask_out), _ptr(list_out), _ptr(count_out)),
+            "hrom_sample_rre")
 
     def reconstruct(self, v: torch.Tensor, mask: Optional[torch.Tensor] = None,
                     y_out: Optional[torch.Tensor] = None, eps_out: Optional[torch.Tensor] = None):

@@ -97,6 +97,7 @@ class Workload:
     eig_rel_cutoff: float = 1e-8
     lsq_rel_cutoff: float = 1e-12
     z: int = 0             # full-HDM period of Algorithm 1; 0 = infinity (A20)
+    delta: float = 0.0     # > 0: RRE-delta selection instead of the fraction f
 
     @property
     def c(self) -> int:

@@ -600,3 +600,78 @@ def test_algorithm1_metrics_driver(inputs):
     assert m.p_bar == 0.0 and m.speedup > 0.0
     s = m.summary()
     assert s["hybrid_steps"] == sum(m.hybrid)
+
+
+def _rre_cases(rng, N):
+    """Indicator vectors for the RRE-delta rule: ties + zeros, wide exponents incl. subnormals
+    and values near DBL_MAX, all-zero, and deltas exactly on a prefix ratio."""
+    out = []
+    e = np.round(rng.random(N) * 50) / 50.0 * (rng.random(N) < 0.4)
+    for d in (0.3, 0.9, 0.999, 1.0):
+        out.append((e, d))
+    e = rng.random(N) * 2.0 ** rng.integers(-1074, 1000, N).astype(float)
+    e[rng.random(N) < 0.3] = 0.0
+    e[10:40] = e[5]  # ties
+    for d in (1e-300, 0.5, 0.999999, 1.0):
+        out.append((e, d))
+    e = rng.random(N) * 2.0 ** rng.integers(-30, 0, N).astype(float)  # a realistic spread
+    out.append((e, 0.99))
+    e = np.zeros(N)
+    e[[3, 77]] = [1.0, 3.0]
+    out.append((e, 0.75))  # exactly RRE(1) = 3/4 -> one cell
+    e = np.zeros(N)
+    e[[1, 2, 900, 901, 5000]] = 2.0 ** -1074
+    out.append((e, 0.5))   # tied subnormals: ceil(2.5) = 3 cells, lowest indices
+    e = np.zeros(N)
+    e[[0, 1, N - 1]] = [1e308, 1e308, 1e-308]
+    out.append((e, 1.0))
+    out.append((np.zeros(N), 0.5))
+    return out
+
+
+@pytest.mark.parametrize("nx,ny", [(130, 77), (1024, 1024)])
+def test_sample_rre_bit_exact(orc, inputs, nx, ny):
+    """H8 with the RRE-delta rule fed the same indicator as the oracle: S-hat,
+    its ascending list and n_g bit-exact; the sums are exact on both sides (reading A35)."""
+    wl = small2d(inputs, nx=nx, ny=ny, bc=1)
+    rom = H.HybridROM(wl)
+    rom.set_state(dev(inputs.initial_condition(wl, "random")))
+    rng = np.random.default_rng(11)
+    mw = torch.zeros(rom.mask_words, dtype=torch.int32, device="cuda")
+    lst = torch.zeros(wl.N, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for t, (eps, delta) in enumerate(_rre_cases(rng, wl.N)):
+        m_o, k_o = orc.select_rre(eps, delta)
+        rom.sample_rre(delta, eps=dev(eps), mask_out=mw, list_out=lst, count_out=cnt)
+        torch.cuda.synchronize()
+        assert np.array_equal(H.cells_from_mask(wl, mw), m_o), (t, delta)
+        n = int(cnt.item())
+        assert n == k_o, (t, delta, n, k_o)
+        assert np.array_equal(lst[:n].cpu().numpy(), np.nonzero(m_o)[0])
+    with pytest.raises(H.HromError):
+        rom.sample_rre(0.0)
+    with pytest.raises(H.HromError):
+        rom.sample_rre(1.5)
+
+
+def test_trajectory_rre_config2(orc, inputs):
+    """Algorithm 1 on config 2 with the RRE-delta selection (delta = 0.99) instead of
+    the fixed fraction: step by step, S-hat identical to the oracle's and state <= 1e-11."""
+    wl = inputs.config(2, steps=inputs.config(2).w + 6, delta=0.99)
+    q0 = inputs.initial_condition(wl)
+    rom = H.HybridROM(wl)
+    rom.set_state(dev(q0))
+    R = orc.Run(wl, q0)
+    worst = 0.0
+    sizes = []
+    for k in range(1, wl.steps + 1):
+        rom.step()
+        R.step()
+        worst = max(worst, rel(rom.get_state().cpu().numpy(), R.state()))
+        if k >= wl.w - 1:
+            m_o = R.mask()
+            assert np.array_equal(H.cells_from_mask(wl, rom.mask()), m_o), k
+            sizes.append(int(m_o.sum()))
+    rom.sync()
+    assert all(0 < s < wl.N // 4 for s in sizes), sizes
+    assert worst <= 1e-11, worst
