@@ -186,6 +186,10 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
 
   hrom_ctx* c = new hrom_ctx();
   c->P = *p;
+  {
+    const char* ev = std::getenv("HROM_GRAM_LEGACY");
+    c->gram_legacy = ev && ev[0] == '1';
+  }
   if (c->P.rebase_period <= 0) c->P.rebase_period = p->window;
   c->w = p->window;
   c->r = p->rank;

@@ -173,6 +173,7 @@ struct hrom_ctx {
   // sampling and the next step's dt / masked RK3 / gathered Gram (which do not need it)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_basis_in = nullptr, ev_basis_done = nullptr;
+  bool gram_legacy = false;   // HROM_GRAM_LEGACY=1: window Gram on gather_gram_kernel (A/B measurements)
   bool basis_pending = false;  // eigen-solve launched on the side stream, not yet joined
   bool eig_todo = false;       // eigen-solve deferred (launched after the sampling kernel)
   cudaEvent_t ev_bg_in = nullptr, ev_bg_done = nullptr;

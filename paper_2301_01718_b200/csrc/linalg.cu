@@ -7,6 +7,9 @@
 // reading A13 (pinv cut 1e-12 on lambda), A14 (lagged centring; shifted Gram with
 // periodic re-base), A15 (Gram + Jacobi eigen, keep lambda_i >= 1e-8 lambda_1, sign on V).
 #include <algorithm>
+#include <cstring>
+#include <utility>
+#include <vector>
 #include "internal.cuh"
 #include "eig.cuh"
 #include "async.cuh"
@@ -216,6 +219,297 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
       }
     }
   }
+}
+
+// ---------------- H10 / K11: window Gram of contiguous (slab) rows ----------------
+// C = (S - rho 1^T)^T (S - rho 1^T) over D rows of ncol columns, ncol = 16 NSB + TAIL.  The
+// 16 NSB leading columns run on the FP64 tensor cores; the TAIL (<= 2) trailing columns -- the
+// "+1" of the w+1 window columns (A14) -- would otherwise cost a whole padded 16-column super
+// block of DMMAs (17 of 153 per k-step at w = 128, 9 of 45 at w = 64), so the producer threads
+// that already touch every element for the rho shift accumulate them with FMAs instead.
+// 4 producer warps (one per SM sub-partition, thread = one tile row, warp = one column part)
+// and 16 consumer warps (4 per sub-partition); the upper super-block pairs are assigned by the
+// host so that every sub-partition's tensor pipe gets the same DMMA count (warp w runs on
+// sub-partition w mod 4).
+constexpr int SG_PW = 4, SG_CW = 16, SG_TPW = 3;
+constexpr int SG_THREADS = 32 * (SG_PW + SG_CW);
+struct SGArgs {
+  const double* const* cols;
+  int64_t ns;       // slab slots per tile of the columns (1: plain vectors)
+  int64_t rows;
+  SRef rho;         // shift (rho.p nullable)
+  double* part;     // [grid][ncp][ncp]
+  int ncp;
+  uint8_t task[SG_CW][SG_TPW];  // (sa << 4) | sb, 0xff = none
+};
+// RPT rows per producer thread (tile = 32 RPT rows: fewer per-tile pipeline drains when the
+// per-tile DMMA work is small), STAGES smem stages, LOOK tiles in flight per producer
+template <int NSB, int TAIL>
+struct SGCfg {
+  static constexpr int ncd = 16 * NSB;
+  static constexpr int rpt = 2;
+  static constexpr int rt = 32 * rpt, ldt = rt + 4;
+  static constexpr int fit = (int)((210 * 1024) / ((size_t)ncd * ldt * sizeof(double)));
+  static constexpr int stages = fit > 8 ? 8 : fit;
+  static constexpr int lmax = NSB >= 6 || TAIL == 2 ? 2 : 3;
+  static constexpr int look = stages - 2 < lmax ? stages - 2 : lmax;
+  static constexpr size_t smem = (size_t)stages * ncd * ldt * sizeof(double);
+};
+
+template <int NSB, int TAIL>
+__global__ void __launch_bounds__(SG_THREADS, 1) slab_gram_kernel(SGArgs a) {
+  using CF = SGCfg<NSB, TAIL>;
+  constexpr int NCD = 16 * NSB, ST = CF::stages, LOOK = CF::look, NPC = NCD / SG_PW;
+  constexpr int RPT = CF::rpt, RT = CF::rt, LDT = CF::ldt, TT = TAIL > 0 ? TAIL : 1;
+  extern __shared__ double smem[];
+  __shared__ __align__(8) uint64_t full[ST], empty[ST];
+  __shared__ const double* scol[NCD + 2];
+  for (int col = threadIdx.x; col < NCD + TAIL; col += SG_THREADS) scol[col] = a.cols[col];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < ST; ++q) {
+      mbar_init(&full[q], 32 * SG_PW);
+      mbar_init(&empty[q], SG_CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ntiles = (a.rows + RT - 1) / RT;
+  const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  double* out = a.part + (int64_t)blockIdx.x * a.ncp * a.ncp;
+  if (warp < SG_PW) {
+    // ---- producers: lane = tile rows lane + 32 q (q < RPT), warp = column part (part + 4 i) ----
+    const int part = warp;
+    const SRef slab{nullptr, a.ns};
+    double rq[LOOK + 1][RPT], xq[LOOK + 1][RPT][TT];
+    bool vq[LOOK + 1][RPT];
+#pragma unroll
+    for (int q = 0; q <= LOOK; ++q)
+#pragma unroll
+      for (int h = 0; h < RPT; ++h) {
+        rq[q][h] = 0.0;
+        vq[q][h] = false;
+#pragma unroll
+        for (int t = 0; t < TT; ++t) xq[q][h][t] = 0.0;
+      }
+    double acc[TT][NPC];
+    double att[3] = {0.0, 0.0, 0.0};  // tail x tail (part 0)
+#pragma unroll
+    for (int t = 0; t < TT; ++t)
+#pragma unroll
+      for (int i = 0; i < NPC; ++i) acc[t][i] = 0.0;
+    for (int64_t it = 0; it < my_tiles + LOOK; ++it) {
+      double r_cur[RPT], x_cur[RPT][TT];
+      bool v_cur[RPT];
+#pragma unroll
+      for (int h = 0; h < RPT; ++h) {
+        r_cur[h] = 0.0;
+        v_cur[h] = false;
+#pragma unroll
+        for (int t = 0; t < TT; ++t) x_cur[h][t] = 0.0;
+      }
+      if (it < my_tiles) {
+        const int st = (int)(it % ST);
+        if (it >= ST) mbar_wait(&empty[st], (uint32_t)(((it / ST) - 1) & 1));
+        double* tile = smem + (size_t)st * NCD * LDT;
+#pragma unroll
+        for (int h = 0; h < RPT; ++h) {
+          const int k = lane + 32 * h;
+          const int64_t row = (blockIdx.x + it * gridDim.x) * RT + k;
+          if (row < a.rows) {
+            const int64_t se = sidx(slab, row);
+#pragma unroll
+            for (int i = 0; i < NPC; ++i) cp_async8(tile + (part + SG_PW * i) * LDT + k, scol[part + SG_PW * i] + se);
+            r_cur[h] = a.rho.p ? __ldg(a.rho.p + sidx(a.rho, row)) : 0.0;
+#pragma unroll
+            for (int t = 0; t < TAIL; ++t) x_cur[h][t] = __ldg(scol[NCD + t] + se);
+            v_cur[h] = true;
+          } else {
+#pragma unroll
+            for (int i = 0; i < NPC; ++i) tile[(part + SG_PW * i) * LDT + k] = 0.0;
+          }
+        }
+      }
+      cp_async_commit();
+#pragma unroll
+      for (int q = 0; q < LOOK; ++q)
+#pragma unroll
+        for (int h = 0; h < RPT; ++h) {
+          rq[q][h] = rq[q + 1][h];
+          vq[q][h] = vq[q + 1][h];
+#pragma unroll
+          for (int t = 0; t < TT; ++t) xq[q][h][t] = xq[q + 1][h][t];
+        }
+#pragma unroll
+      for (int h = 0; h < RPT; ++h) {
+        rq[LOOK][h] = r_cur[h];
+        vq[LOOK][h] = v_cur[h];
+#pragma unroll
+        for (int t = 0; t < TT; ++t) xq[LOOK][h][t] = x_cur[h][t];
+      }
+      if (it >= LOOK) {  // tile it-LOOK has landed: shift by rho, tail products, publish
+        cp_async_wait<LOOK>();
+        const int ps = (int)((it - LOOK) % ST);
+        double* tile = smem + (size_t)ps * NCD * LDT;
+#pragma unroll
+        for (int h = 0; h < RPT; ++h) {
+          if (!vq[0][h]) continue;
+          const int k = lane + 32 * h;
+          double xt[TT];
+#pragma unroll
+          for (int t = 0; t < TAIL; ++t) xt[t] = xq[0][h][t] - rq[0][h];
+#pragma unroll
+          for (int i = 0; i < NPC; ++i) {
+            double* e = tile + (part + SG_PW * i) * LDT + k;
+            const double v = *e - rq[0][h];
+            *e = v;
+#pragma unroll
+            for (int t = 0; t < TAIL; ++t) acc[t][i] = fma(xt[t], v, acc[t][i]);
+          }
+          if (TAIL > 0 && part == 0) {
+            att[0] = fma(xt[0], xt[0], att[0]);
+            if (TAIL > 1) {
+              att[1] = fma(xt[0], xt[TT - 1], att[1]);
+              att[2] = fma(xt[TT - 1], xt[TT - 1], att[2]);
+            }
+          }
+        }
+        mbar_arrive(&full[ps]);
+      }
+    }
+    cp_async_wait<0>();
+    if (TAIL > 0) {  // fixed-order butterfly over the 32 lanes of the warp
+#pragma unroll
+      for (int t = 0; t < TAIL; ++t)
+#pragma unroll
+        for (int i = 0; i < NPC; ++i) {
+          double v = acc[t][i];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if (lane == 0) out[(part + SG_PW * i) * a.ncp + NCD + t] = v;
+        }
+      if (part == 0) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) att[q] += __shfl_xor_sync(0xffffffffu, att[q], o);
+        if (lane == 0) {
+          out[NCD * a.ncp + NCD] = att[0];
+          if (TAIL > 1) {
+            out[NCD * a.ncp + NCD + 1] = att[1];
+            out[(NCD + 1) * a.ncp + NCD + 1] = att[2];
+          }
+        }
+      }
+    }
+  } else {
+    // ---- consumers: up to SG_TPW upper super-block pairs (host-balanced per sub-partition) ----
+    const int cwarp = warp - SG_PW;
+    const int gid = lane >> 2, tig = lane & 3;
+    int sa[SG_TPW], sb[SG_TPW];
+    bool has[SG_TPW];
+#pragma unroll
+    for (int t = 0; t < SG_TPW; ++t) {
+      const int v = a.task[cwarp][t];
+      has[t] = v != 0xff;
+      sa[t] = has[t] ? v >> 4 : 0;
+      sb[t] = has[t] ? v & 15 : 0;
+    }
+    double acc[SG_TPW][8];
+#pragma unroll
+    for (int t = 0; t < SG_TPW; ++t)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[t][q] = 0.0;
+    for (int64_t it = 0; it < my_tiles; ++it) {
+      const int st = (int)(it % ST);
+      mbar_wait(&full[st], (uint32_t)((it / ST) & 1));
+      const double* tile = smem + (size_t)st * NCD * LDT;
+#pragma unroll
+      for (int t = 0; t < SG_TPW; ++t) {
+        if (!has[t]) continue;
+        const double* pa = tile + (16 * sa[t] + gid) * LDT + tig;
+        const double* pb = tile + (16 * sb[t] + gid) * LDT + tig;
+        if (sa[t] != sb[t]) {
+#pragma unroll
+          for (int kk = 0; kk < RT; kk += 4) {
+            const double a0 = pa[kk], a1 = pa[8 * LDT + kk], b0 = pb[kk], b1 = pb[8 * LDT + kk];
+            dmma(acc[t][0], acc[t][1], a0, b0);
+            dmma(acc[t][2], acc[t][3], a0, b1);
+            dmma(acc[t][4], acc[t][5], a1, b0);
+            dmma(acc[t][6], acc[t][7], a1, b1);
+          }
+        } else {  // diagonal pair: the lower 8 x 8 block is the mirror of the upper one
+#pragma unroll
+          for (int kk = 0; kk < RT; kk += 4) {
+            const double a0 = pa[kk], a1 = pa[8 * LDT + kk];
+            dmma(acc[t][0], acc[t][1], a0, a0);
+            dmma(acc[t][2], acc[t][3], a0, a1);
+            dmma(acc[t][6], acc[t][7], a1, a1);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+#pragma unroll
+    for (int t = 0; t < SG_TPW; ++t) {
+      if (!has[t]) continue;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int bi = 16 * sa[t] + 8 * (q >> 1), bj = 16 * sb[t] + 8 * (q & 1);
+        out[(bi + gid) * a.ncp + bj + 2 * tig] = acc[t][2 * q];
+        out[(bi + gid) * a.ncp + bj + 2 * tig + 1] = acc[t][2 * q + 1];
+      }
+    }
+  }
+}
+
+// host: balance the upper super-block pairs (diagonal 3 DMMAs per k-step, off-diagonal 4) over
+// the 4 sub-partitions (longest first, least-loaded bin), then over each one's 4 warps
+bool sg_tasks(int nsb, SGArgs& a) {
+  std::vector<std::pair<int, int>> t;  // (cost, code)
+  for (int x = 0; x < nsb; ++x)
+    for (int y = x; y < nsb; ++y) t.push_back({x == y ? 3 : 4, (x << 4) | y});
+  std::stable_sort(t.begin(), t.end(), [](const std::pair<int, int>& u, const std::pair<int, int>& v) {
+    return u.first > v.first;
+  });
+  int load[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
+  std::memset(a.task, 0xff, sizeof(a.task));
+  for (auto& q : t) {
+    int b = 0;
+    for (int i = 1; i < 4; ++i)
+      if (load[i] < load[b]) b = i;
+    const int slot = cnt[b] / 4, w = b + 4 * (cnt[b] % 4);  // consumer warp w: sub-partition w mod 4
+    if (slot >= SG_TPW) return false;
+    a.task[w][slot] = (uint8_t)q.second;
+    load[b] += q.first;
+    ++cnt[b];
+  }
+  return true;
+}
+
+template <int NSB, int TAIL>
+hrom_status launch_slab_gram(hrom_ctx* c, SGArgs& a, int grid) {
+  const size_t smem = SGCfg<NSB, TAIL>::smem;
+  HROM_CK(cudaFuncSetAttribute(slab_gram_kernel<NSB, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  slab_gram_kernel<NSB, TAIL><<<grid, SG_THREADS, smem, c->st>>>(a);
+  HROM_LAUNCH_CK();
+  return HROM_OK;
+}
+
+// dispatch: returns HROM_E_INVALID when (ncol) has no instantiation (caller falls back)
+hrom_status run_slab_gram(hrom_ctx* c, SGArgs& a, int ncol, int grid) {
+  const int nsb = ncol / 16, tail = ncol - 16 * nsb;
+  if (!sg_tasks(nsb, a)) return HROM_E_INVALID;
+#define SG_CASE(N, T) \
+  if (nsb == N && tail == T) return launch_slab_gram<N, T>(c, a, grid);
+  SG_CASE(2, 0) SG_CASE(2, 1) SG_CASE(2, 2)
+  SG_CASE(3, 0) SG_CASE(3, 1) SG_CASE(3, 2)
+  SG_CASE(4, 0) SG_CASE(4, 1) SG_CASE(4, 2)
+  SG_CASE(6, 0) SG_CASE(6, 1)
+  SG_CASE(8, 0) SG_CASE(8, 1)
+#undef SG_CASE
+  return HROM_E_INVALID;
 }
 
 // ---------------- G7: incremental gathered Gram ----------------
@@ -1018,6 +1312,24 @@ hrom_status run_gather_gram(hrom_ctx* c, GGArgs& a, int ncol, int grid, double* 
 // Full Gram of ncol columns over `rows` rows, shifted by rho (nullable): dev_C[i*ldc+j].
 hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int64_t ns, int ncol, int64_t rows, SRef rho,
                       double* dev_C, int ldc, const int32_t* map) {
+  const int grid = c->basis_pending ? c->nsm - 1 : c->nsm;
+  if (!c->gram_legacy) {
+    SGArgs sg{};
+    sg.cols = dev_cols;
+    sg.ns = ns;
+    sg.rows = rows;
+    sg.rho = rho;
+    sg.part = c->b.part;
+    sg.ncp = 16 * (ncol / 16) + 16;
+    if ((int64_t)grid * sg.ncp * sg.ncp <= c->b.part_len && run_slab_gram(c, sg, ncol, grid) == HROM_OK) {
+      ++c->nlaunch;
+      gram_reduce<<<(ncol * ncol * GR_TPE + 255) / 256, 256, 0, c->st>>>(c->b.part, grid, sg.ncp, ncol, dev_C, ldc,
+                                                                         map);
+      HROM_LAUNCH_CK();
+      ++c->nlaunch;
+      return HROM_OK;
+    }
+  }
   GGArgs a{};
   a.mode = 0;
   a.cols = dev_cols;

@@ -468,6 +468,8 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
       }
       if (blockIdx.x == 0 && tid == 0) a.counts[8] = tot;
       for (int i = blockIdx.x * blockDim.x + tid; i < 2 * NBIN; i += G * blockDim.x) a.hist[i] = 0;
+      if (a.rre)  // the sum buffers of passes 0 and 1
+        for (int i = blockIdx.x * blockDim.x + tid; i < 4 * NBIN; i += G * blockDim.x) a.hsum[i] = 0ull;
     } else {
       const int64_t bchunk = (fw + G - 1) / G;
       const int64_t b0 = min((int64_t)blockIdx.x * bchunk, fw), b1 = min(b0 + bchunk, fw);
@@ -478,6 +480,8 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
       if (blockIdx.x == 0 && tid == 0) a.counts[8] = tot;
       // zero the first two histogram buffers
       for (int i = blockIdx.x * blockDim.x + tid; i < 2 * NBIN; i += G * blockDim.x) a.hist[i] = 0;
+      if (a.rre)  // the sum buffers of passes 0 and 1
+        for (int i = blockIdx.x * blockDim.x + tid; i < 4 * NBIN; i += G * blockDim.x) a.hsum[i] = 0ull;
     }
     grid.sync();
   sstamp(a.tdbg, ts);

@@ -196,7 +196,11 @@ def test_full_sample_set_equals_full_step(inputs):
 def test_gram_dmma_vs_oracle(orc, inputs):
     wl = small2d(inputs)
     rom = H.HybridROM(wl)
-    for ncol, rows in [(7, 1000), (33, 4097), (65, 20011), (130, 3001)]:
+    # slab_gram_kernel instantiations (16 NSB DMMA columns + a tail of <= 2 FMA columns) and
+    # column counts that fall back to gather_gram_kernel (7, 40, 130); ragged row counts
+    for ncol, rows in [(7, 1000), (32, 777), (33, 4097), (34, 3001), (40, 999), (48, 2049), (49, 5003),
+                       (50, 1001), (64, 4096), (65, 20011), (66, 2047), (96, 3333), (97, 1025), (128, 4099),
+                       (129, 3001), (130, 3001)]:
         S = inputs.random_values(ncol + 1, ncol * rows, 0.5, 1.5).reshape(ncol, rows)
         rho = inputs.random_values(ncol + 2, rows, 0.5, 1.5)
         Cg = rom.gram(dev(S), dev(rho)).cpu().numpy()
