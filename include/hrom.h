@@ -52,7 +52,8 @@ typedef struct {
   int32_t window;            /* w: snapshots in the POD window */
   int32_t rank;              /* r: POD modes ("m"), r <= w */
   int32_t halo;              /* h: per-RK-stage stencil halo, h >= recon */
-  int32_t band;              /* W: seam-band half width (square), reading A21 */
+  int32_t band;              /* W: seam-band half width (square), reading A21; -1: the whole
+                                hybrid state off S-hat (the paper's filter domain) */
   int32_t filter_orders[3];  /* Shapiro cascade, default {2,4,6} */
   int32_t n_filter_orders;
   int32_t filter_max_sweeps; /* j_max^f = 10; n_filter_orders * j_max^f <= 64 */

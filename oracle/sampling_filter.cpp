@@ -33,8 +33,13 @@ void orc_dilate_cross(const orc_grid* g, const uint8_t* in, int32_t h, uint8_t* 
 }
 
 // square Q_W = {(a,b): |a|,|b| <= W} (O13 band, reading A21)
+// W < 0: the whole grid (the paper's filter over the whole hybrid state; NEXT-2)
 void orc_dilate_square(const orc_grid* g, const uint8_t* in, int32_t W, uint8_t* out) {
   Grid G(g);
+  if (W < 0) {
+    for (int64_t n = 0; n < G.N; ++n) out[n] = 1;
+    return;
+  }
   const int Wy = (G.dim == 2) ? W : 0;
   for (int j = 0; j < G.ny; ++j)
     for (int i = 0; i < G.nx; ++i) {

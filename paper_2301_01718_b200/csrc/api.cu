@@ -172,7 +172,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   if (!(gamma > 1.0) || !(cfl > 0.0)) return HROM_E_INVALID;
   if (p->window < 2 || p->window > kMaxW || p->rank < 1 || p->rank > p->window || p->rank > kMaxR)
     return HROM_E_INVALID;
-  if (p->halo < grid->recon || p->halo > 16 || p->band < 0 || p->band > 16) return HROM_E_INVALID;
+  if (p->halo < grid->recon || p->halo > 16 || p->band < -1 || p->band > 16) return HROM_E_INVALID;
   if (p->n_filter_orders < 0 || p->n_filter_orders > 3 || p->filter_max_sweeps < 0 ||
       p->n_filter_orders * p->filter_max_sweeps > 64)
     return HROM_E_INVALID;

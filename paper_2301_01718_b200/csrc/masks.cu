@@ -678,7 +678,8 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
     const BlockRange r = thread_range(nw);
     for (int64_t w = r.w0; w < r.w1; ++w) {
       const int wq = (int)w, jq = wq / g.wpr;
-      TMP[w] = xdil_word(S, g, jq, wq - jq * g.wpr, a.band);
+      // band < 0: B = every cell off S-hat (whole-domain filter)
+      TMP[w] = a.band < 0 ? row_valid(g, wq - jq * g.wpr) : xdil_word(S, g, jq, wq - jq * g.wpr, a.band);
       HM[w] = 0u;
       const uint32_t sn = __ldcg(S + w), sp = a.do_select ? SPREV[w] : sn;
       MADD[w] = sn & ~sp;
@@ -691,7 +692,7 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
     const BlockRange r = thread_range(nw);
     for (int64_t w = r.w0; w < r.w1; ++w) {
       const int j = (int)w / g.wpr, wi = (int)w - j * g.wpr;
-      const uint32_t sq = (g.dim == 2) ? ydil_word(TMP, g, j, wi, a.band) : __ldcg(TMP + w);
+      const uint32_t sq = (g.dim == 2 && a.band >= 0) ? ydil_word(TMP, g, j, wi, a.band) : __ldcg(TMP + w);
       const uint32_t sv = __ldcg(S + w);
       B[w] = sq & ~sv;
       T[w] = sq | sv;

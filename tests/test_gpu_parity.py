@@ -115,8 +115,9 @@ def _replay_case(orc, inputs, wl, seed=5, frac=0.12, amp=0.03):
 
 
 @pytest.mark.parametrize("kw", [dict(), dict(bc=1, nx=64, ny=40), dict(dim=1, nx=500, ny=1, recon=1, w=12, r=6),
-                                dict(w=90, r=20, nx=48, ny=40)],
-                         ids=["2d-transmissive", "2d-periodic", "1d", "2d-wide-window"])
+                                dict(w=90, r=20, nx=48, ny=40), dict(W=-1), dict(W=-1, bc=1, nx=64, ny=40)],
+                         ids=["2d-transmissive", "2d-periodic", "1d", "2d-wide-window", "2d-whole-domain-filter",
+                              "2d-periodic-whole-domain-filter"])
 def test_hybrid_step_replay_parity(orc, inputs, kw):
     """One hybrid step from the same window and S-hat on both sides (Alg. 1)."""
     wl = small2d(inputs, **kw)
@@ -678,4 +679,66 @@ def test_trajectory_rre_config2(orc, inputs):
             sizes.append(int(m_o.sum()))
     rom.sync()
     assert all(0 < s < wl.N // 4 for s in sizes), sizes
+    assert worst <= 1e-11, worst
+
+
+@pytest.mark.parametrize("dim,nx,ny,bc,frac,seed", [(2, 70, 45, 0, 0.1, 7), (2, 64, 64, 1, 0.3, 8),
+                                                    (1, 3000, 1, 0, 0.05, 9)])
+def test_whole_domain_filter_parity(orc, inputs, dim, nx, ny, bc, frac, seed):
+    """W = -1 (the paper's filter over the whole hybrid state; NEXT-2): every cell off
+    S-hat is filtered; kept set and sweeps identical to the oracle, values to rounding."""
+    wl = small2d(inputs, dim=dim, nx=nx, ny=ny, bc=bc, seed=seed, W=-1)
+    rng = np.random.default_rng(seed)
+    F = inputs.initial_condition(wl, "random")
+    v = F * (1.0 + 0.05 * rng.standard_normal(F.shape))
+    S = (rng.random(wl.N) < frac).astype(np.uint8)
+    v[:, S == 1] = F[:, S == 1]
+    out, kept, sweeps = orc.seam_filter(wl, v, F, S)
+    rom = H.HybridROM(wl)
+    vg = dev(v)
+    kg = torch.zeros(wl.N, dtype=torch.uint8, device="cuda")
+    rom.filter(vg, dev(F), _mask_dev(wl, S), kept_out=kg)
+    rom.sync()
+    assert np.array_equal(kg.cpu().numpy(), kept)
+    assert kept.sum() > 0 and kept[S == 1].sum() == 0
+    cnt = rom.debug_counters(8)
+    assert list(cnt[4:4 + len(sweeps)]) == list(sweeps)
+    assert rel(vg.cpu().numpy(), out) <= 1e-14
+
+
+def test_whole_domain_filter_nyquist_gpu(inputs):
+    """Closed form (as the oracle pin): constant + exact checkerboard, periodic, S-hat empty,
+    W = -1: the order-2 sweep returns the constant bit for bit on every cell."""
+    wl = small2d(inputs, nx=64, ny=40, bc=1, W=-1)
+    F = np.empty((wl.c, wl.N))
+    F[:] = np.array([1.0, 0.25, -0.5, 2.5])[:, None]
+    i, j = np.meshgrid(np.arange(wl.nx), np.arange(wl.ny))
+    cb = ((-1.0) ** (i + j)).reshape(-1)
+    v = F + np.array([2.0 ** -10, 2.0 ** -9, 2.0 ** -8, 2.0 ** -7])[:, None] * cb[None, :]
+    rom = H.HybridROM(wl)
+    vg = dev(v)
+    kg = torch.zeros(wl.N, dtype=torch.uint8, device="cuda")
+    rom.filter(vg, dev(F), _mask_dev(wl, np.zeros(wl.N, np.uint8)), kept_out=kg)
+    rom.sync()
+    assert np.array_equal(vg.cpu().numpy(), F)
+    assert int(kg.sum().item()) == wl.N
+    assert int(rom.debug_counters(8)[4]) == 2
+
+
+def test_trajectory_whole_domain_filter_config2(orc, inputs):
+    """Algorithm 1 on config 2 with the whole-domain filter (W = -1): S-hat identical to the
+    oracle's and state <= 1e-11 step by step."""
+    wl = inputs.config(2, steps=inputs.config(2).w + 4, W=-1)
+    q0 = inputs.initial_condition(wl)
+    rom = H.HybridROM(wl)
+    rom.set_state(dev(q0))
+    R = orc.Run(wl, q0)
+    worst = 0.0
+    for k in range(1, wl.steps + 1):
+        rom.step()
+        R.step()
+        worst = max(worst, rel(rom.get_state().cpu().numpy(), R.state()))
+        if k >= wl.w - 1:
+            assert np.array_equal(H.cells_from_mask(wl, rom.mask()), R.mask()), k
+    rom.sync()
     assert worst <= 1e-11, worst

@@ -1,6 +1,7 @@
 """Pins of the oracle's sampling sets, indicator selection and seam
 filter.  Brute-force set algebra, SPEC hand examples and the closed-form
 Shapiro response 1 - sin^{2n}(theta/2)."""
+import dataclasses
 import math
 import os
 
@@ -239,3 +240,38 @@ def test_seam_filter_degenerate_bands(orc, inputs):
     # residual already zero everywhere: nothing can strictly decrease
     out, kept, _ = orc.seam_filter(wl, F, F, S)
     assert np.array_equal(out, F) and kept.sum() == 0
+
+
+@pytest.mark.parametrize("bc,seed", [(0, 5), (1, 6)])
+def test_whole_domain_filter(orc, inputs, bc, seed):
+    """W = -1: the filter runs on every cell off S-hat (the paper's whole hybrid state,
+    P:424-432; SURVEY §8(f) NEXT-2).  Same result as a square band wide enough to cover the grid;
+    S-hat untouched; the per-cell residual gate holds."""
+    wl, v, F, S = _filter_case(orc, inputs, bc, seed)
+    whole = dataclasses.replace(wl, W=-1)
+    out, kept, sweeps = orc.seam_filter(whole, v, F, S)
+    out2, kept2, sweeps2 = orc.seam_filter(dataclasses.replace(wl, W=max(wl.nx, wl.ny)), v, F, S)
+    assert np.array_equal(out, out2) and np.array_equal(kept, kept2) and sweeps == sweeps2
+    assert np.array_equal(out[:, S == 1], v[:, S == 1]) and kept[S == 1].sum() == 0
+    r_in = np.max(np.abs(v - F), axis=0)
+    r_out = np.max(np.abs(out - F), axis=0)
+    assert np.all(r_out <= r_in + 1e-14)
+    assert kept.sum() > 0
+
+
+def test_whole_domain_filter_nyquist(orc, inputs):
+    """Closed form: a constant state plus a checkerboard a(-1)^(i+j) on a periodic grid with
+    S-hat empty.  The order-2 x-pass annihilates the Nyquist mode ((1, 2, 1)/4 of (-1, 1, -1) is
+    0), so the first sweep returns the constant exactly on every cell (residual 0 < a: all kept),
+    the second keeps nothing (no strict decrease of a zero residual): output = F bit for bit."""
+    wl = _wl(inputs, nx=24, ny=16, bc=1, seed=1)
+    wl = dataclasses.replace(wl, W=-1)
+    F = np.empty((wl.c, wl.N))
+    F[:] = np.array([1.0, 0.25, -0.5, 2.5])[:, None]
+    i, j = np.meshgrid(np.arange(wl.nx), np.arange(wl.ny))
+    cb = ((-1.0) ** (i + j)).reshape(-1)
+    v = F + np.array([2.0 ** -10, 2.0 ** -9, 2.0 ** -8, 2.0 ** -7])[:, None] * cb[None, :]  # exact sums
+    out, kept, sweeps = orc.seam_filter(wl, v, F, np.zeros(wl.N, np.uint8))
+    assert np.array_equal(out, F)
+    assert kept.sum() == wl.N
+    assert sweeps[0] == 2
