@@ -72,6 +72,7 @@ def lib():
             "orc_dilate_square": (None, [P(Grid), u8, i32, u8]),
             "orc_select": (i64, [d, i64, i64, u8]),
             "orc_select_rre": (i64, [d, i64, C.c_double, u8]),
+            "orc_odeim": (i32, [d, i64, i32, i64, i32, C.c_double, C.c_void_p, C.c_void_p]),
             "orc_n_g": (i64, [C.c_double, i64]),
             "orc_lsq": (i32, [d, i64, i32, d, C.c_double, d]),
             "orc_svd": (None, [d, i64, i32, d, d, d]),
@@ -223,6 +224,19 @@ def select(eps, n_g_):
     out = np.empty(e.size, dtype=np.uint8)
     k = lib().orc_select(_d(e), e.size, n_g_, _u8(out))
     return out, k
+
+
+def odeim(phi, N, n_p, cut=1e-12):
+    """ODEIM points of phi (m x D array: column-major D x m), DOF e in cell e mod N (A36)."""
+    phi = _c(phi)
+    m, D = phi.shape
+    cells = np.zeros(n_p, dtype=np.int32)
+    rows = np.zeros(n_p, dtype=np.int64)
+    k = lib().orc_odeim(_d(phi), D, m, N, n_p, cut, cells.ctypes.data_as(C.c_void_p),
+                        rows.ctypes.data_as(C.c_void_p))
+    if k < 0:
+        raise ValueError("orc_odeim: n_p > N or m < 1")
+    return cells, rows
 
 
 def select_rre(eps, delta):

@@ -70,6 +70,11 @@ int64_t orc_select(const double* eps, int64_t N, int64_t n_g, uint8_t* mask_out)
 int64_t orc_n_g(double f, int64_t N); /* ceil(f*N) */
 /* RRE-delta rule (P:373-380 Eq. rre), used by the NEXT-1 pins */
 int64_t orc_select_rre(const double* eps, int64_t N, double delta, uint8_t* mask_out);
+/* ODEIM_{n_p} points (Eq. 10; reading A36, greedy DEIM-and-continue of S:279/S:295):
+ * Phi D x m col-major, DOF e in cell e mod N; cells_out[n_p], rows_out[n_p] (the DOF rows).
+ * Returns n_p, -1 on bad arguments (n_p > N). */
+int32_t orc_odeim(const double* Phi, int64_t D, int32_t m, int64_t N, int32_t n_p, double cut,
+                  int32_t* cells_out, int64_t* rows_out);
 
 /* ---- dense linear algebra (Eq. 8, Eq. 9) ---- */
 /* min-norm LSQ: x = A^+ b discarding sigma_i^2 < cut*sigma_1^2. A m x n col-major.

@@ -170,6 +170,50 @@ int64_t orc_select_rre(const double* eps, int64_t N, double delta, uint8_t* mask
   return ng;
 }
 
+// ODEIM_{n_p}(Phi) (Eq. 10; NEXT-1).  The cited algorithm is not in the container:
+// reading A36 = SPEC's greedy DEIM-and-continue.  Phi is D x m (col-major,
+// orthonormal columns), DOF e belongs to cell e mod N.  Point j = 1..n_p uses mode
+// l = ((j-1) mod m) + 1: c = min-norm LSQ of Phi[P, 1..l-1] c = phi_l[P] (A13 cut; P = the DOF
+// rows chosen so far), residual rho = phi_l - Phi[:, 1..l-1] c with the rows of already chosen
+// cells excluded, p_j = argmax_e |rho_e| (ties: lowest e).  The first m points are DEIM
+// (interpolation), the rest oversample.  Returns n_p, or -1 if n_p > N or m < 1.
+int32_t orc_odeim(const double* Phi, int64_t D, int32_t m, int64_t N, int32_t n_p, double cut,
+                  int32_t* cells_out, int64_t* rows_out) {
+  if (m < 1 || n_p < 0 || n_p > N) return -1;
+  std::vector<uint8_t> chosen(N, 0);
+  std::vector<int64_t> P;
+  for (int32_t j = 0; j < n_p; ++j) {
+    const int l = j % m;  // 0-based mode index
+    const double* phil = Phi + (int64_t)l * D;
+    std::vector<double> c(l, 0.0);
+    if (l > 0) {
+      const int64_t np = (int64_t)P.size();
+      std::vector<double> A(np * l), b(np);
+      for (int i = 0; i < l; ++i)
+        for (int64_t q = 0; q < np; ++q) A[(int64_t)i * np + q] = Phi[(int64_t)i * D + P[q]];
+      for (int64_t q = 0; q < np; ++q) b[q] = phil[P[q]];
+      orc_lsq(A.data(), np, l, b.data(), cut, c.data());
+    }
+    int64_t best = -1;
+    double bv = -1.0;
+    for (int64_t e = 0; e < D; ++e) {
+      if (chosen[e % N]) continue;
+      double r = phil[e];
+      for (int i = 0; i < l; ++i) r -= Phi[(int64_t)i * D + e] * c[i];
+      const double a = std::fabs(r);
+      if (a > bv) {  // strict: ties keep the lowest e
+        bv = a;
+        best = e;
+      }
+    }
+    P.push_back(best);
+    chosen[best % N] = 1;
+    cells_out[j] = (int32_t)(best % N);
+    rows_out[j] = best;
+  }
+  return n_p;
+}
+
 // Shapiro stencils (reading A24): order 2 (1,2,1)/4, 4 (-1,4,10,4,-1)/16,
 // 6 (1,-6,15,44,15,-6,1)/64.  Line ends: zeroth-order extrapolation or wrap.
 static int shapiro_coef(int order, const double** c, double* den) {

@@ -275,3 +275,64 @@ def test_whole_domain_filter_nyquist(orc, inputs):
     assert np.array_equal(out, F)
     assert kept.sum() == wl.N
     assert sweeps[0] == 2
+
+
+# ---------------- ODEIM points (Eq. 10; reading A36) ----------------
+def test_odeim_spec_examples(orc):
+    """S:295-296 worked examples: a single canonical mode e_7 -> cell 7; two canonical modes
+    e_3, e_9 -> cells {3, 9} (here D = N: one variable per cell)."""
+    e = np.zeros((1, 20))
+    e[0, 7] = 1.0
+    cells, rows = orc.odeim(e, 20, 1)
+    assert list(cells) == [7] and list(rows) == [7]
+    e = np.zeros((2, 20))
+    e[0, 3] = 1.0
+    e[1, 9] = 1.0
+    cells, rows = orc.odeim(e, 20, 2)
+    assert list(cells) == [3, 9]
+    with pytest.raises(ValueError):
+        orc.odeim(e, 20, 21)
+
+
+def _odeim_brute(phi, N, n_p):
+    """Independent re-statement of reading A36 with numpy's least squares (no shared code)."""
+    m, D = phi.shape
+    P, chosen = [], set()
+    for j in range(n_p):
+        l = j % m
+        r = phi[l].copy()
+        if l > 0:
+            A = phi[:l][:, P].T
+            c = np.linalg.lstsq(A, phi[l][P], rcond=None)[0]
+            r = phi[l] - phi[:l].T @ c
+        a = np.abs(r)
+        for e in range(D):
+            if e % N in chosen:
+                a[e] = -1.0
+        e = int(np.argmax(a))  # first maximum: lowest index
+        P.append(e)
+        chosen.add(e % N)
+    return np.array([e % N for e in P]), np.array(P)
+
+
+@pytest.mark.parametrize("m,c,N,n_p,seed", [(3, 1, 20, 3, 1), (4, 3, 30, 8, 2), (6, 4, 50, 12, 3),
+                                            (5, 4, 40, 13, 4)])
+def test_odeim_vs_brute_force_and_deim_property(orc, m, c, N, n_p, seed):
+    """Random orthonormal Phi: the same points as an independent greedy; the first m points
+    interpolate (P^T Phi nonsingular, the DEIM projector reproduces every mode), points are
+    distinct cells, oversampled points reduce the LSQ conditioning."""
+    rng = np.random.default_rng(seed)
+    Q, _ = np.linalg.qr(rng.standard_normal((c * N, m)))
+    phi = Q.T.copy()
+    cells, rows = orc.odeim(phi, N, n_p)
+    cb, rb = _odeim_brute(phi, N, n_p)
+    assert np.array_equal(rows, rb) and np.array_equal(cells, cb)
+    assert len(set(cells.tolist())) == n_p
+    PtP = phi[:, rows[:m]].T  # P^T Phi, m x m
+    assert np.linalg.matrix_rank(PtP) == m    # DEIM interpolation is well posed
+    # each point carries a nonzero greedy residual, so no column of P^T Phi is dependent
+    assert np.all(np.abs(np.diag(np.linalg.qr(PtP)[1])) > 1e-12)
+    if n_p > m:
+        s_int = np.linalg.svd(phi[:, rows[:m]], compute_uv=False)[-1]
+        s_ovs = np.linalg.svd(phi[:, rows], compute_uv=False)[-1]
+        assert s_ovs >= s_int - 1e-15  # adding rows never lowers sigma_min (Cauchy interlacing)
