@@ -123,6 +123,14 @@ hrom_status hrom_sample(hrom_ctx* ctx, double fraction, const double* dev_eps, u
 hrom_status hrom_sample_rre(hrom_ctx* ctx, double delta, const double* dev_eps, uint32_t* dev_mask_out,
                             int32_t* dev_list_out, int32_t* dev_count_out);
 
+/* NEXT-1: ODEIM_{n_p} sampling points of a basis (Eq. 10; reading A36 = greedy
+ * DEIM-and-continue over DOF rows, one row per cell, ties by lowest DOF index).
+ * dev_phi: D x m column-major (D = c N; e.g. the basis of hrom_get_basis), 1 <= m <= 64,
+ * 0 <= n_p <= min(256, N) (else HROM_E_INVALID).  Outputs (device): dev_cells_out[n_p] (int32
+ * cells), dev_rows_out[n_p] (int64 DOF rows), in selection order.  Enqueued on the stream. */
+hrom_status hrom_odeim(hrom_ctx* ctx, const double* dev_phi, int32_t m, int32_t n_p, int32_t* dev_cells_out,
+                       int64_t* dev_rows_out);
+
 /* H4-H6 standalone (gappy POD): with the current basis (Phi_{k+1}, psi_{k+1}), take the
  * values of dev_v on the cells of S-hat (dev_mask or the current sets) as HDM values,
  * y = argmin ||Phi_S y - (v - psi)_S|| (min-norm), and overwrite dev_v off S-hat

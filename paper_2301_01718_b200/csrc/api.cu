@@ -289,6 +289,13 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   A(dalloc(&b.fcnt, c->filter_blocks));
   A(dalloc(&b.colptr, 2 * kMaxSlots));
   A(dalloc(&b.slot_tab, 2 * kMaxSlots));
+  A(dalloc(&b.ochosen, g.N));
+  A(dalloc(&b.ocoef, kMaxR + 1));
+  A(dalloc(&b.orows, kOdeimMax));
+  A(dalloc(&b.opart_v, kOdeimBlocks));
+  A(dalloc(&b.opart_e, kOdeimBlocks));
+  A(dalloc(&b.ocnt, 1));
+  if (s == HROM_OK && cudaMemset(b.ocnt, 0, sizeof(unsigned int)) != cudaSuccess) s = HROM_E_CUDA;
   if (s != HROM_OK) {
     hrom_destroy(c);
     return s;
@@ -336,7 +343,7 @@ void hrom_destroy(hrom_ctx* c) {
   Bufs& b = c->b;
   void* ptrs[] = {b.ring, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
                   b.kept, b.fidx, b.ftab, b.fcur, b.fF, b.C, b.part, b.gpart, b.K, b.Khi, b.Klo, b.Rd, b.vpart, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
-                  b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.hsum, b.fstat, b.l1part, b.fcnt, (void*)b.colptr, b.slot_tab};
+                  b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.hsum, b.fstat, b.l1part, b.fcnt, (void*)b.colptr, b.slot_tab, b.ochosen, b.ocoef, b.orows, b.opart_v, b.opart_e, b.ocnt};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete c;

@@ -54,6 +54,8 @@ constexpr int kMaxW = 128;           // largest window supported (config 5)
 constexpr int kMaxSlots = kMaxW + 2; // ring slots
 constexpr int kMaxR = 64;
 constexpr int kL1Blocks = 1024;  // relative-L1 partial sums
+constexpr int kOdeimMax = 256;   // ODEIM points per call (n_p)
+constexpr int kOdeimBlocks = 4 * 148;
 
 // Geometry passed by value to kernels.
 struct Geo {
@@ -130,6 +132,13 @@ struct Bufs {
   int32_t* fcnt = nullptr;
   const double** colptr = nullptr;  // device array of column pointers (Gram)
   int32_t* slot_tab = nullptr;      // slot_tab[i] = i mod nslots
+  // ODEIM workspace (odeim.cu)
+  uint8_t* ochosen = nullptr;       // N: cell already a point
+  double* ocoef = nullptr;          // kMaxR + 1 LSQ coefficients
+  int64_t* orows = nullptr;         // kOdeimMax chosen DOF rows
+  double* opart_v = nullptr;        // per-block argmax partials
+  int64_t* opart_e = nullptr;
+  unsigned int* ocnt = nullptr;     // last-block counter
 };
 
 }  // namespace hrom

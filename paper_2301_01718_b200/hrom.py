@@ -54,6 +54,7 @@ _SIGS = {
     "hrom_update_basis": (C.c_int, [_VP]),
     "hrom_sample": (C.c_int, [_VP, C.c_double, _VP, _VP, _VP, _VP]),
     "hrom_sample_rre": (C.c_int, [_VP, C.c_double, _VP, _VP, _VP, _VP]),
+    "hrom_odeim": (C.c_int, [_VP, _VP, C.c_int32, C.c_int32, _VP, _VP]),
     "hrom_reconstruct": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "hrom_filter": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "hrom_step": (C.c_int, [_VP, C.c_double]),
@@ -214,6 +215,14 @@ class HybridROM:
         d = self.wl.delta if delta is None else delta
         _ck(self.lib.hrom_sample_rre(self.h, d, _ptr(eps), _ptr(mask_out), _ptr(list_out), _ptr(count_out)),
             "hrom_sample_rre")
+
+    def odeim(self, phi: torch.Tensor, n_p: int):
+        """ODEIM points of phi ((m, D) contiguous = D x m column-major): (cells int32, rows int64)."""
+        assert phi.dtype == torch.float64 and phi.is_contiguous() and phi.shape[1] == self.wl.D
+        cells = torch.empty(n_p, dtype=torch.int32, device="cuda")
+        rows = torch.empty(n_p, dtype=torch.int64, device="cuda")
+        _ck(self.lib.hrom_odeim(self.h, _ptr(phi), phi.shape[0], n_p, _ptr(cells), _ptr(rows)), "hrom_odeim")
+        return cells, rows
 
     def reconstruct(self, v: torch.Tensor, mask: Optional[torch.Tensor] = None,
                     y_out: Optional[torch.Tensor] = None, eps_out: Optional[torch.Tensor] = None):

@@ -742,3 +742,30 @@ def test_trajectory_whole_domain_filter_config2(orc, inputs):
             assert np.array_equal(H.cells_from_mask(wl, rom.mask()), R.mask()), k
     rom.sync()
     assert worst <= 1e-11, worst
+
+
+@pytest.mark.parametrize("kind", ["random", "pod"])
+def test_odeim_points_parity(orc, inputs, kind):
+    """NEXT-1 ODEIM points (Eq. 10, reading A36) on the device vs the oracle, both fed
+    the same basis: identical points (cells and DOF rows, in selection order) for n_p = m (DEIM)
+    and n_p = 2m + 3 (oversampling, the SPEC default 2m plus a ragged cycle)."""
+    wl = small2d(inputs, nx=70, ny=45)
+    if kind == "random":
+        rng = np.random.default_rng(12)
+        Q, _ = np.linalg.qr(rng.standard_normal((wl.D, 12)))
+        phi = np.ascontiguousarray(Q.T)
+    else:  # the oracle's POD basis of a smooth window (modes localised like the solver's)
+        snaps, S = _replay_case(orc, inputs, wl)
+        R = orc.Run(wl, snaps[0])
+        R.set_window(wl.w + 5, snaps, S)
+        phi = np.ascontiguousarray(R.basis().T)
+    m = phi.shape[0]
+    rom = H.HybridROM(wl)
+    for n_p in (m, 2 * m + 3):
+        co, ro = orc.odeim(phi, wl.N, n_p)
+        cg, rg = rom.odeim(dev(phi), n_p)
+        torch.cuda.synchronize()
+        assert np.array_equal(rg.cpu().numpy(), ro), (n_p, rg.cpu().numpy()[:8], ro[:8])
+        assert np.array_equal(cg.cpu().numpy(), co)
+    with pytest.raises(H.HromError):
+        rom.odeim(dev(phi), wl.N + 1)
