@@ -71,6 +71,9 @@ typedef struct {
                                 step k is skipped when (k+1) mod z = 0; <= 0: z = infinity */
   int32_t sample_mode;       /* selection rule of hrom_step: 0 fixed fraction (A18), 1 RRE-delta */
   double rre_delta;          /* delta of the RRE rule, in (0, 1] (sample_mode 1) */
+  int32_t odeim_points;      /* n_p > 0: S-hat_{k+1} = G_{k+1} u ODEIM_{n_p}(Phi_{k+1}) (Eq. 10)
+                                and the gappy rows are the points' DOF rows (Eq. 8); costs a lifted
+                                basis (D x r) and n_p arg-max passes per step; 0: P = S-hat (A11) */
 } hrom_params;
 
 /* Create a context for one grid.  cuda_stream: a cudaStream_t (NULL = legacy default).

@@ -85,6 +85,8 @@ def lib():
             "orc_run_step": (i32, [C.c_void_p, C.c_double]),
             "orc_run_set_full_period": (None, [C.c_void_p, i32]),
             "orc_run_set_rre": (None, [C.c_void_p, C.c_double]),
+            "orc_run_set_odeim": (None, [C.c_void_p, i32]),
+            "orc_run_points": (i32, [C.c_void_p, C.c_void_p]),
             "orc_run_k": (i64, [C.c_void_p]),
             "orc_run_state": (None, [C.c_void_p, d]),
             "orc_run_mask": (None, [C.c_void_p, u8]),
@@ -318,6 +320,8 @@ class Run:
             lib().orc_run_set_full_period(self.h, int(wl.z))
         if getattr(wl, "delta", 0.0) > 0.0:
             lib().orc_run_set_rre(self.h, float(wl.delta))
+        if getattr(wl, "n_p", 0) > 0:
+            lib().orc_run_set_odeim(self.h, int(wl.n_p))
 
     def __del__(self):
         h, self.h = getattr(self, "h", None), None
@@ -343,6 +347,12 @@ class Run:
         m = np.empty(self.wl.N, dtype=np.uint8)
         lib().orc_run_mask(self.h, _u8(m))
         return m
+
+    def points(self):
+        """DOF rows of the ODEIM points chosen for the next step (empty without ODEIM)."""
+        rows = np.zeros(max(int(getattr(self.wl, "n_p", 0)), 1), dtype=np.int64)
+        k = lib().orc_run_points(self.h, rows.ctypes.data_as(C.c_void_p))
+        return rows[:k]
 
     def mask_used(self):
         m = np.empty(self.wl.N, dtype=np.uint8)

@@ -37,6 +37,8 @@ struct orc_run {
   int32_t sweeps[3] = {0, 0, 0};
   int32_t z = 0;  // full-HDM period; <= 0: infinity
   double delta = 0.0;  // > 0: RRE-delta selection instead of the fraction f
+  int32_t odeim_np = 0;  // > 0: S-hat = G u ODEIM points, gappy rows = the points' DOF rows (Eq. 8, 10)
+  std::vector<int64_t> prow, prow_next;  // ODEIM DOF rows used by / chosen for the next step
   orc_run(const orc_grid* gg, const orc_params* pp) : g(*gg), p(*pp), G(gg) {}
 };
 
@@ -74,10 +76,19 @@ void refresh_basis(orc_run* R, const std::vector<double>& psi_k) {
 }
 
 // S-hat_{k+1} from eps: the fraction rule (A18) or, when set, the RRE-delta rule
+// With ODEIM (NEXT-1): S-hat_{k+1} = G_{k+1} u P_{k+1}, P_{k+1} = ODEIM(Phi_{k+1}).
 void select_next(orc_run* R) {
   const int64_t N = R->g.nx * (int64_t)R->g.ny;
   if (R->delta > 0.0) orc_select_rre(R->eps.data(), N, R->delta, R->mask_next.data());
   else orc_select(R->eps.data(), N, orc_n_g(R->p.f, N), R->mask_next.data());
+  R->prow_next.clear();
+  if (R->odeim_np > 0 && R->reff > 0) {
+    const int32_t np = (int32_t)std::min<int64_t>(R->odeim_np, N);
+    std::vector<int32_t> cells(np);
+    R->prow_next.resize(np);
+    orc_odeim(R->Phi.data(), R->G.D, R->reff, N, np, R->p.lsq_rel_cutoff, cells.data(), R->prow_next.data());
+    for (int32_t q = 0; q < np; ++q) R->mask_next[cells[q]] = 1;
+  }
 }
 
 void reconstruct(const orc_run* R, const std::vector<double>& y, int64_t n, double* out) {
@@ -146,20 +157,25 @@ int32_t orc_run_step(orc_run* R, double dt_override) {
     for (int64_t n = 0; n < N; ++n) T[n] = (S[n] || sq[n]) ? 1 : 0;
     std::vector<double> F(D);
     orc_masked_step(&R->g, prev.data(), R->dt, T.data(), R->p.h, F.data());
-    // gappy coordinates on the rows of S-hat (Eq. 8 with P = S-hat, A11, A12)
-    std::vector<int64_t> cells;
-    for (int64_t n = 0; n < N; ++n)
-      if (S[n]) cells.push_back(n);
-    const int64_t m = (int64_t)cells.size() * G.c;
+    // gappy coordinates on the rows of S-hat (Eq. 8 with P = S-hat, A11, A12), or on the DOF
+    // rows of the ODEIM points (Eq. 8 with P = ODEIM(Phi_k))
+    std::vector<int64_t> erows;
+    R->prow = R->prow_next;
+    if (R->odeim_np > 0) {
+      erows = R->prow;
+    } else {
+      for (int64_t n = 0; n < N; ++n)
+        if (S[n])
+          for (int v = 0; v < G.c; ++v) erows.push_back(v * N + n);
+    }
+    const int64_t m = (int64_t)erows.size();
     const int reff = R->reff;
     std::vector<double> A(m * (int64_t)reff), b(m);
-    for (size_t t = 0; t < cells.size(); ++t)
-      for (int v = 0; v < G.c; ++v) {
-        const int64_t row = (int64_t)t * G.c + v;
-        const int64_t e = v * N + cells[t];
-        b[row] = F[e] - R->psi[e];
-        for (int i = 0; i < reff; ++i) A[(int64_t)i * m + row] = R->Phi[(int64_t)i * D + e];
-      }
+    for (int64_t row = 0; row < m; ++row) {
+      const int64_t e = erows[row];
+      b[row] = F[e] - R->psi[e];
+      for (int i = 0; i < reff; ++i) A[(int64_t)i * m + row] = R->Phi[(int64_t)i * D + e];
+    }
     R->y.assign(reff, 0.0);
     orc_lsq(A.data(), m, reff, b.data(), R->p.lsq_rel_cutoff, R->y.data());
     R->ny_last = reff;
@@ -222,6 +238,11 @@ int32_t orc_run_step(orc_run* R, double dt_override) {
 
 void orc_run_set_full_period(orc_run* R, int32_t z) { R->z = z; }
 void orc_run_set_rre(orc_run* R, double delta) { R->delta = delta; }
+void orc_run_set_odeim(orc_run* R, int32_t n_p) { R->odeim_np = n_p; }
+int32_t orc_run_points(const orc_run* R, int64_t* rows) {
+  std::copy(R->prow_next.begin(), R->prow_next.end(), rows);
+  return (int32_t)R->prow_next.size();
+}
 
 int64_t orc_run_k(const orc_run* R) { return R->k; }
 void orc_run_state(const orc_run* R, double* q) { std::copy(R->snaps.back().begin(), R->snaps.back().end(), q); }
@@ -252,6 +273,15 @@ void orc_run_set_window(orc_run* R, int64_t k, const double* snaps, int32_t nsna
   const std::vector<double> psik = mean_of(R->snaps, 0, w, D);  // gamma_{k-w..k-1}
   refresh_basis(R, psik);
   std::copy(mask_next, mask_next + R->G.N, R->mask_next.begin());
+  // with ODEIM the given mask is G_{k+1}: add the points of Phi_{k+1} (as select_next does)
+  R->prow_next.clear();
+  if (R->odeim_np > 0 && R->reff > 0) {
+    const int32_t np = (int32_t)std::min<int64_t>(R->odeim_np, R->G.N);
+    std::vector<int32_t> cells(np);
+    R->prow_next.resize(np);
+    orc_odeim(R->Phi.data(), D, R->reff, R->G.N, np, R->p.lsq_rel_cutoff, cells.data(), R->prow_next.data());
+    for (int32_t q = 0; q < np; ++q) R->mask_next[cells[q]] = 1;
+  }
 }
 
 }  // extern "C"

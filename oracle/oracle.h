@@ -109,6 +109,8 @@ int32_t orc_run_step(orc_run* R, double dt_override);
 /* full-HDM period z of Algorithm 1; <= 0: infinity (the default) */
 void orc_run_set_full_period(orc_run* R, int32_t z);
 void orc_run_set_rre(orc_run* R, double delta);  /* > 0: RRE-delta sampling */
+void orc_run_set_odeim(orc_run* R, int32_t n_p);  /* > 0: S-hat = G u ODEIM points, gappy on their rows */
+int32_t orc_run_points(const orc_run* R, int64_t* rows);  /* ODEIM DOF rows chosen for the next step */
 int64_t orc_run_k(const orc_run* R);
 void orc_run_state(const orc_run* R, double* q);             /* gamma_k */
 void orc_run_mask(const orc_run* R, uint8_t* m);             /* S-hat for the NEXT step */

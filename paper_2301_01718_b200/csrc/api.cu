@@ -180,6 +180,9 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
     if (p->filter_orders[i] != 2 && p->filter_orders[i] != 4 && p->filter_orders[i] != 6) return HROM_E_INVALID;
   if (!(p->sample_fraction > 0.0 && p->sample_fraction <= 1.0)) return HROM_E_INVALID;
   if (p->sample_mode != 0 && p->sample_mode != 1) return HROM_E_INVALID;
+  if (p->odeim_points < 0 || p->odeim_points > kOdeimMax ||
+      (int64_t)p->odeim_points > (int64_t)grid->nx * (grid->dim == 2 ? grid->ny : 1))
+    return HROM_E_INVALID;
   if (p->sample_mode == 1 && !(p->rre_delta > 0.0 && p->rre_delta <= 1.0)) return HROM_E_INVALID;
   if (p->gram_mode != 0 && p->gram_mode != 1) return HROM_E_INVALID;
   if (p->gather_mode != 0 && p->gather_mode != 1) return HROM_E_INVALID;
@@ -295,6 +298,8 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   A(dalloc(&b.opart_v, kOdeimBlocks));
   A(dalloc(&b.opart_e, kOdeimBlocks));
   A(dalloc(&b.ocnt, 1));
+  A(dalloc(&b.ocells, kOdeimMax));
+  if (c->P.odeim_points > 0) A(dalloc(&b.ophi, (size_t)c->r * g.D));
   if (s == HROM_OK && cudaMemset(b.ocnt, 0, sizeof(unsigned int)) != cudaSuccess) s = HROM_E_CUDA;
   if (s != HROM_OK) {
     hrom_destroy(c);
@@ -343,7 +348,7 @@ void hrom_destroy(hrom_ctx* c) {
   Bufs& b = c->b;
   void* ptrs[] = {b.ring, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
                   b.kept, b.fidx, b.ftab, b.fcur, b.fF, b.C, b.part, b.gpart, b.K, b.Khi, b.Klo, b.Rd, b.vpart, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
-                  b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.hsum, b.fstat, b.l1part, b.fcnt, (void*)b.colptr, b.slot_tab, b.ochosen, b.ocoef, b.orows, b.opart_v, b.opart_e, b.ocnt};
+                  b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.hsum, b.fstat, b.l1part, b.fcnt, (void*)b.colptr, b.slot_tab, b.ochosen, b.ocoef, b.orows, b.opart_v, b.opart_e, b.ocnt, b.ocells, b.ophi};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete c;
@@ -496,6 +501,7 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
   const int w = c->w;
   const int64_t k = c->k;
   if (k < w - 1) return HROM_OK;
+  c->odeim_k = -1;  // a new basis: its ODEIM points are computed by the next sampling
   hrom_status s;
   basis_join(c);  // C is rewritten below
   prof_begin(c, SEC_BASIS);
@@ -578,6 +584,7 @@ hrom_status hrom_sample(hrom_ctx* c, double fraction, const double* dev_eps, uin
   // the deferred eigen-solve starts first on the side stream; the cooperative sampling kernel
   // then runs on the other SMs (grid nsm - 1), so the eigen overlaps the sampling too
   if ((s = flush_eigen(c)) != HROM_OK) return s;
+  if (c->P.odeim_points > 0 && (s = odeim_for_basis(c)) != HROM_OK) return s;
   prof_begin(c, SEC_SAMPLE);
   if ((s = select_and_build(c, dev_eps ? dev_eps : c->b.eps, n_g)) != HROM_OK) return s;
   prof_end(c, SEC_SAMPLE);
@@ -604,6 +611,7 @@ hrom_status hrom_sample_rre(hrom_ctx* c, double delta, const double* dev_eps, ui
   if (!(delta > 0.0 && delta <= 1.0)) return HROM_E_INVALID;
   hrom_status s;
   if ((s = flush_eigen(c)) != HROM_OK) return s;
+  if (c->P.odeim_points > 0 && (s = odeim_for_basis(c)) != HROM_OK) return s;
   prof_begin(c, SEC_SAMPLE);
   if ((s = select_and_build(c, dev_eps ? dev_eps : c->b.eps, 0, delta)) != HROM_OK) return s;
   prof_end(c, SEC_SAMPLE);

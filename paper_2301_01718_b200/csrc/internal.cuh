@@ -139,6 +139,8 @@ struct Bufs {
   double* opart_v = nullptr;        // per-block argmax partials
   int64_t* opart_e = nullptr;
   unsigned int* ocnt = nullptr;     // last-block counter
+  int32_t* ocells = nullptr;        // kOdeimMax point cells (Algorithm 1 with ODEIM)
+  double* ophi = nullptr;           // D x r materialised basis (only when odeim_points > 0)
 };
 
 }  // namespace hrom
@@ -182,6 +184,8 @@ struct hrom_ctx {
   // sampling and the next step's dt / masked RK3 / gathered Gram (which do not need it)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_basis_in = nullptr, ev_basis_done = nullptr;
+  int odeim_n = 0;            // ODEIM points of the current basis (0: none / not computed)
+  int64_t odeim_k = -1;       // k of the basis they belong to
   bool gram_legacy = false;   // HROM_GRAM_LEGACY=1: window Gram on gather_gram_kernel (A/B measurements)
   bool basis_pending = false;  // eigen-solve launched on the side stream, not yet joined
   bool eig_todo = false;       // eigen-solve deferred (launched after the sampling kernel)
@@ -241,6 +245,8 @@ hrom_status launch_positivity(hrom_ctx* c, SRef qprev, SRef q, int64_t kq);
 // masks.cu
 hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S);
 hrom_status select_and_build(hrom_ctx* c, const double* eps, int64_t n_g, double rre_delta = 0.0);
+hrom_status odeim_for_basis(hrom_ctx* c);           // ODEIM points of the current basis (odeim.cu)
+hrom_status or_cells_into_mask(hrom_ctx* c, uint32_t* mask, const int32_t* cells, int n);
 int sets_occupancy();
 // linalg.cu
 // dev_cols: column base pointers, all with slab stride ns (1 = plain vectors); rho: SRef or p == nullptr

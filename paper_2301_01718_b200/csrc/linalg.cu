@@ -63,6 +63,8 @@ struct GGArgs {
   const int32_t* list;
   const int32_t* count;
   SRef src_b;
+  const int64_t* rowlist;    // mode 2: explicit DOF rows (ODEIM points), count nrow2
+  int nrow2;
   // both
   SRef rho;                  // shift (rho.p nullable in mode 0)
   double* part;              // [grid][ncp][ncp]
@@ -75,12 +77,13 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
   __shared__ __align__(8) uint64_t full[ST], empty[ST];
   __shared__ const double* scol[NCP];  // column base pointers (mode 0: caller's; mode 1: ring slots)
   const int nS = a.mode == 1 ? *a.count : 0;
-  const int64_t total_rows = a.mode == 1 ? (int64_t)nS * a.g.c : a.rows;
+  const int64_t total_rows = a.mode == 1 ? (int64_t)nS * a.g.c : a.mode == 2 ? a.nrow2 : a.rows;
   const int64_t ntiles = (total_rows + RT - 1) / RT;
-  const int nU = a.mode == 1 ? a.W.nU : a.ncol0;
-  const int ncol = a.mode == 1 ? nU + 1 : a.ncol0;  // mode 1: union slots + b
+  const bool gath = a.mode >= 1;
+  const int nU = gath ? a.W.nU : a.ncol0;
+  const int ncol = gath ? nU + 1 : a.ncol0;  // modes 1, 2: union slots + b
   for (int col = threadIdx.x; col < ncol; col += CFG::threads)
-    scol[col] = a.mode == 1 ? (col < nU ? a.ring + (int64_t)a.W.slot[col] * TILE : nullptr) : a.cols[col];
+    scol[col] = gath ? (col < nU ? a.ring + (int64_t)a.W.slot[col] * TILE : nullptr) : a.cols[col];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < ST * NCP * LDT; i += CFG::threads) smem[i] = 0.0;  // padding stays 0
   if (threadIdx.x == 0) {
@@ -96,7 +99,7 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
     // ---- producers: thread (k, part) owns row k, columns part, part + parts, ... of every tile ----
     constexpr int PARTS = CFG::parts, LOOK = CFG::look;
     const int k = threadIdx.x % RT, part = threadIdx.x / RT;
-    const SRef slab{nullptr, a.mode == 1 ? a.g.nsr : a.ns};
+    const SRef slab{nullptr, gath ? a.g.nsr : a.ns};
     double rq[LOOK + 1];
     bool vq[LOOK + 1];
 #pragma unroll
@@ -114,9 +117,13 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
         const int64_t row = (blockIdx.x + it * gridDim.x) * RT + k;
         if (row < total_rows) {
           int64_t e;
-          if (a.mode == 1) {
-            const int var = (int)row / nS;  // 32-bit: c * |S-hat| < 2^31
-            e = (int64_t)var * a.g.N + __ldg(a.list + ((int)row - var * nS));
+          if (gath) {
+            if (a.mode == 2) {
+              e = __ldg(a.rowlist + row);
+            } else {
+              const int var = (int)row / nS;  // 32-bit: c * |S-hat| < 2^31
+              e = (int64_t)var * a.g.N + __ldg(a.list + ((int)row - var * nS));
+            }
             const int64_t se = sidx(slab, e);
             for (int col = part; col < nU; col += PARTS) cp_async8(tile + col * LDT + k, scol[col] + se);
             if (nU % PARTS == part) cp_async8(tile + nU * LDT + k, a.src_b.p + sidx(a.src_b, e));
@@ -1357,6 +1364,14 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   const int grid = c->basis_pending ? c->nsm - 1 : c->nsm;
   const int ncol = a.W.nU + 1;
   double* R = c->b.eigV;
+  if (c->P.odeim_points > 0) {  // gappy rows = the DOF rows of the ODEIM points (Eq. 8, 10)
+    a.mode = 2;
+    a.rowlist = c->b.orows;
+    a.nrow2 = c->odeim_n;
+    c->kinc_valid = false;
+    c->samples_since_gather = 0;
+    return run_gather_gram(c, a, ncol, grid, R, ncol, nullptr);
+  }
   const bool inc = c->P.gather_mode == 0 && c->kinc_valid && c->samples_since_gather == 1 && c->kinc_newest == c->k - 1 &&
                    c->kinc_rebase == c->rebase_k;
   hrom_status s;

@@ -104,6 +104,8 @@ struct SetsArgs {
   unsigned long long rre_dm;  // delta = rre_dm * 2^-rre_sh exactly (rre_dm < 2^53)
   int rre_sh;
   unsigned long long* hsum;  // 3 x 2 x NBIN exact bucket sums (RRE mode)
+  const int32_t* extra;      // cells OR'ed into S-hat after the selection (ODEIM points)
+  int n_extra;
   int halo, band, rmax;
   uint32_t* masks;     // M_COUNT masks of mwords
   int64_t mwords;
@@ -665,6 +667,11 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
           atomicOr(&S[(int64_t)j * g.wpr + (i >> 5)], 1u << (i & 31));
         }
       }
+      if (blockIdx.x == 0)  // S-hat = G u P (ODEIM points)
+        for (int q = tid; q < a.n_extra; q += blockDim.x) {
+          const int ci = __ldg(a.extra + q), j = ci / g.nx, i = ci - j * g.nx;
+          atomicOr(&S[(int64_t)j * g.wpr + (i >> 5)], 1u << (i & 31));
+        }
     }
     grid.sync();
   sstamp(a.tdbg, ts);
@@ -899,6 +906,10 @@ hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long lon
     a.rre_sh = 53 - ex;
   }
   a.hsum = c->b.hsum;
+  if (do_select && c->P.odeim_points > 0) {
+    a.extra = c->b.ocells;
+    a.n_extra = c->odeim_n;
+  }
   a.cand = sparse ? c->b.lists + (int64_t)L_T * c->g.N : nullptr;
   a.ncand = c->b.counts + L_T;
   a.g = c->g;
@@ -939,6 +950,21 @@ namespace {
 
 }  // namespace
 
+__global__ void or_cells_kernel(Geo g, uint32_t* S, const int32_t* cells, int n) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int ci = cells[q], j = ci / g.nx, i = ci - j * g.nx;
+    atomicOr(&S[(int64_t)j * g.wpr + (i >> 5)], 1u << (i & 31));
+  }
+}
+
+hrom_status or_cells_into_mask(hrom_ctx* c, uint32_t* mask, const int32_t* cells, int n) {
+  if (n <= 0) return HROM_OK;
+  or_cells_kernel<<<1, 256, 0, c->st>>>(c->g, mask, cells, n);
+  HROM_LAUNCH_CK();
+  ++c->nlaunch;
+  return HROM_OK;
+}
+
 // S-hat bitmap (in masks[M_S]) -> B, T, A2, A1 bitmaps, their ascending lists and the
 // seam-filter tables.
 hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S) {
@@ -946,6 +972,11 @@ hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S) {
   uint32_t* S = c->b.masks + (int64_t)M_S * c->mwords;
   if (dev_mask_S && dev_mask_S != S)
     HROM_CK(cudaMemcpyAsync(S, dev_mask_S, c->mwords * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->st));
+  if (c->P.odeim_points > 0 && c->basis_ready) {  // an explicit mask is G: S-hat = G u ODEIM points
+    hrom_status s = odeim_for_basis(c);
+    if (s != HROM_OK) return s;
+    if ((s = or_cells_into_mask(c, S, c->b.ocells, c->odeim_n)) != HROM_OK) return s;
+  }
   return launch_sets(c, false, nullptr, 0);
 }
 

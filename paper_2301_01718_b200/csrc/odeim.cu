@@ -176,3 +176,25 @@ extern "C" hrom_status hrom_odeim(hrom_ctx* c, const double* dev_phi, int32_t m,
   }
   return HROM_OK;
 }
+
+namespace hrom {
+// Algorithm 1 with ODEIM: the points of Phi_{k+1} (lifted into b.ophi) for the next step.  The
+// greedy needs r_eff on the host (one stream synchronisation per basis); only in this mode.
+hrom_status odeim_for_basis(hrom_ctx* c) {
+  if (c->odeim_k == c->k && c->odeim_n > 0) return HROM_OK;
+  if (!c->basis_ready) return HROM_E_STATE;
+  basis_join(c);
+  hrom_status s = lift(c, c->win, c->b.ophi, nullptr);
+  if (s != HROM_OK) return s;
+  int32_t reff = 0;
+  HROM_CK(cudaMemcpyAsync(&reff, c->b.ireg, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
+  HROM_CK(cudaStreamSynchronize(c->st));
+  const int np = (int)std::min<int64_t>(c->P.odeim_points, c->g.N);
+  c->odeim_n = 0;
+  if (reff < 1) return HROM_OK;
+  if ((s = hrom_odeim(c, c->b.ophi, reff, np, c->b.ocells, c->b.orows)) != HROM_OK) return s;
+  c->odeim_n = np;
+  c->odeim_k = c->k;
+  return HROM_OK;
+}
+}  // namespace hrom

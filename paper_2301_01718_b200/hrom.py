@@ -39,7 +39,7 @@ class Params(C.Structure):
                 ("eig_rel_cutoff", C.c_double), ("lsq_rel_cutoff", C.c_double),
                 ("sample_fraction", C.c_double), ("gram_mode", C.c_int32), ("rebase_period", C.c_int32),
                 ("gather_mode", C.c_int32), ("full_period", C.c_int32),
-                ("sample_mode", C.c_int32), ("rre_delta", C.c_double)]
+                ("sample_mode", C.c_int32), ("rre_delta", C.c_double), ("odeim_points", C.c_int32)]
 
 
 # every entry point of include/hrom.h with its ctypes signature
@@ -164,7 +164,8 @@ class HybridROM:
         p = Params(wl.w, wl.r, wl.h, wl.W, fo, len(wl.filter_orders), wl.filter_max_sweeps, wl.filter_eps,
                    wl.eig_rel_cutoff, wl.lsq_rel_cutoff, wl.f, gram_mode, rebase_period, gather_mode,
                    getattr(wl, "z", 0) if full_period is None else full_period,
-                   1 if getattr(wl, "delta", 0.0) > 0.0 else 0, float(getattr(wl, "delta", 0.0)))
+                   1 if getattr(wl, "delta", 0.0) > 0.0 else 0, float(getattr(wl, "delta", 0.0)),
+                   int(getattr(wl, "n_p", 0)))
         h = C.c_void_p()
         _ck(self.lib.hrom_create(C.byref(g), wl.gamma, wl.cfl, C.byref(p), C.c_void_p(self.stream.cuda_stream),
                                  C.byref(h)), "hrom_create")

@@ -98,6 +98,7 @@ class Workload:
     lsq_rel_cutoff: float = 1e-12
     z: int = 0             # full-HDM period of Algorithm 1; 0 = infinity (A20)
     delta: float = 0.0     # > 0: RRE-delta selection instead of the fraction f
+    n_p: int = 0           # > 0: ODEIM points added to S-hat; gappy rows = their DOF rows
 
     @property
     def c(self) -> int:

@@ -769,3 +769,46 @@ def test_odeim_points_parity(orc, inputs, kind):
         assert np.array_equal(cg.cpu().numpy(), co)
     with pytest.raises(H.HromError):
         rom.odeim(dev(phi), wl.N + 1)
+
+
+@pytest.mark.parametrize("kw", [dict(n_p=10), dict(n_p=13, bc=1, nx=64, ny=40), dict(dim=1, nx=500, ny=1, recon=1, w=12,
+                                                                                   r=6, n_p=12)],
+                         ids=["2d", "2d-periodic", "1d"])
+def test_hybrid_step_replay_odeim(orc, inputs, kw):
+    """Algorithm 1 with ODEIM points (NEXT-1): the given mask is G, S-hat = G u P with
+    P = ODEIM(Phi_{k+1}); the gappy rows are the points' DOF rows (Eq. 8).  Same S-hat and the
+    same hybrid step as the oracle (<= 1e-12)."""
+    wl = small2d(inputs, **kw)
+    snaps, S = _replay_case(orc, inputs, wl, frac=0.05)
+    k = wl.w + 5
+    R = orc.Run(wl, snaps[0])
+    R.set_window(k, snaps, S)
+    rom = H.HybridROM(wl)
+    rom.set_window(k, dev(snaps.reshape(wl.w + 1, -1)), _mask_dev(wl, S))
+    mo = R.mask()
+    assert mo.sum() > S.sum()  # the points add cells
+    assert np.array_equal(H.cells_from_mask(wl, rom.mask()), mo)
+    dt = orc.dt(wl, snaps[-1])
+    R.step(dt)
+    rom.hybrid_step(dt=dt)
+    rom.sync()
+    assert rel(rom.get_state().cpu().numpy(), R.state()) <= 1e-12
+
+
+def test_trajectory_odeim_config1(orc, inputs):
+    """Config 1 with ODEIM points (n_p = 2r = 20, the SPEC default) added to the fraction rule:
+    S-hat identical to the oracle's and state <= 1e-11 step by step."""
+    wl = inputs.config(1, steps=inputs.config(1).w + 20, n_p=20)
+    q0 = inputs.initial_condition(wl)
+    rom = H.HybridROM(wl)
+    rom.set_state(dev(q0))
+    R = orc.Run(wl, q0)
+    worst = 0.0
+    for k in range(1, wl.steps + 1):
+        rom.step()
+        R.step()
+        worst = max(worst, rel(rom.get_state().cpu().numpy(), R.state()))
+        if k >= wl.w - 1:
+            assert np.array_equal(H.cells_from_mask(wl, rom.mask()), R.mask()), k
+    rom.sync()
+    assert worst <= 1e-11, worst
