@@ -41,7 +41,9 @@ struct GGCfg {
   static constexpr int nsb = NSB, rt = RT, tpw = TPW, cw = CW, stages = STAGES, look = LOOK;
   static constexpr int pw = PW, ncp = 16 * NSB, ldt = RT + 4, threads = 32 * (PW + CW);
   static constexpr int parts = 32 * PW / RT;  // producer threads per tile row (columns split)
-  static constexpr size_t smem = (size_t)STAGES * ncp * ldt * sizeof(double);
+  // per stage: the tile, then each producer part's copy of the shift of its rows (cp.async'd
+  // with the tile, so no pending global load is carried across iterations in registers)
+  static constexpr size_t smem = (size_t)STAGES * (ncp * ldt + parts * RT) * sizeof(double);
   static_assert(CW * TPW >= NSB * (NSB + 1) / 2, "tasks");
   static_assert((32 * PW) % RT == 0 && STAGES >= LOOK + 2, "producer layout");
 };
@@ -100,16 +102,8 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
     constexpr int PARTS = CFG::parts, LOOK = CFG::look;
     const int k = threadIdx.x % RT, part = threadIdx.x / RT;
     const SRef slab{nullptr, gath ? a.g.nsr : a.ns};
-    double rq[LOOK + 1];
-    bool vq[LOOK + 1];
-#pragma unroll
-    for (int q = 0; q <= LOOK; ++q) {
-      rq[q] = 0.0;
-      vq[q] = false;
-    }
+    double* ext0 = smem + (size_t)ST * NCP * LDT;  // [stage][part][RT] shifts
     for (int64_t it = 0; it < my_tiles + LOOK; ++it) {
-      double r_cur = 0.0;
-      bool v_cur = false;
       if (it < my_tiles) {
         const int st = (int)(it % ST);
         if (it >= ST) mbar_wait(&empty[st], (uint32_t)(((it / ST) - 1) & 1));
@@ -132,27 +126,23 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
             const int64_t se = sidx(slab, e);
             for (int col = part; col < ncol; col += PARTS) cp_async8(tile + col * LDT + k, scol[col] + se);
           }
-          r_cur = a.rho.p ? __ldg(a.rho.p + sidx(a.rho, e)) : 0.0;
-          v_cur = true;
+          double* ext = ext0 + ((size_t)st * PARTS + part) * RT;
+          if (a.rho.p) cp_async8(ext + k, a.rho.p + sidx(a.rho, e));
+          else ext[k] = 0.0;
         } else {
           for (int col = part; col < ncol; col += PARTS) tile[col * LDT + k] = 0.0;
         }
       }
       cp_async_commit();
-      // register ring of the shifts of the tiles in flight (static indices after unrolling)
-#pragma unroll
-      for (int q = 0; q < LOOK; ++q) {
-        rq[q] = rq[q + 1];
-        vq[q] = vq[q + 1];
-      }
-      rq[LOOK] = r_cur;
-      vq[LOOK] = v_cur;
       if (it >= LOOK) {  // tile it-LOOK has landed: shift by rho, publish
         cp_async_wait<LOOK>();
-        const int ps = (int)((it - LOOK) % ST);
+        const int64_t pit = it - LOOK;
+        const int ps = (int)(pit % ST);
         double* tile = smem + (size_t)ps * NCP * LDT;
-        if (vq[0])
-          for (int col = part; col < ncol; col += PARTS) tile[col * LDT + k] -= rq[0];
+        if ((blockIdx.x + pit * gridDim.x) * RT + k < total_rows) {
+          const double rh = ext0[((size_t)ps * PARTS + part) * RT + k];
+          for (int col = part; col < ncol; col += PARTS) tile[col * LDT + k] -= rh;
+        }
         mbar_arrive(&full[ps]);
       }
     }
@@ -256,11 +246,14 @@ struct SGCfg {
   static constexpr int ncd = 16 * NSB;
   static constexpr int rpt = 2;
   static constexpr int rt = 32 * rpt, ldt = rt + 4;
-  static constexpr int fit = (int)((210 * 1024) / ((size_t)ncd * ldt * sizeof(double)));
+  // per stage: the tile, and per producer warp the shift and tail values of its rows (landed by
+  // cp.async with the tile: no global load result is carried across iterations in registers)
+  static constexpr int ext = SG_PW * (1 + TAIL) * rt;
+  static constexpr size_t stage_bytes = ((size_t)ncd * ldt + ext) * sizeof(double);
+  static constexpr int fit = (int)((225 * 1024) / stage_bytes);
   static constexpr int stages = fit > 8 ? 8 : fit;
-  static constexpr int lmax = NSB >= 6 || TAIL == 2 ? 2 : 3;
-  static constexpr int look = stages - 2 < lmax ? stages - 2 : lmax;
-  static constexpr size_t smem = (size_t)stages * ncd * ldt * sizeof(double);
+  static constexpr int look = stages - 2 < 3 ? stages - 2 : 3;
+  static constexpr size_t smem = (size_t)stages * stage_bytes;
 };
 
 template <int NSB, int TAIL>
@@ -288,17 +281,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) slab_gram_kernel(SGArgs a) {
     // ---- producers: lane = tile rows lane + 32 q (q < RPT), warp = column part (part + 4 i) ----
     const int part = warp;
     const SRef slab{nullptr, a.ns};
-    double rq[LOOK + 1][RPT], xq[LOOK + 1][RPT][TT];
-    bool vq[LOOK + 1][RPT];
-#pragma unroll
-    for (int q = 0; q <= LOOK; ++q)
-#pragma unroll
-      for (int h = 0; h < RPT; ++h) {
-        rq[q][h] = 0.0;
-        vq[q][h] = false;
-#pragma unroll
-        for (int t = 0; t < TT; ++t) xq[q][h][t] = 0.0;
-      }
+    double* ext0 = smem + (size_t)ST * NCD * LDT;  // [stage][part][1 + TAIL][RT]
     double acc[TT][NPC];
     double att[3] = {0.0, 0.0, 0.0};  // tail x tail (part 0)
 #pragma unroll
@@ -306,19 +289,11 @@ __global__ void __launch_bounds__(SG_THREADS, 1) slab_gram_kernel(SGArgs a) {
 #pragma unroll
       for (int i = 0; i < NPC; ++i) acc[t][i] = 0.0;
     for (int64_t it = 0; it < my_tiles + LOOK; ++it) {
-      double r_cur[RPT], x_cur[RPT][TT];
-      bool v_cur[RPT];
-#pragma unroll
-      for (int h = 0; h < RPT; ++h) {
-        r_cur[h] = 0.0;
-        v_cur[h] = false;
-#pragma unroll
-        for (int t = 0; t < TT; ++t) x_cur[h][t] = 0.0;
-      }
       if (it < my_tiles) {
         const int st = (int)(it % ST);
         if (it >= ST) mbar_wait(&empty[st], (uint32_t)(((it / ST) - 1) & 1));
         double* tile = smem + (size_t)st * NCD * LDT;
+        double* ext = ext0 + ((size_t)st * SG_PW + part) * (1 + TAIL) * RT;
 #pragma unroll
         for (int h = 0; h < RPT; ++h) {
           const int k = lane + 32 * h;
@@ -327,10 +302,10 @@ __global__ void __launch_bounds__(SG_THREADS, 1) slab_gram_kernel(SGArgs a) {
             const int64_t se = sidx(slab, row);
 #pragma unroll
             for (int i = 0; i < NPC; ++i) cp_async8(tile + (part + SG_PW * i) * LDT + k, scol[part + SG_PW * i] + se);
-            r_cur[h] = a.rho.p ? __ldg(a.rho.p + sidx(a.rho, row)) : 0.0;
+            if (a.rho.p) cp_async8(ext + k, a.rho.p + sidx(a.rho, row));
+            else ext[k] = 0.0;
 #pragma unroll
-            for (int t = 0; t < TAIL; ++t) x_cur[h][t] = __ldg(scol[NCD + t] + se);
-            v_cur[h] = true;
+            for (int t = 0; t < TAIL; ++t) cp_async8(ext + (1 + t) * RT + k, scol[NCD + t] + se);
           } else {
 #pragma unroll
             for (int i = 0; i < NPC; ++i) tile[(part + SG_PW * i) * LDT + k] = 0.0;
@@ -338,37 +313,24 @@ __global__ void __launch_bounds__(SG_THREADS, 1) slab_gram_kernel(SGArgs a) {
         }
       }
       cp_async_commit();
-#pragma unroll
-      for (int q = 0; q < LOOK; ++q)
-#pragma unroll
-        for (int h = 0; h < RPT; ++h) {
-          rq[q][h] = rq[q + 1][h];
-          vq[q][h] = vq[q + 1][h];
-#pragma unroll
-          for (int t = 0; t < TT; ++t) xq[q][h][t] = xq[q + 1][h][t];
-        }
-#pragma unroll
-      for (int h = 0; h < RPT; ++h) {
-        rq[LOOK][h] = r_cur[h];
-        vq[LOOK][h] = v_cur[h];
-#pragma unroll
-        for (int t = 0; t < TT; ++t) xq[LOOK][h][t] = x_cur[h][t];
-      }
       if (it >= LOOK) {  // tile it-LOOK has landed: shift by rho, tail products, publish
         cp_async_wait<LOOK>();
-        const int ps = (int)((it - LOOK) % ST);
+        const int64_t pit = it - LOOK;
+        const int ps = (int)(pit % ST);
         double* tile = smem + (size_t)ps * NCD * LDT;
+        const double* ext = ext0 + ((size_t)ps * SG_PW + part) * (1 + TAIL) * RT;
 #pragma unroll
         for (int h = 0; h < RPT; ++h) {
-          if (!vq[0][h]) continue;
           const int k = lane + 32 * h;
+          if ((blockIdx.x + pit * gridDim.x) * RT + k >= a.rows) continue;
+          const double rh = ext[k];
           double xt[TT];
 #pragma unroll
-          for (int t = 0; t < TAIL; ++t) xt[t] = xq[0][h][t] - rq[0][h];
+          for (int t = 0; t < TAIL; ++t) xt[t] = ext[(1 + t) * RT + k] - rh;
 #pragma unroll
           for (int i = 0; i < NPC; ++i) {
             double* e = tile + (part + SG_PW * i) * LDT + k;
-            const double v = *e - rq[0][h];
+            const double v = *e - rh;
             *e = v;
 #pragma unroll
             for (int t = 0; t < TAIL; ++t) acc[t][i] = fma(xt[t], v, acc[t][i]);
