@@ -193,6 +193,12 @@ int64_t hrom_mask_words(const hrom_ctx* ctx);                        /* words pe
  * dev_rho (nullable = 0), dev_C: ncol*ncol output. Standalone op (config 5). */
 hrom_status hrom_gram(hrom_ctx* ctx, const double* const* dev_cols, int32_t ncol, int64_t rows,
                       const double* dev_rho, double* dev_C);
+/* Projection of the window on a basis (config 5 kernel op):
+ * dev_C[i * (w+1) + j] = sum_e Phi[e][i] gamma_{k-w+j}[e] for the w + 1 window columns of the
+ * current basis (oldest first), on FP64 tensor cores.  dev_phi: D x m column-major (device,
+ * m <= 64; e.g. hrom_get_basis), dev_C: m (w+1) doubles.  Supported (ceil(m/16), ceil((w+1)/16)):
+ * (1,1..5) (2,2..5) (4,9), else HROM_E_INVALID.  HROM_E_STATE before the first basis. */
+hrom_status hrom_project(hrom_ctx* ctx, const double* dev_phi, int32_t m, double* dev_C);
 /* Overwrite gamma_k (the latest snapshot) in place, without touching the schedule
  * (end-to-end benchmarking of host-resident states).  The window Gram and the basis already
  * built from gamma_k are kept: the caller supplies the same state (e.g. a host round trip);

@@ -827,6 +827,15 @@ hrom_status hrom_gram(hrom_ctx* c, const double* const* dev_cols, int32_t ncol, 
   return gram_full(c, dev_cols, 1, ncol, rows, plain(dev_rho), dev_C, ncol, nullptr);
 }
 
+hrom_status hrom_project(hrom_ctx* c, const double* dev_phi, int32_t m, double* dev_C) {
+  if (!c || !dev_phi || !dev_C || m < 1 || m > kMaxR) return HROM_E_INVALID;
+  if (!c->basis_ready) return HROM_E_STATE;
+  basis_join(c);
+  std::vector<const double*> cols(m);
+  for (int i = 0; i < m; ++i) cols[i] = dev_phi + (int64_t)i * c->g.D;
+  return project_window(c, cols.data(), m, dev_C);
+}
+
 hrom_status hrom_put_state(hrom_ctx* c, const double* any_q) {
   if (!c || !any_q) return HROM_E_INVALID;
   if (c->k < 0) return HROM_E_STATE;

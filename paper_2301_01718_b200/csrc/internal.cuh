@@ -245,7 +245,8 @@ hrom_status launch_positivity(hrom_ctx* c, SRef qprev, SRef q, int64_t kq);
 // masks.cu
 hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S);
 hrom_status select_and_build(hrom_ctx* c, const double* eps, int64_t n_g, double rre_delta = 0.0);
-hrom_status odeim_for_basis(hrom_ctx* c);           // ODEIM points of the current basis (odeim.cu)
+hrom_status odeim_for_basis(hrom_ctx* c);
+hrom_status project_window(hrom_ctx* c, const double* const* phicols, int m, double* dev_C);           // ODEIM points of the current basis (odeim.cu)
 hrom_status or_cells_into_mask(hrom_ctx* c, uint32_t* mask, const int32_t* cells, int n);
 int sets_occupancy();
 // linalg.cu

@@ -481,6 +481,172 @@ hrom_status run_slab_gram(hrom_ctx* c, SGArgs& a, int ncol, int grid) {
   return HROM_E_INVALID;
 }
 
+// ---------------- config 5: projection Phi^T S of the window (cross Gram, DMMA) ----------------
+// C[i][j] = sum_e Phi[e][i] S_j[e] over the D rows: Phi (D x m, plain columns, m <= 64) against the
+// w + 1 ring columns of the window (slab layout).  Same warp specialisation as slab_gram_kernel:
+// 4 producer warps (lane = row, warp = column part) stage 32-row tiles of all 16 (NA + NB) columns
+// (padding columns stay zero), 16 consumer warps own 16 x 16 (A block, B block) pairs balanced per
+// sub-partition by the host.  Per-CTA partials reduced in fixed order by cross_reduce.
+constexpr int XG_RT = 32, XG_LDT = XG_RT + 4;
+struct XGArgs {
+  const double* colA[kMaxR];
+  int ncA;
+  const double* ring;
+  Win W;               // B columns: the nU union slots (window order)
+  int64_t nsr, rows;
+  double* part;        // [grid][16 NA][16 NB]
+  uint8_t task[SG_CW][SG_TPW];  // (a << 4) | b
+};
+template <int NA, int NB>
+struct XGCfg {
+  static constexpr int nc = 16 * (NA + NB);
+  static constexpr size_t stage_bytes = (size_t)nc * XG_LDT * sizeof(double);
+  static constexpr int fit = (int)((225 * 1024) / stage_bytes);
+  static constexpr int stages = fit > 6 ? 6 : fit;
+  static constexpr int look = stages - 2 < 3 ? stages - 2 : 3;
+  static constexpr size_t smem = (size_t)stages * stage_bytes;
+};
+
+template <int NA, int NB>
+__global__ void __launch_bounds__(SG_THREADS, 1) cross_gram_kernel(XGArgs a) {
+  using CF = XGCfg<NA, NB>;
+  constexpr int NC = CF::nc, ST = CF::stages, LOOK = CF::look, RT = XG_RT, LDT = XG_LDT;
+  extern __shared__ double smem[];
+  __shared__ __align__(8) uint64_t full[ST], empty[ST];
+  __shared__ const double* scol[NC];
+  __shared__ int64_t sns[NC];
+  for (int col = threadIdx.x; col < NC; col += SG_THREADS) {
+    const int cb = col - 16 * NA;
+    if (col < 16 * NA) {
+      scol[col] = col < a.ncA ? a.colA[col] : nullptr;
+      sns[col] = 1;
+    } else {
+      scol[col] = cb < a.W.nU ? a.ring + (int64_t)a.W.slot[cb] * TILE : nullptr;
+      sns[col] = a.nsr;
+    }
+  }
+  for (int i = threadIdx.x; i < ST * NC * LDT; i += SG_THREADS) smem[i] = 0.0;  // padding columns stay 0
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < ST; ++q) {
+      mbar_init(&full[q], 32 * SG_PW);
+      mbar_init(&empty[q], SG_CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ntiles = (a.rows + RT - 1) / RT;
+  const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (warp < SG_PW) {
+    const int part = warp, k = lane;
+    for (int64_t it = 0; it < my_tiles + LOOK; ++it) {
+      if (it < my_tiles) {
+        const int st = (int)(it % ST);
+        if (it >= ST) mbar_wait(&empty[st], (uint32_t)(((it / ST) - 1) & 1));
+        double* tile = smem + (size_t)st * NC * LDT;
+        const int64_t row = (blockIdx.x + it * gridDim.x) * RT + k;
+        for (int col = part; col < NC; col += SG_PW) {
+          const double* src = scol[col];
+          if (!src) continue;
+          if (row < a.rows) cp_async8(tile + col * LDT + k, src + sidx(SRef{nullptr, sns[col]}, row));
+          else tile[col * LDT + k] = 0.0;
+        }
+      }
+      cp_async_commit();
+      if (it >= LOOK) {
+        cp_async_wait<LOOK>();
+        mbar_arrive(&full[(int)((it - LOOK) % ST)]);
+      }
+    }
+    cp_async_wait<0>();
+  } else {
+    const int cwarp = warp - SG_PW;
+    const int gid = lane >> 2, tig = lane & 3;
+    int sa[SG_TPW], sb[SG_TPW];
+    bool has[SG_TPW];
+#pragma unroll
+    for (int t = 0; t < SG_TPW; ++t) {
+      const int v = a.task[cwarp][t];
+      has[t] = v != 0xff;
+      sa[t] = has[t] ? v >> 4 : 0;
+      sb[t] = has[t] ? v & 15 : 0;
+    }
+    double acc[SG_TPW][8];
+#pragma unroll
+    for (int t = 0; t < SG_TPW; ++t)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[t][q] = 0.0;
+    for (int64_t it = 0; it < my_tiles; ++it) {
+      const int st = (int)(it % ST);
+      mbar_wait(&full[st], (uint32_t)((it / ST) & 1));
+      const double* tile = smem + (size_t)st * NC * LDT;
+#pragma unroll
+      for (int t = 0; t < SG_TPW; ++t) {
+        if (!has[t]) continue;
+        const double* pa = tile + (16 * sa[t] + gid) * LDT + tig;
+        const double* pb = tile + (16 * (NA + sb[t]) + gid) * LDT + tig;
+#pragma unroll
+        for (int kk = 0; kk < RT; kk += 4) {
+          const double a0 = pa[kk], a1 = pa[8 * LDT + kk], b0 = pb[kk], b1 = pb[8 * LDT + kk];
+          dmma(acc[t][0], acc[t][1], a0, b0);
+          dmma(acc[t][2], acc[t][3], a0, b1);
+          dmma(acc[t][4], acc[t][5], a1, b0);
+          dmma(acc[t][6], acc[t][7], a1, b1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    double* out = a.part + (int64_t)blockIdx.x * (16 * NA) * (16 * NB);
+#pragma unroll
+    for (int t = 0; t < SG_TPW; ++t) {
+      if (!has[t]) continue;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int bi = 16 * sa[t] + 8 * (q >> 1), bj = 16 * sb[t] + 8 * (q & 1);
+        out[(bi + gid) * (16 * NB) + bj + 2 * tig] = acc[t][2 * q];
+        out[(bi + gid) * (16 * NB) + bj + 2 * tig + 1] = acc[t][2 * q + 1];
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) cross_reduce(const double* __restrict__ part, int nblk, int lda, int ldb, int m,
+                                                    int n, double* __restrict__ C) {
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int idx = (int)(gt / GR_TPE), sub = (int)(gt % GR_TPE);
+  const int i = idx / n, j = idx % n;
+  const bool act = idx < m * n;
+  double s = 0.0;
+  if (act)
+    for (int b = sub; b < nblk; b += GR_TPE) s += part[(int64_t)b * lda * ldb + i * ldb + j];
+  for (int o = GR_TPE / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (act && sub == 0) C[i * n + j] = s;
+}
+
+// host: all NA x NB pairs cost 4 DMMAs per k-step; round-robin over the sub-partitions
+bool xg_tasks(int na, int nb, XGArgs& a) {
+  std::memset(a.task, 0xff, sizeof(a.task));
+  int cnt[4] = {0, 0, 0, 0}, q = 0;
+  for (int x = 0; x < na; ++x)
+    for (int y = 0; y < nb; ++y, ++q) {
+      const int b = q % 4, slot = cnt[b] / 4, w = b + 4 * (cnt[b] % 4);
+      if (slot >= SG_TPW) return false;
+      a.task[w][slot] = (uint8_t)((x << 4) | y);
+      ++cnt[b];
+    }
+  return true;
+}
+
+template <int NA, int NB>
+hrom_status launch_cross(hrom_ctx* c, XGArgs& a, int grid) {
+  const size_t smem = XGCfg<NA, NB>::smem;
+  HROM_CK(cudaFuncSetAttribute(cross_gram_kernel<NA, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cross_gram_kernel<NA, NB><<<grid, SG_THREADS, smem, c->st>>>(a);
+  HROM_LAUNCH_CK();
+  return HROM_OK;
+}
+
 // ---------------- G7: incremental gathered Gram ----------------
 // S-hat moves little from one step to the next (measured churn ~0.1-1 % of its cells at config
 // 4), and the union window shifts by one snapshot.  So the Gram of the old columns over the rows
@@ -1307,6 +1473,34 @@ hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int64_t ns, in
   a.rows = rows;
   a.rho = rho;
   return run_gather_gram(c, a, ncol, c->basis_pending ? c->nsm - 1 : c->nsm, dev_C, ldc, map);
+}
+
+// config 5: C = Phi^T S over the w + 1 window columns (S = the ring slots of the current window)
+hrom_status project_window(hrom_ctx* c, const double* const* phicols, int m, double* dev_C) {
+  const Win& W = c->win;
+  const int na = (m + 15) / 16, nb = (W.nU + 15) / 16;
+  XGArgs a{};
+  for (int i = 0; i < m; ++i) a.colA[i] = phicols[i];
+  a.ncA = m;
+  a.ring = c->b.ring;
+  a.W = W;
+  a.nsr = c->g.nsr;
+  a.rows = c->g.D;
+  a.part = c->b.part;
+  const int grid = c->basis_pending ? c->nsm - 1 : c->nsm;
+  if ((int64_t)grid * 256 * na * nb > c->b.part_len || !xg_tasks(na, nb, a)) return HROM_E_INVALID;
+  hrom_status s = HROM_E_INVALID;
+#define XG_CASE(A_, B_) \
+  if (na == A_ && nb == B_) s = launch_cross<A_, B_>(c, a, grid);
+  XG_CASE(1, 1) XG_CASE(1, 2) XG_CASE(1, 3) XG_CASE(1, 4) XG_CASE(1, 5)
+  XG_CASE(2, 2) XG_CASE(2, 3) XG_CASE(2, 4) XG_CASE(2, 5) XG_CASE(4, 9)
+#undef XG_CASE
+  if (s != HROM_OK) return s;
+  ++c->nlaunch;
+  cross_reduce<<<(m * W.nU * GR_TPE + 255) / 256, 256, 0, c->st>>>(c->b.part, grid, 16 * na, 16 * nb, m, W.nU, dev_C);
+  HROM_LAUNCH_CK();
+  ++c->nlaunch;
+  return HROM_OK;
 }
 
 // gathered Gram R of [U, b] over the rows of S-hat (shifted by rho, union order, (nU+1)^2 in

@@ -55,6 +55,7 @@ _SIGS = {
     "hrom_sample": (C.c_int, [_VP, C.c_double, _VP, _VP, _VP, _VP]),
     "hrom_sample_rre": (C.c_int, [_VP, C.c_double, _VP, _VP, _VP, _VP]),
     "hrom_odeim": (C.c_int, [_VP, _VP, C.c_int32, C.c_int32, _VP, _VP]),
+    "hrom_project": (C.c_int, [_VP, _VP, C.c_int32, _VP]),
     "hrom_reconstruct": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "hrom_filter": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "hrom_step": (C.c_int, [_VP, C.c_double]),
@@ -224,6 +225,13 @@ class HybridROM:
         rows = torch.empty(n_p, dtype=torch.int64, device="cuda")
         _ck(self.lib.hrom_odeim(self.h, _ptr(phi), phi.shape[0], n_p, _ptr(cells), _ptr(rows)), "hrom_odeim")
         return cells, rows
+
+    def project(self, phi: torch.Tensor) -> torch.Tensor:
+        """Phi^T [gamma_{k-w}, ..., gamma_k] (m x (w+1)) on the FP64 tensor cores."""
+        assert phi.dtype == torch.float64 and phi.is_contiguous() and phi.shape[1] == self.wl.D
+        out = torch.empty((phi.shape[0], self.wl.w + 1), dtype=torch.float64, device="cuda")
+        _ck(self.lib.hrom_project(self.h, _ptr(phi), phi.shape[0], _ptr(out)), "hrom_project")
+        return out
 
     def reconstruct(self, v: torch.Tensor, mask: Optional[torch.Tensor] = None,
                     y_out: Optional[torch.Tensor] = None, eps_out: Optional[torch.Tensor] = None):

@@ -158,6 +158,19 @@ def run_config5(fracs=(0.02, 0.05, 0.10, 0.20), side=4096):
     e1.synchronize()
     res["lift_ms"] = e0.elapsed_time(e1)
     res["lift_bytes_GBs"] = 8 * wl.D * (ncol + res["r_eff"] + 1) / (res["lift_ms"] / 1e3) / 1e9
+    res["lift_tflops"] = 2.0 * wl.D * wl.w * res["r_eff"] / (res["lift_ms"] / 1e3) / 1e12
+    # projection Phi^T S of the window (r_eff x (w+1)) on the FP64 tensor cores
+    phi = phi.contiguous()
+    pt = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rom.project(phi)
+        e1.record()
+        e1.synchronize()
+        pt.append(e0.elapsed_time(e1))
+    res["project_PhiTS_ms"] = min(pt)
+    res["project_PhiTS_tflops"] = 2.0 * wl.D * res["r_eff"] * (wl.w + 1) / (res["project_PhiTS_ms"] / 1e3) / 1e12
     del phi, psi
     torch.cuda.empty_cache()
     # held-out column q* and its projection-error indicator (reconstruct with S-hat = all cells)
