@@ -103,11 +103,39 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
     for (int i = threadIdx.x; i < 2 * kFilterSlots; i += blockDim.x) a.fdec[i] = 0ull;
   grid.sync();
   stamp(a.tdbg, 1);
-  // each CTA owns a contiguous chunk of the band: its stencil tables and F values are staged in
-  // shared memory once (the sweeps then pay one L2 round trip per phase, for the values only)
+  // Each CTA owns a contiguous chunk of the band made of WHOLE grid rows (the band list is
+  // row-major): the x-stencil of a band cell then only reads cells of its own chunk or fixed
+  // halo values, so the x-pass of sweep s+1 follows the y-pass of sweep s after a block barrier,
+  // and one grid barrier per sweep remains (the y-pass reads x-filtered values of other rows).
+  // The stop decision of sweep s is read after that barrier, so the x-pass of sweep s+1 runs
+  // speculatively (its values are scratch when the order stops).  Stencil tables and F of the
+  // chunk are staged in shared memory once.
   extern __shared__ double fsm[];
-  const int64_t chunk = ((int64_t)nb + gridDim.x - 1) / gridDim.x;
-  const int64_t c0 = min((int64_t)blockIdx.x * chunk, (int64_t)nb), c1 = min(c0 + chunk, (int64_t)nb);
+  __shared__ int s_bound[2];
+  const int64_t nominal = ((int64_t)nb + gridDim.x - 1) / gridDim.x;
+  for (int side = 0; side < 2; ++side) {
+    // first list index >= the nominal split that starts a new grid row (one parallel probe:
+    // a row holds at most nx band cells)
+    const int64_t s0 = min((int64_t)(blockIdx.x + side) * nominal, (int64_t)nb);
+    if (threadIdx.x == 0) s_bound[side] = (int)nb;
+    __syncthreads();
+    if (s0 == 0 || s0 >= nb) {
+      if (threadIdx.x == 0) s_bound[side] = (int)s0;
+    } else {
+      const int r0 = a.list[s0 - 1] / g.nx;
+      const int64_t span = g.nx + 1, per = (span + blockDim.x - 1) / blockDim.x;
+      for (int64_t q = 0; q < per; ++q) {
+        const int64_t t = s0 + (int64_t)threadIdx.x * per + q;
+        if (t < nb && a.list[t] / g.nx != r0) {
+          atomicMin(&s_bound[side], (int)t);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  const int64_t c0 = s_bound[0], c1 = max(s_bound[1], s_bound[0]);
+  const int64_t chunk = c1 - c0;
   const bool tsm = chunk * (14 * sizeof(int32_t) + g.c * sizeof(double)) <= (size_t)a.smem_bytes;
   double* sFb = fsm;                                      // [var][chunk]
   int32_t* stab = reinterpret_cast<int32_t*>(fsm + (tsm ? g.c * chunk : 0));  // [14][chunk]
@@ -121,9 +149,6 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
     }
     __syncthreads();
   }
-  // Sweeps, two grid barriers each.  The y-pass owns its cell: a kept value is written straight
-  // into cur (no other thread of that phase reads cur at a band cell -- the y-stencil reads Vp),
-  // so the next x-pass sees the applied keep-set without a separate apply phase.
   const int32_t* __restrict__ tab = a.tab;
   double* __restrict__ cur = a.cur;
   double* __restrict__ Vp = a.Vp;
@@ -137,10 +162,8 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
     double cfr[7];
 #pragma unroll
     for (int m = 0; m < 7; ++m) cfr[m] = m <= 2 * rad ? cf[m] : 0.0;
-    int sweeps = 0;
-    for (int sw = 0; sw < a.maxsw; ++sw, ++gs) {
-      ++sweeps;
-      // P1: v' = S^x(cur) on B
+    // P1: v' = S^x(cur) on the chunk
+    auto x_pass = [&]() {
       for (int64_t t = c0 + threadIdx.x; t < c1; t += blockDim.x) {
         const int64_t lt = t - c0;
         int nbr[7];
@@ -162,8 +185,20 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
           Vp[var * N + t] = sx / den;
         }
       }
-      grid.sync();
-      // P2: v'' = S^y(v') on B, residual gate, kept values applied in place
+    };
+    int sweeps = 0;
+    if (a.maxsw > 0) x_pass();
+    for (int sw = 0;; ++sw) {
+      grid.sync();  // Vp of sweep sw everywhere; statistics of sweep sw-1 complete
+      if (sw > 0) {  // identical stop decision in every block
+        const double md = __longlong_as_double((long long)__ldcg(a.fdec + gs - 1));
+        const long long tot = (long long)__ldcg(a.fdec + kFilterSlots + gs - 1);
+        stamp(a.tdbg, 1 + gs);
+        if (tot == 0 || md < a.eps_f) break;
+      }
+      if (sw == a.maxsw) break;
+      ++sweeps;
+      // P2: v'' = S^y(v') on the chunk, residual gate, kept values applied in place
       double mdec = 0.0;
       int cnt = 0;
       for (int64_t t = c0 + threadIdx.x; t < c1; t += blockDim.x) {
@@ -218,7 +253,7 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
         sdec[threadIdx.x >> 5] = mdec;
         scnt[threadIdx.x >> 5] = cnt;
       }
-      __syncthreads();
+      __syncthreads();  // also orders this block's cur writes before the next x-pass reads them
       if (threadIdx.x == 0) {
         double md = 0.0;
         int c = 0;
@@ -231,20 +266,13 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
         atomicMax(a.fdec + gs, (unsigned long long)__double_as_longlong(md));
         atomicAdd(a.fdec + kFilterSlots + gs, (unsigned long long)c);
       }
-      grid.sync();
-      // identical stop decision in every block
-      {
-        const double md = __longlong_as_double((long long)__ldcg(a.fdec + gs));
-        const long long tot = (long long)__ldcg(a.fdec + kFilterSlots + gs);
-        stamp(a.tdbg, 2 + gs);
-        if (tot == 0 || md < a.eps_f) {
-          ++gs;
-          break;
-        }
-      }
+      ++gs;
+      if (sw + 1 < a.maxsw) x_pass();  // speculative: scratch if the order stops after sweep sw
     }
     if (gtid == 0 && a.sweeps_out) a.sweeps_out[oi] = sweeps;
+    __syncthreads();  // this block's last y-pass before the next order's x-pass
   }
+  grid.sync();  // every chunk's final values before the write-back
   // write the kept band values back, and the indicator on kept band cells:
   // eps_n = sum_v (v - (psi + Phi y))^2 (pre-filter value = psi + Phi y)
   for (int64_t t = gtid; t < nb; t += gstride) {
