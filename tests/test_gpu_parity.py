@@ -283,7 +283,8 @@ def test_determinism_bitwise(inputs):
 
 
 @pytest.mark.parametrize("dim,nx,ny,bc,frac,seed", [(2, 70, 45, 0, 0.05, 1), (2, 300, 211, 1, 0.1, 2),
-                                                    (2, 64, 64, 1, 0.6, 3), (1, 5000, 1, 0, 0.05, 4)])
+                                                    (2, 64, 64, 1, 0.6, 3), (1, 5000, 1, 0, 0.05, 4),
+                                                    (2, 30, 25, 0, 0.1, 5), (1, 900, 1, 1, 0.08, 6)])
 def test_seam_filter_parity(orc, inputs, dim, nx, ny, bc, frac, seed):
     """H7 standalone vs the oracle's seam filter (A21-A24): kept set and sweeps
     identical, values to rounding (same stencil sums in the same order)."""
