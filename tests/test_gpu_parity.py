@@ -471,6 +471,63 @@ def test_fullsize_config4_properties(orc, inputs):
     want = np.zeros(wl.N, np.uint8)
     want[nz[order[:n_g]]] = 1
     assert np.array_equal(H.cells_from_mask(wl, rom.mask()), want)
+    # (iv) the RRE-delta rule at full size on the same indicator (A35): bit-exact vs the oracle
+    for delta in (0.5, 0.99, 0.999999):
+        m_o, k_o = orc.select_rre(eps, delta)
+        cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+        rom.sample_rre(delta, eps=dev(eps), count_out=cnt)
+        assert np.array_equal(H.cells_from_mask(wl, rom.mask()), m_o), delta
+        assert int(cnt.item()) == k_o
+
+
+def test_replay_config3_fullsize(orc, inputs):
+    """Config 3 at full size (1024^2, w = 48, r = 24, BJ:9): the window gamma_0..gamma_w from the
+    oracle's full steps, S-hat = a seeded 10 % of the cells, then one hybrid step on both sides
+    from the same window and mask (Alg. 1): state within the POD's own conditioning
+    (A15: max(1e-12, 10 eps lambda_1 / gap at r_eff)), S-hat rows = the full step, indicator
+    support equal up to filter near-ties and values to 1e3 x that bound; then the next S-hat from
+    the GPU's indicator is
+    the oracle's selection on that indicator, bit for bit (A18)."""
+    wl = inputs.config(3)
+    q = inputs.initial_condition(wl)
+    snaps = [q]
+    for _ in range(wl.w):
+        snaps.append(orc.full_step(wl, snaps[-1], orc.dt(wl, snaps[-1])))
+    snaps = np.stack(snaps)
+    S = (np.random.default_rng(33).random(wl.N) < wl.f).astype(np.uint8)
+    k = wl.w
+    R = orc.Run(wl, snaps[0])
+    R.set_window(k, snaps, S)
+    rom = H.HybridROM(wl)
+    rom.set_window(k, dev(snaps.reshape(wl.w + 1, -1)), _mask_dev(wl, S))
+    assert rom.effective_rank() == R.reff()
+    # A15: POD_m of this window is only determined to eps lambda_1 / (lambda_reff - lambda_reff+1)
+    # (its trailing modes sit just above the 1e-8 cut with small gaps); the state parity bar is
+    # 1e-12 or 10x that subspace bound, whichever is larger
+    lam = R.sigma() ** 2
+    re = R.reff()
+    gap = lam[re - 1] - (lam[re] if re < lam.size else 0.0)
+    tol = max(1e-12, 10 * 2.2e-16 * lam[0] / gap)
+    dt = orc.dt(wl, snaps[-1])
+    R.step(dt)
+    rom.hybrid_step(dt=dt)
+    rom.sync()
+    g = rom.get_state().cpu().numpy()
+    o = R.state()
+    assert rel(g, o) <= tol, (rel(g, o), tol)
+    full = orc.full_step(wl, snaps[-1], dt)
+    assert rel(g[:, S == 1], full[:, S == 1]) <= 1e-13
+    eg, eo = rom.indicator().cpu().numpy(), R.eps()
+    # the filter's keep decisions (strict residual decrease) flip for near-ties at the state's
+    # difference level, so the indicator support may differ on a few band cells
+    flip = (eg > 0) ^ (eo > 0)
+    assert flip.sum() <= 1e-3 * max(int((eo > 0).sum()), 1), int(flip.sum())
+    both = (eg > 0) & (eo > 0)
+    assert rel(eg[both], eo[both]) <= max(1e-6, 1e3 * tol), rel(eg[both], eo[both])
+    m_o, k_o = orc.select(eg, orc.n_g(wl.f, wl.N))
+    rom.update_basis()
+    rom.sample(eps=dev(eg))
+    assert np.array_equal(H.cells_from_mask(wl, rom.mask()), m_o)
 
 
 def test_fullsize_gram_config5_rows(orc, inputs):
