@@ -495,6 +495,7 @@ struct XGArgs {
   Win W;               // B columns: the nU union slots (window order)
   int64_t nsr, rows;
   double* part;        // [grid][16 NA][16 NB]
+  int tma;             // 1: 16-byte aligned column runs (D even): TMA bulk copies
   uint8_t task[SG_CW][SG_TPW];  // (a << 4) | b
 };
 template <int NA, int NB>
@@ -538,18 +539,29 @@ __global__ void __launch_bounds__(SG_THREADS, 1) cross_gram_kernel(XGArgs a) {
   const int64_t ntiles = (a.rows + RT - 1) / RT;
   const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (warp < SG_PW) {
-    const int part = warp, k = lane;
+    // ---- producers: 16-byte cp.async, a half-warp per 32-row column run (tiles never straddle
+    // a slab run of 128 rows), 8 columns per 4-warp pass; element copies for the ragged last
+    // tile or when the runs are not 16-byte aligned.  No producer arithmetic.
+    const int half = lane >> 4, ch = lane & 15;
     for (int64_t it = 0; it < my_tiles + LOOK; ++it) {
       if (it < my_tiles) {
         const int st = (int)(it % ST);
         if (it >= ST) mbar_wait(&empty[st], (uint32_t)(((it / ST) - 1) & 1));
         double* tile = smem + (size_t)st * NC * LDT;
-        const int64_t row = (blockIdx.x + it * gridDim.x) * RT + k;
-        for (int col = part; col < NC; col += SG_PW) {
-          const double* src = scol[col];
-          if (!src) continue;
-          if (row < a.rows) cp_async8(tile + col * LDT + k, src + sidx(SRef{nullptr, sns[col]}, row));
-          else tile[col * LDT + k] = 0.0;
+        const int64_t row0 = (blockIdx.x + it * gridDim.x) * RT;
+        if (a.tma && row0 + RT <= a.rows) {
+          for (int col = 2 * warp + half; col < NC; col += 2 * SG_PW) {
+            const double* src = scol[col];
+            if (src) cp_async16(tile + col * LDT + 2 * ch, src + sidx(SRef{nullptr, sns[col]}, row0) + 2 * ch);
+          }
+        } else {
+          for (int col = warp; col < NC; col += SG_PW) {
+            const double* src = scol[col];
+            if (!src) continue;
+            const int64_t row = row0 + lane;
+            if (row < a.rows) cp_async8(tile + col * LDT + lane, src + sidx(SRef{nullptr, sns[col]}, row));
+            else tile[col * LDT + lane] = 0.0;
+          }
         }
       }
       cp_async_commit();
@@ -1487,6 +1499,9 @@ hrom_status project_window(hrom_ctx* c, const double* const* phicols, int m, dou
   a.nsr = c->g.nsr;
   a.rows = c->g.D;
   a.part = c->b.part;
+  a.tma = (c->g.D % 2 == 0) ? 1 : 0;
+  for (int i = 0; i < m; ++i)
+    if ((reinterpret_cast<uintptr_t>(phicols[i]) & 15) != 0) a.tma = 0;
   const int grid = c->basis_pending ? c->nsm - 1 : c->nsm;
   if ((int64_t)grid * 256 * na * nb > c->b.part_len || !xg_tasks(na, nb, a)) return HROM_E_INVALID;
   hrom_status s = HROM_E_INVALID;
