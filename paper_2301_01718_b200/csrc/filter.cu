@@ -34,7 +34,7 @@ struct FilterArgs {
   double* cur0;          // compact: pre-filter values (band)
   double* Fb;            // compact: F on the band
   double* Vp;            // compact: x-filtered values (band) / fixed values (halo)
-  double* Vpp;           // compact: y-filtered values (band)
+  double* Vpp;           // compact: second x-filtered buffer (x-passes alternate Vp / Vpp)
   uint8_t* flag;         // compact: bit0 ever kept, bits 1/2 keep-set of even/odd sweeps
   uint8_t* kept_cells;   // nullable: per-cell 1 where kept in some sweep (zeroed by the launcher)
   double* eps;
@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
         a.cur0[var * N + t] = x;
         a.Fb[var * N + t] = a.F.p[sidx(a.F, var * N + n)];
       } else {
-        a.Vp[var * N + t] = x;
+        a.Vp[var * N + t] = x;   // halo: fixed values in both x-pass buffers
+        a.Vpp[var * N + t] = x;
       }
     }
     a.flag[t] = 0;
@@ -151,7 +152,11 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
   }
   const int32_t* __restrict__ tab = a.tab;
   double* __restrict__ cur = a.cur;
-  double* __restrict__ Vp = a.Vp;
+  // x-passes alternate between two buffers: the speculative x-pass of sweep s+1 of one CTA may
+  // run while another CTA's y-pass of sweep s still reads the x-filtered values of s (the grid
+  // barrier after x-pass s+1 orders x-pass s+2, which reuses s's buffer, after every y-pass s)
+  double* const Vbuf[2] = {a.Vp, a.Vpp};
+  int xp = 0;  // x-passes issued (identical in every CTA)
   const double* __restrict__ Fb = a.Fb;
   uint8_t* __restrict__ flag = a.flag;
   int gs = 0;  // sweeps done over all orders
@@ -164,6 +169,8 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
     for (int m = 0; m < 7; ++m) cfr[m] = m <= 2 * rad ? cf[m] : 0.0;
     // P1: v' = S^x(cur) on the chunk
     auto x_pass = [&]() {
+      double* __restrict__ Vp = Vbuf[xp & 1];
+      ++xp;
       for (int64_t t = c0 + threadIdx.x; t < c1; t += blockDim.x) {
         const int64_t lt = t - c0;
         int nbr[7];
@@ -199,6 +206,7 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
       if (sw == a.maxsw) break;
       ++sweeps;
       // P2: v'' = S^y(v') on the chunk, residual gate, kept values applied in place
+      const double* __restrict__ Vp = Vbuf[(xp - 1) & 1];
       double mdec = 0.0;
       int cnt = 0;
       for (int64_t t = c0 + threadIdx.x; t < c1; t += blockDim.x) {

@@ -1362,8 +1362,18 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
         const int st = (int)(it % LF_STAGES);
         if (it >= LF_STAGES) mbar_wait(&empty[st], (uint32_t)(((it / LF_STAGES) - 1) & 1));
         double* tile = tiles + (size_t)st * LF_NCOL * LF_LDT;
-        const int64_t e = (blockIdx.x + it * gridDim.x) * LF_RT + k;
-        if (e < g.D) {
+        const int64_t e0 = (blockIdx.x + it * gridDim.x) * LF_RT, e = e0 + k;
+        if (e0 + LF_RT <= g.D) {
+          // full tile: 16-byte cp.async, a half-warp per 32-row column run (a 64-row tile lies
+          // inside one slab run of 128 rows, so each run is 256 contiguous bytes)
+          const int hw = k >> 4, ch = k & 15;
+          for (int q = hw; q < 2 * nU; q += 2 * LF_PW) {
+            const int col = q >> 1, part = q & 1;
+            cp_async16(tile + col * LF_LDT + 32 * part + 2 * ch,
+                       ring + (int64_t)W.slot[col] * TILE + sidx(slab, e0 + 32 * part) + 2 * ch);
+          }
+          e_cur = e;
+        } else if (e < g.D) {
           const int64_t se = sidx(slab, e);
           for (int col = 0; col < nU; ++col) cp_async8(tile + col * LF_LDT + k, ring + (int64_t)W.slot[col] * TILE + se);
           e_cur = e;
@@ -1374,6 +1384,7 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
       cp_async_commit();
       if (it >= 1) {
         cp_async_wait<1>();
+        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * LF_PW) : "memory");  // rows landed by other lanes
         const int ps = (int)((it - 1) % LF_STAGES);
         double* tile = tiles + (size_t)ps * LF_NCOL * LF_LDT;
         if (e_prev >= 0) {
