@@ -1401,49 +1401,37 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
     }
     cp_async_wait<0>();
   } else {
-    // consumer warp cw: rows 16 rb .. 16 rb + 15 (rb = cw mod 4) x columns 16 cb .. 16 cb + 15
-    // (cb = cw / 4): two A and two B fragments feed four DMMAs per k-step (1 shared-memory load
-    // per DMMA instead of 1.25: the lift shares the SM's shared-memory bandwidth with the
-    // producers' shift pass)
     const int cw = warp - LF_PW;
-    const int rb = cw & 3, cb = cw >> 2;
+    const int db = cw & 7, mb0 = (cw >> 3) * 4;
     const int gid = lane >> 2, tig = lane & 3;
     for (int64_t it = 0; it < my_tiles; ++it) {
       const int st = (int)(it % LF_STAGES);
       mbar_wait(&full[st], (uint32_t)((it / LF_STAGES) & 1));
       const double* tile = tiles + (size_t)st * LF_NCOL * LF_LDT;
-      double acc[2][2][2];
+      double acc[4][2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-      if (phi && 16 * cb < re) {
-        const double* pa = tile + (xoff + tig) * LF_LDT + 16 * rb + gid;
-        const double* pb = As + tig * LF_LDA + 16 * cb + gid;
-#pragma unroll 2
+      for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
+      if (phi && 8 * mb0 < re) {
         for (int kk = 0; kk < kpad; kk += 4) {
-          const double a0 = pa[kk * LF_LDT], a1 = pa[kk * LF_LDT + 8];
-          const double b0 = pb[kk * LF_LDA], b1 = pb[kk * LF_LDA + 8];
-          dmma(acc[0][0][0], acc[0][0][1], a0, b0);
-          dmma(acc[0][1][0], acc[0][1][1], a0, b1);
-          dmma(acc[1][0][0], acc[1][0][1], a1, b0);
-          dmma(acc[1][1][0], acc[1][1][1], a1, b1);
+          const double av = tile[(xoff + kk + tig) * LF_LDT + 8 * db + gid];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double bv = As[(kk + tig) * LF_LDA + 8 * (mb0 + q) + gid];
+            dmma(acc[q][0], acc[q][1], av, bv);
+          }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
-      if (phi && 16 * cb < re) {
+      if (phi) {
+        const int64_t e0 = (blockIdx.x + it * gridDim.x) * LF_RT + 8 * db + gid;
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int64_t e0 = (blockIdx.x + it * gridDim.x) * LF_RT + 16 * rb + 8 * i + gid;
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
-          for (int jb = 0; jb < 2; ++jb)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int j = 16 * cb + 8 * jb + 2 * tig + h;
-              if (j < re && e0 < g.D) phi[(int64_t)j * g.D + e0] = acc[i][jb][h];
-            }
-        }
+          for (int h = 0; h < 2; ++h) {
+            const int j = 8 * (mb0 + q) + 2 * tig + h;
+            if (j < re && e0 < g.D) phi[(int64_t)j * g.D + e0] = acc[q][h];
+          }
       }
     }
   }
