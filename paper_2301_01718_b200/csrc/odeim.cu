@@ -109,10 +109,20 @@ __global__ void __launch_bounds__(OD_T) odeim_argmax_kernel(const double* __rest
   ArgMax best{-1.0, INT64_MAX};
   const int64_t stride = (int64_t)gridDim.x * OD_T;
   const double* pl = phi + (int64_t)l * D;
+  const bool small = D < (int64_t)INT32_MAX;  // 32-bit cell index (D <= 67 M in every config)
   for (int64_t e = blockIdx.x * (int64_t)OD_T + tid; e < D; e += stride) {
-    if (chosen[e % N]) continue;
+    if (chosen[small ? (int)((unsigned)e % (unsigned)N) : e % N]) continue;
     double r = pl[e];
-    for (int i = 0; i < l; ++i) r = __dsub_rn(r, __dmul_rn(phi[(int64_t)i * D + e], c[i]));
+    const double* col = phi + e;
+    int i = 0;
+    for (; i + 8 <= l; i += 8) {  // eight column loads in flight before the (ordered) updates
+      double p[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) p[u] = col[(int64_t)(i + u) * D];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) r = __dsub_rn(r, __dmul_rn(p[u], c[i + u]));
+    }
+    for (; i < l; ++i) r = __dsub_rn(r, __dmul_rn(col[(int64_t)i * D], c[i]));
     best = amax(best, ArgMax{fabs(r), e});
   }
   best = shfl_amax(best);
