@@ -1,3 +1,5 @@
+"""Conditioning of POD_r for the full-size config-3 replay window: eigenvalues
+around r_eff and the subspace bound eps * lambda_1 / gap used by test_replay_config3_fullsize."""
 import sys, os, numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle as orc
