@@ -168,3 +168,28 @@ def test_finite_z_schedule_skip_and_projection_indicator(orc, inputs):
             alpha[-1] += 1.0
             np.testing.assert_allclose(X @ alpha, d, rtol=0, atol=1e-13 * np.abs(d).max())
     assert seen_full_refresh
+
+
+def test_rre_and_odeim_driver_sets(orc, inputs):
+    """Algorithm 1 with the paper's own sampling (NEXT-1): RRE-delta selection of G (P:373-380,
+    A35) and ODEIM points P of Phi_{k+1} (A36).  Each refresh: G is the oracle's own
+    RRE rule on the step's indicator, P = ODEIM(Phi_{k+1}) recomputed from the driver's basis,
+    S-hat = G u cells(P), and the hybrid step uses exactly those points (gappy rows = P)."""
+    wl = _small(inputs, delta=0.9, n_p=2 * 3)
+    q0 = inputs.initial_condition(wl, "quadrant")
+    R = orc.Run(wl, q0)
+    for k in range(1, wl.w + 6):
+        R.step()
+        if k < wl.w - 1:
+            continue
+        S = R.mask()
+        G, _ = orc.select_rre(R.eps(), wl.delta)
+        rows = R.points()
+        phi = R.basis().T.copy()  # (reff, D)
+        cells, rows_o = orc.odeim(phi, wl.N, min(wl.n_p, wl.N))
+        assert np.array_equal(rows, rows_o)
+        want = G.copy()
+        want[cells] = 1
+        assert np.array_equal(S, want), k
+        assert len(set(cells.tolist())) == len(cells)
+    assert np.all(np.isfinite(R.state()))
