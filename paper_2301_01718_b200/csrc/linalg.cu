@@ -1388,9 +1388,20 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
         const int ps = (int)((it - 1) % LF_STAGES);
         double* tile = tiles + (size_t)ps * LF_NCOL * LF_LDT;
         if (e_prev >= 0) {
-          double sp = 0.0, sc = 0.0;
-          for (int s = 0; s < w; ++s) sp += tile[s * LF_LDT + k];
-          for (int s = xoff; s < nU; ++s) sc += tile[s * LF_LDT + k];
+          // four independent partial sums per mean (short dependency chains: the producers'
+          // pass is on the critical path of a tile; eight were slower)
+          double p4[4] = {0.0, 0.0, 0.0, 0.0}, c4[4] = {0.0, 0.0, 0.0, 0.0};
+          int s = 0;
+          for (; s + 4 <= w; s += 4)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) p4[u] += tile[(s + u) * LF_LDT + k];
+          for (; s < w; ++s) p4[0] += tile[s * LF_LDT + k];
+          s = xoff;
+          for (; s + 4 <= nU; s += 4)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) c4[u] += tile[(s + u) * LF_LDT + k];
+          for (; s < nU; ++s) c4[0] += tile[s * LF_LDT + k];
+          const double sp = (p4[0] + p4[1]) + (p4[2] + p4[3]), sc = (c4[0] + c4[1]) + (c4[2] + c4[3]);
           if (psi) psi[e_prev] = sc * inv_w;
           const double pp = sp * inv_w;
           for (int s = xoff; s < nU; ++s) tile[s * LF_LDT + k] -= pp;
@@ -1402,7 +1413,9 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
     cp_async_wait<0>();
   } else {
     const int cw = warp - LF_PW;
-    const int db = cw & 7, mb0 = (cw >> 3) * 4;
+    // r_eff <= 32: each warp takes 2 column blocks so that all 16 warps work (else 4 blocks)
+    const int nbk = re > 32 ? 4 : 2;
+    const int db = cw & 7, mb0 = (cw >> 3) * nbk;
     const int gid = lane >> 2, tig = lane & 3;
     for (int64_t it = 0; it < my_tiles; ++it) {
       const int st = (int)(it % LF_STAGES);
@@ -1412,12 +1425,23 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
       if (phi && 8 * mb0 < re) {
-        for (int kk = 0; kk < kpad; kk += 4) {
-          const double av = tile[(xoff + kk + tig) * LF_LDT + 8 * db + gid];
+        if (nbk == 4) {
+          for (int kk = 0; kk < kpad; kk += 4) {
+            const double av = tile[(xoff + kk + tig) * LF_LDT + 8 * db + gid];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const double bv = As[(kk + tig) * LF_LDA + 8 * (mb0 + q) + gid];
-            dmma(acc[q][0], acc[q][1], av, bv);
+            for (int q = 0; q < 4; ++q) {
+              const double bv = As[(kk + tig) * LF_LDA + 8 * (mb0 + q) + gid];
+              dmma(acc[q][0], acc[q][1], av, bv);
+            }
+          }
+        } else {
+          for (int kk = 0; kk < kpad; kk += 4) {
+            const double av = tile[(xoff + kk + tig) * LF_LDT + 8 * db + gid];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const double bv = As[(kk + tig) * LF_LDA + 8 * (mb0 + q) + gid];
+              dmma(acc[q][0], acc[q][1], av, bv);
+            }
           }
         }
       }
@@ -1430,7 +1454,7 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int j = 8 * (mb0 + q) + 2 * tig + h;
-            if (j < re && e0 < g.D) phi[(int64_t)j * g.D + e0] = acc[q][h];
+            if (q < nbk && j < re && e0 < g.D) phi[(int64_t)j * g.D + e0] = acc[q][h];
           }
       }
     }
