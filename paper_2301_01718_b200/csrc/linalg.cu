@@ -1322,7 +1322,7 @@ __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ 
 // warps gather a 64-DOF tile of all nU window slots (cp.async), form X - psi_prev in place and
 // publish it; 16 consumer warps each own one 8-DOF block x four 8-mode blocks of the product
 // with A (staged in smem once per CTA) and write Phi straight from the accumulators.
-constexpr int LF_RT = 64, LF_LDT = LF_RT + 4, LF_PW = 2, LF_CW = 16, LF_T = 32 * (LF_PW + LF_CW);
+constexpr int LF_RT = 64, LF_LDT = LF_RT + 4, LF_PW = 4, LF_CW = 16, LF_T = 32 * (LF_PW + LF_CW);
 constexpr int LF_STAGES = 2, LF_NCOL = kMaxW + 5, LF_LDA = kMaxR + 4;
 
 __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const double* __restrict__ ring,
@@ -1343,7 +1343,7 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
   for (int i = threadIdx.x; i < LF_STAGES * LF_NCOL * LF_LDT; i += LF_T) tiles[i] = 0.0;
   if (threadIdx.x == 0) {
     for (int q = 0; q < LF_STAGES; ++q) {
-      mbar_init(&full[q], LF_RT);
+      mbar_init(&full[q], 32 * LF_PW);
       mbar_init(&empty[q], LF_CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -1353,8 +1353,13 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
   const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const double inv_w = 1.0 / (double)w;
   if (warp < LF_PW) {
-    const int k = threadIdx.x;
+    // producers: two threads per tile row (hf = column half); the row's window means are two
+    // half sums exchanged through shared memory
+    __shared__ double xch[2][2][LF_RT];
+    const int kt = threadIdx.x, k = kt & (LF_RT - 1), hf = kt / LF_RT;
     const SRef slab{nullptr, g.nsr};
+    const int wh = w / 2;
+    const int s0 = hf ? wh : 0, s1 = hf ? w : wh;  // this thread's half of each mean's columns
     int64_t e_prev = -1;
     for (int64_t it = 0; it <= my_tiles; ++it) {
       int64_t e_cur = -1;
@@ -1366,7 +1371,7 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
         if (e0 + LF_RT <= g.D) {
           // full tile: 16-byte cp.async, a half-warp per 32-row column run (a 64-row tile lies
           // inside one slab run of 128 rows, so each run is 256 contiguous bytes)
-          const int hw = k >> 4, ch = k & 15;
+          const int hw = kt >> 4, ch = kt & 15;
           for (int q = hw; q < 2 * nU; q += 2 * LF_PW) {
             const int col = q >> 1, part = q & 1;
             cp_async16(tile + col * LF_LDT + 32 * part + 2 * ch,
@@ -1375,10 +1380,10 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
           e_cur = e;
         } else if (e < g.D) {
           const int64_t se = sidx(slab, e);
-          for (int col = 0; col < nU; ++col) cp_async8(tile + col * LF_LDT + k, ring + (int64_t)W.slot[col] * TILE + se);
+          for (int col = hf; col < nU; col += 2) cp_async8(tile + col * LF_LDT + k, ring + (int64_t)W.slot[col] * TILE + se);
           e_cur = e;
         } else {
-          for (int col = 0; col < nU; ++col) tile[col * LF_LDT + k] = 0.0;
+          for (int col = hf; col < nU; col += 2) tile[col * LF_LDT + k] = 0.0;
         }
       }
       cp_async_commit();
@@ -1387,24 +1392,28 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
         asm volatile("bar.sync 1, %0;\n" ::"n"(32 * LF_PW) : "memory");  // rows landed by other lanes
         const int ps = (int)((it - 1) % LF_STAGES);
         double* tile = tiles + (size_t)ps * LF_NCOL * LF_LDT;
+        double p2[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
         if (e_prev >= 0) {
-          // four independent partial sums per mean (short dependency chains: the producers'
-          // pass is on the critical path of a tile; eight were slower)
-          double p4[4] = {0.0, 0.0, 0.0, 0.0}, c4[4] = {0.0, 0.0, 0.0, 0.0};
-          int s = 0;
-          for (; s + 4 <= w; s += 4)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) p4[u] += tile[(s + u) * LF_LDT + k];
-          for (; s < w; ++s) p4[0] += tile[s * LF_LDT + k];
-          s = xoff;
-          for (; s + 4 <= nU; s += 4)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) c4[u] += tile[(s + u) * LF_LDT + k];
-          for (; s < nU; ++s) c4[0] += tile[s * LF_LDT + k];
-          const double sp = (p4[0] + p4[1]) + (p4[2] + p4[3]), sc = (c4[0] + c4[1]) + (c4[2] + c4[3]);
-          if (psi) psi[e_prev] = sc * inv_w;
+          int s = s0;
+          for (; s + 2 <= s1; s += 2) {
+            p2[0] += tile[s * LF_LDT + k];
+            p2[1] += tile[(s + 1) * LF_LDT + k];
+            c2[0] += tile[(xoff + s) * LF_LDT + k];
+            c2[1] += tile[(xoff + s + 1) * LF_LDT + k];
+          }
+          if (s < s1) {
+            p2[0] += tile[s * LF_LDT + k];
+            c2[0] += tile[(xoff + s) * LF_LDT + k];
+          }
+          xch[hf][0][k] = p2[0] + p2[1];
+          xch[hf][1][k] = c2[0] + c2[1];
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * LF_PW) : "memory");  // both halves' sums
+        if (e_prev >= 0) {
+          const double sp = xch[0][0][k] + xch[1][0][k], sc = xch[0][1][k] + xch[1][1][k];
+          if (psi && hf == 0) psi[e_prev] = sc * inv_w;
           const double pp = sp * inv_w;
-          for (int s = xoff; s < nU; ++s) tile[s * LF_LDT + k] -= pp;
+          for (int s = xoff + s0; s < xoff + s1; ++s) tile[s * LF_LDT + k] -= pp;
         }
         mbar_arrive(&full[ps]);
       }
