@@ -1322,7 +1322,8 @@ __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ 
 // warps gather a 64-DOF tile of all nU window slots (cp.async), form X - psi_prev in place and
 // publish it; 16 consumer warps each own one 8-DOF block x four 8-mode blocks of the product
 // with A (staged in smem once per CTA) and write Phi straight from the accumulators.
-constexpr int LF_RT = 64, LF_LDT = LF_RT + 4, LF_PW = 4, LF_CW = 16, LF_T = 32 * (LF_PW + LF_CW);
+constexpr int LF_RT = 64, LF_LDT = LF_RT + 4, LF_PW = 8, LF_CW = 16, LF_T = 32 * (LF_PW + LF_CW);
+constexpr int LF_NH = 32 * LF_PW / LF_RT;  // producer threads per tile row
 constexpr int LF_STAGES = 2, LF_NCOL = kMaxW + 5, LF_LDA = kMaxR + 4;
 
 __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const double* __restrict__ ring,
@@ -1353,13 +1354,12 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
   const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const double inv_w = 1.0 / (double)w;
   if (warp < LF_PW) {
-    // producers: two threads per tile row (hf = column half); the row's window means are two
-    // half sums exchanged through shared memory
-    __shared__ double xch[2][2][LF_RT];
+    // producers: LF_NH threads per tile row (hf = column part); the row's window means are
+    // LF_NH part sums exchanged through shared memory
+    __shared__ double xch[LF_NH][2][LF_RT];
     const int kt = threadIdx.x, k = kt & (LF_RT - 1), hf = kt / LF_RT;
     const SRef slab{nullptr, g.nsr};
-    const int wh = w / 2;
-    const int s0 = hf ? wh : 0, s1 = hf ? w : wh;  // this thread's half of each mean's columns
+    const int s0 = (w * hf) / LF_NH, s1 = (w * (hf + 1)) / LF_NH;  // this thread's part of each mean
     int64_t e_prev = -1;
     for (int64_t it = 0; it <= my_tiles; ++it) {
       int64_t e_cur = -1;
@@ -1380,10 +1380,10 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
           e_cur = e;
         } else if (e < g.D) {
           const int64_t se = sidx(slab, e);
-          for (int col = hf; col < nU; col += 2) cp_async8(tile + col * LF_LDT + k, ring + (int64_t)W.slot[col] * TILE + se);
+          for (int col = hf; col < nU; col += LF_NH) cp_async8(tile + col * LF_LDT + k, ring + (int64_t)W.slot[col] * TILE + se);
           e_cur = e;
         } else {
-          for (int col = hf; col < nU; col += 2) tile[col * LF_LDT + k] = 0.0;
+          for (int col = hf; col < nU; col += LF_NH) tile[col * LF_LDT + k] = 0.0;
         }
       }
       cp_async_commit();
@@ -1410,7 +1410,12 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
         }
         asm volatile("bar.sync 1, %0;\n" ::"n"(32 * LF_PW) : "memory");  // both halves' sums
         if (e_prev >= 0) {
-          const double sp = xch[0][0][k] + xch[1][0][k], sc = xch[0][1][k] + xch[1][1][k];
+          double sp = xch[0][0][k], sc = xch[0][1][k];
+#pragma unroll
+          for (int h = 1; h < LF_NH; ++h) {
+            sp += xch[h][0][k];
+            sc += xch[h][1][k];
+          }
           if (psi && hf == 0) psi[e_prev] = sc * inv_w;
           const double pp = sp * inv_w;
           for (int s = xoff + s0; s < xoff + s1; ++s) tile[s * LF_LDT + k] -= pp;
