@@ -144,6 +144,7 @@ def run_hrom(args, rank, world, local_rank):
         ev0.record(stream)
         for _ in range(args.steps):
             rom.step()
+        rom.join()  # the last step's eigen-solve runs on the library's side stream: inside the timed region
         ev1.record(stream)
         torch.cuda.nvtx.range_pop()
         ev1.synchronize()
@@ -171,6 +172,7 @@ def run_hrom(args, rank, world, local_rank):
             rom.put_state(host)
             rom.step()
             rom.get_state(host)
+        rom.join()
         e1.record(stream)
         e1.synchronize()
         rom.sync()
@@ -250,6 +252,19 @@ def H_count(rom, wl):
     return int(cells_from_mask(wl, rom.mask()).sum())
 
 
+def host_cpu():
+    """The GPU box's host: logical CPUs and model name (the oracle runs on one of them)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"host_nproc": os.cpu_count(), "cpu_model": model}
+
+
 def cpu_sample(steps: int = 1, side: int = 256):
     """The oracle (oracle/, untuned) on a bounded sample of the config-4 workload: a
     side x side periodic tile with the config-4 method parameters (w = 64, r = 32,
@@ -271,7 +286,7 @@ def cpu_sample(steps: int = 1, side: int = 256):
         t1 = time.perf_counter()
         times.append(t1 - t0)
     t = float(np.median(times))
-    return {"value": wl.N / t, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
+    return {"value": wl.N / t, "unit": "cell-updates/s", "cores": 1, "kind": "oracle", **host_cpu(),
             "sample": f"one oracle hybrid step (H1-H12, incl. POD of the 65-column window) on a {side}x{side} periodic tile "
                       f"with config-4 parameters (w=64, r=32, f=10%), median of {steps}; per-cell work is size-independent",
             "seconds_per_step": t}
@@ -306,7 +321,7 @@ def main():
             samples.append(cpu_sample(1, side)["seconds_per_step"])
         ms = 1000.0 * sum(samples) / len(samples)
         value = side * side / (ms / 1000.0)
-        base = {"value": value, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
+        base = {"value": value, "unit": "cell-updates/s", "cores": 1, "kind": "oracle", **host_cpu(),
                 "sample": f"one oracle hybrid step on a {side}x{side} periodic tile with config-4 parameters per step"}
         print(json.dumps({"impl": "reference", "metric": METRIC, "value": value, "unit": "cell-updates/s",
                           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

@@ -107,7 +107,8 @@ hrom_status hrom_hybrid_step(hrom_ctx* ctx, const uint32_t* dev_mask, double dt_
 
 /* H9-H12: push gamma_k into the window; Gram (incremental shifted or full DMMA),
  * lagged centring (Eq. 9 / P:585-587), thin eigen, r_eff; psi_{k+1}.
- * No-op while k < w-1.  At k = w-1 it also sets the bootstrap indicator (reading A19). */
+ * No-op while k < w-1.  At k = w-1 it also sets the bootstrap indicator: the projection error
+ * (reading A19) when S-hat = G, or zero in ODEIM mode, where G_w = {} and S-hat_w = P_w. */
 hrom_status hrom_update_basis(hrom_ctx* ctx);
 
 /* H8: S-hat_{k+1} = top ceil(f N) cells of eps > 0, ties by ascending index,
@@ -163,6 +164,16 @@ hrom_status hrom_step_ex(hrom_ctx* ctx, double dt_override, int32_t* dev_count_o
  * Enqueued on the context stream; synchronises and writes the value to *host_out.
  * Fixed-order reductions: bitwise reproducible. */
 hrom_status hrom_rel_l1_error(hrom_ctx* ctx, const double* dev_a, const double* dev_b, double* host_out);
+
+/* ODEIM points (n_p)_k used by the latest step k (the p-bar average): the count of
+ * points of the basis that step was solved with in ODEIM mode (odeim_points > 0), 0 for a full
+ * step or when S-hat = G (odeim_points = 0, reading A11).  Host-side value, no synchronisation. */
+int32_t hrom_points_used(const hrom_ctx* ctx);
+
+/* Make the context stream wait for work the library enqueued on its internal side stream (the
+ * eigen-solve of the last basis update, band Gram rows): an event recorded on the context stream
+ * after this call covers every kernel of the steps enqueued so far.  No host synchronisation. */
+hrom_status hrom_join(hrom_ctx* ctx);
 
 /* Synchronise the stream; returns latched device errors. */
 hrom_status hrom_sync(hrom_ctx* ctx);

@@ -79,6 +79,7 @@ def lib():
             "orc_pod": (i32, [d, i64, i32, i32, C.c_double, d, d, d]),
             "orc_shapiro_1d": (None, [d, i32, i32, i32, d]),
             "orc_gram": (None, [d, i32, i64, d, d]),
+            "orc_project": (None, [d, i64, i32, d, i32, d]),
             "orc_seam_filter": (i64, [P(Grid), P(Params), d, d, u8, u8, P(C.c_int32)]),
             "orc_run_create": (C.c_void_p, [P(Grid), P(Params), d]),
             "orc_run_destroy": (None, [C.c_void_p]),
@@ -286,6 +287,18 @@ def gram(S, rho=None):
     C_ = np.zeros((ncol, ncol))
     r = None if rho is None else _c(rho)
     lib().orc_gram(_d(S), ncol, rows, None if r is None else _d(r), _d(C_))
+    return C_
+
+
+def project(Phi, S):
+    """Phi: (m, D), S: (ncol, D) arrays; C = Phi S^T (m x ncol) with compensated sums."""
+    Phi = _c(Phi)
+    S = _c(S)
+    m, D = Phi.shape
+    ncol = S.shape[0]
+    assert S.shape[1] == D
+    C_ = np.zeros((m, ncol))
+    lib().orc_project(_d(Phi), D, m, _d(S), ncol, _d(C_))
     return C_
 
 

@@ -223,7 +223,12 @@ int32_t orc_run_step(orc_run* R, double dt_override) {
     // offset bootstrap: psi_{w-1} = mean(gamma_0..gamma_{w-1})
     const std::vector<double> psi0 = mean_of(R->snaps, R->snaps.size() - w, w, D);
     refresh_basis(R, psi0);
-    projection_indicator(R);  // bootstrap indicator (A19)
+    if (R->odeim_np > 0) {
+      // Algorithm 1: G_w = {} at k = w-1, so S-hat_w = P_w (the ODEIM points only)
+      std::fill(R->eps.begin(), R->eps.end(), 0.0);
+    } else {
+      projection_indicator(R);  // bootstrap indicator (A19: P = S-hat mode, where P_w is empty)
+    }
     select_next(R);
   } else if (k >= w) {
     // psi_k = mean(gamma_{k-w..k-1}) (lagged centring, A14; by its formula also

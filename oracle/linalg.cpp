@@ -201,4 +201,12 @@ void orc_gram(const double* S, int32_t ncol, int64_t rows, const double* rho, do
     }
 }
 
+// Projection of snapshots on a basis (config-5 kernel op; the POD
+// coefficients Phi^T (gamma - .) of P:266/P:281): C[i * ncol + j] = sum_e Phi[i][e] S[j][e],
+// Phi: m columns of D rows, S: ncol columns of D rows (both column-major), compensated sums.
+void orc_project(const double* Phi, int64_t D, int32_t m, const double* S, int32_t ncol, double* C) {
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < ncol; ++j) C[(int64_t)i * ncol + j] = dot(Phi + (int64_t)i * D, S + (int64_t)j * D, D);
+}
+
 }  // extern "C"

@@ -90,6 +90,8 @@ int32_t orc_pod(const double* X, int64_t m, int32_t w, int32_t r, double cut,
 /* Gram of shifted columns: C_ij = sum_e (S_ie - rho_e)(S_je - rho_e), S: ncol x rows
  * (row-major per column), rho nullable.  The snapshot Gram of the POD remark P:634. */
 void orc_gram(const double* S, int32_t ncol, int64_t rows, const double* rho, double* C);
+/* C = Phi^T S (m x ncol, row-major) over D rows, compensated sums (config-5 projection op) */
+void orc_project(const double* Phi, int64_t D, int32_t m, const double* S, int32_t ncol, double* C);
 
 /* ---- Shapiro filters and seam filter (A21-A24) ---- */
 void orc_shapiro_1d(const double* line, int32_t n, int32_t order, int32_t periodic, double* out);

@@ -8,7 +8,8 @@ refresh skipped before full steps) beside a full-HDM reference trajectory
   e-bar = (1/N_t) sum_k e_k
   s-bar = (1/N_t) sum_k n_{gamma_k}, n = N (full) or |S-hat|
   s-bar* = the same mean over the hybrid steps only
-  p-bar = mean ODEIM points over hybrid steps: 0 here, S-hat = G (reading A11)
+  p-bar = mean ODEIM points (n_p)_k over the hybrid steps, from hrom_points_used:
+          n_p in ODEIM mode (odeim_points > 0), 0 when S-hat = G (reading A11)
   S = t_H / t_R, the speed-up of Eq. (speedup), from CUDA-event times of the
       two trajectories' own steps on the shared stream.
 
@@ -34,6 +35,7 @@ class Algorithm1Metrics:
     e: list            # e_k, k = 1..N_t
     n_gamma: list      # n_{gamma_k}
     hybrid: list       # k has a partial HDM solve
+    points: list       # (n_p)_k, ODEIM points used by step k
     t_R_ms: float      # mean adaptive step time
     t_H_ms: Optional[float]  # mean full-HDM step time (reference trajectory)
 
@@ -52,7 +54,8 @@ class Algorithm1Metrics:
 
     @property
     def p_bar(self) -> float:
-        return 0.0
+        h = [p for p, hy in zip(self.points, self.hybrid) if hy]
+        return float(np.mean(h)) if h else 0.0
 
     @property
     def speedup(self) -> Optional[float]:
@@ -82,7 +85,7 @@ def run(wl, steps: Optional[int] = None, z: Optional[int] = None, reference: boo
     counts = torch.zeros(steps, dtype=torch.int32, device="cuda")
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     t_r = t_h = 0.0
-    es, hyb = [], []
+    es, hyb, pts = [], [], []
     ga = torch.empty((wl.c, wl.N), dtype=torch.float64, device="cuda")
     gb = torch.empty_like(ga)
     for k in range(1, steps + 1):
@@ -90,6 +93,7 @@ def run(wl, steps: Optional[int] = None, z: Optional[int] = None, reference: boo
         rom.step(count_out=counts[k - 1:k])
         ev[1].record()
         hyb.append(not (k + 1 <= wl.w or (z > 0 and k % z == 0)))
+        pts.append(rom.points_used())
         if ref is not None:
             ev[2].record()
             ref.step()
@@ -103,7 +107,7 @@ def run(wl, steps: Optional[int] = None, z: Optional[int] = None, reference: boo
         t_r += ev[0].elapsed_time(ev[1])
     rom.sync()
     n_gamma = counts.cpu().tolist()
-    out = Algorithm1Metrics(steps=steps, z=z, e=es, n_gamma=n_gamma, hybrid=hyb, t_R_ms=t_r / steps,
+    out = Algorithm1Metrics(steps=steps, z=z, e=es, n_gamma=n_gamma, hybrid=hyb, points=pts, t_R_ms=t_r / steps,
                             t_H_ms=(t_h / steps) if ref is not None else None)
     rom.close()
     if ref is not None:

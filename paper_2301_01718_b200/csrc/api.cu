@@ -189,10 +189,6 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
 
   hrom_ctx* c = new hrom_ctx();
   c->P = *p;
-  {
-    const char* ev = std::getenv("HROM_GRAM_LEGACY");
-    c->gram_legacy = ev && ev[0] == '1';
-  }
   if (c->P.rebase_period <= 0) c->P.rebase_period = p->window;
   c->w = p->window;
   c->r = p->rank;
@@ -295,6 +291,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   A(dalloc(&b.ochosen, g.N));
   A(dalloc(&b.ocoef, kMaxR + 1));
   A(dalloc(&b.orows, kOdeimMax));
+  A(dalloc(&b.orows_pub, kOdeimMax));
   A(dalloc(&b.opart_v, kOdeimBlocks));
   A(dalloc(&b.opart_e, kOdeimBlocks));
   A(dalloc(&b.ocnt, 1));
@@ -348,7 +345,7 @@ void hrom_destroy(hrom_ctx* c) {
   Bufs& b = c->b;
   void* ptrs[] = {b.ring, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
                   b.kept, b.fidx, b.ftab, b.fcur, b.fF, b.C, b.part, b.gpart, b.K, b.Khi, b.Klo, b.Rd, b.vpart, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
-                  b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.hsum, b.fstat, b.l1part, b.fcnt, (void*)b.colptr, b.slot_tab, b.ochosen, b.ocoef, b.orows, b.opart_v, b.opart_e, b.ocnt, b.ocells, b.ophi};
+                  b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.hsum, b.fstat, b.l1part, b.fcnt, (void*)b.colptr, b.slot_tab, b.ochosen, b.ocoef, b.orows, b.orows_pub, b.opart_v, b.opart_e, b.ocnt, b.ocells, b.ophi};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete c;
@@ -413,6 +410,7 @@ hrom_status hrom_full_step(hrom_ctx* c, double dt_override, double* dev_dt_out) 
   if ((s = launch_stage(c, 3, qn, U2, out, nullptr, 0, dt_override)) != HROM_OK) return s;
   prof_end(c, SEC_FULL);
   c->k = kn;
+  c->points_used = 0;
   c->last_hybrid = false;
   c->full_since_update = true;
   c->gram_row_ready = false;
@@ -488,6 +486,7 @@ hrom_status hrom_hybrid_step(hrom_ctx* c, const uint32_t* dev_mask, double dt_ov
   if ((s = launch_positivity(c, qn, out, kn)) != HROM_OK) return s;
   prof_end(c, SEC_POS);
   c->k = kn;
+  c->points_used = (c->P.odeim_points > 0 && c->odeim_k == c->k - 1) ? c->odeim_n : 0;
   c->last_hybrid = true;
   c->eps_sparse = true;  // eps: memset, then written on S-hat (fill) and kept band cells (filter)
   c->gram_row_ready = (c->P.gram_mode == 0);
@@ -560,7 +559,11 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
   c->n_owed = 0;
   const bool proj = k == w - 1 || c->full_since_update;
   c->full_since_update = false;
-  if (proj) {  // projection indicator: bootstrap (reading A19), or after a full step k >= w (G8)
+  if (proj && k == w - 1 && c->P.odeim_points > 0) {
+    // Algorithm 1: G_w = {} at k = w-1, so S-hat_w = P_w, the ODEIM points alone
+    HROM_CK(cudaMemsetAsync(c->b.eps, 0, c->g.N * sizeof(double), c->st));
+    c->eps_sparse = false;
+  } else if (proj) {  // projection indicator: bootstrap (reading A19, P = S-hat mode), or after a full step k >= w (G8)
     basis_join(c);
     zvec_kernel<<<1, 128, 0, c->st>>>(c->b.A, c->b.lam, c->b.ireg, w, k == w - 1 ? 0.0 : 1.0 / w, c->b.zvec);
     HROM_LAUNCH_CK();
@@ -731,6 +734,14 @@ hrom_status hrom_sync(hrom_ctx* c) {
     c->last_err_cell = (int64_t)bad;
     return HROM_E_POSITIVITY;
   }
+  return HROM_OK;
+}
+
+int32_t hrom_points_used(const hrom_ctx* c) { return c ? c->points_used : 0; }
+
+hrom_status hrom_join(hrom_ctx* c) {
+  if (!c) return HROM_E_INVALID;
+  basis_join(c);
   return HROM_OK;
 }
 

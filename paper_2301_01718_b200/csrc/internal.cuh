@@ -135,7 +135,8 @@ struct Bufs {
   // ODEIM workspace (odeim.cu)
   uint8_t* ochosen = nullptr;       // N: cell already a point
   double* ocoef = nullptr;          // kMaxR + 1 LSQ coefficients
-  int64_t* orows = nullptr;         // kOdeimMax chosen DOF rows
+  int64_t* orows = nullptr;         // kOdeimMax chosen DOF rows (the context's points: gappy rows)
+  int64_t* orows_pub = nullptr;     // kOdeimMax: workspace of the public hrom_odeim
   double* opart_v = nullptr;        // per-block argmax partials
   int64_t* opart_e = nullptr;
   unsigned int* ocnt = nullptr;     // last-block counter
@@ -185,8 +186,8 @@ struct hrom_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_basis_in = nullptr, ev_basis_done = nullptr;
   int odeim_n = 0;            // ODEIM points of the current basis (0: none / not computed)
+  int points_used = 0;        // ODEIM points used by the latest step (p-bar)
   int64_t odeim_k = -1;       // k of the basis they belong to
-  bool gram_legacy = false;   // HROM_GRAM_LEGACY=1: window Gram on gather_gram_kernel (A/B measurements)
   bool basis_pending = false;  // eigen-solve launched on the side stream, not yet joined
   bool eig_todo = false;       // eigen-solve deferred (launched after the sampling kernel)
   cudaEvent_t ev_bg_in = nullptr, ev_bg_done = nullptr;

@@ -1318,9 +1318,9 @@ __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ 
 
 // Phi_{k+1}[:, j] = X A[:, j] (materialised; tests/config 5), psi_cur
 // H12 lift on FP64 tensor cores: Phi[:, j] = (X - psi_prev 1^T) A[:, j] (D x r, column-major),
-// psi_cur = mean of the last w slots.  Warp-specialised like the gathered Gram: 2 producer
-// warps gather a 64-DOF tile of all nU window slots (cp.async), form X - psi_prev in place and
-// publish it; 16 consumer warps each own one 8-DOF block x four 8-mode blocks of the product
+// psi_cur = mean of the last w slots.  Warp-specialised like the gathered Gram: LF_PW = 8
+// producer warps (LF_NH = 4 threads per tile row, window means split over the four) gather a
+// 64-DOF tile of all nU window slots (cp.async), form X - psi_prev in place and publish it; 16 consumer warps each own one 8-DOF block x four 8-mode blocks of the product
 // with A (staged in smem once per CTA) and write Phi straight from the accumulators.
 constexpr int LF_RT = 64, LF_LDT = LF_RT + 4, LF_PW = 8, LF_CW = 16, LF_T = 32 * (LF_PW + LF_CW);
 constexpr int LF_NH = 32 * LF_PW / LF_RT;  // producer threads per tile row
@@ -1509,7 +1509,7 @@ hrom_status run_gather_gram(hrom_ctx* c, GGArgs& a, int ncol, int grid, double* 
 hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int64_t ns, int ncol, int64_t rows, SRef rho,
                       double* dev_C, int ldc, const int32_t* map) {
   const int grid = c->basis_pending ? c->nsm - 1 : c->nsm;
-  if (!c->gram_legacy) {
+  {
     SGArgs sg{};
     sg.cols = dev_cols;
     sg.ns = ns;

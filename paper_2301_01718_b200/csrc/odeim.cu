@@ -162,10 +162,12 @@ __global__ void __launch_bounds__(OD_T) odeim_argmax_kernel(const double* __rest
 
 using namespace hrom;
 
-extern "C" hrom_status hrom_odeim(hrom_ctx* c, const double* dev_phi, int32_t m, int32_t n_p,
-                                  int32_t* dev_cells_out, int64_t* dev_rows_out) {
-  if (!c || !dev_phi || !dev_cells_out || !dev_rows_out) return HROM_E_INVALID;
-  if (m < 1 || m > kMaxR || n_p < 0 || n_p > kOdeimMax || n_p > c->g.N) return HROM_E_INVALID;
+namespace hrom {
+// the greedy of hrom_odeim with its chosen-rows workspace `rows_ws` (kOdeimMax entries):
+// b.orows for the context's own points (the gappy rows of the ODEIM-mode step), b.orows_pub for
+// the public call, so that inspecting another basis never overwrites the rows of the next step
+static hrom_status odeim_points(hrom_ctx* c, const double* dev_phi, int32_t m, int32_t n_p, int64_t* rows_ws,
+                                int32_t* dev_cells_out, int64_t* dev_rows_out) {
   const int64_t D = c->g.D, N = c->g.N;
   HROM_CK(cudaMemsetAsync(c->b.ochosen, 0, N, c->st));
   const int grid = (int)std::min<int64_t>(kOdeimBlocks, std::max<int64_t>(1, (D + OD_T - 1) / OD_T));
@@ -174,17 +176,25 @@ extern "C" hrom_status hrom_odeim(hrom_ctx* c, const double* dev_phi, int32_t m,
     if (l > 0) {
       const size_t smem = (size_t)(l + 1) * j * sizeof(double);
       HROM_CK(cudaFuncSetAttribute(odeim_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      odeim_solve_kernel<<<1, OD_T, smem, c->st>>>(dev_phi, D, c->b.orows, j, l, c->P.lsq_rel_cutoff, c->b.ocoef);
+      odeim_solve_kernel<<<1, OD_T, smem, c->st>>>(dev_phi, D, rows_ws, j, l, c->P.lsq_rel_cutoff, c->b.ocoef);
       HROM_LAUNCH_CK();
       ++c->nlaunch;
     }
     odeim_argmax_kernel<<<grid, OD_T, 0, c->st>>>(dev_phi, D, N, l, c->b.ocoef, c->b.ochosen, c->b.opart_v,
-                                                   c->b.opart_e, c->b.ocnt, c->b.orows, j, dev_cells_out,
+                                                   c->b.opart_e, c->b.ocnt, rows_ws, j, dev_cells_out,
                                                    dev_rows_out);
     HROM_LAUNCH_CK();
     ++c->nlaunch;
   }
   return HROM_OK;
+}
+}  // namespace hrom
+
+extern "C" hrom_status hrom_odeim(hrom_ctx* c, const double* dev_phi, int32_t m, int32_t n_p,
+                                  int32_t* dev_cells_out, int64_t* dev_rows_out) {
+  if (!c || !dev_phi || !dev_cells_out || !dev_rows_out) return HROM_E_INVALID;
+  if (m < 1 || m > kMaxR || n_p < 0 || n_p > kOdeimMax || n_p > c->g.N) return HROM_E_INVALID;
+  return odeim_points(c, dev_phi, m, n_p, c->b.orows_pub, dev_cells_out, dev_rows_out);
 }
 
 namespace hrom {
@@ -202,7 +212,7 @@ hrom_status odeim_for_basis(hrom_ctx* c) {
   const int np = (int)std::min<int64_t>(c->P.odeim_points, c->g.N);
   c->odeim_n = 0;
   if (reff < 1) return HROM_OK;
-  if ((s = hrom_odeim(c, c->b.ophi, reff, np, c->b.ocells, c->b.orows)) != HROM_OK) return s;
+  if ((s = odeim_points(c, c->b.ophi, reff, np, c->b.orows, c->b.ocells, c->b.orows)) != HROM_OK) return s;
   c->odeim_n = np;
   c->odeim_k = c->k;
   return HROM_OK;

@@ -62,6 +62,8 @@ _SIGS = {
     "hrom_step_ex": (C.c_int, [_VP, C.c_double, _VP]),
     "hrom_rel_l1_error": (C.c_int, [_VP, _VP, _VP, C.POINTER(C.c_double)]),
     "hrom_sync": (C.c_int, [_VP]),
+    "hrom_join": (C.c_int, [_VP]),
+    "hrom_points_used": (C.c_int32, [_VP]),
     "hrom_error_cell": (C.c_int64, [_VP]),
     "hrom_step_index": (C.c_int64, [_VP]),
     "hrom_effective_rank": (C.c_int32, [_VP]),
@@ -262,6 +264,14 @@ class HybridROM:
         if code == 3:
             raise HromError(code, f"hrom_sync (cell {self.lib.hrom_error_cell(self.h)})")
         _ck(code, "hrom_sync")
+
+    def join(self):
+        """Context stream waits for the library's side-stream work (no host sync)."""
+        _ck(self.lib.hrom_join(self.h), "hrom_join")
+
+    def points_used(self) -> int:
+        """ODEIM points (n_p)_k of the latest step; 0 for full steps / S-hat = G."""
+        return int(self.lib.hrom_points_used(self.h))
 
     @property
     def k(self) -> int:

@@ -191,5 +191,9 @@ def test_rre_and_odeim_driver_sets(orc, inputs):
         want = G.copy()
         want[cells] = 1
         assert np.array_equal(S, want), k
+        if k == wl.w - 1:
+            # Algorithm 1: G_w = {} at k = w-1, so S-hat_w = P_w exactly
+            assert not np.any(R.eps()) and G.sum() == 0
+            assert np.array_equal(np.nonzero(S)[0], np.unique(cells))
         assert len(set(cells.tolist())) == len(cells)
     assert np.all(np.isfinite(R.state()))

@@ -144,3 +144,24 @@ def test_gram_matches_definition(orc, inputs):
     ref = np.array([[float(np.sum((S[i] - rho) * (S[j] - rho))) for j in range(7)] for i in range(7)])
     np.testing.assert_allclose(C, ref, rtol=1e-13)
     assert np.array_equal(C, C.T)
+
+
+def test_project_exact_integers_and_coefficients(orc, inputs):
+    """orc_project (C = Phi^T S, the config-5 projection op): (i) small-integer Phi and S give the
+    exact integer product (every partial sum is an integer < 2^53), checked against int64
+    arithmetic, with m != ncol so a transposed operand or swapped index fails; (ii) for
+    orthonormal Phi and S = Phi Y + (I - Phi Phi^T) Z the projection returns Y (the POD
+    coefficients) to rounding."""
+    rng = np.random.default_rng(12)
+    D, m, ncol = 257, 5, 7
+    Pi = rng.integers(-9, 10, size=(m, D))
+    Si = rng.integers(-9, 10, size=(ncol, D))
+    C = orc.project(Pi.astype(np.float64), Si.astype(np.float64))
+    assert C.shape == (m, ncol)
+    assert np.array_equal(C, (Pi @ Si.T).astype(np.float64))
+    Q, _ = np.linalg.qr(inputs.random_matrix(13, 2000, 6))
+    Y = inputs.random_matrix(14, 6, 9)
+    Z = inputs.random_matrix(15, 2000, 9)
+    S = Q @ Y + (Z - Q @ (Q.T @ Z))
+    C = orc.project(Q.T.copy(), S.T.copy())
+    np.testing.assert_allclose(C, Y, rtol=0, atol=1e-13 * np.abs(Y).max())

@@ -336,3 +336,113 @@ def test_odeim_vs_brute_force_and_deim_property(orc, m, c, N, n_p, seed):
         s_int = np.linalg.svd(phi[:, rows[:m]], compute_uv=False)[-1]
         s_ovs = np.linalg.svd(phi[:, rows], compute_uv=False)[-1]
         assert s_ovs >= s_int - 1e-15  # adding rows never lowers sigma_min (Cauchy interlacing)
+
+
+# ---------------- seam filter vs an independent brute force ----------------
+def _brute_seam_filter(orc, wl, v, F, S, eps_rule="relative"):
+    """Independent statement of the residual-gated filter cascade of P:424-438 (readings
+    A21-A24): band B = (S-hat (+) Q_W) \\ S-hat; per order of the cascade 2 -> 4 -> 6, sweeps
+    j = 1..j_max of  v' = S^x(v) on B  (whole grid lines through orc.shapiro_1d, pinned by the
+    closed-form responses above), then  v'' = S^y(v')  on B, residual r = max_var |. - F| per
+    cell, keep v'' where r strictly decreases; stop the order when nothing is kept or the largest
+    decrease is below eps_f ("relative": (r_old - r_new) / r_old, reading A23; "absolute":
+    r_old - r_new, the literal alternative -- used only to show the pins can tell them apart)."""
+    nx, ny, N, c = wl.nx, (wl.ny if wl.dim == 2 else 1), wl.N, wl.c
+    per = wl.bc == 1
+    if wl.W < 0:
+        B = (S == 0).astype(np.uint8)
+    else:
+        offs = [(a, b) for a in range(-wl.W, wl.W + 1) for b in (range(-wl.W, wl.W + 1) if wl.dim == 2 else [0])]
+        B = _brute_dilate(wl, S, offs) & (1 - S)
+    band = np.nonzero(B)[0]
+    v = v.copy()
+    kept = np.zeros(N, np.uint8)
+    sweeps = []
+    for order in wl.filter_orders:
+        nsw = 0
+        for _ in range(wl.filter_max_sweeps):
+            nsw += 1
+            vp = v.copy()
+            for var in range(c):
+                g = v[var].reshape(ny, nx)
+                xs = np.stack([orc.shapiro_1d(g[j], order, per) for j in range(ny)])
+                vp[var, band] = xs.reshape(-1)[band]
+            vpp = vp.copy()
+            if wl.dim == 2:
+                for var in range(c):
+                    g = vp[var].reshape(ny, nx)
+                    ys = np.stack([orc.shapiro_1d(g[:, i], order, per) for i in range(nx)], axis=1)
+                    vpp[var, band] = ys.reshape(-1)[band]
+            r_old = np.max(np.abs(v[:, band] - F[:, band]), axis=0)
+            r_new = np.max(np.abs(vpp[:, band] - F[:, band]), axis=0)
+            keep = r_new < r_old
+            if not keep.any():
+                break
+            cells = band[keep]
+            kept[cells] = 1
+            v[:, cells] = vpp[:, cells]
+            dec = r_old[keep] - r_new[keep]
+            if eps_rule == "relative":
+                dec = dec / r_old[keep]
+            if dec.max() < wl.filter_eps:
+                break
+        sweeps.append(nsw)
+    return v, kept, sweeps
+
+
+@pytest.mark.parametrize("dim,nx,ny,bc,W,nS,seed", [(2, 28, 20, 0, 3, 12, 1), (2, 28, 20, 1, 3, 12, 2),
+                                                    (2, 17, 23, 0, 2, 30, 3), (2, 20, 16, 1, -1, 8, 4),
+                                                    (1, 90, 1, 0, 3, 6, 5), (1, 64, 1, 1, 3, 5, 6)])
+def test_seam_filter_vs_brute_force(orc, inputs, dim, nx, ny, bc, W, nS, seed):
+    """orc_seam_filter equals the numpy brute force above on random hybrid states: same output
+    bit for bit (the same stencil sums in the same order), kept set and sweep counts."""
+    wl = _wl(inputs, dim=dim, nx=nx, ny=ny, bc=bc, seed=seed, W=W)
+    rng = np.random.default_rng(seed)
+    F = inputs.initial_condition(wl, "random")
+    v = F * (1.0 + 0.05 * rng.standard_normal(F.shape))
+    S = np.zeros(wl.N, np.uint8)
+    S[rng.choice(wl.N, nS, replace=False)] = 1
+    v[:, S == 1] = F[:, S == 1]
+    out, kept, sweeps = orc.seam_filter(wl, v, F, S)
+    bo, bk, bs = _brute_seam_filter(orc, wl, v, F, S)
+    assert list(sweeps[:len(bs)]) == bs
+    assert np.array_equal(kept, bk)
+    np.testing.assert_allclose(out, bo, rtol=2e-16, atol=0)
+
+
+def test_seam_filter_x_only_checkerboard(orc, inputs):
+    """Closed form that separates the x- and y-passes: F constant plus a(-1)^i (varying in x only)
+    on a periodic grid, whole-domain band (S-hat empty).  The order-2 x-pass annihilates the x
+    Nyquist mode, so v' = F and v'' = S^y(v') = F on every cell: all cells kept in sweep 1, nothing
+    in sweep 2, output = F bit for bit.  A y-pass reading v instead of v' would return v (constant
+    along y) and keep nothing."""
+    wl = dataclasses.replace(_wl(inputs, nx=24, ny=18, bc=1, seed=1), W=-1)
+    F = np.empty((wl.c, wl.N))
+    F[:] = np.array([1.0, 0.25, -0.5, 2.5])[:, None]
+    i = np.tile(np.arange(wl.nx), wl.ny)
+    v = F + np.array([2.0 ** -10, 2.0 ** -9, 2.0 ** -8, 2.0 ** -7])[:, None] * ((-1.0) ** i)[None, :]
+    out, kept, sweeps = orc.seam_filter(wl, v, F, np.zeros(wl.N, np.uint8))
+    assert np.array_equal(out, F)
+    assert kept.sum() == wl.N and sweeps[0] == 2
+    bo, bk, bs = _brute_seam_filter(orc, wl, v, F, np.zeros(wl.N, np.uint8))
+    assert np.array_equal(bo, F) and bs == list(sweeps[:len(bs)])
+
+
+def test_seam_filter_relative_not_absolute_eps(orc, inputs):
+    """The eps_f stop is relative (reading A23): with residuals of order 1e-6 every absolute
+    decrease is far below eps_f = 1e-2, so an absolute stop would end each order after its first
+    sweep; the relative rule keeps sweeping while some cell's residual drops by >= 1 %.  The oracle
+    follows the relative brute force, and the two rules give different sweep counts here."""
+    wl = _wl(inputs, nx=28, ny=20, bc=1, seed=7)
+    rng = np.random.default_rng(7)
+    F = np.empty((wl.c, wl.N))
+    F[:] = np.array([1.0, 0.25, -0.5, 2.5])[:, None]  # smooth reference: the filter removes the noise
+    v = F + 1e-6 * rng.standard_normal(F.shape)
+    S = np.zeros(wl.N, np.uint8)
+    S[rng.choice(wl.N, 10, replace=False)] = 1
+    v[:, S == 1] = F[:, S == 1]
+    out, kept, sweeps = orc.seam_filter(wl, v, F, S)
+    _, _, rel_sw = _brute_seam_filter(orc, wl, v, F, S, "relative")
+    _, _, abs_sw = _brute_seam_filter(orc, wl, v, F, S, "absolute")
+    assert list(sweeps[:len(rel_sw)]) == rel_sw
+    assert rel_sw != abs_sw and max(rel_sw) > 1 and abs_sw == [1] * len(abs_sw)

@@ -1,8 +1,7 @@
 """Window-Gram (H10 / K11) timing through hrom_gram: C = (S - rho)^T (S - rho) over `rows` rows of
 `ncol` plain fp64 columns on the FP64 tensor cores.  Reports ms, the symmetric flop count
 rows * ncol * (ncol + 1) per second and its fraction of the measured DMMA peak
-(profiles/r1_dmma_peak.json, 37.1 TF/s at 1965 MHz).  HROM_GRAM_LEGACY=1 selects the previous
-kernel (gather_gram_kernel) for A/B comparisons.
+(profiles/r1_dmma_peak.json, 37.1 TF/s at 1965 MHz).
 
 python tools/gram_bench.py --rows 67108864 --ncol 129     (config 5: 4096^2 x 4 vars, w = 128)
 python tools/gram_bench.py --rows 16777216 --ncol 65      (config 4 re-base: 2048^2 x 4, w = 64)
@@ -45,7 +44,7 @@ for _ in range(args.reps):
     ts.append(e0.elapsed_time(e1))
 ms = min(ts)
 fl = args.rows * args.ncol * (args.ncol + 1)
-out = {"rows": args.rows, "ncol": args.ncol, "legacy": os.environ.get("HROM_GRAM_LEGACY") == "1",
+out = {"rows": args.rows, "ncol": args.ncol, 
        "ms_best": ms, "ms_all": ts, "tflops_symmetric": fl / ms / 1e9, "frac_dmma_peak": fl / ms / 1e9 / PEAK}
 if args.check:
     X = S - rho
