@@ -62,7 +62,9 @@ typedef struct {
   double lsq_rel_cutoff;     /* pinv cut on lambda(A^T A) (1e-12, A13) */
   double sample_fraction;    /* f: n_g = ceil(f N) HDM cells per hybrid step (A18) */
   int32_t gram_mode;         /* 0 incremental shifted Gram (default), 1 full DMMA Gram every step */
-  int32_t rebase_period;     /* steps between shifted-Gram re-bases (<= 0: w) */
+  int32_t rebase_period;     /* steps between shifted-Gram re-bases (<= 0: never; the window Gram
+                                is double-double, G11, so the shift's cancellation in the
+                                centring algebra stays below fp64 output precision) */
   int32_t gather_mode;       /* 0: gathered Gram of the S-hat rows updated from the previous
                                 step (S-hat churn rows + the new snapshot and HDM columns),
                                 1: recomputed over all S-hat rows every step (G7) */
@@ -158,6 +160,18 @@ hrom_status hrom_filter(hrom_ctx* ctx, const uint32_t* dev_mask, double* dev_v, 
  * step), for the sampling averages s-bar, s-bar* of P:715-727. */
 hrom_status hrom_step(hrom_ctx* ctx, double dt_override);
 hrom_status hrom_step_ex(hrom_ctx* ctx, double dt_override, int32_t* dev_count_out);
+
+/* CUDA-graph replay of hrom_step (NEXT-3).  enable != 0: a steady-state step of Algorithm 1
+ * (a hybrid step, then the basis update and the sampling; z = infinity, no ODEIM points,
+ * incremental Grams, profiling off, no count output) is captured into a CUDA graph the first
+ * time its ring phase k mod (w + 2) occurs -- its kernel arguments depend on k only through the
+ * ring slots -- and replayed with cudaGraphLaunch afterwards, the host bookkeeping advanced as
+ * the captured step left it.  Other steps run eagerly.  In graph mode the eigen-solve of a basis
+ * starts with the next step (not with the sampling), so a captured step joins all its side-
+ * stream work.  Results are bitwise identical to eager steps.  Graphs are freed by
+ * hrom_set_graph(ctx, 0) and hrom_destroy. */
+hrom_status hrom_set_graph(hrom_ctx* ctx, int32_t enable);
+int64_t hrom_graph_launches(const hrom_ctx* ctx);  /* steps run from a graph so far */
 
 /* Relative L1 error of Algorithm 1: e = sum |a - b| / sum |b| over the D entries
  * of two device states (uniform cell volumes; the per-cell 1-norm over the c variables).

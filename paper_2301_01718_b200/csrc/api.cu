@@ -189,7 +189,9 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
 
   hrom_ctx* c = new hrom_ctx();
   c->P = *p;
-  if (c->P.rebase_period <= 0) c->P.rebase_period = p->window;
+  // the window Gram is double-double (G11): the shift's cancellation in the centring algebra
+  // costs nothing at fp64 output precision, so by default the shift is never re-based
+  if (c->P.rebase_period <= 0) c->P.rebase_period = INT32_MAX;
   c->w = p->window;
   c->r = p->rank;
   c->nslots = c->w + 2;
@@ -257,22 +259,28 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   A(dalloc(&b.fcur, g.Dp));
   A(dalloc(&b.fF, g.Dp));
   A(dalloc(&b.C, (size_t)kMaxSlots * kMaxSlots));
+  A(dalloc(&b.Clo, (size_t)kMaxSlots * kMaxSlots));
+  A(dalloc(&b.Rlo, (size_t)(kMaxW + 2) * (kMaxW + 2)));
+  A(dalloc(&b.Mdd, (size_t)2 * kMaxSlots * kMaxSlots));
+  A(dalloc(&b.Zf, (size_t)kMaxSlots * kMaxSlots));
+  A(dalloc(&b.rfws, (size_t)5 * kMaxSlots * kMaxSlots));
+  A(dalloc(&b.Tg, (size_t)2 * (kMaxW + 1) * kMaxR));
   b.part_len = (int64_t)2 * c->nsm * 144 * 144;
   A(dalloc(&b.part, b.part_len));
-  b.gpart_len = (int64_t)(c->fill_blocks + c->band_blocks) * (kMaxSlots + 1);
+  b.gpart_len = (int64_t)(c->fill_blocks + c->band_blocks) * (kMaxSlots + 1) * 2;  // double-double
   A(dalloc(&b.gpart, b.gpart_len));
-  A(dalloc(&b.K, (size_t)(kMaxW + 2) * (kMaxW + 2)));
+  A(dalloc(&b.K, (size_t)2 * (kMaxW + 2) * (kMaxW + 2)));
   A(dalloc(&b.Khi, (size_t)kMaxSlots * kMaxSlots));
   A(dalloc(&b.Klo, (size_t)kMaxSlots * kMaxSlots));
-  A(dalloc(&b.Rd, (size_t)2 * (kMaxW + 2) * (kMaxW + 2)));
-  A(dalloc(&b.vpart, (size_t)8 * c->nsm * (2 * kMaxSlots + 2)));
+  A(dalloc(&b.Rd, (size_t)4 * (kMaxW + 2) * (kMaxW + 2)));
+  A(dalloc(&b.vpart, (size_t)2 * 8 * c->nsm * (2 * kMaxSlots + 2)));
   A(dalloc(&b.A, (size_t)kMaxW * kMaxR));
   A(dalloc(&b.lam, kMaxSlots));
   A(dalloc(&b.y, kMaxR));
   A(dalloc(&b.cvec, kMaxW));
   A(dalloc(&b.zvec, kMaxW));
   A(dalloc(&b.eigV, (size_t)kMaxSlots * kMaxSlots));
-  A(dalloc(&b.eigA, (size_t)5 * kMaxSlots * (kMaxR + 1)));  // eigen-solve LU workspace when not in smem
+  A(dalloc(&b.eigA, (size_t)5 * kMaxSlots * (kMaxSlots + 1)));  // eigen-solve LU workspace when not in smem
   A(dalloc(&b.ireg, 16));
   A(dalloc(&b.dreg, 16));
   A(dalloc(&b.ureg, 4));
@@ -310,6 +318,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   if (cudaMemcpy(b.colptr, tab.data(), tab.size() * sizeof(double*), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(b.slot_tab, stab.data(), stab.size() * sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemset(b.C, 0, sizeof(double) * kMaxSlots * kMaxSlots) != cudaSuccess ||
+      cudaMemset(b.Clo, 0, sizeof(double) * kMaxSlots * kMaxSlots) != cudaSuccess ||
       cudaMemset(b.ureg, 0xff, 4 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMemset(b.ireg, 0, 16 * sizeof(int32_t)) != cudaSuccess ||
       cudaMemset(b.eps, 0, g.N * sizeof(double)) != cudaSuccess ||
@@ -342,9 +351,11 @@ void hrom_destroy(hrom_ctx* c) {
   if (c->ev_bg_in) cudaEventDestroy(c->ev_bg_in);
   if (c->ev_bg_done) cudaEventDestroy(c->ev_bg_done);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  for (auto& gs : c->graphs)
+    if (gs.exec) cudaGraphExecDestroy(gs.exec);
   Bufs& b = c->b;
   void* ptrs[] = {b.ring, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
-                  b.kept, b.fidx, b.ftab, b.fcur, b.fF, b.C, b.part, b.gpart, b.K, b.Khi, b.Klo, b.Rd, b.vpart, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
+                  b.kept, b.fidx, b.ftab, b.fcur, b.fF, b.C, b.Clo, b.Rlo, b.Mdd, b.Zf, b.rfws, b.Tg, b.part, b.gpart, b.K, b.Khi, b.Klo, b.Rd, b.vpart, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
                   b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.hsum, b.fstat, b.l1part, b.fcnt, (void*)b.colptr, b.slot_tab, b.ochosen, b.ocoef, b.orows, b.orows_pub, b.opart_v, b.opart_e, b.ocnt, b.ocells, b.ophi};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -520,8 +531,8 @@ hrom_status hrom_update_basis(hrom_ctx* c) {
     const int s0 = W.slot[0];
     // consecutive slots are contiguous in the pointer table (see hrom_create); the Gram is
     // written straight into the slot-indexed C through the slot table
-    if ((s = gram_full(c, c->b.colptr + s0, c->g.nsr, W.nU, c->g.D, c->rho_ref(), c->b.C, kMaxSlots,
-                       c->b.slot_tab + s0)) != HROM_OK)
+    if ((s = gram_full_dd(c, c->b.colptr + s0, c->g.nsr, W.nU, c->g.D, c->rho_ref(), c->b.C, c->b.Clo, kMaxSlots,
+                          c->b.slot_tab + s0)) != HROM_OK)
       return s;
     prof_end(c, SEC_REBASE);
     prof_begin(c, SEC_BASIS);
@@ -585,8 +596,9 @@ hrom_status hrom_sample(hrom_ctx* c, double fraction, const double* dev_eps, uin
   const int64_t n_g = (int64_t)std::ceil(fraction * (double)c->g.N);
   hrom_status s;
   // the deferred eigen-solve starts first on the side stream; the cooperative sampling kernel
-  // then runs on the other SMs (grid nsm - 1), so the eigen overlaps the sampling too
-  if ((s = flush_eigen(c)) != HROM_OK) return s;
+  // then runs on the other SMs (grid nsm - 1), so the eigen overlaps the sampling too.  In graph
+  // mode it starts with the next step instead (a captured step must join its side-stream work)
+  if (!c->graph_on && (s = flush_eigen(c)) != HROM_OK) return s;
   if (c->P.odeim_points > 0 && (s = odeim_for_basis(c)) != HROM_OK) return s;
   prof_begin(c, SEC_SAMPLE);
   if ((s = select_and_build(c, dev_eps ? dev_eps : c->b.eps, n_g)) != HROM_OK) return s;
@@ -613,7 +625,7 @@ hrom_status hrom_sample_rre(hrom_ctx* c, double delta, const double* dev_eps, ui
   if (!c) return HROM_E_INVALID;
   if (!(delta > 0.0 && delta <= 1.0)) return HROM_E_INVALID;
   hrom_status s;
-  if ((s = flush_eigen(c)) != HROM_OK) return s;
+  if (!c->graph_on && (s = flush_eigen(c)) != HROM_OK) return s;
   if (c->P.odeim_points > 0 && (s = odeim_for_basis(c)) != HROM_OK) return s;
   prof_begin(c, SEC_SAMPLE);
   if ((s = select_and_build(c, dev_eps ? dev_eps : c->b.eps, 0, delta)) != HROM_OK) return s;
@@ -666,9 +678,146 @@ hrom_status hrom_filter(hrom_ctx* c, const uint32_t* dev_mask, double* dev_v, co
   return HROM_OK;
 }
 
+namespace {
+HostSnap snap_get(const hrom_ctx* c, double dt_override) {
+  HostSnap h;
+  h.k = c->k;
+  h.rebase_k = c->rebase_k;
+  h.smax_k = c->smax_k;
+  h.kinc_newest = c->kinc_newest;
+  h.kinc_rebase = c->kinc_rebase;
+  h.odeim_k = c->odeim_k;
+  h.nlaunch = c->nlaunch;
+  h.last_err_cell = c->last_err_cell;
+  h.basis_ready = c->basis_ready;
+  h.sets_ready = c->sets_ready;
+  h.gram_row_ready = c->gram_row_ready;
+  h.full_since_update = c->full_since_update;
+  h.last_hybrid = c->last_hybrid;
+  h.basis_pending = c->basis_pending;
+  h.eig_todo = c->eig_todo;
+  h.bg_pending = c->bg_pending;
+  h.kinc_valid = c->kinc_valid;
+  h.eps_sparse = c->eps_sparse;
+  h.n_owed = c->n_owed;
+  h.samples_since_gather = c->samples_since_gather;
+  h.fill_grid = c->fill_grid;
+  h.odeim_n = c->odeim_n;
+  h.points_used = c->points_used;
+  for (int i = 0; i < 4; ++i) h.owed_rows[i] = c->owed_rows[i];
+  h.dt_override = dt_override;
+  h.win = c->win;
+  h.eig_win = c->eig_win;
+  return h;
+}
+// the entry state of a captured step, up to the shift of the k-tracking fields by a whole
+// number of ring periods
+bool snap_same(const HostSnap& a, const HostSnap& b, int nslots) {
+  const int64_t dk = b.k - a.k;
+  return dk % nslots == 0 && b.smax_k - a.smax_k == dk && b.kinc_newest - a.kinc_newest == dk &&
+         a.rebase_k == b.rebase_k && a.kinc_rebase == b.kinc_rebase && a.odeim_k == b.odeim_k &&
+         a.basis_ready == b.basis_ready && a.sets_ready == b.sets_ready && a.gram_row_ready == b.gram_row_ready &&
+         a.full_since_update == b.full_since_update && a.last_hybrid == b.last_hybrid &&
+         a.basis_pending == b.basis_pending && a.eig_todo == b.eig_todo && a.bg_pending == b.bg_pending &&
+         a.kinc_valid == b.kinc_valid && a.eps_sparse == b.eps_sparse && a.n_owed == b.n_owed &&
+         a.samples_since_gather == b.samples_since_gather && a.fill_grid == b.fill_grid &&
+         a.odeim_n == b.odeim_n && a.dt_override == b.dt_override;
+}
+void snap_apply(hrom_ctx* c, const HostSnap& post, int64_t dk, int64_t dlaunch) {
+  c->k = post.k + dk;
+  c->rebase_k = post.rebase_k;
+  c->smax_k = post.smax_k + dk;
+  c->kinc_newest = post.kinc_newest + dk;
+  c->kinc_rebase = post.kinc_rebase;
+  c->odeim_k = post.odeim_k;
+  c->nlaunch += dlaunch;
+  c->basis_ready = post.basis_ready;
+  c->sets_ready = post.sets_ready;
+  c->gram_row_ready = post.gram_row_ready;
+  c->full_since_update = post.full_since_update;
+  c->last_hybrid = post.last_hybrid;
+  c->basis_pending = post.basis_pending;
+  c->eig_todo = post.eig_todo;
+  c->bg_pending = post.bg_pending;
+  c->kinc_valid = post.kinc_valid;
+  c->eps_sparse = post.eps_sparse;
+  c->n_owed = post.n_owed;
+  c->samples_since_gather = post.samples_since_gather;
+  c->fill_grid = post.fill_grid;
+  c->odeim_n = post.odeim_n;
+  c->points_used = post.points_used;
+  c->win = post.win;
+  c->eig_win = post.eig_win;
+}
+// a step the graph path may capture / replay: Algorithm 1 in its steady state (a hybrid step
+// followed by the basis update and the sampling, z = infinity), no host-visible outputs
+bool graph_eligible(const hrom_ctx* c, int32_t* dev_count_out) {
+  return c->graph_on && !c->prof && dev_count_out == nullptr && c->P.full_period <= 0 && c->P.odeim_points == 0 &&
+         c->P.gram_mode == 0 && c->P.gather_mode == 0 && c->k >= c->w + 1 && c->last_hybrid && c->sets_ready &&
+         c->basis_ready && c->eig_todo && !c->basis_pending && !c->bg_pending && c->kinc_valid &&
+         c->samples_since_gather == 1 && c->kinc_newest == c->k && c->smax_k == c->k && c->n_owed == 0 &&
+         !hrom_sync_debug();
+}
+hrom_status step_eager(hrom_ctx* c, double dt_override, int32_t* dev_count_out);
+}  // namespace
+
 hrom_status hrom_step_ex(hrom_ctx* c, double dt_override, int32_t* dev_count_out) {
   if (!c) return HROM_E_INVALID;
   if (c->k < 0) return HROM_E_STATE;
+  if (!graph_eligible(c, dev_count_out)) return step_eager(c, dt_override, dev_count_out);
+  GraphSlot& gs = c->graphs[c->slot_of(c->k)];
+  const HostSnap entry = snap_get(c, dt_override);
+  if (gs.exec && snap_same(gs.pre, entry, c->nslots)) {
+    snap_apply(c, gs.post, entry.k - gs.pre.k, gs.post.nlaunch - gs.pre.nlaunch);
+    HROM_CK(cudaGraphLaunch(gs.exec, c->st));
+    ++c->graph_launches;
+    return HROM_OK;
+  }
+  // capture this step (nothing executes while capturing), instantiate, then launch it
+  if (gs.exec) {
+    cudaGraphExecDestroy(gs.exec);
+    gs.exec = nullptr;
+  }
+  HROM_CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+  const hrom_status s = step_eager(c, dt_override, nullptr);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(c->st, &graph);
+  if (s != HROM_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return s;
+  }
+  HROM_CK(ec);
+  const cudaError_t ei = cudaGraphInstantiate(&gs.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  HROM_CK(ei);
+  gs.pre = entry;
+  gs.post = snap_get(c, dt_override);
+  ++c->graph_captures;
+  HROM_CK(cudaGraphLaunch(gs.exec, c->st));
+  ++c->graph_launches;
+  return HROM_OK;
+}
+
+hrom_status hrom_set_graph(hrom_ctx* c, int32_t enable) {
+  if (!c) return HROM_E_INVALID;
+  c->graph_on = enable != 0;
+  if (c->graph_on && c->graphs.empty()) c->graphs.resize(c->nslots);
+  if (!c->graph_on) {
+    // the eager path flushes the deferred eigen-solve at the sampling; a pending one (graph mode
+    // defers it to the next step) is launched by the next step's flush_eigen as well
+    for (auto& gs : c->graphs)
+      if (gs.exec) {
+        cudaGraphExecDestroy(gs.exec);
+        gs.exec = nullptr;
+      }
+  }
+  return HROM_OK;
+}
+
+int64_t hrom_graph_launches(const hrom_ctx* c) { return c ? c->graph_launches : 0; }
+
+namespace {
+hrom_status step_eager(hrom_ctx* c, double dt_override, int32_t* dev_count_out) {
   const int64_t kn = c->k + 1;
   const int64_t z = c->P.full_period;
   // Algorithm 1 line P:557: full HDM step while k+1 <= w or k mod z = 0
@@ -706,6 +855,7 @@ hrom_status hrom_step_ex(hrom_ctx* c, double dt_override, int32_t* dev_count_out
   }
   return HROM_OK;
 }
+}  // namespace
 
 hrom_status hrom_step(hrom_ctx* c, double dt_override) { return hrom_step_ex(c, dt_override, nullptr); }
 

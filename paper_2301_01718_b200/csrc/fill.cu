@@ -7,19 +7,21 @@
 //     partial-HDM value on S-hat (Eq. 6b),
 //   * writes the per-DOF squared reconstruction error on S-hat,
 //   * accumulates the new row of the shifted window Gram <gamma_k - rho, gamma_s - rho>
-//     for every window slot s (reading A14), skipping seam-band cells (added after the
-//     filter by filter.cu).
+//     for every window slot s (reading A14) in double-double (G11), skipping seam-band cells
+//     (added after the filter by the band GEMV).
 // psi_prev / psi_cur are recomputed from the columns in registers: the
 // reference state is never stored or drifted.
 //
 // Data path: the ring is in slab layout (internal.cuh), so a tile -- all w+3 slab slots of
 // TILE DOFs -- is ONE contiguous run fetched by ONE cp.async.bulk (TMA) into a ring of
-// shared-memory stages by a producer warp.  NCW compute warps each own 32 DOFs of the tile
-// (one per lane), run over the slots twice (sums -> gamma_k, then the Gram row into per-lane
-// accumulators) and release the stage through an mbarrier: no CTA-wide barrier in the stream.
+// shared-memory stages by a producer warp.  NCW compute warps each own 16 DOFs of the tile
+// (one lane pair per DOF), run over the slots twice (sums -> gamma_k, then the Gram row into
+// per-lane double-double accumulators) and release the stage through an mbarrier: no CTA-wide
+// barrier in the stream.
 #include <algorithm>
 #include "internal.cuh"
 #include "async.cuh"
+#include "dd.cuh"
 
 namespace hrom {
 namespace {
@@ -45,14 +47,16 @@ struct FillArgs {
   const uint32_t* mS;
   const uint32_t* mB;
   double* eps_elem;
-  double* part;            // [grid][nU+1]
+  double* part;            // [grid][nU+1][hi, lo]
   const unsigned long long* run_if;  // nullable: run only if *run_if != ~0 (escalated step)
 };
 
 // SH: compile-time upper bound of the physical slots per half (ceil((w + 2) / 2)).
-// A DOF is owned by a lane pair (l, l ^ 16) of a compute warp; each lane holds its half of
-// the DOF's slot values in registers (SH doubles) and SH Gram accumulators.
-template <int SH>
+// A DOF is owned by a lane pair (l, l ^ 16) of a compute warp; each lane reads its half of the
+// DOF's slot values from the staged tile and holds SH double-double Gram accumulators.
+// GRAM: the instantiation accumulates the Gram row (do_gram); without it the double-double
+// accumulators are compiled out (projection mode, wide windows).
+template <int SH, bool GRAM>
 __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   if (a.run_if && *a.run_if == ~0ull) return;  // conditional re-run (positivity escalation)
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -64,7 +68,7 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   uint64_t* empty = full + a.nstage;
   // per PHYSICAL slot p: in-window flag (cA) and coefficient c (cX)
   __shared__ double cA[kMaxSlots + 2], cX[kMaxSlots + 2];
-  __shared__ double wred[NCW][2 * SH + 1];
+  __shared__ double wred[NCW][2 * SH + 1], wredl[NCW][2 * SH + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Geo& g = a.g;
   const int xoff = nU - w;  // logical: psi_cur and X use slots >= xoff; psi_prev uses slots < w
@@ -108,10 +112,11 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   for (int q = 0; q < nsl; ++q) csum += cX[q];
   const double inv_w = 1.0 / (double)w;
   const int roff = a.rho_slot * TILE;
-  double acc[SH];
+  // Gram-row accumulators in double-double (dd.cuh, G11): the row enters the POD's Gram
+  double acc[SH], accl[SH];
 #pragma unroll
-  for (int i = 0; i < SH; ++i) acc[i] = 0.0;
-  double acc_self = 0.0;
+  for (int i = 0; i < SH; ++i) acc[i] = accl[i] = 0.0;
+  double acc_self = 0.0, acc_selfl = 0.0;
   // per-DOF side data (mask words, HDM value / new column) is fetched one tile ahead
   uint32_t wS = 0, wB = 0;
   int bitpos = 0;
@@ -154,24 +159,22 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     mbar_wait(&full[st], (uint32_t)((it / a.nstage) & 1));
     const double* T = stage0 + st * stage_elems + el;
     const double rh = T[roff];
-    // pass 1 on this lane's physical slots (x = gamma - rho, kept in registers for pass 2):
+    // pass 1 on this lane's physical slots (x = gamma - rho, re-read from shared memory in
+    // pass 2: the registers hold the double-double row accumulators):
     //   sa = sum of the window slots, tr = sum_{s>=xoff} c_{s-xoff} x_s
-    double x[SH];
     double sa = 0.0, tr = 0.0, sa2 = 0.0, tr2 = 0.0;
 #pragma unroll
     for (int i = 0; i < SH; ++i) {
       const int q = q0 + i;
       if (q < qn) {
-        x[i] = T[q * TILE] - rh;
+        const double xi = T[q * TILE] - rh;
         if (i & 1) {
-          sa2 = fma(cA[q], x[i], sa2);
-          tr2 = fma(cX[q], x[i], tr2);
+          sa2 = fma(cA[q], xi, sa2);
+          tr2 = fma(cX[q], xi, tr2);
         } else {
-          sa = fma(cA[q], x[i], sa);
-          tr = fma(cX[q], x[i], tr);
+          sa = fma(cA[q], xi, sa);
+          tr = fma(cX[q], xi, tr);
         }
-      } else {
-        x[i] = 0.0;
       }
     }
     sa += sa2;
@@ -206,30 +209,45 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
       }
     }
     // pass 2: new Gram row on this lane's physical slots (band DOFs are added after the filter)
-    if (a.do_gram && valid && !inB) {
+    if (GRAM && valid && !inB) {
       const double gr = gval - rh;
-      if (half == 0) acc_self += gr * gr;
+      if (half == 0) dd_fma(acc_self, acc_selfl, gr, gr);
 #pragma unroll
-      for (int i = 0; i < SH; ++i) acc[i] = fma(gr, x[i], acc[i]);
+      for (int i = 0; i < SH; ++i) {
+        const int q = q0 + i;
+        if (q < qn) dd_fma(acc[i], accl[i], gr, T[q * TILE] - rh);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
-  if (!a.do_gram) return;
+  if constexpr (GRAM) {
   // fixed-order reductions: the 16 lanes of each half (shuffle tree), then warps -> part[block][s]
 #pragma unroll
   for (int i = 0; i < SH; ++i) {
-    double v = acc[i];
-    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((lane & 15) == 0) wred[warp][half * SH + i] = v;
+    double v = acc[i], vl = accl[i];
+    for (int o = 8; o > 0; o >>= 1) {
+      const double oh = __shfl_xor_sync(0xffffffffu, v, o), ol = __shfl_xor_sync(0xffffffffu, vl, o);
+      dd_add(v, vl, oh, ol);
+    }
+    if ((lane & 15) == 0) {
+      wred[warp][half * SH + i] = v;
+      wredl[warp][half * SH + i] = vl;
+    }
   }
   {
-    double v = acc_self;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) wred[warp][2 * SH] = v;
+    double v = acc_self, vl = acc_selfl;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oh = __shfl_xor_sync(0xffffffffu, v, o), ol = __shfl_xor_sync(0xffffffffu, vl, o);
+      dd_add(v, vl, oh, ol);
+    }
+    if (lane == 0) {
+      wred[warp][2 * SH] = v;
+      wredl[warp][2 * SH] = vl;
+    }
   }
   __syncthreads();
-  double* outp = a.part + (int64_t)blockIdx.x * (nU + 1);
+  double* outp = a.part + (int64_t)blockIdx.x * (nU + 1) * 2;
   for (int s = tid; s <= nU; s += 32 * NCW) {
     int idx;
     if (s == nU) {
@@ -238,39 +256,53 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
       const int q = a.W.slot[s];
       idx = (q < h0) ? q : SH + (q - h0);
     }
-    double v = 0.0;
-    for (int k = 0; k < NCW; ++k) v += wred[k][idx];
-    outp[s] = v;
+    double v = 0.0, vl = 0.0;
+    for (int k = 0; k < NCW; ++k) dd_add(v, vl, wred[k][idx], wredl[k][idx]);
+    outp[2 * s] = v;
+    outp[2 * s + 1] = vl;
+  }
   }
 }
 
 // C[new][U[s]] = sum over blocks of fill partials, fixed order
 // C row of the new slot = sum of the fill partials (+ the seam-band partials), 16 threads per
 // entry with a fixed-order tree (deterministic)
+// (double-double partials [blk][nU + 1][hi, lo]; row written to Chi / Clo)
 __global__ void __launch_bounds__(1024) gram_row_reduce(const double* __restrict__ part, int nblk,
                                                         const double* __restrict__ bpart, int nbblk, Win W,
-                                                        int new_slot, double* __restrict__ C, int ldc,
-                                                        const unsigned long long* __restrict__ esc) {
+                                                        int new_slot, double* __restrict__ C, double* __restrict__ Clo,
+                                                        int ldc, const unsigned long long* __restrict__ esc) {
   const int nU = W.nU;
   if (esc && *esc != ~0ull) bpart = nullptr;  // escalated step: the row was recomputed from gamma_k
   constexpr int TPE = 16;
   for (int base = 0; base < (nU + 1) * TPE; base += blockDim.x) {
     const int idx = base + threadIdx.x, s = idx / TPE, sub = idx % TPE;
-    double a = 0.0, bsum = 0.0;
+    double a = 0.0, al = 0.0, bsum = 0.0, bl = 0.0;
     if (s <= nU) {
-      for (int b = sub; b < nblk; b += TPE) a += part[(int64_t)b * (nU + 1) + s];
+      for (int b = sub; b < nblk; b += TPE) {
+        const double* p = part + ((int64_t)b * (nU + 1) + s) * 2;
+        dd_add(a, al, p[0], p[1]);
+      }
       if (bpart)
-        for (int b = sub; b < nbblk; b += TPE) bsum += bpart[(int64_t)b * (nU + 1) + s];
+        for (int b = sub; b < nbblk; b += TPE) {
+          const double* p = bpart + ((int64_t)b * (nU + 1) + s) * 2;
+          dd_add(bsum, bl, p[0], p[1]);
+        }
     }
     for (int o = TPE / 2; o > 0; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
+      double oh = __shfl_xor_sync(0xffffffffu, a, o), ol = __shfl_xor_sync(0xffffffffu, al, o);
+      dd_add(a, al, oh, ol);
+      oh = __shfl_xor_sync(0xffffffffu, bsum, o);
+      ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      dd_add(bsum, bl, oh, ol);
     }
     if (s <= nU && sub == 0) {
-      const double v = a + bsum;
+      dd_add(a, al, bsum, bl);
       const int cs_ = (s < nU) ? W.slot[s] : new_slot;
-      C[new_slot * ldc + cs_] = v;
-      C[cs_ * ldc + new_slot] = v;
+      C[new_slot * ldc + cs_] = a;
+      C[cs_ * ldc + new_slot] = a;
+      Clo[new_slot * ldc + cs_] = al;
+      Clo[cs_ * ldc + new_slot] = al;
     }
   }
 }
@@ -297,10 +329,10 @@ __global__ void eps_all_kernel(Geo g, const double* __restrict__ eps_elem, doubl
 
 // out (rho or psi) = mean of the last w window slots
 
-template <int NU>
+template <int NU, bool GRAM>
 hrom_status launch_fill_t(hrom_ctx* c, const FillArgs& a, size_t smem) {
-  HROM_CK(cudaFuncSetAttribute(fill_kernel<NU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  fill_kernel<NU><<<c->nsm, FILL_THREADS, smem, c->st>>>(a);
+  HROM_CK(cudaFuncSetAttribute(fill_kernel<NU, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fill_kernel<NU, GRAM><<<c->nsm, FILL_THREADS, smem, c->st>>>(a);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   c->fill_grid = c->nsm;
@@ -335,13 +367,12 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef ou
   a.eps_elem = c->b.eps_elem;
   a.part = c->b.gpart;
   const int sh = (c->nslots + 1) / 2;
-  if (sh <= 6) return launch_fill_t<6>(c, a, smem);
-  if (sh <= 12) return launch_fill_t<12>(c, a, smem);
-  if (sh <= 18) return launch_fill_t<18>(c, a, smem);
-  if (sh <= 26) return launch_fill_t<26>(c, a, smem);
-  if (sh <= 34) return launch_fill_t<34>(c, a, smem);
-  if (!a.do_gram && sh <= 50) return launch_fill_t<50>(c, a, smem);
-  if (!a.do_gram && sh <= 66) return launch_fill_t<66>(c, a, smem);
+#define FILL_CASE(SH_)                                                                            \
+  if (sh <= SH_) return a.do_gram ? launch_fill_t<SH_, true>(c, a, smem) : launch_fill_t<SH_, false>(c, a, smem);
+  FILL_CASE(6) FILL_CASE(12) FILL_CASE(18) FILL_CASE(26) FILL_CASE(34)
+#undef FILL_CASE
+  if (!a.do_gram && sh <= 50) return launch_fill_t<50, false>(c, a, smem);
+  if (!a.do_gram && sh <= 66) return launch_fill_t<66, false>(c, a, smem);
   return HROM_E_INVALID;  // wider windows use gram_mode = 1 (hrom_create enforces it)
 }
 
@@ -352,8 +383,8 @@ hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot, const unsig
 hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_band,
                             const unsigned long long* esc) {
   gram_row_reduce<<<1, 1024, 0, c->st>>>(c->b.gpart, c->fill_grid,
-                                         with_band ? c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1) : nullptr,
-                                         c->band_blocks, W, new_slot, c->b.C, kMaxSlots, esc);
+                                         with_band ? c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1) * 2 : nullptr,
+                                         c->band_blocks, W, new_slot, c->b.C, c->b.Clo, kMaxSlots, esc);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;

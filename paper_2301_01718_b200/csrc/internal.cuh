@@ -98,15 +98,21 @@ struct Bufs {
   int32_t* ftab = nullptr;    // 14 N: seam-filter stencil tables
   double* fcur = nullptr;     // Dp: compact current values (seam filter)
   double* fF = nullptr;       // Dp: compact full-step values on the band
-  double* C = nullptr;        // kMaxSlots^2
+  double* C = nullptr;        // kMaxSlots^2 window Gram by ring slot (hi part; double-double, G11)
+  double* Clo = nullptr;      // kMaxSlots^2 (lo part)
+  double* Rlo = nullptr;      // (kMaxW+2)^2: lo part of the gathered Gram R (hi: eigV)
+  double* Mdd = nullptr;      // 2 kMaxSlots^2: M = X^T X (hi, lo) for the eigenvector refinement
+  double* Zf = nullptr;       // kMaxSlots^2: all w eigenvectors of hi(M) (refined by refine_kernel)
+  double* rfws = nullptr;     // 5 kMaxSlots^2: refine_kernel workspace for wide windows
+  double* Tg = nullptr;       // 2 (kMaxW+1) kMaxR: solve_kernel's T = K A (hi, lo) for wide windows
   double* part = nullptr;     // partial sums
   int64_t part_len = 0;
   double* gpart = nullptr;    // Gram-row partials (fill + band)
   int64_t gpart_len = 0;
-  double* K = nullptr;        // (kMaxW+1)^2 gathered Gram
+  double* K = nullptr;        // 2 (kMaxW+2)^2 centred gathered Gram (hi, lo) when not in smem
   double* Khi = nullptr;      // kMaxSlots^2: incremental gathered Gram by ring slot (double-double)
   double* Klo = nullptr;
-  double* Rd = nullptr;       // 2 (kMaxW+2)^2: Gram of the rows entering / leaving S-hat
+  double* Rd = nullptr;       // 4 (kMaxW+2)^2: Gram of the rows entering / leaving S-hat (hi, lo each)
   double* vpart = nullptr;    // per-CTA partials of the S-hat GEMVs
   double* A = nullptr;        // w x r (column j: mode j)
   double* lam = nullptr;      // w eigenvalues
@@ -144,6 +150,26 @@ struct Bufs {
   double* ophi = nullptr;           // D x r materialised basis (only when odeim_points > 0)
 };
 
+}  // namespace hrom
+
+namespace hrom {
+// Host bookkeeping of a context that one step of Algorithm 1 advances (graph replay, api.cu):
+// a steady-state step changes only k and the fields that track it.
+struct HostSnap {
+  int64_t k, rebase_k, smax_k, kinc_newest, kinc_rebase, odeim_k, nlaunch, last_err_cell;
+  bool basis_ready, sets_ready, gram_row_ready, full_since_update, last_hybrid, basis_pending, eig_todo,
+      bg_pending, kinc_valid, eps_sparse;
+  int n_owed, samples_since_gather, fill_grid, odeim_n, points_used;
+  int64_t owed_rows[4];
+  double dt_override;
+  Win win, eig_win;
+};
+// one captured steady-state step per ring phase k mod nslots (its kernel arguments depend on k
+// only through the ring slots)
+struct GraphSlot {
+  cudaGraphExec_t exec = nullptr;
+  HostSnap pre{}, post{};
+};
 }  // namespace hrom
 
 struct hrom_ctx {
@@ -199,6 +225,10 @@ struct hrom_ctx {
   bool eps_sparse = false;   // the indicator is nonzero only on the T list (set by a hybrid step)
   int64_t kinc_newest = -1, kinc_rebase = -1;
   hrom::Win eig_win{};
+  // CUDA-graph replay of steady-state steps (hrom_set_graph)
+  bool graph_on = false;
+  std::vector<hrom::GraphSlot> graphs;
+  int64_t graph_launches = 0, graph_captures = 0;
   int slot_of(int64_t kk) const { return (int)(kk % nslots); }
   hrom::SRef slot_ref(int s) const { return hrom::SRef{b.ring + (int64_t)s * hrom::TILE, g.nsr}; }
   hrom::SRef rho_ref() const { return hrom::SRef{b.rho, g.nsr}; }
@@ -254,6 +284,8 @@ int sets_occupancy();
 // dev_cols: column base pointers, all with slab stride ns (1 = plain vectors); rho: SRef or p == nullptr
 hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int64_t ns, int ncol, int64_t rows, SRef rho,
                       double* dev_C, int ldc, const int32_t* map);
+hrom_status gram_full_dd(hrom_ctx* c, const double* const* dev_cols, int64_t ns, int ncol, int64_t rows, SRef rho,
+                         double* dev_Chi, double* dev_Clo, int ldc, const int32_t* map);
 hrom_status gram_gathered(hrom_ctx* c, SRef src_b);
 hrom_status band_gram_rows(hrom_ctx* c, const Win& W, SRef v);
 hrom_status small_solve(hrom_ctx* c);

@@ -13,6 +13,7 @@
 #include "internal.cuh"
 #include "eig.cuh"
 #include "async.cuh"
+#include "dd.cuh"
 
 namespace hrom {
 namespace {
@@ -36,20 +37,26 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // (DMMA m8n8k4) and release the stage through empty[s].  No CTA-wide barrier in the stream.
 // NSB 16-column super blocks (ncol <= 16 NSB), RT rows per tile (= producer threads),
 // TPW super-block pairs per consumer warp, CW consumer warps.
-template <int NSB, int RT, int TPW, int CW, int STAGES, int PW, int LOOK>
+// DD: double-double consumers (dd.cuh, G11) instead of DMMA: each consumer thread owns TPW
+// 2 x 2 column blocks of the upper triangle and accumulates TwoProduct/TwoSum; odd tile stride
+// (conflict-free column gathers of one row).
+template <int NSB, int RT, int TPW, int CW, int STAGES, int PW, int LOOK, bool DD = false>
 struct GGCfg {
   static constexpr int nsb = NSB, rt = RT, tpw = TPW, cw = CW, stages = STAGES, look = LOOK;
-  static constexpr int pw = PW, ncp = 16 * NSB, ldt = RT + 4, threads = 32 * (PW + CW);
+  static constexpr bool dd = DD;
+  static constexpr int pw = PW, ncp = 16 * NSB, ldt = DD ? RT + 1 : RT + 4, threads = 32 * (PW + CW);
   static constexpr int parts = 32 * PW / RT;  // producer threads per tile row (columns split)
   // per stage: the tile, then each producer part's copy of the shift of its rows (cp.async'd
   // with the tile, so no pending global load is carried across iterations in registers)
   static constexpr size_t smem = (size_t)STAGES * (ncp * ldt + parts * RT) * sizeof(double);
-  static_assert(CW * TPW >= NSB * (NSB + 1) / 2, "tasks");
+  static_assert(DD ? 32 * CW * TPW >= (8 * NSB) * (8 * NSB + 1) / 2 : CW * TPW >= NSB * (NSB + 1) / 2, "tasks");
   static_assert((32 * PW) % RT == 0 && STAGES >= LOOK + 2, "producer layout");
 };
 // producers run LOOK tiles ahead of the tile they publish (DRAM latency of the 8-byte gathers)
 using GGSmall = GGCfg<5, 64, 1, 15, 4, 6, 2>;  // ncol <= 80 (w <= 78)
 using GGWide = GGCfg<9, 32, 3, 15, 4, 2, 2>;   // ncol <= 144 (w <= kMaxW)
+using GGDSmall = GGCfg<5, 64, 2, 15, 4, 6, 2, true>;  // double-double, ncol <= 80
+using GGDWide = GGCfg<9, 32, 6, 15, 4, 2, 2, true>;   // double-double, ncol <= 144
 
 struct GGArgs {
   int mode;                  // 0: contiguous rows of ncol columns (cols, slab stride ns), 1: S-hat rows
@@ -147,6 +154,62 @@ __global__ void __launch_bounds__(CFG::threads, 1) gather_gram_kernel(GGArgs a) 
       }
     }
     cp_async_wait<0>();
+  } else if constexpr (CFG::dd) {
+    // ---- double-double consumers: thread t owns the 2 x 2 column blocks t, t + T, ... of the
+    // upper triangle (bi <= bj over nb = ceil(ncol / 2) block indices) ----
+    constexpr int BPT = CFG::tpw, T = 32 * CFG::cw;
+    const int t = threadIdx.x - 32 * CFG::pw;
+    const int nb = (ncol + 1) / 2, nblk = nb * (nb + 1) / 2;
+    int ci[BPT], cj[BPT];
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+      const int task = t + q * T;
+      int x = 0, rem = task < nblk ? task : 0;
+      while (rem >= nb - x) {
+        rem -= nb - x;
+        ++x;
+      }
+      ci[q] = task < nblk ? 2 * x : -1;
+      cj[q] = 2 * (x + rem);
+    }
+    double hi[BPT][4], lo[BPT][4];
+#pragma unroll
+    for (int q = 0; q < BPT; ++q)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) hi[q][u] = lo[q][u] = 0.0;
+    for (int64_t it = 0; it < my_tiles; ++it) {
+      const int st = (int)(it % ST);
+      mbar_wait(&full[st], (uint32_t)((it / ST) & 1));
+      const double* tile = smem + (size_t)st * NCP * LDT;
+#pragma unroll
+      for (int q = 0; q < BPT; ++q) {
+        if (ci[q] < 0) continue;
+        const double* xa = tile + ci[q] * LDT;
+        const double* xb = tile + cj[q] * LDT;
+        for (int kk = 0; kk < RT; ++kk) {
+          const double a0 = xa[kk], a1 = xa[LDT + kk], b0 = xb[kk], b1 = xb[LDT + kk];
+          dd_fma(hi[q][0], lo[q][0], a0, b0);
+          dd_fma(hi[q][1], lo[q][1], a0, b1);
+          dd_fma(hi[q][2], lo[q][2], a1, b0);
+          dd_fma(hi[q][3], lo[q][3], a1, b1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    double* out = a.part + (int64_t)blockIdx.x * NCP * NCP * 2;
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+      if (ci[q] < 0) continue;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = ci[q] + (u >> 1), j = cj[q] + (u & 1);
+        if (i > j) continue;  // diagonal block: the lower entry duplicates the upper one
+        dd_norm(hi[q][u], lo[q][u]);
+        out[2 * (i * NCP + j)] = hi[q][u];
+        out[2 * (i * NCP + j) + 1] = lo[q][u];
+      }
+    }
   } else {
     // ---- consumers: TPW upper super-block pairs (sa <= sb) per warp ----
     const int cwarp = warp - CFG::pw;
@@ -676,11 +739,11 @@ constexpr int GV_T = 256, GV_W = GV_T / 32, GV_U = 2;
 // NEWCOL = false, BANDOUT = true: the seam-band part of the new window Gram row (H10): one
 // product vector b = gamma_k on the band rows, partials [blk][nU + 1] ([nU] = sum b^2).
 template <int SPW, bool NEWCOL = true, bool BANDOUT = false>
-__global__ void __launch_bounds__(GV_T) gemv_gather_kernel(Geo g, Win W, const double* __restrict__ ring,
+__global__ void __launch_bounds__(GV_T, 2) gemv_gather_kernel(Geo g, Win W, const double* __restrict__ ring,
                                                            const SRef rho, const int32_t* __restrict__ list,
                                                            const int32_t* __restrict__ count, const SRef src_b,
                                                            double* __restrict__ vpart) {
-  __shared__ double red[GV_W][2 * SPW + 1];
+  __shared__ double red[GV_W][2 * SPW + 1], redl[GV_W][2 * SPW + 1];
   const int nU = W.nU, nS = *count;
   const int64_t total = (int64_t)nS * g.c;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -692,10 +755,12 @@ __global__ void __launch_bounds__(GV_T) gemv_gather_kernel(Geo g, Win W, const d
     const int sl = warp + GV_W * j;
     col[j] = sl < nU ? ring + (int64_t)W.slot[sl] * TILE : nullptr;
   }
-  double an[SPW], ab[SPW];
+  // double-double accumulators (G11): these GEMVs are rows / columns of the POD's and the
+  // gappy normal equations' Grams
+  double an[SPW], ab[SPW], anl[SPW], abl[SPW];
 #pragma unroll
-  for (int j = 0; j < SPW; ++j) an[j] = ab[j] = 0.0;
-  double bb = 0.0;
+  for (int j = 0; j < SPW; ++j) an[j] = ab[j] = anl[j] = abl[j] = 0.0;
+  double bb = 0.0, bbl = 0.0;
   const int64_t gstep = (int64_t)gridDim.x * 32 * GV_U;
   // the S-hat list entries of the next chunk are fetched one iteration ahead (the value loads
   // depend on them: without the prefetch every chunk pays two dependent memory latencies)
@@ -746,79 +811,95 @@ __global__ void __launch_bounds__(GV_T) gemv_gather_kernel(Geo g, Win W, const d
 #pragma unroll
       for (int j = 0; j < SPW; ++j) {
         const double v = val[u][j] - r[u];
-        if (NEWCOL) an[j] += v * x;
-        ab[j] += v * y;
+        if (NEWCOL) dd_fma(an[j], anl[j], v, x);
+        dd_fma(ab[j], abl[j], v, y);
       }
-      if (warp == 0) bb += y * y;
+      if (warp == 0) dd_fma(bb, bbl, y, y);
     }
   }
+  auto wsum = [&](double& h, double& l) {
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oh = __shfl_xor_sync(0xffffffffu, h, o), ol = __shfl_xor_sync(0xffffffffu, l, o);
+      dd_add(h, l, oh, ol);
+    }
+  };
 #pragma unroll
   for (int j = 0; j < SPW; ++j) {
-    double x = an[j], y = ab[j];
-    for (int o = 16; o > 0; o >>= 1) {
-      x += __shfl_xor_sync(0xffffffffu, x, o);
-      y += __shfl_xor_sync(0xffffffffu, y, o);
-    }
+    if (NEWCOL) wsum(an[j], anl[j]);
+    wsum(ab[j], abl[j]);
     if (lane == 0) {
-      red[warp][j] = x;
-      red[warp][SPW + j] = y;
+      red[warp][j] = an[j];
+      redl[warp][j] = anl[j];
+      red[warp][SPW + j] = ab[j];
+      redl[warp][SPW + j] = abl[j];
     }
   }
-  for (int o = 16; o > 0; o >>= 1) bb += __shfl_xor_sync(0xffffffffu, bb, o);
-  if (lane == 0) red[warp][2 * SPW] = bb;
+  wsum(bb, bbl);
+  if (lane == 0) {
+    red[warp][2 * SPW] = bb;
+    redl[warp][2 * SPW] = bbl;
+  }
   __syncthreads();
+  // partials [blk][n][hi, lo]
   if (BANDOUT) {
-    double* out = vpart + (int64_t)blockIdx.x * (nU + 1);
-    for (int k = threadIdx.x; k <= nU; k += GV_T) out[k] = k == nU ? red[0][2 * SPW] : red[k % GV_W][SPW + k / GV_W];
+    double* out = vpart + (int64_t)blockIdx.x * (nU + 1) * 2;
+    for (int k = threadIdx.x; k <= nU; k += GV_T) {
+      const int wi = k == nU ? 0 : k % GV_W, ji = k == nU ? 2 * SPW : SPW + k / GV_W;
+      out[2 * k] = red[wi][ji];
+      out[2 * k + 1] = redl[wi][ji];
+    }
     return;
   }
-  double* out = vpart + (int64_t)blockIdx.x * (2 * nU + 1);
+  double* out = vpart + (int64_t)blockIdx.x * (2 * nU + 1) * 2;
   for (int k = threadIdx.x; k <= 2 * nU; k += GV_T) {
-    double v;
+    int wi, ji;
     if (k == 2 * nU) {
-      v = red[0][2 * SPW];
+      wi = 0;
+      ji = 2 * SPW;
     } else {
       const int sl = k < nU ? k : k - nU;  // slot sl is (warp sl % GV_W, j = sl / GV_W)
-      v = red[sl % GV_W][(k < nU ? 0 : SPW) + sl / GV_W];
+      wi = sl % GV_W;
+      ji = (k < nU ? 0 : SPW) + sl / GV_W;
     }
-    out[k] = v;
+    out[2 * k] = red[wi][ji];
+    out[2 * k + 1] = redl[wi][ji];
   }
 }
 
-// fixed-order reduce of the GEMV partials, 16 threads per entry
+// fixed-order reduce of the GEMV partials [blk][n][hi, lo], 16 threads per entry -> v[n][hi, lo]
 __global__ void __launch_bounds__(256) vpart_reduce(const double* __restrict__ vpart, int nblk, int n,
                                                     double* __restrict__ v) {
   const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int k = (int)(gt / GR_TPE), sub = (int)(gt % GR_TPE);
-  double s = 0.0;
+  double h = 0.0, l = 0.0;
   if (k < n)
-    for (int b = sub; b < nblk; b += GR_TPE) s += vpart[(int64_t)b * n + k];
-  for (int o = GR_TPE / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (k < n && sub == 0) v[k] = s;
+    for (int b = sub; b < nblk; b += GR_TPE) dd_add(h, l, vpart[((int64_t)b * n + k) * 2], vpart[((int64_t)b * n + k) * 2 + 1]);
+  for (int o = GR_TPE / 2; o > 0; o >>= 1) {
+    const double oh = __shfl_xor_sync(0xffffffffu, h, o), ol = __shfl_xor_sync(0xffffffffu, l, o);
+    dd_add(h, l, oh, ol);
+  }
+  if (k < n && sub == 0) {
+    v[2 * k] = h;
+    v[2 * k + 1] = l;
+  }
 }
 
-__device__ __forceinline__ void dd_add(double& hi, double& lo, double x) {  // (hi, lo) += x
-  const double s = hi + x;
-  const double bp = s - hi;
-  const double e = (hi - (s - bp)) + (x - bp);  // TwoSum error
-  lo += e;
-  hi = s + lo;
-  lo = lo - (hi - s);
-}
-
-// Ks (by ring slot) <- update; Rout ((nU+1)^2, union order) <- the gathered Gram for the solve.
-// init: Rout holds a full gathered Gram -> Ks = Rout.  Otherwise: old-old block += R+ - R-,
-// newest-slot row/column and the b row/column from the reduced GEMV partials.
+// Ks (by ring slot) <- update; Rout ((nU+1)^2, union order, hi / lo) <- the gathered Gram for
+// the solve.  init: Rout holds a full gathered Gram -> Ks = Rout.  Otherwise: old-old block
+// += R+ - R- (all double-double), newest-slot row/column and the b row/column from the reduced
+// GEMV partials v[n][hi, lo].
 __global__ void __launch_bounds__(512) kinc_update_kernel(Win W, int init, const double* __restrict__ Rp,
-                                                          const double* __restrict__ Rm, const double* __restrict__ v,
-                                                          double* __restrict__ Khi, double* __restrict__ Klo,
-                                                          double* __restrict__ Rout) {
+                                                          const double* __restrict__ Rpl,
+                                                          const double* __restrict__ Rm, const double* __restrict__ Rml,
+                                                          const double* __restrict__ v, double* __restrict__ Khi,
+                                                          double* __restrict__ Klo, double* __restrict__ Rout,
+                                                          double* __restrict__ Routl) {
   const int nU = W.nU, ldr = nU + 1;
   if (init) {
     for (int idx = threadIdx.x; idx < nU * nU; idx += blockDim.x) {
       const int i = idx / nU, j = idx % nU;
       Khi[W.slot[i] * kMaxSlots + W.slot[j]] = Rout[i * ldr + j];
-      Klo[W.slot[i] * kMaxSlots + W.slot[j]] = 0.0;
+      Klo[W.slot[i] * kMaxSlots + W.slot[j]] = Routl[i * ldr + j];
     }
     return;
   }
@@ -827,23 +908,28 @@ __global__ void __launch_bounds__(512) kinc_update_kernel(Win W, int init, const
     const int si = W.slot[i], sj = W.slot[j];
     double hi, lo;
     if (i == nU - 1 || j == nU - 1) {
-      hi = v[i == nU - 1 ? j : i];
-      lo = 0.0;
+      const int k = i == nU - 1 ? j : i;
+      hi = v[2 * k];
+      lo = v[2 * k + 1];
     } else {
       hi = Khi[si * kMaxSlots + sj];
       lo = Klo[si * kMaxSlots + sj];
-      dd_add(hi, lo, Rp[i * ldr + j]);
-      dd_add(hi, lo, -Rm[i * ldr + j]);
+      dd_add(hi, lo, Rp[i * ldr + j], Rpl[i * ldr + j]);
+      dd_add(hi, lo, -Rm[i * ldr + j], -Rml[i * ldr + j]);
     }
     Khi[si * kMaxSlots + sj] = hi;
     Klo[si * kMaxSlots + sj] = lo;
-    Rout[i * ldr + j] = hi + lo;
+    Rout[i * ldr + j] = hi;
+    Routl[i * ldr + j] = lo;
   }
   for (int i = threadIdx.x; i < nU; i += blockDim.x) {
-    Rout[i * ldr + nU] = v[nU + i];
-    Rout[nU * ldr + i] = v[nU + i];
+    Rout[i * ldr + nU] = Rout[nU * ldr + i] = v[2 * (nU + i)];
+    Routl[i * ldr + nU] = Routl[nU * ldr + i] = v[2 * (nU + i) + 1];
   }
-  if (threadIdx.x == 0) Rout[nU * ldr + nU] = v[2 * nU];
+  if (threadIdx.x == 0) {
+    Rout[nU * ldr + nU] = v[4 * nU];
+    Routl[nU * ldr + nU] = v[4 * nU + 1];
+  }
 }
 
 // deterministic fixed-order reduction over CTAs, 16 threads per entry (block-strided sub-sums,
@@ -865,6 +951,33 @@ __global__ void __launch_bounds__(256) gram_reduce(const double* __restrict__ pa
   }
 }
 
+// double-double version of gram_reduce: partials [blk][ncp][ncp][hi, lo] -> (Chi, Clo)
+__global__ void __launch_bounds__(256) gram_reduce_dd(const double* __restrict__ part, int nblk, int ncp, int ncol,
+                                                      double* __restrict__ Chi, double* __restrict__ Clo, int ldc,
+                                                      const int32_t* __restrict__ map) {
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int idx = (int)(gt / GR_TPE), sub = (int)(gt % GR_TPE);
+  const int i = idx / ncol, j = idx % ncol;
+  const bool act = idx < ncol * ncol && i <= j;
+  double h = 0.0, l = 0.0;
+  if (act)
+    for (int b = sub; b < nblk; b += GR_TPE) {
+      const double* p = part + ((int64_t)b * ncp * ncp + i * ncp + j) * 2;
+      dd_add(h, l, p[0], p[1]);
+    }
+  for (int o = GR_TPE / 2; o > 0; o >>= 1) {
+    const double oh = __shfl_xor_sync(0xffffffffu, h, o), ol = __shfl_xor_sync(0xffffffffu, l, o);
+    dd_add(h, l, oh, ol);
+  }
+  if (act && sub == 0) {
+    const int ci = map ? map[i] : i, cj = map ? map[j] : j;
+    Chi[ci * ldc + cj] = h;
+    Chi[cj * ldc + ci] = h;
+    Clo[ci * ldc + cj] = l;
+    Clo[cj * ldc + ci] = l;
+  }
+}
+
 // smem layout of the eigen-solve workspace (eig.cuh), shared by the basis and solve kernels
 struct EigLayout {
   int ldn, ldz;
@@ -878,10 +991,17 @@ __host__ __device__ inline EigLayout eig_layout(int n, int nvec_cap) {
   L.ldz = nvec_cap | 1;
   const size_t base = (size_t)L.ldn * L.ldn + (size_t)n * L.ldz + 8 * kMaxSlots + 64;
   const size_t fac = (size_t)4 * n * L.ldz + ((size_t)n * L.ldz + 7) / 8;
-  L.fac_smem = (base + fac) * 8 <= 200 * 1024;
+  L.fac_smem = (base + fac) * 8 <= 216 * 1024;
   L.doubles = base + (L.fac_smem ? fac : 0);
   L.bytes = L.doubles * sizeof(double);
   return L;
+}
+// dynamic doubles of the eigen-solve workspace with the LU factors in (fac_smem) or out of smem
+__host__ __device__ inline size_t eig_doubles(int n, int nvec_cap, bool fac_smem) {
+  const EigLayout L = eig_layout(n, nvec_cap);
+  const size_t base = (size_t)L.ldn * L.ldn + (size_t)n * L.ldz + 8 * kMaxSlots + 64;
+  const size_t fac = (size_t)4 * n * L.ldz + ((size_t)n * L.ldz + 7) / 8;
+  return base + (fac_smem ? fac : 0);
 }
 __device__ inline EigWork eig_work(double* sm, int n, const EigLayout& L, double* gfac) {
   EigWork W;
@@ -902,53 +1022,205 @@ __device__ inline EigWork eig_work(double* sm, int n, const EigLayout& L, double
   return W;
 }
 
-// basis from the shifted Gram (one CTA): M = X^T X by lagged centring, eigen, A = V_r L_r^-1/2
-__global__ void __launch_bounds__(512) basis_kernel(const double* __restrict__ C, int ldc, Win W, int r, double cut,
-                                                    double* __restrict__ Aout, double* __restrict__ lam_out,
+// basis from the shifted Gram (one CTA): M = X^T X by lagged centring in double-double (G11),
+// all w eigenvectors of hi(M) (eig.cuh) -> Zf, lam; M (hi, lo) -> Mh, Ml for refine_kernel
+__global__ void __launch_bounds__(512) basis_kernel(const double* __restrict__ C, const double* __restrict__ Clo,
+                                                    int ldc, Win W, double* __restrict__ Mh, double* __restrict__ Ml,
+                                                    double* __restrict__ Zf, double* __restrict__ lam_out,
                                                     int32_t* __restrict__ reff_out, double* __restrict__ gfac) {
   extern __shared__ double sm[];
   const int w = W.w, nU = W.nU;
-  const EigLayout L = eig_layout(w, r);
+  const EigLayout L = eig_layout(w, w);
   const int ldn = L.ldn;
   double* M = sm;
   const EigWork E = eig_work(sm, w, L, gfac);
-  double* mrow = E.lam + kMaxSlots;  // kMaxSlots
-  double* msum = mrow + kMaxSlots;   // kMaxSlots
+  double* mrow = E.lam + kMaxSlots;  // kMaxSlots: m_i (hi)
+  double* mrowl = mrow + kMaxSlots;  // kMaxSlots: m_i (lo)
+  __shared__ double msum[2 * kMaxSlots];
+  __shared__ double s_mu[2];
   const int tid = threadIdx.x;
-  // m_i = (1/w) sum_{p<w} C[x_i][u_p];  mu = (1/w^2) sum_{p,q<w} C[u_p][u_q]
+  // m_i = (1/w) sum_{p<w} C[x_i][u_p];  mu = (1/w^2) sum_{p,q<w} C[u_p][u_q]  (double-double)
   for (int i = tid; i < w; i += blockDim.x) {
     const int xi = W.slot[nU - w + i];
-    double s = 0.0;
-    for (int p = 0; p < w; ++p) s += C[xi * ldc + W.slot[p]];
-    mrow[i] = s / (double)w;
+    double h = 0.0, l = 0.0;
+    for (int p = 0; p < w; ++p) dd_add(h, l, C[xi * ldc + W.slot[p]], Clo[xi * ldc + W.slot[p]]);
+    dd_div1(h, l, (double)w);
+    mrow[i] = h;
+    mrowl[i] = l;
   }
   for (int p = tid; p < w; p += blockDim.x) {
-    double s = 0.0;
-    for (int q = 0; q < w; ++q) s += C[W.slot[p] * ldc + W.slot[q]];
-    msum[p] = s;
+    double h = 0.0, l = 0.0;
+    for (int q = 0; q < w; ++q) dd_add(h, l, C[W.slot[p] * ldc + W.slot[q]], Clo[W.slot[p] * ldc + W.slot[q]]);
+    msum[2 * p] = h;
+    msum[2 * p + 1] = l;
   }
   __syncthreads();
-  double mu = 0.0;
-  for (int p = 0; p < w; ++p) mu += msum[p];
-  mu /= (double)w * (double)w;
+  if (tid == 0) {
+    double h = 0.0, l = 0.0;
+    for (int p = 0; p < w; ++p) dd_add(h, l, msum[2 * p], msum[2 * p + 1]);
+    dd_div1(h, l, (double)w * (double)w);
+    s_mu[0] = h;
+    s_mu[1] = l;
+  }
+  __syncthreads();
   for (int idx = tid; idx < w * w; idx += blockDim.x) {
     const int i = idx / w, j = idx % w;
     const int xi = W.slot[nU - w + i], xj = W.slot[nU - w + j];
     // when psi_prev == psi_cur (bootstrap, nU == w) this is the plain centred Gram
-    double mi = mrow[i], mj = mrow[j];
-    M[i * ldn + j] = ((C[xi * ldc + xj] - mi) - mj) + mu;
+    double h = C[xi * ldc + xj], l = Clo[xi * ldc + xj];
+    dd_add(h, l, -mrow[i], -mrowl[i]);
+    dd_add(h, l, -mrow[j], -mrowl[j]);
+    dd_add(h, l, s_mu[0], s_mu[1]);
+    M[i * ldn + j] = h;
+    Mh[i * w + j] = h;
+    Ml[i * w + j] = l;
   }
   __syncthreads();
-  const int re = sym_eig(M, w, ldn, E, r, cut, reff_out + 10);
-  if (tid == 0) {
-    *reff_out = re;
-    reff_out[8] = 0;
-  }
-  for (int idx = tid; idx < w * r; idx += blockDim.x) {
-    const int i = idx % w, j = idx / w;  // A column-major: A[j*w + i]
-    Aout[j * w + i] = (j < re) ? E.Z[i * E.ldz + j] / sqrt(E.lam[j]) : 0.0;
+  // every eigenvector (the refinement couples the kept modes with all the others)
+  const int nv = sym_eig(M, w, ldn, E, w, -1.0, reff_out + 10);
+  if (tid == 0) reff_out[8] = 0;
+  for (int idx = tid; idx < w * w; idx += blockDim.x) {
+    const int i = idx / w, j = idx % w;
+    Zf[idx] = j < nv ? E.Z[i * E.ldz + j] : 0.0;
   }
   for (int i = tid; i < w; i += blockDim.x) lam_out[i] = E.lam[i];
+}
+
+// One step of the Ogita-Aishima eigenvector refinement (G11) of the eigen-decomposition of
+// hi(M), driven by the double-double M: R = I - Z^T Z, S = Z^T M Z (double-double),
+// lam~_i = S_ii / (1 - R_ii), E_ij = (S_ij + lam~_j R_ij) / (lam~_j - lam~_i) for
+// |lam~_i - lam~_j| > delta = 2 (||S - diag lam~||_F + ||M||_F ||R||_F), else R_ij / 2;
+// Z' = Z + Z E.  The subspace error eps lambda_1 / gap of the fp64 solve becomes its square,
+// i.e. the eigenvectors are those of the exact Gram to fp64 precision (SVD class, A15).
+// Then r_eff = #{j < r : lam~_j >= cut lam~_0} (consecutive), sign (largest |Z_ij| positive),
+// A = V_r L_r^-1/2 (column-major A[j*w + i]), lam_out = lam~.
+constexpr int RF_T = 512;
+__device__ __forceinline__ double rf_block_sum(double v, double* red) {  // all threads get the sum
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int q = 0; q < RF_T / 32; ++q) t += red[q];  // fixed order
+  return t;
+}
+// Workspace: 5 w (w | 1) doubles in shared memory, or in the global scratch gws (wide windows,
+// w > 72: L2-resident)
+__global__ void __launch_bounds__(RF_T) refine_kernel(const double* __restrict__ Mh, const double* __restrict__ Ml,
+                                                      const double* __restrict__ Zg, int w, int r, double cut,
+                                                      double* __restrict__ lam_io, double* __restrict__ Aout,
+                                                      int32_t* __restrict__ reff_out, double* gws) {
+  extern __shared__ double sm[];
+  const int ld = w | 1;
+  const size_t B = (size_t)w * ld;
+  double* Z = gws ? gws : sm;  // Z[a * ld + j]
+  double* Yh = Z + B;        // Y = M Z (hi), then E
+  double* Yl = Yh + B;       // Y (lo), then Z' = Z + Z E
+  double* M0 = Yl + B;       // M (hi), then S (rounded)
+  double* M1 = M0 + B;       // M (lo), then R (rounded)
+  __shared__ double lt[kMaxSlots], red[RF_T / 32];
+  __shared__ int s_reff;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < w * w; idx += RF_T) {
+    const int a = idx / w, j = idx % w;
+    Z[a * ld + j] = Zg[idx];
+    M0[a * ld + j] = Mh[idx];
+    M1[a * ld + j] = Ml[idx];
+  }
+  __syncthreads();
+  // Y = M Z (double-double); ||M||_F
+  double fm = 0.0;
+  for (int idx = tid; idx < w * w; idx += RF_T) {
+    const int a = idx / w, j = idx % w;
+    double h = 0.0, l = 0.0;
+    for (int b = 0; b < w; ++b) {
+      const double z = Z[b * ld + j];
+      dd_fma(h, l, M0[a * ld + b], z);
+      l = fma(M1[a * ld + b], z, l);
+    }
+    dd_norm(h, l);
+    Yh[a * ld + j] = h;
+    Yl[a * ld + j] = l;
+    fm += M0[a * ld + j] * M0[a * ld + j];
+  }
+  const double normM = sqrt(rf_block_sum(fm, red));  // (its barriers also retire M)
+  // S = Z^T Y and R = I - Z^T Z (double-double, rounded to fp64) over M's storage
+  for (int idx = tid; idx < w * w; idx += RF_T) {
+    const int i = idx / w, j = idx % w;
+    double sh = 0.0, sl = 0.0, rh = i == j ? 1.0 : 0.0, rl = 0.0;
+    for (int a = 0; a < w; ++a) {
+      const double zi = Z[a * ld + i];
+      dd_fma(sh, sl, zi, Yh[a * ld + j]);
+      sl = fma(zi, Yl[a * ld + j], sl);
+      dd_fma(rh, rl, -zi, Z[a * ld + j]);
+    }
+    M0[i * ld + j] = sh + sl;
+    M1[i * ld + j] = rh + rl;
+  }
+  __syncthreads();
+  for (int i = tid; i < w; i += RF_T) lt[i] = M0[i * ld + i] / (1.0 - M1[i * ld + i]);
+  __syncthreads();
+  double fs = 0.0, fr = 0.0;
+  for (int idx = tid; idx < w * w; idx += RF_T) {
+    const int i = idx / w, j = idx % w;
+    const double sv = i == j ? M0[i * ld + i] - lt[i] : M0[i * ld + j];
+    fs += sv * sv;
+    fr += M1[i * ld + j] * M1[i * ld + j];
+  }
+  const double nS = sqrt(rf_block_sum(fs, red));
+  const double nR = sqrt(rf_block_sum(fr, red));
+  const double delta = 2.0 * (nS + normM * nR);
+  // E (over Y hi)
+  for (int idx = tid; idx < w * w; idx += RF_T) {
+    const int i = idx / w, j = idx % w;
+    double e;
+    if (i == j) e = 0.5 * M1[i * ld + i];
+    else if (fabs(lt[i] - lt[j]) > delta) e = (M0[i * ld + j] + lt[j] * M1[i * ld + j]) / (lt[j] - lt[i]);
+    else e = 0.5 * M1[i * ld + j];
+    Yh[i * ld + j] = e;
+  }
+  __syncthreads();
+  // Z' = Z + Z E (over Y lo)
+  for (int idx = tid; idx < w * w; idx += RF_T) {
+    const int a = idx / w, j = idx % w;
+    double s = 0.0;
+    for (int i = 0; i < w; ++i) s = fma(Z[a * ld + i], Yh[i * ld + j], s);
+    Yl[a * ld + j] = Z[a * ld + j] + s;
+  }
+  __syncthreads();
+  // sign: the largest |Z'_ij| of each vector (ties: lowest i) positive (A15)
+  for (int j = tid; j < w; j += RF_T) {
+    int im = 0;
+    double vm = -1.0;
+    for (int i = 0; i < w; ++i) {
+      const double a = fabs(Yl[i * ld + j]);
+      if (a > vm) {
+        vm = a;
+        im = i;
+      }
+    }
+    if (Yl[im * ld + j] < 0.0)
+      for (int i = 0; i < w; ++i) Yl[i * ld + j] = -Yl[i * ld + j];
+  }
+  if (tid == 0) {
+    int re = 0;
+    const double l0 = lt[0];
+    if (l0 > 0.0)
+      for (int j = 0; j < min(r, w); ++j) {
+        if (lt[j] >= cut * l0) ++re;
+        else break;
+      }
+    s_reff = re;
+    *reff_out = re;
+  }
+  __syncthreads();
+  const int re = s_reff;
+  for (int idx = tid; idx < w * r; idx += RF_T) {
+    const int i = idx % w, j = idx / w;  // A column-major: A[j*w + i]
+    Aout[j * w + i] = (j < re) ? Yl[i * ld + j] / sqrt(lt[j]) : 0.0;
+  }
+  for (int i = tid; i < w; i += RF_T) lam_io[i] = lt[i];
 }
 
 // H5 (one CTA): K = lagged centring of the gathered R (A14), G = A^T K_XX A, g = A^T K_Xb,
@@ -967,27 +1239,32 @@ __device__ __forceinline__ void sstamp(long long* t, int& i) {
 }
 
 constexpr int SV_T = 256, SV_W = SV_T / 32;
+// Workspace of solve_kernel (offsets in doubles of the dynamic shared memory; a buffer whose
+// flag is set lives in the global scratch instead -- wide windows).  Region X holds K (hi, lo)
+// and T (hi, lo) until G is formed, then the eigen-solve workspace of the pinv route.
 struct SolveLayout {
-  size_t ks, rs, as, t, mp, mc, lm, vec, eig, total;  // offsets in doubles
-  int mode;  // 2: R staged + K in smem, 1: K in smem (R read from global), 0: K in the global scratch
+  size_t as, x, kh, kl, th, tl, gh, gl, lm, mp, vec, eig, total;
+  bool kg, tg;  // K / T in global memory
 };
-// As and T are stored with the odd leading dimension w + 1, the Cholesky factor with r + 1
-// (conflict-free walks along either index)
-__host__ __device__ inline SolveLayout solve_layout(int w, int r, int mode) {
+__host__ __device__ inline SolveLayout solve_layout(int w, int r, bool kg, bool tg, size_t eig_doubles) {
   SolveLayout S;
-  S.mode = mode;
-  S.ks = 0;
-  S.rs = S.ks + (mode >= 1 ? (size_t)(w + 1) * (w + 1) : 0);
-  S.as = S.rs + (mode == 2 ? (size_t)(w + 2) * (w + 2) : 0);
-  S.t = S.as + (size_t)(w + 1) * r;
-  // T (w x r) is dead once G is formed: the Cholesky factor reuses it
-  const size_t treg = (size_t)(w + 1) * r > (size_t)r * (r + 1) ? (size_t)(w + 1) * r : (size_t)r * (r + 1);
-  S.lm = S.t;
-  S.mp = S.t + treg;
-  S.mc = S.mp + (kMaxW + 2);
-  S.vec = S.mc + (kMaxW + 2);           // rhs, y, u, misc: 4 * kMaxSlots
-  S.eig = S.vec + 4 * kMaxSlots + 2 * SV_W;
-  S.total = S.eig;                       // + EigLayout(r).doubles
+  S.kg = kg;
+  S.tg = tg;
+  const size_t ka = (size_t)(w + 1) * (w + 1), ta = (size_t)(w + 1) * r;
+  S.as = 0;
+  S.x = S.as + ta;
+  S.kh = S.x;
+  S.kl = S.kh + (kg ? 0 : ka);
+  S.th = S.kl + (kg ? 0 : ka);
+  S.tl = S.th + (tg ? 0 : ta);
+  const size_t xend = S.tl + (tg ? 0 : ta);
+  S.eig = S.x;
+  S.gh = (xend > S.eig + eig_doubles ? xend : S.eig + eig_doubles);
+  S.gl = S.gh + (size_t)r * (r | 1);
+  S.lm = S.gl + (size_t)r * (r | 1);
+  S.mp = S.lm + (size_t)r * (r | 1);  // mp, mpl, mc, mcl: 4 (kMaxW + 2)
+  S.vec = S.mp + 4 * (kMaxW + 2);     // g hi, g lo, y, u, misc, res: 6 kMaxSlots + 2 SV_W
+  S.total = S.vec + 6 * kMaxSlots + 2 * SV_W;
   return S;
 }
 
@@ -1134,121 +1411,207 @@ __device__ void trsolve_t_warp(const double* Lm, int ld, int n, const double* di
   if (lane + 32 < n) y[lane + 32] = v1;
 }
 
-__global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ R, Win W, int r,
-                                                     const double* __restrict__ A, const int32_t* __restrict__ reffp,
-                                                     double cut, double* __restrict__ y_out,
-                                                     double* __restrict__ c_out, int32_t* __restrict__ status,
-                                                     double* __restrict__ gfac, bool fac_smem,
-                                                     double* __restrict__ Kg, int mode, long long* tdbg) {
+// One warp: forward substitution L x = b (lanes own rows lane, lane + 32)
+__device__ void trsolve_warp(const double* Lm, int ld, int n, const double* dinv, const double* b, double* x) {
+  const int lane = threadIdx.x & 31;
+  double v0 = lane < n ? b[lane] : 0.0, v1 = lane + 32 < n ? b[lane + 32] : 0.0;
+  for (int k = 0; k < n; ++k) {
+    const double xk = __shfl_sync(0xffffffffu, k < 32 ? v0 : v1, k & 31) * dinv[k];
+    if (lane == (k & 31)) {
+      if (k < 32) v0 = xk;
+      else v1 = xk;
+    }
+    if (lane > k && lane < n) v0 -= Lm[lane * ld + k] * xk;
+    if (lane + 32 > k && lane + 32 < n) v1 -= Lm[(lane + 32) * ld + k] * xk;
+  }
+  if (lane < n) x[lane] = v0;
+  if (lane + 32 < n) x[lane + 32] = v1;
+}
+
+// out(m, n) = sum_p X(m, p) Y(n, p), X and Y double-double (lo parts nullable), layouts
+// X[m ldx + p], Y[n ldy + p]; CN outputs per thread share the X loads; UPPER: only n >= m
+template <int CN, bool UPPER, class F>
+__device__ __forceinline__ void smem_gemm_dd(const double* Xh, const double* Xl, int ldx, const double* Yh,
+                                             const double* Yl, int ldy, int M, int N, int P, F store) {
+  const int nb = (N + CN - 1) / CN;
+  for (int blk = threadIdx.x; blk < M * nb; blk += blockDim.x) {
+    const int m = blk % M, n0 = CN * (blk / M);
+    if (UPPER && n0 + CN - 1 < m) continue;
+    double h[CN], l[CN];
+#pragma unroll
+    for (int c = 0; c < CN; ++c) h[c] = l[c] = 0.0;
+    const double* xh = Xh + (int64_t)m * ldx;
+    const double* xl = Xl ? Xl + (int64_t)m * ldx : nullptr;
+    for (int p = 0; p < P; ++p) {
+      const double a = xh[p], al = xl ? xl[p] : 0.0;
+#pragma unroll
+      for (int c = 0; c < CN; ++c) {
+        const int n = min(n0 + c, N - 1);
+        const double b = Yh[(int64_t)n * ldy + p];
+        dd_fma(h[c], l[c], a, b);
+        l[c] = fma(al, b, l[c]);
+        if (Yl) l[c] = fma(a, Yl[(int64_t)n * ldy + p], l[c]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CN; ++c)
+      if (n0 + c < N) {
+        dd_norm(h[c], l[c]);
+        store(m, n0 + c, h[c], l[c]);
+      }
+  }
+}
+
+// H5 (one CTA), double-double throughout (G11): K = lagged centring of the gathered R (A14),
+// T = K_XX A, G = A^T T, g = A^T K_Xb; y = G^+ g with the 1e-12 cut on lambda (A13) from
+// hi(G) -- Cholesky (fast path, trace(G^-1) bound as before) or the eigen route -- refined
+// twice against the double-double G and g (residual g - G y in double-double); c = A y.
+__global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ R, const double* __restrict__ Rlo,
+                                                     Win W, int r, const double* __restrict__ A,
+                                                     const int32_t* __restrict__ reffp, double cut,
+                                                     double* __restrict__ y_out, double* __restrict__ c_out,
+                                                     int32_t* __restrict__ status, double* __restrict__ gfac,
+                                                     bool fac_smem, double* __restrict__ Kg, double* __restrict__ Tg,
+                                                     long long* tdbg) {
   extern __shared__ double sm[];
   int ts = 0;
   sstamp(tdbg, ts);
   const int re = *reffp;
-  const int w = W.w, nU = W.nU, xoff = nU - w, ldk = w + 1, lda = w + 1, ldl = re | 1;
+  const int w = W.w, nU = W.nU, xoff = nU - w, ldk = w + 1, lda = w + 1, ldl = re | 1, ldg = r | 1;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  const SolveLayout S = solve_layout(w, r, mode);
-  double* Ks = mode >= 1 ? sm + S.ks : Kg;
-  double* As = sm + S.as;  // As[j * lda + i] = A[j * w + i]
-  double* T = sm + S.t;    // T[j * lda + i]
-  double* mp = sm + S.mp;
-  double* mc = sm + S.mc;
-  double* Lm = sm + S.lm;  // Lm[i * ldl + k]
-  double* rhs = sm + S.vec;
-  double* y = rhs + kMaxSlots;
-  double* u = y + kMaxSlots;
-  double* misc = u + kMaxSlots;
-  double* wtr = misc + kMaxSlots;  // per-warp partials
   EigLayout L = eig_layout(re > 0 ? re : 1, re > 0 ? re : 1);
   L.fac_smem = fac_smem;  // the host sized the smem for r >= r_eff: its choice is safe
+  const SolveLayout S = solve_layout(w, r, Kg != nullptr, Tg != nullptr, eig_doubles(r, r, fac_smem));
+  const size_t ka = (size_t)(w + 1) * (w + 1), ta = (size_t)(w + 1) * r;
+  double* As = sm + S.as;  // As[j * lda + i] = A[j * w + i]
+  double* Kh = S.kg ? Kg : sm + S.kh;
+  double* Kl = S.kg ? Kg + ka : sm + S.kl;
+  double* Th = S.tg ? Tg : sm + S.th;  // T[j * lda + i]
+  double* Tl = S.tg ? Tg + ta : sm + S.tl;
+  double* Gh = sm + S.gh;  // G[i * ldg + j]
+  double* Gl = sm + S.gl;
+  double* Lm = sm + S.lm;  // Lm[i * ldl + k]
+  double* mp = sm + S.mp;
+  double* mpl = mp + (kMaxW + 2);
+  double* mc = mpl + (kMaxW + 2);
+  double* mcl = mc + (kMaxW + 2);
+  double* gh = sm + S.vec;
+  double* gl = gh + kMaxSlots;
+  double* y = gl + kMaxSlots;
+  double* u = y + kMaxSlots;
+  double* misc = u + kMaxSlots;
+  double* res = misc + kMaxSlots;
+  double* wtr = res + kMaxSlots;  // per-warp partials (2 SV_W)
+  double* Ge = sm + S.eig;        // eigen route: matrix + workspace over region X
+  const EigWork E = eig_work(Ge, re > 0 ? re : 1, L, gfac);
   const int ldn = L.ldn;
-  double* G = sm + S.eig;
-  const EigWork E = eig_work(G, re > 0 ? re : 1, L, gfac);
-  __shared__ double gm[3];
+  __shared__ double gm[6];
   __shared__ int s_fast;
-  // ---- centring of R into K (same algebra as the window Gram, A14) ----
-  int ldr = nU + 1;
-  const double* Rr = R;
+  // ---- centring of R into K (same algebra as the window Gram, A14), double-double ----
+  const int ldr = nU + 1;
   for (int i = tid; i < w * re; i += nt) As[(i / w) * lda + (i % w)] = A[i];
-  if (mode == 2) {  // stage R (coalesced, all loads independent)
-    double* Rs = sm + S.rs;
-    for (int i = tid; i < ldr * ldr; i += nt) Rs[i] = R[i];
-    Rr = Rs;
-    __syncthreads();
-  }
   for (int a = warp; a <= nU; a += SV_W) {  // warp per row of R
-    double sp = 0.0, sc = 0.0;
+    double ph = 0.0, pl = 0.0, ch = 0.0, cl = 0.0;
     for (int q = lane; q < nU; q += 32) {
-      const double v = Rr[a * ldr + q];
-      if (q < w) sp += v;
-      if (q >= xoff) sc += v;
+      const double vh = R[a * ldr + q], vl = Rlo[a * ldr + q];
+      if (q < w) dd_add(ph, pl, vh, vl);
+      if (q >= xoff) dd_add(ch, cl, vh, vl);
     }
     for (int o = 16; o > 0; o >>= 1) {
-      sp += __shfl_xor_sync(0xffffffffu, sp, o);
-      sc += __shfl_xor_sync(0xffffffffu, sc, o);
+      double oh = __shfl_xor_sync(0xffffffffu, ph, o), ol = __shfl_xor_sync(0xffffffffu, pl, o);
+      dd_add(ph, pl, oh, ol);
+      oh = __shfl_xor_sync(0xffffffffu, ch, o);
+      ol = __shfl_xor_sync(0xffffffffu, cl, o);
+      dd_add(ch, cl, oh, ol);
     }
     if (lane == 0) {
-      mp[a] = sp / (double)w;
-      mc[a] = sc / (double)w;
+      dd_div1(ph, pl, (double)w);
+      dd_div1(ch, cl, (double)w);
+      mp[a] = ph;
+      mpl[a] = pl;
+      mc[a] = ch;
+      mcl[a] = cl;
     }
   }
   __syncthreads();
   sstamp(tdbg, ts);
-  if (warp == 0) {
-    double pp = 0.0, pc = 0.0, cc = 0.0;
-    for (int q = lane; q < w; q += 32) {
-      pp += mp[q];
-      pc += mc[q];
-      cc += mc[xoff + q];
+  if (tid == 0) {
+    double pp = 0.0, ppl = 0.0, pc = 0.0, pcl = 0.0, cc = 0.0, ccl = 0.0;
+    for (int q = 0; q < w; ++q) {
+      dd_add(pp, ppl, mp[q], mpl[q]);
+      dd_add(pc, pcl, mc[q], mcl[q]);
+      dd_add(cc, ccl, mc[xoff + q], mcl[xoff + q]);
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      pp += __shfl_xor_sync(0xffffffffu, pp, o);
-      pc += __shfl_xor_sync(0xffffffffu, pc, o);
-      cc += __shfl_xor_sync(0xffffffffu, cc, o);
-    }
-    if (lane == 0) {
-      gm[0] = pp / (double)w;
-      gm[1] = pc / (double)w;
-      gm[2] = cc / (double)w;
-    }
+    dd_div1(pp, ppl, (double)w);
+    dd_div1(pc, pcl, (double)w);
+    dd_div1(cc, ccl, (double)w);
+    gm[0] = pp;
+    gm[1] = ppl;
+    gm[2] = pc;
+    gm[3] = pcl;
+    gm[4] = cc;
+    gm[5] = ccl;
   }
   __syncthreads();
   for (int idx = tid; idx < ldk * ldk; idx += nt) {
     const int i = idx / ldk, j = idx % ldk;
-    double v;
+    double h, l;
     if (i < w && j < w) {
       const int a = xoff + i, b = xoff + j;
-      v = ((Rr[a * ldr + b] - mp[a]) - mp[b]) + gm[0];
+      h = R[a * ldr + b];
+      l = Rlo[a * ldr + b];
+      dd_add(h, l, -mp[a], -mpl[a]);
+      dd_add(h, l, -mp[b], -mpl[b]);
+      dd_add(h, l, gm[0], gm[1]);
     } else if (i < w || j < w) {
       const int a = xoff + (i < w ? i : j);
-      v = ((Rr[a * ldr + nU] - mc[a]) - mp[nU]) + gm[1];
+      h = R[a * ldr + nU];
+      l = Rlo[a * ldr + nU];
+      dd_add(h, l, -mc[a], -mcl[a]);
+      dd_add(h, l, -mp[nU], -mpl[nU]);
+      dd_add(h, l, gm[2], gm[3]);
     } else {
-      v = ((Rr[nU * ldr + nU] - mc[nU]) - mc[nU]) + gm[2];
+      h = R[nU * ldr + nU];
+      l = Rlo[nU * ldr + nU];
+      dd_add(h, l, -mc[nU], -mcl[nU]);
+      dd_add(h, l, -mc[nU], -mcl[nU]);
+      dd_add(h, l, gm[4], gm[5]);
     }
-    Ks[i * ldk + j] = v;
+    Kh[i * ldk + j] = h;
+    Kl[i * ldk + j] = l;
   }
   __syncthreads();
   sstamp(tdbg, ts);
-  // ---- T = K_XX A, g = A^T K_Xb, G = A^T T ----
-  smem_gemm_nt<2, 4, false>(Ks, ldk, As, lda, w, re, w, [&](int i, int j, double v) { T[j * lda + i] = v; });
+  // ---- T = K_XX A, g = A^T K_Xb, G = A^T T (double-double) ----
+  smem_gemm_dd<4, false>(Kh, Kl, ldk, As, nullptr, lda, w, re, w, [&](int i, int j, double h, double l) {
+    Th[j * lda + i] = h;
+    Tl[j * lda + i] = l;
+  });
   for (int j = tid; j < re; j += nt) {
-    double s = 0.0;
-    for (int p = 0; p < w; ++p) s += As[j * lda + p] * Ks[p * ldk + w];
-    rhs[j] = s;
+    double h = 0.0, l = 0.0;
+    for (int p = 0; p < w; ++p) {
+      const double a = As[j * lda + p];
+      dd_fma(h, l, a, Kh[p * ldk + w]);
+      l = fma(a, Kl[p * ldk + w], l);
+    }
+    dd_norm(h, l);
+    gh[j] = h;
+    gl[j] = l;
   }
   __syncthreads();
   sstamp(tdbg, ts);
-  smem_gemm_nt<1, 4, true>(As, lda, T, lda, re, re, w, [&](int i, int j, double v) {
+  smem_gemm_dd<4, true>(Th, Tl, lda, As, nullptr, lda, re, re, w, [&](int i, int j, double h, double l) {
     if (j >= i) {
-      G[i * ldn + j] = v;
-      G[j * ldn + i] = v;
+      Gh[i * ldg + j] = Gh[j * ldg + i] = h;
+      Gl[i * ldg + j] = Gl[j * ldg + i] = l;
     }
   });
   __syncthreads();
   sstamp(tdbg, ts);
-  // ---- fast path: Cholesky G = L L^T + trace(G^-1) bound ----
+  // ---- fast path: Cholesky hi(G) = L L^T + trace(G^-1) bound ----
   double gf = 0.0;  // ||G||_F^2
   for (int idx = tid; idx < re * re; idx += nt) {
-    const double v = G[(idx / re) * ldn + idx % re];
+    const double v = Gh[(idx / re) * ldg + idx % re];
     Lm[(idx / re) * ldl + idx % re] = v;
     gf += v * v;
   }
@@ -1263,7 +1626,7 @@ __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ 
   bool ok = s_fast != 0;
   sstamp(tdbg, ts);
   if (ok) {
-    const double tr = trinv_cols(Lm, ldl, re, misc, rhs, u);  // trace(G^-1) = ||L^-1||_F^2, u = L^-1 g
+    const double tr = trinv_cols(Lm, ldl, re, misc, gh, u);  // trace(G^-1) = ||L^-1||_F^2, u = L^-1 g
     if (lane == 0) wtr[warp] = tr;
     __syncthreads();
     if (warp == 0) {
@@ -1281,22 +1644,15 @@ __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ 
     ok = s_fast != 0;
   }
   sstamp(tdbg, ts);
-  if (ok) {
-    if (tid == 0) {
-      *status = 0;
-      status[7] = 0;  // fast path
-    }
+  int nk = 0;
+  if (!ok) {
+    // eigen route on hi(G) (its workspace overlays K and T, dead now)
+    for (int idx = tid; idx < re * re; idx += nt) Ge[(idx / re) * ldn + idx % re] = Gh[(idx / re) * ldg + idx % re];
     __syncthreads();
-  } else {
-    const int nk = re > 0 ? sym_eig(G, re, ldn, E, re, cut) : 0;
-    if (tid == 0) {
-      *status = (re == 0 || !(E.lam[0] > 0.0)) ? 1 : 0;
-      status[7] = 1;  // eigen route
-    }
-    // y = sum_{kept} z_k (z_k^T rhs) / lam_k
+    nk = re > 0 ? sym_eig(Ge, re, ldn, E, re, cut) : 0;
     for (int kk = tid; kk < nk; kk += nt) {
       double d = 0.0;
-      for (int p = 0; p < re; ++p) d += E.Z[p * E.ldz + kk] * rhs[p];
+      for (int p = 0; p < re; ++p) d += E.Z[p * E.ldz + kk] * gh[p];
       misc[kk] = d / E.lam[kk];
     }
     __syncthreads();
@@ -1304,6 +1660,44 @@ __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ 
       double s = 0.0;
       for (int kk = 0; kk < nk; ++kk) s += E.Z[i * E.ldz + kk] * misc[kk];
       y[i] = s;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    *status = (!ok && (re == 0 || !(E.lam[0] > 0.0))) ? 1 : 0;
+    status[7] = ok ? 0 : 1;  // fast path / eigen route
+  }
+  // ---- iterative refinement: res = g - G y in double-double, y += G^+ res (same route) ----
+  for (int itr = 0; itr < 2 && re > 0; ++itr) {
+    for (int i = tid; i < re; i += nt) {
+      double h = gh[i], l = gl[i];
+      for (int j = 0; j < re; ++j) {
+        dd_fma(h, l, -Gh[i * ldg + j], y[j]);
+        l = fma(-Gl[i * ldg + j], y[j], l);
+      }
+      res[i] = h + l;
+    }
+    __syncthreads();
+    if (ok) {
+      if (warp == 0) {
+        trsolve_warp(Lm, ldl, re, misc, res, u);
+        __syncwarp();
+        trsolve_t_warp(Lm, ldl, re, misc, u, res);
+        __syncwarp();
+        for (int i = lane; i < re; i += 32) y[i] += res[i];
+      }
+    } else {
+      for (int kk = tid; kk < nk; kk += nt) {
+        double d = 0.0;
+        for (int p = 0; p < re; ++p) d += E.Z[p * E.ldz + kk] * res[p];
+        misc[kk] = d / E.lam[kk];
+      }
+      __syncthreads();
+      for (int i = tid; i < re; i += nt) {
+        double s = 0.0;
+        for (int kk = 0; kk < nk; ++kk) s += E.Z[i * E.ldz + kk] * misc[kk];
+        y[i] += s;
+      }
     }
     __syncthreads();
   }
@@ -1475,6 +1869,35 @@ __global__ void __launch_bounds__(LF_T, 1) lift_kernel(Geo g, Win W, const doubl
   }
 }
 
+// double-double Gram (G11): GGDSmall / GGDWide consumers, partials reduced into (Chi, Clo)
+hrom_status run_gather_gram_dd(hrom_ctx* c, GGArgs& a, int ncol, int grid, double* Chi, double* Clo, int ldc,
+                               const int32_t* map) {
+  a.part = c->b.part;
+  int ncp;
+  if (ncol <= GGDSmall::ncp) {
+    ncp = GGDSmall::ncp;
+    if ((int64_t)grid * ncp * ncp * 2 > c->b.part_len) return HROM_E_INVALID;
+    HROM_CK(cudaFuncSetAttribute(gather_gram_kernel<GGDSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)GGDSmall::smem));
+    gather_gram_kernel<GGDSmall><<<grid, GGDSmall::threads, GGDSmall::smem, c->st>>>(a);
+  } else if (ncol <= GGDWide::ncp) {
+    ncp = GGDWide::ncp;
+    if ((int64_t)grid * ncp * ncp * 2 > c->b.part_len) return HROM_E_INVALID;
+    HROM_CK(cudaFuncSetAttribute(gather_gram_kernel<GGDWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)GGDWide::smem));
+    gather_gram_kernel<GGDWide><<<grid, GGDWide::threads, GGDWide::smem, c->st>>>(a);
+  } else {
+    return HROM_E_INVALID;
+  }
+  HROM_LAUNCH_CK();
+  ++c->nlaunch;
+  gram_reduce_dd<<<(ncol * ncol * GR_TPE + 255) / 256, 256, 0, c->st>>>(c->b.part, grid, ncp, ncol, Chi, Clo, ldc,
+                                                                         map);
+  HROM_LAUNCH_CK();
+  ++c->nlaunch;
+  return HROM_OK;
+}
+
 // launch the pipelined Gram (both modes) and reduce its per-CTA partials into C
 hrom_status run_gather_gram(hrom_ctx* c, GGArgs& a, int ncol, int grid, double* dev_C, int ldc,
                                    const int32_t* map) {
@@ -1536,6 +1959,20 @@ hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int64_t ns, in
   return run_gather_gram(c, a, ncol, c->basis_pending ? c->nsm - 1 : c->nsm, dev_C, ldc, map);
 }
 
+// Window Gram of the basis path in double-double (G11): dev_Chi / dev_Clo[i*ldc+j] (mapped),
+// rows of ncol slab columns shifted by rho, FMA consumers (gather_gram_kernel<GGD*>)
+hrom_status gram_full_dd(hrom_ctx* c, const double* const* dev_cols, int64_t ns, int ncol, int64_t rows, SRef rho,
+                         double* dev_Chi, double* dev_Clo, int ldc, const int32_t* map) {
+  GGArgs a{};
+  a.mode = 0;
+  a.cols = dev_cols;
+  a.ns = ns;
+  a.ncol0 = ncol;
+  a.rows = rows;
+  a.rho = rho;
+  return run_gather_gram_dd(c, a, ncol, c->basis_pending ? c->nsm - 1 : c->nsm, dev_Chi, dev_Clo, ldc, map);
+}
+
 // config 5: C = Phi^T S over the w + 1 window columns (S = the ring slots of the current window)
 hrom_status project_window(hrom_ctx* c, const double* const* phicols, int m, double* dev_C) {
   const Win& W = c->win;
@@ -1567,8 +2004,8 @@ hrom_status project_window(hrom_ctx* c, const double* const* phicols, int m, dou
   return HROM_OK;
 }
 
-// gathered Gram R of [U, b] over the rows of S-hat (shifted by rho, union order, (nU+1)^2 in
-// b.eigV); the lagged centring is applied by solve_kernel
+// gathered Gram R of [U, b] over the rows of S-hat (shifted by rho, union order, (nU+1)^2,
+// double-double: hi in b.eigV, lo in b.Rlo); the lagged centring is applied by solve_kernel
 hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   GGArgs a{};
   a.g = c->g;
@@ -1584,37 +2021,42 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   const int grid = c->basis_pending ? c->nsm - 1 : c->nsm;
   const int ncol = a.W.nU + 1;
   double* R = c->b.eigV;
+  double* Rl = c->b.Rlo;
   if (c->P.odeim_points > 0) {  // gappy rows = the DOF rows of the ODEIM points (Eq. 8, 10)
     a.mode = 2;
     a.rowlist = c->b.orows;
     a.nrow2 = c->odeim_n;
     c->kinc_valid = false;
     c->samples_since_gather = 0;
-    return run_gather_gram(c, a, ncol, grid, R, ncol, nullptr);
+    return run_gather_gram_dd(c, a, ncol, grid, R, Rl, ncol, nullptr);
   }
   const bool inc = c->P.gather_mode == 0 && c->kinc_valid && c->samples_since_gather == 1 && c->kinc_newest == c->k - 1 &&
                    c->kinc_rebase == c->rebase_k;
   hrom_status s;
   if (!inc) {
-    if ((s = run_gather_gram(c, a, ncol, grid, R, ncol, nullptr)) != HROM_OK) return s;
+    if ((s = run_gather_gram_dd(c, a, ncol, grid, R, Rl, ncol, nullptr)) != HROM_OK) return s;
     if (c->P.gather_mode == 0) {
-      kinc_update_kernel<<<1, 512, 0, c->st>>>(a.W, 1, nullptr, nullptr, nullptr, c->b.Khi, c->b.Klo, R);
+      kinc_update_kernel<<<1, 512, 0, c->st>>>(a.W, 1, nullptr, nullptr, nullptr, nullptr, nullptr, c->b.Khi, c->b.Klo,
+                                               R, Rl);
       HROM_LAUNCH_CK();
       ++c->nlaunch;
     }
   } else {
-    // rows entering and leaving S-hat (cells of the last sampling's churn)
+    // rows entering and leaving S-hat (cells of the last sampling's churn), double-double
+    const size_t S2 = (size_t)(kMaxW + 2) * (kMaxW + 2);
     double* Rp = c->b.Rd;
-    double* Rm = c->b.Rd + (size_t)(kMaxW + 2) * (kMaxW + 2);
+    double* Rpl = Rp + S2;
+    double* Rm = Rp + 2 * S2;
+    double* Rml = Rp + 3 * S2;
     GGArgs d = a;
     d.list = c->b.lists + (int64_t)L_ADD * c->g.N;
     d.count = c->b.counts + L_ADD;
-    if ((s = run_gather_gram(c, d, ncol, grid, Rp, ncol, nullptr)) != HROM_OK) return s;
+    if ((s = run_gather_gram_dd(c, d, ncol, grid, Rp, Rpl, ncol, nullptr)) != HROM_OK) return s;
     d.list = c->b.lists + (int64_t)L_REM * c->g.N;
     d.count = c->b.counts + L_REM;
-    if ((s = run_gather_gram(c, d, ncol, grid, Rm, ncol, nullptr)) != HROM_OK) return s;
+    if ((s = run_gather_gram_dd(c, d, ncol, grid, Rm, Rml, ncol, nullptr)) != HROM_OK) return s;
     // GEMVs of the newest snapshot and of b over all S-hat rows
-    // one wave (2 CTAs per SM at 126 registers); static split: avoid the eigen's SM
+    // one wave (2 CTAs per SM); static split: avoid the eigen's SM
     const int gblocks = 2 * (c->basis_pending ? c->nsm - 1 : c->nsm);
     const int nv = 2 * a.W.nU + 1;
     if (a.W.nU <= 9 * GV_W)
@@ -1622,10 +2064,10 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
     else
       gemv_gather_kernel<17><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b, c->b.vpart);
     HROM_LAUNCH_CK();
-    double* v = c->b.vpart + (size_t)gblocks * nv;
+    double* v = c->b.vpart + (size_t)gblocks * nv * 2;
     vpart_reduce<<<(nv * GR_TPE + 255) / 256, 256, 0, c->st>>>(c->b.vpart, gblocks, nv, v);
     HROM_LAUNCH_CK();
-    kinc_update_kernel<<<1, 512, 0, c->st>>>(a.W, 0, Rp, Rm, v, c->b.Khi, c->b.Klo, R);
+    kinc_update_kernel<<<1, 512, 0, c->st>>>(a.W, 0, Rp, Rpl, Rm, Rml, v, c->b.Khi, c->b.Klo, R, Rl);
     HROM_LAUNCH_CK();
     c->nlaunch += 3;
   }
@@ -1638,12 +2080,13 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   return HROM_OK;
 }
 
-// seam-band part of the new window Gram row (band DOFs' final values), partials after the fill's
+// seam-band part of the new window Gram row (band DOFs' final values), double-double partials
+// after the fill's
 hrom_status band_gram_rows(hrom_ctx* c, const Win& W, SRef v) {
   if (W.nU > 9 * GV_W) return HROM_E_INVALID;  // the fused row is limited to nU <= 68 anyway
   gemv_gather_kernel<9, false, true><<<c->band_blocks, GV_T, 0, c->st>>>(
       c->g, W, c->b.ring, c->rho_ref(), c->b.lists + (int64_t)L_B * c->g.N, c->b.counts + L_B, v,
-      c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1));
+      c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1) * 2);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;
@@ -1651,14 +2094,20 @@ hrom_status band_gram_rows(hrom_ctx* c, const Win& W, SRef v) {
 
 hrom_status small_solve(hrom_ctx* c) {
   // the solve reads r_eff on the device: size the workspace for the largest possible (r)
-  const EigLayout L = eig_layout(c->r, c->r);
-  SolveLayout S = solve_layout(c->win.w, c->r, 2);
-  if ((S.total * sizeof(double) + L.bytes) > 220 * 1024) S = solve_layout(c->win.w, c->r, 1);  // wide windows
-  if ((S.total * sizeof(double) + L.bytes) > 220 * 1024) S = solve_layout(c->win.w, c->r, 0);
-  const size_t smem = S.total * sizeof(double) + L.bytes;
+  const int w = c->win.w, r = c->r;
+  bool fac = eig_layout(r, r).fac_smem;
+  const size_t lim = 220 * 1024 / sizeof(double);
+  bool kg = false, tg = false;
+  SolveLayout S = solve_layout(w, r, kg, tg, eig_doubles(r, r, fac));
+  if (S.total > lim) S = solve_layout(w, r, kg = true, tg, eig_doubles(r, r, fac));  // wide windows: K in global
+  if (S.total > lim) S = solve_layout(w, r, kg, tg = true, eig_doubles(r, r, fac));  // ... and T
+  if (S.total > lim) S = solve_layout(w, r, kg, tg, eig_doubles(r, r, fac = false));  // ... and the eigen LU
+  if (S.total > lim) return HROM_E_INVALID;
+  const size_t smem = S.total * sizeof(double);
   HROM_CK(cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  solve_kernel<<<1, SV_T, smem, c->st>>>(c->b.eigV, c->win, c->r, c->b.A, c->b.ireg, c->P.lsq_rel_cutoff, c->b.y,
-                                         c->b.cvec, c->b.ireg + 2, c->b.eigA, L.fac_smem, c->b.K, S.mode,
+  solve_kernel<<<1, SV_T, smem, c->st>>>(c->b.eigV, c->b.Rlo, c->win, r, c->b.A, c->b.ireg, c->P.lsq_rel_cutoff,
+                                         c->b.y, c->b.cvec, c->b.ireg + 2, c->b.eigA, fac,
+                                         kg ? c->b.K : nullptr, tg ? c->b.Tg : nullptr,
                                          c->prof ? c->b.dbg + 64 : nullptr);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
@@ -1666,12 +2115,25 @@ hrom_status small_solve(hrom_ctx* c) {
 }
 
 hrom_status basis_from_gram(hrom_ctx* c, const Win& W) {
-  const EigLayout L = eig_layout(W.w, c->r);
-  HROM_CK(cudaFuncSetAttribute(basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
-  basis_kernel<<<1, 512, L.bytes, c->st>>>(c->b.C, kMaxSlots, W, c->r, c->P.eig_rel_cutoff, c->b.A, c->b.lam,
-                                           c->b.ireg, c->b.eigA);
+  const EigLayout L = eig_layout(W.w, W.w);
+  const size_t smem = L.bytes + 2 * kMaxSlots * sizeof(double);  // + the centring row means (hi, lo)
+  HROM_CK(cudaFuncSetAttribute(basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  double* Mh = c->b.Mdd;
+  double* Ml = c->b.Mdd + (size_t)kMaxSlots * kMaxSlots;
+  basis_kernel<<<1, 512, smem, c->st>>>(c->b.C, c->b.Clo, kMaxSlots, W, Mh, Ml, c->b.Zf, c->b.lam, c->b.ireg,
+                                        c->b.eigA);
   HROM_LAUNCH_CK();
-  ++c->nlaunch;
+  size_t rsm = (size_t)5 * W.w * (W.w | 1) * sizeof(double);
+  double* gws = nullptr;
+  if (rsm > 200 * 1024) {  // wide windows: workspace in the (L2-resident) global scratch
+    gws = c->b.rfws;
+    rsm = 0;
+  }
+  HROM_CK(cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+  refine_kernel<<<1, RF_T, rsm, c->st>>>(Mh, Ml, c->b.Zf, W.w, c->r, c->P.eig_rel_cutoff, c->b.lam, c->b.A,
+                                         c->b.ireg, gws);
+  HROM_LAUNCH_CK();
+  c->nlaunch += 2;
   return HROM_OK;
 }
 

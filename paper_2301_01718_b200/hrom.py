@@ -63,6 +63,8 @@ _SIGS = {
     "hrom_rel_l1_error": (C.c_int, [_VP, _VP, _VP, C.POINTER(C.c_double)]),
     "hrom_sync": (C.c_int, [_VP]),
     "hrom_join": (C.c_int, [_VP]),
+    "hrom_set_graph": (C.c_int, [_VP, C.c_int32]),
+    "hrom_graph_launches": (C.c_int64, [_VP]),
     "hrom_points_used": (C.c_int32, [_VP]),
     "hrom_error_cell": (C.c_int64, [_VP]),
     "hrom_step_index": (C.c_int64, [_VP]),
@@ -264,6 +266,13 @@ class HybridROM:
         if code == 3:
             raise HromError(code, f"hrom_sync (cell {self.lib.hrom_error_cell(self.h)})")
         _ck(code, "hrom_sync")
+
+    def set_graph(self, enable: bool = True):
+        """Replay steady-state steps from per-ring-phase CUDA graphs (hrom_set_graph)."""
+        _ck(self.lib.hrom_set_graph(self.h, int(enable)), "hrom_set_graph")
+
+    def graph_launches(self) -> int:
+        return int(self.lib.hrom_graph_launches(self.h))
 
     def join(self):
         """Context stream waits for the library's side-stream work (no host sync)."""
