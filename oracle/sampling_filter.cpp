@@ -284,20 +284,24 @@ int64_t orc_seam_filter(const orc_grid* g, const orc_params* p, double* v, const
             vpp[var * G.N + n] = s / den;
           }
         }
-      // residual gate: r = max_var |v - F| per cell; keep where r_new < r_old
+      // residual gate: r = max_var |v - F| per cell; keep where r_new < r_old.
+      // eps_f stop (reading A23'): the relative decrease counts only cells whose old residual is
+      // above the rounding level of the state, r_old > 2^-40 max_var |F| (rounding noise would
+      // otherwise decide the sweep count)
       int64_t nkept = 0;
       double maxdec = 0.0;
       for (int64_t n : band) {
-        double rold = 0.0, rnew = 0.0;
+        double rold = 0.0, rnew = 0.0, fs = 0.0;
         for (int var = 0; var < G.c; ++var) {
           const int64_t e = var * G.N + n;
           rold = std::max(rold, std::fabs(v[e] - F[e]));
           rnew = std::max(rnew, std::fabs(vpp[e] - F[e]));
+          fs = std::max(fs, std::fabs(F[e]));
         }
         if (rnew < rold) {
           ++nkept;
           kept[n] = 1;
-          maxdec = std::max(maxdec, (rold - rnew) / rold);
+          if (rold > 0x1p-40 * fs) maxdec = std::max(maxdec, (rold - rnew) / rold);
           for (int var = 0; var < G.c; ++var) v[var * G.N + n] = vpp[var * G.N + n];
         }
       }

@@ -353,6 +353,12 @@ void hrom_destroy(hrom_ctx* c) {
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (auto& gs : c->graphs)
     if (gs.exec) cudaGraphExecDestroy(gs.exec);
+  if (c->gst) {
+    cudaStreamSynchronize(c->gst);
+    cudaStreamDestroy(c->gst);
+  }
+  if (c->ev_g0) cudaEventDestroy(c->ev_g0);
+  if (c->ev_g1) cudaEventDestroy(c->ev_g1);
   Bufs& b = c->b;
   void* ptrs[] = {b.ring, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
                   b.kept, b.fidx, b.ftab, b.fcur, b.fF, b.C, b.Clo, b.Rlo, b.Mdd, b.Zf, b.rfws, b.Tg, b.part, b.gpart, b.K, b.Khi, b.Klo, b.Rd, b.vpart, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
@@ -755,7 +761,7 @@ bool graph_eligible(const hrom_ctx* c, int32_t* dev_count_out) {
   return c->graph_on && !c->prof && dev_count_out == nullptr && c->P.full_period <= 0 && c->P.odeim_points == 0 &&
          c->P.gram_mode == 0 && c->P.gather_mode == 0 && c->k >= c->w + 1 && c->last_hybrid && c->sets_ready &&
          c->basis_ready && c->eig_todo && !c->basis_pending && !c->bg_pending && c->kinc_valid &&
-         c->samples_since_gather == 1 && c->kinc_newest == c->k && c->smax_k == c->k && c->n_owed == 0 &&
+         c->samples_since_gather == 1 && c->kinc_newest == c->k - 1 && c->smax_k == c->k && c->n_owed == 0 &&
          !hrom_sync_debug();
 }
 hrom_status step_eager(hrom_ctx* c, double dt_override, int32_t* dev_count_out);
@@ -767,34 +773,42 @@ hrom_status hrom_step_ex(hrom_ctx* c, double dt_override, int32_t* dev_count_out
   if (!graph_eligible(c, dev_count_out)) return step_eager(c, dt_override, dev_count_out);
   GraphSlot& gs = c->graphs[c->slot_of(c->k)];
   const HostSnap entry = snap_get(c, dt_override);
+  // graphs run on the library's own capture stream, ordered after / before the context stream
+  // (which may be the legacy default stream, where capture is not permitted)
+  cudaStream_t user = c->st;
+  HROM_CK(cudaEventRecord(c->ev_g0, user));
+  HROM_CK(cudaStreamWaitEvent(c->gst, c->ev_g0, 0));
   if (gs.exec && snap_same(gs.pre, entry, c->nslots)) {
     snap_apply(c, gs.post, entry.k - gs.pre.k, gs.post.nlaunch - gs.pre.nlaunch);
-    HROM_CK(cudaGraphLaunch(gs.exec, c->st));
-    ++c->graph_launches;
-    return HROM_OK;
+    HROM_CK(cudaGraphLaunch(gs.exec, c->gst));
+  } else {
+    // capture this step (nothing executes while capturing), instantiate, then launch it
+    if (gs.exec) {
+      cudaGraphExecDestroy(gs.exec);
+      gs.exec = nullptr;
+    }
+    HROM_CK(cudaStreamBeginCapture(c->gst, cudaStreamCaptureModeThreadLocal));
+    c->st = c->gst;
+    const hrom_status s = step_eager(c, dt_override, nullptr);
+    c->st = user;
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(c->gst, &graph);
+    if (s != HROM_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return s;
+    }
+    HROM_CK(ec);
+    const cudaError_t ei = cudaGraphInstantiate(&gs.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    HROM_CK(ei);
+    gs.pre = entry;
+    gs.post = snap_get(c, dt_override);
+    ++c->graph_captures;
+    HROM_CK(cudaGraphLaunch(gs.exec, c->gst));
   }
-  // capture this step (nothing executes while capturing), instantiate, then launch it
-  if (gs.exec) {
-    cudaGraphExecDestroy(gs.exec);
-    gs.exec = nullptr;
-  }
-  HROM_CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
-  const hrom_status s = step_eager(c, dt_override, nullptr);
-  cudaGraph_t graph = nullptr;
-  const cudaError_t ec = cudaStreamEndCapture(c->st, &graph);
-  if (s != HROM_OK) {
-    if (graph) cudaGraphDestroy(graph);
-    return s;
-  }
-  HROM_CK(ec);
-  const cudaError_t ei = cudaGraphInstantiate(&gs.exec, graph, 0);
-  cudaGraphDestroy(graph);
-  HROM_CK(ei);
-  gs.pre = entry;
-  gs.post = snap_get(c, dt_override);
-  ++c->graph_captures;
-  HROM_CK(cudaGraphLaunch(gs.exec, c->st));
   ++c->graph_launches;
+  HROM_CK(cudaEventRecord(c->ev_g1, c->gst));
+  HROM_CK(cudaStreamWaitEvent(user, c->ev_g1, 0));
   return HROM_OK;
 }
 
@@ -802,6 +816,11 @@ hrom_status hrom_set_graph(hrom_ctx* c, int32_t enable) {
   if (!c) return HROM_E_INVALID;
   c->graph_on = enable != 0;
   if (c->graph_on && c->graphs.empty()) c->graphs.resize(c->nslots);
+  if (c->graph_on && !c->gst) {
+    HROM_CK(cudaStreamCreateWithFlags(&c->gst, cudaStreamNonBlocking));
+    HROM_CK(cudaEventCreateWithFlags(&c->ev_g0, cudaEventDisableTiming));
+    HROM_CK(cudaEventCreateWithFlags(&c->ev_g1, cudaEventDisableTiming));
+  }
   if (!c->graph_on) {
     // the eager path flushes the deferred eigen-solve at the sampling; a pending one (graph mode
     // defers it to the next step) is launched by the next step's flush_eigen as well

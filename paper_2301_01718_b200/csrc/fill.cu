@@ -48,8 +48,21 @@ struct FillArgs {
   const uint32_t* mB;
   double* eps_elem;
   double* part;            // [grid][nU+1][hi, lo]
+  const double* C;         // window Gram (hi) by ring slot: its diagonal sets the accumulator bias
+  int ldc;
   const unsigned long long* run_if;  // nullable: run only if *run_if != ~0 (escalated step)
 };
+
+// (hi, lo) += a * b with hi biased far above every partial sum and product (|hi| >= |a b|):
+// TwoProduct by FMA, then the exact Fast2Sum
+__device__ __forceinline__ void biased_fma(double& hi, double& lo, double a, double b) {
+  const double p = a * b;
+  const double pe = fma(a, b, -p);
+  const double s = hi + p;
+  const double e = p - (s - hi);
+  hi = s;
+  lo += e + pe;
+}
 
 // SH: compile-time upper bound of the physical slots per half (ceil((w + 2) / 2)).
 // A DOF is owned by a lane pair (l, l ^ 16) of a compute warp; each lane reads its half of the
@@ -69,6 +82,7 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   // per PHYSICAL slot p: in-window flag (cA) and coefficient c (cX)
   __shared__ double cA[kMaxSlots + 2], cX[kMaxSlots + 2];
   __shared__ double wred[NCW][2 * SH + 1], wredl[NCW][2 * SH + 1];
+  __shared__ double s_bias;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Geo& g = a.g;
   const int xoff = nU - w;  // logical: psi_cur and X use slots >= xoff; psi_prev uses slots < w
@@ -85,6 +99,15 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
       mbar_init(&empty[q], NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    // Gram-row accumulator bias B = a power of two >= 256 max_s ||gamma_s - rho||^2 (the window
+    // Gram's diagonal): every partial sum and product of the row then stays below B / 2, so
+    // hi = B + S is updated by the exact Fast2Sum (3 operations instead of TwoSum's 6) and
+    // (hi - B) + lo is the double-double row (G11).  A new snapshot 8x farther from rho than the
+    // whole window would only degrade the row towards fp64 accuracy.
+    double mc = 0.0;
+    if (GRAM && a.C)
+      for (int s2 = 0; s2 < nU; ++s2) mc = fmax(mc, a.C[a.W.slot[s2] * (a.ldc + 1)]);
+    s_bias = mc > 0.0 ? ldexp(1.0, ilogb(256.0 * mc) + 1) : 1.0;
   }
   __syncthreads();
   const int64_t ntiles = (g.D + TILE - 1) / TILE;
@@ -112,11 +135,15 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   for (int q = 0; q < nsl; ++q) csum += cX[q];
   const double inv_w = 1.0 / (double)w;
   const int roff = a.rho_slot * TILE;
-  // Gram-row accumulators in double-double (dd.cuh, G11): the row enters the POD's Gram
+  // Gram-row accumulators in double-double (dd.cuh, G11), biased by B (see s_bias)
+  const double bias = s_bias;
   double acc[SH], accl[SH];
 #pragma unroll
-  for (int i = 0; i < SH; ++i) acc[i] = accl[i] = 0.0;
-  double acc_self = 0.0, acc_selfl = 0.0;
+  for (int i = 0; i < SH; ++i) {
+    acc[i] = bias;
+    accl[i] = 0.0;
+  }
+  double acc_self = bias, acc_selfl = 0.0;
   // per-DOF side data (mask words, HDM value / new column) is fetched one tile ahead
   uint32_t wS = 0, wB = 0;
   int bitpos = 0;
@@ -211,12 +238,12 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     // pass 2: new Gram row on this lane's physical slots (band DOFs are added after the filter)
     if (GRAM && valid && !inB) {
       const double gr = gval - rh;
-      if (half == 0) dd_fma(acc_self, acc_selfl, gr, gr);
+      if (half == 0) biased_fma(acc_self, acc_selfl, gr, gr);
+      // h0 slots per half (uniform): for an odd slot count the last of half 1 is rho's slot,
+      // accumulated and discarded
 #pragma unroll
-      for (int i = 0; i < SH; ++i) {
-        const int q = q0 + i;
-        if (q < qn) dd_fma(acc[i], accl[i], gr, T[q * TILE] - rh);
-      }
+      for (int i = 0; i < SH; ++i)
+        if (i < h0) biased_fma(acc[i], accl[i], gr, T[(q0 + i) * TILE] - rh);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
@@ -225,7 +252,7 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   // fixed-order reductions: the 16 lanes of each half (shuffle tree), then warps -> part[block][s]
 #pragma unroll
   for (int i = 0; i < SH; ++i) {
-    double v = acc[i], vl = accl[i];
+    double v = acc[i] - bias, vl = accl[i];  // exact (Sterbenz)
     for (int o = 8; o > 0; o >>= 1) {
       const double oh = __shfl_xor_sync(0xffffffffu, v, o), ol = __shfl_xor_sync(0xffffffffu, vl, o);
       dd_add(v, vl, oh, ol);
@@ -236,7 +263,7 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     }
   }
   {
-    double v = acc_self, vl = acc_selfl;
+    double v = acc_self - bias, vl = acc_selfl;
     for (int o = 16; o > 0; o >>= 1) {
       const double oh = __shfl_xor_sync(0xffffffffu, v, o), ol = __shfl_xor_sync(0xffffffffu, vl, o);
       dd_add(v, vl, oh, ol);
@@ -366,6 +393,8 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef ou
   a.mB = (mode == MODE_FILL) ? c->b.masks + (int64_t)M_B * c->mwords : nullptr;
   a.eps_elem = c->b.eps_elem;
   a.part = c->b.gpart;
+  a.C = c->b.C;
+  a.ldc = kMaxSlots;
   const int sh = (c->nslots + 1) / 2;
 #define FILL_CASE(SH_)                                                                            \
   if (sh <= SH_) return a.do_gram ? launch_fill_t<SH_, true>(c, a, smem) : launch_fill_t<SH_, false>(c, a, smem);

@@ -6,7 +6,8 @@
 // where the residual decreases; stop on an empty keep-set, a decrease below eps_f, or
 // j_max^f sweeps; cascade 2 -> 4 -> 6.  Readings A21-A24: band
 // B = (S-hat (+) Q_W) \ S-hat, residual per cell ||v - F||_inf over the c variables
-// (F = full-RK3 values on B), relative eps_f test, x then y, stencils of S:386.
+// (F = full-RK3 values on B), relative eps_f test above the rounding level (A23'), x then y,
+// stencils of S:386.
 #include <cooperative_groups.h>
 #include <algorithm>
 #include "internal.cuh"
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
 #pragma unroll
           for (int m = 0; m < 7; ++m) y[var][m] = (g.dim == 2 && var < g.c && m <= 2 * rad) ? __ldcg(Vp + var * N + nbr[m]) : 0.0;
         }
-        double rold = 0.0, rnew = 0.0;
+        double rold = 0.0, rnew = 0.0, fs = 0.0;
         double vpp[4];
 #pragma unroll
         for (int var = 0; var < 4; ++var) {
@@ -243,13 +244,14 @@ __global__ void __launch_bounds__(FT) filter_kernel(FilterArgs a) {
           vpp[var] = xv;
           rold = fmax(rold, fabs(own[var] - fe[var]));
           rnew = fmax(rnew, fabs(xv - fe[var]));
+          fs = fmax(fs, fabs(fe[var]));
         }
         if (rnew < rold) {
 #pragma unroll
           for (int var = 0; var < 4; ++var)
             if (var < g.c) cur[var * N + t] = vpp[var];
           if (!(flag[t] & 1)) flag[t] = 1;
-          mdec = fmax(mdec, (rold - rnew) / rold);
+          if (rold > 0x1p-40 * fs) mdec = fmax(mdec, (rold - rnew) / rold);  // A23': above rounding level
           ++cnt;
         }
       }
@@ -358,7 +360,7 @@ __global__ void __launch_bounds__(FT) filter_small_kernel(FilterArgs a) {
       double mdec = 0.0;
       int cnt = 0;
       for (int t = threadIdx.x; t < nb; t += FT) {  // P2: v'' = S^y(v'), gate, apply
-        double rold = 0.0, rnew = 0.0, vpp[4];
+        double rold = 0.0, rnew = 0.0, fs = 0.0, vpp[4];
         for (int var = 0; var < g.c; ++var) {
           double xv;
           if (g.dim == 2) {
@@ -374,11 +376,12 @@ __global__ void __launch_bounds__(FT) filter_small_kernel(FilterArgs a) {
           const double fe = sF[var * nb + t];
           rold = fmax(rold, fabs(scur[var * M + t] - fe));
           rnew = fmax(rnew, fabs(xv - fe));
+          fs = fmax(fs, fabs(fe));
         }
         if (rnew < rold) {
           for (int var = 0; var < g.c; ++var) scur[var * M + t] = vpp[var];
           sflag[t] = 1;
-          mdec = fmax(mdec, (rold - rnew) / rold);
+          if (rold > 0x1p-40 * fs) mdec = fmax(mdec, (rold - rnew) / rold);  // A23': above rounding level
           ++cnt;
         }
       }

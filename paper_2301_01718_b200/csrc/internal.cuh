@@ -229,6 +229,8 @@ struct hrom_ctx {
   bool graph_on = false;
   std::vector<hrom::GraphSlot> graphs;
   int64_t graph_launches = 0, graph_captures = 0;
+  cudaStream_t gst = nullptr;               // capture / replay stream of the graphs
+  cudaEvent_t ev_g0 = nullptr, ev_g1 = nullptr;
   int slot_of(int64_t kk) const { return (int)(kk % nslots); }
   hrom::SRef slot_ref(int s) const { return hrom::SRef{b.ring + (int64_t)s * hrom::TILE, g.nsr}; }
   hrom::SRef rho_ref() const { return hrom::SRef{b.rho, g.nsr}; }

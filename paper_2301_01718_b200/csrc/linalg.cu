@@ -735,7 +735,7 @@ hrom_status launch_cross(hrom_ctx* c, XGArgs& a, int grid) {
 // S-hat (x = slot - rho, b = src_b - rho).  Lanes own consecutive rows (one slot load per warp
 // instruction = 32 consecutive list DOFs, coalesced); warp w of the CTA owns slots w, w + 8, ...;
 // GV_U row chunks in flight per lane.  Per-CTA partials [blk][2 nU + 1], reduced in fixed order.
-constexpr int GV_T = 256, GV_W = GV_T / 32, GV_U = 2;
+constexpr int GV_T = 256, GV_W = GV_T / 32, GV_U = 1;
 // NEWCOL = false, BANDOUT = true: the seam-band part of the new window Gram row (H10): one
 // product vector b = gamma_k on the band rows, partials [blk][nU + 1] ([nU] = sum b^2).
 template <int SPW, bool NEWCOL = true, bool BANDOUT = false>
@@ -749,11 +749,11 @@ __global__ void __launch_bounds__(GV_T, 2) gemv_gather_kernel(Geo g, Win W, cons
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const SRef slab{nullptr, g.nsr};
   const double* xnew_col = ring + (int64_t)W.slot[nU - 1] * TILE;
-  const double* col[SPW];
+  int coff[SPW];  // slab offsets of the warp's slots (-1: none); 32-bit to save registers
 #pragma unroll
   for (int j = 0; j < SPW; ++j) {
     const int sl = warp + GV_W * j;
-    col[j] = sl < nU ? ring + (int64_t)W.slot[sl] * TILE : nullptr;
+    coff[j] = sl < nU ? W.slot[sl] * TILE : -1;
   }
   // double-double accumulators (G11): these GEMVs are rows / columns of the POD's and the
   // gappy normal equations' Grams
@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(GV_T, 2) gemv_gather_kernel(Geo g, Win W, cons
 #pragma unroll
     for (int u = 0; u < GV_U; ++u)
 #pragma unroll
-      for (int j = 0; j < SPW; ++j) val[u][j] = (ok[u] && col[j]) ? __ldg(col[j] + se[u]) : 0.0;
+      for (int j = 0; j < SPW; ++j) val[u][j] = (ok[u] && coff[j] >= 0) ? __ldg(ring + coff[j] + se[u]) : 0.0;
 #pragma unroll
     for (int u = 0; u < GV_U; ++u) {
       if (!ok[u]) continue;

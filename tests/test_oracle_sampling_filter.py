@@ -346,7 +346,8 @@ def _brute_seam_filter(orc, wl, v, F, S, eps_rule="relative"):
     closed-form responses above), then  v'' = S^y(v')  on B, residual r = max_var |. - F| per
     cell, keep v'' where r strictly decreases; stop the order when nothing is kept or the largest
     decrease is below eps_f ("relative": (r_old - r_new) / r_old, reading A23; "absolute":
-    r_old - r_new, the literal alternative -- used only to show the pins can tell them apart)."""
+    r_old - r_new, the literal alternative -- used only to show the pins can tell them apart);
+    only cells whose old residual exceeds 2^-40 max_var |F| enter the stop test (reading A23')."""
     nx, ny, N, c = wl.nx, (wl.ny if wl.dim == 2 else 1), wl.N, wl.c
     per = wl.bc == 1
     if wl.W < 0:
@@ -375,6 +376,7 @@ def _brute_seam_filter(orc, wl, v, F, S, eps_rule="relative"):
                     vpp[var, band] = ys.reshape(-1)[band]
             r_old = np.max(np.abs(v[:, band] - F[:, band]), axis=0)
             r_new = np.max(np.abs(vpp[:, band] - F[:, band]), axis=0)
+            fscale = np.max(np.abs(F[:, band]), axis=0)
             keep = r_new < r_old
             if not keep.any():
                 break
@@ -384,7 +386,9 @@ def _brute_seam_filter(orc, wl, v, F, S, eps_rule="relative"):
             dec = r_old[keep] - r_new[keep]
             if eps_rule == "relative":
                 dec = dec / r_old[keep]
-            if dec.max() < wl.filter_eps:
+            # reading A23': only residuals above the rounding level of the state enter the stop test
+            dec = dec[r_old[keep] > 2.0 ** -40 * fscale[keep]]
+            if (dec.max() if dec.size else 0.0) < wl.filter_eps:
                 break
         sweeps.append(nsw)
     return v, kept, sweeps
@@ -446,3 +450,21 @@ def test_seam_filter_relative_not_absolute_eps(orc, inputs):
     _, _, abs_sw = _brute_seam_filter(orc, wl, v, F, S, "absolute")
     assert list(sweeps[:len(rel_sw)]) == rel_sw
     assert rel_sw != abs_sw and max(rel_sw) > 1 and abs_sw == [1] * len(abs_sw)
+
+
+def test_seam_filter_stop_ignores_rounding_level_residuals(orc, inputs):
+    """Reading A23': a band cell whose residual is at the rounding level of the state (here
+    exactly 2^-52 |F|, one ulp) does not keep the cascade sweeping, however large its relative
+    decrease.  A constant state with one-ulp perturbations on a periodic grid: the order-2 sweep
+    removes them (relative decrease 1 on every perturbed cell), yet the first sweep already stops
+    each order (sweeps == [1, 1, 1]); without the floor the relative rule would sweep again."""
+    wl = dataclasses.replace(_wl(inputs, nx=24, ny=20, bc=1, seed=3), W=-1)
+    F = np.empty((wl.c, wl.N))
+    F[:] = np.array([1.0, 0.5, 0.25, 2.0])[:, None]
+    rng = np.random.default_rng(3)
+    v = F * (1.0 + 2.0 ** -52 * rng.integers(-1, 2, size=F.shape))
+    out, kept, sweeps = orc.seam_filter(wl, v, F, np.zeros(wl.N, np.uint8))
+    assert kept.sum() > 0
+    assert list(sweeps) == [1, 1, 1]
+    _, _, bs = _brute_seam_filter(orc, wl, v, F, np.zeros(wl.N, np.uint8))
+    assert bs == [1, 1, 1]

@@ -23,8 +23,9 @@ def row(tag, rec):
     eg, eo = rec["eg"], rec["eo"]
     both = eo > 0
     return {"case": tag, "rel_l2": T.rel(g, o), "max_elem": T.maxerr(g, o), "bar": rec["bar"],
-            "eps_rel": T.rel(eg[both], eo[both]) if both.any() else 0.0,
-            "eps_support_flips": int(((eg > 0) ^ (eo > 0)).sum())}
+            "eps_rel": T.rel(eg, eo), "eps_max_elem": float(np.max(np.abs(eg - eo)) / np.max(eo)),
+            "eps_support_flips": int(((eg > 0) ^ (eo > 0)).sum()),
+            "eps_flip_max": float(np.max(np.maximum(eg, eo)[(eg > 0) ^ (eo > 0)], initial=0.0) / np.max(eo))}
 
 
 def main():
