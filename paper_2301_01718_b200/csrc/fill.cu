@@ -26,8 +26,9 @@
 namespace hrom {
 namespace {
 
-constexpr int NCW = TILE / 16;  // warps (16 DOFs each: one lane pair per DOF); thread 0 also issues the copies
-constexpr int FILL_STAGES = 2;  // slab-tile stages in shared memory
+constexpr int NQ = 4;            // slot quarters: four warps cooperate on the same 32 DOFs
+constexpr int NCW = NQ * TILE / 32;  // compute warps (16); thread 0 also issues the copies
+constexpr int FILL_STAGES = 2;   // slab-tile stages in shared memory
 constexpr int FILL_THREADS = 32 * NCW;
 
 enum { MODE_FILL = 0, MODE_READ = 1, MODE_PROJ = 2 };
@@ -64,12 +65,13 @@ __device__ __forceinline__ void biased_fma(double& hi, double& lo, double a, dou
   lo += e + pe;
 }
 
-// SH: compile-time upper bound of the physical slots per half (ceil((w + 2) / 2)).
-// A DOF is owned by a lane pair (l, l ^ 16) of a compute warp; each lane reads its half of the
-// DOF's slot values from the staged tile and holds SH double-double Gram accumulators.
-// GRAM: the instantiation accumulates the Gram row (do_gram); without it the double-double
-// accumulators are compiled out (projection mode, wide windows).
-template <int SH, bool GRAM>
+// SQ: compile-time upper bound of the physical slots per quarter (ceil((w + 2) / 4)).
+// Warp w owns DOF group grp = w / 4 (32 DOFs, one per lane) and slot quarter qq = w % 4
+// (physical slots [qq SQ, qq SQ + SQ)): every shared-memory load of a warp reads 32 consecutive
+// DOFs of one slot (conflict-free), and each lane holds SQ double-double Gram accumulators.
+// The four quarters' partial window sums meet in shared memory behind a 128-thread named
+// barrier per DOF group (double-buffered by tile parity).
+template <int SQ, bool GRAM>
 __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   if (a.run_if && *a.run_if == ~0ull) return;  // conditional re-run (positivity escalation)
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -81,17 +83,22 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   uint64_t* empty = full + a.nstage;
   // per PHYSICAL slot p: in-window flag (cA) and coefficient c (cX)
   __shared__ double cA[kMaxSlots + 2], cX[kMaxSlots + 2];
-  __shared__ double wred[NCW][2 * SH + 1], wredl[NCW][2 * SH + 1];
+  // quarter partials [parity][group][quarter][lane]: window sum, c-weighted sum; quarter 0 also
+  // publishes the DOF's side data (S-hat / band bits, HDM value)
+  __shared__ double xsa[2][NCW / NQ][NQ][32], xtr[2][NCW / NQ][NQ][32], xside[2][NCW / NQ][32];
+  __shared__ uint8_t xflag[2][NCW / NQ][32];
+  __shared__ double wred[NCW][2 * SQ + 2];  // end-of-kernel row reduction (hi, lo per slot)
   __shared__ double s_bias;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = warp / NQ, qq = warp % NQ;
   const Geo& g = a.g;
   const int xoff = nU - w;  // logical: psi_cur and X use slots >= xoff; psi_prev uses slots < w
   for (int q = tid; q < kMaxSlots + 2; q += FILL_THREADS) cA[q] = cX[q] = 0.0;
   __syncthreads();
-  for (int s = tid; s < nU; s += FILL_THREADS) {
-    const int q = a.W.slot[s];
+  for (int s2 = tid; s2 < nU; s2 += FILL_THREADS) {
+    const int q = a.W.slot[s2];
     cA[q] = 1.0;
-    cX[q] = (s >= xoff && a.cvec) ? a.cvec[s - xoff] : 0.0;
+    cX[q] = (s2 >= xoff && a.cvec) ? a.cvec[s2 - xoff] : 0.0;
   }
   if (tid == 0) {
     for (int q = 0; q < a.nstage; ++q) {
@@ -125,26 +132,24 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   if (tid == 0)
     for (int q = 0; q < a.nstage; ++q) issue(q);
 
-  // ---------------- compute warps: DOF el = warp*16 + (lane & 15), slot half = lane >> 4
-  const int half = lane >> 4;
-  const int el = warp * 16 + (lane & 15);
-  const int h0 = (nsl + 1) / 2;                  // physical slots [0, h0) | [h0, nsl)
-  const int q0 = half ? h0 : 0, qn = half ? nsl : h0;
+  // ---------------- compute warps: DOF el = grp*32 + lane, physical slots [q0, q0 + SQ)
+  const int el = grp * 32 + lane;
+  const int q0 = qq * SQ;
+  const int nq = min(SQ, nsl - q0);  // real slots of this quarter (warp-uniform; may be <= 0)
   const int p_first = a.W.slot[0], p_last = a.W.slot[nU - 1];
   double csum = 0.0;
   for (int q = 0; q < nsl; ++q) csum += cX[q];
   const double inv_w = 1.0 / (double)w;
   const int roff = a.rho_slot * TILE;
-  // Gram-row accumulators in double-double (dd.cuh, G11), biased by B (see s_bias)
   const double bias = s_bias;
-  double acc[SH], accl[SH];
+  double acc[SQ], accl[SQ];
 #pragma unroll
-  for (int i = 0; i < SH; ++i) {
+  for (int i = 0; i < SQ; ++i) {
     acc[i] = bias;
     accl[i] = 0.0;
   }
   double acc_self = bias, acc_selfl = 0.0;
-  // per-DOF side data (mask words, HDM value / new column) is fetched one tile ahead
+  // per-DOF side data (mask words, HDM value / new column), fetched by quarter 0 one tile ahead
   uint32_t wS = 0, wB = 0;
   int bitpos = 0;
   double pre = 0.0;
@@ -152,7 +157,7 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     const int64_t e = tile * TILE + el;
     wS = wB = 0;
     pre = 0.0;
-    if (half == 0 && tile < ntiles && e < g.D && a.mode != MODE_PROJ) {
+    if (qq == 0 && tile < ntiles && e < g.D && a.mode != MODE_PROJ) {
       const int64_t n = e % g.N;
       const int i = (int)(n % g.nx), j = (int)(n / g.nx);
       const int64_t wi = (int64_t)j * g.wpr + (i >> 5);
@@ -169,7 +174,7 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   fetch(first);
   int it = 0;
   for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
-    const int st = it % a.nstage;
+    const int st = it % a.nstage, par = it & 1;
     if (tid == 0 && it >= 1) {
       // the stage of tile it-1 is free once every warp released it: refill it with tile it-1+stages
       const int pst = (it - 1) % a.nstage;
@@ -179,21 +184,21 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     }
     const int64_t e = tile * TILE + el;
     const bool valid = e < g.D;
-    const bool inS = __shfl_sync(0xffffffffu, (wS >> bitpos) & 1u, lane & 15);
-    const bool inB = __shfl_sync(0xffffffffu, (wB >> bitpos) & 1u, lane & 15);
-    const double side = __shfl_sync(0xffffffffu, pre, lane & 15);
+    if (qq == 0) {
+      xflag[par][grp][lane] = (uint8_t)(((wS >> bitpos) & 1u) | (((wB >> bitpos) & 1u) << 1));
+      xside[par][grp][lane] = pre;
+    }
     fetch(tile + gridDim.x);
     mbar_wait(&full[st], (uint32_t)((it / a.nstage) & 1));
     const double* T = stage0 + st * stage_elems + el;
     const double rh = T[roff];
-    // pass 1 on this lane's physical slots (x = gamma - rho, re-read from shared memory in
-    // pass 2: the registers hold the double-double row accumulators):
+    // pass 1 on this quarter's physical slots (x = gamma - rho; re-read in pass 2):
     //   sa = sum of the window slots, tr = sum_{s>=xoff} c_{s-xoff} x_s
     double sa = 0.0, tr = 0.0, sa2 = 0.0, tr2 = 0.0;
 #pragma unroll
-    for (int i = 0; i < SH; ++i) {
-      const int q = q0 + i;
-      if (q < qn) {
+    for (int i = 0; i < SQ; ++i) {
+      if (i < nq) {
+        const int q = q0 + i;
         const double xi = T[q * TILE] - rh;
         if (i & 1) {
           sa2 = fma(cA[q], xi, sa2);
@@ -204,11 +209,15 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
         }
       }
     }
-    sa += sa2;
-    tr += tr2;
-    // combine the two halves (a + b == b + a: both lanes of the pair get identical sums)
-    sa += __shfl_xor_sync(0xffffffffu, sa, 16);
-    tr += __shfl_xor_sync(0xffffffffu, tr, 16);
+    xsa[par][grp][qq][lane] = sa + sa2;
+    xtr[par][grp][qq][lane] = tr + tr2;
+    asm volatile("barrier.sync %0, %1;\n" ::"r"(1 + grp), "n"(32 * NQ) : "memory");  // thread 0 may lag (producer)
+    // the four quarters in a fixed order: every warp of the group gets identical sums
+    sa = ((xsa[par][grp][0][lane] + xsa[par][grp][1][lane]) + xsa[par][grp][2][lane]) + xsa[par][grp][3][lane];
+    tr = ((xtr[par][grp][0][lane] + xtr[par][grp][1][lane]) + xtr[par][grp][2][lane]) + xtr[par][grp][3][lane];
+    const uint8_t fl = xflag[par][grp][lane];
+    const bool inS = fl & 1, inB = fl & 2;
+    const double side = xside[par][grp][lane];
     // psi_prev and psi_cur differ from the window sum by one end slot each (when nU = w + 1)
     double sp = sa, sc = sa;
     if (xoff == 1) {
@@ -222,7 +231,7 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
       if (a.mode == MODE_FILL) {
         const double rec = (rh + sc * inv_w) + dev;
         gval = inS ? side : rec;
-        if (half == 0) {
+        if (qq == 0) {
           if (inS) {
             const double d = gval - rec;
             a.eps_elem[e] = d * d;
@@ -231,63 +240,63 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
         }
       } else if (a.mode == MODE_READ) {
         gval = side;
-      } else if (half == 0) {  // MODE_PROJ: residual of the projection (bootstrap indicator)
+      } else if (qq == 0) {  // MODE_PROJ: residual of the projection (bootstrap indicator)
         a.eps_elem[e] = dev * dev;
       }
     }
-    // pass 2: new Gram row on this lane's physical slots (band DOFs are added after the filter)
+    // pass 2: the new Gram row on this quarter's slots (band DOFs are added after the filter)
     if (GRAM && valid && !inB) {
       const double gr = gval - rh;
-      if (half == 0) biased_fma(acc_self, acc_selfl, gr, gr);
-      // h0 slots per half (uniform): for an odd slot count the last of half 1 is rho's slot,
-      // accumulated and discarded
+      if (qq == 0) biased_fma(acc_self, acc_selfl, gr, gr);
 #pragma unroll
-      for (int i = 0; i < SH; ++i)
-        if (i < h0) biased_fma(acc[i], accl[i], gr, T[(q0 + i) * TILE] - rh);
+      for (int i = 0; i < SQ; ++i)
+        if (i < nq) biased_fma(acc[i], accl[i], gr, T[(q0 + i) * TILE] - rh);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
   if constexpr (GRAM) {
-  // fixed-order reductions: the 16 lanes of each half (shuffle tree), then warps -> part[block][s]
+    // fixed-order reductions: the 32 lanes (shuffle tree), then the DOF groups -> part[block][s]
 #pragma unroll
-  for (int i = 0; i < SH; ++i) {
-    double v = acc[i] - bias, vl = accl[i];  // exact (Sterbenz)
-    for (int o = 8; o > 0; o >>= 1) {
-      const double oh = __shfl_xor_sync(0xffffffffu, v, o), ol = __shfl_xor_sync(0xffffffffu, vl, o);
-      dd_add(v, vl, oh, ol);
+    for (int i = 0; i < SQ; ++i) {
+      double v = acc[i] - bias, vl = accl[i];  // exact (Sterbenz)
+      for (int o = 16; o > 0; o >>= 1) {
+        const double oh = __shfl_xor_sync(0xffffffffu, v, o), ol = __shfl_xor_sync(0xffffffffu, vl, o);
+        dd_add(v, vl, oh, ol);
+      }
+      if (lane == 0) {
+        wred[warp][2 * i] = v;
+        wred[warp][2 * i + 1] = vl;
+      }
     }
-    if ((lane & 15) == 0) {
-      wred[warp][half * SH + i] = v;
-      wredl[warp][half * SH + i] = vl;
+    {
+      double v = acc_self - bias, vl = acc_selfl;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double oh = __shfl_xor_sync(0xffffffffu, v, o), ol = __shfl_xor_sync(0xffffffffu, vl, o);
+        dd_add(v, vl, oh, ol);
+      }
+      if (lane == 0) {
+        wred[warp][2 * SQ] = v;  // meaningful in quarter-0 warps only
+        wred[warp][2 * SQ + 1] = vl;
+      }
     }
-  }
-  {
-    double v = acc_self - bias, vl = acc_selfl;
-    for (int o = 16; o > 0; o >>= 1) {
-      const double oh = __shfl_xor_sync(0xffffffffu, v, o), ol = __shfl_xor_sync(0xffffffffu, vl, o);
-      dd_add(v, vl, oh, ol);
+    __syncthreads();
+    double* outp = a.part + (int64_t)blockIdx.x * (nU + 1) * 2;
+    for (int s2 = tid; s2 <= nU; s2 += FILL_THREADS) {
+      int qw, idx;  // quarter and accumulator index of the union slot s2
+      if (s2 == nU) {
+        qw = 0;
+        idx = SQ;
+      } else {
+        const int q = a.W.slot[s2];
+        qw = q / SQ;
+        idx = q - qw * SQ;
+      }
+      double v = 0.0, vl = 0.0;
+      for (int k = 0; k < NCW / NQ; ++k) dd_add(v, vl, wred[k * NQ + qw][2 * idx], wred[k * NQ + qw][2 * idx + 1]);
+      outp[2 * s2] = v;
+      outp[2 * s2 + 1] = vl;
     }
-    if (lane == 0) {
-      wred[warp][2 * SH] = v;
-      wredl[warp][2 * SH] = vl;
-    }
-  }
-  __syncthreads();
-  double* outp = a.part + (int64_t)blockIdx.x * (nU + 1) * 2;
-  for (int s = tid; s <= nU; s += 32 * NCW) {
-    int idx;
-    if (s == nU) {
-      idx = 2 * SH;
-    } else {
-      const int q = a.W.slot[s];
-      idx = (q < h0) ? q : SH + (q - h0);
-    }
-    double v = 0.0, vl = 0.0;
-    for (int k = 0; k < NCW; ++k) dd_add(v, vl, wred[k][idx], wredl[k][idx]);
-    outp[2 * s] = v;
-    outp[2 * s + 1] = vl;
-  }
   }
 }
 
@@ -395,13 +404,13 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef ou
   a.part = c->b.gpart;
   a.C = c->b.C;
   a.ldc = kMaxSlots;
-  const int sh = (c->nslots + 1) / 2;
-#define FILL_CASE(SH_)                                                                            \
-  if (sh <= SH_) return a.do_gram ? launch_fill_t<SH_, true>(c, a, smem) : launch_fill_t<SH_, false>(c, a, smem);
-  FILL_CASE(6) FILL_CASE(12) FILL_CASE(18) FILL_CASE(26) FILL_CASE(34)
+  const int sq = (c->nslots + NQ - 1) / NQ;
+#define FILL_CASE(SQ_)                                                                            \
+  if (sq <= SQ_) return a.do_gram ? launch_fill_t<SQ_, true>(c, a, smem) : launch_fill_t<SQ_, false>(c, a, smem);
+  FILL_CASE(3) FILL_CASE(6) FILL_CASE(9) FILL_CASE(13) FILL_CASE(17)
 #undef FILL_CASE
-  if (!a.do_gram && sh <= 50) return launch_fill_t<50, false>(c, a, smem);
-  if (!a.do_gram && sh <= 66) return launch_fill_t<66, false>(c, a, smem);
+  if (!a.do_gram && sq <= 25) return launch_fill_t<25, false>(c, a, smem);
+  if (!a.do_gram && sq <= 33) return launch_fill_t<33, false>(c, a, smem);
   return HROM_E_INVALID;  // wider windows use gram_mode = 1 (hrom_create enforces it)
 }
 
