@@ -758,7 +758,8 @@ void snap_apply(hrom_ctx* c, const HostSnap& post, int64_t dk, int64_t dlaunch) 
 // a step the graph path may capture / replay: Algorithm 1 in its steady state (a hybrid step
 // followed by the basis update and the sampling, z = infinity), no host-visible outputs
 bool graph_eligible(const hrom_ctx* c, int32_t* dev_count_out) {
-  return c->graph_on && !c->prof && dev_count_out == nullptr && c->P.full_period <= 0 && c->P.odeim_points == 0 &&
+  static const bool nocap = getenv("HROM_GRAPH_NOCAPTURE") != nullptr;  // debug: graph-mode order, eager launches
+  return c->graph_on && !nocap && !c->prof && dev_count_out == nullptr && c->P.full_period <= 0 && c->P.odeim_points == 0 &&
          c->P.gram_mode == 0 && c->P.gather_mode == 0 && c->k >= c->w + 1 && c->last_hybrid && c->sets_ready &&
          c->basis_ready && c->eig_todo && !c->basis_pending && !c->bg_pending && c->kinc_valid &&
          c->samples_since_gather == 1 && c->kinc_newest == c->k - 1 && c->smax_k == c->k && c->n_owed == 0 &&

@@ -28,7 +28,7 @@ namespace {
 
 constexpr int NQ = 4;            // slot quarters: four warps cooperate on the same 32 DOFs
 constexpr int NCW = NQ * TILE / 32;  // compute warps (16); thread 0 also issues the copies
-constexpr int FILL_STAGES = 2;   // slab-tile stages in shared memory
+constexpr int FILL_STAGES = 3;   // slab-tile stages in shared memory (at most; launch_fill_t)
 constexpr int FILL_THREADS = 32 * NCW;
 
 enum { MODE_FILL = 0, MODE_READ = 1, MODE_PROJ = 2 };
@@ -194,23 +194,20 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     const double rh = T[roff];
     // pass 1 on this quarter's physical slots (x = gamma - rho; re-read in pass 2):
     //   sa = sum of the window slots, tr = sum_{s>=xoff} c_{s-xoff} x_s
-    double sa = 0.0, tr = 0.0, sa2 = 0.0, tr2 = 0.0;
+    // four independent chains of each sum (fixed order: chain i & 3, then ((0 + 1) + (2 + 3)))
+    double sa4[4] = {0.0, 0.0, 0.0, 0.0}, tr4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int i = 0; i < SQ; ++i) {
       if (i < nq) {
         const int q = q0 + i;
         const double xi = T[q * TILE] - rh;
-        if (i & 1) {
-          sa2 = fma(cA[q], xi, sa2);
-          tr2 = fma(cX[q], xi, tr2);
-        } else {
-          sa = fma(cA[q], xi, sa);
-          tr = fma(cX[q], xi, tr);
-        }
+        sa4[i & 3] = fma(cA[q], xi, sa4[i & 3]);
+        tr4[i & 3] = fma(cX[q], xi, tr4[i & 3]);
       }
     }
-    xsa[par][grp][qq][lane] = sa + sa2;
-    xtr[par][grp][qq][lane] = tr + tr2;
+    xsa[par][grp][qq][lane] = (sa4[0] + sa4[1]) + (sa4[2] + sa4[3]);
+    xtr[par][grp][qq][lane] = (tr4[0] + tr4[1]) + (tr4[2] + tr4[3]);
+    double sa, tr;
     asm volatile("barrier.sync %0, %1;\n" ::"r"(1 + grp), "n"(32 * NQ) : "memory");  // thread 0 may lag (producer)
     // the four quarters in a fixed order: every warp of the group gets identical sums
     sa = ((xsa[par][grp][0][lane] + xsa[par][grp][1][lane]) + xsa[par][grp][2][lane]) + xsa[par][grp][3][lane];
@@ -365,8 +362,20 @@ __global__ void eps_all_kernel(Geo g, const double* __restrict__ eps_elem, doubl
 
 // out (rho or psi) = mean of the last w window slots
 
+// stages: as many slab tiles in flight as fit next to the kernel's static shared memory (3 at
+// w = 64: the producer can run a tile ahead of the slowest warp)
 template <int NU, bool GRAM>
-hrom_status launch_fill_t(hrom_ctx* c, const FillArgs& a, size_t smem) {
+hrom_status launch_fill_t(hrom_ctx* c, FillArgs a, size_t stage) {
+  cudaFuncAttributes fa{};
+  HROM_CK(cudaFuncGetAttributes(&fa, fill_kernel<NU, GRAM>));
+  int dev = 0, optin = 0;
+  HROM_CK(cudaGetDevice(&dev));
+  HROM_CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const size_t avail = (size_t)optin - fa.sharedSizeBytes;
+  a.nstage = FILL_STAGES;
+  while (a.nstage > 1 && a.nstage * (stage + 16) > avail) --a.nstage;
+  if (a.nstage * (stage + 16) > avail) return HROM_E_INVALID;
+  const size_t smem = a.nstage * stage + 2 * a.nstage * sizeof(uint64_t);
   HROM_CK(cudaFuncSetAttribute(fill_kernel<NU, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   fill_kernel<NU, GRAM><<<c->nsm, FILL_THREADS, smem, c->st>>>(a);
   HROM_LAUNCH_CK();
@@ -388,10 +397,7 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef ou
   a.mode = mode;
   a.do_gram = (mode != MODE_PROJ) && out_in_ring && c->P.gram_mode == 0 ? 1 : 0;
   const size_t stage = (size_t)c->g.nsr * TILE * sizeof(double);
-  a.nstage = FILL_STAGES;
-  while (a.nstage > 1 && a.nstage * stage > 216 * 1024) --a.nstage;  // wide windows (w = 128): one stage
-  if (a.nstage * stage > 216 * 1024) return HROM_E_INVALID;
-  const size_t smem = a.nstage * stage + 2 * a.nstage * sizeof(uint64_t);
+
   a.rho_slot = c->nslots;
   a.nslots = c->nslots;
   a.ring = c->b.ring;
@@ -406,11 +412,11 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef ou
   a.ldc = kMaxSlots;
   const int sq = (c->nslots + NQ - 1) / NQ;
 #define FILL_CASE(SQ_)                                                                            \
-  if (sq <= SQ_) return a.do_gram ? launch_fill_t<SQ_, true>(c, a, smem) : launch_fill_t<SQ_, false>(c, a, smem);
+  if (sq <= SQ_) return a.do_gram ? launch_fill_t<SQ_, true>(c, a, stage) : launch_fill_t<SQ_, false>(c, a, stage);
   FILL_CASE(3) FILL_CASE(6) FILL_CASE(9) FILL_CASE(13) FILL_CASE(17)
 #undef FILL_CASE
-  if (!a.do_gram && sq <= 25) return launch_fill_t<25, false>(c, a, smem);
-  if (!a.do_gram && sq <= 33) return launch_fill_t<33, false>(c, a, smem);
+  if (!a.do_gram && sq <= 25) return launch_fill_t<25, false>(c, a, stage);
+  if (!a.do_gram && sq <= 33) return launch_fill_t<33, false>(c, a, stage);
   return HROM_E_INVALID;  // wider windows use gram_mode = 1 (hrom_create enforces it)
 }
 
