@@ -68,4 +68,22 @@ __device__ __forceinline__ void dd_div1(double& hi, double& lo, double d) {
   lo = q2 - (hi - q);
 }
 
+// (hi, lo) += a * b with hi biased far above every partial sum and product (|hi| >= |a b|,
+// hi = B + S, B a power of two >= 2 max |S|): TwoProduct by FMA, then the exact Fast2Sum
+// (3 operations instead of TwoSum's 6); the value is (hi - B) + lo, hi - B exact (Sterbenz)
+__device__ __forceinline__ void biased_fma(double& hi, double& lo, double a, double b) {
+  const double p = a * b;
+  const double pe = fma(a, b, -p);
+  const double s = hi + p;
+  const double e = p - (s - hi);
+  hi = s;
+  lo += e + pe;
+}
+
+// bias for Gram entries of columns whose squared norms are at most cmax: every partial sum
+// |sum x_i x_j| <= ||x_i|| ||x_j|| stays below B / 2 with an 8x margin on the norms
+__device__ __forceinline__ double gram_bias(double cmax) {
+  return cmax > 0.0 ? ldexp(1.0, ilogb(256.0 * cmax) + 1) : 1.0;
+}
+
 }  // namespace hrom

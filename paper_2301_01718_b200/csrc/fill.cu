@@ -54,17 +54,6 @@ struct FillArgs {
   const unsigned long long* run_if;  // nullable: run only if *run_if != ~0 (escalated step)
 };
 
-// (hi, lo) += a * b with hi biased far above every partial sum and product (|hi| >= |a b|):
-// TwoProduct by FMA, then the exact Fast2Sum
-__device__ __forceinline__ void biased_fma(double& hi, double& lo, double a, double b) {
-  const double p = a * b;
-  const double pe = fma(a, b, -p);
-  const double s = hi + p;
-  const double e = p - (s - hi);
-  hi = s;
-  lo += e + pe;
-}
-
 // SQ: compile-time upper bound of the physical slots per quarter (ceil((w + 2) / 4)).
 // Warp w owns DOF group grp = w / 4 (32 DOFs, one per lane) and slot quarter qq = w % 4
 // (physical slots [qq SQ, qq SQ + SQ)): every shared-memory load of a warp reads 32 consecutive
@@ -78,7 +67,11 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   const int nU = a.W.nU, w = a.W.w, nsl = a.nslots;
   const int64_t nsr = a.g.nsr;
   double* stage0 = reinterpret_cast<double*>(smraw);
-  const size_t stage_elems = (size_t)nsr * TILE;
+  // a stage holds the nsr slab rows of a tile (one bulk copy) and zero rows up to NQ * SQ, so
+  // every quarter walks SQ rows without bounds tests (cA = cX = 0 there; its Gram accumulators
+  // for rows >= nslots are discarded)
+  const int srows = (int)(nsr > NQ * SQ ? nsr : NQ * SQ);
+  const size_t stage_elems = (size_t)srows * TILE;
   uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + a.nstage * stage_elems);
   uint64_t* empty = full + a.nstage;
   // per PHYSICAL slot p: in-window flag (cA) and coefficient c (cX)
@@ -94,6 +87,8 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   const Geo& g = a.g;
   const int xoff = nU - w;  // logical: psi_cur and X use slots >= xoff; psi_prev uses slots < w
   for (int q = tid; q < kMaxSlots + 2; q += FILL_THREADS) cA[q] = cX[q] = 0.0;
+  for (int st = 0; st < a.nstage; ++st)
+    for (int i = (int)nsr * TILE + tid; i < srows * TILE; i += FILL_THREADS) stage0[st * stage_elems + i] = 0.0;
   __syncthreads();
   for (int s2 = tid; s2 < nU; s2 += FILL_THREADS) {
     const int q = a.W.slot[s2];
@@ -114,12 +109,12 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     double mc = 0.0;
     if (GRAM && a.C)
       for (int s2 = 0; s2 < nU; ++s2) mc = fmax(mc, a.C[a.W.slot[s2] * (a.ldc + 1)]);
-    s_bias = mc > 0.0 ? ldexp(1.0, ilogb(256.0 * mc) + 1) : 1.0;
+    s_bias = gram_bias(mc);
   }
   __syncthreads();
   const int64_t ntiles = (g.D + TILE - 1) / TILE;
   const int64_t first = blockIdx.x;
-  const uint32_t tile_bytes = (uint32_t)(stage_elems * sizeof(double));
+  const uint32_t tile_bytes = (uint32_t)(nsr * TILE * sizeof(double));
 
   // producer role: thread 0 keeps FILL_STAGES slab tiles in flight, one bulk copy each
   auto issue = [&](int it2) {
@@ -127,7 +122,7 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     if (tile >= ntiles) return;
     const int st = it2 % a.nstage;
     mbar_expect(&full[st], tile_bytes);
-    bulk_g2s(stage0 + st * stage_elems, a.ring + tile * stage_elems, tile_bytes, &full[st]);
+    bulk_g2s(stage0 + st * stage_elems, a.ring + tile * nsr * TILE, tile_bytes, &full[st]);
   };
   if (tid == 0)
     for (int q = 0; q < a.nstage; ++q) issue(q);
@@ -135,7 +130,6 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   // ---------------- compute warps: DOF el = grp*32 + lane, physical slots [q0, q0 + SQ)
   const int el = grp * 32 + lane;
   const int q0 = qq * SQ;
-  const int nq = min(SQ, nsl - q0);  // real slots of this quarter (warp-uniform; may be <= 0)
   const int p_first = a.W.slot[0], p_last = a.W.slot[nU - 1];
   double csum = 0.0;
   for (int q = 0; q < nsl; ++q) csum += cX[q];
@@ -158,10 +152,11 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     wS = wB = 0;
     pre = 0.0;
     if (qq == 0 && tile < ntiles && e < g.D && a.mode != MODE_PROJ) {
-      const int64_t n = e % g.N;
-      const int i = (int)(n % g.nx), j = (int)(n / g.nx);
-      const int64_t wi = (int64_t)j * g.wpr + (i >> 5);
-      bitpos = i & 31;
+      // 32-bit unsigned index arithmetic (D < 2^31, hrom_create)
+      const unsigned n = (unsigned)e % (unsigned)g.N;
+      const unsigned i = n % (unsigned)g.nx, j = n / (unsigned)g.nx;
+      const unsigned wi = j * (unsigned)g.wpr + (i >> 5);
+      bitpos = (int)(i & 31);
       if (a.mode == MODE_FILL) {
         wS = a.mS[wi];
         if (a.mB) wB = a.mB[wi];
@@ -198,12 +193,10 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     double sa4[4] = {0.0, 0.0, 0.0, 0.0}, tr4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int i = 0; i < SQ; ++i) {
-      if (i < nq) {
-        const int q = q0 + i;
-        const double xi = T[q * TILE] - rh;
-        sa4[i & 3] = fma(cA[q], xi, sa4[i & 3]);
-        tr4[i & 3] = fma(cX[q], xi, tr4[i & 3]);
-      }
+      const int q = q0 + i;
+      const double xi = T[q * TILE] - rh;
+      sa4[i & 3] = fma(cA[q], xi, sa4[i & 3]);
+      tr4[i & 3] = fma(cX[q], xi, tr4[i & 3]);
     }
     xsa[par][grp][qq][lane] = (sa4[0] + sa4[1]) + (sa4[2] + sa4[3]);
     xtr[par][grp][qq][lane] = (tr4[0] + tr4[1]) + (tr4[2] + tr4[3]);
@@ -246,8 +239,7 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
       const double gr = gval - rh;
       if (qq == 0) biased_fma(acc_self, acc_selfl, gr, gr);
 #pragma unroll
-      for (int i = 0; i < SQ; ++i)
-        if (i < nq) biased_fma(acc[i], accl[i], gr, T[(q0 + i) * TILE] - rh);
+      for (int i = 0; i < SQ; ++i) biased_fma(acc[i], accl[i], gr, T[(q0 + i) * TILE] - rh);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
@@ -396,7 +388,7 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef ou
   a.W = W;
   a.mode = mode;
   a.do_gram = (mode != MODE_PROJ) && out_in_ring && c->P.gram_mode == 0 ? 1 : 0;
-  const size_t stage = (size_t)c->g.nsr * TILE * sizeof(double);
+  const int64_t sq_host = (c->nslots + NQ - 1) / NQ;  // stage rows padded to NQ * SQ (fill_kernel)
 
   a.rho_slot = c->nslots;
   a.nslots = c->nslots;
@@ -411,12 +403,16 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef ou
   a.C = c->b.C;
   a.ldc = kMaxSlots;
   const int sq = (c->nslots + NQ - 1) / NQ;
+  (void)sq_host;
+#define FILL_STAGE(SQ_) ((size_t)std::max<int64_t>(c->g.nsr, (int64_t)NQ * SQ_) * TILE * sizeof(double))
 #define FILL_CASE(SQ_)                                                                            \
-  if (sq <= SQ_) return a.do_gram ? launch_fill_t<SQ_, true>(c, a, stage) : launch_fill_t<SQ_, false>(c, a, stage);
+  if (sq <= SQ_)                                                                                  \
+    return a.do_gram ? launch_fill_t<SQ_, true>(c, a, FILL_STAGE(SQ_)) : launch_fill_t<SQ_, false>(c, a, FILL_STAGE(SQ_));
   FILL_CASE(3) FILL_CASE(6) FILL_CASE(9) FILL_CASE(13) FILL_CASE(17)
 #undef FILL_CASE
-  if (!a.do_gram && sq <= 25) return launch_fill_t<25, false>(c, a, stage);
-  if (!a.do_gram && sq <= 33) return launch_fill_t<33, false>(c, a, stage);
+  if (!a.do_gram && sq <= 25) return launch_fill_t<25, false>(c, a, FILL_STAGE(25));
+  if (!a.do_gram && sq <= 33) return launch_fill_t<33, false>(c, a, FILL_STAGE(33));
+#undef FILL_STAGE
   return HROM_E_INVALID;  // wider windows use gram_mode = 1 (hrom_create enforces it)
 }
 

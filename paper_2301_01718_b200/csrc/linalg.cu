@@ -742,8 +742,16 @@ template <int SPW, bool NEWCOL = true, bool BANDOUT = false>
 __global__ void __launch_bounds__(GV_T, 2) gemv_gather_kernel(Geo g, Win W, const double* __restrict__ ring,
                                                            const SRef rho, const int32_t* __restrict__ list,
                                                            const int32_t* __restrict__ count, const SRef src_b,
-                                                           double* __restrict__ vpart) {
+                                                           double* __restrict__ vpart, const double* __restrict__ C) {
   __shared__ double red[GV_W][2 * SPW + 1], redl[GV_W][2 * SPW + 1];
+  __shared__ double s_bias;
+  if (threadIdx.x == 0) {  // accumulator bias from the window Gram's diagonal (dd.cuh gram_bias)
+    double mc = 0.0;
+    for (int s2 = 0; s2 < W.nU; ++s2) mc = fmax(mc, C[W.slot[s2] * (kMaxSlots + 1)]);
+    s_bias = gram_bias(mc);
+  }
+  __syncthreads();
+  const double bias = s_bias;
   const int nU = W.nU, nS = *count;
   const int64_t total = (int64_t)nS * g.c;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -759,8 +767,11 @@ __global__ void __launch_bounds__(GV_T, 2) gemv_gather_kernel(Geo g, Win W, cons
   // gappy normal equations' Grams
   double an[SPW], ab[SPW], anl[SPW], abl[SPW];
 #pragma unroll
-  for (int j = 0; j < SPW; ++j) an[j] = ab[j] = anl[j] = abl[j] = 0.0;
-  double bb = 0.0, bbl = 0.0;
+  for (int j = 0; j < SPW; ++j) {
+    an[j] = ab[j] = bias;
+    anl[j] = abl[j] = 0.0;
+  }
+  double bb = bias, bbl = 0.0;
   const int64_t gstep = (int64_t)gridDim.x * 32 * GV_U;
   // the S-hat list entries of the next chunk are fetched one iteration ahead (the value loads
   // depend on them: without the prefetch every chunk pays two dependent memory latencies)
@@ -811,12 +822,18 @@ __global__ void __launch_bounds__(GV_T, 2) gemv_gather_kernel(Geo g, Win W, cons
 #pragma unroll
       for (int j = 0; j < SPW; ++j) {
         const double v = val[u][j] - r[u];
-        if (NEWCOL) dd_fma(an[j], anl[j], v, x);
-        dd_fma(ab[j], abl[j], v, y);
+        if (NEWCOL) biased_fma(an[j], anl[j], v, x);
+        biased_fma(ab[j], abl[j], v, y);
       }
-      if (warp == 0) dd_fma(bb, bbl, y, y);
+      if (warp == 0) biased_fma(bb, bbl, y, y);
     }
   }
+#pragma unroll
+  for (int j = 0; j < SPW; ++j) {  // remove the bias (exact)
+    an[j] -= bias;
+    ab[j] -= bias;
+  }
+  bb -= bias;
   auto wsum = [&](double& h, double& l) {
     for (int o = 16; o > 0; o >>= 1) {
       const double oh = __shfl_xor_sync(0xffffffffu, h, o), ol = __shfl_xor_sync(0xffffffffu, l, o);
@@ -2060,9 +2077,11 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
     const int gblocks = 2 * (c->basis_pending ? c->nsm - 1 : c->nsm);
     const int nv = 2 * a.W.nU + 1;
     if (a.W.nU <= 9 * GV_W)
-      gemv_gather_kernel<9><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b, c->b.vpart);
+      gemv_gather_kernel<9><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b, c->b.vpart,
+                                                         c->b.C);
     else
-      gemv_gather_kernel<17><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b, c->b.vpart);
+      gemv_gather_kernel<17><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b,
+                                                          c->b.vpart, c->b.C);
     HROM_LAUNCH_CK();
     double* v = c->b.vpart + (size_t)gblocks * nv * 2;
     vpart_reduce<<<(nv * GR_TPE + 255) / 256, 256, 0, c->st>>>(c->b.vpart, gblocks, nv, v);
@@ -2086,7 +2105,7 @@ hrom_status band_gram_rows(hrom_ctx* c, const Win& W, SRef v) {
   if (W.nU > 9 * GV_W) return HROM_E_INVALID;  // the fused row is limited to nU <= 68 anyway
   gemv_gather_kernel<9, false, true><<<c->band_blocks, GV_T, 0, c->st>>>(
       c->g, W, c->b.ring, c->rho_ref(), c->b.lists + (int64_t)L_B * c->g.N, c->b.counts + L_B, v,
-      c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1) * 2);
+      c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1) * 2, c->b.C);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;
