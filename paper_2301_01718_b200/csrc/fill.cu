@@ -131,6 +131,16 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   const int el = grp * 32 + lane;
   const int q0 = qq * SQ;
   const int p_first = a.W.slot[0], p_last = a.W.slot[nU - 1];
+  // physical rows of this quarter that are not window slots: padding rows (zero, >= nsr), the
+  // rho row (x = 0) and at most one dead snapshot slot (not in the union)
+  // (nU = w + 1: one dead slot; nU = w at the bootstrap: two)
+  int dead0 = -1, dead1 = -1;
+  for (int q = q0; q < min(q0 + SQ, nsl); ++q)
+    if (cA[q] == 0.0) {
+      if (dead0 < 0) dead0 = q;
+      else dead1 = q;
+    }
+  const int npad_q = max(0, min(q0 + SQ, srows) - max(q0, (int)nsr));
   double csum = 0.0;
   for (int q = 0; q < nsl; ++q) csum += cX[q];
   const double inv_w = 1.0 / (double)w;
@@ -143,7 +153,9 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     accl[i] = 0.0;
   }
   double acc_self = bias, acc_selfl = 0.0;
-  // per-DOF side data (mask words, HDM value / new column), fetched by quarter 0 one tile ahead
+  // per-DOF side data, fetched one tile ahead and spread over the quarters so that no warp of a
+  // group carries all of it: quarter 1 the S-hat / band mask bits, quarter 2 the HDM value (or
+  // the new column); quarter 0 writes gamma_k, quarter 3 the squared error
   uint32_t wS = 0, wB = 0;
   int bitpos = 0;
   double pre = 0.0;
@@ -151,19 +163,18 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     const int64_t e = tile * TILE + el;
     wS = wB = 0;
     pre = 0.0;
-    if (qq == 0 && tile < ntiles && e < g.D && a.mode != MODE_PROJ) {
+    if (tile >= ntiles || e >= g.D || a.mode == MODE_PROJ) return;
+    if (qq == 1 && a.mode == MODE_FILL) {
       // 32-bit unsigned index arithmetic (D < 2^31, hrom_create)
       const unsigned n = (unsigned)e % (unsigned)g.N;
       const unsigned i = n % (unsigned)g.nx, j = n / (unsigned)g.nx;
       const unsigned wi = j * (unsigned)g.wpr + (i >> 5);
       bitpos = (int)(i & 31);
-      if (a.mode == MODE_FILL) {
-        wS = a.mS[wi];
-        if (a.mB) wB = a.mB[wi];
-        pre = a.src_S.p[sidx(a.src_S, e)];  // read unconditionally; used on S-hat only
-      } else {
-        pre = a.out.p[sidx(a.out, e)];
-      }
+      wS = a.mS[wi];
+      if (a.mB) wB = a.mB[wi];
+    } else if (qq == 2) {
+      pre = a.mode == MODE_FILL ? a.src_S.p[sidx(a.src_S, e)]  // read unconditionally; used on S-hat only
+                                : a.out.p[sidx(a.out, e)];
     }
   };
   fetch(first);
@@ -179,10 +190,8 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     }
     const int64_t e = tile * TILE + el;
     const bool valid = e < g.D;
-    if (qq == 0) {
-      xflag[par][grp][lane] = (uint8_t)(((wS >> bitpos) & 1u) | (((wB >> bitpos) & 1u) << 1));
-      xside[par][grp][lane] = pre;
-    }
+    if (qq == 1) xflag[par][grp][lane] = (uint8_t)(((wS >> bitpos) & 1u) | (((wB >> bitpos) & 1u) << 1));
+    if (qq == 2) xside[par][grp][lane] = pre;
     fetch(tile + gridDim.x);
     mbar_wait(&full[st], (uint32_t)((it / a.nstage) & 1));
     const double* T = stage0 + st * stage_elems + el;
@@ -190,15 +199,21 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
     // pass 1 on this quarter's physical slots (x = gamma - rho; re-read in pass 2):
     //   sa = sum of the window slots, tr = sum_{s>=xoff} c_{s-xoff} x_s
     // four independent chains of each sum (fixed order: chain i & 3, then ((0 + 1) + (2 + 3)))
+    // every row of the quarter enters sa; rows outside the window are removed after the loop:
+    // rho's row contributes x = 0, each zero padding row -rho, the dead slot its own x
     double sa4[4] = {0.0, 0.0, 0.0, 0.0}, tr4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int i = 0; i < SQ; ++i) {
       const int q = q0 + i;
       const double xi = T[q * TILE] - rh;
-      sa4[i & 3] = fma(cA[q], xi, sa4[i & 3]);
+      sa4[i & 3] += xi;
       tr4[i & 3] = fma(cX[q], xi, tr4[i & 3]);
     }
-    xsa[par][grp][qq][lane] = (sa4[0] + sa4[1]) + (sa4[2] + sa4[3]);
+    double sq_ = (sa4[0] + sa4[1]) + (sa4[2] + sa4[3]);
+    if (npad_q) sq_ += npad_q * rh;
+    if (dead0 >= 0) sq_ -= T[dead0 * TILE] - rh;
+    if (dead1 >= 0) sq_ -= T[dead1 * TILE] - rh;
+    xsa[par][grp][qq][lane] = sq_;
     xtr[par][grp][qq][lane] = (tr4[0] + tr4[1]) + (tr4[2] + tr4[3]);
     double sa, tr;
     asm volatile("barrier.sync %0, %1;\n" ::"r"(1 + grp), "n"(32 * NQ) : "memory");  // thread 0 may lag (producer)
@@ -221,16 +236,14 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
       if (a.mode == MODE_FILL) {
         const double rec = (rh + sc * inv_w) + dev;
         gval = inS ? side : rec;
-        if (qq == 0) {
-          if (inS) {
-            const double d = gval - rec;
-            a.eps_elem[e] = d * d;
-          }
-          a.out.p[sidx(a.out, e)] = gval;
+        if (qq == 3 && inS) {
+          const double d = gval - rec;
+          a.eps_elem[e] = d * d;
         }
+        if (qq == 0) a.out.p[sidx(a.out, e)] = gval;
       } else if (a.mode == MODE_READ) {
         gval = side;
-      } else if (qq == 0) {  // MODE_PROJ: residual of the projection (bootstrap indicator)
+      } else if (qq == 3) {  // MODE_PROJ: residual of the projection (bootstrap indicator)
         a.eps_elem[e] = dev * dev;
       }
     }
