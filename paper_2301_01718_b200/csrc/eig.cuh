@@ -311,10 +311,16 @@ __device__ int sym_eig(double* A, int n, int ldn, const EigWork& W, int nvec_cap
         if (lane == 0) coef[i] = s;
       }
       __syncthreads();
-      for (int rr = tid; rr < n; rr += nt) {
-        double s = W.Z[rr * ldz + j];
-        for (int i = 0; i < j; ++i) s -= coef[i] * W.Z[rr * ldz + i];
-        W.Z[rr * ldz + j] = s;
+      // z_j -= sum_i coef_i z_i: NP consecutive threads per row split the i range (fixed order:
+      // strided partial sums, then a shuffle tree over the NP threads)
+      const int NP = nt >= 8 * n ? 8 : (nt >= 4 * n ? 4 : (nt >= 2 * n ? 2 : 1));
+      for (int base = 0; base < n * NP; base += nt) {
+        const int t = base + tid, rr = t / NP, part = t % NP;
+        double s = 0.0;
+        if (rr < n)
+          for (int i = part; i < j; i += NP) s += coef[i] * W.Z[rr * ldz + i];
+        for (int o = 1; o < NP; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (rr < n && part == 0) W.Z[rr * ldz + j] -= s;
       }
       __syncthreads();
     }
@@ -330,18 +336,43 @@ __device__ int sym_eig(double* A, int n, int ldn, const EigWork& W, int nvec_cap
     __syncthreads();
   }
   mark(3);
-  // ---- 4. back-transformation Z <- H_0 ... H_{n-3} Z: one warp per eigenvector, all reflectors
-  // applied with warp reductions only (the reflectors are read-only now: no block barriers) ----
-  for (int j = warp; j < nvec; j += nw) {
-    for (int k = n - 3; k >= 0; --k) {
-      const double tau = W.tau[k];
-      if (tau == 0.0) continue;  // uniform within the warp
-      const int m = n - k - 1;
-      double s = 0.0;
-      for (int i = lane; i < m; i += 32) s += (i == 0 ? 1.0 : A[(k + 1 + i) * ldn + k]) * W.Z[(k + 1 + i) * ldz + j];
-      s = eig_warp_sum(s) * tau;
-      for (int i = lane; i < m; i += 32) W.Z[(k + 1 + i) * ldz + j] -= (i == 0 ? 1.0 : A[(k + 1 + i) * ldn + k]) * s;
-      __syncwarp();
+  // ---- 4. back-transformation Z <- H_0 ... H_{n-3} Z: each warp owns a contiguous run of up to
+  // BT eigenvectors and applies every reflector to all of them at once (BT independent dot
+  // products and warp reductions in flight); the reflectors are read-only now: no block
+  // barriers ----
+  {
+    constexpr int BT = 8;
+    const int per = (nvec + nw - 1) / nw;
+    const int jend = min(nvec, (warp + 1) * per);
+    for (int j0 = warp * per; j0 < jend; j0 += BT) {
+      const int nb = min(BT, jend - j0);
+      for (int k = n - 3; k >= 0; --k) {
+        const double tau = W.tau[k];
+        if (tau == 0.0) continue;  // uniform within the warp
+        const int m = n - k - 1;
+        double sb[BT];
+#pragma unroll
+        for (int b = 0; b < BT; ++b) sb[b] = 0.0;
+        for (int i = lane; i < m; i += 32) {
+          const double v = i == 0 ? 1.0 : A[(k + 1 + i) * ldn + k];
+          const double* zr = W.Z + (k + 1 + i) * ldz + j0;
+#pragma unroll
+          for (int b = 0; b < BT; ++b)
+            if (b < nb) sb[b] += v * zr[b];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int b = 0; b < BT; ++b) sb[b] += __shfl_xor_sync(0xffffffffu, sb[b], o);
+        for (int i = lane; i < m; i += 32) {
+          const double v = i == 0 ? 1.0 : A[(k + 1 + i) * ldn + k];
+          double* zr = W.Z + (k + 1 + i) * ldz + j0;
+#pragma unroll
+          for (int b = 0; b < BT; ++b)
+            if (b < nb) zr[b] -= v * (sb[b] * tau);
+        }
+        __syncwarp();
+      }
     }
   }
   __syncthreads();
