@@ -82,11 +82,13 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   __shared__ uint8_t xflag[2][NCW / NQ][32];
   __shared__ double wred[NCW][2 * SQ + 2];  // end-of-kernel row reduction (hi, lo per slot)
   __shared__ double s_bias;
+  __shared__ int srel[FILL_STAGES];  // per stage: warps done with it
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = warp / NQ, qq = warp % NQ;
   const Geo& g = a.g;
   const int xoff = nU - w;  // logical: psi_cur and X use slots >= xoff; psi_prev uses slots < w
   for (int q = tid; q < kMaxSlots + 2; q += FILL_THREADS) cA[q] = cX[q] = 0.0;
+  if (tid < FILL_STAGES) srel[tid] = 0;
   for (int st = 0; st < a.nstage; ++st)
     for (int i = (int)nsr * TILE + tid; i < srows * TILE; i += FILL_THREADS) stage0[st * stage_elems + i] = 0.0;
   __syncthreads();
@@ -181,13 +183,7 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   int it = 0;
   for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
     const int st = it % a.nstage, par = it & 1;
-    if (tid == 0 && it >= 1) {
-      // the stage of tile it-1 is free once every warp released it: refill it with tile it-1+stages
-      const int pst = (it - 1) % a.nstage;
-      mbar_wait(&empty[pst], (uint32_t)(((it - 1) / a.nstage) & 1));
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      issue(it - 1 + a.nstage);
-    }
+
     const int64_t e = tile * TILE + el;
     const bool valid = e < g.D;
     if (qq == 1) xflag[par][grp][lane] = (uint8_t)(((wS >> bitpos) & 1u) | (((wB >> bitpos) & 1u) << 1));
@@ -254,8 +250,17 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
 #pragma unroll
       for (int i = 0; i < SQ; ++i) biased_fma(acc[i], accl[i], gr, T[(q0 + i) * TILE] - rh);
     }
+    // release the stage: the last warp to finish with it refills it with tile it + nstage (no
+    // thread ever blocks waiting for the others)
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&srel[st], 1) == NCW - 1) {
+        srel[st] = 0;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(it + a.nstage);
+      }
+    }
   }
   if constexpr (GRAM) {
     // fixed-order reductions: the 32 lanes (shuffle tree), then the DOF groups -> part[block][s]
