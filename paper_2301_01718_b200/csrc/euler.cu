@@ -311,24 +311,51 @@ __global__ void dt_finalize(const unsigned long long* smax, const unsigned long 
 // O11: lowest cell with rho <= 0 or p <= 0 (or NaN); fused with H1's max wave speed of the same
 // state (the next step's dt reads it instead of a second pass over the state)
 template <int DIM>
+// Positivity (O11) and the wave-speed maximum of the next dt (H1) in one pass.  The oracle's
+// divided forms (O7) are evaluated exactly only where they can matter: a cell is tested with
+// the division-free p rho = (gamma - 1)(E rho - |m|^2 / 2) (positive with a 1e-10 relative margin
+// => p > 0 in the exact form too) and its wave speed screened in fp32 (relative error < 1e-5);
+// the exact divided s is computed when the screen comes within 1e-3 of the thread's running
+// screened maximum (the cell that raised it was computed exactly, so no exact maximum is
+// missed), and the exact p whenever the margin test is inconclusive.  Same bad-cell latch and
+// maximum, bit for bit, at ~1/10 of the divisions.
 __global__ void __launch_bounds__(256) positivity_kernel(Geo g, const SRef q, unsigned long long* __restrict__ bad,
                                                          unsigned long long* __restrict__ smax,
                                                          const unsigned long long* __restrict__ run_if) {
   constexpr int C = DIM + 2;
   if (run_if && *run_if == ~0ull) return;
+  const double gm1 = g.gamma - 1.0;
   double m = 0.0;
+  float amax = 0.0f;  // running screened maximum (of cells not evaluated exactly, a lower bound)
+  const float frdx = (float)(g.pow2 ? g.rdx : 1.0 / g.dx), frdy = (float)(g.pow2 ? g.rdy : 1.0 / g.dy);
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N;
        n += (int64_t)gridDim.x * blockDim.x) {
     double U[C];
 #pragma unroll
     for (int v = 0; v < C; ++v) U[v] = q.p[sidx(q, v * g.N + n)];
-    // the divided forms of the CFL rule (O7): dt matches the oracle's bit for bit
-    const double p = pressure<DIM>(U, g.gamma - 1.0);
-    if (!(U[0] > 0.0) || !(p > 0.0)) atomicMin(bad, (unsigned long long)n);
-    const double cs = sqrt(g.gamma * p / U[0]);
-    double s = div_dx(g, fabs(U[1] / U[0]) + cs);
-    if (DIM == 2) s = s + div_dy(g, fabs(U[2] / U[0]) + cs);
-    if (!(s <= m)) m = s;  // NaN sticks
+    double m2 = U[1] * U[1];
+    if (DIM == 2) m2 += U[2] * U[2];
+    const double pr = gm1 * fma(U[C - 1], U[0], -0.5 * m2);  // ~ p rho
+    const bool sure = U[0] > 0.0 && pr > 1e-10 * gm1 * (fabs(U[C - 1]) * U[0] + 0.5 * m2);
+    float sa = 0.0f;
+    bool exact = !sure;
+    if (sure) {
+      const float rf = 1.0f / (float)U[0];
+      const float cf = sqrtf((float)(g.gamma * pr)) * rf;
+      sa = (fabsf((float)U[1]) * rf + cf) * frdx;
+      if (DIM == 2) sa += (fabsf((float)U[2]) * rf + cf) * frdy;
+      exact = !(sa < amax * 0.999f);  // NaN / inf: exact
+      if (sa > amax) amax = sa;
+    }
+    if (exact) {
+      // the divided forms of the CFL rule (O7): dt matches the oracle's bit for bit
+      const double p = pressure<DIM>(U, gm1);
+      if (!(U[0] > 0.0) || !(p > 0.0)) atomicMin(bad, (unsigned long long)n);
+      const double cs = sqrt(g.gamma * p / U[0]);
+      double sx = div_dx(g, fabs(U[1] / U[0]) + cs);
+      if (DIM == 2) sx = sx + div_dy(g, fabs(U[2] / U[0]) + cs);
+      if (!(sx <= m)) m = sx;  // NaN sticks
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     const double t = __shfl_xor_sync(0xffffffffu, m, o);

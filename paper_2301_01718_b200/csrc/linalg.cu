@@ -734,11 +734,14 @@ hrom_status launch_cross(hrom_ctx* c, XGArgs& a, int grid) {
 // S-hat GEMVs: v_new[i] = sum_r x_i x_new, v_b[i] = sum_r x_i b, bb = sum_r b^2 over the rows of
 // S-hat (x = slot - rho, b = src_b - rho).  Lanes own consecutive rows (one slot load per warp
 // instruction = 32 consecutive list DOFs, coalesced); warp w of the CTA owns slots w, w + 8, ...;
-// GV_U row chunks in flight per lane.  Per-CTA partials [blk][2 nU + 1], reduced in fixed order.
-constexpr int GV_T = 256, GV_W = GV_T / 32, GV_U = 1;
+// GV_U row chunks in flight per lane (1 with both product vectors, 2 for the band rows' one).
+// Per-CTA partials [blk][2 nU + 1], reduced in fixed order.
+constexpr int GV_T = 256, GV_W = GV_T / 32;
 // NEWCOL = false, BANDOUT = true: the seam-band part of the new window Gram row (H10): one
 // product vector b = gamma_k on the band rows, partials [blk][nU + 1] ([nU] = sum b^2).
-template <int SPW, bool NEWCOL = true, bool BANDOUT = false>
+// DD = false: plain fp64 accumulation (the gathered Gram of the gappy normal equations when
+// gather_precision = 1, G11; lo parts stay 0)
+template <int SPW, bool NEWCOL = true, bool BANDOUT = false, bool DD = true, int GV_U = NEWCOL ? 1 : 2>
 __global__ void __launch_bounds__(GV_T, 2) gemv_gather_kernel(Geo g, Win W, const double* __restrict__ ring,
                                                            const SRef rho, const int32_t* __restrict__ list,
                                                            const int32_t* __restrict__ count, const SRef src_b,
@@ -751,7 +754,7 @@ __global__ void __launch_bounds__(GV_T, 2) gemv_gather_kernel(Geo g, Win W, cons
     s_bias = gram_bias(mc);
   }
   __syncthreads();
-  const double bias = s_bias;
+  const double bias = DD ? s_bias : 0.0;
   const int nU = W.nU, nS = *count;
   const int64_t total = (int64_t)nS * g.c;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -822,10 +825,18 @@ __global__ void __launch_bounds__(GV_T, 2) gemv_gather_kernel(Geo g, Win W, cons
 #pragma unroll
       for (int j = 0; j < SPW; ++j) {
         const double v = val[u][j] - r[u];
-        if (NEWCOL) biased_fma(an[j], anl[j], v, x);
-        biased_fma(ab[j], abl[j], v, y);
+        if (DD) {
+          if (NEWCOL) biased_fma(an[j], anl[j], v, x);
+          biased_fma(ab[j], abl[j], v, y);
+        } else {
+          if (NEWCOL) an[j] = fma(v, x, an[j]);
+          ab[j] = fma(v, y, ab[j]);
+        }
       }
-      if (warp == 0) biased_fma(bb, bbl, y, y);
+      if (warp == 0) {
+        if (DD) biased_fma(bb, bbl, y, y);
+        else bb = fma(y, y, bb);
+      }
     }
   }
 #pragma unroll
@@ -2039,19 +2050,27 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   const int ncol = a.W.nU + 1;
   double* R = c->b.eigV;
   double* Rl = c->b.Rlo;
+  // gather_precision 1: the gathered Gram in fp64 (DMMA + FMA GEMVs, lo = 0), 0: double-double
+  static const bool g64 = getenv("HROM_GATHER_FP64") != nullptr;
+  const bool dd = !g64;
+  auto gram = [&](GGArgs& aa, double* hi, double* lo) -> hrom_status {
+    if (dd) return run_gather_gram_dd(c, aa, ncol, grid, hi, lo, ncol, nullptr);
+    HROM_CK(cudaMemsetAsync(lo, 0, (size_t)ncol * ncol * sizeof(double), c->st));
+    return run_gather_gram(c, aa, ncol, grid, hi, ncol, nullptr);
+  };
   if (c->P.odeim_points > 0) {  // gappy rows = the DOF rows of the ODEIM points (Eq. 8, 10)
     a.mode = 2;
     a.rowlist = c->b.orows;
     a.nrow2 = c->odeim_n;
     c->kinc_valid = false;
     c->samples_since_gather = 0;
-    return run_gather_gram_dd(c, a, ncol, grid, R, Rl, ncol, nullptr);
+    return gram(a, R, Rl);
   }
   const bool inc = c->P.gather_mode == 0 && c->kinc_valid && c->samples_since_gather == 1 && c->kinc_newest == c->k - 1 &&
                    c->kinc_rebase == c->rebase_k;
   hrom_status s;
   if (!inc) {
-    if ((s = run_gather_gram_dd(c, a, ncol, grid, R, Rl, ncol, nullptr)) != HROM_OK) return s;
+    if ((s = gram(a, R, Rl)) != HROM_OK) return s;
     if (c->P.gather_mode == 0) {
       kinc_update_kernel<<<1, 512, 0, c->st>>>(a.W, 1, nullptr, nullptr, nullptr, nullptr, nullptr, c->b.Khi, c->b.Klo,
                                                R, Rl);
@@ -2068,15 +2087,18 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
     GGArgs d = a;
     d.list = c->b.lists + (int64_t)L_ADD * c->g.N;
     d.count = c->b.counts + L_ADD;
-    if ((s = run_gather_gram_dd(c, d, ncol, grid, Rp, Rpl, ncol, nullptr)) != HROM_OK) return s;
+    if ((s = gram(d, Rp, Rpl)) != HROM_OK) return s;
     d.list = c->b.lists + (int64_t)L_REM * c->g.N;
     d.count = c->b.counts + L_REM;
-    if ((s = run_gather_gram_dd(c, d, ncol, grid, Rm, Rml, ncol, nullptr)) != HROM_OK) return s;
+    if ((s = gram(d, Rm, Rml)) != HROM_OK) return s;
     // GEMVs of the newest snapshot and of b over all S-hat rows
     // one wave (2 CTAs per SM); static split: avoid the eigen's SM
     const int gblocks = 2 * (c->basis_pending ? c->nsm - 1 : c->nsm);
     const int nv = 2 * a.W.nU + 1;
-    if (a.W.nU <= 9 * GV_W)
+    if (a.W.nU <= 9 * GV_W && !dd)
+      gemv_gather_kernel<9, true, false, false><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count,
+                                                                             src_b, c->b.vpart, c->b.C);
+    else if (a.W.nU <= 9 * GV_W)
       gemv_gather_kernel<9><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b, c->b.vpart,
                                                          c->b.C);
     else

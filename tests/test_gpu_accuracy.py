@@ -166,7 +166,7 @@ def test_fullsize_config4_replay_step(orc, inputs):
     wl = inputs.config(4)
     snaps = inputs.smooth_window(wl, wl.w + 1, seed=404, amp=0.03)
     S = (np.random.default_rng(404).random(wl.N) < wl.f).astype(np.uint8)
-    rec = replay(orc, inputs, wl, snaps, wl.w + 3, S)[0]
+    rec = replay(orc, inputs, wl, snaps, wl.w, S)[0]
     g, o, bar = rec["g"], rec["o"], rec["bar"]
     assert rel(g, o) <= bar, (rel(g, o), bar)
     assert maxerr(g, o) <= bar, (maxerr(g, o), bar)
