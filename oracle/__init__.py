@@ -16,7 +16,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
-_SOURCES = ["euler.cpp", "linalg.cpp", "sampling_filter.cpp", "driver.cpp"]
+_SOURCES = ["euler.cpp", "linalg.cpp", "sampling_filter.cpp", "driver.cpp", "implicit.cpp"]
 
 
 def build(force: bool = False) -> str:
@@ -101,6 +101,14 @@ def lib():
             "orc_run_dt": (C.c_double, [C.c_void_p]),
             "orc_run_filter_stats": (None, [C.c_void_p, P(C.c_int64), P(C.c_int32)]),
             "orc_run_set_window": (None, [C.c_void_p, i64, d, i32, u8]),
+            "orc_roe": (i32, [i32, i32, C.c_double, d, d, d]),
+            "orc_rhs2": (i32, [P(Grid), i32, d, d]),
+            "orc_bdf_residual": (None, [P(Grid), i32, i32, C.c_double, d, d, d, d]),
+            "orc_newton": (i32, [P(Grid), i32, i32, C.c_double, d, d, C.c_void_p, d, C.c_double, i32, d]),
+            "orc_seam_filter_implicit": (i64, [P(Grid), P(Params), i32, i32, C.c_double, d, d, d, u8, u8,
+                                               P(C.c_int32)]),
+            "orc_run_set_implicit": (None, [C.c_void_p, i32, C.c_double, C.c_double, i32, C.c_double, i32]),
+            "orc_run_implicit_stats": (None, [C.c_void_p, P(C.c_int32), P(C.c_int64)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -320,6 +328,58 @@ def seam_filter(wl, v, F, mask_S):
     return v, kept, list(sweeps)
 
 
+def roe(dim, axis, gamma, UL, UR):
+    UL, UR = _c(UL), _c(UR)
+    F = np.zeros(dim + 2)
+    rc = lib().orc_roe(dim, axis, gamma, _d(UL), _d(UR), _d(F))
+    if rc != 0:
+        raise ValueError("orc_roe: non-admissible Roe average")
+    return F
+
+
+def rhs2(wl, q, flux=1):
+    q = _c(q)
+    L = np.empty_like(q)
+    g = grid_of(wl)
+    lib().orc_rhs2(C.byref(g), flux, _d(q), _d(L))
+    return L
+
+
+def bdf_residual(wl, q, qm1, qm2, dt_, order=2, flux=1):
+    q, qm1 = _c(q), _c(qm1)
+    qm2 = _c(qm1 if qm2 is None else qm2)
+    R = np.empty_like(q)
+    g = grid_of(wl)
+    lib().orc_bdf_residual(C.byref(g), flux, order, dt_, _d(q), _d(qm1), _d(qm2), _d(R))
+    return R
+
+
+def newton(wl, q0, qm1, qm2, dt_, order=2, flux=1, mask=None, tol=1e-12, maxit=30):
+    """Newton-Krylov root of R_k (cells of mask; None: all).  Returns (q, iterations, stats)."""
+    q = _c(q0).copy()
+    qm1 = _c(qm1)
+    qm2 = _c(qm1 if qm2 is None else qm2)
+    m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+    st = np.zeros(2)
+    g = grid_of(wl)
+    its = lib().orc_newton(C.byref(g), flux, order, dt_, _d(qm1), _d(qm2),
+                           None if m is None else m.ctypes.data_as(C.c_void_p), _d(q), tol, maxit, _d(st))
+    return q, its, st
+
+
+def seam_filter_implicit(wl, v, qm1, qm2, mask_S, dt_, order=2, flux=1):
+    v = _c(v).copy()
+    qm1 = _c(qm1)
+    qm2 = _c(qm1 if qm2 is None else qm2)
+    m = np.ascontiguousarray(mask_S, dtype=np.uint8)
+    kept = np.zeros(wl.N, dtype=np.uint8)
+    sweeps = (C.c_int32 * 3)()
+    g, p = grid_of(wl), params_of(wl)
+    lib().orc_seam_filter_implicit(C.byref(g), C.byref(p), flux, order, dt_, _d(qm1), _d(qm2), _d(v),
+                                   _u8(m), _u8(kept), sweeps)
+    return v, kept, list(sweeps)
+
+
 class Run:
     """Algorithm 1 (explicit; z = wl.z, 0 = infinity) driver of the oracle."""
 
@@ -335,6 +395,16 @@ class Run:
             lib().orc_run_set_rre(self.h, float(wl.delta))
         if getattr(wl, "n_p", 0) > 0:
             lib().orc_run_set_odeim(self.h, int(wl.n_p))
+        if getattr(wl, "hdm", "explicit") == "implicit":
+            lib().orc_run_set_implicit(self.h, int(wl.flux), float(wl.dt), float(wl.eps_y), int(wl.j_max),
+                                       float(wl.newton_tol), int(wl.newton_maxit))
+
+    def implicit_stats(self):
+        """(J of the last step, total Newton iterations so far)."""
+        J = C.c_int32()
+        its = C.c_int64()
+        lib().orc_run_implicit_stats(self.h, C.byref(J), C.byref(its))
+        return J.value, its.value
 
     def __del__(self):
         h, self.h = getattr(self, "h", None), None

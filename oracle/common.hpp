@@ -58,4 +58,9 @@ void apply_q(const std::vector<std::vector<double>>& V, int64_t m, double* x);
 void apply_qt(const std::vector<std::vector<double>>& V, int64_t m, double* x);
 void jacobi_svd_square(double* B, int64_t m, int n, double* V, double* S);
 
+// implicit HDM function F_k(q) at cell n (implicit.cpp; NEXT-4); returns nonzero
+// when a Roe average was not admissible
+int implicit_Fk_cell(const Grid& G, int flux, int order, double dt, const double* q, const double* qm1,
+                     const double* qm2, int64_t n, double* F);
+
 }  // namespace orc

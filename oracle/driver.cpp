@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <deque>
+#include <limits>
 #include <vector>
 #include "common.hpp"
 
@@ -39,6 +40,13 @@ struct orc_run {
   double delta = 0.0;  // > 0: RRE-delta selection instead of the fraction f
   int32_t odeim_np = 0;  // > 0: S-hat = G u ODEIM points, gappy rows = the points' DOF rows (Eq. 8, 10)
   std::vector<int64_t> prow, prow_next;  // ODEIM DOF rows used by / chosen for the next step
+  // NEXT-4: the paper's implicit HDM (BDF2 + MUSCL/Roe, Newton-Krylov) with partial-HDM
+  // subiterations; fixed dt
+  int32_t imp = 0, flux = 1, jmax = 10, nmaxit = 30;
+  double imp_dt = 0.0, eps_y = 1e-4, ntol = 1e-12;
+  int32_t J_last = 0;
+  int64_t newton_its = 0;
+  int32_t imp_fail = 0;
   orc_run(const orc_grid* gg, const orc_params* pp) : g(*gg), p(*pp), G(gg) {}
 };
 
@@ -120,6 +128,119 @@ void projection_indicator(orc_run* R) {
   }
 }
 
+// the least-squares coordinates y = (P^T Phi)^+ P^T (v - psi) on the rows erows (Eq. 8)
+std::vector<double> gappy_y(const orc_run* R, const std::vector<int64_t>& erows, const double* v) {
+  const int64_t m = (int64_t)erows.size(), D = R->G.D;
+  const int reff = R->reff;
+  std::vector<double> A(m * (int64_t)reff), b(m), y(reff, 0.0);
+  for (int64_t row = 0; row < m; ++row) {
+    const int64_t e = erows[row];
+    b[row] = v[e] - R->psi[e];
+    for (int i = 0; i < reff; ++i) A[(int64_t)i * m + row] = R->Phi[(int64_t)i * D + e];
+  }
+  orc_lsq(A.data(), m, reff, b.data(), R->p.lsq_rel_cutoff, y.data());
+  return y;
+}
+
+// NEXT-4 hybrid step k (Algorithm 1 lines 7-14, with the subiterations of
+// P:317-343): the partial HDM on S-hat with S-tilde = Neighbors(S-hat) frozen (Eq. 6b,
+// P:238-245), y from the P rows (Eq. 8), S-tilde refreshed from psi + Phi y, until
+// ||y^(j+1) - y^(j)||_2 < eps_y or j = j_max (reading A41: the test needs two iterates, so
+// J >= 2 unless j_max = 1); then the fill, the indicator and the filter gated by
+// the implicit residual.  Returns 1, or -1 when a partial Newton solve failed.
+int implicit_hybrid(orc_run* R, int order, const double* qm1, const double* qm2, std::vector<double>& gam) {
+  const Grid& G = R->G;
+  const int64_t N = G.N, D = G.D;
+  const std::vector<uint8_t>& S = R->mask_next;
+  R->mask_used = S;
+  std::vector<uint8_t> dil(N), St(N);
+  orc_dilate_cross(&R->g, S.data(), R->p.h, dil.data());
+  for (int64_t n = 0; n < N; ++n) St[n] = (dil[n] && !S[n]) ? 1 : 0;
+  // working state: S-hat u S-tilde from gamma_{k-1} (Alg. 1 line 7); every other entry NaN,
+  // so a stencil that reaches past S-tilde shows up as a failed solve
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  std::vector<double> v(D, nan);
+  for (int64_t n = 0; n < N; ++n)
+    if (S[n] || St[n])
+      for (int c = 0; c < G.c; ++c) v[c * N + n] = qm1[c * N + n];
+  std::vector<int64_t> erows;
+  R->prow = R->prow_next;
+  if (R->odeim_np > 0) {
+    erows = R->prow;
+  } else {
+    for (int64_t n = 0; n < N; ++n)
+      if (S[n])
+        for (int c = 0; c < G.c; ++c) erows.push_back(c * N + n);
+  }
+  std::vector<double> y, yprev;
+  int J = 0;
+  for (int j = 1; j <= R->jmax; ++j) {
+    const int its = orc_newton(&R->g, R->flux, order, R->imp_dt, qm1, qm2, S.data(), v.data(), R->ntol,
+                               R->nmaxit, nullptr);
+    if (its < 0) return -1;
+    R->newton_its += its;
+    y = gappy_y(R, erows, v.data());
+    J = j;
+    if (j > 1) {
+      double d2 = 0.0;
+      for (size_t i = 0; i < y.size(); ++i) d2 += (y[i] - yprev[i]) * (y[i] - yprev[i]);
+      if (std::sqrt(d2) < R->eps_y) break;
+    }
+    if (j == R->jmax) break;
+    for (int64_t n = 0; n < N; ++n)
+      if (St[n]) {
+        double rec[4];
+        reconstruct(R, y, n, rec);
+        for (int c = 0; c < G.c; ++c) v[c * N + n] = rec[c];
+      }
+    yprev = y;
+  }
+  R->J_last = J;
+  R->y = y;
+  R->ny_last = R->reff;
+  std::fill(R->eps.begin(), R->eps.end(), 0.0);
+  for (int64_t n = 0; n < N; ++n) {
+    double rec[4];
+    reconstruct(R, y, n, rec);
+    if (S[n]) {
+      double e2 = 0.0;
+      for (int c = 0; c < G.c; ++c) {
+        gam[c * N + n] = v[c * N + n];
+        const double d = v[c * N + n] - rec[c];
+        e2 += d * d;
+      }
+      R->eps[n] = e2;
+    } else {
+      for (int c = 0; c < G.c; ++c) gam[c * N + n] = rec[c];
+    }
+  }
+  std::vector<uint8_t> kept(N, 0);
+  R->kept = orc_seam_filter_implicit(&R->g, &R->p, R->flux, order, R->imp_dt, qm1, qm2, gam.data(), S.data(),
+                                     kept.data(), R->sweeps);
+  for (int64_t n = 0; n < N; ++n)
+    if (kept[n]) {
+      double rec[4];
+      reconstruct(R, y, n, rec);
+      double e2 = 0.0;
+      for (int c = 0; c < G.c; ++c) {
+        const double d = gam[c * N + n] - rec[c];
+        e2 += d * d;
+      }
+      R->eps[n] = e2;
+    }
+  return 1;
+}
+
+// full implicit HDM step (Alg. 1 line 4): Newton from gamma_{k-1}; -1 on failure
+int implicit_full(orc_run* R, int order, const double* qm1, const double* qm2, std::vector<double>& gam) {
+  std::copy(qm1, qm1 + R->G.D, gam.begin());
+  const int its = orc_newton(&R->g, R->flux, order, R->imp_dt, qm1, qm2, nullptr, gam.data(), R->ntol,
+                             R->nmaxit, nullptr);
+  if (its < 0) return -1;
+  R->newton_its += its;
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -141,9 +262,27 @@ int32_t orc_run_step(orc_run* R, double dt_override) {
   const int64_t N = G.N, D = G.D;
   const int64_t k = R->k + 1;
   const std::vector<double>& prev = R->snaps.back();
-  R->dt = (dt_override > 0.0) ? dt_override : orc_dt(&R->g, prev.data());
   std::vector<double> gam(D);
   int32_t kind = 0;
+  if (R->imp) {
+    // NEXT-4: BDF1 at k = 1, BDF2 afterwards (A39); fixed dt
+    R->dt = R->imp_dt;
+    const int order = (k == 1 || R->snaps.size() < 2) ? 1 : 2;
+    const double* qm1 = prev.data();
+    const double* qm2 = order == 2 ? R->snaps[R->snaps.size() - 2].data() : prev.data();
+    R->J_last = 0;
+    if (k + 1 <= w || (R->z > 0 && k % R->z == 0)) {
+      std::fill(R->mask_used.begin(), R->mask_used.end(), 1);
+      if (implicit_full(R, order, qm1, qm2, gam) < 0) { R->imp_fail = 1; return -1; }
+    } else {
+      kind = implicit_hybrid(R, order, qm1, qm2, gam);
+      if (kind < 0 || orc_positivity(&R->g, gam.data()) >= 0) {  // escalation
+        if (implicit_full(R, order, qm1, qm2, gam) < 0) { R->imp_fail = 1; return -1; }
+        kind = 2;
+      }
+    }
+  } else {
+  R->dt = (dt_override > 0.0) ? dt_override : orc_dt(&R->g, prev.data());
   if (k + 1 <= w || (R->z > 0 && k % R->z == 0)) {
     orc_full_step(&R->g, prev.data(), R->dt, gam.data());
     std::fill(R->mask_used.begin(), R->mask_used.end(), 1);
@@ -215,6 +354,7 @@ int32_t orc_run_step(orc_run* R, double dt_override) {
       kind = 2;
     }
   }
+  }  // explicit
   R->snaps.push_back(std::move(gam));
   while ((int)R->snaps.size() > w + 1) R->snaps.pop_front();
   R->k = k;
@@ -244,6 +384,20 @@ int32_t orc_run_step(orc_run* R, double dt_override) {
 void orc_run_set_full_period(orc_run* R, int32_t z) { R->z = z; }
 void orc_run_set_rre(orc_run* R, double delta) { R->delta = delta; }
 void orc_run_set_odeim(orc_run* R, int32_t n_p) { R->odeim_np = n_p; }
+void orc_run_set_implicit(orc_run* R, int32_t flux, double dt, double eps_y, int32_t j_max, double newton_tol,
+                          int32_t newton_maxit) {
+  R->imp = 1;
+  R->flux = flux;
+  R->imp_dt = dt;
+  R->eps_y = eps_y;
+  R->jmax = j_max;
+  R->ntol = newton_tol;
+  R->nmaxit = newton_maxit;
+}
+void orc_run_implicit_stats(const orc_run* R, int32_t* J_last, int64_t* newton_its) {
+  *J_last = R->J_last;
+  *newton_its = R->newton_its;
+}
 int32_t orc_run_points(const orc_run* R, int64_t* rows) {
   std::copy(R->prow_next.begin(), R->prow_next.end(), rows);
   return (int32_t)R->prow_next.size();

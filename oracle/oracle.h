@@ -131,6 +131,26 @@ void orc_run_filter_stats(const orc_run* R, int64_t* kept, int32_t* sweeps);
 void orc_run_set_window(orc_run* R, int64_t k, const double* snaps, int32_t nsnaps,
                         const uint8_t* mask_next);
 
+/* ---- NEXT-4: the paper's implicit HDM (implicit.cpp) ----
+ * Roe flux, walls (bc = 2), BDF1/BDF2, R_k(q) = q - F_k(q)
+ * by Newton-Krylov, partial HDM on S-hat with S-tilde frozen (Eq. 6b,
+ * P:238-245), subiterations. */
+int32_t orc_roe(int32_t dim, int32_t axis, double gamma, const double* UL, const double* UR, double* F);
+int32_t orc_rhs2(const orc_grid* g, int32_t flux, const double* q, double* L); /* flux 0 Rusanov, 1 Roe */
+void orc_bdf_residual(const orc_grid* g, int32_t flux, int32_t order, double dt, const double* q,
+                      const double* qm1, const double* qm2, double* R);
+int32_t orc_newton(const orc_grid* g, int32_t flux, int32_t order, double dt, const double* qm1,
+                   const double* qm2, const uint8_t* mask, double* q, double tol, int32_t maxit,
+                   double* stats);
+int64_t orc_seam_filter_implicit(const orc_grid* g, const orc_params* p, int32_t flux, int32_t order,
+                                 double dt, const double* qm1, const double* qm2, double* v,
+                                 const uint8_t* mask_S, uint8_t* kept_out, int32_t* sweeps_out);
+/* Algorithm 1 with the implicit HDM: fixed dt, eps_y / j_max of P:336-340, Newton tolerance
+ * on ||R||_inf.  orc_run_step then returns -1 if a full Newton solve failed. */
+void orc_run_set_implicit(orc_run* R, int32_t flux, double dt, double eps_y, int32_t j_max, double newton_tol,
+                          int32_t newton_maxit);
+void orc_run_implicit_stats(const orc_run* R, int32_t* J_last, int64_t* newton_its);
+
 #ifdef __cplusplus
 }
 #endif

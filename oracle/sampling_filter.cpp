@@ -241,9 +241,17 @@ void orc_shapiro_1d(const double* line, int32_t n, int32_t order, int32_t period
   }
 }
 
-// H7 / O13 seam filter (readings A21-A24).
-int64_t orc_seam_filter(const orc_grid* g, const orc_params* p, double* v, const double* F,
-                        const uint8_t* mask_S, uint8_t* kept_out, int32_t* sweeps_out) {
+}  // extern "C"
+
+namespace {
+
+// H7 / O13 seam filter (readings A21-A24).  Fcell(state, n, F4) gives the HDM
+// function F_k at cell n for the given state: the explicit path's F does not depend on the
+// state (the full RK3 map of gamma_{k-1}, A22); the implicit path's F_k(v) does (NEXT-4,
+// P:179-189), so the residual v - F_k(v) is re-evaluated on the filtered candidate.
+template <class FC>
+int64_t seam_filter_impl(const orc_grid* g, const orc_params* p, double* v, const uint8_t* mask_S,
+                         uint8_t* kept_out, int32_t* sweeps_out, const FC& Fcell) {
   Grid G(g);
   std::vector<uint8_t> sq(G.N), B(G.N), kept(G.N, 0);
   orc_dilate_square(g, mask_S, p->W, sq.data());
@@ -290,13 +298,20 @@ int64_t orc_seam_filter(const orc_grid* g, const orc_params* p, double* v, const
       // otherwise decide the sweep count)
       int64_t nkept = 0;
       double maxdec = 0.0;
-      for (int64_t n : band) {
+      // (all residuals of the sweep are evaluated before v changes)
+      std::vector<double> Fo((size_t)band.size() * G.c), Fn((size_t)band.size() * G.c);
+      for (size_t b = 0; b < band.size(); ++b) {
+        Fcell(v, band[b], &Fo[b * G.c]);
+        Fcell(vpp.data(), band[b], &Fn[b * G.c]);
+      }
+      for (size_t b = 0; b < band.size(); ++b) {
+        const int64_t n = band[b];
         double rold = 0.0, rnew = 0.0, fs = 0.0;
         for (int var = 0; var < G.c; ++var) {
           const int64_t e = var * G.N + n;
-          rold = std::max(rold, std::fabs(v[e] - F[e]));
-          rnew = std::max(rnew, std::fabs(vpp[e] - F[e]));
-          fs = std::max(fs, std::fabs(F[e]));
+          rold = std::max(rold, std::fabs(v[e] - Fo[b * G.c + var]));
+          rnew = std::max(rnew, std::fabs(vpp[e] - Fn[b * G.c + var]));
+          fs = std::max(fs, std::fabs(Fo[b * G.c + var]));
         }
         if (rnew < rold) {
           ++nkept;
@@ -316,6 +331,30 @@ int64_t orc_seam_filter(const orc_grid* g, const orc_params* p, double* v, const
     total += kept[n];
   }
   return total;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t orc_seam_filter(const orc_grid* g, const orc_params* p, double* v, const double* F,
+                        const uint8_t* mask_S, uint8_t* kept_out, int32_t* sweeps_out) {
+  Grid G(g);
+  auto Fcell = [&](const double*, int64_t n, double* F4) {
+    for (int var = 0; var < G.c; ++var) F4[var] = F[var * G.N + n];
+  };
+  return seam_filter_impl(g, p, v, mask_S, kept_out, sweeps_out, Fcell);
+}
+
+// the same filter gated by the implicit residual v - F_k(v) (NEXT-4; P:419-432 with Eq. hdm)
+int64_t orc_seam_filter_implicit(const orc_grid* g, const orc_params* p, int32_t flux, int32_t order,
+                                 double dt, const double* qm1, const double* qm2, double* v,
+                                 const uint8_t* mask_S, uint8_t* kept_out, int32_t* sweeps_out) {
+  Grid G(g);
+  auto Fcell = [&](const double* state, int64_t n, double* F4) {
+    implicit_Fk_cell(G, flux, order, dt, state, qm1, qm2, n, F4);
+  };
+  return seam_filter_impl(g, p, v, mask_S, kept_out, sweeps_out, Fcell);
 }
 
 }  // extern "C"

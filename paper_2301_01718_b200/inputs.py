@@ -99,6 +99,15 @@ class Workload:
     z: int = 0             # full-HDM period of Algorithm 1; 0 = infinity (A20)
     delta: float = 0.0     # > 0: RRE-delta selection instead of the fraction f
     n_p: int = 0           # > 0: ODEIM points added to S-hat; gappy rows = their DOF rows
+    # NEXT-4, the paper's implicit HDM: BDF2 + MUSCL/Roe by Newton-Krylov with
+    # partial-HDM subiterations; fixed time step dt
+    hdm: str = "explicit"  # "explicit" (SSP-RK3, BASELINE configs) or "implicit"
+    flux: int = 0          # 0 Rusanov (BASELINE, A2), 1 Roe
+    dt: float = 0.0        # fixed step of the implicit HDM
+    eps_y: float = 1e-4    # subiteration tolerance on ||y^(j+1) - y^(j)||_2
+    j_max: int = 10        # maximum subiterations
+    newton_tol: float = 1e-12   # Newton stop on ||R_k||_inf (reading A40)
+    newton_maxit: int = 30
 
     @property
     def c(self) -> int:
@@ -170,6 +179,25 @@ def config(idx: int, **overrides) -> Workload:
     return dataclasses.replace(wl, **overrides)
 
 
+def preset(name: str, **overrides) -> Workload:
+    """The paper's own experiments (NEXT-4): Sod's shock tube (N = 499, N_t = 999 on
+    (0, 0.2), w = 5, m = 4, delta = 0.80, filters 2-4-6) and the model implosion (P:906-921:
+    100 x 100 on (0, 0.3)^2, walls, N_t = 1650 on (0, 0.5), z = 7, delta = 0.90, w = 6, m = 4),
+    implicit BDF2 + MUSCL/Roe HDM.  n_p (never printed by the paper): S:296 defaults 2m = 8
+    for Sod and 23 for the implosion (p-bar = 0.23 % of 10 000 cells).  The filter acts on
+    the whole hybrid state (W = -1, reading G9)."""
+    if name == "sod":
+        wl = Workload("next4-sod-499", dim=1, nx=499, ny=1, bc=0, recon=2, steps=999, w=5, r=4,
+                      f=0.1, h=2, W=-1, delta=0.80, n_p=8, hdm="implicit", flux=1, dt=0.2 / 999)
+    elif name == "implosion":
+        wl = Workload("next4-implosion-100", dim=2, nx=100, ny=100, x1=0.3, y1=0.3, bc=2, recon=2,
+                      steps=1650, w=6, r=4, f=0.1, h=2, W=-1, z=7, delta=0.90, n_p=23,
+                      hdm="implicit", flux=1, dt=0.5 / 1650)
+    else:
+        raise ValueError(f"no preset {name}")
+    return dataclasses.replace(wl, **overrides)
+
+
 def initial_condition(wl: Workload, kind: Optional[str] = None) -> np.ndarray:
     """Seeded IC of a workload as SoA conservative (c, N) float64.
 
@@ -178,6 +206,10 @@ def initial_condition(wl: Workload, kind: Optional[str] = None) -> np.ndarray:
     if kind is None:
         kind = {"config1": "sod", "config2": "quadrant", "config3": "randquad",
                 "config4": "blasts", "config5": "blasts"}.get(wl.name.split("-")[0], "blasts")
+        if wl.name.startswith("next4-sod"):
+            kind = "sod_clean"
+        elif wl.name.startswith("next4-implosion"):
+            kind = "implosion"
     X, Y = wl.cell_centres()
     N = wl.N
     g = wl.gamma
@@ -232,6 +264,13 @@ def initial_condition(wl: Workload, kind: Optional[str] = None) -> np.ndarray:
             best = np.where(inside, np.maximum(best, Pi[b]), best)
         p = np.where(best > 0, best, 1.0)
         rho = np.where(best > 0, best ** (1.0 / g), 1.0)
+        zero = np.zeros(N)
+        return primitive_to_conservative(2, g, rho, zero, zero, p)
+    if kind == "implosion":
+        # rho, p = 0.125, 0.14 inside D = {x_1 + x_2 <= 0.15}, 1, 1 outside, u = 0
+        inside = (X + Y) <= 0.15
+        rho = np.where(inside, 0.125, 1.0)
+        p = np.where(inside, 0.14, 1.0)
         zero = np.zeros(N)
         return primitive_to_conservative(2, g, rho, zero, zero, p)
     if kind == "uniform":
