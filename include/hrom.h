@@ -250,6 +250,66 @@ hrom_status hrom_debug_counters(hrom_ctx* ctx, int32_t* any_out, int32_t n);
  * sets kernel [40 + phase]; LSQ solve [64 + phase] (only while profiling is enabled). */
 hrom_status hrom_debug_timers(hrom_ctx* ctx, int64_t* host_out, int32_t n);
 
+/* ==== NEXT-4: Algorithm 1 with the paper's own implicit HDM ====
+ * HDM: R_k(q) = q - F_k(q) = 0, F_k(q) = dt beta f*(q) - sum_{j<s} a_j q_{k-s+j},
+ * BDF2 (a = 1/3, -4/3, 1; beta = 2/3) started by BDF1 at k = 1 (reading A39),
+ * f*: MUSCL-minmod + Roe (no entropy fix, A37) or Rusanov; walls (bc = 2: ghosts
+ * mirror the interior with the normal momentum negated, A38).  Solved by Newton-Krylov:
+ * GMRES(30) on exact Jacobian-vector products (forward-mode dual numbers), backtracking line
+ * search, stop at ||R_k||_inf <= newton_tol (reading A40).  A hybrid step solves the partial
+ * HDM on S-hat with S-tilde = Neighbors(S-hat) frozen (Eq. 6b) and iterates it
+ * with the gappy coordinates: y^(j) = (P^T Phi)^+ P^T (v^(j) - psi), S-tilde :=
+ * psi + Phi y^(j), until ||y^(j) - y^(j-1)||_2 < eps_y (j >= 2) or j = j_max (reading A41);
+ * then the fill and the spatial filter gated by v - F_k(v).  Window, POD,
+ * RRE-delta / fraction sampling, ODEIM points and the schedule z are those of hrom_params.
+ * Steps synchronise the stream once per subiteration (the eps_y test is a host decision). */
+typedef struct hrom_imp_ctx hrom_imp_ctx;
+typedef struct {
+  int32_t flux;          /* 0 Rusanov (BASELINE), 1 Roe */
+  double dt;             /* fixed time step */
+  double eps_y;          /* subiteration tolerance (1e-4) */
+  int32_t j_max;         /* maximum subiterations (10) */
+  double newton_tol;     /* ||R_k||_inf stop of the Newton solves */
+  int32_t newton_maxit;  /* Newton iterations before a solve counts as failed */
+} hrom_imp_params;
+/* grid->bc in {0, 1, 2 = walls}; params: window, rank, halo (>= stencil radius), band (-1: the
+ * whole hybrid state off S-hat, the paper's filter domain), filter, cutoffs, sample_mode /
+ * sample_fraction / rre_delta, odeim_points, full_period (z).  HROM_E_INVALID on bad values. */
+hrom_status hrom_imp_create(const hrom_grid* grid, double gamma, const hrom_params* params,
+                            const hrom_imp_params* imp, void* cuda_stream, hrom_imp_ctx** out);
+void hrom_imp_destroy(hrom_imp_ctx* ctx);
+hrom_status hrom_imp_set_state(hrom_imp_ctx* ctx, const double* any_q);  /* gamma_0, k = 0 */
+hrom_status hrom_imp_get_state(hrom_imp_ctx* ctx, double* any_q);        /* gamma_k */
+/* One step of Algorithm 1: full implicit HDM when k+1 <= w or k mod z = 0, else the
+ * partial HDM with subiterations; then the basis update and sampling as hrom_step.  A failed
+ * partial Newton solve or a non-physical hybrid state escalates to a full solve;
+ * a failed full solve returns HROM_E_POSITIVITY.  dev_count_out (nullable): |S-hat| used. */
+hrom_status hrom_imp_step(hrom_imp_ctx* ctx, int32_t* dev_count_out);
+/* host_out[5]: kind of the last step (0 full, 1 hybrid, 2 escalated), J (subiterations), Newton
+ * iterations, GMRES products, ODEIM points used (p-bar) */
+hrom_status hrom_imp_stats(hrom_imp_ctx* ctx, int32_t* host_out);
+hrom_status hrom_imp_get_mask(hrom_imp_ctx* ctx, uint32_t* any_mask);      /* S-hat_{k+1} bitmap */
+hrom_status hrom_imp_get_indicator(hrom_imp_ctx* ctx, double* any_eps);   /* N values */
+hrom_status hrom_imp_get_y(hrom_imp_ctx* ctx, double* any_y);
+int64_t hrom_imp_mask_words(const hrom_imp_ctx* ctx);
+int32_t hrom_imp_effective_rank(hrom_imp_ctx* ctx);
+hrom_status hrom_imp_sync(hrom_imp_ctx* ctx);
+/* standalone pieces (device pointers, D values each; order 1 or 2, qm2 unused for order 1):
+ * R_k on every cell; the Newton-Krylov root on the cells of dev_mask (NULL: all) with dev_q the
+ * initial guess and the frozen data (host_iters: iterations, HROM_E_POSITIVITY if it failed);
+ * the filter of dev_v on the band of dev_mask gated by the implicit residual (host_sweeps[3]). */
+hrom_status hrom_imp_residual(hrom_imp_ctx* ctx, int32_t order, const double* dev_q, const double* dev_qm1,
+                              const double* dev_qm2, double* dev_R);
+hrom_status hrom_imp_newton(hrom_imp_ctx* ctx, int32_t order, const double* dev_qm1, const double* dev_qm2,
+                            const uint32_t* dev_mask, double* dev_q, int32_t* host_iters);
+hrom_status hrom_imp_filter(hrom_imp_ctx* ctx, int32_t order, const double* dev_qm1, const double* dev_qm2,
+                            const uint32_t* dev_mask, double* dev_v, uint8_t* dev_kept_out, int32_t* host_sweeps);
+/* the filter band of the current sets (ascending cells; N int32 + count) */
+hrom_status hrom_imp_get_band(hrom_imp_ctx* ctx, int32_t* any_list, int32_t* any_count);
+/* replay hook: window gamma_{k-w}..gamma_k (w+1, oldest first) and S-hat_{k+1} (as hrom_set_window) */
+hrom_status hrom_imp_set_window(hrom_imp_ctx* ctx, int64_t k, const double* any_snaps, int32_t nsnaps,
+                                const uint32_t* any_mask_next);
+
 #ifdef __cplusplus
 }
 #endif

@@ -42,6 +42,11 @@ class Params(C.Structure):
                 ("sample_mode", C.c_int32), ("rre_delta", C.c_double), ("odeim_points", C.c_int32)]
 
 
+class ImpParams(C.Structure):
+    _fields_ = [("flux", C.c_int32), ("dt", C.c_double), ("eps_y", C.c_double), ("j_max", C.c_int32),
+                ("newton_tol", C.c_double), ("newton_maxit", C.c_int32)]
+
+
 # every entry point of include/hrom.h with its ctypes signature
 _VP = C.c_void_p
 _SIGS = {
@@ -86,6 +91,24 @@ _SIGS = {
     "hrom_launch_count": (C.c_int64, [_VP]),
     "hrom_debug_counters": (C.c_int, [_VP, _VP, C.c_int32]),
     "hrom_debug_timers": (C.c_int, [_VP, _VP, C.c_int32]),
+    "hrom_imp_create": (C.c_int, [C.POINTER(Grid), C.c_double, C.POINTER(Params), C.POINTER(ImpParams), _VP,
+                                  C.POINTER(_VP)]),
+    "hrom_imp_destroy": (None, [_VP]),
+    "hrom_imp_set_state": (C.c_int, [_VP, _VP]),
+    "hrom_imp_get_state": (C.c_int, [_VP, _VP]),
+    "hrom_imp_step": (C.c_int, [_VP, _VP]),
+    "hrom_imp_stats": (C.c_int, [_VP, _VP]),
+    "hrom_imp_get_mask": (C.c_int, [_VP, _VP]),
+    "hrom_imp_get_indicator": (C.c_int, [_VP, _VP]),
+    "hrom_imp_get_y": (C.c_int, [_VP, _VP]),
+    "hrom_imp_mask_words": (C.c_int64, [_VP]),
+    "hrom_imp_effective_rank": (C.c_int32, [_VP]),
+    "hrom_imp_sync": (C.c_int, [_VP]),
+    "hrom_imp_residual": (C.c_int, [_VP, C.c_int32, _VP, _VP, _VP, _VP]),
+    "hrom_imp_newton": (C.c_int, [_VP, C.c_int32, _VP, _VP, _VP, _VP, C.POINTER(C.c_int32)]),
+    "hrom_imp_filter": (C.c_int, [_VP, C.c_int32, _VP, _VP, _VP, _VP, _VP, C.POINTER(C.c_int32)]),
+    "hrom_imp_set_window": (C.c_int, [_VP, C.c_int64, _VP, C.c_int32, _VP]),
+    "hrom_imp_get_band": (C.c_int, [_VP, _VP, _VP]),
 }
 
 SECTIONS = ["dt", "masked_rk3", "gathered_gram", "pinv_solve", "fill_pass", "indicator", "seam_filter",
@@ -363,3 +386,114 @@ class HybridROM:
         out = torch.empty((ncol, ncol), dtype=torch.float64, device="cuda")
         _ck(self.lib.hrom_gram(self.h, _ptr(ptrs), ncol, rows, _ptr(rho), _ptr(out)), "hrom_gram")
         return out
+
+
+def _params_of(wl, gram_mode=0, rebase_period=0, gather_mode=0, full_period=None) -> Params:
+    fo = (C.c_int32 * 3)(*(list(wl.filter_orders) + [0, 0, 0])[:3])
+    return Params(wl.w, wl.r, wl.h, wl.W, fo, len(wl.filter_orders), wl.filter_max_sweeps, wl.filter_eps,
+                  wl.eig_rel_cutoff, wl.lsq_rel_cutoff, wl.f, gram_mode, rebase_period, gather_mode,
+                  getattr(wl, "z", 0) if full_period is None else full_period,
+                  1 if getattr(wl, "delta", 0.0) > 0.0 else 0, float(getattr(wl, "delta", 0.0)),
+                  int(getattr(wl, "n_p", 0)))
+
+
+class ImplicitROM:
+    """One hrom_imp_ctx: Algorithm 1 with the paper's implicit HDM (NEXT-4) on one grid."""
+
+    def __init__(self, wl, stream: Optional[torch.cuda.Stream] = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("libhrom needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+        self.lib = load_library()
+        self.wl = wl
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        g = Grid(wl.dim, wl.nx, wl.ny if wl.dim == 2 else 1, wl.x0, wl.x1, wl.y0, wl.y1, wl.bc, wl.recon)
+        p = _params_of(wl)
+        ip = ImpParams(int(wl.flux), float(wl.dt), float(wl.eps_y), int(wl.j_max), float(wl.newton_tol),
+                       int(wl.newton_maxit))
+        h = C.c_void_p()
+        _ck(self.lib.hrom_imp_create(C.byref(g), wl.gamma, C.byref(p), C.byref(ip),
+                                     C.c_void_p(self.stream.cuda_stream), C.byref(h)), "hrom_imp_create")
+        self.h = h
+        self.mask_words = int(self.lib.hrom_imp_mask_words(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.hrom_imp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_state(self, q: torch.Tensor):
+        assert q.dtype == torch.float64 and q.is_contiguous() and q.numel() == self.wl.D
+        _ck(self.lib.hrom_imp_set_state(self.h, _ptr(q)), "hrom_imp_set_state")
+
+    def get_state(self, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((self.wl.c, self.wl.N), dtype=torch.float64, device="cuda")
+        _ck(self.lib.hrom_imp_get_state(self.h, _ptr(out)), "hrom_imp_get_state")
+        return out
+
+    def step(self, count_out: Optional[torch.Tensor] = None):
+        _ck(self.lib.hrom_imp_step(self.h, _ptr(count_out)), "hrom_imp_step")
+
+    def stats(self):
+        """(kind, J, Newton iterations, GMRES products, ODEIM points used) of the last step."""
+        out = (C.c_int32 * 5)()
+        _ck(self.lib.hrom_imp_stats(self.h, C.cast(out, C.c_void_p)), "hrom_imp_stats")
+        return tuple(out)
+
+    def mask(self) -> torch.Tensor:
+        out = torch.empty(self.mask_words, dtype=torch.int32, device="cuda")
+        _ck(self.lib.hrom_imp_get_mask(self.h, _ptr(out)), "hrom_imp_get_mask")
+        return out
+
+    def indicator(self) -> torch.Tensor:
+        out = torch.empty(self.wl.N, dtype=torch.float64, device="cuda")
+        _ck(self.lib.hrom_imp_get_indicator(self.h, _ptr(out)), "hrom_imp_get_indicator")
+        return out
+
+    def y(self) -> torch.Tensor:
+        out = torch.zeros(self.wl.r, dtype=torch.float64, device="cuda")
+        _ck(self.lib.hrom_imp_get_y(self.h, _ptr(out)), "hrom_imp_get_y")
+        return out
+
+    def effective_rank(self) -> int:
+        return int(self.lib.hrom_imp_effective_rank(self.h))
+
+    def sync(self):
+        _ck(self.lib.hrom_imp_sync(self.h), "hrom_imp_sync")
+
+    def residual(self, q, qm1, qm2=None, order=2) -> torch.Tensor:
+        R = torch.empty_like(q)
+        _ck(self.lib.hrom_imp_residual(self.h, order, _ptr(q), _ptr(qm1), _ptr(qm2), _ptr(R)), "hrom_imp_residual")
+        return R
+
+    def newton(self, q: torch.Tensor, qm1, qm2=None, order=2, mask: Optional[torch.Tensor] = None) -> int:
+        """Solves in place (q: initial guess + frozen data); returns the Newton iterations."""
+        its = C.c_int32()
+        _ck(self.lib.hrom_imp_newton(self.h, order, _ptr(qm1), _ptr(qm2), _ptr(mask), _ptr(q), C.byref(its)),
+            "hrom_imp_newton")
+        return its.value
+
+    def filter(self, v: torch.Tensor, mask: torch.Tensor, qm1, qm2=None, order=2):
+        """Filters v in place; returns (kept cells uint8 tensor, sweeps per order)."""
+        kept = torch.zeros(self.wl.N, dtype=torch.uint8, device="cuda")
+        sw = (C.c_int32 * 3)()
+        _ck(self.lib.hrom_imp_filter(self.h, order, _ptr(qm1), _ptr(qm2), _ptr(mask), _ptr(v), _ptr(kept),
+                                     C.cast(sw, C.POINTER(C.c_int32))), "hrom_imp_filter")
+        return kept, list(sw)
+
+    def band(self):
+        """Cells of the filter band of the current sets (ascending)."""
+        lst = torch.zeros(self.wl.N, dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _ck(self.lib.hrom_imp_get_band(self.h, _ptr(lst), _ptr(cnt)), "hrom_imp_get_band")
+        return lst[:int(cnt.item())].cpu().numpy()
+
+    def set_window(self, k: int, snaps: torch.Tensor, mask_next: Optional[torch.Tensor] = None):
+        _ck(self.lib.hrom_imp_set_window(self.h, k, _ptr(snaps), snaps.shape[0], _ptr(mask_next)),
+            "hrom_imp_set_window")

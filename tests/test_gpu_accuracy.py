@@ -10,6 +10,7 @@ fed the oracle's indicator, and the GPU's own selection equal to the oracle's ex
 whose indicator lies within 1e-12 (relative) of the selection threshold.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -23,6 +24,11 @@ if not torch.cuda.is_available():  # pragma: no cover
 from paper_2301_01718_b200 import hrom as H  # noqa: E402
 
 EPS = 2.220446049250313e-16
+# the full replay set (k in {w, w+1, w+50} at configs 3 and 4, and the 2048^2 config-4 step whose
+# single-threaded oracle POD takes ~18 min) runs with HROM_SLOW_TESTS=1; the default GPU suite
+# keeps one replay per config (k = w + 1).  Full-set log: profiles/r2_pytest_gpu_full_12ae8a2.txt
+SLOW = os.environ.get("HROM_SLOW_TESTS") == "1"
+K_OFFS = [0, 1, 50] if SLOW else [1]
 
 
 def rel(a, b):
@@ -116,7 +122,7 @@ def check_step(rec, wl, orc, S_used):
     return e_rel, e_max
 
 
-@pytest.mark.parametrize("k_off", [0, 1, 50])
+@pytest.mark.parametrize("k_off", K_OFFS)
 def test_replay_config3_fullsize(orc, inputs, k_off):
     """Config 3 at full size (1024^2, w = 48, r = 24, BJ:9): the window gamma_{k-w}..gamma_k from
     the oracle's full steps, S-hat = a seeded 10 % of the cells, one hybrid step on both sides
@@ -124,7 +130,7 @@ def test_replay_config3_fullsize(orc, inputs, k_off):
     indicator to 1e-9; next S-hat: bit-exact when the GPU is fed the oracle's indicator, and from
     its own indicator equal to the oracle's mask off the threshold's 1e-12 neighbourhood."""
     wl0 = inputs.config(3)
-    wl, snaps = hdm_trajectory(orc, inputs, 3, wl0.w + 50)
+    wl, snaps = hdm_trajectory(orc, inputs, 3, wl0.w + max(K_OFFS))
     k = wl.w + k_off
     S = (np.random.default_rng(33 + k_off).random(wl.N) < wl.f).astype(np.uint8)
     rec = replay(orc, inputs, wl, snaps, k, S)[0]
@@ -143,14 +149,14 @@ def test_replay_config3_fullsize(orc, inputs, k_off):
     assert not np.any(diff & ~near_threshold(rec["eo"], n_g)), int((diff & ~near_threshold(rec["eo"], n_g)).sum())
 
 
-@pytest.mark.parametrize("k_off", [0, 1, 50])
+@pytest.mark.parametrize("k_off", K_OFFS)
 def test_replay_config4_params_512(orc, inputs, k_off):
     """Config-4 parameters (periodic blasts, w = 64, r = 32, f = 10 %, BJ:10) on a 512^2 grid:
     the headline instantiation fill_kernel<34> (w + 2 = 66 ring slots) with its fused
     double-double Gram row.  Two hybrid steps from the oracle's window at k = w + k_off: the
     second step's basis is built from the first step's fused row, so the row is checked
     against the oracle too (the GPU is fed the oracle's next mask)."""
-    wl, snaps = hdm_trajectory(orc, inputs, 4, inputs.config(4).w + 50, nx=512, ny=512)
+    wl, snaps = hdm_trajectory(orc, inputs, 4, inputs.config(4).w + max(K_OFFS) + 1, nx=512, ny=512)
     k = wl.w + k_off
     S = (np.random.default_rng(44 + k_off).random(wl.N) < wl.f).astype(np.uint8)
     recs = replay(orc, inputs, wl, snaps, k, S, steps=2)
@@ -158,6 +164,7 @@ def test_replay_config4_params_512(orc, inputs, k_off):
         check_step(rec, wl, orc, S)
 
 
+@pytest.mark.skipif(not SLOW, reason="~18 min of single-threaded oracle POD; HROM_SLOW_TESTS=1")
 def test_fullsize_config4_replay_step(orc, inputs):
     """One config-4 hybrid step at full size (2048^2, w = 64, r = 32, f = 10 %) in bench.py's
     launch configuration against the oracle: window = the shared generator's smooth blast-like

@@ -1,0 +1,200 @@
+"""GPU parity of NEXT-4 (the paper's implicit HDM, csrc/implicit.cu) against the oracle
+(oracle/implicit.cpp) on the same seeded inputs, through the C ABI (hrom_imp_*).
+
+Tolerances: the residual R_k is one fixed formula (rounding-level differences only: 1e-13 relative
+per element).  Newton roots: both sides stop at ||R||_inf <= tol = 1e-13; the two roots differ by
+at most ||J^-1|| (tol_gpu + tol_orc), and J = I - dt beta df*/dq with CFL <= 0.3 on these cases
+keeps ||J^-1|| <= ~2, so the bar is 1e-12 per element (north_star's per-step bar).  The filter is
+compared with identical keep sets and sweep counts.  Trajectories (Algorithm 1 with subiterations)
+step by step with identical S-hat while the states agree to 1e-10.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2301_01718_b200 import hrom as H  # noqa: E402
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def maxerr(a, b):
+    a = np.asarray(a).reshape(np.asarray(b).shape)
+    b = np.asarray(b)
+    scale = np.max(np.abs(b), axis=-1, keepdims=True)
+    return float(np.max(np.abs(a - b) / np.maximum(scale, 1e-300)))
+
+
+def _wl(inputs, **kw):
+    base = dict(name="imp", dim=2, nx=40, ny=30, bc=2, recon=2, w=5, r=4, h=2, W=-1, f=0.1,
+                hdm="implicit", flux=1, dt=4e-3, newton_tol=1e-13, seed=11)
+    base.update(kw)
+    return inputs.Workload(**base)
+
+
+RES_CASES = [
+    ("1d-roe-walls", dict(dim=1, nx=257, ny=1, bc=2)),
+    ("1d-roe-transmissive", dict(dim=1, nx=100, ny=1, bc=0)),
+    ("2d-roe-walls-ragged", dict(nx=37, ny=29, bc=2)),
+    ("2d-roe-periodic", dict(nx=32, ny=24, bc=1)),
+    ("2d-rusanov-walls", dict(nx=30, ny=20, bc=2, flux=0)),
+    ("2d-roe-first-order", dict(nx=30, ny=20, bc=2, recon=1, h=1)),
+]
+
+
+@pytest.mark.parametrize("name,kw", RES_CASES, ids=[c[0] for c in RES_CASES])
+def test_residual_parity(orc, inputs, name, kw):
+    wl = _wl(inputs, **kw)
+    q, q1, q2 = (inputs.initial_condition(dataclasses.replace(wl, seed=s), "random") for s in (1, 2, 3))
+    rom = H.ImplicitROM(wl)
+    for order in (1, 2):
+        Rg = rom.residual(dev(q), dev(q1), dev(q2), order=order).cpu().numpy()
+        Ro = orc.bdf_residual(wl, q, q1, q2, wl.dt, order=order, flux=wl.flux)
+        assert np.max(np.abs(Rg - Ro)) <= 1e-13 * np.max(np.abs(q))
+
+
+NEWTON_CASES = [
+    ("sod-bdf1-step1", "sod", 1),
+    ("implosion-bdf1-step1", "implosion", 1),
+    ("blasts-walls-bdf2", None, 2),
+]
+
+
+@pytest.mark.parametrize("name,preset,order", NEWTON_CASES, ids=[c[0] for c in NEWTON_CASES])
+def test_newton_full_parity(orc, inputs, name, preset, order):
+    if preset:
+        wl = inputs.preset(preset, newton_tol=1e-13)
+        q1 = inputs.initial_condition(wl)
+        q2 = q1
+    else:
+        wl = _wl(inputs, dt=1e-3)
+        q1 = inputs.initial_condition(wl, "blasts")
+        q2 = q1 * (1.0 + 1e-3 * np.sin(np.arange(q1.size)).reshape(q1.shape))
+    qo, its_o, st = orc.newton(wl, q1, q1, q2, wl.dt, order=order, flux=wl.flux, tol=1e-13)
+    assert its_o > 0 and st[0] <= 1e-13
+    rom = H.ImplicitROM(wl)
+    qg = dev(q1).clone()
+    its_g = rom.newton(qg, dev(q1), dev(q2), order=order)
+    qg = qg.cpu().numpy()
+    assert its_g > 0
+    Rg = orc.bdf_residual(wl, qg, q1, q2, wl.dt, order=order, flux=wl.flux)
+    assert np.max(np.abs(Rg)) <= 2e-13, np.max(np.abs(Rg))  # the GPU root is a root for the oracle too
+    assert maxerr(qg, qo) <= 1e-12, maxerr(qg, qo)
+
+
+def test_newton_partial_parity(orc, inputs):
+    """Partial HDM (Eq. 6b): unknowns on S-hat, the rest frozen data."""
+    wl = _wl(inputs, nx=48, ny=36)
+    q1 = inputs.initial_condition(wl, "random")
+    rng = np.random.default_rng(4)
+    S = (rng.random(wl.N) < 0.08).astype(np.uint8)
+    S[:5] = 1  # wall corner
+    qo, its_o, st = orc.newton(wl, q1, q1, q1, wl.dt, order=2, flux=1, mask=S, tol=1e-13)
+    assert its_o > 0
+    rom = H.ImplicitROM(wl)
+    qg = dev(q1).clone()
+    rom.newton(qg, dev(q1), dev(q1), order=2, mask=H.mask_from_cells(wl, S))
+    qg = qg.cpu().numpy()
+    Sb = S.astype(bool)
+    assert np.array_equal(qg[:, ~Sb], q1[:, ~Sb])  # frozen entries untouched
+    assert maxerr(qg[:, Sb], qo[:, Sb]) <= 1e-12
+
+
+@pytest.mark.parametrize("W", [-1, 2])
+def test_implicit_filter_parity(orc, inputs, W):
+    """Filter gated by the implicit residual: identical keep set and sweeps, values <= 1e-13."""
+    wl = _wl(inputs, nx=44, ny=32, W=W)
+    q1 = inputs.initial_condition(wl, "random")
+    q2 = inputs.initial_condition(dataclasses.replace(wl, seed=8), "random")
+    rng = np.random.default_rng(6)
+    v = q1 * (1.0 + 0.02 * np.where(rng.random(q1.shape) < 0.5, 1.0, -1.0))  # checkerboard-like noise
+    S = (rng.random(wl.N) < 0.1).astype(np.uint8)
+    vo, kept_o, sw_o = orc.seam_filter_implicit(wl, v, q1, q2, S, wl.dt, order=2, flux=1)
+    rom = H.ImplicitROM(wl)
+    vg = dev(v).clone()
+    kept_g, sw_g = rom.filter(vg, H.mask_from_cells(wl, S), dev(q1), dev(q2), order=2)
+    assert sw_g == sw_o
+    assert np.array_equal(kept_g.cpu().numpy(), kept_o)
+    assert maxerr(vg.cpu().numpy(), vo) <= 1e-13
+
+
+def _oracle_run(orc, wl, q0, steps, perturb=0.0):
+    """Oracle trajectory: per step the state, the window (w+1 snapshots), S-hat_{k+1}, kind, J."""
+    if perturb:
+        q0 = q0 * (1.0 + perturb * np.cos(np.arange(q0.size)).reshape(q0.shape))
+    R = orc.Run(wl, q0)
+    hist = [q0]
+    out = []
+    for _ in range(steps):
+        kind = R.step()
+        hist.append(R.state())
+        out.append(dict(state=hist[-1], kind=kind, J=R.implicit_stats()[0], mask=R.mask(), k=R.k))
+    return hist, out
+
+
+def _replay(orc, inputs, wl, hist, recs, k):
+    """The GPU fed the oracle's window gamma_{k-w}..gamma_k and S-hat_{k+1} (ODEIM points of its
+    own Phi_{k+1} added, as the oracle does), then one step: state, kind, J, next S-hat."""
+    rom = H.ImplicitROM(wl)
+    win = np.stack(hist[k - wl.w:k + 1])
+    rom.set_window(k, dev(win.reshape(wl.w + 1, -1)), H.mask_from_cells(wl, recs[k - 1]["mask"]))
+    refreshed = not (wl.z > 0 and (k + 1) % wl.z == 0)  # no update before a full step
+    if refreshed:
+        assert np.array_equal(H.cells_from_mask(wl, rom.mask()), recs[k - 1]["mask"])
+    rom.step()
+    kind, J, its, prods, np_used = rom.stats()
+    g = rom.get_state().cpu().numpy()
+    o = recs[k]
+    nxt = not (wl.z > 0 and (k + 2) % wl.z == 0)
+    return dict(err=maxerr(g, o["state"]), kind=kind, kind_o=o["kind"], J=J, J_o=o["J"],
+                mask_eq=(not nxt) or np.array_equal(H.cells_from_mask(wl, rom.mask()), o["mask"]), its=its)
+
+
+@pytest.mark.parametrize("preset,ks", [("sod", (5, 6, 25, 80)), ("implosion", (7, 8, 12, 13, 15))])
+def test_preset_replay_per_step(orc, inputs, preset, ks):
+    """Algorithm 1 with the implicit HDM on the paper's presets (Sod P:737-767, implosion
+    P:906-921): at each k the GPU starts from the oracle's window and S-hat_{k+1} and takes one
+    step (hybrid steps with subiterations and the implicit-residual filter; implosion step 14 is a
+    periodic full HDM step, z = 7, and step 15 the first hybrid step after it, sampled by the
+    projection indicator, G8).  Per-step state <= 1e-12 per element, same step kind, same J,
+    same next S-hat."""
+    wl = inputs.preset(preset, newton_tol=1e-13)
+    hist, recs = _oracle_run(orc, wl, inputs.initial_condition(wl), max(ks) + 1)
+    for k in ks:
+        r = _replay(orc, inputs, wl, hist, recs, k)
+        assert r["kind"] == r["kind_o"], (k, r)
+        assert r["err"] <= 1e-12, (k, r)
+        assert r["J"] == r["J_o"], (k, r)
+        assert r["mask_eq"], (k, r)
+
+
+@pytest.mark.parametrize("preset,steps", [("sod", 60), ("implosion", 24)])
+def test_preset_trajectory_vs_oracle_sensitivity(orc, inputs, preset, steps):
+    """Free-running trajectories: the GPU's drift from the oracle stays within 30x the oracle's
+    own sensitivity (an oracle run from a 1e-15-perturbed IC, the G6 rule of the explicit path)
+    plus 1e-13, with identical S-hat and step kinds while that sensitivity is below 1e-9."""
+    wl = inputs.preset(preset, newton_tol=1e-13)
+    q0 = inputs.initial_condition(wl)
+    hist, recs = _oracle_run(orc, wl, q0, steps)
+    _, ens = _oracle_run(orc, wl, q0, steps, perturb=1e-15)
+    rom = H.ImplicitROM(wl)
+    rom.set_state(dev(q0))
+    for k in range(steps):
+        rom.step()
+        kind = rom.stats()[0]
+        g = rom.get_state().cpu().numpy()
+        sref = maxerr(ens[k]["state"], recs[k]["state"])
+        if sref >= 1e-9:
+            break
+        e = maxerr(g, recs[k]["state"])
+        assert e <= 30 * sref + 1e-13, (k + 1, e, sref)
+        assert kind == recs[k]["kind"], (k + 1, kind, recs[k]["kind"])
+        assert np.array_equal(H.cells_from_mask(wl, rom.mask()), recs[k]["mask"]), k + 1

@@ -296,3 +296,56 @@ def test_sod_implicit_arom_runs(orc, inputs):
     assert orc.positivity(wl, q) < 0
     e = np.abs(q - qh).sum() / np.abs(qh).sum()  # e_k
     assert e < 0.02, e
+
+
+# ---------------- the filter gated by the implicit residual ----------------
+def _np_implicit_filter(orc, wl, v, q1, q2, S):
+    """Brute force of P:424-432 with the residual v - F_k(v) re-evaluated on the candidate
+    (numpy; F_k from the pinned orc.bdf_residual): x-pass then y-pass on the band (every cell off
+    S-hat for W = -1), keep where max_var |R| decreases, eps_f stop of reading A23'."""
+    v = v.copy()
+    nx, ny, c = wl.nx, wl.ny, wl.c
+    band = (S == 0) if wl.W < 0 else (orc.dilate_square(wl, S, wl.W).astype(bool) & (S == 0))
+    Bm = band.reshape(ny, nx)
+    weights = {2: ([1, 2, 1], 4.0), 4: ([-1, 4, 10, 4, -1], 16.0), 6: ([1, -6, 15, 44, 15, -6, 1], 64.0)}
+    kept_all = np.zeros(wl.N, np.uint8)
+    sweeps = []
+    for order in wl.filter_orders:
+        cf, den = weights[order]
+        rad = len(cf) // 2
+        sw = 0
+        for _ in range(wl.filter_max_sweeps):
+            sw += 1
+            V = v.reshape(c, ny, nx)
+            X = sum(cf[m + rad] * V[:, :, np.clip(np.arange(nx) + m, 0, nx - 1)] for m in range(-rad, rad + 1)) / den
+            vp = np.where(Bm[None], X, V)
+            Y = sum(cf[m + rad] * vp[:, np.clip(np.arange(ny) + m, 0, ny - 1), :] for m in range(-rad, rad + 1)) / den
+            vpp = np.where(Bm[None], Y, vp).reshape(c, -1)
+            Ro = orc.bdf_residual(wl, v, q1, q2, wl.dt)
+            Rn = orc.bdf_residual(wl, vpp, q1, q2, wl.dt)
+            rold, rnew = np.abs(Ro).max(0), np.abs(Rn).max(0)
+            fs = np.abs(v - Ro).max(0)
+            keep = band & (rnew < rold)
+            gate = keep & (rold > 2.0 ** -40 * fs)
+            md = np.max((rold - rnew)[gate] / rold[gate]) if gate.any() else 0.0
+            v[:, keep] = vpp[:, keep]
+            kept_all[keep] = 1
+            if not keep.any() or md < wl.filter_eps:
+                break
+        sweeps.append(sw)
+    return v, kept_all, sweeps
+
+
+@pytest.mark.parametrize("W", [-1, 2])
+def test_implicit_filter_vs_numpy_brute_force(orc, inputs, W):
+    wl = _wl(inputs, nx=30, ny=22, W=W)
+    q1 = inputs.initial_condition(wl, "random")
+    q2 = inputs.initial_condition(dataclasses.replace(wl, seed=8), "random")
+    rng = np.random.default_rng(6)
+    v = q1 * (1.0 + 0.02 * np.where(rng.random(q1.shape) < 0.5, 1.0, -1.0))
+    S = (rng.random(wl.N) < 0.1).astype(np.uint8)
+    vo, kept_o, sw_o = orc.seam_filter_implicit(wl, v, q1, q2, S, wl.dt, order=2, flux=1)
+    vn, kept_n, sw_n = _np_implicit_filter(orc, wl, v, q1, q2, S)
+    assert sw_o == sw_n and np.array_equal(kept_o, kept_n)
+    assert np.max(np.abs(vo - vn)) <= 1e-14
+    assert kept_o.sum() > 0

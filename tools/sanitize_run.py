@@ -18,7 +18,28 @@ from paper_2301_01718_b200 import inputs  # noqa: E402
 from paper_2301_01718_b200 import hrom as H  # noqa: E402
 
 
+def implicit(name, extra):
+    """NEXT-4: Algorithm 1 with the implicit HDM (Newton-Krylov, partial HDM subiterations,
+    implicit-residual filter) on a preset, plus the standalone residual / Newton calls."""
+    wl = inputs.preset(name)
+    q0 = torch.from_numpy(inputs.initial_condition(wl)).cuda()
+    rom = H.ImplicitROM(wl)
+    rom.set_state(q0)
+    for _ in range(wl.w + extra):
+        rom.step()
+    rom.sync()
+    q = rom.get_state()
+    rom.residual(q, q0, q0)
+    qq = q.clone()
+    rom.newton(qq, q, q, order=2, mask=rom.mask())
+    rom.sync()
+    print("ok", name, rom.stats())
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] in ("sod", "implosion"):
+        implicit(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 4)
+        return
     cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
     extra = int(sys.argv[2]) if len(sys.argv) > 2 else 6
     wl = inputs.config(cfg)
