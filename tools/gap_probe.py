@@ -35,7 +35,7 @@ def main():
         tail = lam[r] if r < len(lam) else 0.0
         gap_r = lam[r - 1] - tail
         gaps = [lam[i] - lam[i + 1] for i in range(r - 1)]
-        rows.append({"k": rom.k(), "reff": int(r), "lam1": float(l1), "lam_r": float(lam[r - 1]),
+        rows.append({"k": rom.k, "reff": int(r), "lam1": float(l1), "lam_r": float(lam[r - 1]),
                      "kappa_subspace": float(eps * l1 / max(gap_r, 1e-300)),
                      "min_rel_gap_retained": float(min(gaps) / l1) if gaps else None})
     print(json.dumps({"config": cfg, "rows": rows,
