@@ -741,12 +741,14 @@ constexpr int GV_T = 256, GV_W = GV_T / 32;
 // product vector b = gamma_k on the band rows, partials [blk][nU + 1] ([nU] = sum b^2).
 // DD = false: plain fp64 accumulation (the gathered Gram of the gappy normal equations when
 // gather_precision = 1, G11; lo parts stay 0)
-template <int SPW, bool NEWCOL = true, bool BANDOUT = false, bool DD = true, int GV_U = NEWCOL ? 1 : 2>
-__global__ void __launch_bounds__(GV_T, 2) gemv_gather_kernel(Geo g, Win W, const double* __restrict__ ring,
+// NT: threads per block (GV_T for every current launch).
+template <int SPW, bool NEWCOL = true, bool BANDOUT = false, bool DD = true, int GV_U = NEWCOL ? 1 : 2, int NT = GV_T>
+__global__ void __launch_bounds__(NT, NT == GV_T ? 2 : 1) gemv_gather_kernel(Geo g, Win W, const double* __restrict__ ring,
                                                            const SRef rho, const int32_t* __restrict__ list,
                                                            const int32_t* __restrict__ count, const SRef src_b,
                                                            double* __restrict__ vpart, const double* __restrict__ C) {
-  __shared__ double red[GV_W][2 * SPW + 1], redl[GV_W][2 * SPW + 1];
+  constexpr int NW = NT / 32;
+  __shared__ double red[NW][2 * SPW + 1], redl[NW][2 * SPW + 1];
   __shared__ double s_bias;
   if (threadIdx.x == 0) {  // accumulator bias from the window Gram's diagonal (dd.cuh gram_bias)
     double mc = 0.0;
@@ -763,7 +765,7 @@ __global__ void __launch_bounds__(GV_T, 2) gemv_gather_kernel(Geo g, Win W, cons
   int coff[SPW];  // slab offsets of the warp's slots (-1: none); 32-bit to save registers
 #pragma unroll
   for (int j = 0; j < SPW; ++j) {
-    const int sl = warp + GV_W * j;
+    const int sl = warp + NW * j;
     coff[j] = sl < nU ? W.slot[sl] * TILE : -1;
   }
   // double-double accumulators (G11): these GEMVs are rows / columns of the POD's and the
@@ -871,23 +873,23 @@ __global__ void __launch_bounds__(GV_T, 2) gemv_gather_kernel(Geo g, Win W, cons
   // partials [blk][n][hi, lo]
   if (BANDOUT) {
     double* out = vpart + (int64_t)blockIdx.x * (nU + 1) * 2;
-    for (int k = threadIdx.x; k <= nU; k += GV_T) {
-      const int wi = k == nU ? 0 : k % GV_W, ji = k == nU ? 2 * SPW : SPW + k / GV_W;
+    for (int k = threadIdx.x; k <= nU; k += NT) {
+      const int wi = k == nU ? 0 : k % NW, ji = k == nU ? 2 * SPW : SPW + k / NW;
       out[2 * k] = red[wi][ji];
       out[2 * k + 1] = redl[wi][ji];
     }
     return;
   }
   double* out = vpart + (int64_t)blockIdx.x * (2 * nU + 1) * 2;
-  for (int k = threadIdx.x; k <= 2 * nU; k += GV_T) {
+  for (int k = threadIdx.x; k <= 2 * nU; k += NT) {
     int wi, ji;
     if (k == 2 * nU) {
       wi = 0;
       ji = 2 * SPW;
     } else {
-      const int sl = k < nU ? k : k - nU;  // slot sl is (warp sl % GV_W, j = sl / GV_W)
-      wi = sl % GV_W;
-      ji = (k < nU ? 0 : SPW) + sl / GV_W;
+      const int sl = k < nU ? k : k - nU;  // slot sl is (warp sl % NW, j = sl / NW)
+      wi = sl % NW;
+      ji = (k < nU ? 0 : SPW) + sl / NW;
     }
     out[2 * k] = red[wi][ji];
     out[2 * k + 1] = redl[wi][ji];
@@ -2050,13 +2052,8 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   const int ncol = a.W.nU + 1;
   double* R = c->b.eigV;
   double* Rl = c->b.Rlo;
-  // gather_precision 1: the gathered Gram in fp64 (DMMA + FMA GEMVs, lo = 0), 0: double-double
-  static const bool g64 = getenv("HROM_GATHER_FP64") != nullptr;
-  const bool dd = !g64;
   auto gram = [&](GGArgs& aa, double* hi, double* lo) -> hrom_status {
-    if (dd) return run_gather_gram_dd(c, aa, ncol, grid, hi, lo, ncol, nullptr);
-    HROM_CK(cudaMemsetAsync(lo, 0, (size_t)ncol * ncol * sizeof(double), c->st));
-    return run_gather_gram(c, aa, ncol, grid, hi, ncol, nullptr);
+    return run_gather_gram_dd(c, aa, ncol, grid, hi, lo, ncol, nullptr);
   };
   if (c->P.odeim_points > 0) {  // gappy rows = the DOF rows of the ODEIM points (Eq. 8, 10)
     a.mode = 2;
@@ -2091,14 +2088,14 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
     d.list = c->b.lists + (int64_t)L_REM * c->g.N;
     d.count = c->b.counts + L_REM;
     if ((s = gram(d, Rm, Rml)) != HROM_OK) return s;
-    // GEMVs of the newest snapshot and of b over all S-hat rows
-    // one wave (2 CTAs per SM); static split: avoid the eigen's SM
+    // GEMVs of the newest snapshot and of b over all S-hat rows: one wave (2 CTAs per SM), static
+    // split that avoids the eigen's SM.  (Tried: 512 threads with 5 slots per warp and 4 row
+    // chunks in flight -- 0.64 ms against 0.47 ms for the whole gathered Gram: the 16 warps'
+    // redundant rho / x_new / b loads of the same rows cost more than the extra memory-level
+    // parallelism gains.)
     const int gblocks = 2 * (c->basis_pending ? c->nsm - 1 : c->nsm);
     const int nv = 2 * a.W.nU + 1;
-    if (a.W.nU <= 9 * GV_W && !dd)
-      gemv_gather_kernel<9, true, false, false><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count,
-                                                                             src_b, c->b.vpart, c->b.C);
-    else if (a.W.nU <= 9 * GV_W)
+    if (a.W.nU <= 9 * GV_W)
       gemv_gather_kernel<9><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b, c->b.vpart,
                                                          c->b.C);
     else
