@@ -285,7 +285,7 @@ __device__ __forceinline__ bool admissible_cell(const IGeo& g, const double* U) 
 }
 
 // ---------------- the Newton-Krylov solve (one cooperative kernel) ----------------
-constexpr int NK_T = 256, NK_W = NK_T / 32;
+constexpr int NK_T = 512, NK_W = NK_T / 32;
 constexpr int kMaxKrylov = 30;  // GMRES restart length
 
 struct NArgs {
@@ -310,6 +310,9 @@ struct NArgs {
   int* stat;     // [0] Newton iterations (or -1 / -2), [1] J products, [2] final ||R||_inf bits lo, hi
   double* rstat;  // [0] final ||R||_inf
   const int* run_if;  // nullable: run only when *run_if != 0
+  double* ff;         // 4 * 4 * ncell face-flux tangents of the face-parallel Jacobian products
+  long long* tdbg;    // nullable: block 0's clock64 per phase [0] products (JVP + barriers),
+                      // [1] Gram-Schmidt, [2] norms + Givens, [3] line search, [4] whole kernel
 };
 
 struct NShared {
@@ -330,22 +333,41 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// barrier of a Newton / filter kernel: a block barrier when the solve runs in ONE block (small
+// partial systems: no grid barrier, no global partials), else a cooperative grid barrier
+template <bool ONE>
+struct GSync {
+  __device__ __forceinline__ void sync() const {
+    if (ONE) __syncthreads();
+    else cg::this_grid().sync();
+  }
+};
+
 // grid-wide reduction of K <= 32 per-thread values (the caller has put warp results in S.red):
 // block partial -> part[blk][k] -> grid sync -> every block sums the partials in block order.
 // mode: 0 sum, 1 max.  Result in S.tot[k], identical in every block.
-__device__ void grid_finish(cg::grid_group& G, NShared& S, double* part, int K, const int* modes) {
+template <class GS>
+__device__ void grid_finish(const GS& G, NShared& S, double* part, int K, const int* modes) {
   __syncthreads();
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   if (t < K) {
     double a = S.red[0][t];
     for (int w = 1; w < NK_W; ++w) a = modes && modes[t] ? fmax(a, S.red[w][t]) : a + S.red[w][t];
     part[blockIdx.x * 32 + t] = a;
   }
   G.sync();
-  if (t < K) {
-    double a = part[t];
-    for (int b = 1; b < (int)gridDim.x; ++b) a = modes && modes[t] ? fmax(a, part[b * 32 + t]) : a + part[b * 32 + t];
-    S.tot[t] = a;
+  // every block sums the partials in the same fixed order: lane l takes blocks l, l + 32, ...,
+  // then a fixed xor tree over the lanes (no serial walk over the blocks)
+  const int nb = gridDim.x;
+  for (int k = warp; k < K; k += NK_W) {
+    const bool mx = modes && modes[k];
+    double a = 0.0;  // identity of both (the max mode's values are >= 0)
+    for (int b = lane; b < nb; b += 32) a = mx ? fmax(a, part[b * 32 + k]) : a + part[b * 32 + k];
+    for (int o = 16; o > 0; o >>= 1) {
+      const double x = __shfl_xor_sync(0xffffffffu, a, o);
+      a = mx ? fmax(a, x) : a + x;
+    }
+    if (lane == 0) S.tot[k] = a;
   }
   __syncthreads();
 }
@@ -383,40 +405,93 @@ __device__ void residual_phase(const NArgs& a, int nc, const double* s, double* 
 }
 
 // w = J V_j on the unknown cells (directional derivative of R at q)
-__device__ void jvp_phase(const NArgs& a, int nc, const double* V, double* w) {
+// the tangent of one face flux of cell n (f: 0 x+, 1 x-, 2 y+, 3 y-) in direction V
+template <int DIM>
+__device__ __forceinline__ void face_tangent(const NArgs& a, const double* V, int n, int f, double* out) {
   const IGeo& g = a.g;
-  for (int idx = blockIdx.x * NK_T + threadIdx.x; idx < nc; idx += gridDim.x * NK_T) {
+  const int i = n % g.nx, j = n / g.nx;
+  dual F[DIM + 2];
+  if (f == 0) face_flux<dual, DIM, 0>(g, a.q, V, a.unk, i, j, F);
+  else if (f == 1) face_flux<dual, DIM, 0>(g, a.q, V, a.unk, i - 1, j, F);
+  else if (DIM == 2 && f == 2) face_flux<dual, DIM, DIM - 1>(g, a.q, V, a.unk, i, j, F);
+  else face_flux<dual, DIM, DIM - 1>(g, a.q, V, a.unk, i, j - 1, F);
+#pragma unroll
+  for (int v = 0; v < DIM + 2; ++v) out[v] = F[v].d;
+}
+
+// w = J V on the unknown cells (directional derivative of R at q).  Face-parallel: one thread per
+// (cell, face) computes the face flux's tangent (a cell's residual is four long dependent chains
+// of Roe arithmetic; with one thread per cell a small partial system waits on their latency),
+// then one thread per unknown entry combines them as cell_residual does.
+template <class GS>
+__device__ void jvp_phase(const GS& G, const NArgs& a, int nc, const double* V, double* w) {
+  const IGeo& g = a.g;
+  const int nf = 2 * g.dim;
+  const int gt = blockIdx.x * NK_T + threadIdx.x, gs = gridDim.x * NK_T;
+  for (int t = gt; t < nc * nf; t += gs) {
+    const int idx = t / nf, f = t - idx * nf;
+    double* o = a.ff + (int64_t)t * 4;
+    if (g.dim == 2) face_tangent<2>(a, V, cell_of(a, idx), f, o);
+    else face_tangent<1>(a, V, cell_of(a, idx), f, o);
+  }
+  G.sync();
+  const double sdt = a.B.dt * a.B.beta;
+  for (int t = gt; t < nc * g.c; t += gs) {
+    const int v = t / nc, idx = t - v * nc;
     const int n = cell_of(a, idx);
-    dual R[4];
-    cell_residual<dual>(g, a.B, a.q, V, a.unk, a.qm1, a.qm2, n, R);
-    for (int v = 0; v < g.c; ++v) w[v * g.N + n] = R[v].d;
+    const double* o = a.ff + (int64_t)idx * nf * 4;
+    double L = (o[0 * 4 + v] - o[1 * 4 + v]) / (-g.dx);
+    if (g.dim == 2) L = L - (o[2 * 4 + v] - o[3 * 4 + v]) / g.dy;
+    const int e = v * g.N + n;
+    w[e] = V[e] - sdt * L;  // every listed cell is an unknown: its tangent is V[e]
   }
 }
 
-// entry e of unknown entry index t (t = v * nc + idx)
+// entry e of unknown entry index t, cell-major (t = idx * C + v): no division by the run-time
+// cell count in the vector loops
 __device__ __forceinline__ int entry(const NArgs& a, int nc, int t) {
-  const int v = t / nc, idx = t - v * nc;
+  (void)nc;
+  int idx, v;
+  if (a.g.c == 4) {
+    idx = t >> 2;
+    v = t & 3;
+  } else {
+    idx = t / 3;
+    v = t - 3 * idx;
+  }
   return v * a.g.N + cell_of(a, idx);
 }
 
-// dots <x, V_i> for i < K over the unknown entries -> S.tot[i]
-__device__ void dots_phase(cg::grid_group& G, const NArgs& a, int nc, const double* x, const double* Vb, int K,
+// dots <x, V_i>, i < K, over the unknown entries with each thread's OWN entries (the mapping of
+// the CGS updates and of the norm: no barrier between an update and the next reduction); per
+// vector a warp tree, then the fixed-order block / grid sums of grid_finish
+template <class GS>
+__device__ void dots_phase(const GS& G, const NArgs& a, int nc, const double* x, const double* Vb, int K,
                            NShared& S) {
   const int ne = nc * a.g.c;
   const int64_t D = a.g.D;
+  const int gt = blockIdx.x * NK_T + threadIdx.x, gs = gridDim.x * NK_T;
+  int es[4];
+  int m = 0;
+  for (int t = gt; t < ne && m < 4; t += gs) es[m++] = entry(a, nc, t);
+  const bool more = gt + 4 * gs < ne;  // (not the case for the launch grids used: <= 4 entries each)
   for (int i = 0; i < K; ++i) {
-    double s = 0.0;
-    for (int t = blockIdx.x * NK_T + threadIdx.x; t < ne; t += gridDim.x * NK_T) {
-      const int e = entry(a, nc, t);
-      s = fma(x[e], Vb[i * D + e], s);
-    }
-    s = warp_sum(s);
-    if ((threadIdx.x & 31) == 0) S.red[threadIdx.x >> 5][i] = s;
+    const double* vi = Vb + i * D;
+    double sv = 0.0;
+    for (int k = 0; k < m; ++k) sv = fma(x[es[k]], vi[es[k]], sv);
+    if (more)
+      for (int t = gt + 4 * gs; t < ne; t += gs) {
+        const int e = entry(a, nc, t);
+        sv = fma(x[e], vi[e], sv);
+      }
+    sv = warp_sum(sv);
+    if ((threadIdx.x & 31) == 0) S.red[threadIdx.x >> 5][i] = sv;
   }
   grid_finish(G, S, a.part, K, nullptr);
 }
 
-__device__ double norm2_phase(cg::grid_group& G, const NArgs& a, int nc, const double* x, NShared& S) {
+template <class GS>
+__device__ double norm2_phase(const GS& G, const NArgs& a, int nc, const double* x, NShared& S) {
   const int ne = nc * a.g.c;
   double s = 0.0;
   for (int t = blockIdx.x * NK_T + threadIdx.x; t < ne; t += gridDim.x * NK_T) {
@@ -429,9 +504,12 @@ __device__ double norm2_phase(cg::grid_group& G, const NArgs& a, int nc, const d
   return sqrt(S.tot[0]);
 }
 
+template <bool ONE>
 __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
   if (a.run_if && *a.run_if == 0) return;
-  cg::grid_group G = cg::this_grid();
+  const GSync<ONE> G;
+  const long long t_start = clock64();
+  long long tph[4] = {0, 0, 0, 0};
   __shared__ NShared S;
   const IGeo& g = a.g;
   const int nc = a.ncell_dev ? *a.ncell_dev : a.ncell;
@@ -448,6 +526,10 @@ __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
   bool bad = S.tot[2] > 0.0;
   int it = 0, prods = 0;
   int status = 0;
+  // forcing term: 1e-4 first, then 0.9 (||R_k|| / ||R_k-1||)^2 (Eisenstat-Walker choice 2)
+  // clipped to [rtol, 1e-4], and rtol once ||R||_inf < 1e4 tol; the Jacobian products are
+  // exact, so Newton stays superlinear
+  double eta = 1e-4, r2prev = r2;
   if (bad) status = -2;
   while (status == 0) {
     if (rinf <= a.tol) break;
@@ -458,6 +540,7 @@ __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
     // ---- GMRES(m) for J dq = -R, dq = 0 initially
     for (int t = gt; t < ne; t += gs) a.dq[entry(a, nc, t)] = 0.0;
     const double bnorm = r2;
+    const double tolk = eta * bnorm;  // inexact Newton: GMRES to eta ||R|| (Eisenstat-Walker)
     double beta = r2;
     // V_0 = -R / beta
     for (int t = gt; t < ne; t += gs) {
@@ -469,7 +552,7 @@ __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
       if (!first) {
         // restart: r = -R - J dq
         G.sync();
-        jvp_phase(a, nc, a.dq, a.wv);
+        jvp_phase(G, a, nc, a.dq, a.wv);
         ++prods;
         G.sync();
         for (int t = gt; t < ne; t += gs) {
@@ -478,7 +561,7 @@ __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
         }
         G.sync();
         beta = norm2_phase(G, a, nc, a.wv, S);
-        if (beta <= a.rtol * bnorm) break;
+        if (beta <= tolk) break;
         for (int t = gt; t < ne; t += gs) {
           const int e = entry(a, nc, t);
           a.Vk[e] = a.wv[e] / beta;
@@ -492,22 +575,34 @@ __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
       __syncthreads();
       int j = 0;
       for (; j < kMaxKrylov && prods < a.maxprod; ++j) {
+        long long c0 = clock64();
         G.sync();  // V_j complete
-        jvp_phase(a, nc, a.Vk + j * D, a.wv);
+        jvp_phase(G, a, nc, a.Vk + j * D, a.wv);
         ++prods;
         G.sync();
         // classical Gram-Schmidt, twice (CGS2)
         double h[kMaxKrylov + 1];
         for (int pass = 0; pass < 2; ++pass) {
+          if (pass == 0) {
+            const long long c1 = clock64();
+            tph[0] += c1 - c0;
+            c0 = c1;
+          }
           dots_phase(G, a, nc, a.wv, a.Vk, j + 1, S);
           for (int i = 0; i <= j; ++i) h[i] = (pass ? h[i] : 0.0) + S.tot[i];
           for (int t = gt; t < ne; t += gs) {
             const int e = entry(a, nc, t);
             double wv = a.wv[e];
+#pragma unroll 8
             for (int i = 0; i <= j; ++i) wv = fma(-S.tot[i], a.Vk[i * D + e], wv);
             a.wv[e] = wv;
           }
-          G.sync();
+          // no barrier: the next dots pass and the norm read each thread's own entries
+        }
+        {
+          const long long c1 = clock64();
+          tph[1] += c1 - c0;
+          c0 = c1;
         }
         const double hn = norm2_phase(G, a, nc, a.wv, S);
         if (hn > 0.0)
@@ -534,7 +629,8 @@ __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
           S.gv[j] = S.cs[j] * S.gv[j];
         }
         __syncthreads();
-        if (fabs(S.gv[j + 1]) <= a.rtol * bnorm || S.H[j * kMaxKrylov + j] == 0.0) {
+        tph[2] += clock64() - c0;
+        if (fabs(S.gv[j + 1]) <= tolk || S.H[j * kMaxKrylov + j] == 0.0) {
           ++j;
           break;
         }
@@ -551,13 +647,15 @@ __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
       for (int t = gt; t < ne; t += gs) {
         const int e = entry(a, nc, t);
         double x = a.dq[e];
+#pragma unroll 8
         for (int i = 0; i < j; ++i) x = fma(S.y[i], a.Vk[i * D + e], x);
         a.dq[e] = x;
       }
-      if (fabs(S.gv[j]) <= a.rtol * bnorm || j == 0) break;
+      if (fabs(S.gv[j]) <= tolk || j == 0) break;
     }
     G.sync();
     // ---- line search: q + lambda dq, lambda halved until admissible and ||R||_2 decreases
+    const long long cls = clock64();
     bool accepted = false;
     double lam = 1.0;
     for (int ls = 0; ls <= 12; ++ls, lam *= 0.5) {
@@ -587,12 +685,22 @@ __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
       status = -2;
       break;
     }
+    tph[3] += clock64() - cls;
+    eta = fmax(a.rtol, fmin(1e-4, 0.9 * (r2 / r2prev) * (r2 / r2prev)));
+    if (rinf < 1e4 * a.tol) eta = a.rtol;  // the last steps tight: the root, not just ||R|| <= tol
+    r2prev = r2;
     ++it;
   }
   if (gt == 0) {
     a.stat[0] = status == 0 ? it : status;
     a.stat[1] = prods;
     a.rstat[0] = rinf;
+    if (a.tdbg) {
+      for (int k = 0; k < 4; ++k) a.tdbg[k] += tph[k];
+      a.tdbg[4] += clock64() - t_start;
+      a.tdbg[5] += prods;
+      a.tdbg[6] += 1;
+    }
   }
 }
 
@@ -644,8 +752,9 @@ __device__ __forceinline__ int wrap_or_clamp(int i, int n, bool periodic) {
   return i < 0 ? 0 : (i >= n ? n - 1 : i);
 }
 
+template <bool ONE>
 __global__ void __launch_bounds__(FI_T) imp_filter_kernel(FArgs a) {
-  cg::grid_group G = cg::this_grid();
+  const GSync<ONE> G;
   __shared__ double red[FI_W][2];
   __shared__ double tot[2];
   const IGeo& g = a.g;
@@ -720,11 +829,15 @@ __global__ void __launch_bounds__(FI_T) imp_filter_kernel(FArgs a) {
         a.part[blockIdx.x * 32 + threadIdx.x] = s;
       }
       G.sync();
-      if (threadIdx.x < 2) {
-        double s = a.part[threadIdx.x];
-        for (int b = 1; b < (int)gridDim.x; ++b)
-          s = threadIdx.x ? fmax(s, a.part[b * 32 + 1]) : s + a.part[b * 32];
-        tot[threadIdx.x] = s;
+      if (threadIdx.x < 64) {  // fixed-order cross-block sums: lane l takes blocks l, l + 32, ...
+        const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        double s = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) s = k ? fmax(s, a.part[b * 32 + 1]) : s + a.part[b * 32];
+        for (int o = 16; o > 0; o >>= 1) {
+          const double x = __shfl_xor_sync(0xffffffffu, s, o);
+          s = k ? fmax(s, x) : s + x;
+        }
+        if (lane == 0) tot[k] = s;
       }
       for (int b = gt; b < nb; b += gs)  // apply the kept values
         if (a.keep[b]) {
@@ -836,10 +949,11 @@ struct hrom_imp_ctx {
   // device buffers (plain layout, Dp each)
   double *q1 = nullptr, *q2 = nullptr, *V = nullptr, *qt = nullptr, *R = nullptr, *Rt = nullptr, *dq = nullptr;
   double *Vk = nullptr, *wv = nullptr, *vp = nullptr, *vpp = nullptr, *vorig = nullptr, *part = nullptr;
-  double *yprev = nullptr, *rstat = nullptr;
+  double *yprev = nullptr, *rstat = nullptr, *ff = nullptr;
   uint8_t *flags = nullptr, *keep = nullptr, *kept = nullptr;
   int32_t *list = nullptr, *count = nullptr, *istat = nullptr, *fsweeps = nullptr;
   int* posflag = nullptr;
+  long long* tdbg = nullptr;  // Newton phase clocks (hrom_imp_debug_timers)
   // pinned host mirror of small results
   double* hres = nullptr;   // [0] ||dy||, [1] final ||R||_inf
   int32_t* hint = nullptr;  // [0] newton status, [1] products, [2] positivity flag, [3..5] sweeps
@@ -888,7 +1002,7 @@ hrom_status slot_copy(hrom_imp_ctx* ic, int64_t kk, const double* src_plain, dou
 
 // one Newton-Krylov solve on the unknown cells (cells == nullptr: every cell), state in q
 hrom_status newton(hrom_imp_ctx* c, int order, const double* qm1, const double* qm2, const int32_t* cells,
-                   const int32_t* ncell_dev, const uint8_t* unk, double* q, const int* run_if) {
+                   const int32_t* ncell_dev, const uint8_t* unk, double* q, const int* run_if, int ncells_hint) {
   NArgs a{};
   a.g = c->g;
   a.B = bdf_of(c, order);
@@ -913,15 +1027,25 @@ hrom_status newton(hrom_imp_ctx* c, int order, const double* qm1, const double* 
   a.stat = c->istat;
   a.rstat = c->rstat;
   a.run_if = run_if;
-  void* args[] = {&a};
-  HROM_CK(cudaLaunchCooperativeKernel((void*)newton_kernel, dim3(c->nk_grid), dim3(NK_T), args, 0, c->st));
+  a.ff = c->ff;
+  a.tdbg = c->tdbg;
+  // ~16 cells per block: a small partial system is latency-bound (each face flux is a long
+  // dependent chain), so it is spread over many SMs rather than packed into one block
+  const int grid = std::max(1, std::min(c->nk_grid, (ncells_hint + 15) / 16));
+  if (grid == 1) {
+    newton_kernel<true><<<1, NK_T, 0, c->st>>>(a);
+  } else {
+    void* args[] = {&a};
+    HROM_CK(cudaLaunchCooperativeKernel((void*)newton_kernel<false>, dim3(grid), dim3(NK_T), args, 0, c->st));
+  }
   HROM_LAUNCH_CK();
   ++c->aux->nlaunch;
   return HROM_OK;
 }
 
 hrom_status filter_launch(hrom_imp_ctx* c, int order, const double* qm1, const double* qm2, double* v,
-                          const int32_t* band, const int32_t* nband_dev, uint8_t* kept_cell, double* eps) {
+                          const int32_t* band, const int32_t* nband_dev, uint8_t* kept_cell, double* eps,
+                          int nband_hint) {
   FArgs a{};
   a.g = c->g;
   a.B = bdf_of(c, order);
@@ -942,8 +1066,13 @@ hrom_status filter_launch(hrom_imp_ctx* c, int order, const double* qm1, const d
   a.eps_f = c->P.filter_eps;
   a.part = c->part;
   a.sweeps_out = c->fsweeps;
-  void* args[] = {&a};
-  HROM_CK(cudaLaunchCooperativeKernel((void*)imp_filter_kernel, dim3(c->fi_grid), dim3(FI_T), args, 0, c->st));
+  const int grid = std::max(1, std::min(c->fi_grid, (nband_hint + FI_T - 1) / FI_T));
+  if (grid == 1) {
+    imp_filter_kernel<true><<<1, FI_T, 0, c->st>>>(a);
+  } else {
+    void* args[] = {&a};
+    HROM_CK(cudaLaunchCooperativeKernel((void*)imp_filter_kernel<false>, dim3(grid), dim3(FI_T), args, 0, c->st));
+  }
   HROM_LAUNCH_CK();
   ++c->aux->nlaunch;
   return HROM_OK;
@@ -961,7 +1090,7 @@ hrom_status read_newton(hrom_imp_ctx* c, int* status) {
 // full implicit HDM step into c->V from gamma_{k} (= q1), Alg. 1 line 4
 hrom_status full_solve(hrom_imp_ctx* c, int order) {
   HROM_CK(cudaMemcpyAsync(c->V, c->q1, c->g.D * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
-  hrom_status s = newton(c, order, c->q1, order == 2 ? c->q2 : c->q1, nullptr, nullptr, nullptr, c->V, nullptr);
+  hrom_status s = newton(c, order, c->q1, order == 2 ? c->q2 : c->q1, nullptr, nullptr, nullptr, c->V, nullptr, c->g.N);
   if (s != HROM_OK) return s;
   int st = 0;
   if ((s = read_newton(c, &st)) != HROM_OK) return s;
@@ -983,6 +1112,11 @@ hrom_status hybrid_solve(hrom_imp_ctx* c, int order, int* kind) {
   HROM_LAUNCH_CK();
   const int32_t* Sl = x->b.lists + (int64_t)L_S * xg.N;
   const int32_t* Sn = x->b.counts + L_S;
+  // |S-hat| and |B| on the host: the solve and the filter size their grids by them (one block,
+  // block barriers only, when the set fits)
+  HROM_CK(cudaMemcpyAsync(c->hint + 6, x->b.counts, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
+  HROM_CK(cudaStreamSynchronize(c->st));
+  const int nS = c->hint[6 + L_S], nB = c->hint[6 + L_B];
   HROM_CK(cudaMemcpyAsync(c->V, c->q1, c->g.D * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
   HROM_CK(cudaMemsetAsync(c->yprev, 0, kMaxR * sizeof(double), c->st));
   const int gm = x->P.gather_mode;
@@ -990,7 +1124,7 @@ hrom_status hybrid_solve(hrom_imp_ctx* c, int order, int* kind) {
   bool failed = false;
   int J = 0;
   for (int j = 1; j <= c->I.j_max; ++j) {
-    if ((s = newton(c, order, c->q1, qm2, Sl, Sn, c->flags, c->V, nullptr)) != HROM_OK) break;
+    if ((s = newton(c, order, c->q1, qm2, Sl, Sn, c->flags, c->V, nullptr, nS)) != HROM_OK) break;
     // y = (P^T Phi)^+ P^T (v - psi) on the rows of P (Eq. 8), then v := psi + Phi y off S-hat
     // (S-tilde included: the next subiteration's frozen values, Alg. 1 line 10)
     if ((s = gram_gathered(x, plain(c->V))) != HROM_OK) break;
@@ -1019,7 +1153,7 @@ hrom_status hybrid_solve(hrom_imp_ctx* c, int order, int* kind) {
     // filter gated by the implicit residual on the band, indicator on kept cells
     if (c->P.n_filter_orders > 0 && c->P.filter_max_sweeps > 0) {
       if ((s = filter_launch(c, order, c->q1, qm2, c->V, x->b.lists + (int64_t)L_B * xg.N, x->b.counts + L_B, c->kept,
-                             x->b.eps)) != HROM_OK)
+                             x->b.eps, nB)) != HROM_OK)
         return s;
     }
     HROM_CK(cudaMemsetAsync(c->posflag, 0, sizeof(int), c->st));
@@ -1082,10 +1216,10 @@ hrom_status hrom_imp_create(const hrom_grid* grid, double gamma, const hrom_para
   }
   // cooperative grids: one block per SM at most, and no more blocks than the work needs
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, newton_kernel, NK_T, 0);
-  const int want = std::max(1, std::min(64, (g.N + 127) / 128));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, newton_kernel<false>, NK_T, 0);
+  const int want = std::max(1, std::min(c->nsm, (g.N + 15) / 16));
   c->nk_grid = std::max(1, std::min(want, occ * c->nsm));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, imp_filter_kernel, FI_T, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, imp_filter_kernel<false>, FI_T, 0);
   c->fi_grid = std::max(1, std::min(want, occ * c->nsm));
   bool ok = true;
   auto al = [&](auto** ptr, size_t n) {
@@ -1097,6 +1231,7 @@ hrom_status hrom_imp_create(const hrom_grid* grid, double gamma, const hrom_para
   al(&c->Vk, vb * (kMaxKrylov + 1)); al(&c->wv, vb); al(&c->vp, vb); al(&c->vpp, vb); al(&c->vorig, vb);
   al(&c->part, 64 * 32 * sizeof(double) + 4096 * sizeof(double));
   al(&c->yprev, kMaxR * sizeof(double));
+  al(&c->ff, (size_t)16 * g.N * sizeof(double));
   al(&c->rstat, 4 * sizeof(double));
   al(&c->flags, g.N);
   al(&c->keep, g.N);
@@ -1106,8 +1241,9 @@ hrom_status hrom_imp_create(const hrom_grid* grid, double gamma, const hrom_para
   al(&c->istat, 4 * sizeof(int32_t));
   al(&c->fsweeps, 4 * sizeof(int32_t));
   al(&c->posflag, 4 * sizeof(int));
+  al(&c->tdbg, 8 * sizeof(long long));
   if (cudaMallocHost((void**)&c->hres, 4 * sizeof(double)) != cudaSuccess) ok = false;
-  if (cudaMallocHost((void**)&c->hint, 8 * sizeof(int32_t)) != cudaSuccess) ok = false;
+  if (cudaMallocHost((void**)&c->hint, 16 * sizeof(int32_t)) != cudaSuccess) ok = false;
   if (!ok) {
     hrom_imp_destroy(c);
     return HROM_E_NOMEM;
@@ -1121,8 +1257,8 @@ void hrom_imp_destroy(hrom_imp_ctx* c) {
   if (c->st) cudaStreamSynchronize(c->st);
   for (void* ptr : {(void*)c->q1, (void*)c->q2, (void*)c->V, (void*)c->qt, (void*)c->R, (void*)c->Rt, (void*)c->dq,
                     (void*)c->Vk, (void*)c->wv, (void*)c->vp, (void*)c->vpp, (void*)c->vorig, (void*)c->part,
-                    (void*)c->yprev, (void*)c->rstat, (void*)c->flags, (void*)c->keep, (void*)c->kept, (void*)c->list,
-                    (void*)c->count, (void*)c->istat, (void*)c->fsweeps, (void*)c->posflag})
+                    (void*)c->yprev, (void*)c->rstat, (void*)c->ff, (void*)c->flags, (void*)c->keep, (void*)c->kept, (void*)c->list,
+                    (void*)c->count, (void*)c->istat, (void*)c->fsweeps, (void*)c->posflag, (void*)c->tdbg})
     if (ptr) cudaFree(ptr);
   if (c->hres) cudaFreeHost(c->hres);
   if (c->hint) cudaFreeHost(c->hint);
@@ -1244,9 +1380,12 @@ hrom_status hrom_imp_newton(hrom_imp_ctx* c, int32_t order, const double* dev_qm
     HROM_LAUNCH_CK();
     list_from_flags_kernel<<<1, 1024, 0, c->st>>>(c->g.N, c->flags, c->list, c->count);
     HROM_LAUNCH_CK();
-    s = newton(c, order, dev_qm1, order == 2 ? dev_qm2 : dev_qm1, c->list, c->count, c->flags, dev_q, nullptr);
+    HROM_CK(cudaMemcpyAsync(c->hint + 6, c->count, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
+    HROM_CK(cudaStreamSynchronize(c->st));
+    s = newton(c, order, dev_qm1, order == 2 ? dev_qm2 : dev_qm1, c->list, c->count, c->flags, dev_q, nullptr,
+               c->hint[6]);
   } else {
-    s = newton(c, order, dev_qm1, order == 2 ? dev_qm2 : dev_qm1, nullptr, nullptr, nullptr, dev_q, nullptr);
+    s = newton(c, order, dev_qm1, order == 2 ? dev_qm2 : dev_qm1, nullptr, nullptr, nullptr, dev_q, nullptr, c->g.N);
   }
   if (s != HROM_OK) return s;
   int st = 0;
@@ -1263,14 +1402,24 @@ hrom_status hrom_imp_filter(hrom_imp_ctx* c, int32_t order, const double* dev_qm
   hrom_status s;
   if ((s = build_sets(x, dev_mask)) != HROM_OK) return s;
   x->sets_ready = true;
+  HROM_CK(cudaMemcpyAsync(c->hint + 6, x->b.counts + L_B, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
+  HROM_CK(cudaStreamSynchronize(c->st));
   if ((s = filter_launch(c, order, dev_qm1, order == 2 ? dev_qm2 : dev_qm1, dev_v, x->b.lists + (int64_t)L_B * x->g.N,
-                         x->b.counts + L_B, dev_kept_out ? dev_kept_out : c->kept, nullptr)) != HROM_OK)
+                         x->b.counts + L_B, dev_kept_out ? dev_kept_out : c->kept, nullptr, c->hint[6])) != HROM_OK)
     return s;
   if (host_sweeps) {
     HROM_CK(cudaMemcpyAsync(c->hint + 3, c->fsweeps, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
     HROM_CK(cudaStreamSynchronize(c->st));
     for (int i = 0; i < 3; ++i) host_sweeps[i] = i < c->P.n_filter_orders ? c->hint[3 + i] : 0;
   }
+  return HROM_OK;
+}
+
+hrom_status hrom_imp_debug_timers(hrom_imp_ctx* c, int64_t* host_out) {
+  if (!c || !host_out) return HROM_E_INVALID;
+  HROM_CK(cudaMemcpyAsync(host_out, c->tdbg, 8 * sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+  HROM_CK(cudaStreamSynchronize(c->st));
+  HROM_CK(cudaMemsetAsync(c->tdbg, 0, 8 * sizeof(long long), c->st));
   return HROM_OK;
 }
 

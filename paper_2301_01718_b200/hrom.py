@@ -109,6 +109,7 @@ _SIGS = {
     "hrom_imp_filter": (C.c_int, [_VP, C.c_int32, _VP, _VP, _VP, _VP, _VP, C.POINTER(C.c_int32)]),
     "hrom_imp_set_window": (C.c_int, [_VP, C.c_int64, _VP, C.c_int32, _VP]),
     "hrom_imp_get_band": (C.c_int, [_VP, _VP, _VP]),
+    "hrom_imp_debug_timers": (C.c_int, [_VP, _VP]),
 }
 
 SECTIONS = ["dt", "masked_rk3", "gathered_gram", "pinv_solve", "fill_pass", "indicator", "seam_filter",
@@ -486,6 +487,13 @@ class ImplicitROM:
         _ck(self.lib.hrom_imp_filter(self.h, order, _ptr(qm1), _ptr(qm2), _ptr(mask), _ptr(v), _ptr(kept),
                                      C.cast(sw, C.POINTER(C.c_int32))), "hrom_imp_filter")
         return kept, list(sw)
+
+    def debug_timers(self):
+        """Newton phase clocks since the last read (block 0, clock64 cycles): products, Gram-Schmidt,
+        norms + Givens, line searches, whole kernels, products, solves."""
+        out = (C.c_int64 * 8)()
+        _ck(self.lib.hrom_imp_debug_timers(self.h, C.cast(out, C.c_void_p)), "hrom_imp_debug_timers")
+        return list(out)[:7]
 
     def band(self):
         """Cells of the filter band of the current sets (ascending)."""
