@@ -281,6 +281,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   A(dalloc(&b.zvec, kMaxW));
   A(dalloc(&b.eigV, (size_t)kMaxSlots * kMaxSlots));
   A(dalloc(&b.eigA, (size_t)5 * kMaxSlots * (kMaxSlots + 1)));  // eigen-solve LU workspace when not in smem
+  A(dalloc(&b.eigZ, (size_t)kMaxSlots * (kMaxSlots + 1)));      // eigenvectors when not in smem (w = 128)
   A(dalloc(&b.ireg, 16));
   A(dalloc(&b.dreg, 16));
   A(dalloc(&b.ureg, 4));
@@ -361,7 +362,7 @@ void hrom_destroy(hrom_ctx* c) {
   if (c->ev_g1) cudaEventDestroy(c->ev_g1);
   Bufs& b = c->b;
   void* ptrs[] = {b.ring, b.U1, b.U2, b.U3, b.Vorig, b.eps, b.eps_elem, b.masks, b.lists, b.counts,
-                  b.kept, b.fidx, b.ftab, b.fcur, b.fF, b.C, b.Clo, b.Rlo, b.Mdd, b.Zf, b.rfws, b.Tg, b.part, b.gpart, b.K, b.Khi, b.Klo, b.Rd, b.vpart, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.ireg,
+                  b.kept, b.fidx, b.ftab, b.fcur, b.fF, b.C, b.Clo, b.Rlo, b.Mdd, b.Zf, b.rfws, b.Tg, b.part, b.gpart, b.K, b.Khi, b.Klo, b.Rd, b.vpart, b.A, b.lam, b.y, b.cvec, b.zvec, b.eigV, b.eigA, b.eigZ, b.ireg,
                   b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.hsum, b.fstat, b.l1part, b.fcnt, (void*)b.colptr, b.slot_tab, b.ochosen, b.ocoef, b.orows, b.orows_pub, b.opart_v, b.opart_e, b.ocnt, b.ocells, b.ophi};
   for (void* q : ptrs)
     if (q) cudaFree(q);

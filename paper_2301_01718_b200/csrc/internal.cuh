@@ -121,6 +121,8 @@ struct Bufs {
   double* zvec = nullptr;     // w (bootstrap projection coefficients)
   double* eigV = nullptr;     // kMaxSlots^2 scratch (eigenvectors when not in smem)
   double* eigA = nullptr;     // kMaxSlots^2 scratch
+  double* eigZ = nullptr;     // kMaxSlots (kMaxSlots + 1): the basis eigen-solve's eigenvectors when
+                              // they do not fit shared memory (w = 128)
   int32_t* ireg = nullptr;    // small int registers: [0] reff, [1] err cell lo, ...
   double* dreg = nullptr;     // small double registers: [0] dt, ...
   unsigned long long* ureg = nullptr;  // [0] smax bits, [1] latched min bad cell, [2] fused smax, [3] step flag

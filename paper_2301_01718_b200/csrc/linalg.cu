@@ -1012,14 +1012,18 @@ __global__ void __launch_bounds__(256) gram_reduce_dd(const double* __restrict__
 struct EigLayout {
   int ldn, ldz;
   bool fac_smem;
-  size_t doubles;  // dynamic smem doubles (matrix + Z + vectors [+ LU workspace])
+  bool z_smem;     // eigenvectors in shared memory (else the caller's global gz: w = 128 windows)
+  size_t doubles;  // dynamic smem doubles (matrix [+ Z] + vectors [+ LU workspace])
   size_t bytes;
 };
 __host__ __device__ inline EigLayout eig_layout(int n, int nvec_cap) {
   EigLayout L;
   L.ldn = n + (n & 1) + 1;  // odd strides: column accesses are bank-conflict free
   L.ldz = nvec_cap | 1;
-  const size_t base = (size_t)L.ldn * L.ldn + (size_t)n * L.ldz + 8 * kMaxSlots + 64;
+  const size_t zsz = (size_t)n * L.ldz;
+  const size_t core = (size_t)L.ldn * L.ldn + 8 * kMaxSlots + 64;
+  L.z_smem = (core + zsz) * 8 <= 216 * 1024;
+  const size_t base = core + (L.z_smem ? zsz : 0);
   const size_t fac = (size_t)4 * n * L.ldz + ((size_t)n * L.ldz + 7) / 8;
   L.fac_smem = (base + fac) * 8 <= 216 * 1024;
   L.doubles = base + (L.fac_smem ? fac : 0);
@@ -1027,17 +1031,22 @@ __host__ __device__ inline EigLayout eig_layout(int n, int nvec_cap) {
   return L;
 }
 // dynamic doubles of the eigen-solve workspace with the LU factors in (fac_smem) or out of smem
-__host__ __device__ inline size_t eig_doubles(int n, int nvec_cap, bool fac_smem) {
+__host__ __device__ inline size_t eig_doubles(int n, int nvec_cap, bool fac_smem, bool z_global = false) {
   const EigLayout L = eig_layout(n, nvec_cap);
-  const size_t base = (size_t)L.ldn * L.ldn + (size_t)n * L.ldz + 8 * kMaxSlots + 64;
+  const bool zs = L.z_smem && !z_global;
+  const size_t core = (size_t)L.ldn * L.ldn + 8 * kMaxSlots + 64 + (zs ? (size_t)n * L.ldz : 0);
   const size_t fac = (size_t)4 * n * L.ldz + ((size_t)n * L.ldz + 7) / 8;
-  return base + (fac_smem ? fac : 0);
+  return core + (fac_smem ? fac : 0);
 }
-__device__ inline EigWork eig_work(double* sm, int n, const EigLayout& L, double* gfac) {
+__device__ inline EigWork eig_work(double* sm, int n, const EigLayout& L, double* gfac, double* gz = nullptr) {
   EigWork W;
   double* p = sm + (size_t)L.ldn * L.ldn;
-  W.Z = p;
-  p += (size_t)n * L.ldz;
+  if (L.z_smem) {
+    W.Z = p;
+    p += (size_t)n * L.ldz;
+  } else {
+    W.Z = gz;
+  }
   W.ldz = L.ldz;
   W.d = p; p += kMaxSlots;
   W.e = p; p += kMaxSlots;
@@ -1057,13 +1066,14 @@ __device__ inline EigWork eig_work(double* sm, int n, const EigLayout& L, double
 __global__ void __launch_bounds__(512) basis_kernel(const double* __restrict__ C, const double* __restrict__ Clo,
                                                     int ldc, Win W, double* __restrict__ Mh, double* __restrict__ Ml,
                                                     double* __restrict__ Zf, double* __restrict__ lam_out,
-                                                    int32_t* __restrict__ reff_out, double* __restrict__ gfac) {
+                                                    int32_t* __restrict__ reff_out, double* __restrict__ gfac,
+                                                    double* __restrict__ gz) {
   extern __shared__ double sm[];
   const int w = W.w, nU = W.nU;
   const EigLayout L = eig_layout(w, w);
   const int ldn = L.ldn;
   double* M = sm;
-  const EigWork E = eig_work(sm, w, L, gfac);
+  const EigWork E = eig_work(sm, w, L, gfac, gz);
   double* mrow = E.lam + kMaxSlots;  // kMaxSlots: m_i (hi)
   double* mrowl = mrow + kMaxSlots;  // kMaxSlots: m_i (lo)
   __shared__ double msum[2 * kMaxSlots];
@@ -1502,7 +1512,7 @@ __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ 
                                                      double* __restrict__ y_out, double* __restrict__ c_out,
                                                      int32_t* __restrict__ status, double* __restrict__ gfac,
                                                      bool fac_smem, double* __restrict__ Kg, double* __restrict__ Tg,
-                                                     long long* tdbg) {
+                                                     long long* tdbg, double* __restrict__ gz) {
   extern __shared__ double sm[];
   int ts = 0;
   sstamp(tdbg, ts);
@@ -1511,7 +1521,8 @@ __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ 
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   EigLayout L = eig_layout(re > 0 ? re : 1, re > 0 ? re : 1);
   L.fac_smem = fac_smem;  // the host sized the smem for r >= r_eff: its choice is safe
-  const SolveLayout S = solve_layout(w, r, Kg != nullptr, Tg != nullptr, eig_doubles(r, r, fac_smem));
+  if (gz) L.z_smem = false;  // eigenvectors in global memory (w = 128, r = 64: config 5)
+  const SolveLayout S = solve_layout(w, r, Kg != nullptr, Tg != nullptr, eig_doubles(r, r, fac_smem, gz != nullptr));
   const size_t ka = (size_t)(w + 1) * (w + 1), ta = (size_t)(w + 1) * r;
   double* As = sm + S.as;  // As[j * lda + i] = A[j * w + i]
   double* Kh = S.kg ? Kg : sm + S.kh;
@@ -1533,7 +1544,7 @@ __global__ void __launch_bounds__(SV_T) solve_kernel(const double* __restrict__ 
   double* res = misc + kMaxSlots;
   double* wtr = res + kMaxSlots;  // per-warp partials (2 SV_W)
   double* Ge = sm + S.eig;        // eigen route: matrix + workspace over region X
-  const EigWork E = eig_work(Ge, re > 0 ? re : 1, L, gfac);
+  const EigWork E = eig_work(Ge, re > 0 ? re : 1, L, gfac, gz);
   const int ldn = L.ldn;
   __shared__ double gm[6];
   __shared__ int s_fast;
@@ -2140,13 +2151,15 @@ hrom_status small_solve(hrom_ctx* c) {
   if (S.total > lim) S = solve_layout(w, r, kg = true, tg, eig_doubles(r, r, fac));  // wide windows: K in global
   if (S.total > lim) S = solve_layout(w, r, kg, tg = true, eig_doubles(r, r, fac));  // ... and T
   if (S.total > lim) S = solve_layout(w, r, kg, tg, eig_doubles(r, r, fac = false));  // ... and the eigen LU
+  bool zg = false;  // ... and the eigenvectors of the eigen route (the double-double G, g need the room)
+  if (S.total > lim) S = solve_layout(w, r, kg, tg, eig_doubles(r, r, fac, zg = true));
   if (S.total > lim) return HROM_E_INVALID;
   const size_t smem = S.total * sizeof(double);
   HROM_CK(cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   solve_kernel<<<1, SV_T, smem, c->st>>>(c->b.eigV, c->b.Rlo, c->win, r, c->b.A, c->b.ireg, c->P.lsq_rel_cutoff,
                                          c->b.y, c->b.cvec, c->b.ireg + 2, c->b.eigA, fac,
                                          kg ? c->b.K : nullptr, tg ? c->b.Tg : nullptr,
-                                         c->prof ? c->b.dbg + 64 : nullptr);
+                                         c->prof ? c->b.dbg + 64 : nullptr, zg ? c->b.eigZ : nullptr);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;
@@ -2159,7 +2172,7 @@ hrom_status basis_from_gram(hrom_ctx* c, const Win& W) {
   double* Mh = c->b.Mdd;
   double* Ml = c->b.Mdd + (size_t)kMaxSlots * kMaxSlots;
   basis_kernel<<<1, 512, smem, c->st>>>(c->b.C, c->b.Clo, kMaxSlots, W, Mh, Ml, c->b.Zf, c->b.lam, c->b.ireg,
-                                        c->b.eigA);
+                                        c->b.eigA, c->b.eigZ);
   HROM_LAUNCH_CK();
   size_t rsm = (size_t)5 * W.w * (W.w | 1) * sizeof(double);
   double* gws = nullptr;

@@ -131,9 +131,10 @@ def _replay_case(orc, inputs, wl, seed=5, frac=0.12, amp=0.03):
 
 
 @pytest.mark.parametrize("kw", [dict(), dict(bc=1, nx=64, ny=40), dict(dim=1, nx=500, ny=1, recon=1, w=12, r=6),
-                                dict(w=90, r=20, nx=48, ny=40), dict(W=-1), dict(W=-1, bc=1, nx=64, ny=40)],
-                         ids=["2d-transmissive", "2d-periodic", "1d", "2d-wide-window", "2d-whole-domain-filter",
-                              "2d-periodic-whole-domain-filter"])
+                                dict(w=90, r=20, nx=48, ny=40), dict(w=128, r=64, nx=48, ny=40, bc=1),
+                                dict(W=-1), dict(W=-1, bc=1, nx=64, ny=40)],
+                         ids=["2d-transmissive", "2d-periodic", "1d", "2d-wide-window", "2d-w128-config5-window",
+                              "2d-whole-domain-filter", "2d-periodic-whole-domain-filter"])
 def test_hybrid_step_replay_parity(orc, inputs, kw):
     """One hybrid step from the same window and S-hat on both sides (Alg. 1)."""
     wl = small2d(inputs, **kw)
