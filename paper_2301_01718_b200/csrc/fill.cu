@@ -119,15 +119,14 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   const uint32_t tile_bytes = (uint32_t)(nsr * TILE * sizeof(double));
 
   // producer role: thread 0 keeps FILL_STAGES slab tiles in flight, one bulk copy each
-  auto issue = [&](int it2) {
+  auto issue = [&](int it2, int st) {  // st = it2 mod nstage (tracked by the caller)
     const int64_t tile = first + (int64_t)it2 * gridDim.x;
     if (tile >= ntiles) return;
-    const int st = it2 % a.nstage;
     mbar_expect(&full[st], tile_bytes);
     bulk_g2s(stage0 + st * stage_elems, a.ring + tile * nsr * TILE, tile_bytes, &full[st]);
   };
   if (tid == 0)
-    for (int q = 0; q < a.nstage; ++q) issue(q);
+    for (int q = 0; q < a.nstage; ++q) issue(q, q);
 
   // ---------------- compute warps: DOF el = grp*32 + lane, physical slots [q0, q0 + SQ)
   const int el = grp * 32 + lane;
@@ -181,15 +180,17 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   };
   fetch(first);
   int it = 0;
+  int st = 0;            // stage of tile it (it mod nstage) and the parity of its use
+  uint32_t sphase = 0;   // ((it / nstage) & 1), tracked without divisions
   for (int64_t tile = first; tile < ntiles; tile += gridDim.x, ++it) {
-    const int st = it % a.nstage, par = it & 1;
+    const int par = it & 1;
 
     const int64_t e = tile * TILE + el;
     const bool valid = e < g.D;
     if (qq == 1) xflag[par][grp][lane] = (uint8_t)(((wS >> bitpos) & 1u) | (((wB >> bitpos) & 1u) << 1));
     if (qq == 2) xside[par][grp][lane] = pre;
     fetch(tile + gridDim.x);
-    mbar_wait(&full[st], (uint32_t)((it / a.nstage) & 1));
+    mbar_wait(&full[st], sphase);
     const double* T = stage0 + st * stage_elems + el;
     const double rh = T[roff];
     // pass 1 on this quarter's physical slots (x = gamma - rho; re-read in pass 2):
@@ -258,8 +259,12 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
       if (atomicAdd(&srel[st], 1) == NCW - 1) {
         srel[st] = 0;
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        issue(it + a.nstage);
+        issue(it + a.nstage, st);
       }
+    }
+    if (++st == a.nstage) {
+      st = 0;
+      sphase ^= 1u;
     }
   }
   if constexpr (GRAM) {
