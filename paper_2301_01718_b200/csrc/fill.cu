@@ -160,20 +160,43 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
   uint32_t wS = 0, wB = 0;
   int bitpos = 0;
   double pre = 0.0;
+  // quarter 1's cell (n = e mod N, column i, row j) of the next fetched DOF, advanced by the grid
+  // stride each tile without divisions (32-bit unsigned arithmetic: D < 2^31, hrom_create)
+  unsigned fn = 0, fi = 0, fj = 0, sN = 0, sdi = 0, sdj = 0;
+  if (qq == 1 && a.mode == MODE_FILL) {
+    const unsigned e0 = (unsigned)(first * TILE + el), N = (unsigned)g.N, nx = (unsigned)g.nx;
+    fn = e0 % N;
+    fi = fn % nx;
+    fj = fn / nx;
+    sN = (unsigned)(((uint64_t)gridDim.x * TILE) % N);
+    sdi = sN % nx;
+    sdj = sN / nx;
+  }
   auto fetch = [&](int64_t tile) {
     const int64_t e = tile * TILE + el;
     wS = wB = 0;
     pre = 0.0;
-    if (tile >= ntiles || e >= g.D || a.mode == MODE_PROJ) return;
     if (qq == 1 && a.mode == MODE_FILL) {
-      // 32-bit unsigned index arithmetic (D < 2^31, hrom_create)
-      const unsigned n = (unsigned)e % (unsigned)g.N;
-      const unsigned i = n % (unsigned)g.nx, j = n / (unsigned)g.nx;
+      const unsigned i = fi, j = fj;
+      // advance to the DOF of tile + gridDim.x: n += s mod N (rows carry, a wrap past N restarts them)
+      fn += sN;
+      fi += sdi;
+      fj += sdj;
+      if (fi >= (unsigned)g.nx) {
+        fi -= (unsigned)g.nx;
+        ++fj;
+      }
+      if (fn >= (unsigned)g.N) {
+        fn -= (unsigned)g.N;
+        fj -= (unsigned)g.ny;
+      }
+      if (tile >= ntiles || e >= g.D) return;
       const unsigned wi = j * (unsigned)g.wpr + (i >> 5);
       bitpos = (int)(i & 31);
       wS = a.mS[wi];
       if (a.mB) wB = a.mB[wi];
     } else if (qq == 2) {
+      if (tile >= ntiles || e >= g.D || a.mode == MODE_PROJ) return;
       pre = a.mode == MODE_FILL ? a.src_S.p[sidx(a.src_S, e)]  // read unconditionally; used on S-hat only
                                 : a.out.p[sidx(a.out, e)];
     }
