@@ -100,9 +100,13 @@ __global__ void __launch_bounds__(1024) l1_final_kernel(const double* __restrict
   }
 }
 
+// every workspace starts zeroed: a context's results never depend on what an earlier allocation
+// left in the memory (two runs are bitwise identical whatever ran before them)
 template <typename T>
 hrom_status dalloc(T** p, size_t n) {
-  if (cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) return HROM_E_NOMEM;
+  const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+  if (cudaMalloc((void**)p, bytes) != cudaSuccess) return HROM_E_NOMEM;
+  if (cudaMemset(*p, 0, bytes) != cudaSuccess) return HROM_E_CUDA;
   return HROM_OK;
 }
 

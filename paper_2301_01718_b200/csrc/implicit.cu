@@ -285,7 +285,7 @@ __device__ __forceinline__ bool admissible_cell(const IGeo& g, const double* U) 
 }
 
 // ---------------- the Newton-Krylov solve (one cooperative kernel) ----------------
-constexpr int NK_T = 512, NK_W = NK_T / 32;
+constexpr int NK_T = 256, NK_W = NK_T / 32;  // 256: up to 255 registers (dual-number face fluxes)
 constexpr int kMaxKrylov = 30;  // GMRES restart length
 
 struct NArgs {
@@ -320,6 +320,7 @@ struct NShared {
   double cs[kMaxKrylov], sn[kMaxKrylov], gv[kMaxKrylov + 1], y[kMaxKrylov];
   double red[NK_W][32];
   double tot[32];
+  double hcol[kMaxKrylov + 1];  // Arnoldi column j (both Gram-Schmidt passes), thread 0
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -581,7 +582,6 @@ __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
         ++prods;
         G.sync();
         // classical Gram-Schmidt, twice (CGS2)
-        double h[kMaxKrylov + 1];
         for (int pass = 0; pass < 2; ++pass) {
           if (pass == 0) {
             const long long c1 = clock64();
@@ -589,7 +589,8 @@ __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
             c0 = c1;
           }
           dots_phase(G, a, nc, a.wv, a.Vk, j + 1, S);
-          for (int i = 0; i <= j; ++i) h[i] = (pass ? h[i] : 0.0) + S.tot[i];
+          if (threadIdx.x == 0)
+            for (int i = 0; i <= j; ++i) S.hcol[i] = (pass ? S.hcol[i] : 0.0) + S.tot[i];
           for (int t = gt; t < ne; t += gs) {
             const int e = entry(a, nc, t);
             double wv = a.wv[e];
@@ -612,7 +613,7 @@ __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
           }
         // Givens rotations on column j (identical in every block)
         if (threadIdx.x == 0) {
-          for (int i = 0; i <= j; ++i) S.H[i * kMaxKrylov + j] = h[i];
+          for (int i = 0; i <= j; ++i) S.H[i * kMaxKrylov + j] = S.hcol[i];
           S.H[(j + 1) * kMaxKrylov + j] = hn;
           for (int i = 0; i < j; ++i) {
             const double x0 = S.H[i * kMaxKrylov + j], x1 = S.H[(i + 1) * kMaxKrylov + j];
