@@ -306,7 +306,8 @@ hrom_status hrom_imp_filter(hrom_imp_ctx* ctx, int32_t order, const double* dev_
                             const uint32_t* dev_mask, double* dev_v, uint8_t* dev_kept_out, int32_t* host_sweeps);
 /* measurement hook: block 0's clock64 sums since the last read over the Newton solves:
  * [0] Jacobian products (incl. barriers), [1] Gram-Schmidt, [2] norms + Givens, [3] line
- * searches, [4] whole kernels, [5] products, [6] solves; then resets them */
+ * searches, [4] whole kernels, [5] products, [6] solves, [7] block 0 thread 0's own face tasks,
+ * [8] its wait at the barrier after them; host_out: 10 values; then resets them */
 hrom_status hrom_imp_debug_timers(hrom_imp_ctx* ctx, int64_t* host_out);
 /* the filter band of the current sets (ascending cells; N int32 + count) */
 hrom_status hrom_imp_get_band(hrom_imp_ctx* ctx, int32_t* any_list, int32_t* any_count);

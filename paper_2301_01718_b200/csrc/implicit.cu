@@ -52,9 +52,12 @@ __device__ __forceinline__ dual operator+(dual a, dual b) { return {a.v + b.v, a
 __device__ __forceinline__ dual operator-(dual a, dual b) { return {a.v - b.v, a.d - b.d}; }
 __device__ __forceinline__ dual operator-(dual a) { return {-a.v, -a.d}; }
 __device__ __forceinline__ dual operator*(dual a, dual b) { return {a.v * b.v, a.d * b.v + a.v * b.d}; }
+// one division per dual division: only the tangents of dual results are used (Jacobian products,
+// accurate far beyond the GMRES tolerance with a reciprocal), the values come from the double path
 __device__ __forceinline__ dual operator/(dual a, dual b) {
-  const double q = a.v / b.v;
-  return {q, (a.d - q * b.d) / b.v};
+  const double r = 1.0 / b.v;
+  const double q = a.v * r;
+  return {q, (a.d - q * b.d) * r};
 }
 __device__ __forceinline__ dual operator*(double s, dual a) { return {s * a.v, s * a.d}; }
 __device__ __forceinline__ dual operator+(double s, dual a) { return {s + a.v, a.d}; }
@@ -64,7 +67,7 @@ __device__ __forceinline__ double val(dual a) { return a.v; }
 __device__ __forceinline__ double tsqrt(double a) { return sqrt(a); }
 __device__ __forceinline__ dual tsqrt(dual a) {
   const double s = sqrt(a.v);
-  return {s, a.d / (2.0 * s)};
+  return {s, (0.5 * a.d) / s};
 }
 __device__ __forceinline__ double tabs(double a) { return fabs(a); }
 __device__ __forceinline__ dual tabs(dual a) { return a.v < 0.0 ? -a : a; }
@@ -112,9 +115,14 @@ __device__ __forceinline__ void load_cell(const IGeo& g, const double* q, const 
     j = DIM == 2 ? (j < 0 ? 0 : (j >= g.ny ? g.ny - 1 : j)) : 0;
   }
   const int n = j * g.nx + i;
+  // the tangent loads do not wait for the unknown flag (no control dependency): V of a frozen
+  // cell is read and discarded
+  double vt[DIM + 2];
+#pragma unroll
+  for (int v = 0; v < DIM + 2; ++v) vt[v] = V ? V[v * g.N + n] : 0.0;
   const bool tan = V && (!unk || (unk[n] & 1));
 #pragma unroll
-  for (int v = 0; v < DIM + 2; ++v) U[v] = tmk<T>(q[v * g.N + n], tan ? V[v * g.N + n] : 0.0);
+  for (int v = 0; v < DIM + 2; ++v) U[v] = tmk<T>(q[v * g.N + n], tan ? vt[v] : 0.0);
   if (fx) U[1] = -U[1];
   if (DIM == 2 && fy) U[2] = -U[2];
 }
@@ -410,12 +418,14 @@ __device__ void residual_phase(const NArgs& a, int nc, const double* s, double* 
 template <int DIM>
 __device__ __forceinline__ void face_tangent(const NArgs& a, const double* V, int n, int f, double* out) {
   const IGeo& g = a.g;
-  const int i = n % g.nx, j = n / g.nx;
+  int i = n % g.nx, j = n / g.nx;
+  if (f == 1) --i;
+  else if (f == 3) --j;
   dual F[DIM + 2];
-  if (f == 0) face_flux<dual, DIM, 0>(g, a.q, V, a.unk, i, j, F);
-  else if (f == 1) face_flux<dual, DIM, 0>(g, a.q, V, a.unk, i - 1, j, F);
-  else if (DIM == 2 && f == 2) face_flux<dual, DIM, DIM - 1>(g, a.q, V, a.unk, i, j, F);
-  else face_flux<dual, DIM, DIM - 1>(g, a.q, V, a.unk, i, j - 1, F);
+  // two call sites (one per axis), not four: the dual-number Roe flux is long straight-line code,
+  // and a per-face copy of it overflowed the instruction cache (~25 us per face task)
+  if (DIM == 1 || f < 2) face_flux<dual, DIM, 0>(g, a.q, V, a.unk, i, j, F);
+  else face_flux<dual, DIM, DIM - 1>(g, a.q, V, a.unk, i, j, F);
 #pragma unroll
   for (int v = 0; v < DIM + 2; ++v) out[v] = F[v].d;
 }
@@ -425,17 +435,23 @@ __device__ __forceinline__ void face_tangent(const NArgs& a, const double* V, in
 // of Roe arithmetic; with one thread per cell a small partial system waits on their latency),
 // then one thread per unknown entry combines them as cell_residual does.
 template <class GS>
-__device__ void jvp_phase(const GS& G, const NArgs& a, int nc, const double* V, double* w) {
+__device__ void jvp_phase(const GS& G, const NArgs& a, int nc, const double* V, double* w, long long* tj = nullptr) {
   const IGeo& g = a.g;
   const int nf = 2 * g.dim;
   const int gt = blockIdx.x * NK_T + threadIdx.x, gs = gridDim.x * NK_T;
+  const long long c0 = clock64();
   for (int t = gt; t < nc * nf; t += gs) {
     const int idx = t / nf, f = t - idx * nf;
     double* o = a.ff + (int64_t)t * 4;
     if (g.dim == 2) face_tangent<2>(a, V, cell_of(a, idx), f, o);
     else face_tangent<1>(a, V, cell_of(a, idx), f, o);
   }
+  const long long c1 = clock64();
   G.sync();
+  if (tj) {
+    tj[0] += c1 - c0;          // this thread's face task
+    tj[1] += clock64() - c1;   // waiting for the other blocks' tasks + the barrier
+  }
   const double sdt = a.B.dt * a.B.beta;
   for (int t = gt; t < nc * g.c; t += gs) {
     const int v = t / nc, idx = t - v * nc;
@@ -476,10 +492,13 @@ __device__ void dots_phase(const GS& G, const NArgs& a, int nc, const double* x,
   int m = 0;
   for (int t = gt; t < ne && m < 4; t += gs) es[m++] = entry(a, nc, t);
   const bool more = gt + 4 * gs < ne;  // (not the case for the launch grids used: <= 4 entries each)
-  for (int i = 0; i < K; ++i) {
+  double xs[4];
+  for (int k = 0; k < m; ++k) xs[k] = x[es[k]];
+#pragma unroll 4
+  for (int i = 0; i < K; ++i) {  // unrolled: four vectors' loads in flight (L2 latency)
     const double* vi = Vb + i * D;
     double sv = 0.0;
-    for (int k = 0; k < m; ++k) sv = fma(x[es[k]], vi[es[k]], sv);
+    for (int k = 0; k < m; ++k) sv = fma(xs[k], vi[es[k]], sv);
     if (more)
       for (int t = gt + 4 * gs; t < ne; t += gs) {
         const int e = entry(a, nc, t);
@@ -511,6 +530,7 @@ __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
   const GSync<ONE> G;
   const long long t_start = clock64();
   long long tph[4] = {0, 0, 0, 0};
+  long long tj[2] = {0, 0};
   __shared__ NShared S;
   const IGeo& g = a.g;
   const int nc = a.ncell_dev ? *a.ncell_dev : a.ncell;
@@ -578,7 +598,7 @@ __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
       for (; j < kMaxKrylov && prods < a.maxprod; ++j) {
         long long c0 = clock64();
         G.sync();  // V_j complete
-        jvp_phase(G, a, nc, a.Vk + j * D, a.wv);
+        jvp_phase(G, a, nc, a.Vk + j * D, a.wv, tj);
         ++prods;
         G.sync();
         // classical Gram-Schmidt, twice (CGS2)
@@ -701,6 +721,8 @@ __global__ void __launch_bounds__(NK_T) newton_kernel(NArgs a) {
       a.tdbg[4] += clock64() - t_start;
       a.tdbg[5] += prods;
       a.tdbg[6] += 1;
+      a.tdbg[7] += tj[0];  // block 0 thread 0's face tasks
+      a.tdbg[8] += tj[1];  // ... and its wait for the other tasks + the barrier after them
     }
   }
 }
@@ -1242,7 +1264,7 @@ hrom_status hrom_imp_create(const hrom_grid* grid, double gamma, const hrom_para
   al(&c->istat, 4 * sizeof(int32_t));
   al(&c->fsweeps, 4 * sizeof(int32_t));
   al(&c->posflag, 4 * sizeof(int));
-  al(&c->tdbg, 8 * sizeof(long long));
+  al(&c->tdbg, 16 * sizeof(long long));
   if (cudaMallocHost((void**)&c->hres, 4 * sizeof(double)) != cudaSuccess) ok = false;
   if (cudaMallocHost((void**)&c->hint, 16 * sizeof(int32_t)) != cudaSuccess) ok = false;
   if (!ok) {
@@ -1418,9 +1440,9 @@ hrom_status hrom_imp_filter(hrom_imp_ctx* c, int32_t order, const double* dev_qm
 
 hrom_status hrom_imp_debug_timers(hrom_imp_ctx* c, int64_t* host_out) {
   if (!c || !host_out) return HROM_E_INVALID;
-  HROM_CK(cudaMemcpyAsync(host_out, c->tdbg, 8 * sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+  HROM_CK(cudaMemcpyAsync(host_out, c->tdbg, 10 * sizeof(long long), cudaMemcpyDeviceToHost, c->st));
   HROM_CK(cudaStreamSynchronize(c->st));
-  HROM_CK(cudaMemsetAsync(c->tdbg, 0, 8 * sizeof(long long), c->st));
+  HROM_CK(cudaMemsetAsync(c->tdbg, 0, 16 * sizeof(long long), c->st));
   return HROM_OK;
 }
 

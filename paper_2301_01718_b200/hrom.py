@@ -491,9 +491,9 @@ class ImplicitROM:
     def debug_timers(self):
         """Newton phase clocks since the last read (block 0, clock64 cycles): products, Gram-Schmidt,
         norms + Givens, line searches, whole kernels, products, solves."""
-        out = (C.c_int64 * 8)()
+        out = (C.c_int64 * 10)()
         _ck(self.lib.hrom_imp_debug_timers(self.h, C.cast(out, C.c_void_p)), "hrom_imp_debug_timers")
-        return list(out)[:7]
+        return list(out)[:9]
 
     def band(self):
         """Cells of the filter band of the current sets (ascending)."""

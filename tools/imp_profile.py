@@ -33,3 +33,5 @@ tm = rom.debug_timers()
 ghz = 1.965
 print("Newton per step (ms): products %.3f  GS %.3f  norms+Givens %.3f  line search %.3f  kernels %.3f;  products %d  solves %d"
       % tuple([x / 7 / ghz / 1e6 for x in tm[:5]] + [tm[5] / 7, tm[6] / 7]))
+print("per product (us): own face task %.2f, wait for the slowest task + barrier %.2f"
+      % (tm[7] / max(tm[5], 1) / ghz / 1e3, tm[8] / max(tm[5], 1) / ghz / 1e3))
