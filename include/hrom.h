@@ -315,6 +315,54 @@ hrom_status hrom_imp_get_band(hrom_imp_ctx* ctx, int32_t* any_list, int32_t* any
 hrom_status hrom_imp_set_window(hrom_imp_ctx* ctx, int64_t k, const double* any_snaps, int32_t nsnaps,
                                 const uint32_t* any_mask_next);
 
+/* ---- Row-slab sharding of ONE problem across ranks -----------------------------
+ * The HDM residual is local (Eq. partial_hdm2), so the grid can be cut into slabs of
+ * consecutive rows, one per rank: every rank keeps its rows of the snapshot window, of Phi (implicit),
+ * psi and the indicator, plus `halo` = max(3 h, 2 h + W) rows of each neighbour (the reach of a
+ * three-stage step with per-stage stencil halo h, and of the set dilations of reading A21).  Per step
+ * the ranks exchange: the halo rows of gamma_k (H3/H6) and of S-hat (H8) with their two neighbours,
+ * and all-reduce the gathered normal matrix of Eq. 8 (H4, (w+2)^2 double-doubles), the new row of the
+ * window Gram of Eq. 9 (H10, w+1 double-doubles), the radix-select histograms of the sampling rule
+ * (H8, 2048 counts per pass) and the CFL maximum (H1).  The small solves (H5, H11) are
+ * replicated: they run on every rank on bitwise identical inputs.
+ *
+ * A slab context is an hrom_ctx (destroy with hrom_destroy; hrom_sync, hrom_step_index,
+ * hrom_effective_rank, hrom_get_y, hrom_get_eigen apply).  Transport stays outside the library:
+ * hrom_slab_step runs the local work up to the next exchange and writes ONE message into the
+ * caller's device buffer dev_send (capacity >= max_message_bytes); the caller all-gathers the
+ * nranks messages of *send_bytes_out bytes each, in rank order, into one device buffer and passes
+ * it to the next call as dev_gathered (NULL on the first call of a step).  *send_bytes_out == 0
+ * means the step (stage, basis update and sampling of Algorithm 1, z = infinity, fixed
+ * sampling fraction, P = S-hat) is complete.  Every reduction is done by the library itself on the
+ * gathered buffer in rank order (double-double sums): all ranks obtain identical bits, and a run
+ * is bitwise reproducible.  Messages of all ranks have equal length in every phase.
+ * Refused (HROM_E_INVALID): dim != 2, the seam filter, ODEIM points, RRE-delta, finite z, W = -1,
+ * w + 1 > 68, fewer than `halo` own rows per rank.  A non-physical hybrid state on any rank is
+ * latched on every rank (hrom_sync -> HROM_E_POSITIVITY); a slab does not escalate. */
+typedef struct {
+  int32_t rank, nranks;
+  int32_t ny_global;          /* rows of the whole grid */
+  int32_t row0, rows_own;     /* first global row and number of rows this rank owns */
+  int32_t halo_lo, halo_hi;   /* halo rows kept below / above (0 at a non-periodic end) */
+  int32_t halo;               /* halo depth of an interior edge */
+  int64_t cells_own, cells_local, cells_global;
+  int64_t max_message_bytes;  /* capacity the send buffer needs */
+} hrom_slab_info;
+/* host-only: the row partition (rows_own differ by at most one; rank r owns rows after rank r-1) */
+hrom_status hrom_slab_partition(int32_t ny_global, int32_t nranks, int32_t rank, int32_t periodic, int32_t halo_rows,
+                                hrom_slab_info* out);
+/* grid: the WHOLE grid; params as hrom_create with no filter orders */
+hrom_status hrom_slab_create(const hrom_grid* grid, double gamma, double cfl, const hrom_params* params,
+                             void* cuda_stream, int32_t rank, int32_t nranks, hrom_ctx** out);
+hrom_status hrom_slab_get_info(const hrom_ctx* ctx, hrom_slab_info* out);
+/* any_q_global: the whole initial state q[v*N_global + n] (every rank passes the same array) */
+hrom_status hrom_slab_set_state(hrom_ctx* ctx, const double* any_q_global);
+/* the own rows: q[v*cells_own + n], rows_own*ceil(nx/32) mask words, cells_own indicator values */
+hrom_status hrom_slab_get_state(hrom_ctx* ctx, double* any_q_own);
+hrom_status hrom_slab_get_mask(hrom_ctx* ctx, uint32_t* any_mask_own);
+hrom_status hrom_slab_get_indicator(hrom_ctx* ctx, double* any_eps_own);
+hrom_status hrom_slab_step(hrom_ctx* ctx, const void* dev_gathered, void* dev_send, int64_t* send_bytes_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -129,6 +129,13 @@ Win window_at(const hrom_ctx* c, int64_t k) {
 using namespace hrom;
 
 namespace hrom {
+Win window_of(const hrom_ctx* c, int64_t k) { return window_at(c, k); }
+hrom_status launch_zvec(hrom_ctx* c, int w, double am) {
+  zvec_kernel<<<1, 128, 0, c->st>>>(c->b.A, c->b.lam, c->b.ireg, w, am, c->b.zvec);
+  HROM_LAUNCH_CK();
+  ++c->nlaunch;
+  return HROM_OK;
+}
 hrom_status flush_eigen(hrom_ctx* c) {
   if (!c->eig_todo) return HROM_OK;
   c->eig_todo = false;
@@ -206,6 +213,7 @@ hrom_status hrom_create(const hrom_grid* grid, double gamma, double cfl, const h
   g.ny = ny;
   g.c = dim + 2;
   g.bc = grid->bc;
+  g.bcy = grid->bc;
   g.recon = grid->recon;
   g.wpr = (grid->nx + 31) / 32;
   g.N = (int64_t)g.nx * g.ny;
@@ -370,6 +378,7 @@ void hrom_destroy(hrom_ctx* c) {
                   b.dreg, b.ureg, b.dbg, b.sel_val, b.sel_cell, b.blk, b.hist, b.hsum, b.fstat, b.l1part, b.fcnt, (void*)b.colptr, b.slot_tab, b.ochosen, b.ocoef, b.orows, b.orows_pub, b.opart_v, b.opart_e, b.ocnt, b.ocells, b.ophi};
   for (void* q : ptrs)
     if (q) cudaFree(q);
+  slab_destroy(c);
   delete c;
 }
 

@@ -113,7 +113,7 @@ __device__ __forceinline__ void cell_rhs(const Geo& g, const SRef q, int i, int 
         for (int v = 0; v < C; ++v) Uy[R][v] = Ux[R][v];
         continue;
       }
-      const int64_t n = (int64_t)wrap(j + m, g.ny, g.bc) * g.nx + i;
+      const int64_t n = (int64_t)wrap(j + m, g.ny, g.bcy) * g.nx + i;
 #pragma unroll
       for (int v = 0; v < C; ++v) Uy[m + R][v] = __ldg(q.p + sidx(q, v * g.N + n));
     }
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(TX * TY) stage_tile_kernel(Geo g, int stage, c
       const int ly = idx / SX, lx = idx % SX;
       const bool xin = lx >= TH && lx < TH + TX, yin = ly >= TH && ly < TH + TY;
       if (!xin && !yin) continue;  // corner
-      const int gi = wrap(i0 + lx - TH, g.nx, g.bc), gj = wrap(j0 + ly - TH, g.ny, g.bc);
+      const int gi = wrap(i0 + lx - TH, g.nx, g.bc), gj = wrap(j0 + ly - TH, g.ny, g.bcy);
       const int64_t n = (int64_t)gj * g.nx + gi;
 #pragma unroll
       for (int v = 0; v < C; ++v) U[v][ly][lx] = __ldg(qin.p + sidx(qin, v * g.N + n));
@@ -263,10 +263,11 @@ __global__ void __launch_bounds__(TX * TY) stage_tile_kernel(Geo g, int stage, c
 // H1: max_n S_n with S_n = (|u|+c)/dx [+ (|v|+c)/dy]; S_n >= 0 so its IEEE bits order like
 // the value and an integer atomicMax is exact and order-free (deterministic).
 template <int DIM>
-__global__ void __launch_bounds__(256) smax_kernel(Geo g, const SRef q, unsigned long long* __restrict__ smax) {
+__global__ void __launch_bounds__(256) smax_kernel(Geo g, const SRef q, unsigned long long* __restrict__ smax,
+                                                   int64_t n0, int64_t n1) {
   constexpr int C = DIM + 2;
   double m = 0.0;
-  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N;
+  for (int64_t n = n0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n1;
        n += (int64_t)gridDim.x * blockDim.x) {
     double U[C];
 #pragma unroll
@@ -321,14 +322,15 @@ template <int DIM>
 // maximum, bit for bit, at ~1/10 of the divisions.
 __global__ void __launch_bounds__(256) positivity_kernel(Geo g, const SRef q, unsigned long long* __restrict__ bad,
                                                          unsigned long long* __restrict__ smax,
-                                                         const unsigned long long* __restrict__ run_if) {
+                                                         const unsigned long long* __restrict__ run_if,
+                                                         int64_t n0, int64_t n1) {
   constexpr int C = DIM + 2;
   if (run_if && *run_if == ~0ull) return;
   const double gm1 = g.gamma - 1.0;
   double m = 0.0;
   float amax = 0.0f;  // running screened maximum (of cells not evaluated exactly, a lower bound)
   const float frdx = (float)(g.pow2 ? g.rdx : 1.0 / g.dx), frdy = (float)(g.pow2 ? g.rdy : 1.0 / g.dy);
-  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N;
+  for (int64_t n = n0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n1;
        n += (int64_t)gridDim.x * blockDim.x) {
     double U[C];
 #pragma unroll
@@ -389,8 +391,8 @@ hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override, int64_t kq) {
     } else {
       HROM_CK(cudaMemsetAsync(c->b.ureg, 0, sizeof(unsigned long long), c->st));
       const int grid = c->nsm * 8;
-      if (c->g.dim == 1) smax_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg);
-      else smax_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg);
+      if (c->g.dim == 1) smax_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg, 0, c->g.N);
+      else smax_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, c->b.ureg, 0, c->g.N);
       HROM_LAUNCH_CK();
       ++nl;
     }
@@ -434,24 +436,47 @@ hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, co
 // O11 after a hybrid step: per-step flag ureg[3] and the wave-speed maximum ureg[2]; then, only
 // if the flag is set (device-side condition, S:478 escalation): the step is redone as a full
 // step from gamma_{k-1} with the same dt, re-checked (latched error ureg[1], maximum ureg[0]).
-hrom_status launch_positivity(hrom_ctx* c, SRef qprev, SRef q, int64_t kq) {
+hrom_status launch_positivity_check(hrom_ctx* c, SRef q, int64_t n0, int64_t n1) {
   const int grid = c->nsm * 8;
   unsigned long long* u = c->b.ureg;
+  if (n1 < 0) n1 = c->g.N;
   // ureg[0] = 0, ureg[2] = 0, ureg[3] = ~0 were set by this step's dt_finalize
-  if (c->g.dim == 1) positivity_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, u + 3, u + 2, nullptr);
-  else positivity_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, u + 3, u + 2, nullptr);
+  if (c->g.dim == 1) positivity_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, u + 3, u + 2, nullptr, n0, n1);
+  else positivity_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, u + 3, u + 2, nullptr, n0, n1);
   HROM_LAUNCH_CK();
   c->nlaunch += 1;
+  return HROM_OK;
+}
+
+hrom_status launch_positivity_redo(hrom_ctx* c, SRef qprev, SRef q, int64_t kq) {
+  unsigned long long* u = c->b.ureg;
   hrom_status s;
   const SRef U1 = plain(c->b.U1), U2 = plain(c->b.U2);
   if ((s = launch_stage(c, 1, qprev, qprev, U1, nullptr, 0, 0.0, u + 3)) != HROM_OK) return s;
   if ((s = launch_stage(c, 2, qprev, U1, U2, nullptr, 0, 0.0, u + 3)) != HROM_OK) return s;
   if ((s = launch_stage(c, 3, qprev, U2, q, nullptr, 0, 0.0, u + 3)) != HROM_OK) return s;
-  if (c->g.dim == 1) positivity_kernel<1><<<c->nsm * 2, 256, 0, c->st>>>(c->g, q, u + 1, u, u + 3);
-  else positivity_kernel<2><<<c->nsm * 2, 256, 0, c->st>>>(c->g, q, u + 1, u, u + 3);
+  if (c->g.dim == 1) positivity_kernel<1><<<c->nsm * 2, 256, 0, c->st>>>(c->g, q, u + 1, u, u + 3, 0, c->g.N);
+  else positivity_kernel<2><<<c->nsm * 2, 256, 0, c->st>>>(c->g, q, u + 1, u, u + 3, 0, c->g.N);
   HROM_LAUNCH_CK();
   c->nlaunch += 1;
   c->smax_k = kq;
+  return HROM_OK;
+}
+
+hrom_status launch_positivity(hrom_ctx* c, SRef qprev, SRef q, int64_t kq) {
+  hrom_status s = launch_positivity_check(c, q, 0, -1);
+  if (s != HROM_OK) return s;
+  return launch_positivity_redo(c, qprev, q, kq);
+}
+
+// H1's wave-speed maximum of q alone (row slabs exchange it before dt, slab.cu); *dev_out must be
+// zeroed by the caller on the same stream
+hrom_status launch_smax(hrom_ctx* c, SRef q, unsigned long long* dev_out, int64_t n0, int64_t n1) {
+  const int grid = c->nsm * 8;
+  if (c->g.dim == 1) smax_kernel<1><<<grid, 256, 0, c->st>>>(c->g, q, dev_out, n0, n1);
+  else smax_kernel<2><<<grid, 256, 0, c->st>>>(c->g, q, dev_out, n0, n1);
+  HROM_LAUNCH_CK();
+  c->nlaunch += 1;
   return HROM_OK;
 }
 

@@ -443,7 +443,8 @@ hrom_status launch_fill(hrom_ctx* c, const Win& W, int mode, SRef src_S, SRef ou
   a.src_S = src_S;
   a.out = out;
   a.mS = c->b.masks + (int64_t)M_S * c->mwords;
-  a.mB = (mode == MODE_FILL) ? c->b.masks + (int64_t)M_B * c->mwords : nullptr;
+  a.mB = (mode == MODE_FILL) ? (c->fill_mB_override ? c->fill_mB_override : c->b.masks + (int64_t)M_B * c->mwords)
+                            : nullptr;
   a.eps_elem = c->b.eps_elem;
   a.part = c->b.gpart;
   a.C = c->b.C;

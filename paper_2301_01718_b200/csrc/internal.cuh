@@ -60,6 +60,7 @@ constexpr int kOdeimBlocks = 4 * 148;
 // Geometry passed by value to kernels.
 struct Geo {
   int dim, nx, ny, c, bc, recon, wpr;  // wpr = mask words per row
+  int bcy;  // boundary rule of the y ends (= bc; 0 on a row slab whose y ends are halo rows, slab.cu)
   int64_t N, D, Dp;                    // Dp: D rounded up to a multiple of TILE
   int64_t nsr;                         // slab slots per tile (w + 3)
   double dx, dy, gamma, cfl;
@@ -174,7 +175,11 @@ struct GraphSlot {
 };
 }  // namespace hrom
 
+struct hrom_slab;  // slab.cu: row-slab state of a sharded problem
+
 struct hrom_ctx {
+  hrom_slab* slab = nullptr;                 // non-null: this context owns one row slab of a sharded grid
+  const uint32_t* fill_mB_override = nullptr;  // fill pass: cells left out of the fused Gram row (band u halo rows)
   hrom::Geo g;
   hrom_params P;
   int w, r, nslots;
@@ -277,6 +282,11 @@ hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override, int64_t kq);
 hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, const int32_t* list, int list_idx,
                          double dt_override, const unsigned long long* run_if = nullptr);
 hrom_status launch_positivity(hrom_ctx* c, SRef qprev, SRef q, int64_t kq);
+// flag ureg[3] and maximum ureg[2] over the cells [n0, n1) (n1 < 0: all)
+hrom_status launch_positivity_check(hrom_ctx* c, SRef q, int64_t n0, int64_t n1);
+hrom_status launch_positivity_redo(hrom_ctx* c, SRef qprev, SRef q, int64_t kq);  // conditional full-step redo
+// max wave speed bits of the cells [n0, n1) (atomicMax into *dev_out)
+hrom_status launch_smax(hrom_ctx* c, SRef q, unsigned long long* dev_out, int64_t n0, int64_t n1);
 // masks.cu
 hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S);
 hrom_status select_and_build(hrom_ctx* c, const double* eps, int64_t n_g, double rre_delta = 0.0);
@@ -292,6 +302,10 @@ hrom_status gram_full_dd(hrom_ctx* c, const double* const* dev_cols, int64_t ns,
                          double* dev_Chi, double* dev_Clo, int ldc, const int32_t* map);
 hrom_status gram_gathered(hrom_ctx* c, SRef src_b);
 hrom_status band_gram_rows(hrom_ctx* c, const Win& W, SRef v);
+// the same kernels on an explicit cell list (row slabs: the own rows of a set)
+hrom_status band_gram_rows_list(hrom_ctx* c, const Win& W, SRef v, const int32_t* list, const int32_t* count);
+hrom_status gram_gathered_list(hrom_ctx* c, const Win& W, SRef src_b, const int32_t* list, const int32_t* count,
+                               double* Rhi, double* Rlo);
 hrom_status small_solve(hrom_ctx* c);
 hrom_status basis_from_gram(hrom_ctx* c, const Win& W);
 hrom_status lift(hrom_ctx* c, const Win& W, double* phi, double* psi);
@@ -302,6 +316,12 @@ hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot, const unsig
 hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_band,
                             const unsigned long long* esc = nullptr);
 hrom_status launch_eps_cells(hrom_ctx* c);
+// api.cu
+Win window_of(const hrom_ctx* c, int64_t k);           // slots of the window whose newest snapshot is gamma_k
+hrom_status launch_zvec(hrom_ctx* c, int w, double am);  // projection-indicator coefficients (A19, G8)
+hrom_status launch_eps_all(hrom_ctx* c);
+// slab.cu
+void slab_destroy(hrom_ctx* c);
 // filter.cu
 hrom_status launch_filter(hrom_ctx* c, SRef v, SRef F, uint8_t* kept_cells);
 }  // namespace hrom

@@ -2131,14 +2131,34 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
 
 // seam-band part of the new window Gram row (band DOFs' final values), double-double partials
 // after the fill's
-hrom_status band_gram_rows(hrom_ctx* c, const Win& W, SRef v) {
+hrom_status band_gram_rows_list(hrom_ctx* c, const Win& W, SRef v, const int32_t* list, const int32_t* count) {
   if (W.nU > 9 * GV_W) return HROM_E_INVALID;  // the fused row is limited to nU <= 68 anyway
   gemv_gather_kernel<9, false, true><<<c->band_blocks, GV_T, 0, c->st>>>(
-      c->g, W, c->b.ring, c->rho_ref(), c->b.lists + (int64_t)L_B * c->g.N, c->b.counts + L_B, v,
-      c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1) * 2, c->b.C);
+      c->g, W, c->b.ring, c->rho_ref(), list, count, v, c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1) * 2, c->b.C);
   HROM_LAUNCH_CK();
   ++c->nlaunch;
   return HROM_OK;
+}
+
+hrom_status band_gram_rows(hrom_ctx* c, const Win& W, SRef v) {
+  return band_gram_rows_list(c, W, v, c->b.lists + (int64_t)L_B * c->g.N, c->b.counts + L_B);
+}
+
+// gathered Gram of [U, b] over the DOF rows of an explicit cell list (row slabs: the own rows of
+// S-hat, or every own cell for the window Gram of the bootstrap), (nU+1)^2 double-double
+hrom_status gram_gathered_list(hrom_ctx* c, const Win& W, SRef src_b, const int32_t* list, const int32_t* count,
+                               double* Rhi, double* Rlo) {
+  GGArgs a{};
+  a.g = c->g;
+  a.W = W;
+  a.ring = c->b.ring;
+  a.rho = c->rho_ref();
+  a.list = list;
+  a.count = count;
+  a.src_b = src_b;
+  a.mode = 1;
+  const int ncol = a.W.nU + 1;
+  return run_gather_gram_dd(c, a, ncol, c->basis_pending ? c->nsm - 1 : c->nsm, Rhi, Rlo, ncol, nullptr);
 }
 
 hrom_status small_solve(hrom_ctx* c) {

@@ -80,7 +80,7 @@ __device__ __forceinline__ uint32_t ydil_word(const uint32_t* in, const Geo& g, 
   uint32_t out = 0;
   for (int b = -h; b <= h; ++b) {
     bool ok;
-    const int jj = wrapi(j + b, g.ny, g.bc, &ok);
+    const int jj = wrapi(j + b, g.ny, g.bcy, &ok);
     if (ok) out |= __ldcg(in + (int64_t)jj * g.wpr + wi);
   }
   return out;
@@ -853,7 +853,7 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
       const int iic = ok ? ii : (i + m < 0 ? 0 : g.nx - 1);  // transmissive: clamp
       if (!get_bit(B, g, iic, j)) atomicOr(&HM[(int64_t)j * g.wpr + (iic >> 5)], 1u << (iic & 31));
       if (g.dim == 2) {
-        const int jj = wrapi(j + m, g.ny, g.bc, &ok);
+        const int jj = wrapi(j + m, g.ny, g.bcy, &ok);
         const int jjc = ok ? jj : (j + m < 0 ? 0 : g.ny - 1);
         if (!get_bit(B, g, i, jjc)) atomicOr(&HM[(int64_t)jjc * g.wpr + (i >> 5)], 1u << (i & 31));
       }
@@ -885,7 +885,7 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
       if (!ok) ii = i + m < 0 ? 0 : g.nx - 1;
       a.tab[(int64_t)(m + 3) * N + t] = __ldcg(a.idx + (int64_t)j * g.nx + ii);
       if (g.dim == 2) {
-        int jj = wrapi(j + m, g.ny, g.bc, &ok);
+        int jj = wrapi(j + m, g.ny, g.bcy, &ok);
         if (!ok) jj = j + m < 0 ? 0 : g.ny - 1;
         a.tab[(int64_t)(7 + m + 3) * N + t] = __ldcg(a.idx + (int64_t)jj * g.nx + i);
       }

@@ -42,6 +42,13 @@ class Params(C.Structure):
                 ("sample_mode", C.c_int32), ("rre_delta", C.c_double), ("odeim_points", C.c_int32)]
 
 
+class SlabInfo(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("ny_global", C.c_int32), ("row0", C.c_int32),
+                ("rows_own", C.c_int32), ("halo_lo", C.c_int32), ("halo_hi", C.c_int32), ("halo", C.c_int32),
+                ("cells_own", C.c_int64), ("cells_local", C.c_int64), ("cells_global", C.c_int64),
+                ("max_message_bytes", C.c_int64)]
+
+
 class ImpParams(C.Structure):
     _fields_ = [("flux", C.c_int32), ("dt", C.c_double), ("eps_y", C.c_double), ("j_max", C.c_int32),
                 ("newton_tol", C.c_double), ("newton_maxit", C.c_int32)]
@@ -110,6 +117,15 @@ _SIGS = {
     "hrom_imp_set_window": (C.c_int, [_VP, C.c_int64, _VP, C.c_int32, _VP]),
     "hrom_imp_get_band": (C.c_int, [_VP, _VP, _VP]),
     "hrom_imp_debug_timers": (C.c_int, [_VP, _VP]),
+    "hrom_slab_partition": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(SlabInfo)]),
+    "hrom_slab_create": (C.c_int, [C.POINTER(Grid), C.c_double, C.c_double, C.POINTER(Params), _VP, C.c_int32,
+                                   C.c_int32, C.POINTER(_VP)]),
+    "hrom_slab_get_info": (C.c_int, [_VP, C.POINTER(SlabInfo)]),
+    "hrom_slab_set_state": (C.c_int, [_VP, _VP]),
+    "hrom_slab_get_state": (C.c_int, [_VP, _VP]),
+    "hrom_slab_get_mask": (C.c_int, [_VP, _VP]),
+    "hrom_slab_get_indicator": (C.c_int, [_VP, _VP]),
+    "hrom_slab_step": (C.c_int, [_VP, _VP, _VP, C.POINTER(C.c_int64)]),
 }
 
 SECTIONS = ["dt", "masked_rk3", "gathered_gram", "pinv_solve", "fill_pass", "indicator", "seam_filter",
