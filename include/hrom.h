@@ -336,8 +336,11 @@ hrom_status hrom_imp_set_window(hrom_imp_ctx* ctx, int64_t k, const double* any_
  * sampling fraction, P = S-hat) is complete.  Every reduction is done by the library itself on the
  * gathered buffer in rank order (double-double sums): all ranks obtain identical bits, and a run
  * is bitwise reproducible.  Messages of all ranks have equal length in every phase.
- * Refused (HROM_E_INVALID): dim != 2, the seam filter, ODEIM points, RRE-delta, finite z, W = -1,
- * w + 1 > 68, fewer than `halo` own rows per rank.  A non-physical hybrid state on any rank is
+ * The seam filter runs one exchange per sweep (edge rows + the sweep's keep count and
+ * largest relative decrease); its stop decision is taken on the host from the gathered statistics,
+ * so a call that consumes a sweep message synchronises the context's stream.
+ * Refused (HROM_E_INVALID): dim != 2, ODEIM points, RRE-delta, finite z, W = -1, w + 1 > 68, fewer
+ * than `halo` own rows per rank.  A non-physical hybrid state on any rank is
  * latched on every rank (hrom_sync -> HROM_E_POSITIVITY); a slab does not escalate. */
 typedef struct {
   int32_t rank, nranks;
@@ -351,7 +354,7 @@ typedef struct {
 /* host-only: the row partition (rows_own differ by at most one; rank r owns rows after rank r-1) */
 hrom_status hrom_slab_partition(int32_t ny_global, int32_t nranks, int32_t rank, int32_t periodic, int32_t halo_rows,
                                 hrom_slab_info* out);
-/* grid: the WHOLE grid; params as hrom_create with no filter orders */
+/* grid: the WHOLE grid; params as hrom_create (gather_mode is ignored) */
 hrom_status hrom_slab_create(const hrom_grid* grid, double gamma, double cfl, const hrom_params* params,
                              void* cuda_stream, int32_t rank, int32_t nranks, hrom_ctx** out);
 hrom_status hrom_slab_get_info(const hrom_ctx* ctx, hrom_slab_info* out);
@@ -362,6 +365,11 @@ hrom_status hrom_slab_get_state(hrom_ctx* ctx, double* any_q_own);
 hrom_status hrom_slab_get_mask(hrom_ctx* ctx, uint32_t* any_mask_own);
 hrom_status hrom_slab_get_indicator(hrom_ctx* ctx, double* any_eps_own);
 hrom_status hrom_slab_step(hrom_ctx* ctx, const void* dev_gathered, void* dev_send, int64_t* send_bytes_out);
+/* H8 alone (the slab counterpart of hrom_sample with an explicit indicator): S-hat := the top
+ * ceil(f N_global) cells of the ranks' indicators any_eps_own (cells_own values each; eps > 0 only,
+ * ties at the threshold by ascending global cell), then the sets.  Starts the selection phases:
+ * writes the first message; continue with hrom_slab_step until *send_bytes_out == 0. */
+hrom_status hrom_slab_resample(hrom_ctx* ctx, const double* any_eps_own, void* dev_send, int64_t* send_bytes_out);
 
 #ifdef __cplusplus
 }

@@ -12,6 +12,9 @@
 //   S   max wave speed (H1)                          all-reduce MAX of one word (first step only;
 //                                                     later steps carry it in the END message)
 //   R   gathered Gram of the own S-hat rows (H4)     all-reduce SUM of (w+2)^2 double-doubles
+//   F0  halo rows of the pre-filter gamma_k (H6)       neighbour rows (only when the seam filter is on)
+//   Fs  per filter sweep (H7): band values of the edge
+//       rows + the sweep's statistics                 neighbour rows + all-reduce MAX / SUM, host decision
 //   END halo rows of gamma_k (H3/H6), new window-Gram
 //       row (H10), max wave speed, positivity flag   neighbour rows + all-reduce SUM / MAX / MIN
 //   B   bootstrap window Gram (k = w-1, H10)         all-reduce SUM of (w+1)^2 double-doubles
@@ -30,9 +33,15 @@
 // Reductions never include halo rows: S-hat and band sums run on own-row sub-lists, and the
 // fused window-Gram row of the fill pass skips halo cells through its band mask.
 //
-// Not supported on a slab (hrom_slab_create refuses / reports): the seam filter (its stop test
-// needs an all-reduce per sweep), ODEIM points, RRE-delta, finite z, and the positivity
-// escalation (a non-physical hybrid state is latched and reported by hrom_sync on every rank).
+// The seam filter (H7, readings A21-A24, A23') runs sweep by sweep: the x-pass on every
+// local band cell (halo rows included: it reads its own row only), the y-pass and the residual gate
+// on the own band cells, then the edge rows and the sweep's statistics travel; the stop decision
+// (empty keep-set, relative decrease below eps_f, j_max sweeps) is taken on the host from the
+// gathered statistics, the same on every rank.  Same arithmetic as filter.cu on the dense field.
+//
+// Not supported on a slab (hrom_slab_create refuses / reports): ODEIM points, RRE-delta, finite z,
+// the whole-domain filter (W = -1), and the positivity escalation (a non-physical hybrid state is
+// latched and reported by hrom_sync on every rank).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -47,6 +56,9 @@ struct hrom_slab {
   int phase = 0;
   int sel_pass = 0;
   bool step_hybrid = false;
+  int f_order = 0, f_sw = 0;  // seam filter: cascade order and sweep in flight
+  int f_sweeps[3] = {0, 0, 0};
+  unsigned long long* fstat = nullptr;  // [0] max relative decrease (bits) [1] kept count of the sweep
   // message geometry (bytes)
   int64_t halo_doubles = 0;  // c * H * nx: one edge block of the state
   int64_t mask_words = 0;    // H * wpr: one edge block of a bitmap
@@ -68,7 +80,7 @@ namespace {
 constexpr int RADIX = 11, NBIN = 1 << RADIX;
 constexpr int ROW_SLOTS = kMaxW + 2;  // fixed length of the Gram-row part of an END message
 
-enum Phase { PH_IDLE = 0, PH_SMAX, PH_R, PH_END, PH_BOOT, PH_SEL, PH_MASK };
+enum Phase { PH_IDLE = 0, PH_SMAX, PH_R, PH_HALO1, PH_FSWEEP, PH_END, PH_BOOT, PH_SEL, PH_MASK };
 
 __host__ __device__ inline int sel_shift(int p) { return p < 5 ? 53 - RADIX * p : 0; }
 
@@ -238,7 +250,7 @@ __global__ void __launch_bounds__(1024) sel_hist_kernel(const double* __restrict
   const int shift = sel_shift(pass);
   const int width = shift == 0 ? 9 : RADIX;
   const unsigned long long hm = pass == 0 ? 0ull : (~0ull << (shift + width));
-  const unsigned long long prefix = sel[0];
+  const unsigned long long prefix = pass == 0 ? 0ull : sel[0];  // sel[0] still holds the previous selection's prefix
   const bool skip = pass > 0 && sel[5] != 0ull;  // every positive cell is selected: nothing to count
   int run_bin = -1, run = 0;  // run-length cache: neighbouring cells mostly share a digit
   if (!skip)
@@ -362,6 +374,141 @@ __global__ void __launch_bounds__(1024) sel_ties_kernel(Geo g, const double* __r
     if (threadIdx.x == 1023) s_base += sc[1023];
     __syncthreads();
     if ((unsigned long long)s_base >= quota) break;  // uniform
+  }
+}
+
+// ---- seam filter on the dense field (same stencils, order of operations and gate as filter.cu) ----
+__constant__ double fc2[3] = {1, 2, 1};
+__constant__ double fc4[5] = {-1, 4, 10, 4, -1};
+__constant__ double fc6[7] = {1, -6, 15, 44, 15, -6, 1};
+__device__ __forceinline__ int fshapiro(int order, const double** c, double* den) {
+  if (order == 2) { *c = fc2; *den = 4.0; return 1; }
+  if (order == 4) { *c = fc4; *den = 16.0; return 2; }
+  *c = fc6; *den = 64.0; return 3;
+}
+__device__ __forceinline__ int fwrap(int i, int n, int bc) {  // periodic wrap, else zeroth-order end
+  if (bc == 1) {
+    i %= n;
+    return i < 0 ? i + n : i;
+  }
+  return i < 0 ? 0 : (i >= n ? n - 1 : i);
+}
+// pre-filter values of the own band cells (the indicator on kept cells needs them), flags cleared
+__global__ void filt_init_kernel(Geo g, SRef v, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+                                 double* __restrict__ v0, uint8_t* __restrict__ flag) {
+  const int nb = *count;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += gridDim.x * blockDim.x) {
+    const int64_t n = list[t];
+    for (int var = 0; var < g.c; ++var) v0[var * g.N + n] = v.p[sidx(v, var * g.N + n)];
+    flag[n] = 0;
+  }
+}
+// P1: v' = S^x(v) on every local band cell
+__global__ void filt_x_kernel(Geo g, SRef v, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+                              int order, double* __restrict__ Vp) {
+  const double* cf;
+  double den;
+  const int rad = fshapiro(order, &cf, &den);
+  double cfr[7];
+#pragma unroll
+  for (int m = 0; m < 7; ++m) cfr[m] = m <= 2 * rad ? cf[m] : 0.0;
+  const int nb = *count;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += gridDim.x * blockDim.x) {
+    const int n = list[t];
+    const int j = n / g.nx, i = n - j * g.nx;
+    for (int var = 0; var < g.c; ++var) {
+      double sx = 0.0;
+#pragma unroll
+      for (int m = 0; m < 7; ++m)
+        if (m <= 2 * rad) {
+          const int64_t nn = (int64_t)j * g.nx + fwrap(i + m - rad, g.nx, g.bc);
+          sx += cfr[m] * v.p[sidx(v, var * g.N + nn)];
+        }
+      Vp[var * g.N + n] = sx / den;
+    }
+  }
+}
+// P2 on the own band cells: v'' = S^y(v') (band neighbours: x-filtered, others: fixed values),
+// residual gate against F, kept values applied in place, sweep statistics
+__global__ void __launch_bounds__(256) filt_y_kernel(Geo g, SRef v, const double* __restrict__ Vp,
+                                                     const double* __restrict__ F, const uint32_t* __restrict__ mB,
+                                                     const int32_t* __restrict__ list,
+                                                     const int32_t* __restrict__ count, int order,
+                                                     uint8_t* __restrict__ flag, unsigned long long* __restrict__ stat) {
+  const double* cf;
+  double den;
+  const int rad = fshapiro(order, &cf, &den);
+  double cfr[7];
+#pragma unroll
+  for (int m = 0; m < 7; ++m) cfr[m] = m <= 2 * rad ? cf[m] : 0.0;
+  const int nb = *count;
+  double mdec = 0.0;
+  int cnt = 0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += gridDim.x * blockDim.x) {
+    const int n = list[t];
+    const int j = n / g.nx, i = n - j * g.nx;
+    double rold = 0.0, rnew = 0.0, fs = 0.0, vpp[4];
+    for (int var = 0; var < g.c; ++var) {
+      double sy = 0.0;
+#pragma unroll
+      for (int m = 0; m < 7; ++m)
+        if (m <= 2 * rad) {
+          const int jj = fwrap(j + m - rad, g.ny, g.bcy);
+          const int64_t nn = (int64_t)jj * g.nx + i;
+          const bool inB = (mB[(int64_t)jj * g.wpr + (i >> 5)] >> (i & 31)) & 1u;
+          const double yv = inB ? Vp[var * g.N + nn] : v.p[sidx(v, var * g.N + nn)];
+          sy += cfr[m] * yv;
+        }
+      const double xv = sy / den;
+      vpp[var] = xv;
+      const double own = v.p[sidx(v, var * g.N + n)], fe = F[var * g.N + n];
+      rold = fmax(rold, fabs(own - fe));
+      rnew = fmax(rnew, fabs(xv - fe));
+      fs = fmax(fs, fabs(fe));
+    }
+    if (rnew < rold) {
+      for (int var = 0; var < g.c; ++var) v.p[sidx(v, var * g.N + n)] = vpp[var];
+      flag[n] = 1;
+      if (rold > 0x1p-40 * fs) mdec = fmax(mdec, (rold - rnew) / rold);  // A23': above the rounding level
+      ++cnt;
+    }
+  }
+  __shared__ double sdec[8];
+  __shared__ int scnt[8];
+  for (int o = 16; o > 0; o >>= 1) {
+    mdec = fmax(mdec, __shfl_xor_sync(0xffffffffu, mdec, o));
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sdec[threadIdx.x >> 5] = mdec;
+    scnt[threadIdx.x >> 5] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double md = 0.0;
+    int c = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      md = fmax(md, sdec[k]);
+      c += scnt[k];
+    }
+    atomicMax(stat, (unsigned long long)__double_as_longlong(md));  // non-negative doubles order like their bits
+    atomicAdd(stat + 1, (unsigned long long)c);
+  }
+}
+// indicator on the kept own band cells: eps_n = sum_v (v - (psi + Phi y))^2 (filter.cu write-back)
+__global__ void filt_final_kernel(Geo g, SRef v, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+                                  const double* __restrict__ v0, const uint8_t* __restrict__ flag,
+                                  double* __restrict__ eps) {
+  const int nb = *count;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += gridDim.x * blockDim.x) {
+    const int64_t n = list[t];
+    if (!flag[n]) continue;
+    double sum = 0.0;
+    for (int var = 0; var < g.c; ++var) {
+      const double d = v.p[sidx(v, var * g.N + n)] - v0[var * g.N + n];
+      sum += d * d;
+    }
+    eps[n] = sum;
   }
 }
 
@@ -506,12 +653,88 @@ hrom_status begin_update(hrom_ctx* c, unsigned char* send, int64_t* bytes) {
   return HROM_OK;
 }
 
+
+bool filter_on(const hrom_ctx* c) { return c->P.n_filter_orders > 0 && c->P.filter_max_sweeps > 0; }
+
+// one filter sweep of cascade order f_order: x-pass on every local band cell, y-pass + gate on the
+// own band cells; message = END layout with the edge rows and the sweep's statistics in the tail
+hrom_status run_sweep(hrom_ctx* c, unsigned char* send, int64_t* bytes) {
+  hrom_slab* s = c->slab;
+  const Geo& g = c->g;
+  Bufs& b = c->b;
+  const SRef v = c->slot_ref(c->slot_of(c->k + 1));
+  const int order = c->P.filter_orders[s->f_order];
+  const EndLayout L = end_layout(s);
+  HROM_CK(cudaMemsetAsync(s->fstat, 0, 2 * sizeof(unsigned long long), c->st));
+  const int grid = 4 * c->nsm;
+  filt_x_kernel<<<grid, 256, 0, c->st>>>(g, v, b.lists + (int64_t)L_B * g.N, b.counts + L_B, order, b.U1);
+  filt_y_kernel<<<grid, 256, 0, c->st>>>(g, v, b.U1, b.U3, b.masks + (int64_t)M_B * c->mwords, s->listB, s->cnt + 1,
+                                         order, b.kept, s->fstat);
+  HROM_LAUNCH_CK();
+  c->nlaunch += 2;
+  hrom_status st = pack_halo(c, v, send);
+  if (st != HROM_OK) return st;
+  HROM_CK(cudaMemsetAsync(send + L.row, 0, 2 * ROW_SLOTS * 8, c->st));
+  HROM_CK(cudaMemcpyAsync(send + L.tail, s->fstat, 16, cudaMemcpyDeviceToDevice, c->st));
+  ++s->f_sweeps[s->f_order];
+  *bytes = L.bytes;
+  s->phase = PH_FSWEEP;
+  return HROM_OK;
+}
+
+// after the fill (and the filter): band part of the Gram row, positivity + wave speeds of the own
+// rows, the END message
+hrom_status finish_hybrid(hrom_ctx* c, unsigned char* send, int64_t* bytes) {
+  hrom_slab* s = c->slab;
+  const Geo& g = c->g;
+  Bufs& b = c->b;
+  const int64_t kn = c->k + 1;
+  const SRef out = c->slot_ref(c->slot_of(kn));
+  const int64_t own_lo = (int64_t)s->hlo * g.nx, own_hi = (int64_t)(s->hlo + s->own) * g.nx;
+  hrom_status st;
+  if ((st = band_gram_rows_list(c, c->win, out, s->listB, s->cnt + 1)) != HROM_OK) return st;
+  if ((st = launch_positivity_check(c, out, own_lo, own_hi)) != HROM_OK) return st;
+  const EndLayout L = end_layout(s);
+  slab_row_reduce<<<1, 1024, 0, c->st>>>(b.gpart, c->fill_grid, b.gpart + (int64_t)c->fill_blocks * (c->win.nU + 1) * 2,
+                                         c->band_blocks, c->win.nU, reinterpret_cast<double*>(send + L.row));
+  HROM_LAUNCH_CK();
+  ++c->nlaunch;
+  if ((st = pack_halo(c, out, send)) != HROM_OK) return st;
+  // tail: the own rows' wave-speed maximum (H1 of the next step) and positivity flag
+  HROM_CK(cudaMemcpyAsync(send + L.tail, b.ureg + 2, 8, cudaMemcpyDeviceToDevice, c->st));
+  HROM_CK(cudaMemcpyAsync(send + L.tail + 8, b.ureg + 3, 8, cudaMemcpyDeviceToDevice, c->st));
+  c->k = kn;
+  c->points_used = 0;
+  c->last_hybrid = true;
+  c->eps_sparse = true;
+  c->gram_row_ready = false;
+  c->sets_ready = false;
+  s->step_hybrid = true;
+  *bytes = L.bytes;
+  s->phase = PH_END;
+  return HROM_OK;
+}
+
+// the filter is over: indicator on the kept own band cells, sweep counts where the unsharded
+// filter reports them (ireg[4..6]), then the rest of the step
+hrom_status end_filter(hrom_ctx* c, unsigned char* send, int64_t* bytes) {
+  hrom_slab* s = c->slab;
+  const SRef v = c->slot_ref(c->slot_of(c->k + 1));
+  filt_final_kernel<<<4 * c->nsm, 256, 0, c->st>>>(c->g, v, s->listB, s->cnt + 1, c->b.Vorig, c->b.kept, c->b.eps);
+  HROM_LAUNCH_CK();
+  ++c->nlaunch;
+  int32_t sw[3] = {s->f_sweeps[0], s->f_sweeps[1], s->f_sweeps[2]};
+  HROM_CK(cudaMemcpyAsync(c->b.ireg + 4, sw, sizeof(sw), cudaMemcpyHostToDevice, c->st));
+  HROM_CK(cudaStreamSynchronize(c->st));  // sw is a stack array
+  return finish_hybrid(c, send, bytes);
+}
+
 }  // namespace
 
 void slab_destroy(hrom_ctx* c) {
   hrom_slab* s = c->slab;
   if (!s) return;
-  void* ptrs[] = {s->listS, s->listB, s->listA, s->cnt, s->mBH, s->sel, s->hist, s->stage};
+  void* ptrs[] = {s->listS, s->listB, s->listA, s->cnt, s->mBH, s->sel, s->hist, s->stage, s->fstat};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete s;
@@ -535,7 +758,6 @@ hrom_status hrom_slab_create(const hrom_grid* grid, double gamma, double cfl, co
   if (!grid || !p || !out) return HROM_E_INVALID;
   *out = nullptr;
   if (grid->dim != 2) return HROM_E_INVALID;  // a 1-D grid has no rows to split
-  if (p->n_filter_orders > 0 && p->filter_max_sweeps > 0) return HROM_E_INVALID;  // seam filter: not on a slab
   if (p->odeim_points > 0 || p->sample_mode != 0 || p->full_period > 0 || p->band < 0 || p->gram_mode != 0)
     return HROM_E_INVALID;
   hrom_slab_info info;
@@ -586,6 +808,7 @@ hrom_status hrom_slab_create(const hrom_grid* grid, double gamma, double cfl, co
   A(salloc(&s->sel, 8));
   A(salloc(&s->hist, NBIN));
   A(salloc(&s->stage, g.Dp));
+  A(salloc(&s->fstat, 2));
   if (st != HROM_OK) {
     hrom_destroy(c);
     return st;
@@ -664,6 +887,21 @@ hrom_status hrom_slab_get_indicator(hrom_ctx* c, double* any_eps_own) {
   const hrom_slab* s = c->slab;
   HROM_CK(cudaMemcpyAsync(any_eps_own, c->b.eps + (int64_t)s->hlo * c->g.nx,
                           (size_t)s->own * c->g.nx * sizeof(double), cudaMemcpyDefault, c->st));
+  return HROM_OK;
+}
+
+hrom_status hrom_slab_resample(hrom_ctx* c, const double* any_eps_own, void* dev_send, int64_t* send_bytes_out) {
+  if (!c || !c->slab || !any_eps_own || !dev_send || !send_bytes_out) return HROM_E_INVALID;
+  hrom_slab* s = c->slab;
+  if (s->phase != PH_IDLE) return HROM_E_STATE;
+  HROM_CK(cudaMemsetAsync(c->b.eps, 0, c->g.N * sizeof(double), c->st));
+  HROM_CK(cudaMemcpyAsync(c->b.eps + (int64_t)s->hlo * c->g.nx, any_eps_own, (size_t)s->own * c->g.nx * sizeof(double),
+                          cudaMemcpyDefault, c->st));
+  s->sel_pass = 0;
+  hrom_status st = sel_pass(c, 0, static_cast<unsigned char*>(dev_send));
+  if (st != HROM_OK) return st;
+  *send_bytes_out = NBIN * sizeof(int32_t);
+  s->phase = PH_SEL;
   return HROM_OK;
 }
 
@@ -767,27 +1005,52 @@ hrom_status hrom_slab_step(hrom_ctx* c, const void* dev_gathered, void* dev_send
     c->fill_mB_override = nullptr;
     if (st != HROM_OK) return st;
     if ((st = launch_eps_cells(c)) != HROM_OK) return st;
-    if ((st = band_gram_rows_list(c, c->win, out, s->listB, s->cnt + 1)) != HROM_OK) return st;
-    if ((st = launch_positivity_check(c, out, own_lo, own_hi)) != HROM_OK) return st;
+    if (!filter_on(c)) return finish_hybrid(c, send, send_bytes_out);
+    // H7: the neighbours' pre-filter rows first (the filter's stencils reach into the halo)
     const EndLayout L = end_layout(s);
-    slab_row_reduce<<<1, 1024, 0, c->st>>>(b.gpart, c->fill_grid, b.gpart + (int64_t)c->fill_blocks * (c->win.nU + 1) * 2,
-                                           c->band_blocks, c->win.nU, reinterpret_cast<double*>(send + L.row));
+    if ((st = pack_halo(c, out, send)) != HROM_OK) return st;
+    HROM_CK(cudaMemsetAsync(send + L.row, 0, L.bytes - L.row, c->st));
+    *send_bytes_out = L.bytes;
+    s->phase = PH_HALO1;
+    return HROM_OK;
+  }
+
+  if (s->phase == PH_HALO1) {
+    const EndLayout L = end_layout(s);
+    const SRef v = c->slot_ref(c->slot_of(c->k + 1));
+    if ((st = unpack_halo(c, v, gath, L.bytes)) != HROM_OK) return st;
+    filt_init_kernel<<<4 * c->nsm, 256, 0, c->st>>>(g, v, s->listB, s->cnt + 1, b.Vorig, b.kept);
     HROM_LAUNCH_CK();
     ++c->nlaunch;
-    if ((st = pack_halo(c, out, send)) != HROM_OK) return st;
-    // tail: the own rows' wave-speed maximum (H1 of the next step) and positivity flag
-    HROM_CK(cudaMemcpyAsync(send + L.tail, b.ureg + 2, 8, cudaMemcpyDeviceToDevice, c->st));
-    HROM_CK(cudaMemcpyAsync(send + L.tail + 8, b.ureg + 3, 8, cudaMemcpyDeviceToDevice, c->st));
-    c->k = kn;
-    c->points_used = 0;
-    c->last_hybrid = true;
-    c->eps_sparse = true;
-    c->gram_row_ready = false;
-    c->sets_ready = false;
-    s->step_hybrid = true;
-    *send_bytes_out = L.bytes;
-    s->phase = PH_END;
-    return HROM_OK;
+    s->f_order = s->f_sw = 0;
+    s->f_sweeps[0] = s->f_sweeps[1] = s->f_sweeps[2] = 0;
+    return run_sweep(c, send, send_bytes_out);
+  }
+
+  if (s->phase == PH_FSWEEP) {
+    const EndLayout L = end_layout(s);
+    const SRef v = c->slot_ref(c->slot_of(c->k + 1));
+    if ((st = unpack_halo(c, v, gath, L.bytes)) != HROM_OK) return st;
+    // stop decision from the gathered statistics (A23): identical on every rank
+    unsigned long long hs[2 * 64];
+    if (P > 64) return HROM_E_INVALID;
+    HROM_CK(cudaMemcpy2DAsync(hs, 16, gath + L.tail, (size_t)L.bytes, 16, (size_t)P, cudaMemcpyDeviceToHost, c->st));
+    HROM_CK(cudaStreamSynchronize(c->st));
+    unsigned long long mb = 0ull, tot = 0ull;
+    for (int r = 0; r < P; ++r) {
+      mb = std::max(mb, hs[2 * r]);
+      tot += hs[2 * r + 1];
+    }
+    double md;
+    std::memcpy(&md, &mb, sizeof(md));
+    const bool stop = tot == 0ull || md < c->P.filter_eps || s->f_sw + 1 == c->P.filter_max_sweeps;
+    if (!stop) {
+      ++s->f_sw;
+      return run_sweep(c, send, send_bytes_out);
+    }
+    s->f_sw = 0;
+    if (++s->f_order < c->P.n_filter_orders) return run_sweep(c, send, send_bytes_out);
+    return end_filter(c, send, send_bytes_out);
   }
 
   if (s->phase == PH_END) {

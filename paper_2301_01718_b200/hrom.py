@@ -126,6 +126,7 @@ _SIGS = {
     "hrom_slab_get_mask": (C.c_int, [_VP, _VP]),
     "hrom_slab_get_indicator": (C.c_int, [_VP, _VP]),
     "hrom_slab_step": (C.c_int, [_VP, _VP, _VP, C.POINTER(C.c_int64)]),
+    "hrom_slab_resample": (C.c_int, [_VP, _VP, _VP, C.POINTER(C.c_int64)]),
 }
 
 SECTIONS = ["dt", "masked_rk3", "gathered_gram", "pinv_solve", "fill_pass", "indicator", "seam_filter",

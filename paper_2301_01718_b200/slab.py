@@ -71,10 +71,10 @@ class SlabROM:
         self.wl = wl
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         g = H.Grid(wl.dim, wl.nx, wl.ny if wl.dim == 2 else 1, wl.x0, wl.x1, wl.y0, wl.y1, wl.bc, wl.recon)
-        fo = (C.c_int32 * 3)(0, 0, 0)
-        # a slab runs Algorithm 1 with z = infinity, the fixed sampling fraction and no seam filter
-        p = H.Params(wl.w, wl.r, wl.h, wl.W, fo, 0, 0, wl.filter_eps, wl.eig_rel_cutoff, wl.lsq_rel_cutoff,
-                     wl.f, 0, 0, 1, 0, 0, 0.0, 0)
+        fo = (C.c_int32 * 3)(*(list(wl.filter_orders) + [0, 0, 0])[:3])
+        # a slab runs Algorithm 1 with z = infinity and the fixed sampling fraction (P = S-hat)
+        p = H.Params(wl.w, wl.r, wl.h, wl.W, fo, len(wl.filter_orders), wl.filter_max_sweeps, wl.filter_eps,
+                     wl.eig_rel_cutoff, wl.lsq_rel_cutoff, wl.f, 0, 0, 1, 0, 0, 0.0, 0)
         h = C.c_void_p()
         H._ck(self.lib.hrom_slab_create(C.byref(g), wl.gamma, wl.cfl, C.byref(p), C.c_void_p(self.stream.cuda_stream),
                                         rank, nranks, C.byref(h)), "hrom_slab_create")
@@ -148,6 +148,18 @@ class SlabROM:
         H._ck(self.lib.hrom_slab_step(self.h, H._ptr(gathered), H._ptr(self.send), C.byref(n)), "hrom_slab_step")
         return self.send[: n.value] if n.value > 0 else None
 
+    def resample_begin(self, eps_own: torch.Tensor) -> torch.Tensor:
+        """Start H8 alone on an explicit indicator of the own cells (hrom_slab_resample)."""
+        assert eps_own.dtype == torch.float64 and eps_own.is_contiguous() and eps_own.numel() == int(self.info.cells_own)
+        n = C.c_int64(0)
+        H._ck(self.lib.hrom_slab_resample(self.h, H._ptr(eps_own), H._ptr(self.send), C.byref(n)), "hrom_slab_resample")
+        return self.send[: n.value]
+
+    def resample(self, eps_own: torch.Tensor, comm: DistComm):
+        msg = self.resample_begin(eps_own)
+        while msg is not None:
+            msg = self.phase(comm.all_gather(msg))
+
     def step(self, comm: DistComm):
         """One step of Algorithm 1 on this rank's slab; collective over `comm`."""
         msg = self.phase(None)
@@ -163,6 +175,17 @@ def step_all(roms: List[SlabROM], comm: LocalComm):
         gathered = comm.all_gather_many(msgs)
         msgs = [r.phase(gathered) for r in roms]
     assert all(m is None for m in msgs)
+
+
+def resample_all(roms: List[SlabROM], comm: LocalComm, eps_global: torch.Tensor):
+    """H8 alone on all slabs of one process from a whole-grid indicator."""
+    msgs = []
+    for r in roms:
+        lo = int(r.info.row0) * r.wl.nx
+        msgs.append(r.resample_begin(eps_global[lo: lo + int(r.info.cells_own)].contiguous()))
+    while msgs[0] is not None:
+        gathered = comm.all_gather_many(msgs)
+        msgs = [r.phase(gathered) for r in roms]
 
 
 def assemble(roms: List[SlabROM], what: str = "state") -> torch.Tensor:

@@ -19,10 +19,12 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _mk(inputs, cfg, nranks, **over):
+def _mk(inputs, cfg, nranks, filt=False, **over):
     from paper_2301_01718_b200.hrom import HybridROM
     from paper_2301_01718_b200 import slab
-    wl = dataclasses.replace(inputs.config(cfg, **over), filter_orders=())
+    wl = inputs.config(cfg, **over)
+    if not filt:
+        wl = dataclasses.replace(wl, filter_orders=())
     q0 = torch.from_numpy(inputs.initial_condition(wl)).cuda()
     ref = HybridROM(wl, gather_mode=1)
     ref.set_state(q0)
@@ -50,12 +52,13 @@ def test_slab_full_steps_bitwise(inputs, cfg, nx, ny, nranks):
     assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("filt", [False, True])
 @pytest.mark.parametrize("cfg,nx,ny,nranks,w,r", [(2, 96, 96, 2, 8, 4), (4, 128, 128, 2, 12, 6), (4, 128, 144, 3, 8, 4),
                                                    (4, 64, 64, 1, 8, 4)])
-def test_slab_algorithm1_matches_unsharded(inputs, cfg, nx, ny, nranks, w, r):
+def test_slab_algorithm1_matches_unsharded(inputs, cfg, nx, ny, nranks, w, r, filt):
     from paper_2301_01718_b200 import slab
     from paper_2301_01718_b200.hrom import cells_from_mask
-    wl, q0, ref, roms, comm = _mk(inputs, cfg, nranks, nx=nx, ny=ny, w=w, r=r)
+    wl, q0, ref, roms, comm = _mk(inputs, cfg, nranks, filt=filt, nx=nx, ny=ny, w=w, r=r)
     nsteps = w + 6
     for k in range(1, nsteps + 1):
         ref.step()
@@ -94,31 +97,57 @@ def test_slab_algorithm1_matches_unsharded(inputs, cfg, nx, ny, nranks, w, r):
     for x in roms:
         x.sync()
     assert all(x.effective_rank() == ref.effective_rank() for x in roms)
+    if filt:  # sweeps of the last step's cascade (ireg[4..6]) as the unsharded filter counted them
+        import ctypes as C
+        def sweeps(rom):
+            out = (C.c_int32 * 8)()
+            rom.lib.hrom_debug_counters(rom.h, C.cast(out, C.c_void_p), 8)
+            return list(out)[4:7]
+        assert all(sweeps(x) == sweeps(ref) for x in roms), (sweeps(ref), [sweeps(x) for x in roms])
 
 
 def test_slab_selection_matches_unsharded_sample(inputs):
-    """The distributed radix select (histogram all-reduce per pass, ties by ascending cell across
-    ranks) against hrom_sample on the same indicator, including ties at the threshold and fewer
-    positive cells than n_g."""
+    """The distributed radix select (histogram all-reduce per pass, tie quota by rank order, then by
+    cell) against hrom_sample on the same indicator: a trajectory's own indicator, equal values
+    straddling the threshold on every rank (ordered-tie path), and fewer positive cells than n_g."""
     from paper_2301_01718_b200 import slab
     from paper_2301_01718_b200.hrom import cells_from_mask
-    wl, q0, ref, roms, comm = _mk(inputs, 4, 3, nx=96, ny=96, w=8, r=4)
-    # run to the first sampling so that both sides hold an indicator, then compare masks
+    wl, q0, ref, roms, comm = _mk(inputs, 4, 3, filt=True, nx=96, ny=96, w=8, r=4)
     for _ in range(wl.w + 2):
         ref.step()
         slab.step_all(roms, comm)
-    eps = slab.assemble(roms, "indicator")
     m = torch.empty(ref.mask_words, dtype=torch.int32, device="cuda")
-    ref.sample(eps=eps, mask_out=m)
-    ref.sync()
-    assert np.array_equal(cells_from_mask(wl, m), cells_from_mask(wl, slab.assemble(roms, "mask")))
+
+    def check(eps):
+        ref.sample(eps=eps, mask_out=m)
+        ref.sync()
+        slab.resample_all(roms, comm, eps)
+        a, b = cells_from_mask(wl, m), cells_from_mask(wl, slab.assemble(roms, "mask"))
+        assert np.array_equal(a, b), (int(a.sum()), int(b.sum()))
+        return int(a.sum())
+
+    ng = int(np.ceil(wl.f * wl.N))
+    assert check(slab.assemble(roms, "indicator")) == ng
+    rng = np.random.RandomState(3)
+    e = rng.rand(wl.N) ** 3
+    e[rng.rand(wl.N) < 0.5] = 0.0
+    assert check(torch.from_numpy(e).cuda()) == ng
+    t = e.copy()
+    thr = np.sort(t)[::-1][ng - 1]
+    t[5:wl.N:11] = thr  # ~840 equal values at the threshold on every rank: only some are taken
+    assert check(torch.from_numpy(t).cuda()) == ng
+    few = np.zeros(wl.N)
+    few[rng.choice(wl.N, ng // 2, replace=False)] = 1.0 + rng.rand(ng // 2)
+    assert check(torch.from_numpy(few).cuda()) == ng // 2
+    allsame = np.full(wl.N, 0.5)  # every cell ties: the first n_g cells by index
+    assert check(torch.from_numpy(allsame).cuda()) == ng
 
 
 def test_slab_against_oracle(inputs, orc):
     """The sharded path against the CPU oracle (same bar as the unsharded trajectory tests while
     the trajectory is not yet sensitive): per-step relative error <= 1e-11 over w + 5 steps."""
     from paper_2301_01718_b200 import slab
-    wl, q0, ref, roms, comm = _mk(inputs, 4, 2, nx=64, ny=64, w=8, r=4)
+    wl, q0, ref, roms, comm = _mk(inputs, 4, 2, filt=True, nx=64, ny=64, w=8, r=4)
     R = orc.Run(wl, q0.cpu().numpy())
     for k in range(1, wl.w + 6):
         R.step()
