@@ -230,6 +230,8 @@ struct hrom_ctx {
   bool kinc_valid = false;
   int samples_since_gather = 99;  // samplings since the last gathered Gram (churn lists valid iff 1)
   bool eps_sparse = false;   // the indicator is nonzero only on the T list (set by a hybrid step)
+  bool gather_inc = false;          // the gathered Gram in flight took the incremental route (G7)
+  bool gather_skip_finish = false;  // ... or the ODEIM rows (no per-slot state)
   int64_t kinc_newest = -1, kinc_rebase = -1;
   hrom::Win eig_win{};
   // CUDA-graph replay of steady-state steps (hrom_set_graph)
@@ -289,6 +291,7 @@ hrom_status launch_positivity_redo(hrom_ctx* c, SRef qprev, SRef q, int64_t kq);
 hrom_status launch_smax(hrom_ctx* c, SRef q, unsigned long long* dev_out, int64_t n0, int64_t n1);
 // masks.cu
 hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S);
+hrom_status build_sets_with_churn(hrom_ctx* c);  // S-hat in place, its predecessor in M_SPREV
 hrom_status select_and_build(hrom_ctx* c, const double* eps, int64_t n_g, double rre_delta = 0.0);
 hrom_status odeim_for_basis(hrom_ctx* c);
 hrom_status project_window(hrom_ctx* c, const double* const* phicols, int m, double* dev_C);           // ODEIM points of the current basis (odeim.cu)
@@ -301,6 +304,13 @@ hrom_status gram_full(hrom_ctx* c, const double* const* dev_cols, int64_t ns, in
 hrom_status gram_full_dd(hrom_ctx* c, const double* const* dev_cols, int64_t ns, int ncol, int64_t rows, SRef rho,
                          double* dev_Chi, double* dev_Clo, int ldc, const int32_t* map);
 hrom_status gram_gathered(hrom_ctx* c, SRef src_b);
+// the two halves of gram_gathered with explicit cell lists (row slabs: own-row sub-lists)
+struct GatherLists {
+  const int32_t *S, *nS, *add, *nadd, *rem, *nrem;
+};
+hrom_status gram_gathered_partial(hrom_ctx* c, SRef src_b, const GatherLists* L);
+hrom_status gram_gathered_finish(hrom_ctx* c);
+double* gathered_gemv_values(hrom_ctx* c);
 hrom_status band_gram_rows(hrom_ctx* c, const Win& W, SRef v);
 // the same kernels on an explicit cell list (row slabs: the own rows of a set)
 hrom_status band_gram_rows_list(hrom_ctx* c, const Win& W, SRef v, const int32_t* list, const int32_t* count);

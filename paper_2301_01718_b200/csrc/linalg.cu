@@ -2046,15 +2046,20 @@ hrom_status project_window(hrom_ctx* c, const double* const* phicols, int m, dou
 }
 
 // gathered Gram R of [U, b] over the rows of S-hat (shifted by rho, union order, (nU+1)^2,
-// double-double: hi in b.eigV, lo in b.Rlo); the lagged centring is applied by solve_kernel
-hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
+// double-double: hi in b.eigV, lo in b.Rlo); the lagged centring is applied by solve_kernel.
+// Two halves, so that a row slab (slab.cu) can sum the ranks' partials in between: `partial`
+// leaves this context's sums over the rows of the given lists -- the full Gram in (b.eigV, b.Rlo),
+// or, on the incremental route (G7), the Grams of the entering / leaving rows in b.Rd and the two
+// GEMVs' reduced values behind the GEMV partials -- and `finish` turns them into R (and the
+// per-slot state Khi / Klo).  Every quantity is linear in the rows.
+hrom_status gram_gathered_partial(hrom_ctx* c, SRef src_b, const GatherLists* L) {
   GGArgs a{};
   a.g = c->g;
   a.W = c->win;
   a.ring = c->b.ring;
   a.rho = c->rho_ref();
-  a.list = c->b.lists + (int64_t)L_S * c->g.N;
-  a.count = c->b.counts + L_S;
+  a.list = L ? L->S : c->b.lists + (int64_t)L_S * c->g.N;
+  a.count = L ? L->nS : c->b.counts + L_S;
   a.src_b = src_b;
   a.mode = 1;
   // while the one-CTA eigen-solve of the previous update holds an SM (side stream), leave it
@@ -2066,59 +2071,78 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   auto gram = [&](GGArgs& aa, double* hi, double* lo) -> hrom_status {
     return run_gather_gram_dd(c, aa, ncol, grid, hi, lo, ncol, nullptr);
   };
+  c->gather_inc = false;
   if (c->P.odeim_points > 0) {  // gappy rows = the DOF rows of the ODEIM points (Eq. 8, 10)
     a.mode = 2;
     a.rowlist = c->b.orows;
     a.nrow2 = c->odeim_n;
     c->kinc_valid = false;
     c->samples_since_gather = 0;
+    c->gather_skip_finish = true;
     return gram(a, R, Rl);
   }
+  c->gather_skip_finish = false;
   const bool inc = c->P.gather_mode == 0 && c->kinc_valid && c->samples_since_gather == 1 && c->kinc_newest == c->k - 1 &&
                    c->kinc_rebase == c->rebase_k;
+  c->gather_inc = inc;
   hrom_status s;
-  if (!inc) {
-    if ((s = gram(a, R, Rl)) != HROM_OK) return s;
+  if (!inc) return gram(a, R, Rl);
+  // rows entering and leaving S-hat (cells of the last sampling's churn), double-double
+  const size_t S2 = (size_t)(kMaxW + 2) * (kMaxW + 2);
+  double* Rp = c->b.Rd;
+  double* Rpl = Rp + S2;
+  double* Rm = Rp + 2 * S2;
+  double* Rml = Rp + 3 * S2;
+  GGArgs d = a;
+  d.list = L ? L->add : c->b.lists + (int64_t)L_ADD * c->g.N;
+  d.count = L ? L->nadd : c->b.counts + L_ADD;
+  if ((s = gram(d, Rp, Rpl)) != HROM_OK) return s;
+  d.list = L ? L->rem : c->b.lists + (int64_t)L_REM * c->g.N;
+  d.count = L ? L->nrem : c->b.counts + L_REM;
+  if ((s = gram(d, Rm, Rml)) != HROM_OK) return s;
+  // GEMVs of the newest snapshot and of b over all S-hat rows: one wave (2 CTAs per SM), static
+  // split that avoids the eigen's SM.  (Tried: 512 threads with 5 slots per warp and 4 row
+  // chunks in flight -- 0.64 ms against 0.47 ms for the whole gathered Gram: the 16 warps'
+  // redundant rho / x_new / b loads of the same rows cost more than the extra memory-level
+  // parallelism gains.)
+  const int gblocks = 2 * (c->basis_pending ? c->nsm - 1 : c->nsm);
+  const int nv = 2 * a.W.nU + 1;
+  if (a.W.nU <= 9 * GV_W)
+    gemv_gather_kernel<9><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b, c->b.vpart,
+                                                       c->b.C);
+  else
+    gemv_gather_kernel<17><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b,
+                                                        c->b.vpart, c->b.C);
+  HROM_LAUNCH_CK();
+  double* v = gathered_gemv_values(c);
+  vpart_reduce<<<(nv * GR_TPE + 255) / 256, 256, 0, c->st>>>(c->b.vpart, gblocks, nv, v);
+  HROM_LAUNCH_CK();
+  c->nlaunch += 2;
+  return HROM_OK;
+}
+
+// reduced GEMV values v[2 nU + 1][hi, lo] of the incremental route: behind the largest possible
+// block of GEMV partials (fixed place: the same whatever grid the GEMV ran on)
+double* gathered_gemv_values(hrom_ctx* c) { return c->b.vpart + (size_t)2 * c->nsm * (2 * kMaxSlots + 2) * 2; }
+
+hrom_status gram_gathered_finish(hrom_ctx* c) {
+  if (c->gather_skip_finish) return HROM_OK;
+  const Win& W = c->win;
+  double* R = c->b.eigV;
+  double* Rl = c->b.Rlo;
+  if (!c->gather_inc) {
     if (c->P.gather_mode == 0) {
-      kinc_update_kernel<<<1, 512, 0, c->st>>>(a.W, 1, nullptr, nullptr, nullptr, nullptr, nullptr, c->b.Khi, c->b.Klo,
-                                               R, Rl);
+      kinc_update_kernel<<<1, 512, 0, c->st>>>(W, 1, nullptr, nullptr, nullptr, nullptr, nullptr, c->b.Khi, c->b.Klo, R, Rl);
       HROM_LAUNCH_CK();
       ++c->nlaunch;
     }
   } else {
-    // rows entering and leaving S-hat (cells of the last sampling's churn), double-double
     const size_t S2 = (size_t)(kMaxW + 2) * (kMaxW + 2);
     double* Rp = c->b.Rd;
-    double* Rpl = Rp + S2;
-    double* Rm = Rp + 2 * S2;
-    double* Rml = Rp + 3 * S2;
-    GGArgs d = a;
-    d.list = c->b.lists + (int64_t)L_ADD * c->g.N;
-    d.count = c->b.counts + L_ADD;
-    if ((s = gram(d, Rp, Rpl)) != HROM_OK) return s;
-    d.list = c->b.lists + (int64_t)L_REM * c->g.N;
-    d.count = c->b.counts + L_REM;
-    if ((s = gram(d, Rm, Rml)) != HROM_OK) return s;
-    // GEMVs of the newest snapshot and of b over all S-hat rows: one wave (2 CTAs per SM), static
-    // split that avoids the eigen's SM.  (Tried: 512 threads with 5 slots per warp and 4 row
-    // chunks in flight -- 0.64 ms against 0.47 ms for the whole gathered Gram: the 16 warps'
-    // redundant rho / x_new / b loads of the same rows cost more than the extra memory-level
-    // parallelism gains.)
-    const int gblocks = 2 * (c->basis_pending ? c->nsm - 1 : c->nsm);
-    const int nv = 2 * a.W.nU + 1;
-    if (a.W.nU <= 9 * GV_W)
-      gemv_gather_kernel<9><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b, c->b.vpart,
-                                                         c->b.C);
-    else
-      gemv_gather_kernel<17><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b,
-                                                          c->b.vpart, c->b.C);
+    kinc_update_kernel<<<1, 512, 0, c->st>>>(W, 0, Rp, Rp + S2, Rp + 2 * S2, Rp + 3 * S2, gathered_gemv_values(c), c->b.Khi,
+                                             c->b.Klo, R, Rl);
     HROM_LAUNCH_CK();
-    double* v = c->b.vpart + (size_t)gblocks * nv * 2;
-    vpart_reduce<<<(nv * GR_TPE + 255) / 256, 256, 0, c->st>>>(c->b.vpart, gblocks, nv, v);
-    HROM_LAUNCH_CK();
-    kinc_update_kernel<<<1, 512, 0, c->st>>>(a.W, 0, Rp, Rpl, Rm, Rml, v, c->b.Khi, c->b.Klo, R, Rl);
-    HROM_LAUNCH_CK();
-    c->nlaunch += 3;
+    ++c->nlaunch;
   }
   if (c->P.gather_mode == 0) {
     c->kinc_valid = true;
@@ -2127,6 +2151,12 @@ hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
   }
   c->samples_since_gather = 0;
   return HROM_OK;
+}
+
+hrom_status gram_gathered(hrom_ctx* c, SRef src_b) {
+  hrom_status s = gram_gathered_partial(c, src_b, nullptr);
+  if (s != HROM_OK) return s;
+  return gram_gathered_finish(c);
 }
 
 // seam-band part of the new window Gram row (band DOFs' final values), double-double partials

@@ -14,7 +14,7 @@ namespace cg = cooperative_groups;
 
 namespace hrom {
 hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long long n_g, bool sparse = false,
-                        double rre_delta = 0.0);
+                        double rre_delta = 0.0, bool use_prev = false);
 namespace {
 
 __device__ __forceinline__ int wrapi(int i, int n, int bc, bool* valid) {
@@ -98,6 +98,7 @@ constexpr int RADIX = 11, NBIN = 1 << RADIX;
 struct SetsArgs {
   Geo g;
   int do_select;
+  int use_prev;            // no selection, but M_SPREV holds the previous S-hat: build the churn lists from it
   const double* eps;
   long long n_g;
   int rre;                 // 1: RRE-delta rule instead of n_g
@@ -688,7 +689,7 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
       // band < 0: B = every cell off S-hat (whole-domain filter)
       TMP[w] = a.band < 0 ? row_valid(g, wq - jq * g.wpr) : xdil_word(S, g, jq, wq - jq * g.wpr, a.band);
       HM[w] = 0u;
-      const uint32_t sn = __ldcg(S + w), sp = a.do_select ? SPREV[w] : sn;
+      const uint32_t sn = __ldcg(S + w), sp = (a.do_select || a.use_prev) ? SPREV[w] : sn;
       MADD[w] = sn & ~sp;
       MREM[w] = sp & ~sn;
     }
@@ -896,8 +897,9 @@ __global__ void __launch_bounds__(ST_T) sets_kernel(SetsArgs a) {
 }  // namespace
 
 hrom_status launch_sets(hrom_ctx* c, bool do_select, const double* eps, long long n_g, bool sparse,
-                        double rre_delta) {
+                        double rre_delta, bool use_prev) {
   SetsArgs a{};
+  a.use_prev = use_prev ? 1 : 0;
   if (rre_delta > 0.0) {  // delta = dm 2^-sh exactly
     int ex;
     const double mant = std::frexp(rre_delta, &ex);
@@ -978,6 +980,14 @@ hrom_status build_sets(hrom_ctx* c, const uint32_t* dev_mask_S) {
     if ((s = or_cells_into_mask(c, S, c->b.ocells, c->odeim_n)) != HROM_OK) return s;
   }
   return launch_sets(c, false, nullptr, 0);
+}
+
+// the sets of an S-hat bitmap already in place whose predecessor is in M_SPREV (row slabs: the
+// selection ran across ranks, slab.cu): as build_sets, plus the churn lists of the incremental
+// gathered Gram (G7)
+hrom_status build_sets_with_churn(hrom_ctx* c) {
+  ++c->samples_since_gather;
+  return launch_sets(c, false, nullptr, 0, false, 0.0, true);
 }
 
 // top-n_g of eps > 0 -> S-hat (ties at the threshold by ascending cell), then build_sets.

@@ -67,7 +67,10 @@ struct hrom_slab {
   int32_t* listS = nullptr;  // own rows of S-hat (sub-list of L_S)
   int32_t* listB = nullptr;  // own rows of the band
   int32_t* listA = nullptr;  // every own cell
-  int32_t* cnt = nullptr;    // [0] |listS| [1] |listB| [2] |listA|
+  int32_t* listAdd = nullptr;  // own rows of the cells entering / leaving S-hat at the last sampling (G7)
+  int32_t* listRem = nullptr;
+  int32_t* cnt = nullptr;    // [0] |listS| [1] |listB| [2] |listA| [3] |listAdd| [4] |listRem|
+  bool have_prev = false;    // M_SPREV holds the S-hat of the previous sampling
   uint32_t* mBH = nullptr;   // band u halo rows: cells left out of the fused Gram row
   unsigned long long* sel = nullptr;  // [0] prefix [1] remaining [2] tau [3] quota [4] my ties [5] all-positive flag [6] scratch smax
   int32_t* hist = nullptr;   // 2048
@@ -120,16 +123,18 @@ __global__ void smax_reduce_kernel(const unsigned char* __restrict__ gath, int64
 }
 
 // double-double all-reduce SUM in rank order: message part = hi[n] then lo[n]
-__global__ void dd_sum_kernel(const unsigned char* __restrict__ gath, int64_t stride, int64_t off, int P, int n,
-                              double* __restrict__ hi, double* __restrict__ lo) {
+// (il = 1: pairs interleaved [i][hi, lo] on both sides, hi / lo = the arrays' first hi / lo element)
+__global__ void dd_sum_kernel(const unsigned char* __restrict__ gath, int64_t stride, int64_t off, int P, int n, int il,
+                              double* hi, double* lo) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double h = 0.0, l = 0.0;
     for (int r = 0; r < P; ++r) {
       const double* p = reinterpret_cast<const double*>(gath + r * stride + off);
-      dd_add(h, l, p[i], p[n + i]);
+      if (il) dd_add(h, l, p[2 * i], p[2 * i + 1]);
+      else dd_add(h, l, p[i], p[n + i]);
     }
-    hi[i] = h;
-    lo[i] = l;
+    hi[il ? 2 * i : i] = h;
+    lo[il ? 2 * i : i] = l;
   }
 }
 
@@ -596,10 +601,19 @@ hrom_status unpack_halo(hrom_ctx* c, SRef q, const unsigned char* gath, int64_t 
 // own-row sub-lists and the fill's exclusion mask
 hrom_status finish_sets(hrom_ctx* c) {
   hrom_slab* s = c->slab;
-  hrom_status st = build_sets(c, nullptr);
+  // with the previous S-hat in M_SPREV the sets kernel also lists the churn (G7)
+  hrom_status st = s->have_prev ? build_sets_with_churn(c) : build_sets(c, nullptr);
   if (st != HROM_OK) return st;
   const Geo& g = c->g;
   const int lo = s->hlo * g.nx, hi = (s->hlo + s->own) * g.nx;
+  if (s->have_prev) {
+    own_list_kernel<<<grid_for(c, g.N), 256, 0, c->st>>>(c->b.lists + (int64_t)L_ADD * g.N, c->b.counts + L_ADD, lo, hi,
+                                                        s->listAdd, s->cnt + 3);
+    own_list_kernel<<<grid_for(c, g.N), 256, 0, c->st>>>(c->b.lists + (int64_t)L_REM * g.N, c->b.counts + L_REM, lo, hi,
+                                                        s->listRem, s->cnt + 4);
+    c->nlaunch += 2;
+  }
+  s->have_prev = true;
   own_list_kernel<<<grid_for(c, g.N), 256, 0, c->st>>>(c->b.lists + (int64_t)L_S * g.N, c->b.counts + L_S, lo, hi,
                                                       s->listS, s->cnt + 0);
   own_list_kernel<<<grid_for(c, g.N), 256, 0, c->st>>>(c->b.lists + (int64_t)L_B * g.N, c->b.counts + L_B, lo, hi,
@@ -734,7 +748,7 @@ hrom_status end_filter(hrom_ctx* c, unsigned char* send, int64_t* bytes) {
 void slab_destroy(hrom_ctx* c) {
   hrom_slab* s = c->slab;
   if (!s) return;
-  void* ptrs[] = {s->listS, s->listB, s->listA, s->cnt, s->mBH, s->sel, s->hist, s->stage, s->fstat};
+  void* ptrs[] = {s->listS, s->listB, s->listA, s->listAdd, s->listRem, s->cnt, s->mBH, s->sel, s->hist, s->stage, s->fstat};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete s;
@@ -767,7 +781,7 @@ hrom_status hrom_slab_create(const hrom_grid* grid, double gamma, double cfl, co
   hrom_grid lg = *grid;
   lg.ny = info.rows_own + info.halo_lo + info.halo_hi;
   hrom_params lp = *p;
-  lp.gather_mode = 1;  // S-hat arrives as an explicit bitmap every step: no churn lists
+  lp.gather_mode = 0;  // incremental gathered Gram (G7): the churn lists are rebuilt from M_SPREV (finish_sets)
   hrom_ctx* c = nullptr;
   if ((st = hrom_create(&lg, gamma, cfl, &lp, stream, &c)) != HROM_OK) return st;
   if (c->P.gram_mode != 0) {  // the fused Gram row (w + 1 <= 68) carries the halo exclusion
@@ -797,13 +811,15 @@ hrom_status hrom_slab_create(const hrom_grid* grid, double gamma, double cfl, co
   s->N_g = (int64_t)grid->nx * grid->ny;
   s->halo_doubles = (int64_t)g.c * s->H * g.nx;
   s->mask_words = (int64_t)s->H * g.wpr;
-  const int64_t r_bytes = (int64_t)2 * (kMaxW + 2) * (kMaxW + 2) * 8;
+  const int64_t r_bytes = (int64_t)(4 * (kMaxW + 2) * (kMaxW + 2) + 2 * (2 * kMaxW + 3)) * 8;
   s->max_msg = std::max<int64_t>({end_layout(s).bytes, r_bytes, (int64_t)NBIN * 4, 2 * s->mask_words * 4, 16});
   auto A = [&](hrom_status r) { if (r != HROM_OK) st = r; };
   A(salloc(&s->listS, g.N));
   A(salloc(&s->listB, g.N));
   A(salloc(&s->listA, g.N));
-  A(salloc(&s->cnt, 4));
+  A(salloc(&s->listAdd, g.N));
+  A(salloc(&s->listRem, g.N));
+  A(salloc(&s->cnt, 8));
   A(salloc(&s->mBH, c->mwords));
   A(salloc(&s->sel, 8));
   A(salloc(&s->hist, NBIN));
@@ -858,6 +874,7 @@ hrom_status hrom_slab_set_state(hrom_ctx* c, const double* any_q_global) {
     }
   }
   s->phase = PH_IDLE;
+  s->have_prev = false;
   return hrom_set_state(c, s->stage);
 }
 
@@ -977,12 +994,24 @@ hrom_status hrom_slab_step(hrom_ctx* c, const void* dev_gathered, void* dev_send
     if ((st = launch_stage(c, 1, qn, qn, U1, Ls + (int64_t)L_A1 * g.N, L_A1, 0.0)) != HROM_OK) return st;
     if ((st = launch_stage(c, 2, qn, U1, U2, Ls + (int64_t)L_A2 * g.N, L_A2, 0.0)) != HROM_OK) return st;
     if ((st = launch_stage(c, 3, qn, U2, U3, Ls + (int64_t)L_T * g.N, L_T, 0.0)) != HROM_OK) return st;
-    // H4 on the own rows of S-hat
-    if ((st = gram_gathered_list(c, c->win, U3, s->listS, s->cnt + 0, b.eigV, b.Rlo)) != HROM_OK) return st;
+    // H4 on the own rows of S-hat: the full gathered Gram, or (G7) the Grams of the own rows that
+    // entered / left S-hat and the two GEMVs -- every part is a sum over rows, so the ranks' parts add
+    GatherLists GL{s->listS, s->cnt + 0, s->listAdd, s->cnt + 3, s->listRem, s->cnt + 4};
+    if ((st = gram_gathered_partial(c, U3, &GL)) != HROM_OK) return st;
     const int ncol = c->win.nU + 1, n2 = ncol * ncol;
-    HROM_CK(cudaMemcpyAsync(send, b.eigV, (size_t)n2 * 8, cudaMemcpyDeviceToDevice, c->st));
-    HROM_CK(cudaMemcpyAsync(send + (size_t)n2 * 8, b.Rlo, (size_t)n2 * 8, cudaMemcpyDeviceToDevice, c->st));
-    *send_bytes_out = (int64_t)2 * n2 * 8;
+    if (!c->gather_inc) {
+      HROM_CK(cudaMemcpyAsync(send, b.eigV, (size_t)n2 * 8, cudaMemcpyDeviceToDevice, c->st));
+      HROM_CK(cudaMemcpyAsync(send + (size_t)n2 * 8, b.Rlo, (size_t)n2 * 8, cudaMemcpyDeviceToDevice, c->st));
+      *send_bytes_out = (int64_t)2 * n2 * 8;
+    } else {
+      const size_t S2 = (size_t)(kMaxW + 2) * (kMaxW + 2);
+      const int nv = 2 * c->win.nU + 1;
+      for (int q = 0; q < 4; ++q)  // R+ hi, lo, R- hi, lo
+        HROM_CK(cudaMemcpyAsync(send + (size_t)q * n2 * 8, b.Rd + q * S2, (size_t)n2 * 8, cudaMemcpyDeviceToDevice, c->st));
+      HROM_CK(cudaMemcpyAsync(send + (size_t)4 * n2 * 8, gathered_gemv_values(c), (size_t)2 * nv * 8,
+                              cudaMemcpyDeviceToDevice, c->st));
+      *send_bytes_out = (int64_t)(4 * n2 + 2 * nv) * 8;
+    }
     s->phase = PH_R;
     return HROM_OK;
   }
@@ -994,9 +1023,22 @@ hrom_status hrom_slab_step(hrom_ctx* c, const void* dev_gathered, void* dev_send
     const SRef out = c->slot_ref(c->slot_of(kn));
     const SRef U3 = plain(b.U3);
     const int ncol = c->win.nU + 1, n2 = ncol * ncol;
-    dd_sum_kernel<<<(n2 + 255) / 256, 256, 0, c->st>>>(gath, (int64_t)2 * n2 * 8, 0, P, n2, b.eigV, b.Rlo);
+    if (!c->gather_inc) {
+      dd_sum_kernel<<<(n2 + 255) / 256, 256, 0, c->st>>>(gath, (int64_t)2 * n2 * 8, 0, P, n2, 0, b.eigV, b.Rlo);
+      ++c->nlaunch;
+    } else {
+      const size_t S2 = (size_t)(kMaxW + 2) * (kMaxW + 2);
+      const int nv = 2 * c->win.nU + 1;
+      const int64_t stride = (int64_t)(4 * n2 + 2 * nv) * 8;
+      dd_sum_kernel<<<(n2 + 255) / 256, 256, 0, c->st>>>(gath, stride, 0, P, n2, 0, b.Rd, b.Rd + S2);
+      dd_sum_kernel<<<(n2 + 255) / 256, 256, 0, c->st>>>(gath, stride, (int64_t)2 * n2 * 8, P, n2, 0, b.Rd + 2 * S2,
+                                                         b.Rd + 3 * S2);
+      double* v = gathered_gemv_values(c);
+      dd_sum_kernel<<<(nv + 255) / 256, 256, 0, c->st>>>(gath, stride, (int64_t)4 * n2 * 8, P, nv, 1, v, v + 1);
+      c->nlaunch += 3;
+    }
     HROM_LAUNCH_CK();
-    ++c->nlaunch;
+    if ((st = gram_gathered_finish(c)) != HROM_OK) return st;
     basis_join(c);
     if ((st = small_solve(c)) != HROM_OK) return st;  // H5, replicated: identical y on every rank
     HROM_CK(cudaMemsetAsync(b.eps, 0, g.N * sizeof(double), c->st));
@@ -1094,7 +1136,7 @@ hrom_status hrom_slab_step(hrom_ctx* c, const void* dev_gathered, void* dev_send
   if (s->phase == PH_BOOT) {
     const Win W = window_of(c, c->k);
     const int ncol = W.nU + 1, n2 = ncol * ncol;
-    dd_sum_kernel<<<(n2 + 255) / 256, 256, 0, c->st>>>(gath, (int64_t)2 * n2 * 8, 0, P, n2, b.eigV, b.Rlo);
+    dd_sum_kernel<<<(n2 + 255) / 256, 256, 0, c->st>>>(gath, (int64_t)2 * n2 * 8, 0, P, n2, 0, b.eigV, b.Rlo);
     scatter_gram_kernel<<<1, 1024, 0, c->st>>>(b.eigV, b.Rlo, ncol, W, b.C, b.Clo, kMaxSlots);
     HROM_LAUNCH_CK();
     c->nlaunch += 2;
@@ -1116,6 +1158,8 @@ hrom_status hrom_slab_step(hrom_ctx* c, const void* dev_gathered, void* dev_send
     // S-hat_{k+1} on the own rows, then its edge rows for the neighbours
     uint32_t* S = b.masks + (int64_t)M_S * c->mwords;
     const int r0 = s->hlo, r1 = s->hlo + s->own;
+    HROM_CK(cudaMemcpyAsync(b.masks + (int64_t)M_SPREV * c->mwords, S, c->mwords * sizeof(uint32_t),
+                            cudaMemcpyDeviceToDevice, c->st));
     sel_mark_kernel<<<grid_for(c, (int64_t)s->own * g.wpr), 256, 0, c->st>>>(g, b.eps, r0, r1, s->sel, S);
     sel_ties_kernel<<<1, 1024, 0, c->st>>>(g, b.eps, r0, r1, s->sel, S);
     HROM_LAUNCH_CK();
