@@ -263,6 +263,57 @@ def run_hrom(args, rank, world, local_rank):
     return out
 
 
+def run_slab(args, rank, world, local_rank):
+    """--shard slab: ONE config-4 problem cut into row slabs, one per rank:
+    halo rows to the neighbours and the small all-reduces of csrc/slab.cu over NCCL every step;
+    strong scaling (the grid is fixed, value = N / step time).  The driver's default run is the
+    replica mode; this mode exists for multi-GPU boxes and is exercised with one rank on one GPU."""
+    import torch
+    import torch.distributed as dist
+    from paper_2301_01718_b200 import inputs, slab
+    torch.cuda.set_device(local_rank)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=rank, world_size=world)
+    wl = inputs.config(args.config, f=args.fraction, seed=rank_seed(args.config, 0))  # the same problem on every rank
+    q0 = torch.from_numpy(inputs.initial_condition(wl)).cuda()
+    comm = slab.DistComm()
+    rom = slab.SlabROM(wl, rank, world)
+    rom.set_state(q0)
+    for _ in range(wl.w - 1 + args.warmup):
+        rom.step(comm)
+    rom.sync()
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = int(rom.lib.hrom_launch_count(rom.h))
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        rom.step(comm)
+    ev1.record()
+    ev1.synchronize()
+    rom.sync()
+    launches = int(rom.lib.hrom_launch_count(rom.h)) - l0
+    (ms_step,) = reduce_max_over_ranks([ev0.elapsed_time(ev1) / args.steps], dist if world > 1 else None, "cuda")
+    out = None
+    if rank == 0:
+        out = {"metric": METRIC, "value": wl.N / (ms_step / 1000.0), "unit": "cell-updates/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (seeded config-4 blasts, BASELINE.json configs[3]; DESIGN.md §3)",
+               "config": {"workload": wl.name, "grid": f"{wl.nx}x{wl.ny}", "cells": wl.N, "window_w": wl.w,
+                          "rank_r": wl.r, "sample_fraction": wl.f,
+                          "parallelism": f"row slabs x{world} (halo {int(rom.info.halo)} rows, {int(rom.info.rows_own)} own rows on rank 0)",
+                          "l2": "inputs larger than L2"},
+               "gpu_launches": launches}
+    rom.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    return out
+
+
 def H_count(rom, wl):
     from paper_2301_01718_b200.hrom import cells_from_mask
     return int(cells_from_mask(wl, rom.mask()).sum())
@@ -319,6 +370,9 @@ def main():
     ap.add_argument("--fraction", type=float, default=0.10)
     ap.add_argument("--gram-mode", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--shard", default="replicas", choices=["replicas", "slab"],
+                    help="replicas: one independent problem per GPU (default, weak scaling); slab: one problem cut "
+                         "into row slabs across the GPUs (strong scaling, DESIGN.md §6)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -348,6 +402,11 @@ def main():
                           "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
                                   "d2h_bytes_per_step": 0},
                           "wall_s": time.perf_counter() - t0}))
+        return
+    if args.shard == "slab":
+        out = run_slab(args, rank, world, local_rank)
+        if rank == 0 and out is not None:
+            print(json.dumps(out))
         return
     out = run_hrom(args, rank, world, local_rank)
     if rank == 0 and out is not None:
