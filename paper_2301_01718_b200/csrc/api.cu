@@ -438,8 +438,11 @@ hrom_status hrom_full_step(hrom_ctx* c, double dt_override, double* dev_dt_out) 
   if (dev_dt_out) HROM_CK(cudaMemcpyAsync(dev_dt_out, c->b.dreg, sizeof(double), cudaMemcpyDefault, c->st));
   if ((s = launch_stage(c, 1, qn, qn, U1, nullptr, 0, dt_override)) != HROM_OK) return s;
   if ((s = launch_stage(c, 2, qn, U1, U2, nullptr, 0, dt_override)) != HROM_OK) return s;
-  if ((s = launch_stage(c, 3, qn, U2, out, nullptr, 0, dt_override)) != HROM_OK) return s;
+  // 2-D: the last stage also takes the new state's wave-speed maximum (the next step's H1)
+  const bool fuse = c->g.dim == 2 && !c->slab && dt_override <= 0.0;
+  if ((s = launch_stage(c, 3, qn, U2, out, nullptr, 0, dt_override, nullptr, fuse)) != HROM_OK) return s;
   prof_end(c, SEC_FULL);
+  if (fuse) c->smax_k = kn;
   c->k = kn;
   c->points_used = 0;
   c->last_hybrid = false;

@@ -164,12 +164,18 @@ __global__ void __launch_bounds__(256) stage_kernel(Geo g, int stage, const SRef
 // mask (nullable): the stage's cell set (row-padded bitmap; one 32-cell tile row = one word);
 // tiles without an active cell exit at once, inactive cells of active tiles are not written.
 constexpr int TX = 32, TY = 8, TH = 2;  // tile, halo (MUSCL radius)
-template <int RECON>
-__global__ void __launch_bounds__(TX * TY) stage_tile_kernel(Geo g, int stage, const SRef qn, const SRef qin,
+// six resident blocks per SM (40 registers, ~120 B of spills): the kernel is bound by barrier and
+// memory latency, so the occupancy pays (2048^2 full step 0.90 -> 0.64 ms; 5 blocks: 0.67, 8: 0.85)
+#ifndef STAGE_MINB
+#define STAGE_MINB 6
+#endif
+template <int RECON, bool MASKED>
+__global__ void __launch_bounds__(TX * TY, MASKED ? 1 : STAGE_MINB) stage_tile_kernel(Geo g, int stage, const SRef qn, const SRef qin,
                                                            const SRef out, const uint32_t* __restrict__ mask,
                                                            const double* __restrict__ dtp,
                                                            const int32_t* __restrict__ tiles,
-                                                           const int32_t* __restrict__ ntiles_p) {
+                                                           const int32_t* __restrict__ ntiles_p,
+                                                           unsigned long long* __restrict__ smax_out) {
   constexpr int C = 4, R = RECON;
   constexpr int SX = TX + 2 * TH, SY = TY + 2 * TH;
   __shared__ double U[C][SY][SX];        // cross region (corners unused)
@@ -179,15 +185,16 @@ __global__ void __launch_bounds__(TX * TY) stage_tile_kernel(Geo g, int stage, c
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int ntx = (g.nx + TX - 1) / TX;
   // tiles: persistent loop over the listed active tiles (masked stages), or one tile per block
-  const int ntiles = tiles ? *ntiles_p : (int)gridDim.x;
-  for (int it = blockIdx.x; it < ntiles; it += (tiles ? (int)gridDim.x : ntiles)) {
-    const int tile = tiles ? tiles[it] : it;
+  // MASKED = false (full step): one tile per block, no bitmap, no tile list
+  const int ntiles = MASKED ? *ntiles_p : (int)gridDim.x;
+  for (int it = blockIdx.x; it < ntiles; it += (MASKED ? (int)gridDim.x : ntiles)) {
+    const int tile = MASKED ? tiles[it] : it;
     const int bx = tile % ntx, by = tile / ntx;
     const int i0 = bx * TX, j0 = by * TY;
     const int i = i0 + tx, j = j0 + ty;
     // active for this stage's set?
     uint32_t myword = 0;
-    if (mask) {
+    if (MASKED) {
       __syncthreads();  // U / Fx / Fy / any of the previous tile are consumed
       if (threadIdx.x == 0) any = 0;
       __syncthreads();
@@ -240,9 +247,11 @@ __global__ void __launch_bounds__(TX * TY) stage_tile_kernel(Geo g, int stage, c
       for (int v = 0; v < C; ++v) Fy[v][fy][fx] = F[v];
     }
     __syncthreads();
-    if (i < g.nx && j < g.ny && (!mask || ((myword >> tx) & 1u))) {
+    double smx = 0.0;  // H1 of the NEXT step, fused into the last stage of a full step (smax_out)
+    if (i < g.nx && j < g.ny && (!MASKED || ((myword >> tx) & 1u))) {
       const double dt = *dtp;
       const int64_t n = (int64_t)j * g.nx + i;
+      double Unew[C];
 #pragma unroll
       for (int v = 0; v < C; ++v) {
         double L = -div_dx(g, Fx[v][ty][tx + 1] - Fx[v][ty][tx]);
@@ -254,9 +263,35 @@ __global__ void __launch_bounds__(TX * TY) stage_tile_kernel(Geo g, int stage, c
         else if (stage == 2) r = 0.75 * un + 0.25 * (U[v][ty + TH][tx + TH] + dt * L);
         else r = (1.0 / 3.0) * un + (2.0 / 3.0) * (U[v][ty + TH][tx + TH] + dt * L);
         out.p[sidx(out, e)] = r;
+        Unew[v] = r;
+      }
+      if (!MASKED && smax_out) {
+        // the divided forms of the CFL rule (O7), as smax_kernel: the same bits as a separate pass
+        const double p = pressure<2>(Unew, g.gamma - 1.0);
+        const double cs = sqrt(g.gamma * p / Unew[0]);
+        smx = div_dx(g, fabs(Unew[1] / Unew[0]) + cs);
+        smx = smx + div_dy(g, fabs(Unew[2] / Unew[0]) + cs);
       }
     }
-    if (!tiles) break;
+    if (!MASKED && smax_out) {  // block maximum (NaN sticks), one integer atomicMax per tile
+      double m = smx;
+      if (m != m) m = __longlong_as_double(0x7ff8000000000000ll);
+      for (int o = 16; o > 0; o >>= 1) {
+        const double t = __shfl_xor_sync(0xffffffffu, m, o);
+        if (!(t <= m)) m = t;
+      }
+      __shared__ double smw[TX * TY / 32];
+      if ((threadIdx.x & 31) == 0) smw[threadIdx.x >> 5] = m;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int k = 1; k < TX * TY / 32; ++k)
+          if (!(smw[k] <= m)) m = smw[k];
+        unsigned long long bits = (unsigned long long)__double_as_longlong(m);
+        if (m != m) bits = 0x7ff8000000000000ull;
+        atomicMax(smax_out, bits);
+      }
+    }
+    if (!MASKED) break;
   }
 }
 
@@ -404,7 +439,7 @@ hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override, int64_t kq) {
 }
 
 hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, const int32_t* list, int list_idx,
-                         double /*dt_override*/, const unsigned long long* run_if) {
+                         double /*dt_override*/, const unsigned long long* run_if, bool fuse_smax) {
   // conditional (escalation) launches almost always exit at once: a small grid-stride grid
   const int grid = run_if ? c->nsm * 2 : c->nsm * 8;
   const int32_t* cnt = list ? c->b.counts + list_idx : nullptr;
@@ -419,8 +454,16 @@ hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, co
     const int32_t* tl = list ? c->b.lists + (int64_t)L_A2 * g.N : nullptr;  // tile list (2-D)
     const int32_t* tn = c->b.counts + 10;
     const int grid = list ? std::min(tiles, 8 * c->nsm) : tiles;
-    if (g.recon == 1) stage_tile_kernel<1><<<grid, TX * TY, 0, c->st>>>(g, stage, qn, qin, out, mask, c->b.dreg, tl, tn);
-    else stage_tile_kernel<2><<<grid, TX * TY, 0, c->st>>>(g, stage, qn, qin, out, mask, c->b.dreg, tl, tn);
+    // fuse_smax (last stage of a full step over the whole grid): the new state's wave-speed maximum
+    // goes to ureg[2] (zeroed by this step's dt_finalize), as after the positivity pass
+    unsigned long long* sm = (fuse_smax && !list) ? c->b.ureg + 2 : nullptr;
+    if (list) {
+      if (g.recon == 1) stage_tile_kernel<1, true><<<grid, TX * TY, 0, c->st>>>(g, stage, qn, qin, out, mask, c->b.dreg, tl, tn, sm);
+      else stage_tile_kernel<2, true><<<grid, TX * TY, 0, c->st>>>(g, stage, qn, qin, out, mask, c->b.dreg, tl, tn, sm);
+    } else {
+      if (g.recon == 1) stage_tile_kernel<1, false><<<grid, TX * TY, 0, c->st>>>(g, stage, qn, qin, out, mask, c->b.dreg, tl, tn, sm);
+      else stage_tile_kernel<2, false><<<grid, TX * TY, 0, c->st>>>(g, stage, qn, qin, out, mask, c->b.dreg, tl, tn, sm);
+    }
   } else if (g.dim == 1) {
     if (g.recon == 1) stage_kernel<1, 1><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg, run_if, ec);
     else stage_kernel<1, 2><<<grid, 256, 0, c->st>>>(g, stage, qn, qin, out, list, cnt, c->b.dreg, run_if, ec);

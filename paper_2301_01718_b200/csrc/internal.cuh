@@ -282,7 +282,7 @@ __host__ __device__ __forceinline__ double div_dy(const Geo& g, double x) { retu
 // euler.cu
 hrom_status launch_dt(hrom_ctx* c, SRef q, double dt_override, int64_t kq);
 hrom_status launch_stage(hrom_ctx* c, int stage, SRef qn, SRef qin, SRef out, const int32_t* list, int list_idx,
-                         double dt_override, const unsigned long long* run_if = nullptr);
+                         double dt_override, const unsigned long long* run_if = nullptr, bool fuse_smax = false);
 hrom_status launch_positivity(hrom_ctx* c, SRef qprev, SRef q, int64_t kq);
 // flag ureg[3] and maximum ureg[2] over the cells [n0, n1) (n1 < 0: all)
 hrom_status launch_positivity_check(hrom_ctx* c, SRef q, int64_t n0, int64_t n1);
