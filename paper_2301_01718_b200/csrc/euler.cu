@@ -79,8 +79,14 @@ __device__ __forceinline__ void face_flux(const double* Uam, const double* Ua, c
 
 __device__ __forceinline__ int wrap(int i, int n, int bc) {
   if (bc == 1) {
-    i = i % n;
-    return i < 0 ? i + n : i;
+    // stencil offsets are small: one conditional add / subtract almost always lands in range
+    if (i < 0) i += n;
+    else if (i >= n) i -= n;
+    if ((unsigned)i >= (unsigned)n) {
+      i = i % n;
+      if (i < 0) i += n;
+    }
+    return i;
   }
   return i < 0 ? 0 : (i >= n ? n - 1 : i);
 }
@@ -169,8 +175,11 @@ constexpr int TX = 32, TY = 8, TH = 2;  // tile, halo (MUSCL radius)
 #ifndef STAGE_MINB
 #define STAGE_MINB 6
 #endif
+#ifndef STAGE_MINB_MASKED
+#define STAGE_MINB_MASKED 4
+#endif
 template <int RECON, bool MASKED>
-__global__ void __launch_bounds__(TX * TY, MASKED ? 1 : STAGE_MINB) stage_tile_kernel(Geo g, int stage, const SRef qn, const SRef qin,
+__global__ void __launch_bounds__(TX * TY, MASKED ? STAGE_MINB_MASKED : STAGE_MINB) stage_tile_kernel(Geo g, int stage, const SRef qn, const SRef qin,
                                                            const SRef out, const uint32_t* __restrict__ mask,
                                                            const double* __restrict__ dtp,
                                                            const int32_t* __restrict__ tiles,
@@ -213,6 +222,13 @@ __global__ void __launch_bounds__(TX * TY, MASKED ? 1 : STAGE_MINB) stage_tile_k
 #pragma unroll
       for (int v = 0; v < C; ++v) U[v][ly][lx] = __ldg(qin.p + sidx(qin, v * g.N + n));
     }
+    // gamma_n of this thread's cell for the stage combination: issued now, consumed after the
+    // flux phase (stage 1 combines with the staged value itself)
+    const bool mine = i < g.nx && j < g.ny && (!MASKED || ((myword >> tx) & 1u));
+    double unv[C];
+#pragma unroll
+    for (int v = 0; v < C; ++v)
+      unv[v] = (mine && stage != 1) ? qn.p[sidx(qn, v * g.N + (int64_t)j * g.nx + i)] : 0.0;
     __syncthreads();
     // x-faces: face f between local columns f-1 and f (f = 0..TX), rows 0..TY-1
     for (int f = threadIdx.x; f < (TX + 1) * TY; f += TX * TY) {
@@ -248,7 +264,7 @@ __global__ void __launch_bounds__(TX * TY, MASKED ? 1 : STAGE_MINB) stage_tile_k
     }
     __syncthreads();
     double smx = 0.0;  // H1 of the NEXT step, fused into the last stage of a full step (smax_out)
-    if (i < g.nx && j < g.ny && (!MASKED || ((myword >> tx) & 1u))) {
+    if (mine) {
       const double dt = *dtp;
       const int64_t n = (int64_t)j * g.nx + i;
       double Unew[C];
@@ -257,7 +273,7 @@ __global__ void __launch_bounds__(TX * TY, MASKED ? 1 : STAGE_MINB) stage_tile_k
         double L = -div_dx(g, Fx[v][ty][tx + 1] - Fx[v][ty][tx]);
         L = L - div_dy(g, Fy[v][ty + 1][tx] - Fy[v][ty][tx]);
         const int64_t e = v * g.N + n;
-        const double un = qn.p[sidx(qn, e)];
+        const double un = stage == 1 ? U[v][ty + TH][tx + TH] : unv[v];  // stage 1: qin = gamma_n
         double r;
         if (stage == 1) r = un + dt * L;
         else if (stage == 2) r = 0.75 * un + 0.25 * (U[v][ty + TH][tx + TH] + dt * L);
