@@ -339,15 +339,16 @@ __global__ void __launch_bounds__(FILL_THREADS, 1) fill_kernel(FillArgs a) {
 // C row of the new slot = sum of the fill partials (+ the seam-band partials), 16 threads per
 // entry with a fixed-order tree (deterministic)
 // (double-double partials [blk][nU + 1][hi, lo]; row written to Chi / Clo)
-__global__ void __launch_bounds__(1024) gram_row_reduce(const double* __restrict__ part, int nblk,
+// (one 256-thread block per 16 entries: the per-entry order does not depend on the grid)
+__global__ void __launch_bounds__(256) gram_row_reduce(const double* __restrict__ part, int nblk,
                                                         const double* __restrict__ bpart, int nbblk, Win W,
                                                         int new_slot, double* __restrict__ C, double* __restrict__ Clo,
                                                         int ldc, const unsigned long long* __restrict__ esc) {
   const int nU = W.nU;
   if (esc && *esc != ~0ull) bpart = nullptr;  // escalated step: the row was recomputed from gamma_k
   constexpr int TPE = 16;
-  for (int base = 0; base < (nU + 1) * TPE; base += blockDim.x) {
-    const int idx = base + threadIdx.x, s = idx / TPE, sub = idx % TPE;
+  {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x, s = idx / TPE, sub = idx % TPE;
     double a = 0.0, al = 0.0, bsum = 0.0, bl = 0.0;
     if (s <= nU) {
       for (int b = sub; b < nblk; b += TPE) {
@@ -469,7 +470,7 @@ hrom_status launch_gram_row(hrom_ctx* c, const Win& W, int new_slot, const unsig
 
 hrom_status reduce_gram_row(hrom_ctx* c, const Win& W, int new_slot, bool with_band,
                             const unsigned long long* esc) {
-  gram_row_reduce<<<1, 1024, 0, c->st>>>(c->b.gpart, c->fill_grid,
+  gram_row_reduce<<<((W.nU + 1) * 16 + 255) / 256, 256, 0, c->st>>>(c->b.gpart, c->fill_grid,
                                          with_band ? c->b.gpart + (int64_t)c->fill_blocks * (W.nU + 1) * 2 : nullptr,
                                          c->band_blocks, W, new_slot, c->b.C, c->b.Clo, kMaxSlots, esc);
   HROM_LAUNCH_CK();

@@ -151,12 +151,12 @@ __global__ void scatter_gram_kernel(const double* __restrict__ Rh, const double*
 
 // local part of the new window-Gram row: fill partials + band partials in the same fixed order
 // as gram_row_reduce (fill.cu), written to the message (hi[ROW_SLOTS], lo[ROW_SLOTS]) instead of C
-__global__ void __launch_bounds__(1024) slab_row_reduce(const double* __restrict__ part, int nblk,
+__global__ void __launch_bounds__(256) slab_row_reduce(const double* __restrict__ part, int nblk,
                                                         const double* __restrict__ bpart, int nbblk, int nU,
                                                         double* __restrict__ out) {
   constexpr int TPE = 16;
-  for (int base = 0; base < (nU + 1) * TPE; base += blockDim.x) {
-    const int idx = base + threadIdx.x, s = idx / TPE, sub = idx % TPE;
+  {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x, s = idx / TPE, sub = idx % TPE;
     double a = 0.0, al = 0.0, bsum = 0.0, bl = 0.0;
     if (s <= nU) {
       for (int b = sub; b < nblk; b += TPE) {
@@ -182,7 +182,8 @@ __global__ void __launch_bounds__(1024) slab_row_reduce(const double* __restrict
       out[ROW_SLOTS + s] = al;
     }
   }
-  for (int s = nU + 1 + threadIdx.x; s < ROW_SLOTS; s += blockDim.x) out[s] = out[ROW_SLOTS + s] = 0.0;
+  if (blockIdx.x == 0)
+    for (int s = nU + 1 + threadIdx.x; s < ROW_SLOTS; s += blockDim.x) out[s] = out[ROW_SLOTS + s] = 0.0;
 }
 
 // C row / column of the new slot = sum over ranks (rank order) of the row parts
@@ -709,7 +710,7 @@ hrom_status finish_hybrid(hrom_ctx* c, unsigned char* send, int64_t* bytes) {
   if ((st = band_gram_rows_list(c, c->win, out, s->listB, s->cnt + 1)) != HROM_OK) return st;
   if ((st = launch_positivity_check(c, out, own_lo, own_hi)) != HROM_OK) return st;
   const EndLayout L = end_layout(s);
-  slab_row_reduce<<<1, 1024, 0, c->st>>>(b.gpart, c->fill_grid, b.gpart + (int64_t)c->fill_blocks * (c->win.nU + 1) * 2,
+  slab_row_reduce<<<((c->win.nU + 1) * 16 + 255) / 256, 256, 0, c->st>>>(b.gpart, c->fill_grid, b.gpart + (int64_t)c->fill_blocks * (c->win.nU + 1) * 2,
                                          c->band_blocks, c->win.nU, reinterpret_cast<double*>(send + L.row));
   HROM_LAUNCH_CK();
   ++c->nlaunch;
