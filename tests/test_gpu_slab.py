@@ -166,3 +166,32 @@ def test_slab_refuses_unsupported(inputs):
         slab.SlabROM(wl, 0, 16)
     with pytest.raises(HromError):  # 1-D grids have no rows to split
         slab.SlabROM(inputs.config(1), 0, 2)
+
+
+def test_slab_nccl_transport_one_rank(inputs):
+    """The DistComm transport (torch.distributed all_gather_into_tensor over NCCL) with the one GPU
+    this box has: a one-rank group drives SlabROM.step through every phase of the protocol; the
+    result equals the LocalComm run bit for bit."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2301_01718_b200 import slab
+    wl, q0, ref, roms, comm = _mk(inputs, 4, 1, filt=True, nx=64, ny=64, w=8, r=4)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        d = slab.SlabROM(wl, 0, 1)
+        d.set_state(q0)
+        dc = slab.DistComm()
+        for _ in range(wl.w + 5):
+            d.step(dc)
+            slab.step_all(roms, comm)
+        d.sync()
+        assert torch.equal(d.get_state(), roms[0].get_state())
+        assert torch.equal(d.get_mask(), roms[0].get_mask())
+    finally:
+        dist.destroy_process_group()
