@@ -30,13 +30,31 @@ def _sec(d, name):
     return (v[0] / v[1]) if v and v[1] else None
 
 
+def _peak():
+    import bench
+    return bench.measured_peaks()[0]
+
+
+def _roofline(wl, fill_ms, step_ms):
+    """north_star's per-config GB/s and roofline fraction: the fill pass's algorithmic bytes
+    (bench.fill_bytes) over its mean launch time against the measured HBM
+    copy bandwidth, and the same bytes over the whole step (the step's HBM floor is the fill)."""
+    import bench
+    n_s = int(np.ceil(wl.f * wl.N))
+    fb = bench.fill_bytes(wl, n_s)
+    peak = _peak()
+    return {"fill_ms_mean": fill_ms, "fill_algorithmic_bytes": fb, "fill_GBs": fb / (fill_ms / 1e3) / 1e9,
+            "fill_frac_of_hbm_peak": fb / (fill_ms / 1e3) / 1e9 / peak, "step_GBs": fb / (step_ms / 1e3) / 1e9,
+            "step_frac_of_hbm_peak": fb / (step_ms / 1e3) / 1e9 / peak, "hbm_peak_GBs": peak}
+
+
 def run_trajectory(cfg, steps=None, f=None):
     wl = inputs.config(cfg, **({"f": f} if f else {}))
     if steps:
         wl = inputs.config(cfg, steps=steps, **({"f": f} if f else {}))
     rom = HybridROM(wl)
     rom.set_state(torch.from_numpy(inputs.initial_condition(wl)).cuda())
-    full_ms, hyb_ms = [], []
+    full_ms, hyb_ms, fill_ms = [], [], []
     t0 = time.perf_counter()
     for k in range(1, wl.steps + 1):
         rom.profile(True)
@@ -46,7 +64,9 @@ def run_trajectory(cfg, steps=None, f=None):
         e1.record()
         e1.synchronize()
         ms = e0.elapsed_time(e1)
-        rom.profile_read()
+        sec = rom.profile_read()
+        if k >= wl.w and sec.get("fill_pass") and sec["fill_pass"][1]:
+            fill_ms.append(sec["fill_pass"][0] / sec["fill_pass"][1])
         if os.environ.get("HROM_CFG_DEBUG"):
             rom.sync()
         (hyb_ms if k >= wl.w else full_ms).append(ms)
@@ -60,6 +80,8 @@ def run_trajectory(cfg, steps=None, f=None):
            "wall_s": wall}
     if out["hybrid_step_ms_mean"]:
         out["hybrid_cell_updates_per_s"] = wl.N / (out["hybrid_step_ms_mean"] / 1e3)
+        if len(fill_ms) > 3:
+            out["roofline"] = _roofline(wl, float(np.mean(fill_ms[3:])), out["hybrid_step_ms_mean"])
     rom.close()
     return out
 
@@ -84,6 +106,8 @@ def run_config4(f, gram_mode=0, steps=20, warmup=3):
     res = {"f": f, "gram_mode": "full-dmma" if gram_mode else "incremental-shifted", "ms_per_step": ms,
            "cell_updates_per_s": wl.N / (ms / 1e3),
            "sections_ms": {k: round(v[0] / steps, 4) for k, v in sec.items() if v[1]}}
+    if sec.get("fill_pass") and sec["fill_pass"][1]:
+        res["roofline"] = _roofline(wl, sec["fill_pass"][0] / sec["fill_pass"][1], ms)
     rom.close()
     return res
 
