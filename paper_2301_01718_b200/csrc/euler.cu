@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cfloat>
 #include "internal.cuh"
+#include "async.cuh"
 
 namespace hrom {
 namespace {
@@ -219,9 +220,12 @@ __global__ void __launch_bounds__(TX * TY, MASKED ? STAGE_MINB_MASKED : STAGE_MI
       if (!xin && !yin) continue;  // corner
       const int gi = wrap(i0 + lx - TH, g.nx, g.bc), gj = wrap(j0 + ly - TH, g.ny, g.bcy);
       const int64_t n = (int64_t)gj * g.nx + gi;
+      // asynchronous 8-byte copies straight into shared memory: every copy of a thread is in flight
+      // at once and none passes through a register
 #pragma unroll
-      for (int v = 0; v < C; ++v) U[v][ly][lx] = __ldg(qin.p + sidx(qin, v * g.N + n));
+      for (int v = 0; v < C; ++v) cp_async8(&U[v][ly][lx], qin.p + sidx(qin, v * g.N + n));
     }
+    cp_async_commit();
     // gamma_n of this thread's cell for the stage combination: issued now, consumed after the
     // flux phase (stage 1 combines with the staged value itself)
     const bool mine = i < g.nx && j < g.ny && (!MASKED || ((myword >> tx) & 1u));
@@ -229,6 +233,7 @@ __global__ void __launch_bounds__(TX * TY, MASKED ? STAGE_MINB_MASKED : STAGE_MI
 #pragma unroll
     for (int v = 0; v < C; ++v)
       unv[v] = (mine && stage != 1) ? qn.p[sidx(qn, v * g.N + (int64_t)j * g.nx + i)] : 0.0;
+    cp_async_wait<0>();
     __syncthreads();
     // x-faces: face f between local columns f-1 and f (f = 0..TX), rows 0..TY-1
     for (int f = threadIdx.x; f < (TX + 1) * TY; f += TX * TY) {
