@@ -34,7 +34,8 @@ def _mk(inputs, cfg, nranks, filt=False, **over):
     return wl, q0, ref, roms, slab.LocalComm(nranks)
 
 
-@pytest.mark.parametrize("cfg,nx,ny,nranks", [(2, 96, 80, 2), (4, 128, 96, 2), (4, 128, 120, 3), (2, 70, 50, 1)])
+@pytest.mark.parametrize("cfg,nx,ny,nranks", [(2, 96, 80, 2), (4, 128, 96, 2), (4, 128, 120, 3), (2, 70, 50, 1),
+                                              (4, 70, 100, 3), (2, 45, 101, 4)])
 def test_slab_full_steps_bitwise(inputs, cfg, nx, ny, nranks):
     """Warm-up HDM steps: dt from the all-reduced CFL maximum, local RK3 on [halo | own | halo], halo
     exchange -> every own row equals the unsharded step bit for bit (transmissive and periodic)."""
@@ -54,7 +55,7 @@ def test_slab_full_steps_bitwise(inputs, cfg, nx, ny, nranks):
 
 @pytest.mark.parametrize("filt", [False, True])
 @pytest.mark.parametrize("cfg,nx,ny,nranks,w,r", [(2, 96, 96, 2, 8, 4), (4, 128, 128, 2, 12, 6), (4, 128, 144, 3, 8, 4),
-                                                   (4, 64, 64, 1, 8, 4)])
+                                                   (4, 64, 64, 1, 8, 4), (4, 70, 100, 3, 8, 4), (2, 45, 101, 4, 10, 5)])
 def test_slab_algorithm1_matches_unsharded(inputs, cfg, nx, ny, nranks, w, r, filt):
     from paper_2301_01718_b200 import slab
     from paper_2301_01718_b200.hrom import cells_from_mask
