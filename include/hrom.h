@@ -340,8 +340,10 @@ hrom_status hrom_imp_set_window(hrom_imp_ctx* ctx, int64_t k, const double* any_
  * largest relative decrease); its stop decision is taken on the host from the gathered statistics,
  * so a call that consumes a sweep message synchronises the context's stream.
  * Refused (HROM_E_INVALID): dim != 2, ODEIM points, RRE-delta, finite z, W = -1, w + 1 > 68, fewer
- * than `halo` own rows per rank.  A non-physical hybrid state on any rank is
- * latched on every rank (hrom_sync -> HROM_E_POSITIVITY); a slab does not escalate. */
+ * than `halo` own rows per rank.  Positivity escalation: when any rank's hybrid state is
+ * non-physical, every rank redoes the step as a full step with the same dt (host decision on the
+ * gathered flags: a call that consumes an END message of a hybrid step synchronises the stream);
+ * a state that is still non-physical is latched on every rank (hrom_sync -> HROM_E_POSITIVITY). */
 typedef struct {
   int32_t rank, nranks;
   int32_t ny_global;          /* rows of the whole grid */
@@ -370,6 +372,13 @@ hrom_status hrom_slab_step(hrom_ctx* ctx, const void* dev_gathered, void* dev_se
  * ties at the threshold by ascending global cell), then the sets.  Starts the selection phases:
  * writes the first message; continue with hrom_slab_step until *send_bytes_out == 0. */
 hrom_status hrom_slab_resample(hrom_ctx* ctx, const double* any_eps_own, void* dev_send, int64_t* send_bytes_out);
+/* Replay hook (as hrom_set_window): the window gamma_{k-w}..gamma_k (w+1 WHOLE-grid snapshots, oldest
+ * first) and the WHOLE-grid S-hat_{k+1} bitmap; every rank copies its rows and halo rows, the window
+ * Gram of the own rows is summed over the ranks, the basis and the sets are rebuilt.  Writes the
+ * first message; continue with hrom_slab_step until *send_bytes_out == 0. */
+hrom_status hrom_slab_set_window(hrom_ctx* ctx, int64_t k, const double* any_snaps_global, int32_t nsnaps,
+                                 const uint32_t* any_mask_global, void* dev_send, int64_t* send_bytes_out);
+int64_t hrom_slab_escalations(const hrom_ctx* ctx);  /* hybrid steps redone as full steps so far */
 
 #ifdef __cplusplus
 }

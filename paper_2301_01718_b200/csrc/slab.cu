@@ -39,9 +39,13 @@
 // (empty keep-set, relative decrease below eps_f, j_max sweeps) is taken on the host from the
 // gathered statistics, the same on every rank.  Same arithmetic as filter.cu on the dense field.
 //
-// Not supported on a slab (hrom_slab_create refuses / reports): ODEIM points, RRE-delta, finite z,
-// the whole-domain filter (W = -1), and the positivity escalation (a non-physical hybrid state is
-// latched and reported by hrom_sync on every rank).
+// Positivity escalation: the ranks' flags travel in the END message; when any rank holds a
+// non-physical hybrid state, EVERY rank redoes the step as a full step from gamma_{k-1} with the
+// same dt (host decision on the gathered flags), takes the new window-Gram row over all its own
+// cells, and a second END exchange follows.
+//
+// Not supported on a slab (hrom_slab_create refuses): ODEIM points, RRE-delta, finite z, the
+// whole-domain filter (W = -1).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -58,6 +62,7 @@ struct hrom_slab {
   bool step_hybrid = false;
   int f_order = 0, f_sw = 0;  // seam filter: cascade order and sweep in flight
   int f_sweeps[3] = {0, 0, 0};
+  int64_t escalations = 0;  // hybrid steps redone as full steps
   unsigned long long* fstat = nullptr;  // [0] max relative decrease (bits) [1] kept count of the sweep
   // message geometry (bytes)
   int64_t halo_doubles = 0;  // c * H * nx: one edge block of the state
@@ -83,7 +88,7 @@ namespace {
 constexpr int RADIX = 11, NBIN = 1 << RADIX;
 constexpr int ROW_SLOTS = kMaxW + 2;  // fixed length of the Gram-row part of an END message
 
-enum Phase { PH_IDLE = 0, PH_SMAX, PH_R, PH_HALO1, PH_FSWEEP, PH_END, PH_BOOT, PH_SEL, PH_MASK };
+enum Phase { PH_IDLE = 0, PH_SMAX, PH_R, PH_HALO1, PH_FSWEEP, PH_END, PH_END2, PH_BOOT, PH_REBUILD, PH_SEL, PH_MASK };
 
 __host__ __device__ inline int sel_shift(int p) { return p < 5 ? 53 - RADIX * p : 0; }
 
@@ -908,6 +913,73 @@ hrom_status hrom_slab_get_indicator(hrom_ctx* c, double* any_eps_own) {
   return HROM_OK;
 }
 
+int64_t hrom_slab_escalations(const hrom_ctx* c) { return (c && c->slab) ? c->slab->escalations : -1; }
+
+hrom_status hrom_slab_set_window(hrom_ctx* c, int64_t k, const double* any_snaps_global, int32_t nsnaps,
+                                 const uint32_t* any_mask_global, void* dev_send, int64_t* send_bytes_out) {
+  if (!c || !c->slab || !any_snaps_global || !any_mask_global || !dev_send || !send_bytes_out) return HROM_E_INVALID;
+  if (k < c->w || nsnaps != c->w + 1) return HROM_E_INVALID;
+  hrom_slab* s = c->slab;
+  const Geo& g = c->g;
+  Bufs& b = c->b;
+  basis_join(c);
+  hrom_status st;
+  const int64_t Dg = (int64_t)g.c * s->N_g;
+  for (int t = 0; t < nsnaps; ++t) {
+    const double* q = any_snaps_global + (int64_t)t * Dg;
+    for (int v = 0; v < g.c; ++v) {
+      int jl = 0;
+      while (jl < g.ny) {
+        int gj = s->row0 - s->hlo + jl;
+        gj = ((gj % s->ny_g) + s->ny_g) % s->ny_g;
+        const int run = std::min(g.ny - jl, s->ny_g - gj);
+        HROM_CK(cudaMemcpyAsync(s->stage + v * g.N + (int64_t)jl * g.nx, q + v * s->N_g + (int64_t)gj * g.nx,
+                                (size_t)run * g.nx * sizeof(double), cudaMemcpyDefault, c->st));
+        jl += run;
+      }
+    }
+    if ((st = hrom_put_snapshot(c, k - c->w + t, s->stage)) != HROM_OK) return st;
+  }
+  {  // S-hat_{k+1}: the local rows (own + halo) of the global bitmap
+    uint32_t* S = b.masks + (int64_t)M_S * c->mwords;
+    int jl = 0;
+    while (jl < g.ny) {
+      int gj = s->row0 - s->hlo + jl;
+      gj = ((gj % s->ny_g) + s->ny_g) % s->ny_g;
+      const int run = std::min(g.ny - jl, s->ny_g - gj);
+      HROM_CK(cudaMemcpyAsync(S + (int64_t)jl * g.wpr, any_mask_global + (int64_t)gj * g.wpr,
+                              (size_t)run * g.wpr * sizeof(uint32_t), cudaMemcpyDefault, c->st));
+      jl += run;
+    }
+  }
+  HROM_CK(cudaMemsetAsync(b.ureg + 1, 0xff, sizeof(unsigned long long), c->st));
+  c->k = k;
+  c->last_hybrid = false;
+  c->full_since_update = false;
+  c->n_owed = 0;
+  c->kinc_valid = false;
+  c->eps_sparse = false;
+  c->basis_ready = false;
+  c->gram_row_ready = false;
+  c->sets_ready = false;
+  c->smax_k = -1;
+  s->have_prev = false;
+  // window Gram of the own rows (shift rho := the newest snapshot), summed over the ranks next
+  const size_t pitch = (size_t)g.nsr * TILE * sizeof(double);
+  HROM_CK(cudaMemcpy2DAsync(b.rho, pitch, b.ring + (int64_t)c->slot_of(k) * TILE, pitch, TILE * sizeof(double),
+                            (size_t)(g.Dp / TILE), cudaMemcpyDeviceToDevice, c->st));
+  const Win W = window_of(c, k);
+  if ((st = gram_gathered_list(c, W, c->slot_ref(c->slot_of(k)), s->listA, s->cnt + 2, b.eigV, b.Rlo)) != HROM_OK)
+    return st;
+  const int ncol = W.nU + 1, n2 = ncol * ncol;
+  unsigned char* send = static_cast<unsigned char*>(dev_send);
+  HROM_CK(cudaMemcpyAsync(send, b.eigV, (size_t)n2 * 8, cudaMemcpyDeviceToDevice, c->st));
+  HROM_CK(cudaMemcpyAsync(send + (size_t)n2 * 8, b.Rlo, (size_t)n2 * 8, cudaMemcpyDeviceToDevice, c->st));
+  *send_bytes_out = (int64_t)2 * n2 * 8;
+  s->phase = PH_REBUILD;
+  return HROM_OK;
+}
+
 hrom_status hrom_slab_resample(hrom_ctx* c, const double* any_eps_own, void* dev_send, int64_t* send_bytes_out) {
   if (!c || !c->slab || !any_eps_own || !dev_send || !send_bytes_out) return HROM_E_INVALID;
   hrom_slab* s = c->slab;
@@ -1096,11 +1168,47 @@ hrom_status hrom_slab_step(hrom_ctx* c, const void* dev_gathered, void* dev_send
     return end_filter(c, send, send_bytes_out);
   }
 
-  if (s->phase == PH_END) {
+  if (s->phase == PH_END || s->phase == PH_END2) {
+    const bool redo_done = s->phase == PH_END2;
     const EndLayout L = end_layout(s);
     const SRef qk = c->slot_ref(c->slot_of(c->k));
     if ((st = unpack_halo(c, qk, gath, L.bytes)) != HROM_OK) return st;
-    // flags of all ranks (a slab does not escalate: latch)
+    if (s->step_hybrid && !redo_done) {
+      // positivity flags of all ranks: any non-physical hybrid state -> every rank redoes the step
+      // as a full step, decided on the host from the gathered flags (identical everywhere)
+      unsigned long long hf[2 * 64];
+      if (P > 64) return HROM_E_INVALID;
+      HROM_CK(cudaMemcpy2DAsync(hf, 16, gath + L.tail, (size_t)L.bytes, 16, (size_t)P, cudaMemcpyDeviceToHost, c->st));
+      HROM_CK(cudaStreamSynchronize(c->st));
+      bool bad = false;
+      for (int r = 0; r < P; ++r) bad = bad || hf[2 * r + 1] != ~0ull;
+      if (bad) {
+        ++s->escalations;
+        const SRef qprev = c->slot_ref(c->slot_of(c->k - 1));
+        const SRef U1 = plain(b.U1), U2 = plain(b.U2);
+        if ((st = launch_stage(c, 1, qprev, qprev, U1, nullptr, 0, 0.0)) != HROM_OK) return st;  // dt: still in dreg
+        if ((st = launch_stage(c, 2, qprev, U1, U2, nullptr, 0, 0.0)) != HROM_OK) return st;
+        if ((st = launch_stage(c, 3, qprev, U2, qk, nullptr, 0, 0.0)) != HROM_OK) return st;
+        HROM_CK(cudaMemsetAsync(b.ureg + 2, 0, 8, c->st));
+        HROM_CK(cudaMemsetAsync(b.ureg + 3, 0xff, 8, c->st));
+        if ((st = launch_positivity_check(c, qk, own_lo, own_hi)) != HROM_OK) return st;
+        // the window-Gram row of the final gamma_k over every own cell (the band GEMV on the
+        // all-own list), no fill partials
+        if ((st = band_gram_rows_list(c, c->win, qk, s->listA, s->cnt + 2)) != HROM_OK) return st;
+        slab_row_reduce<<<((c->win.nU + 1) * 16 + 255) / 256, 256, 0, c->st>>>(
+            b.gpart, 0, b.gpart + (int64_t)c->fill_blocks * (c->win.nU + 1) * 2, c->band_blocks, c->win.nU,
+            reinterpret_cast<double*>(send + L.row));
+        HROM_LAUNCH_CK();
+        ++c->nlaunch;
+        if ((st = pack_halo(c, qk, send)) != HROM_OK) return st;
+        HROM_CK(cudaMemcpyAsync(send + L.tail, b.ureg + 2, 8, cudaMemcpyDeviceToDevice, c->st));
+        HROM_CK(cudaMemcpyAsync(send + L.tail + 8, b.ureg + 3, 8, cudaMemcpyDeviceToDevice, c->st));
+        *send_bytes_out = L.bytes;
+        s->phase = PH_END2;
+        return HROM_OK;
+      }
+    }
+    // wave-speed maximum of all ranks (and, after a redo, a flag that is still set: latched)
     smax_reduce_kernel<<<1, 1, 0, c->st>>>(gath, L.bytes, L.tail, P, b.ureg, 1);
     HROM_LAUNCH_CK();
     ++c->nlaunch;
@@ -1143,6 +1251,23 @@ hrom_status hrom_slab_step(hrom_ctx* c, const void* dev_gathered, void* dev_send
     c->nlaunch += 2;
     c->rebase_k = c->k;
     return begin_update(c, send, send_bytes_out);
+  }
+
+  if (s->phase == PH_REBUILD) {  // replay hook: the summed window Gram -> C, eigen-solve, sets of the given S-hat
+    const Win W = window_of(c, c->k);
+    const int ncol = W.nU + 1, n2 = ncol * ncol;
+    dd_sum_kernel<<<(n2 + 255) / 256, 256, 0, c->st>>>(gath, (int64_t)2 * n2 * 8, 0, P, n2, 0, b.eigV, b.Rlo);
+    scatter_gram_kernel<<<1, 1024, 0, c->st>>>(b.eigV, b.Rlo, ncol, W, b.C, b.Clo, kMaxSlots);
+    HROM_LAUNCH_CK();
+    c->nlaunch += 2;
+    c->rebase_k = c->k;
+    c->eig_win = W;
+    c->eig_todo = true;
+    if ((st = flush_eigen(c)) != HROM_OK) return st;
+    c->win = W;
+    c->basis_ready = true;
+    s->phase = PH_IDLE;
+    return finish_sets(c);
   }
 
   if (s->phase == PH_SEL) {

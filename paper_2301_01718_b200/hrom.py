@@ -127,6 +127,8 @@ _SIGS = {
     "hrom_slab_get_indicator": (C.c_int, [_VP, _VP]),
     "hrom_slab_step": (C.c_int, [_VP, _VP, _VP, C.POINTER(C.c_int64)]),
     "hrom_slab_resample": (C.c_int, [_VP, _VP, _VP, C.POINTER(C.c_int64)]),
+    "hrom_slab_set_window": (C.c_int, [_VP, C.c_int64, _VP, C.c_int32, _VP, _VP, C.POINTER(C.c_int64)]),
+    "hrom_slab_escalations": (C.c_int64, [_VP]),
 }
 
 SECTIONS = ["dt", "masked_rk3", "gathered_gram", "pinv_solve", "fill_pass", "indicator", "seam_filter",

@@ -160,6 +160,17 @@ class SlabROM:
         while msg is not None:
             msg = self.phase(comm.all_gather(msg))
 
+    def set_window_begin(self, k: int, snaps_global: torch.Tensor, mask_global: torch.Tensor) -> torch.Tensor:
+        """Replay hook: whole-grid window (w+1, c, N) and whole-grid S-hat bitmap (hrom_slab_set_window)."""
+        assert snaps_global.dtype == torch.float64 and snaps_global.is_contiguous()
+        n = C.c_int64(0)
+        H._ck(self.lib.hrom_slab_set_window(self.h, k, H._ptr(snaps_global), snaps_global.shape[0], H._ptr(mask_global),
+                                            H._ptr(self.send), C.byref(n)), "hrom_slab_set_window")
+        return self.send[: n.value]
+
+    def escalations(self) -> int:
+        return int(self.lib.hrom_slab_escalations(self.h))
+
     def step(self, comm: DistComm):
         """One step of Algorithm 1 on this rank's slab; collective over `comm`."""
         msg = self.phase(None)
@@ -183,6 +194,14 @@ def resample_all(roms: List[SlabROM], comm: LocalComm, eps_global: torch.Tensor)
     for r in roms:
         lo = int(r.info.row0) * r.wl.nx
         msgs.append(r.resample_begin(eps_global[lo: lo + int(r.info.cells_own)].contiguous()))
+    while msgs[0] is not None:
+        gathered = comm.all_gather_many(msgs)
+        msgs = [r.phase(gathered) for r in roms]
+
+
+def set_window_all(roms: List[SlabROM], comm: LocalComm, k: int, snaps_global: torch.Tensor, mask_global: torch.Tensor):
+    """Replay hook on all slabs of one process."""
+    msgs = [r.set_window_begin(k, snaps_global, mask_global) for r in roms]
     while msgs[0] is not None:
         gathered = comm.all_gather_many(msgs)
         msgs = [r.phase(gathered) for r in roms]

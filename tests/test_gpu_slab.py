@@ -196,3 +196,73 @@ def test_slab_nccl_transport_one_rank(inputs):
         assert torch.equal(d.get_mask(), roms[0].get_mask())
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seed,nranks,ny", [(1, 2, 30), (5, 3, 45)])
+def test_slab_replay_and_positivity_escalation(orc, inputs, seed, nranks, ny):
+    """hrom_slab_set_window (replay) + S:478 on slabs: a violent window makes the hybrid state
+    non-physical on some rank; every rank then redoes the step as a full step with the same dt, and
+    the sharded state equals the oracle's escalated step and the unsharded context's; the next basis
+    (window-Gram row recomputed over the own rows, summed over the ranks) matches too."""
+    from paper_2301_01718_b200 import slab
+    from paper_2301_01718_b200.hrom import HybridROM, mask_from_cells
+    wl = inputs.Workload("small2d", dim=2, nx=40, ny=ny, bc=0, recon=2, cfl=0.4, w=8, r=2, f=0.12, h=2, W=3, seed=21)
+    snaps = inputs.smooth_window(wl, wl.w + 1, seed=seed, amp=0.9)
+    rng = np.random.default_rng(seed)
+    S = (rng.random(wl.N) < 0.15).astype(np.uint8)
+    k = wl.w + 3
+    R = orc.Run(wl, snaps[0])
+    R.set_window(k, snaps, S)
+    dt = orc.dt(wl, snaps[-1])
+    assert R.step(dt) == 2  # the oracle escalated
+    sn = torch.from_numpy(snaps.reshape(wl.w + 1, -1)).cuda().contiguous()
+    mk = mask_from_cells(wl, S)
+    ref = HybridROM(wl)
+    ref.set_window(k, sn, mk)
+    ref.step()
+    ref.sync()
+    roms = [slab.SlabROM(wl, r, nranks) for r in range(nranks)]
+    comm = slab.LocalComm(nranks)
+    slab.set_window_all(roms, comm, k, sn, mk)
+    slab.step_all(roms, comm)
+    for x in roms:
+        x.sync()  # the full step is admissible: nothing latched
+    assert all(x.escalations() == 1 for x in roms)
+    b = slab.assemble(roms, "state").cpu().numpy()
+    o = R.state().reshape(b.shape)
+    a = ref.get_state().cpu().numpy()
+    assert np.abs(b - o).max() <= 1e-13 * np.abs(o).max()
+    assert np.array_equal(a, b)  # a full step: bitwise the unsharded one
+    # the basis of the window ending at the escalated snapshot
+    lam = roms[0].get_eigen().cpu().numpy()
+    sig = R.sigma()
+    re = R.reff()
+    np.testing.assert_allclose(lam[:re], sig[:re] ** 2, rtol=1e-9, atol=1e-13 * sig[0] ** 2)
+    for x in roms[1:]:
+        assert np.array_equal(x.get_eigen().cpu().numpy(), lam)
+
+
+def test_slab_replay_hybrid_step_matches_oracle(orc, inputs):
+    """Lock-step replay on slabs: one hybrid step from the oracle's window and S-hat (filter on)."""
+    from paper_2301_01718_b200 import slab
+    from paper_2301_01718_b200.hrom import mask_from_cells
+    wl = inputs.Workload("small2d", dim=2, nx=64, ny=60, bc=1, recon=2, cfl=0.4, w=8, r=5, f=0.12, h=2, W=3, seed=21)
+    snaps = inputs.smooth_window(wl, wl.w + 1, seed=3, amp=0.05)
+    rng = np.random.default_rng(3)
+    S = (rng.random(wl.N) < 0.12).astype(np.uint8)
+    k = wl.w + 2
+    R = orc.Run(wl, snaps[0])
+    R.set_window(k, snaps, S)
+    assert R.step(orc.dt(wl, snaps[-1])) != 2
+    roms = [slab.SlabROM(wl, r, 3) for r in range(3)]
+    comm = slab.LocalComm(3)
+    slab.set_window_all(roms, comm, k, torch.from_numpy(snaps.reshape(wl.w + 1, -1)).cuda().contiguous(),
+                        mask_from_cells(wl, S))
+    slab.step_all(roms, comm)
+    for x in roms:
+        x.sync()
+    assert all(x.escalations() == 0 for x in roms)
+    b = slab.assemble(roms, "state").cpu().numpy()
+    o = R.state().reshape(b.shape)
+    scale = np.abs(o).max(axis=1, keepdims=True)
+    assert float((np.abs(b - o) / scale).max()) <= 1e-12
