@@ -249,6 +249,10 @@ hrom_status hrom_debug_counters(hrom_ctx* ctx, int32_t* any_out, int32_t n);
  * launches: seam filter [0] start, [1] after the compaction prologue, [2 + s] after sweep s;
  * sets kernel [40 + phase]; LSQ solve [64 + phase] (only while profiling is enabled). */
 hrom_status hrom_debug_timers(hrom_ctx* ctx, int64_t* host_out, int32_t n);
+/* debug read-back of the small matrices of the basis path (joins the side stream; n doubles):
+ * which = 0 / 1 window Gram C hi / lo by ring slot (130 x 130), 2 M = X^T X hi then lo (w x w each,
+ * packed at 130^2), 3 eigenvectors of hi(M) (w x w), 4 A (w x r, column j at j*w), 5 eigenvalues */
+hrom_status hrom_debug_read(hrom_ctx* ctx, int32_t which, double* any_out, int64_t n);
 
 /* ==== NEXT-4: Algorithm 1 with the paper's own implicit HDM ====
  * HDM: R_k(q) = q - F_k(q) = 0, F_k(q) = dt beta f*(q) - sum_{j<s} a_j q_{k-s+j},

@@ -1086,6 +1086,26 @@ hrom_status hrom_debug_counters(hrom_ctx* c, int32_t* any_out, int32_t n) {
   return HROM_OK;
 }
 
+hrom_status hrom_debug_read(hrom_ctx* c, int32_t which, double* any_out, int64_t n) {
+  if (!c || !any_out || n < 0) return HROM_E_INVALID;
+  basis_join(c);
+  const double* src = nullptr;
+  int64_t cap = 0;
+  const int64_t k2 = (int64_t)kMaxSlots * kMaxSlots;
+  switch (which) {
+    case 0: src = c->b.C; cap = k2; break;
+    case 1: src = c->b.Clo; cap = k2; break;
+    case 2: src = c->b.Mdd; cap = 2 * k2; break;
+    case 3: src = c->b.Zf; cap = k2; break;
+    case 4: src = c->b.A; cap = (int64_t)kMaxW * kMaxR; break;
+    case 5: src = c->b.lam; cap = kMaxSlots; break;
+    default: return HROM_E_INVALID;
+  }
+  if (n > cap) return HROM_E_INVALID;
+  HROM_CK(cudaMemcpyAsync(any_out, src, n * sizeof(double), cudaMemcpyDefault, c->st));
+  return HROM_OK;
+}
+
 hrom_status hrom_debug_timers(hrom_ctx* c, int64_t* host_out, int32_t n) {
   if (!c || !host_out || n < 0 || n > 128) return HROM_E_INVALID;
   basis_join(c);

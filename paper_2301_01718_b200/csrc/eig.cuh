@@ -252,6 +252,12 @@ __device__ int sym_eig(double* A, int n, int ldn, const EigWork& W, int nvec_cap
       }
     }
     u0[(n - 1) * ldz + j] = fabs(p) < pert ? (p < 0.0 ? -pert : pert) : p;
+    // the last row has no super-diagonals: the back substitution multiplies these two entries by
+    // z1 = z2 = 0, so they must be finite -- left unwritten they are whatever the previous block
+    // on this SM left in shared memory, and a NaN / Inf pattern there sent the vector through
+    // the degenerate-restart path (a rounding-level, run-to-run difference of the basis)
+    u1[(n - 1) * ldz + j] = 0.0;
+    u2[(n - 1) * ldz + j] = 0.0;
     for (int i = 0; i + 1 < n; ++i)
       if (fabs(u0[i * ldz + j]) < pert) u0[i * ldz + j] = u0[i * ldz + j] < 0.0 ? -pert : pert;
     // start vector

@@ -98,6 +98,7 @@ _SIGS = {
     "hrom_launch_count": (C.c_int64, [_VP]),
     "hrom_debug_counters": (C.c_int, [_VP, _VP, C.c_int32]),
     "hrom_debug_timers": (C.c_int, [_VP, _VP, C.c_int32]),
+    "hrom_debug_read": (C.c_int, [_VP, C.c_int32, _VP, C.c_int64]),
     "hrom_imp_create": (C.c_int, [C.POINTER(Grid), C.c_double, C.POINTER(Params), C.POINTER(ImpParams), _VP,
                                   C.POINTER(_VP)]),
     "hrom_imp_destroy": (None, [_VP]),
