@@ -778,6 +778,7 @@ hrom_status hrom_slab_create(const hrom_grid* grid, double gamma, double cfl, co
   if (!grid || !p || !out) return HROM_E_INVALID;
   *out = nullptr;
   if (grid->dim != 2) return HROM_E_INVALID;  // a 1-D grid has no rows to split
+  if (nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks) return HROM_E_INVALID;  // host decisions read <= 64 flags
   if (p->odeim_points > 0 || p->sample_mode != 0 || p->full_period > 0 || p->band < 0 || p->gram_mode != 0)
     return HROM_E_INVALID;
   hrom_slab_info info;
