@@ -737,6 +737,8 @@ hrom_status launch_cross(hrom_ctx* c, XGArgs& a, int grid) {
 // GV_U row chunks in flight per lane (1 with both product vectors, 2 for the band rows' one).
 // Per-CTA partials [blk][2 nU + 1], reduced in fixed order.
 constexpr int GV_T = 256, GV_W = GV_T / 32;
+// dynamic shared memory of gemv_gather_kernel: two stages of (3 + SPW) values x 32 lanes per warp and chunk
+constexpr size_t gv_smem(int spw, int gv_u) { return (size_t)2 * GV_W * gv_u * (3 + spw) * 32 * sizeof(double); }
 // NEWCOL = false, BANDOUT = true: the seam-band part of the new window Gram row (H10): one
 // product vector b = gamma_k on the band rows, partials [blk][nU + 1] ([nU] = sum b^2).
 // DD = false: plain fp64 accumulation (the gathered Gram of the gappy normal equations when
@@ -792,52 +794,128 @@ __global__ void __launch_bounds__(NT, NT == GV_T ? 2 : 1) gemv_gather_kernel(Geo
       }
     }
   };
-  fetch_list((int64_t)blockIdx.x * 32 * GV_U);
-  for (int64_t base = (int64_t)blockIdx.x * 32 * GV_U; base < total; base += gstep) {
-    int32_t lcur[GV_U];
-#pragma unroll
-    for (int u = 0; u < GV_U; ++u) lcur[u] = lnext[u];
-    fetch_list(base + gstep);
-    int64_t se[GV_U];
-    double xn[GV_U], bv[GV_U], r[GV_U];
-    bool ok[GV_U];
-#pragma unroll
-    for (int u = 0; u < GV_U; ++u) {
-      const int64_t t = base + 32 * u + lane;
-      ok[u] = t < total;
-      int64_t e = 0;
-      if (ok[u]) {
-        const int var = (int)t / nS;
-        e = (int64_t)var * g.N + lcur[u];
-      }
-      se[u] = sidx(slab, e);
-      r[u] = ok[u] ? __ldg(rho.p + sidx(rho, e)) : 0.0;
-      xn[u] = (NEWCOL && ok[u]) ? __ldg(xnew_col + se[u]) : 0.0;
-      bv[u] = ok[u] ? __ldg(src_b.p + sidx(src_b, e)) : 0.0;
-    }
-    double val[GV_U][SPW];
-#pragma unroll
-    for (int u = 0; u < GV_U; ++u)
-#pragma unroll
-      for (int j = 0; j < SPW; ++j) val[u][j] = (ok[u] && coff[j] >= 0) ? __ldg(ring + coff[j] + se[u]) : 0.0;
-#pragma unroll
-    for (int u = 0; u < GV_U; ++u) {
-      if (!ok[u]) continue;
-      const double x = xn[u] - r[u], y = bv[u] - r[u];
-#pragma unroll
-      for (int j = 0; j < SPW; ++j) {
-        const double v = val[u][j] - r[u];
-        if (DD) {
-          if (NEWCOL) biased_fma(an[j], anl[j], v, x);
-          biased_fma(ab[j], abl[j], v, y);
-        } else {
-          if (NEWCOL) an[j] = fma(v, x, an[j]);
-          ab[j] = fma(v, y, ab[j]);
+  if constexpr (NEWCOL) {
+    // Value loads run one chunk ahead of the arithmetic through shared memory (cp.async, no
+    // registers): stage[s][warp][u][k][lane], k = rho, x_new, b, the warp's SPW slots.  Every lane
+    // reads back only what it copied itself; the sums run in the same order as before.
+    constexpr int NV = 3 + SPW;
+    extern __shared__ double gv_stage[];
+    double* mystage = gv_stage + (size_t)warp * GV_U * NV * 32 + lane;
+    constexpr size_t STG = (size_t)NW * GV_U * NV * 32;  // doubles per stage
+    auto issue = [&](int64_t b0, const int32_t* lcell, int st) {
+  #pragma unroll
+      for (int u = 0; u < GV_U; ++u) {
+        const int64_t t = b0 + 32 * u + lane;
+        if (t < total) {
+          const int var = (int)t / nS;
+          const int64_t e = (int64_t)var * g.N + lcell[u];
+          const int64_t se = sidx(slab, e);
+          double* d = mystage + st * STG + (size_t)u * NV * 32;
+          cp_async8(d, rho.p + sidx(rho, e));
+          if (NEWCOL) cp_async8(d + 32, xnew_col + se);
+          cp_async8(d + 64, src_b.p + sidx(src_b, e));
+  #pragma unroll
+          for (int j = 0; j < SPW; ++j)
+            if (coff[j] >= 0) cp_async8(d + (3 + j) * 32, ring + coff[j] + se);
         }
       }
-      if (warp == 0) {
-        if (DD) biased_fma(bb, bbl, y, y);
-        else bb = fma(y, y, bb);
+      cp_async_commit();
+    };
+    const int64_t base0 = (int64_t)blockIdx.x * 32 * GV_U;
+    fetch_list(base0);
+    {
+      int32_t l0[GV_U];
+  #pragma unroll
+      for (int u = 0; u < GV_U; ++u) l0[u] = lnext[u];
+      issue(base0, l0, 0);
+    }
+    fetch_list(base0 + gstep);
+    int st = 0;
+    for (int64_t base = base0; base < total; base += gstep) {
+      {
+        int32_t l1[GV_U];
+  #pragma unroll
+        for (int u = 0; u < GV_U; ++u) l1[u] = lnext[u];
+        issue(base + gstep, l1, st ^ 1);  // the next chunk's values (a chunk past the end copies nothing)
+      }
+      fetch_list(base + 2 * gstep);
+      cp_async_wait<1>();  // this chunk's copies have landed (the next chunk's may be in flight)
+  #pragma unroll
+      for (int u = 0; u < GV_U; ++u) {
+        const int64_t t = base + 32 * u + lane;
+        if (t >= total) continue;
+        const double* d = mystage + st * STG + (size_t)u * NV * 32;
+        const double r = d[0];
+        const double x = (NEWCOL ? d[32] : 0.0) - r, y = d[64] - r;
+  #pragma unroll
+        for (int j = 0; j < SPW; ++j) {
+          const double v = (coff[j] >= 0 ? d[(3 + j) * 32] : 0.0) - r;
+          if (DD) {
+            if (NEWCOL) biased_fma(an[j], anl[j], v, x);
+            biased_fma(ab[j], abl[j], v, y);
+          } else {
+            if (NEWCOL) an[j] = fma(v, x, an[j]);
+            ab[j] = fma(v, y, ab[j]);
+          }
+        }
+        if (warp == 0) {
+          if (DD) biased_fma(bb, bbl, y, y);
+          else bb = fma(y, y, bb);
+        }
+      }
+      st ^= 1;
+    }
+    cp_async_wait<0>();
+  } else {
+    // band rows (one product vector, two chunks in flight in registers): runs beside the positivity
+    // pass, where the staged variant's shared memory cost more than its overlap gained
+    fetch_list((int64_t)blockIdx.x * 32 * GV_U);
+    for (int64_t base = (int64_t)blockIdx.x * 32 * GV_U; base < total; base += gstep) {
+      int32_t lcur[GV_U];
+  #pragma unroll
+      for (int u = 0; u < GV_U; ++u) lcur[u] = lnext[u];
+      fetch_list(base + gstep);
+      int64_t se[GV_U];
+      double xn[GV_U], bv[GV_U], r[GV_U];
+      bool ok[GV_U];
+  #pragma unroll
+      for (int u = 0; u < GV_U; ++u) {
+        const int64_t t = base + 32 * u + lane;
+        ok[u] = t < total;
+        int64_t e = 0;
+        if (ok[u]) {
+          const int var = (int)t / nS;
+          e = (int64_t)var * g.N + lcur[u];
+        }
+        se[u] = sidx(slab, e);
+        r[u] = ok[u] ? __ldg(rho.p + sidx(rho, e)) : 0.0;
+        xn[u] = (NEWCOL && ok[u]) ? __ldg(xnew_col + se[u]) : 0.0;
+        bv[u] = ok[u] ? __ldg(src_b.p + sidx(src_b, e)) : 0.0;
+      }
+      double val[GV_U][SPW];
+  #pragma unroll
+      for (int u = 0; u < GV_U; ++u)
+  #pragma unroll
+        for (int j = 0; j < SPW; ++j) val[u][j] = (ok[u] && coff[j] >= 0) ? __ldg(ring + coff[j] + se[u]) : 0.0;
+  #pragma unroll
+      for (int u = 0; u < GV_U; ++u) {
+        if (!ok[u]) continue;
+        const double x = xn[u] - r[u], y = bv[u] - r[u];
+  #pragma unroll
+        for (int j = 0; j < SPW; ++j) {
+          const double v = val[u][j] - r[u];
+          if (DD) {
+            if (NEWCOL) biased_fma(an[j], anl[j], v, x);
+            biased_fma(ab[j], abl[j], v, y);
+          } else {
+            if (NEWCOL) an[j] = fma(v, x, an[j]);
+            ab[j] = fma(v, y, ab[j]);
+          }
+        }
+        if (warp == 0) {
+          if (DD) biased_fma(bb, bbl, y, y);
+          else bb = fma(y, y, bb);
+        }
       }
     }
   }
@@ -2108,11 +2186,17 @@ hrom_status gram_gathered_partial(hrom_ctx* c, SRef src_b, const GatherLists* L)
   const int gblocks = 2 * (c->basis_pending ? c->nsm - 1 : c->nsm);
   const int nv = 2 * a.W.nU + 1;
   if (a.W.nU <= 9 * GV_W)
-    gemv_gather_kernel<9><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b, c->b.vpart,
-                                                       c->b.C);
+  {
+    HROM_CK(cudaFuncSetAttribute(gemv_gather_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gv_smem(9, 1)));
+    gemv_gather_kernel<9><<<gblocks, GV_T, gv_smem(9, 1), c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b,
+                                                                   c->b.vpart, c->b.C);
+  }
   else
-    gemv_gather_kernel<17><<<gblocks, GV_T, 0, c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b,
-                                                        c->b.vpart, c->b.C);
+  {
+    HROM_CK(cudaFuncSetAttribute(gemv_gather_kernel<17>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gv_smem(17, 1)));
+    gemv_gather_kernel<17><<<gblocks, GV_T, gv_smem(17, 1), c->st>>>(c->g, a.W, a.ring, a.rho, a.list, a.count, src_b,
+                                                                     c->b.vpart, c->b.C);
+  }
   HROM_LAUNCH_CK();
   double* v = gathered_gemv_values(c);
   vpart_reduce<<<(nv * GR_TPE + 255) / 256, 256, 0, c->st>>>(c->b.vpart, gblocks, nv, v);
